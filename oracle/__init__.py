@@ -1,0 +1,168 @@
+"""ctypes wrapper of the CPU oracle (oracle/oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs. The product package (paper_2404_19249_b200) never imports
+this module and shares no code with it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+OR_OK, OR_E_ARG, OR_E_MESH, OR_E_NONFINITE, OR_E_NOT_SPD, OR_E_NOT_CONVERGED, OR_E_NOMEM = range(7)
+WHICH = {"K": 0, "M": 1, "MV": 2, "H": 3, "A": 4}
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with plain gcc (-O2, no FMA contraction, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c99",
+                               "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(_LIB)
+        vp, i64, i32, dbl = C.c_void_p, C.c_int64, C.c_int, C.c_double
+        L.or_create.restype = vp
+        L.or_create.argtypes = [i64, vp, i64, vp, vp, C.POINTER(C.c_int)]
+        L.or_destroy.argtypes = [vp]
+        L.or_last_error.restype = C.c_char_p
+        L.or_last_error.argtypes = [vp]
+        L.or_sizes.argtypes = [vp, C.POINTER(i64), C.POINTER(i64)]
+        L.or_get_pattern.argtypes = [vp, vp, vp, vp, vp]
+        L.or_get_values.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp]
+        L.or_assemble_veff.restype = i32
+        L.or_assemble_veff.argtypes = [vp, vp, dbl]
+        L.or_spmm.restype = i32
+        L.or_spmm.argtypes = [vp, i32, i32, vp, vp]
+        L.or_block_pcg.restype = i32
+        L.or_block_pcg.argtypes = [vp, i32, vp, vp, vp, dbl, i32, vp, vp, vp]
+        L.or_project.restype = i32
+        L.or_project.argtypes = [vp, i64, vp, vp, vp, i32, vp, vp, vp]
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"oracle status {status}: {msg}")
+        self.status = status
+
+
+class Mesh:
+    """Oracle view of one fine mesh (P1, Dirichlet-eliminated)."""
+
+    def __init__(self, xyz, tets, dirichlet):
+        L = lib()
+        self._keep = (np.ascontiguousarray(xyz, dtype=np.float64),
+                      np.ascontiguousarray(tets, dtype=np.int32),
+                      np.ascontiguousarray(dirichlet, dtype=np.uint8))
+        xyz, tets, dirichlet = self._keep
+        self.n_nodes, self.n_tets = xyz.shape[0], tets.shape[0]
+        st = C.c_int(0)
+        self._h = L.or_create(self.n_nodes, _p(xyz), self.n_tets, _p(tets), _p(dirichlet), C.byref(st))
+        if not self._h:
+            raise MemoryError("or_create")
+        if st.value != OR_OK:
+            msg = L.or_last_error(self._h).decode()
+            L.or_destroy(self._h)
+            self._h = None
+            raise OracleError(st.value, msg)
+        nf, nnz = C.c_int64(), C.c_int64()
+        L.or_sizes(self._h, C.byref(nf), C.byref(nnz))
+        self.n_free, self.nnz = nf.value, nnz.value
+        self.mu = None
+
+    @classmethod
+    def from_problem(cls, p):
+        return cls(p.xyz, p.tets, p.dirichlet)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().or_destroy(self._h)
+            self._h = None
+
+    def pattern(self):
+        row_ptr = np.empty(self.n_free + 1, np.int64)
+        col = np.empty(self.nnz, np.int32)
+        emap = np.empty(16 * self.n_tets, np.int32)
+        fon = np.empty(self.n_nodes, np.int32)
+        lib().or_get_pattern(self._h, _p(row_ptr), _p(col), _p(emap), _p(fon))
+        return row_ptr, col, emap, fon
+
+    def values(self):
+        out = {k: np.empty(self.nnz) for k in ("K", "M", "MV", "H", "A")}
+        out["diag"] = np.empty(self.n_free)
+        out["vol"] = np.empty(self.n_tets)
+        lib().or_get_values(self._h, *[_p(out[k]) for k in ("K", "M", "MV", "H", "A", "diag", "vol")])
+        return out
+
+    def assemble_veff(self, V, mu):
+        V = np.ascontiguousarray(V, dtype=np.float64)
+        assert V.shape == (self.n_nodes,)
+        st = lib().or_assemble_veff(self._h, _p(V), float(mu))
+        self.mu = float(mu)
+        return st
+
+    def spmm(self, which, X):
+        X = np.ascontiguousarray(X, dtype=np.float64)
+        if X.ndim == 1:
+            X = X[:, None]
+        N = X.shape[1]
+        Y = np.empty_like(X)
+        st = lib().or_spmm(self._h, WHICH[which], N, _p(X), _p(Y))
+        if st != OR_OK:
+            raise OracleError(st, "spmm")
+        return Y
+
+    def block_pcg(self, lam, U, tol=1e-10, max_iter=2000):
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        N = U.shape[1]
+        lam = np.ascontiguousarray(lam, dtype=np.float64)
+        Ut = np.empty_like(U)
+        iters = np.empty(N, np.int32)
+        rr = np.empty(N)
+        rt = np.empty(N)
+        st = lib().or_block_pcg(self._h, N, _p(lam), _p(U), _p(Ut), float(tol), int(max_iter),
+                                _p(iters), _p(rr), _p(rt))
+        return dict(Ut=Ut, iters=iters, relres=rr, relres_true=rt, status=st)
+
+    def project(self, n_H, P_rowptr, P_col, P_val, Ut):
+        Ut = np.ascontiguousarray(Ut, dtype=np.float64)
+        N = Ut.shape[1]
+        D = n_H + N
+        FA = np.empty((D, D))
+        FB = np.empty((D, D))
+        pr = np.ascontiguousarray(P_rowptr, dtype=np.int32)
+        pc = np.ascontiguousarray(P_col, dtype=np.int32)
+        pv = np.ascontiguousarray(P_val, dtype=np.float64)
+        st = lib().or_project(self._h, int(n_H), _p(pr), _p(pc), _p(pv), N, _p(Ut), _p(FA), _p(FB))
+        if st != OR_OK:
+            raise OracleError(st, "project")
+        return FA, FB
+
+    def csr(self, which):
+        """scipy CSR of one operator (for brute-force pins in tests)."""
+        import scipy.sparse as sp
+        row_ptr, col, _, _ = self.pattern()
+        return sp.csr_matrix((self.values()[which], col, row_ptr), shape=(self.n_free, self.n_free))

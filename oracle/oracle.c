@@ -1,0 +1,416 @@
+/*
+ * oracle.c -- TEST INFRASTRUCTURE ONLY. A plain, slow, single-threaded CPU implementation of the
+ * hot path of the nonnested augmented subspace method (arXiv 2404.19249). It exists to check the
+ * CUDA library (paper_2404_19249_b200/csrc) element by element. Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load it. It shares no code, header,
+ * table or helper with the CUDA path.
+ *
+ * Build: gcc -O2 -ffp-contract=off -fPIC -shared (no fast-math; no OpenMP).
+ *
+ * Every function follows a passage of /root/reference/PAPER.md ("PAPER.md:L"), with the readings
+ * of SURVEY.md §8c / DESIGN.md §2 where the paper is silent:
+ *   or_create          P1 space S_h in H^1_0 on a tet mesh, Dirichlet elimination (
+ *                      readings Q3, pattern item 2), element-to-nnz map,
+ *                      stiffness and mass of (st3).
+ *   or_assemble_veff   V_eff-weighted mass (st4), H = 1/2 K + M_V, shifted
+ *                      operator A = H + mu M of H~.
+ *   or_spmm            Y = Op X for a block of vectors (definition).
+ *   or_block_pcg       N independent BVPs (Aux_Linear_Problem) by textbook
+ *                      Jacobi-preconditioned CG, one column at a time (reading Q6, Q7).
+ *   or_project         F_A, F_B of (st1)-(st2) with A_H = P^T H P (st5), b_H = P^T H U~ (st6),
+ *                      beta = U~^T H U~ (st7), and the mass counterparts B_H, c_H, gamma
+ *                      (readings Q1, Q4).
+ * Pinning: every function is pinned in tests/test_oracle_*.py against closed forms, invariants and
+ * brute-force dense solves (no function here is "parity unpinned").
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <stdio.h>
+
+enum { OR_OK = 0, OR_E_ARG = 1, OR_E_MESH = 2, OR_E_NONFINITE = 3, OR_E_NOT_SPD = 4,
+       OR_E_NOT_CONVERGED = 5, OR_E_NOMEM = 6 };
+
+typedef struct {
+  int64_t n_nodes, n_tets, n_free, nnz;
+  int32_t *free_of_node;   /* [n_nodes], -1 on Dirichlet nodes */
+  int32_t *node_of_free;   /* [n_free] */
+  int64_t *row_ptr;        /* [n_free+1] */
+  int32_t *col;            /* [nnz], sorted within each row */
+  int32_t *emap;           /* [16*n_tets]: emap[16t+4a+b] = CSR position of (free(v_a), free(v_b)) or -1 */
+  int32_t *tets;           /* copy [4*n_tets] */
+  double *vol;             /* [n_tets] |T| */
+  double *grad;            /* [12*n_tets] grad lambda_a, a=0..3 */
+  double *K, *M, *MV, *H, *A, *diag; /* [nnz], [nnz], ..., diag [n_free] */
+  double mu;               /* shift used by the last or_assemble_veff */
+  char err[256];
+} or_mesh;
+
+static int cmp_i32(const void *a, const void *b) {
+  int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+  return (x > y) - (x < y);
+}
+
+void or_destroy(or_mesh *h) {
+  if (!h) return;
+  free(h->free_of_node); free(h->node_of_free); free(h->row_ptr); free(h->col); free(h->emap);
+  free(h->tets); free(h->vol); free(h->grad); free(h->K); free(h->M); free(h->MV); free(h->H);
+  free(h->A); free(h->diag);
+  free(h);
+}
+
+const char *or_last_error(const or_mesh *h) { return h ? h->err : "null handle"; }
+
+/* position of column c in row r (binary search over the sorted row), -1 if absent */
+static int64_t find_in_row(const or_mesh *h, int64_t r, int32_t c) {
+  int64_t lo = h->row_ptr[r], hi = h->row_ptr[r + 1] - 1;
+  while (lo <= hi) {
+    int64_t mid = lo + (hi - lo) / 2;
+    if (h->col[mid] == c) return mid;
+    if (h->col[mid] < c) lo = mid + 1; else hi = mid - 1;
+  }
+  return -1;
+}
+
+/*
+ * Geometry of one tet (PAPER.md:256-261, P1 on a shape-regular tet mesh):
+ * J = [x1-x0, x2-x0, x3-x0] (columns); |T| = det(J)/6 must be > 0.
+ * grad lambda_a (a=1..3) are the rows of J^{-1}; grad lambda_0 = -(sum of the others).
+ */
+static int tet_geometry(const double *xyz, const int32_t *v, double *vol, double g[4][3]) {
+  double J[3][3];
+  for (int c = 0; c < 3; c++)
+    for (int r = 0; r < 3; r++) J[r][c] = xyz[3 * v[c + 1] + r] - xyz[3 * v[0] + r];
+  double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1])
+             - J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0])
+             + J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+  if (!(det > 0.0)) return 0;
+  /* inverse = adj(J)/det; row a of J^{-1} is grad lambda_{a+1} */
+  double inv[3][3];
+  inv[0][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) / det;
+  inv[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) / det;
+  inv[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) / det;
+  inv[1][0] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) / det;
+  inv[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) / det;
+  inv[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) / det;
+  inv[2][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) / det;
+  inv[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / det;
+  inv[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / det;
+  for (int a = 0; a < 3; a++)
+    for (int d = 0; d < 3; d++) g[a + 1][d] = inv[a][d];
+  for (int d = 0; d < 3; d++) g[0][d] = -(g[1][d] + g[2][d] + g[3][d]);
+  *vol = det / 6.0;
+  return 1;
+}
+
+/*
+ * Build the P1 discretization on the fine mesh:
+ *  1. free[v] = rank of v among non-Dirichlet nodes (Dirichlet elimination, PAPER.md:1120 psi=0 on dOmega).
+ *  2. CSR pattern over free nodes: row i lists the sorted unique free(w) with w sharing a tet with i
+ *     (diagonal included); nothing beyond the FEM stencil.
+ *  3. emap[16t+4a+b] = CSR position of (free(v_a), free(v_b)) or -1 (element-to-nnz scatter map).
+ *  4. |T| and grad lambda_a per tet.
+ *  5. K_ij = sum_T |T| grad l_a . grad l_b,  M_ij = sum_T |T|(1+delta_ab)/20  (st3),
+ *     accumulated val[emap] += elem(a,b) for t ascending, then a, then b.
+ * Returns NULL only on allocation failure; *status reports mesh errors (inverted tet id in err).
+ */
+or_mesh *or_create(int64_t n_nodes, const double *xyz, int64_t n_tets, const int32_t *tets,
+                   const uint8_t *dirichlet, int *status) {
+  or_mesh *h = (or_mesh *)calloc(1, sizeof(or_mesh));
+  if (!h) { *status = OR_E_NOMEM; return NULL; }
+  *status = OR_OK;
+  h->n_nodes = n_nodes; h->n_tets = n_tets;
+
+  /* 1. free numbering */
+  h->free_of_node = (int32_t *)malloc(sizeof(int32_t) * (n_nodes > 0 ? n_nodes : 1));
+  int64_t nf = 0;
+  for (int64_t v = 0; v < n_nodes; v++) h->free_of_node[v] = dirichlet[v] ? -1 : (int32_t)(nf++);
+  h->n_free = nf;
+  h->node_of_free = (int32_t *)malloc(sizeof(int32_t) * (nf > 0 ? nf : 1));
+  for (int64_t v = 0; v < n_nodes; v++) if (!dirichlet[v]) h->node_of_free[h->free_of_node[v]] = (int32_t)v;
+
+  for (int64_t t = 0; t < 4 * n_tets; t++)
+    if (tets[t] < 0 || tets[t] >= n_nodes) {
+      snprintf(h->err, sizeof h->err, "tet %lld has node index %d out of range", (long long)(t / 4), tets[t]);
+      *status = OR_E_MESH; return h;
+    }
+  h->tets = (int32_t *)malloc(sizeof(int32_t) * 4 * (n_tets > 0 ? n_tets : 1));
+  memcpy(h->tets, tets, sizeof(int32_t) * 4 * n_tets);
+
+  /* 2. pattern: node -> incident tets, then per free row collect, sort, unique */
+  int64_t *inc_ptr = (int64_t *)calloc(n_nodes + 1, sizeof(int64_t));
+  for (int64_t t = 0; t < n_tets; t++)
+    for (int a = 0; a < 4; a++) inc_ptr[tets[4 * t + a] + 1]++;
+  for (int64_t v = 0; v < n_nodes; v++) inc_ptr[v + 1] += inc_ptr[v];
+  int32_t *inc = (int32_t *)malloc(sizeof(int32_t) * (4 * n_tets > 0 ? 4 * n_tets : 1));
+  int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (n_nodes > 0 ? n_nodes : 1));
+  for (int64_t v = 0; v < n_nodes; v++) fill[v] = inc_ptr[v];
+  for (int64_t t = 0; t < n_tets; t++)
+    for (int a = 0; a < 4; a++) inc[fill[tets[4 * t + a]]++] = (int32_t)t;
+  free(fill);
+
+  h->row_ptr = (int64_t *)malloc(sizeof(int64_t) * (nf + 1));
+  h->row_ptr[0] = 0;
+  int32_t *buf = NULL; int64_t bufcap = 0;
+  /* first pass: counts */
+  for (int pass = 0; pass < 2; pass++) {
+    for (int64_t i = 0; i < nf; i++) {
+      int64_t v = h->node_of_free[i];
+      int64_t deg = inc_ptr[v + 1] - inc_ptr[v];
+      if (4 * deg > bufcap) { bufcap = 4 * deg; buf = (int32_t *)realloc(buf, sizeof(int32_t) * bufcap); }
+      int64_t m = 0;
+      for (int64_t e = inc_ptr[v]; e < inc_ptr[v + 1]; e++) {
+        int64_t t = inc[e];
+        for (int a = 0; a < 4; a++) {
+          int32_t f = h->free_of_node[tets[4 * t + a]];
+          if (f >= 0) buf[m++] = f;
+        }
+      }
+      qsort(buf, (size_t)m, sizeof(int32_t), cmp_i32);
+      int64_t u = 0;
+      for (int64_t k = 0; k < m; k++) if (u == 0 || buf[k] != buf[u - 1]) buf[u++] = buf[k];
+      if (pass == 0) h->row_ptr[i + 1] = h->row_ptr[i] + u;
+      else memcpy(h->col + h->row_ptr[i], buf, sizeof(int32_t) * u);
+    }
+    if (pass == 0) {
+      h->nnz = h->row_ptr[nf];
+      h->col = (int32_t *)malloc(sizeof(int32_t) * (h->nnz > 0 ? h->nnz : 1));
+    }
+  }
+  free(buf); free(inc); free(inc_ptr);
+
+  /* 3. element-to-nnz scatter map */
+  h->emap = (int32_t *)malloc(sizeof(int32_t) * 16 * (n_tets > 0 ? n_tets : 1));
+  for (int64_t t = 0; t < n_tets; t++)
+    for (int a = 0; a < 4; a++)
+      for (int b = 0; b < 4; b++) {
+        int32_t fa = h->free_of_node[tets[4 * t + a]], fb = h->free_of_node[tets[4 * t + b]];
+        h->emap[16 * t + 4 * a + b] = (fa >= 0 && fb >= 0) ? (int32_t)find_in_row(h, fa, fb) : -1;
+      }
+
+  /* 4. geometry */
+  h->vol = (double *)malloc(sizeof(double) * (n_tets > 0 ? n_tets : 1));
+  h->grad = (double *)malloc(sizeof(double) * 12 * (n_tets > 0 ? n_tets : 1));
+  for (int64_t t = 0; t < n_tets; t++) {
+    double g[4][3];
+    if (!tet_geometry(xyz, tets + 4 * t, &h->vol[t], g)) {
+      snprintf(h->err, sizeof h->err, "tet %lld is inverted or degenerate", (long long)t);
+      *status = OR_E_MESH; return h;
+    }
+    for (int a = 0; a < 4; a++) for (int d = 0; d < 3; d++) h->grad[12 * t + 3 * a + d] = g[a][d];
+  }
+
+  /* 5. K and M values */
+  size_t nb = sizeof(double) * (h->nnz > 0 ? h->nnz : 1);
+  h->K = (double *)calloc(1, nb); h->M = (double *)calloc(1, nb);
+  h->MV = (double *)calloc(1, nb); h->H = (double *)calloc(1, nb); h->A = (double *)calloc(1, nb);
+  h->diag = (double *)calloc(nf > 0 ? nf : 1, sizeof(double));
+  for (int64_t t = 0; t < n_tets; t++) {
+    const double *g = h->grad + 12 * t;
+    for (int a = 0; a < 4; a++)
+      for (int b = 0; b < 4; b++) {
+        int32_t e = h->emap[16 * t + 4 * a + b];
+        if (e < 0) continue;
+        double dot = g[3 * a] * g[3 * b] + g[3 * a + 1] * g[3 * b + 1] + g[3 * a + 2] * g[3 * b + 2];
+        h->K[e] += h->vol[t] * dot;
+        h->M[e] += h->vol[t] * (a == b ? 2.0 : 1.0) / 20.0;
+      }
+  }
+  return h;
+}
+
+void or_sizes(const or_mesh *h, int64_t *n_free, int64_t *nnz) { *n_free = h->n_free; *nnz = h->nnz; }
+
+/* copy-out accessors (row_ptr as int64) */
+void or_get_pattern(const or_mesh *h, int64_t *row_ptr, int32_t *col, int32_t *emap, int32_t *free_of_node) {
+  if (row_ptr) memcpy(row_ptr, h->row_ptr, sizeof(int64_t) * (h->n_free + 1));
+  if (col) memcpy(col, h->col, sizeof(int32_t) * h->nnz);
+  if (emap) memcpy(emap, h->emap, sizeof(int32_t) * 16 * h->n_tets);
+  if (free_of_node) memcpy(free_of_node, h->free_of_node, sizeof(int32_t) * h->n_nodes);
+}
+
+void or_get_values(const or_mesh *h, double *K, double *M, double *MV, double *H, double *A, double *diag,
+                   double *vol) {
+  size_t nb = sizeof(double) * h->nnz;
+  if (K) memcpy(K, h->K, nb);
+  if (M) memcpy(M, h->M, nb);
+  if (MV) memcpy(MV, h->MV, nb);
+  if (H) memcpy(H, h->H, nb);
+  if (A) memcpy(A, h->A, nb);
+  if (diag) memcpy(diag, h->diag, sizeof(double) * h->n_free);
+  if (vol) memcpy(vol, h->vol, sizeof(double) * h->n_tets);
+}
+
+/*
+ * (st4) nonlinear part: (M_V)_ij = ((V_Har+V_xc) phi_i, phi_j), here for a nodal P1
+ * potential V (all nodes, boundary included). The exact element integral of the P1 interpolant
+ * V = sum_k V_k lambda_k against lambda_a lambda_b, from int_T lambda^alpha = 3! alpha! |T| / (3+|alpha|)!:
+ *     MV_T(a,b) = |T| (1 + delta_ab) (V_a + V_b + S_T) / 120,   S_T = sum_{k in T} V_k   (reading Q2).
+ * Accumulated through emap for t ascending, then a, then b. Then H = 1/2 K + M_V and the shifted
+ * operator A = H + mu M (H~ of PAPER.md:553-561), diag = diag(A) (Jacobi preconditioner).
+ * Returns OR_E_NONFINITE if any V is not finite (values are still computed).
+ */
+int or_assemble_veff(or_mesh *h, const double *V, double mu) {
+  int st = OR_OK;
+  for (int64_t v = 0; v < h->n_nodes; v++) if (!isfinite(V[v])) { st = OR_E_NONFINITE; break; }
+  memset(h->MV, 0, sizeof(double) * h->nnz);
+  h->mu = mu;
+  for (int64_t t = 0; t < h->n_tets; t++) {
+    const int32_t *v = h->tets + 4 * t;
+    double S = V[v[0]] + V[v[1]] + V[v[2]] + V[v[3]];
+    for (int a = 0; a < 4; a++)
+      for (int b = 0; b < 4; b++) {
+        int32_t e = h->emap[16 * t + 4 * a + b];
+        if (e < 0) continue;
+        h->MV[e] += h->vol[t] * (a == b ? 2.0 : 1.0) * (V[v[a]] + V[v[b]] + S) / 120.0;
+      }
+  }
+  for (int64_t e = 0; e < h->nnz; e++) {
+    h->H[e] = 0.5 * h->K[e] + h->MV[e];
+    h->A[e] = h->H[e] + mu * h->M[e];
+  }
+  for (int64_t i = 0; i < h->n_free; i++) h->diag[i] = h->A[find_in_row(h, i, (int32_t)i)];
+  return st;
+}
+
+static const double *pick(const or_mesh *h, int which) {
+  switch (which) { case 0: return h->K; case 1: return h->M; case 2: return h->MV;
+                   case 3: return h->H; case 4: return h->A; default: return NULL; }
+}
+
+/* Y = Op X, X and Y are [n_free][N] row-major. which: 0 K, 1 M, 2 MV, 3 H, 4 A. */
+int or_spmm(const or_mesh *h, int which, int N, const double *X, double *Y) {
+  const double *val = pick(h, which);
+  if (!val || N < 1) return OR_E_ARG;
+  for (int64_t i = 0; i < h->n_free; i++)
+    for (int c = 0; c < N; c++) {
+      double s = 0.0;
+      for (int64_t k = h->row_ptr[i]; k < h->row_ptr[i + 1]; k++) s += val[k] * X[(int64_t)h->col[k] * N + c];
+      Y[i * N + c] = s;
+    }
+  return OR_OK;
+}
+
+static double dot_n(const double *a, const double *b, int64_t n) {
+  double s = 0.0;
+  for (int64_t i = 0; i < n; i++) s += a[i] * b[i];
+  return s;
+}
+
+static void matvec(const or_mesh *h, const double *val, const double *x, double *y) {
+  for (int64_t i = 0; i < h->n_free; i++) {
+    double s = 0.0;
+    for (int64_t k = h->row_ptr[i]; k < h->row_ptr[i + 1]; k++) s += val[k] * x[h->col[k]];
+    y[i] = s;
+  }
+}
+
+/*
+ * Algorithm 3, first step (Eq. Aux_Linear_Problem): for i = 1..N independently,
+ *     (H~ psi^_i, v) = (lambda_i + mu)(psi_i, v)  for all v in S_h,
+ * i.e. A u~_i = b_i with A = H + mu M and b_i = (lambda_i + mu) M u_i. Solved by textbook
+ * Jacobi-preconditioned CG (readings Q6, Q7): x0 = u_i, r0 = b - A x0, z = D^{-1} r, p = z;
+ * loop: stop when ||r||_2 <= tol ||b||_2; q = A p; if p.q <= 0 -> NOT_SPD; alpha = r.z / p.q;
+ * x += alpha p; r -= alpha q; z = D^{-1} r; beta = r.z_new / r.z_old; p = z + beta p.
+ * iters[i] = completed updates; relres_rec[i] = ||r||/||b|| (recursive), relres_true[i] =
+ * ||b - A x||/||b||. Returns the worst status over the columns.
+ */
+int or_block_pcg(const or_mesh *h, int N, const double *lambda, const double *U, double *Ut,
+                 double tol, int max_iter, int32_t *iters, double *relres_rec, double *relres_true) {
+  int64_t n = h->n_free;
+  double mu = h->mu;
+  int worst = OR_OK;
+  double *u = (double *)malloc(sizeof(double) * n), *x = (double *)malloc(sizeof(double) * n);
+  double *b = (double *)malloc(sizeof(double) * n), *r = (double *)malloc(sizeof(double) * n);
+  double *z = (double *)malloc(sizeof(double) * n), *p = (double *)malloc(sizeof(double) * n);
+  double *q = (double *)malloc(sizeof(double) * n);
+  for (int c = 0; c < N; c++) {
+    int st = OR_OK;
+    for (int64_t i = 0; i < n; i++) u[i] = U[i * N + c];
+    matvec(h, h->M, u, b);
+    for (int64_t i = 0; i < n; i++) b[i] *= (lambda[c] + mu);
+    matvec(h, h->A, u, q);
+    for (int64_t i = 0; i < n; i++) { x[i] = u[i]; r[i] = b[i] - q[i]; z[i] = r[i] / h->diag[i]; p[i] = z[i]; }
+    double bnorm = sqrt(dot_n(b, b, n));
+    double rz = dot_n(r, z, n);
+    int it = 0;
+    for (;;) {
+      double rnorm = sqrt(dot_n(r, r, n));
+      if (!isfinite(rnorm) || !isfinite(bnorm)) { st = OR_E_NONFINITE; break; }
+      if (rnorm <= tol * bnorm) break;
+      if (it >= max_iter) { st = OR_E_NOT_CONVERGED; break; }
+      matvec(h, h->A, p, q);
+      double pq = dot_n(p, q, n);
+      if (!(pq > 0.0)) { st = OR_E_NOT_SPD; break; }
+      double alpha = rz / pq;
+      for (int64_t i = 0; i < n; i++) { x[i] += alpha * p[i]; r[i] -= alpha * q[i]; z[i] = r[i] / h->diag[i]; }
+      double rz_new = dot_n(r, z, n);
+      double beta = rz_new / rz;
+      rz = rz_new;
+      for (int64_t i = 0; i < n; i++) p[i] = z[i] + beta * p[i];
+      it++;
+    }
+    iters[c] = it;
+    relres_rec[c] = bnorm > 0.0 ? sqrt(dot_n(r, r, n)) / bnorm : sqrt(dot_n(r, r, n));
+    matvec(h, h->A, x, q);
+    for (int64_t i = 0; i < n; i++) q[i] = b[i] - q[i];
+    relres_true[c] = bnorm > 0.0 ? sqrt(dot_n(q, q, n)) / bnorm : sqrt(dot_n(q, q, n));
+    for (int64_t i = 0; i < n; i++) Ut[i * N + c] = x[i];
+    if (st > worst) worst = st;
+  }
+  free(u); free(x); free(b); free(r); free(z); free(p); free(q);
+  return worst;
+}
+
+/*
+ * Projection onto the augmented subspace W = [P | U~]:
+ *   F_A = [[A_H, b_H], [b_H^T, beta]],  F_B = [[B_H, c_H], [c_H^T, gamma]]     (st1-st2)
+ *   A_H = P^T H P (st5), b_H = P^T H U~ (st6), beta = U~^T H U~ (st7),
+ *   B_H = P^T M P, c_H = P^T M U~, gamma = U~^T M U~        (reading Q4)
+ * with the unshifted H = 1/2 K + M_V (reading Q1). P: n_free x n_H CSR. F_* row-major
+ * [(n_H+N)][(n_H+N)], coarse block first. Plain loops over the definitions.
+ */
+int or_project(const or_mesh *h, int64_t n_H, const int32_t *Pptr, const int32_t *Pcol, const double *Pval,
+               int N, const double *Ut, double *FA, double *FB) {
+  int64_t n = h->n_free, D = n_H + N;
+  double *HU = (double *)calloc(n * N > 0 ? n * N : 1, sizeof(double));
+  double *MU = (double *)calloc(n * N > 0 ? n * N : 1, sizeof(double));
+  or_spmm(h, 3, N, Ut, HU);
+  or_spmm(h, 1, N, Ut, MU);
+  memset(FA, 0, sizeof(double) * D * D);
+  memset(FB, 0, sizeof(double) * D * D);
+  /* A_H[c][d] = sum_i sum_j P_ic H_ij P_jd ; B_H with M */
+  for (int64_t i = 0; i < n; i++)
+    for (int64_t k = h->row_ptr[i]; k < h->row_ptr[i + 1]; k++) {
+      int64_t j = h->col[k];
+      for (int32_t s = Pptr[i]; s < Pptr[i + 1]; s++)
+        for (int32_t t = Pptr[j]; t < Pptr[j + 1]; t++) {
+          int64_t c = Pcol[s], d = Pcol[t];
+          FA[c * D + d] += Pval[s] * h->H[k] * Pval[t];
+          FB[c * D + d] += Pval[s] * h->M[k] * Pval[t];
+        }
+    }
+  /* b_H[c][a] = sum_i P_ic (H U~)_ia ; c_H with M */
+  for (int64_t i = 0; i < n; i++)
+    for (int32_t s = Pptr[i]; s < Pptr[i + 1]; s++)
+      for (int a = 0; a < N; a++) {
+        FA[(int64_t)Pcol[s] * D + n_H + a] += Pval[s] * HU[i * N + a];
+        FB[(int64_t)Pcol[s] * D + n_H + a] += Pval[s] * MU[i * N + a];
+      }
+  for (int64_t c = 0; c < n_H; c++)
+    for (int a = 0; a < N; a++) {
+      FA[(n_H + a) * D + c] = FA[c * D + n_H + a];
+      FB[(n_H + a) * D + c] = FB[c * D + n_H + a];
+    }
+  /* beta[a][b] = sum_i U~_ia (H U~)_ib ; gamma with M */
+  for (int a = 0; a < N; a++)
+    for (int b = 0; b < N; b++) {
+      double sa = 0.0, sb = 0.0;
+      for (int64_t i = 0; i < n; i++) { sa += Ut[i * N + a] * HU[i * N + b]; sb += Ut[i * N + a] * MU[i * N + b]; }
+      FA[(n_H + a) * D + n_H + b] = sa;
+      FB[(n_H + a) * D + n_H + b] = sb;
+    }
+  free(HU); free(MU);
+  return OR_OK;
+}
