@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path (one step = ks_assemble_veff + ks_block_solve + ks_project_augmented) on a
+synthetic config of BASELINE.json (default C4: 128^3-cell graded Kuhn mesh, N = 16 orbitals, fp64).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0. Metric (BASELINE.json): orbital-DOF-iterations/s of the block PCG =
+sum over ranks of N * n_free * k / t, k = block iterations of the step's solve, t = max over ranks of the
+device time of the K timed steps. Multi-GPU (torchrun) runs independent problems per rank (weak scaling,
+no data-path collective). `--impl reference` times the CPU oracle (the slow reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import gen  # noqa: E402
+
+METRIC = "orbital-DOF-iterations/s of block PCG"
+UNIT = "orbital-DOF-iterations/s"
+TOL, MAX_ITER = 1e-10, 2000
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+                    help="reference arm: CPU seconds the K+W oracle steps may take in total")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# --------------------------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# --------------------------------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.idx), "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------------------------------
+# algorithmic bytes
+# --------------------------------------------------------------------------------------------------
+def bytes_per_iteration(n, nnz, N, k_v=11):
+    """Textbook Jacobi-PCG iteration: matrix (8 B value + 4 B col per nnz) + row_ptr + d read twice +
+    k_v = 11 touches of [n][N] fp64 vectors (SURVEY.md §8(d) B_it)."""
+    return 12 * nnz + 4 * (n + 1) + 16 * n + 8 * N * n * k_v
+
+
+def bytes_solve_init(n, nnz, N):
+    """Solve prologue r0 = (lambda+mu) M u - A u, x = u, p = z: col + A + M values, row_ptr, d, read u,
+    write r, p, x."""
+    return 20 * nnz + 4 * (n + 1) + 8 * n + 8 * N * n * 4
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+# --------------------------------------------------------------------------------------------------
+# CPU oracle (reference arm / cpu_baseline)
+# --------------------------------------------------------------------------------------------------
+def oracle_step(om, p, ncols):
+    """assemble + block PCG on the first `ncols` orbitals + projection with them (plain oracle, 1 core)."""
+    t0 = time.perf_counter()
+    om.assemble_veff(p.V, p.mu)
+    U = np.ascontiguousarray(p.U[:, :ncols])
+    r = om.block_pcg(p.lam[:ncols], U, tol=TOL, max_iter=MAX_ITER)
+    om.project(p.n_H, p.P_rowptr, p.P_col, p.P_val, r["Ut"])
+    dt = time.perf_counter() - t0
+    k = int(r["iters"].max())
+    return dt, k, ncols * p.n_free * k
+
+
+def run_reference(args, p, rank, world):
+    if rank != 0:
+        return
+    import oracle
+    om = oracle.Mesh.from_problem(p)
+    # size the per-step sample so that all K+W steps fit the budget
+    t1, _, _ = oracle_step(om, p, 1)
+    per_col = max(t1, 1e-3)
+    ncols = int(max(1, min(p.N, args.ref_budget_s / (args.steps + args.warmup) / per_col)))
+    for _ in range(args.warmup):
+        oracle_step(om, p, ncols)
+    tot_t, tot_units, ks = 0.0, 0, []
+    for _ in range(args.steps):
+        dt, k, units = oracle_step(om, p, ncols)
+        tot_t += dt
+        tot_units += units
+        ks.append(k)
+    value = tot_units / tot_t
+    cores = 1
+    sample = (f"{p.cfg['name']}: per step assemble_veff + block PCG on {ncols} of {p.N} orbitals "
+              f"(to tol {TOL:g}, {ks[0]} iterations) + projection with those orbitals; single-threaded C oracle")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(p),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(p):
+    import oracle
+    om = oracle.Mesh.from_problem(p)
+    dt, k, units = oracle_step(om, p, p.N)
+    return {"value": units / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{p.cfg['name']} full step once: assemble_veff + block PCG on all {p.N} orbitals "
+                      f"({k} iterations to tol {TOL:g}) + projection, single-threaded C oracle, {dt:.1f} s",
+            "seconds": dt}
+
+
+def workload_config(p):
+    return {"workload": f"{p.cfg['name']}: graded Kuhn tet mesh {p.n_cells}^3 cells on [-{p.L:g},{p.L:g}]^3, "
+                        f"N={p.N} orbitals, block Jacobi-PCG tol {TOL:g}, coarse {p.nc}^3",
+            "config_id": int(p.cfg["name"][1:]), "nodes": int(p.n_nodes), "n_free": int(p.n_free),
+            "tets": int(p.n_tets), "N": int(p.N), "mu": float(p.mu), "n_H": int(p.n_H),
+            "seed": int(p.cfg["seed"]), "l2": "inputs larger than L2 (working set >> 126 MB); no flush needed"
+            if p.n_free * p.N * 8 * 4 > 126e6 else "working set fits L2 (small config)"}
+
+
+# --------------------------------------------------------------------------------------------------
+# GPU arm
+# --------------------------------------------------------------------------------------------------
+def run_ours(args, p, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2404_19249_b200 as ks
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    ctx = ks.Context(p.xyz, p.tets, p.dirichlet, stream=stream)
+    V = torch.from_numpy(p.V).to(dev)
+    lam = torch.from_numpy(p.lam).to(dev)
+    U = torch.from_numpy(p.U).to(dev)
+    Ut = torch.empty_like(U)
+    D = p.n_H + p.N
+    FA = torch.empty((D, D), dtype=torch.float64, device=dev)
+    FB = torch.empty_like(FA)
+    iters = torch.zeros(p.N, dtype=torch.int32, device=dev)
+    relres = torch.zeros(p.N, dtype=torch.float64, device=dev)
+    ctx.set_coarse(p.n_H, torch.from_numpy(p.P_rowptr).to(dev), torch.from_numpy(p.P_col).to(dev),
+                   torch.from_numpy(p.P_val).to(dev))
+    torch.cuda.synchronize()
+
+    def step():
+        ctx.assemble_veff(V, p.mu)
+        ctx.block_solve(lam, U, Ut, tol=TOL, max_iter=MAX_ITER, iters=iters, relres=relres)
+        ctx.project_augmented(Ut, FA, FB)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    st = ctx.sync()
+    if st != 0:
+        raise RuntimeError(f"warm-up status {st}: {ctx.last_error()}")
+    k_iters = ctx.last_iterations()
+
+    # ---- device-timed region ----
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = ctx.launch_count()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for s in range(args.steps):
+        e0, e1, e2, e3 = ev[s]
+        e0.record(stream)
+        ctx.assemble_veff(V, p.mu)
+        e1.record(stream)
+        ctx.block_solve(lam, U, Ut, tol=TOL, max_iter=MAX_ITER, iters=iters, relres=relres)
+        e2.record(stream)
+        ctx.project_augmented(Ut, FA, FB)
+        e3.record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    launches = ctx.launch_count() - launches0
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    st = ctx.sync()
+    if st != 0:
+        raise RuntimeError(f"timed-run status {st}: {ctx.last_error()}")
+    total_ms = t_start.elapsed_time(t_end)
+    t_asm = float(np.mean([a.elapsed_time(b) for a, b, _, _ in ev]))
+    t_solve = float(np.mean([b.elapsed_time(c) for _, b, c, _ in ev]))
+    t_proj = float(np.mean([c.elapsed_time(d) for _, _, c, d in ev]))
+    k_last = ctx.last_iterations()
+    units_rank = args.steps * p.N * p.n_free * k_last
+
+    # max over ranks of the device time; sum of units
+    if world > 1:
+        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms_max = float(tt.item())
+        uu = torch.tensor([float(units_rank)], dtype=torch.float64, device=dev)
+        dist.all_reduce(uu, op=dist.ReduceOp.SUM)
+        units_all = float(uu.item())
+    else:
+        total_ms_max, units_all = total_ms, float(units_rank)
+    value = units_all / (total_ms_max * 1e-3)
+
+    # ---- e2e through the public API with host (pinned) buffers ----
+    e2e = None
+    if not args.no_e2e:
+        Vh = torch.from_numpy(p.V).pin_memory()
+        lamh = torch.from_numpy(p.lam).pin_memory()
+        Uh = torch.from_numpy(p.U).pin_memory()
+        bufs = None
+        for _ in range(2):
+            _, _, bufs = ks.solve_step_host(ctx, Vh, p.mu, lamh, Uh, bufs, tol=TOL, max_iter=MAX_ITER)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        h0 = torch.cuda.Event(enable_timing=True)
+        h1 = torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
+        for _ in range(args.steps):
+            FAh, FBh, bufs = ks.solve_step_host(ctx, Vh, p.mu, lamh, Uh, bufs, tol=TOL, max_iter=MAX_ITER)
+        h1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = h0.elapsed_time(h1)
+        if world > 1:
+            tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_ms = float(tt.item())
+        h2d = Vh.numel() * 8 + lamh.numel() * 8 + Uh.numel() * 8
+        d2h = 2 * D * D * 8
+        e2e = {"value": units_all / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms / args.steps}
+
+    if rank != 0:
+        return
+    peaks, peak_kind = load_peaks()
+    n, nnz, N = p.n_free, ctx.nnz, p.N
+    alg = bytes_solve_init(n, nnz, N) + k_last * bytes_per_iteration(n, nnz, N)
+    achieved = alg / (t_solve * 1e-3) / 1e9
+    peak = float(peaks["hbm_gbs"])
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", f"traffic_C{p.cfg['name'][1:]}.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": dict(workload_config(p), nnz=int(nnz), block_iters=int(k_last),
+                       parallelism=f"independent problem per GPU x{world}" if world > 1 else "1 GPU"),
+        "roofline": {"bound": "hbm", "kernel": "k_block_pcg (persistent block Jacobi-PCG, one launch per solve)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_kind": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
+                     "alg_bytes_per_launch": int(alg),
+                     "alg_bytes_def": "init (20 nnz + 12 n + 32 N n) + k x textbook B_it (12 nnz + 20 n + 88 N n)"},
+        "phases_ms": {"assemble_veff": t_asm, "block_solve": t_solve, "project_augmented": t_proj},
+        "solve_only_value": N * n * k_last / (t_solve * 1e-3),
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(p)
+        except Exception as ex:  # keep the GPU line even if the oracle cannot run
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                    "sample": f"failed: {ex}"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if world > 1 and args.impl == "ours":
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # independent problem per rank (weak scaling): seed offset by rank
+    p = gen.make_problem(args.config, seed=gen.SEED_BASE + args.config + 1000 * rank)
+    if args.impl == "reference":
+        run_reference(args, p, rank, world)
+    else:
+        run_ours(args, p, rank, world, local)
+    if world > 1 and args.impl == "ours":
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,174 @@
+/*
+ * ks.h -- C ABI of libks, the B200 (sm_100a) hot path of the nonnested augmented subspace method for
+ * the Kohn-Sham equation (arXiv 2404.19249). Citations "PAPER.md:L" are lines of the paper's source.
+ *
+ * The library computes, on one GPU in fp64:
+ *   ks_create             setup once per fine mesh: free numbering (Dirichlet elimination), the CSR
+ *                         pattern of the P1 operators, the element-to-nnz scatter map and its inverse,
+ *                         tet geometry, stiffness K and mass M (st3).
+ *   ks_assemble_veff      V_eff-weighted mass M_V (st4) reassembled on the fixed
+ *                         pattern, H = 1/2 K + M_V, shifted operator A = H + mu M (H~)
+ *                         and its diagonal. Deterministic, no floating-point atomics.
+ *   ks_block_solve        the N linear boundary value problems of Algorithm 3
+ *                         (Aux_Linear_Problem): A u~_i = (lambda_i + mu) M u_i,
+ *                         batched Jacobi-PCG over all N orbitals.
+ *   ks_set_coarse         the interpolation operator P = I_H^h, cached mass blocks.
+ *   ks_project_augmented  F_A, F_B of (st1)-(st2): A_H = P^T H P (st5), b_H = P^T H U~ (st6),
+ *                         beta = U~^T H U~ (st7), B_H = P^T M P, c_H = P^T M U~, gamma = U~^T M U~
+ *                         (PAPER.md:682-759).
+ *
+ * Conventions
+ *   - Pointers named d_* are DEVICE pointers on the context's device; h_* are HOST pointers. The caller
+ *     owns every pointer it passes; the library never frees them and never keeps host pointers past the
+ *     call. Device inputs/outputs must stay valid until the stream work that uses them completes.
+ *   - Internal structures (pattern, maps, values, solver workspace) are allocated by the library with
+ *     cudaMalloc on the context's device in ks_create / ks_set_coarse / on first use of a block size N,
+ *     and freed by ks_destroy. ks_memory_bytes reports the total.
+ *   - Every compute call is asynchronous on the context's stream (a cudaStream_t passed as void*).
+ *     Device-detected conditions (non-finite values, NOT_SPD columns, non-convergence) are latched in a
+ *     device flag word and returned by the next ks_sync. Argument errors are returned immediately and
+ *     launch nothing.
+ *   - Free numbering: free index = rank of a non-Dirichlet node among non-Dirichlet nodes, ascending node
+ *     id. Blocks of orbitals are row-major [n_free][N] (orbital index fastest), 8-byte aligned; 16-byte
+ *     alignment enables the vectorised path.
+ *   - CSR: row_ptr int32 [n_free+1], col int32 [nnz] sorted ascending within a row, diagonal present.
+ *   - emap int32 [16*n_tets]: emap[16 t + 4 a + b] = CSR position of (free(v_a), free(v_b)), -1 if
+ *     either vertex is a Dirichlet node.
+ *   - No exceptions cross the ABI. ks_last_error returns a NUL-terminated message for the last failure.
+ */
+#ifndef KS_H_
+#define KS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KS_ABI_VERSION 1
+
+typedef struct ks_ctx ks_ctx;
+
+typedef enum {
+  KS_OK = 0,
+  KS_E_ARG = 1,            /* invalid argument (null pointer, size, alignment, range) */
+  KS_E_MESH = 2,           /* inverted / degenerate tet or node index out of range (tet id in message) */
+  KS_E_NONFINITE = 3,      /* NaN/Inf met in V_eff or in a solver reduction */
+  KS_E_NOT_SPD = 4,        /* p.Ap <= 0 in some column: A = H + mu M not positive definite (mu too
+                              small, Theorem 1) */
+  KS_E_NOT_CONVERGED = 5,  /* max_iter reached with some column above tolerance; last iterate written */
+  KS_E_CUDA = 6,           /* CUDA runtime error (message has the CUDA error string) */
+  KS_E_NOMEM = 7,          /* device allocation failed */
+  KS_E_STATE = 8           /* call order: e.g. solve before assemble, project before set_coarse */
+} ks_status;
+
+/* Operator selector for ks_spmm / ks_values. */
+typedef enum { KS_OP_K = 0, KS_OP_M = 1, KS_OP_MV = 2, KS_OP_H = 3, KS_OP_A = 4 } ks_op;
+
+/* ABI version (KS_ABI_VERSION) and a static build string. */
+int ks_abi_version(void);
+const char *ks_build_info(void);
+
+/*
+ * Setup of one fine mesh (section 2 of the paper; st3 PAPER.md:733-738).
+ *   h_xyz       [n_nodes][3] f64 node coordinates (host)
+ *   h_tets      [n_tets][4]  i32 node ids, positively oriented (host)
+ *   h_dirichlet [n_nodes]    u8, nonzero = Dirichlet node (psi = 0 on dOmega)
+ *   stream      cudaStream_t (NULL = legacy default stream) on the current device
+ * On success *out is a new context; the call synchronises the stream once (setup is not async).
+ * Errors: KS_E_ARG, KS_E_MESH (first bad tet id in ks_last_error(NULL) and in the ctx message),
+ * KS_E_NOMEM, KS_E_CUDA. On error *out is NULL.
+ */
+ks_status ks_create(int64_t n_nodes, const double *h_xyz, int64_t n_tets, const int32_t *h_tets,
+                    const uint8_t *h_dirichlet, void *stream, ks_ctx **out);
+
+/* Frees the library-owned device memory and the host struct. Safe on NULL. */
+void ks_destroy(ks_ctx *ctx);
+
+/* Re-targets the context to another stream (same device). */
+ks_status ks_set_stream(ks_ctx *ctx, void *stream);
+
+/* Sizes and read-only device views of the setup products (owned by the library). Any out-pointer may
+ * be NULL. d_inv_ptr [nnz+1] / d_inv_idx [contributions] is the inverse scatter map: for nnz e the
+ * entries d_inv_idx[d_inv_ptr[e] .. d_inv_ptr[e+1]) are the emap indices 16 t + 4 a + b that target e,
+ * ascending. */
+ks_status ks_pattern(const ks_ctx *ctx, int64_t *n_free, int64_t *nnz, const int32_t **d_row_ptr,
+                     const int32_t **d_col, const int32_t **d_emap, const int32_t **d_free_of_node,
+                     const int32_t **d_inv_ptr, const int32_t **d_inv_idx);
+
+/* Device views of the value arrays [nnz] and the diagonal of A [n_free]. MV, H, A, diag are defined
+ * after the first ks_assemble_veff (KS_E_STATE before). */
+ks_status ks_values(const ks_ctx *ctx, const double **d_K, const double **d_M, const double **d_MV,
+                    const double **d_H, const double **d_A, const double **d_diag);
+
+/*
+ * (st4) reassembly, and the shifted operator of PAPER.md:553-561:
+ *   (M_V)_ij = sum_T |T| (1+delta_ab) (V_a + V_b + S_T) / 120,  S_T = sum of V over the 4 vertices
+ * (exact integral of the P1 interpolant of the nodal V), then H = 1/2 K + M_V, A = H + mu M, diag(A).
+ *   d_veff [n_nodes] f64, ALL nodes (boundary values enter S_T).   mu >= 0 (shift).
+ * Asynchronous. Deterministic (fixed summation order), no float atomics. Non-finite V latches
+ * KS_E_NONFINITE (reported by ks_sync).
+ */
+ks_status ks_assemble_veff(ks_ctx *ctx, const double *d_veff, double mu);
+
+/* Y = Op X for X, Y [n_free][N] f64 row-major (X != Y). Asynchronous. Parity / benchmarking helper. */
+ks_status ks_spmm(ks_ctx *ctx, ks_op op, int32_t N, const double *d_X, double *d_Y);
+
+/*
+ * Algorithm 3 step 1 (Aux_Linear_Problem): for i = 0..N-1 independently solve
+ *     A u~_i = (lambda_i + mu) M u_i,      A = H + mu M (from the last ks_assemble_veff)
+ * by Jacobi-preconditioned CG from x0 = u_i, batched over the N columns in one persistent kernel:
+ * per-column alpha/beta, a column stops when ||r||_2 <= tol ||b||_2 (recursive residual) and is frozen.
+ *   d_lambda [N] f64, d_U [n_free][N] f64 (input), d_Ut [n_free][N] f64 (output, may not alias d_U)
+ *   tol > 0, max_iter >= 1, 1 <= N <= 64
+ *   d_iters [N] i32 (output, may be NULL): iterations applied to each column
+ *   d_relres [N] f64 (output, may be NULL): recursive ||r||/||b|| at exit
+ * Asynchronous; the status (NOT_SPD, NONFINITE, NOT_CONVERGED) is latched for ks_sync. The last iterate
+ * is always written. Deterministic: fixed partition and reduction order, bitwise reproducible.
+ */
+ks_status ks_block_solve(ks_ctx *ctx, int32_t N, const double *d_lambda, const double *d_U, double *d_Ut,
+                         double tol, int32_t max_iter, int32_t *d_iters, double *d_relres);
+
+/* Number of block iterations (max over columns) of the last ks_block_solve; synchronises the stream. */
+ks_status ks_last_iterations(ks_ctx *ctx, int32_t *h_block_iters);
+
+/* True relative residual ||(lambda_i+mu) M u_i - A u~_i|| / ||(lambda_i+mu) M u_i|| per column into
+ * d_relres [N] (parity helper, one extra SpMM pass). Asynchronous. */
+ks_status ks_true_residual(ks_ctx *ctx, int32_t N, const double *d_lambda, const double *d_U,
+                           const double *d_Ut, double *d_relres);
+
+/*
+ * The interpolation operator P = I_H^h from the coarse space (Alg. 1, 747-753 st5):
+ *   n_H coarse free nodes; d_P_row_ptr [n_free+1] i32, d_P_col [p_nnz] i32 (< n_H), d_P_val [p_nnz] f64.
+ * The library copies P and builds P^T (coarse-major), the pattern of H P, and caches B_H = P^T M P.
+ * Synchronises the stream once. Requires n_H >= 1, at most 4 entries per row.
+ */
+ks_status ks_set_coarse(ks_ctx *ctx, int64_t n_H, const int32_t *d_P_row_ptr, const int32_t *d_P_col,
+                        const double *d_P_val);
+
+/*
+ * Projection onto W = [P | U~] (st1-st7), unshifted H (reading Q1):
+ *   F_A = [[A_H, b_H], [b_H^T, beta]],  F_B = [[B_H, c_H], [c_H^T, gamma]]
+ *   d_Ut [n_free][N] f64; d_FA, d_FB [(n_H+N)][(n_H+N)] f64 row-major, coarse block first.
+ * Asynchronous, deterministic.
+ */
+ks_status ks_project_augmented(ks_ctx *ctx, int32_t N, const double *d_Ut, double *d_FA, double *d_FB);
+
+/* Device memory owned by the library (bytes). */
+ks_status ks_memory_bytes(const ks_ctx *ctx, size_t *bytes);
+
+/* Number of kernel launches issued by this context since creation (for the bench's gpu_launches). */
+ks_status ks_launch_count(const ks_ctx *ctx, int64_t *count);
+
+/* Synchronises the stream, clears and returns the latched device status (worst condition seen since
+ * the previous ks_sync): KS_OK, KS_E_NONFINITE, KS_E_NOT_SPD, KS_E_NOT_CONVERGED, or KS_E_CUDA. */
+ks_status ks_sync(ks_ctx *ctx);
+
+/* Message of the last failure on ctx (or of the last failed ks_create when ctx is NULL). */
+const char *ks_last_error(const ks_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KS_H_ */

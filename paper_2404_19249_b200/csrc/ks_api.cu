@@ -1,0 +1,276 @@
+// ks_api.cu -- C-ABI entry points of libks (include/ks.h): argument validation, context lifetime,
+// status latching, dispatch to the kernels in ks_setup.cu / ks_assemble.cu / ks_pcg.cu / ks_project.cu.
+#include <stdarg.h>
+
+#include <mutex>
+
+#include "ks_internal.cuh"
+
+static std::mutex g_err_mu;
+static std::string g_create_err;
+
+const char *ks_status_name(ks_status s) {
+  switch (s) {
+    case KS_OK: return "KS_OK";
+    case KS_E_ARG: return "KS_E_ARG";
+    case KS_E_MESH: return "KS_E_MESH";
+    case KS_E_NONFINITE: return "KS_E_NONFINITE";
+    case KS_E_NOT_SPD: return "KS_E_NOT_SPD";
+    case KS_E_NOT_CONVERGED: return "KS_E_NOT_CONVERGED";
+    case KS_E_CUDA: return "KS_E_CUDA";
+    case KS_E_NOMEM: return "KS_E_NOMEM";
+    case KS_E_STATE: return "KS_E_STATE";
+  }
+  return "KS_E_?";
+}
+
+ks_status ks_fail(ks_ctx *ctx, ks_status s, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  std::string msg = std::string(ks_status_name(s)) + ": " + buf;
+  if (ctx) ctx->err = msg;
+  return s;
+}
+
+ks_status ks_cuda_check(ks_ctx *ctx, cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return KS_OK;
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return ks_fail(ctx, KS_E_NOMEM, "%s: %s", what, cudaGetErrorString(e));
+  }
+  return ks_fail(ctx, KS_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+ks_status ks_alloc(ks_ctx *ctx, void **ptr, size_t bytes, const char *what) {
+  *ptr = nullptr;
+  cudaError_t e = cudaMalloc(ptr, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *ptr = nullptr;
+    return ks_fail(ctx, KS_E_NOMEM, "cudaMalloc(%zu bytes) for %s: %s", bytes, what, cudaGetErrorString(e));
+  }
+  ctx->bytes += bytes;
+  return KS_OK;
+}
+
+static void free_all(ks_ctx *ctx) {
+  void *ptrs[] = {ctx->tets, ctx->free_of_node, ctx->node_of_free, ctx->row_ptr, ctx->col, ctx->diag_pos,
+                  ctx->emap, ctx->inv_ptr, ctx->inv_idx, ctx->vol, ctx->K, ctx->M, ctx->MV, ctx->H, ctx->A,
+                  ctx->diag, ctx->w_tet, ctx->v_free, ctx->d_flags, ctx->d_block_iters, ctx->r, ctx->p, ctx->q,
+                  ctx->xpad, ctx->upad, ctx->partials, ctx->barrier, ctx->P_ptr, ctx->P_col, ctx->P_val,
+                  ctx->PT_ptr, ctx->PT_row, ctx->PT_val, ctx->G_ptr, ctx->G_col, ctx->G_val, ctx->B_H, ctx->Y_H,
+                  ctx->Y_M, ctx->gram_part};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+}
+
+extern "C" {
+
+int ks_abi_version(void) { return KS_ABI_VERSION; }
+
+#define KS_STR2(x) #x
+#define KS_STR(x) KS_STR2(x)
+const char *ks_build_info(void) {
+  return "libks sm_100a fp64 (nvcc " KS_STR(__CUDACC_VER_MAJOR__) "." KS_STR(__CUDACC_VER_MINOR__) ") " __DATE__;
+}
+
+ks_status ks_create(int64_t n_nodes, const double *h_xyz, int64_t n_tets, const int32_t *h_tets,
+                    const uint8_t *h_dirichlet, void *stream, ks_ctx **out) {
+  if (!out) return KS_E_ARG;
+  *out = nullptr;
+  auto set_err = [](const std::string &m) {
+    std::lock_guard<std::mutex> g(g_err_mu);
+    g_create_err = m;
+  };
+  if (n_nodes < 4 || n_tets < 1 || !h_xyz || !h_tets || !h_dirichlet) {
+    set_err("KS_E_ARG: ks_create needs n_nodes >= 4, n_tets >= 1 and non-null host arrays");
+    return KS_E_ARG;
+  }
+  if (n_nodes > 0x7fffffffLL || 16 * n_tets > 0x7fffffffLL) {
+    set_err("KS_E_ARG: mesh too large for int32 indexing (n_nodes < 2^31, 16 n_tets < 2^31)");
+    return KS_E_ARG;
+  }
+  ks_ctx *ctx = new ks_ctx();
+  ctx->stream = (cudaStream_t)stream;
+  ctx->n_nodes = n_nodes;
+  ctx->n_tets = n_tets;
+  ks_status st = KS_OK;
+  do {
+    if ((st = ks_cuda_check(ctx, cudaGetDevice(&ctx->device), "cudaGetDevice")) != KS_OK) break;
+    if ((st = ks_cuda_check(ctx, cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, ctx->device),
+                            "cudaDeviceGetAttribute")) != KS_OK)
+      break;
+    int coop = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
+    if (!coop) { st = ks_fail(ctx, KS_E_CUDA, "device does not support cooperative launch"); break; }
+    if ((st = ks_alloc_t(ctx, &ctx->d_flags, 1, "flags")) != KS_OK) break;
+    if ((st = ks_alloc_t(ctx, &ctx->d_block_iters, 1, "block iters")) != KS_OK) break;
+    if ((st = ks_alloc_t(ctx, &ctx->barrier, 1, "barrier")) != KS_OK) break;
+    if ((st = ks_cuda_check(ctx, cudaMemsetAsync(ctx->d_flags, 0, 4, ctx->stream), "memset")) != KS_OK) break;
+    if ((st = ks_cuda_check(ctx, cudaMemsetAsync(ctx->d_block_iters, 0, 4, ctx->stream), "memset")) != KS_OK) break;
+    st = ks_setup_mesh(ctx, h_xyz, h_tets, h_dirichlet);
+  } while (0);
+  if (st != KS_OK) {
+    set_err(ctx->err);
+    free_all(ctx);
+    delete ctx;
+    return st;
+  }
+  *out = ctx;
+  return KS_OK;
+}
+
+void ks_destroy(ks_ctx *ctx) {
+  if (!ctx) return;
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  else cudaDeviceSynchronize();
+  free_all(ctx);
+  delete ctx;
+}
+
+ks_status ks_set_stream(ks_ctx *ctx, void *stream) {
+  if (!ctx) return KS_E_ARG;
+  ctx->stream = (cudaStream_t)stream;
+  return KS_OK;
+}
+
+ks_status ks_pattern(const ks_ctx *ctx, int64_t *n_free, int64_t *nnz, const int32_t **d_row_ptr,
+                     const int32_t **d_col, const int32_t **d_emap, const int32_t **d_free_of_node,
+                     const int32_t **d_inv_ptr, const int32_t **d_inv_idx) {
+  if (!ctx) return KS_E_ARG;
+  if (n_free) *n_free = ctx->n_free;
+  if (nnz) *nnz = ctx->nnz;
+  if (d_row_ptr) *d_row_ptr = ctx->row_ptr;
+  if (d_col) *d_col = ctx->col;
+  if (d_emap) *d_emap = ctx->emap;
+  if (d_free_of_node) *d_free_of_node = ctx->free_of_node;
+  if (d_inv_ptr) *d_inv_ptr = ctx->inv_ptr;
+  if (d_inv_idx) *d_inv_idx = ctx->inv_idx;
+  return KS_OK;
+}
+
+ks_status ks_values(const ks_ctx *ctx, const double **d_K, const double **d_M, const double **d_MV,
+                    const double **d_H, const double **d_A, const double **d_diag) {
+  if (!ctx) return KS_E_ARG;
+  if (d_K) *d_K = ctx->K;
+  if (d_M) *d_M = ctx->M;
+  if ((d_MV || d_H || d_A || d_diag) && !ctx->assembled)
+    return ks_fail(const_cast<ks_ctx *>(ctx), KS_E_STATE, "ks_values: call ks_assemble_veff first");
+  if (d_MV) *d_MV = ctx->MV;
+  if (d_H) *d_H = ctx->H;
+  if (d_A) *d_A = ctx->A;
+  if (d_diag) *d_diag = ctx->diag;
+  return KS_OK;
+}
+
+ks_status ks_assemble_veff(ks_ctx *ctx, const double *d_veff, double mu) {
+  if (!ctx) return KS_E_ARG;
+  if (!d_veff) return ks_fail(ctx, KS_E_ARG, "ks_assemble_veff: d_veff is NULL");
+  if (!(mu >= 0.0) || !isfinite(mu)) return ks_fail(ctx, KS_E_ARG, "ks_assemble_veff: mu = %g must be finite and >= 0", mu);
+  return ks_assemble_impl(ctx, d_veff, mu);
+}
+
+static const double *op_values(const ks_ctx *ctx, ks_op op) {
+  switch (op) {
+    case KS_OP_K: return ctx->K;
+    case KS_OP_M: return ctx->M;
+    case KS_OP_MV: return ctx->assembled ? ctx->MV : nullptr;
+    case KS_OP_H: return ctx->assembled ? ctx->H : nullptr;
+    case KS_OP_A: return ctx->assembled ? ctx->A : nullptr;
+  }
+  return nullptr;
+}
+
+ks_status ks_spmm(ks_ctx *ctx, ks_op op, int32_t N, const double *d_X, double *d_Y) {
+  if (!ctx) return KS_E_ARG;
+  if (N < 1 || N > KS_MAX_N) return ks_fail(ctx, KS_E_ARG, "ks_spmm: N = %d outside [1, %d]", N, KS_MAX_N);
+  if (!d_X || !d_Y || d_X == d_Y) return ks_fail(ctx, KS_E_ARG, "ks_spmm: X, Y must be distinct non-null");
+  if (((uintptr_t)d_X & 7) || ((uintptr_t)d_Y & 7)) return ks_fail(ctx, KS_E_ARG, "ks_spmm: X, Y must be 8-byte aligned");
+  const double *v = op_values(ctx, op);
+  if (!v) return ks_fail(ctx, KS_E_STATE, "ks_spmm: operator %d not assembled", (int)op);
+  return ks_spmm_impl(ctx, v, N, d_X, d_Y);
+}
+
+ks_status ks_block_solve(ks_ctx *ctx, int32_t N, const double *d_lambda, const double *d_U, double *d_Ut,
+                         double tol, int32_t max_iter, int32_t *d_iters, double *d_relres) {
+  if (!ctx) return KS_E_ARG;
+  if (N < 1 || N > KS_MAX_N) return ks_fail(ctx, KS_E_ARG, "ks_block_solve: N = %d outside [1, %d]", N, KS_MAX_N);
+  if (!d_lambda || !d_U || !d_Ut) return ks_fail(ctx, KS_E_ARG, "ks_block_solve: null lambda/U/Ut");
+  if (d_U == d_Ut) return ks_fail(ctx, KS_E_ARG, "ks_block_solve: U and Ut must not alias");
+  if (((uintptr_t)d_U & 7) || ((uintptr_t)d_Ut & 7)) return ks_fail(ctx, KS_E_ARG, "ks_block_solve: U/Ut must be 8-byte aligned");
+  if (!(tol > 0.0) || !isfinite(tol)) return ks_fail(ctx, KS_E_ARG, "ks_block_solve: tol = %g must be > 0", tol);
+  if (max_iter < 1) return ks_fail(ctx, KS_E_ARG, "ks_block_solve: max_iter = %d must be >= 1", max_iter);
+  if (!ctx->assembled) return ks_fail(ctx, KS_E_STATE, "ks_block_solve: call ks_assemble_veff first");
+  return ks_solve_impl(ctx, N, d_lambda, d_U, d_Ut, tol, max_iter, d_iters, d_relres);
+}
+
+ks_status ks_last_iterations(ks_ctx *ctx, int32_t *h_block_iters) {
+  if (!ctx || !h_block_iters) return KS_E_ARG;
+  KS_CUDA(ctx, cudaMemcpyAsync(h_block_iters, ctx->d_block_iters, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return KS_OK;
+}
+
+ks_status ks_true_residual(ks_ctx *ctx, int32_t N, const double *d_lambda, const double *d_U, const double *d_Ut,
+                           double *d_relres) {
+  if (!ctx) return KS_E_ARG;
+  if (N < 1 || N > KS_MAX_N || !d_lambda || !d_U || !d_Ut || !d_relres)
+    return ks_fail(ctx, KS_E_ARG, "ks_true_residual: bad arguments");
+  if (!ctx->assembled) return ks_fail(ctx, KS_E_STATE, "ks_true_residual: call ks_assemble_veff first");
+  return ks_true_residual_impl(ctx, N, d_lambda, d_U, d_Ut, d_relres);
+}
+
+ks_status ks_set_coarse(ks_ctx *ctx, int64_t n_H, const int32_t *d_P_row_ptr, const int32_t *d_P_col,
+                        const double *d_P_val) {
+  if (!ctx) return KS_E_ARG;
+  if (n_H < 1 || n_H > 0x7fffffffLL) return ks_fail(ctx, KS_E_ARG, "ks_set_coarse: n_H = %lld", (long long)n_H);
+  if (!d_P_row_ptr || !d_P_col || !d_P_val) return ks_fail(ctx, KS_E_ARG, "ks_set_coarse: null P arrays");
+  ks_status st = ks_set_coarse_impl(ctx, n_H, d_P_row_ptr, d_P_col, d_P_val);
+  if (st != KS_OK) ctx->n_H = 0;
+  return st;
+}
+
+ks_status ks_project_augmented(ks_ctx *ctx, int32_t N, const double *d_Ut, double *d_FA, double *d_FB) {
+  if (!ctx) return KS_E_ARG;
+  if (N < 1 || N > KS_MAX_N) return ks_fail(ctx, KS_E_ARG, "ks_project_augmented: N = %d outside [1, %d]", N, KS_MAX_N);
+  if (!d_Ut || !d_FA || !d_FB || d_FA == d_FB) return ks_fail(ctx, KS_E_ARG, "ks_project_augmented: bad pointers");
+  if (!ctx->assembled) return ks_fail(ctx, KS_E_STATE, "ks_project_augmented: call ks_assemble_veff first");
+  if (ctx->n_H < 1) return ks_fail(ctx, KS_E_STATE, "ks_project_augmented: call ks_set_coarse first");
+  return ks_project_impl(ctx, N, d_Ut, d_FA, d_FB);
+}
+
+ks_status ks_memory_bytes(const ks_ctx *ctx, size_t *bytes) {
+  if (!ctx || !bytes) return KS_E_ARG;
+  *bytes = ctx->bytes;
+  return KS_OK;
+}
+
+ks_status ks_launch_count(const ks_ctx *ctx, int64_t *count) {
+  if (!ctx || !count) return KS_E_ARG;
+  *count = ctx->launches;
+  return KS_OK;
+}
+
+ks_status ks_sync(ks_ctx *ctx) {
+  if (!ctx) return KS_E_ARG;
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) return ks_cuda_check(ctx, e, "cudaStreamSynchronize");
+  unsigned f = 0;
+  KS_CUDA(ctx, cudaMemcpy(&f, ctx->d_flags, 4, cudaMemcpyDeviceToHost));
+  KS_CUDA(ctx, cudaMemset(ctx->d_flags, 0, 4));
+  if (f & KSF_NONFINITE) return ks_fail(ctx, KS_E_NONFINITE, "non-finite value met (V_eff or a solver reduction)");
+  if (f & KSF_NOT_SPD) return ks_fail(ctx, KS_E_NOT_SPD, "p.Ap <= 0 in some column: A = H + mu M not SPD (mu too small)");
+  if (f & KSF_NOT_CONVERGED) return ks_fail(ctx, KS_E_NOT_CONVERGED, "max_iter reached with columns above tolerance");
+  return KS_OK;
+}
+
+const char *ks_last_error(const ks_ctx *ctx) {
+  if (ctx) return ctx->err.c_str();
+  std::lock_guard<std::mutex> g(g_err_mu);
+  return g_create_err.c_str();
+}
+
+}  // extern "C"

@@ -1,0 +1,81 @@
+// ks_assemble.cu -- (st4) reassembly of the V_eff-weighted mass on the fixed pattern,
+// H = 1/2 K + M_V and the shifted operator A = H + mu M. Deterministic, no atomics.
+//
+// The element integral of the P1 interpolant of V against lambda_a lambda_b is
+//     MV_T(a,b) = |T| (1+delta_ab) (V_a + V_b + S_T) / 120,      S_T = V_0 + V_1 + V_2 + V_3.
+// Summed over the tets of an entry it splits into a part proportional to the mass entry and a part that
+// only needs one scalar per tet, w_T = |T| S_T ("assembly"):
+//     off-diagonal (i != j):  (M_V)_ij = (V_i + V_j) M_ij / 6 + sum_{T ∋ i,j} w_T / 120
+//     diagonal:               (M_V)_ii =  V_i M_ii / 3      + sum_{T ∋ i}   w_T / 60
+// since |T| (V_a + V_b)/120 = (V_a + V_b) M_T(a,b)/6 and 2|T| 2V_a/120 = V_a M_T(a,a)/3.
+// Kernel 1 computes w_T per tet and V at free nodes; kernel 2 gathers w_T through the inverse scatter map
+// (the element-to-nnz map grouped by target entry, ascending element) -- a fixed summation order.
+#include "ks_internal.cuh"
+
+namespace {
+
+__global__ void k_tet_weights(const int32_t *__restrict__ tets, const double *__restrict__ vol,
+                              const double *__restrict__ V, int64_t n_tets, const int32_t *__restrict__ node_of_free,
+                              int64_t n_free, double *__restrict__ w, double *__restrict__ v_free,
+                              unsigned *__restrict__ flags) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  bool bad = false;
+  if (i < n_tets) {
+    int4 t = __ldg(reinterpret_cast<const int4 *>(tets) + i);
+    double s = __ldg(V + t.x) + __ldg(V + t.y) + __ldg(V + t.z) + __ldg(V + t.w);
+    bad = !isfinite(s);
+    w[i] = __ldg(vol + i) * s;
+  }
+  if (i < n_free) {
+    double v = __ldg(V + __ldg(node_of_free + i));
+    bad |= !isfinite(v);
+    v_free[i] = v;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, KSF_NONFINITE);
+}
+
+// Half-warp per row: lane j of the half handles entries row_ptr[i] + j, + 16, ...
+__global__ void __launch_bounds__(256) k_assemble_rows(
+    const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col, const int32_t *__restrict__ inv_ptr,
+    const int32_t *__restrict__ inv_idx, const double *__restrict__ w, const double *__restrict__ v_free,
+    const double *__restrict__ K, const double *__restrict__ M, double mu, int64_t n_free, double *__restrict__ MV,
+    double *__restrict__ H, double *__restrict__ A, double *__restrict__ diag) {
+  int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 4;
+  int j = threadIdx.x & 15;
+  if (row >= n_free) return;
+  const double vi = __ldg(v_free + row);
+  const int32_t k1 = __ldg(row_ptr + row + 1);
+  for (int32_t e = __ldg(row_ptr + row) + j; e < k1; e += 16) {
+    const int32_t c = __ldg(col + e);
+    double s = 0.0;
+    const int32_t q1 = __ldg(inv_ptr + e + 1);
+    for (int32_t q = __ldg(inv_ptr + e); q < q1; q++) s += __ldg(w + (__ldg(inv_idx + q) >> 4));
+    const double m = __ldg(M + e);
+    double mv;
+    if (c == row) mv = vi * m / 3.0 + s / 60.0;
+    else mv = (vi + __ldg(v_free + c)) * m / 6.0 + s / 120.0;
+    const double h = 0.5 * __ldg(K + e) + mv;
+    const double a = h + mu * m;
+    MV[e] = mv;
+    H[e] = h;
+    A[e] = a;
+    if (c == row) diag[row] = a;
+  }
+}
+
+}  // namespace
+
+ks_status ks_assemble_impl(ks_ctx *ctx, const double *d_veff, double mu) {
+  cudaStream_t s = ctx->stream;
+  const int64_t n = ctx->n_tets > ctx->n_free ? ctx->n_tets : ctx->n_free;
+  k_tet_weights<<<ks_blocks(n, 256), 256, 0, s>>>(ctx->tets, ctx->vol, d_veff, ctx->n_tets, ctx->node_of_free,
+                                                  ctx->n_free, ctx->w_tet, ctx->v_free, ctx->d_flags);
+  KS_LAUNCHED(ctx);
+  k_assemble_rows<<<ks_blocks(16 * ctx->n_free, 256), 256, 0, s>>>(
+      ctx->row_ptr, ctx->col, ctx->inv_ptr, ctx->inv_idx, ctx->w_tet, ctx->v_free, ctx->K, ctx->M, mu,
+      ctx->n_free, ctx->MV, ctx->H, ctx->A, ctx->diag);
+  KS_LAUNCHED(ctx);
+  ctx->mu = mu;
+  ctx->assembled = true;
+  return KS_OK;
+}

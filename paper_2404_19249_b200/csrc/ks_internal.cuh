@@ -1,0 +1,126 @@
+// ks_internal.cuh -- context struct and device helpers of libks (sm_100a, fp64).
+// Not part of the ABI; see include/ks.h.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string>
+#include <vector>
+
+#include "../../include/ks.h"
+
+// device status bits latched by kernels (reported by ks_sync)
+enum : unsigned {
+  KSF_NONFINITE = 1u,
+  KSF_NOT_SPD = 2u,
+  KSF_NOT_CONVERGED = 4u,
+  KSF_MESH = 8u,
+};
+
+struct ks_ctx {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  int64_t n_nodes = 0, n_tets = 0, n_free = 0, nnz = 0, n_contrib = 0;
+  int64_t launches = 0;
+  size_t bytes = 0;
+  std::vector<void *> allocs;
+
+  // mesh / pattern (library-owned device memory)
+  int32_t *tets = nullptr;          // [4 n_tets]
+  int32_t *free_of_node = nullptr;  // [n_nodes]
+  int32_t *node_of_free = nullptr;  // [n_free]
+  int32_t *row_ptr = nullptr;       // [n_free+1]
+  int32_t *col = nullptr;           // [nnz]
+  int32_t *diag_pos = nullptr;      // [n_free] position of (i,i)
+  int32_t *emap = nullptr;          // [16 n_tets]
+  int32_t *inv_ptr = nullptr;       // [nnz+1]
+  int32_t *inv_idx = nullptr;       // [n_contrib] emap indices 16t+4a+b sorted by target nnz, then index
+  double *vol = nullptr;            // [n_tets]
+  double *K = nullptr, *M = nullptr, *MV = nullptr, *H = nullptr, *A = nullptr;  // [nnz]
+  double *diag = nullptr;           // [n_free] diag(A)
+  double *w_tet = nullptr;          // [n_tets] |T| S_T (assembly scratch)
+  double *v_free = nullptr;         // [n_free] V at free nodes (assembly scratch)
+  double mu = 0.0;
+  bool assembled = false;
+
+  // device status
+  unsigned *d_flags = nullptr;      // latched KSF_* bits
+  int32_t *d_block_iters = nullptr; // [1] block iterations of the last solve
+
+  // solver workspace (grown on demand)
+  int ws_np = 0;                    // padded N the workspace was sized for
+  int64_t ws_rows = 0;
+  double *r = nullptr, *p = nullptr, *q = nullptr, *xpad = nullptr, *upad = nullptr;
+  double *partials = nullptr;       // [grid][4 * 64]
+  unsigned *barrier = nullptr;      // grid barrier counter
+  int64_t partial_cap = 0;
+
+  // coarse space
+  int64_t n_H = 0, p_nnz = 0;
+  int32_t *P_ptr = nullptr, *P_col = nullptr;   // [n_free+1], [p_nnz]
+  double *P_val = nullptr;
+  int32_t *PT_ptr = nullptr, *PT_row = nullptr; // coarse-major P^T: [n_H+1], [p_nnz] fine rows
+  double *PT_val = nullptr;
+  int32_t *G_ptr = nullptr, *G_col = nullptr;   // pattern of H P (n_free x n_H)
+  int64_t g_nnz = 0;
+  double *G_val = nullptr;                      // values of H P (scratch)
+  double *B_H = nullptr;                        // [n_H * n_H] cached P^T M P
+  double *Y_H = nullptr, *Y_M = nullptr;        // [n_free][N] projection scratch
+  int64_t y_cap = 0;
+  double *gram_part = nullptr;                  // [grid][2 N N]
+  int64_t gram_cap = 0;
+
+  std::string err;
+};
+
+#define KS_MAX_N 64
+
+const char *ks_status_name(ks_status s);
+ks_status ks_fail(ks_ctx *ctx, ks_status s, const char *fmt, ...);
+ks_status ks_cuda_check(ks_ctx *ctx, cudaError_t e, const char *what);
+ks_status ks_alloc(ks_ctx *ctx, void **ptr, size_t bytes, const char *what);
+
+#define KS_TRY(expr)                      \
+  do {                                    \
+    ks_status _s = (expr);                \
+    if (_s != KS_OK) return _s;           \
+  } while (0)
+#define KS_CUDA(ctx, expr) KS_TRY(ks_cuda_check((ctx), (expr), #expr))
+
+template <typename T>
+static inline ks_status ks_alloc_t(ks_ctx *ctx, T **ptr, int64_t count, const char *what) {
+  return ks_alloc(ctx, (void **)ptr, sizeof(T) * (size_t)(count > 0 ? count : 1), what);
+}
+
+static inline int ks_blocks(int64_t n, int threads) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > 0x7fffffff) b = 0x7fffffff;
+  return (int)b;
+}
+
+// launch bookkeeping + error check
+#define KS_LAUNCHED(ctx) \
+  do { (ctx)->launches++; KS_CUDA((ctx), cudaGetLastError()); } while (0)
+
+// ---------------------------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// internal entry points implemented in the .cu files
+ks_status ks_setup_mesh(ks_ctx *ctx, const double *h_xyz, const int32_t *h_tets, const uint8_t *h_dir);
+ks_status ks_assemble_impl(ks_ctx *ctx, const double *d_veff, double mu);
+ks_status ks_spmm_impl(ks_ctx *ctx, const double *val, int N, const double *X, double *Y);
+ks_status ks_solve_impl(ks_ctx *ctx, int N, const double *lambda, const double *U, double *Ut, double tol,
+                        int max_iter, int32_t *iters, double *relres);
+ks_status ks_true_residual_impl(ks_ctx *ctx, int N, const double *lambda, const double *U,
+                                const double *Ut, double *relres);
+ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, const int32_t *Pcol,
+                             const double *Pval);
+ks_status ks_project_impl(ks_ctx *ctx, int N, const double *Ut, double *FA, double *FB);

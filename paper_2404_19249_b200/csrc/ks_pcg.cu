@@ -1,0 +1,544 @@
+// ks_pcg.cu -- the N shifted boundary value problems of Algorithm 3 (Aux_Linear_Problem,
+// PAPER.md:634-639):   A u~_i = (lambda_i + mu) M u_i,  A = H + mu M,  i = 1..N,
+// solved as ONE batched Jacobi-preconditioned CG over the [n][NP] orbital block by a persistent
+// cooperative kernel (one launch per solve, no host round trip). Per iteration, with per-column
+// alpha_i, beta_i and masks (DESIGN.md §4 "block PCG"):
+//   S  q = A p                      (multi-RHS CSR SpMM, fused p.q partials)          | grid barrier
+//   U  r -= alpha q, z = r / d      (fused r.z and r.r partials)                       | grid barrier
+//   P  x += alpha p, p = z + beta p (x update deferred to here so p is read once)      | grid barrier
+// Reductions are deterministic: each block owns a fixed, interleaved set of row tiles, reduces in a fixed
+// order and writes one partial per column; after the barrier every block sums the partials in the same
+// fixed order, so all blocks hold bitwise-identical alpha/beta and the result is reproducible run to run.
+// Tiles are interleaved across blocks (tile t -> block t mod G) so that the gathered rows of p form a
+// sweeping front that stays L2-resident.
+#include <cooperative_groups.h>
+
+#include "ks_internal.cuh"
+#include "ks_rowops.cuh"
+
+namespace {
+
+constexpr int PCG_THREADS = 512;
+constexpr int PCG_WARPS = PCG_THREADS / 32;
+
+struct PcgArgs {
+  const int32_t *row_ptr, *col;
+  const double *A, *M, *d;
+  const double *lambda;
+  double mu, tol;
+  const double *U;      // [n][NP] input (possibly padded copy)
+  double *X;            // [n][NP] solution
+  double *r, *p, *q;    // [n][NP] workspace
+  double *partials;     // [G][4*NP]
+  unsigned *bar;
+  unsigned *flags;
+  int32_t *iters_out;   // [N] or null
+  double *relres_out;   // [N] or null
+  int32_t *block_iters_out;
+  int64_t n;
+  int N, ntiles, max_iter;
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid-wide barrier for a cooperative launch (all blocks co-resident). Monotonic counter, reset to 0
+// before the launch; `target` advances by gridDim.x per barrier in every block. The gpu-scope fences
+// make the other blocks' writes visible (and invalidate this SM's L1 lines read before the barrier).
+__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &target) {
+  __syncthreads();
+  target += gridDim.x;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    while (ld_acquire(bar) < target) __nanosleep(20);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// out[j] = sum_{g < G} part[g*stride + j] for j < nv, fixed order, one warp per value.
+__device__ __forceinline__ void reduce_partials(const double *part, int stride, int nv, double *out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = warp; j < nv; j += PCG_WARPS) {
+    double s = 0.0;
+    for (int g = lane; g < (int)gridDim.x; g += 32) s += __ldcg(part + (int64_t)g * stride + j);
+    s = warp_sum(s);
+    if (lane == 0) out[j] = s;
+  }
+  __syncthreads();
+}
+
+template <int NP>
+__global__ void __launch_bounds__(PCG_THREADS, 2) k_block_pcg(PcgArgs a) {
+  constexpr int VEC = Lay<NP>::VEC, LPR = Lay<NP>::LPR, RPW = Lay<NP>::RPW;
+  constexpr int TILE = PCG_WARPS * RPW;              // rows per tile
+  constexpr int TILE_EL = TILE * NP;                 // doubles per tile (1024, or 512 for NP = 1)
+  constexpr int STRIDE = 4 * NP;                     // partial slots per block
+
+  __shared__ double red[PCG_WARPS * 3 * NP];
+  __shared__ double tot[3 * NP];
+  __shared__ double s_alpha[NP], s_beta[NP], s_rho[NP], s_bnorm[NP], s_rr[NP];
+  __shared__ int s_active[NP], s_conv[NP], s_iters[NP];
+  __shared__ int s_any;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = lane / LPR, sub = lane % LPR;
+  const int G = gridDim.x;
+  const int64_t n = a.n;
+  unsigned target = 0;
+  double *part_init = a.partials;                      // region 0: 3 dots (init) / 2 dots (U)
+  double *part_s = a.partials + (int64_t)G * STRIDE;   // region 1: 1 dot (S)
+
+  // ---------------- init: b = (lambda+mu) M u, r = b - A u, x = u, z = r/d, p = z ----------------
+  {
+    double acc[3][VEC];
+#pragma unroll
+    for (int d = 0; d < 3; d++)
+#pragma unroll
+      for (int v = 0; v < VEC; v++) acc[d][v] = 0.0;
+    double sh[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; v++) {
+      int c = sub * VEC + v;
+      sh[v] = (c < a.N ? __ldg(a.lambda + c) : 0.0) + a.mu;
+    }
+    for (int tile = blockIdx.x; tile < a.ntiles; tile += G) {
+      int64_t row = (int64_t)tile * TILE + warp * RPW + slot;
+      if (row < n) {
+        Vec<VEC> au, mu_;
+        row_spmv2<NP>(a.col, a.A, a.M, __ldg(a.row_ptr + row), __ldg(a.row_ptr + row + 1), a.U, sub, au, mu_);
+        const int64_t off = row * NP + sub * VEC;
+        Vec<VEC> u = Vec<VEC>::load(a.U + off);
+        const double dinv = 1.0 / __ldg(a.d + row);
+        Vec<VEC> r, z;
+#pragma unroll
+        for (int v = 0; v < VEC; v++) {
+          double b = sh[v] * mu_.v[v];
+          r.v[v] = b - au.v[v];
+          z.v[v] = r.v[v] * dinv;
+          acc[0][v] += b * b;
+          acc[1][v] += r.v[v] * z.v[v];
+          acc[2][v] += r.v[v] * r.v[v];
+        }
+        r.store(a.r + off);
+        z.store(a.p + off);
+        u.store(a.X + off);
+      }
+    }
+    block_reduce_cols<NP, 3>(acc, red, tot);
+    for (int i = threadIdx.x; i < 3 * NP; i += blockDim.x) part_init[(int64_t)blockIdx.x * STRIDE + i] = tot[i];
+    grid_barrier(a.bar, target);
+    reduce_partials(part_init, STRIDE, 3 * NP, tot);
+    if (threadIdx.x < NP) {
+      const int c = threadIdx.x;
+      double bn = sqrt(tot[c]), rz = tot[NP + c], rr = tot[2 * NP + c];
+      s_bnorm[c] = bn;
+      s_rho[c] = rz;
+      s_rr[c] = rr;
+      s_iters[c] = 0;
+      s_conv[c] = 0;
+      bool real = c < a.N;
+      bool finite = isfinite(bn) && isfinite(rr) && isfinite(rz);
+      if (real && !finite && blockIdx.x == 0) atomicOr(a.flags, KSF_NONFINITE);
+      s_active[c] = real && finite && !(sqrt(rr) <= a.tol * bn);
+    }
+    __syncthreads();
+  }
+
+  // ---------------- iterations ----------------
+  int it = 0;
+  // per-thread streaming layout: element e = tile*TILE_EL + 2*threadIdx.x (+ TILE_EL/2 steps for NP=1)
+  const int c0 = (2 * threadIdx.x) % NP;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      int any = 0;
+      for (int c = 0; c < NP; c++) any |= s_active[c];
+      s_any = any;
+    }
+    __syncthreads();
+    if (!s_any) break;
+    if (it >= a.max_iter) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(a.flags, KSF_NOT_CONVERGED);
+      break;
+    }
+
+    // ---- S: q = A p, p.q ----
+    {
+      double acc[1][VEC];
+#pragma unroll
+      for (int v = 0; v < VEC; v++) acc[0][v] = 0.0;
+      for (int tile = blockIdx.x; tile < a.ntiles; tile += G) {
+        int64_t row = (int64_t)tile * TILE + warp * RPW + slot;
+        if (row < n) {
+          Vec<VEC> q = row_spmv<NP>(a.col, a.A, __ldg(a.row_ptr + row), __ldg(a.row_ptr + row + 1), a.p, sub);
+          const int64_t off = row * NP + sub * VEC;
+          Vec<VEC> pv = Vec<VEC>::load(a.p + off);
+#pragma unroll
+          for (int v = 0; v < VEC; v++) acc[0][v] += pv.v[v] * q.v[v];
+          q.store(a.q + off);
+        }
+      }
+      block_reduce_cols<NP, 1>(acc, red, tot);
+      for (int i = threadIdx.x; i < NP; i += blockDim.x) part_s[(int64_t)blockIdx.x * STRIDE + i] = tot[i];
+      grid_barrier(a.bar, target);
+      reduce_partials(part_s, STRIDE, NP, tot);
+      if (threadIdx.x < NP) {
+        const int c = threadIdx.x;
+        double al = 0.0;
+        if (s_active[c]) {
+          double pq = tot[c];
+          if (!(pq > 0.0)) {
+            if (blockIdx.x == 0) atomicOr(a.flags, isfinite(pq) ? KSF_NOT_SPD : KSF_NONFINITE);
+            s_active[c] = 0;
+          } else {
+            al = s_rho[c] / pq;
+          }
+        }
+        s_alpha[c] = al;
+      }
+      __syncthreads();
+    }
+
+    // ---- U: r -= alpha q; r.z, r.r ----
+    {
+      const double al0 = s_alpha[c0], al1 = s_alpha[(c0 + 1) % NP];
+      double acc[2][VEC];
+#pragma unroll
+      for (int d = 0; d < 2; d++)
+#pragma unroll
+        for (int v = 0; v < VEC; v++) acc[d][v] = 0.0;
+      for (int tile = blockIdx.x; tile < a.ntiles; tile += G) {
+        const int64_t base = (int64_t)tile * TILE_EL;
+        for (int j = 2 * threadIdx.x; j < TILE_EL; j += 2 * PCG_THREADS) {
+          const int64_t e = base + j;
+          if (e >= n * NP) break;
+          double2 r = *reinterpret_cast<const double2 *>(a.r + e);
+          double2 q = *reinterpret_cast<const double2 *>(a.q + e);
+          double d0, d1;
+          if (NP == 1) { d0 = __ldg(a.d + e); d1 = (e + 1 < n) ? __ldg(a.d + e + 1) : 1.0; }
+          else { d0 = d1 = __ldg(a.d + e / NP); }
+          if (NP == 1) {
+            r.x -= al0 * q.x; r.y -= al0 * q.y;
+            double z0 = r.x / d0, z1 = r.y / d1;
+            acc[0][0] += r.x * z0 + r.y * z1;
+            acc[1][0] += r.x * r.x + r.y * r.y;
+          } else {
+            r.x -= al0 * q.x; r.y -= al1 * q.y;
+            acc[0][0] += r.x * (r.x / d0);
+            acc[0][VEC - 1] += r.y * (r.y / d1);
+            acc[1][0] += r.x * r.x;
+            acc[1][VEC - 1] += r.y * r.y;
+          }
+          *reinterpret_cast<double2 *>(a.r + e) = r;
+        }
+      }
+      block_reduce_cols<NP, 2>(acc, red, tot);
+      for (int i = threadIdx.x; i < 2 * NP; i += blockDim.x) part_init[(int64_t)blockIdx.x * STRIDE + i] = tot[i];
+      grid_barrier(a.bar, target);
+      reduce_partials(part_init, STRIDE, 2 * NP, tot);
+      if (threadIdx.x < NP) {
+        const int c = threadIdx.x;
+        double be = 0.0;
+        int conv = 0;
+        if (s_active[c]) {
+          double rz = tot[c], rr = tot[NP + c];
+          s_iters[c] += 1;
+          if (!isfinite(rz) || !isfinite(rr)) {
+            if (blockIdx.x == 0) atomicOr(a.flags, KSF_NONFINITE);
+            conv = 1;
+          } else {
+            be = rz / s_rho[c];
+            s_rho[c] = rz;
+            s_rr[c] = rr;
+            conv = sqrt(rr) <= a.tol * s_bnorm[c];
+          }
+          if (conv) be = 0.0;
+        }
+        s_beta[c] = be;
+        s_conv[c] = conv;
+      }
+      __syncthreads();
+    }
+
+    // ---- P: x += alpha p; p = r/d + beta p ----
+    {
+      const double al0 = s_alpha[c0], al1 = s_alpha[(c0 + 1) % NP];
+      const double be0 = s_beta[c0], be1 = s_beta[(c0 + 1) % NP];
+      for (int tile = blockIdx.x; tile < a.ntiles; tile += G) {
+        const int64_t base = (int64_t)tile * TILE_EL;
+        for (int j = 2 * threadIdx.x; j < TILE_EL; j += 2 * PCG_THREADS) {
+          const int64_t e = base + j;
+          if (e >= n * NP) break;
+          double2 r = *reinterpret_cast<const double2 *>(a.r + e);
+          double2 p = *reinterpret_cast<const double2 *>(a.p + e);
+          double2 x = *reinterpret_cast<const double2 *>(a.X + e);
+          double d0, d1;
+          if (NP == 1) { d0 = __ldg(a.d + e); d1 = (e + 1 < n) ? __ldg(a.d + e + 1) : 1.0; }
+          else { d0 = d1 = __ldg(a.d + e / NP); }
+          x.x += al0 * p.x;
+          x.y += al1 * p.y;
+          p.x = r.x / d0 + be0 * p.x;
+          p.y = r.y / d1 + be1 * p.y;
+          *reinterpret_cast<double2 *>(a.X + e) = x;
+          *reinterpret_cast<double2 *>(a.p + e) = p;
+        }
+      }
+      if (threadIdx.x < NP && s_conv[threadIdx.x]) s_active[threadIdx.x] = 0;
+      it++;
+      grid_barrier(a.bar, target);
+    }
+  }
+
+  if (blockIdx.x == 0) {
+    for (int c = threadIdx.x; c < a.N; c += blockDim.x) {
+      if (a.iters_out) a.iters_out[c] = s_iters[c];
+      if (a.relres_out) a.relres_out[c] = s_bnorm[c] > 0.0 ? sqrt(s_rr[c]) / s_bnorm[c] : sqrt(s_rr[c]);
+    }
+    if (threadIdx.x == 0) *a.block_iters_out = it;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// standalone multi-RHS SpMM (parity / benchmarking) and helpers
+// ---------------------------------------------------------------------------------------------
+template <int NP>
+__global__ void __launch_bounds__(256) k_spmm(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                                              const double *__restrict__ val, const double *__restrict__ X,
+                                              double *__restrict__ Y, int64_t n) {
+  constexpr int VEC = Lay<NP>::VEC, LPR = Lay<NP>::LPR;
+  const int64_t gl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t row = gl / LPR;
+  const int sub = (int)(gl % LPR);
+  if (row >= n) return;
+  Vec<VEC> y = row_spmv<NP>(col, val, __ldg(row_ptr + row), __ldg(row_ptr + row + 1), X, sub);
+  y.store(Y + row * NP + sub * VEC);
+}
+
+__global__ void k_spmm_generic(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                               const double *__restrict__ val, const double *__restrict__ X, double *__restrict__ Y,
+                               int64_t n, int N) {
+  const int64_t gl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gl >= n * N) return;
+  const int64_t row = gl / N;
+  const int c = (int)(gl % N);
+  double s = 0.0;
+  for (int32_t k = row_ptr[row]; k < row_ptr[row + 1]; k++) s = fma(val[k], X[(int64_t)col[k] * N + c], s);
+  Y[gl] = s;
+}
+
+// [n][N] <-> [n][NP] with zero padding
+__global__ void k_pad(const double *__restrict__ src, int N, double *__restrict__ dst, int NP, int64_t n) {
+  const int64_t gl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gl >= n * NP) return;
+  const int64_t row = gl / NP;
+  const int c = (int)(gl % NP);
+  dst[gl] = c < N ? src[row * N + c] : 0.0;
+}
+
+__global__ void k_unpad(const double *__restrict__ src, int NP, double *__restrict__ dst, int N, int64_t n) {
+  const int64_t gl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gl >= n * N) return;
+  dst[gl] = src[(gl / N) * NP + gl % N];
+}
+
+// true residual partials: per block sums of b^2 and (b - A ut)^2 per column (generic layout)
+__global__ void k_true_residual(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                                const double *__restrict__ A, const double *__restrict__ M,
+                                const double *__restrict__ lambda, double mu, const double *__restrict__ U,
+                                const double *__restrict__ Ut, int64_t n, int N, double *__restrict__ part) {
+  // one thread per (row, column); block handles a contiguous range; partial per block per column
+  extern __shared__ double sh[];  // [2][blockDim]
+  const int64_t gl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double bb = 0.0, rr = 0.0;
+  int c = -1;
+  if (gl < n * N) {
+    const int64_t row = gl / N;
+    c = (int)(gl % N);
+    double mu_ = 0.0, au = 0.0;
+    for (int32_t k = row_ptr[row]; k < row_ptr[row + 1]; k++) {
+      mu_ = fma(M[k], U[(int64_t)col[k] * N + c], mu_);
+      au = fma(A[k], Ut[(int64_t)col[k] * N + c], au);
+    }
+    double b = (lambda[c] + mu) * mu_;
+    bb = b * b;
+    rr = (b - au) * (b - au);
+  }
+  sh[threadIdx.x] = bb;
+  sh[blockDim.x + threadIdx.x] = rr;
+  __syncthreads();
+  // column-wise sums in fixed order by thread 0..N-1
+  for (int cc = threadIdx.x; cc < N; cc += blockDim.x) {
+    double sb = 0.0, sr = 0.0;
+    const int64_t first = blockIdx.x * (int64_t)blockDim.x;
+    for (int t = 0; t < (int)blockDim.x; t++) {
+      const int64_t g = first + t;
+      if (g < n * N && (int)(g % N) == cc) { sb += sh[t]; sr += sh[blockDim.x + t]; }
+    }
+    part[(int64_t)blockIdx.x * 2 * N + cc] = sb;
+    part[(int64_t)blockIdx.x * 2 * N + N + cc] = sr;
+  }
+}
+
+__global__ void k_true_residual_final(const double *__restrict__ part, int nblk, int N, double *__restrict__ out) {
+  for (int c = threadIdx.x; c < N; c += blockDim.x) {
+    double sb = 0.0, sr = 0.0;
+    for (int b = 0; b < nblk; b++) { sb += part[(int64_t)b * 2 * N + c]; sr += part[(int64_t)b * 2 * N + N + c]; }
+    out[c] = sb > 0.0 ? sqrt(sr) / sqrt(sb) : sqrt(sr);
+  }
+}
+
+int pad_np(int N) {
+  int np = 1;
+  while (np < N) np <<= 1;
+  return np;
+}
+
+template <int NP>
+ks_status launch_pcg(ks_ctx *ctx, PcgArgs &a) {
+  constexpr int TILE = PCG_WARPS * Lay<NP>::RPW;
+  a.ntiles = (int)((a.n + TILE - 1) / TILE);
+  int per_sm = 0;
+  KS_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_pcg<NP>, PCG_THREADS, 0));
+  if (per_sm < 1) return ks_fail(ctx, KS_E_CUDA, "k_block_pcg<%d> cannot be resident", NP);
+  int G = per_sm * ctx->sm_count;
+  if (G > a.ntiles) G = a.ntiles;
+  if ((int64_t)G * 4 * NP * 2 > ctx->partial_cap) {
+    if (ctx->partials) { cudaFree(ctx->partials); ctx->partials = nullptr; }
+    ctx->partial_cap = (int64_t)G * 4 * NP * 2;
+    KS_TRY(ks_alloc_t(ctx, &ctx->partials, ctx->partial_cap, "pcg partials"));
+  }
+  a.partials = ctx->partials;
+  KS_CUDA(ctx, cudaMemsetAsync(ctx->barrier, 0, sizeof(unsigned), ctx->stream));
+  void *args[] = {&a};
+  KS_CUDA(ctx, cudaLaunchCooperativeKernel((const void *)k_block_pcg<NP>, dim3(G), dim3(PCG_THREADS), args, 0,
+                                           ctx->stream));
+  ctx->launches++;
+  return KS_OK;
+}
+
+template <int NP>
+void launch_spmm(ks_ctx *ctx, const double *val, const double *X, double *Y) {
+  const int64_t threads = ctx->n_free * Lay<NP>::LPR;
+  k_spmm<NP><<<ks_blocks(threads, 256), 256, 0, ctx->stream>>>(ctx->row_ptr, ctx->col, val, X, Y, ctx->n_free);
+}
+
+}  // namespace
+
+static bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+ks_status ks_spmm_impl(ks_ctx *ctx, const double *val, int N, const double *X, double *Y) {
+  const int np = pad_np(N);
+  if (np == N && aligned16(X) && aligned16(Y)) {
+    switch (N) {
+      case 1: launch_spmm<1>(ctx, val, X, Y); break;
+      case 2: launch_spmm<2>(ctx, val, X, Y); break;
+      case 4: launch_spmm<4>(ctx, val, X, Y); break;
+      case 8: launch_spmm<8>(ctx, val, X, Y); break;
+      case 16: launch_spmm<16>(ctx, val, X, Y); break;
+      case 32: launch_spmm<32>(ctx, val, X, Y); break;
+      case 64: launch_spmm<64>(ctx, val, X, Y); break;
+    }
+  } else {
+    k_spmm_generic<<<ks_blocks(ctx->n_free * N, 256), 256, 0, ctx->stream>>>(ctx->row_ptr, ctx->col, val, X, Y,
+                                                                             ctx->n_free, N);
+  }
+  KS_LAUNCHED(ctx);
+  return KS_OK;
+}
+
+static ks_status ensure_solver_ws(ks_ctx *ctx, int np) {
+  if (ctx->ws_np >= np && ctx->ws_rows == ctx->n_free) return KS_OK;
+  for (double **b : {&ctx->r, &ctx->p, &ctx->q, &ctx->xpad, &ctx->upad})
+    if (*b) { cudaFree(*b); *b = nullptr; }
+  const int64_t cnt = ctx->n_free * (int64_t)np + 2;  // +2: NP=1 streaming reads pairs
+  KS_TRY(ks_alloc_t(ctx, &ctx->r, cnt, "pcg r"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->p, cnt, "pcg p"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->q, cnt, "pcg q"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->xpad, cnt, "pcg x pad"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->upad, cnt, "pcg u pad"));
+  ctx->ws_np = np;
+  ctx->ws_rows = ctx->n_free;
+  return KS_OK;
+}
+
+ks_status ks_solve_impl(ks_ctx *ctx, int N, const double *lambda, const double *U, double *Ut, double tol,
+                        int max_iter, int32_t *iters, double *relres) {
+  const int np = pad_np(N);
+  KS_TRY(ensure_solver_ws(ctx, np));
+  const int64_t n = ctx->n_free;
+  // NP = 1 streams element pairs: pad to an even element count via the internal buffers
+  const bool direct = (np == N) && aligned16(U) && aligned16(Ut) && !(np == 1 && (n & 1));
+  const double *u = U;
+  double *x = Ut;
+  if (!direct) {
+    KS_CUDA(ctx, cudaMemsetAsync(ctx->upad, 0, sizeof(double) * (n * np + 2), ctx->stream));
+    KS_CUDA(ctx, cudaMemsetAsync(ctx->xpad, 0, sizeof(double) * (n * np + 2), ctx->stream));
+    k_pad<<<ks_blocks(n * np, 256), 256, 0, ctx->stream>>>(U, N, ctx->upad, np, n);
+    KS_LAUNCHED(ctx);
+    u = ctx->upad;
+    x = ctx->xpad;
+  }
+  if (np == 1) {
+    // keep the odd tail element finite for the pairwise streaming phases
+    KS_CUDA(ctx, cudaMemsetAsync(ctx->r + n, 0, sizeof(double) * 2, ctx->stream));
+    KS_CUDA(ctx, cudaMemsetAsync(ctx->q + n, 0, sizeof(double) * 2, ctx->stream));
+    KS_CUDA(ctx, cudaMemsetAsync(ctx->p + n, 0, sizeof(double) * 2, ctx->stream));
+  }
+  PcgArgs a;
+  a.row_ptr = ctx->row_ptr;
+  a.col = ctx->col;
+  a.A = ctx->A;
+  a.M = ctx->M;
+  a.d = ctx->diag;
+  a.lambda = lambda;
+  a.mu = ctx->mu;
+  a.tol = tol;
+  a.U = u;
+  a.X = x;
+  a.r = ctx->r;
+  a.p = ctx->p;
+  a.q = ctx->q;
+  a.bar = ctx->barrier;
+  a.flags = ctx->d_flags;
+  a.iters_out = iters;
+  a.relres_out = relres;
+  a.block_iters_out = ctx->d_block_iters;
+  a.n = n;
+  a.N = N;
+  a.max_iter = max_iter;
+  switch (np) {
+    case 1: KS_TRY(launch_pcg<1>(ctx, a)); break;
+    case 2: KS_TRY(launch_pcg<2>(ctx, a)); break;
+    case 4: KS_TRY(launch_pcg<4>(ctx, a)); break;
+    case 8: KS_TRY(launch_pcg<8>(ctx, a)); break;
+    case 16: KS_TRY(launch_pcg<16>(ctx, a)); break;
+    case 32: KS_TRY(launch_pcg<32>(ctx, a)); break;
+    case 64: KS_TRY(launch_pcg<64>(ctx, a)); break;
+    default: return ks_fail(ctx, KS_E_ARG, "N=%d unsupported", N);
+  }
+  if (!direct) {
+    k_unpad<<<ks_blocks(n * N, 256), 256, 0, ctx->stream>>>(ctx->xpad, np, Ut, N, n);
+    KS_LAUNCHED(ctx);
+  }
+  return KS_OK;
+}
+
+ks_status ks_true_residual_impl(ks_ctx *ctx, int N, const double *lambda, const double *U, const double *Ut,
+                                double *relres) {
+  const int64_t total = ctx->n_free * N;
+  const int T = 256;
+  const int nblk = ks_blocks(total, T);
+  double *part = nullptr;
+  KS_CUDA(ctx, cudaMallocAsync((void **)&part, sizeof(double) * 2 * N * (size_t)nblk, ctx->stream));
+  k_true_residual<<<nblk, T, 2 * T * sizeof(double), ctx->stream>>>(ctx->row_ptr, ctx->col, ctx->A, ctx->M, lambda,
+                                                                     ctx->mu, U, Ut, ctx->n_free, N, part);
+  KS_LAUNCHED(ctx);
+  k_true_residual_final<<<1, 64, 0, ctx->stream>>>(part, nblk, N, relres);
+  KS_LAUNCHED(ctx);
+  KS_CUDA(ctx, cudaFreeAsync(part, ctx->stream));
+  return KS_OK;
+}

@@ -1,0 +1,288 @@
+"""Thin Python binding of libks (include/ks.h): argument marshalling only.
+
+Every compute step runs in the CUDA kernels of libks.so (sm_100a). PyTorch provides device memory and
+streams. There is no CPU fallback: if libks.so is missing or no CUDA device is present, calls raise.
+Function names follow the C ABI (ks_create -> Context(...), ks_assemble_veff -> ctx.assemble_veff, ...).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libks.so")
+
+KS_OK, KS_E_ARG, KS_E_MESH, KS_E_NONFINITE, KS_E_NOT_SPD, KS_E_NOT_CONVERGED, KS_E_CUDA, KS_E_NOMEM, \
+    KS_E_STATE = range(9)
+STATUS_NAMES = {0: "KS_OK", 1: "KS_E_ARG", 2: "KS_E_MESH", 3: "KS_E_NONFINITE", 4: "KS_E_NOT_SPD",
+                5: "KS_E_NOT_CONVERGED", 6: "KS_E_CUDA", 7: "KS_E_NOMEM", 8: "KS_E_STATE"}
+OPS = {"K": 0, "M": 1, "MV": 2, "H": 3, "A": 4}
+
+# every symbol declared in include/ks.h (checked by tests/test_abi.py)
+EXPORTS = ["ks_abi_version", "ks_build_info", "ks_create", "ks_destroy", "ks_set_stream", "ks_pattern",
+           "ks_values", "ks_assemble_veff", "ks_spmm", "ks_block_solve", "ks_last_iterations",
+           "ks_true_residual", "ks_set_coarse", "ks_project_augmented", "ks_memory_bytes", "ks_launch_count",
+           "ks_sync", "ks_last_error"]
+
+
+class KSError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libks.so (no build, no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libks.so not found at {path}; run __graft_entry__.build() "
+                          "(python -c 'import __graft_entry__ as g; g.build()')")
+    L = C.CDLL(path)
+    vp, i64, i32, dbl, st = C.c_void_p, C.c_int64, C.c_int32, C.c_double, C.c_int
+    sig = {
+        "ks_abi_version": (C.c_int, []),
+        "ks_build_info": (C.c_char_p, []),
+        "ks_create": (st, [i64, vp, i64, vp, vp, vp, C.POINTER(vp)]),
+        "ks_destroy": (None, [vp]),
+        "ks_set_stream": (st, [vp, vp]),
+        "ks_pattern": (st, [vp, C.POINTER(i64), C.POINTER(i64)] + [C.POINTER(vp)] * 6),
+        "ks_values": (st, [vp] + [C.POINTER(vp)] * 6),
+        "ks_assemble_veff": (st, [vp, vp, dbl]),
+        "ks_spmm": (st, [vp, C.c_int, i32, vp, vp]),
+        "ks_block_solve": (st, [vp, i32, vp, vp, vp, dbl, i32, vp, vp]),
+        "ks_last_iterations": (st, [vp, C.POINTER(i32)]),
+        "ks_true_residual": (st, [vp, i32, vp, vp, vp, vp]),
+        "ks_set_coarse": (st, [vp, i64, vp, vp, vp]),
+        "ks_project_augmented": (st, [vp, i32, vp, vp, vp]),
+        "ks_memory_bytes": (st, [vp, C.POINTER(C.c_size_t)]),
+        "ks_launch_count": (st, [vp, C.POINTER(i64)]),
+        "ks_sync": (st, [vp]),
+        "ks_last_error": (C.c_char_p, [vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def _ptr(t) -> int:
+    return t.data_ptr()
+
+
+def _check_cuda_tensor(t, dtype, shape=None, name="tensor"):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA torch.Tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must have dtype {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    return t
+
+
+class Context:
+    """ks_create .. ks_destroy. Host mesh arrays are numpy; everything else lives in torch CUDA tensors."""
+
+    def __init__(self, xyz, tets, dirichlet, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("libks needs a CUDA device (no CPU fallback)")
+        L = load_library()
+        self._L = L
+        xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+        tets = np.ascontiguousarray(tets, dtype=np.int32)
+        dirichlet = np.ascontiguousarray(dirichlet, dtype=np.uint8)
+        self.n_nodes, self.n_tets = xyz.shape[0], tets.shape[0]
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        h = C.c_void_p()
+        s = L.ks_create(self.n_nodes, xyz.ctypes.data, self.n_tets, tets.ctypes.data, dirichlet.ctypes.data,
+                        C.c_void_p(self.stream.cuda_stream), C.byref(h))
+        if s != KS_OK:
+            raise KSError(s, L.ks_last_error(None).decode())
+        self._h = h
+        nf, nnz = C.c_int64(), C.c_int64()
+        self._call(L.ks_pattern(self._h, C.byref(nf), C.byref(nnz), *([None] * 6)))
+        self.n_free, self.nnz = nf.value, nnz.value
+        self.n_H = None
+        self.mu = None
+
+    # -- plumbing --------------------------------------------------------------------------------
+    def _call(self, status):
+        if status != KS_OK:
+            raise KSError(status, self._L.ks_last_error(self._h).decode())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.ks_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream):
+        self.stream = stream
+        self._call(self._L.ks_set_stream(self._h, C.c_void_p(stream.cuda_stream)))
+
+    def _view(self, dptr, count, dtype):
+        """Copy a library-owned device array into a new torch tensor (on the ctx stream)."""
+        import torch
+        out = torch.empty(count, dtype=dtype, device=self.device)
+        if count:
+            with torch.cuda.stream(self.stream):
+                # device-to-device copy through a torch view of the raw pointer
+                src = _raw_tensor(dptr, count, dtype, self.device)
+                out.copy_(src)
+        return out
+
+    # -- ABI calls ---------------------------------------------------------------------------------
+    def pattern(self):
+        """(row_ptr, col, emap, free_of_node, inv_ptr, inv_idx) as new int32 CUDA tensors."""
+        import torch
+        ptrs = [C.c_void_p() for _ in range(6)]
+        self._call(self._L.ks_pattern(self._h, None, None, *[C.byref(p) for p in ptrs]))
+        inv_ptr = self._view(ptrs[4].value, self.nnz + 1, torch.int32)
+        n_contrib = int(inv_ptr[-1].item())
+        sizes = [self.n_free + 1, self.nnz, 16 * self.n_tets, self.n_nodes, self.nnz + 1, n_contrib]
+        out = [self._view(p.value, s, torch.int32) for p, s in zip(ptrs, sizes)]
+        return tuple(out)
+
+    def values(self):
+        """dict K, M, MV, H, A, diag of new float64 CUDA tensors (copies)."""
+        import torch
+        ptrs = [C.c_void_p() for _ in range(6)]
+        self._call(self._L.ks_values(self._h, *[C.byref(p) for p in ptrs]))
+        names = ["K", "M", "MV", "H", "A", "diag"]
+        return {k: self._view(p.value, self.n_free if k == "diag" else self.nnz, torch.float64)
+                for k, p in zip(names, ptrs)}
+
+    def assemble_veff(self, veff, mu: float):
+        import torch
+        _check_cuda_tensor(veff, torch.float64, (self.n_nodes,), "veff")
+        self._call(self._L.ks_assemble_veff(self._h, _ptr(veff), float(mu)))
+        self.mu = float(mu)
+
+    def spmm(self, op: str, X, Y=None):
+        import torch
+        _check_cuda_tensor(X, torch.float64, None, "X")
+        N = X.shape[1] if X.dim() == 2 else 1
+        if Y is None:
+            Y = torch.empty_like(X)
+        self._call(self._L.ks_spmm(self._h, OPS[op], N, _ptr(X), _ptr(Y)))
+        return Y
+
+    def block_solve(self, lam, U, Ut=None, tol=1e-10, max_iter=2000, iters=None, relres=None):
+        import torch
+        _check_cuda_tensor(U, torch.float64, None, "U")
+        N = U.shape[1]
+        _check_cuda_tensor(lam, torch.float64, (N,), "lambda")
+        if Ut is None:
+            Ut = torch.empty_like(U)
+        if iters is None:
+            iters = torch.zeros(N, dtype=torch.int32, device=U.device)
+        if relres is None:
+            relres = torch.zeros(N, dtype=torch.float64, device=U.device)
+        self._call(self._L.ks_block_solve(self._h, N, _ptr(lam), _ptr(U), _ptr(Ut), float(tol), int(max_iter),
+                                          _ptr(iters), _ptr(relres)))
+        return Ut, iters, relres
+
+    def last_iterations(self) -> int:
+        v = C.c_int32()
+        self._call(self._L.ks_last_iterations(self._h, C.byref(v)))
+        return v.value
+
+    def true_residual(self, lam, U, Ut):
+        import torch
+        N = U.shape[1]
+        out = torch.empty(N, dtype=torch.float64, device=U.device)
+        self._call(self._L.ks_true_residual(self._h, N, _ptr(lam), _ptr(U), _ptr(Ut), _ptr(out)))
+        return out
+
+    def set_coarse(self, n_H: int, P_rowptr, P_col, P_val):
+        import torch
+        _check_cuda_tensor(P_rowptr, torch.int32, (self.n_free + 1,), "P_rowptr")
+        _check_cuda_tensor(P_col, torch.int32, None, "P_col")
+        _check_cuda_tensor(P_val, torch.float64, None, "P_val")
+        self._call(self._L.ks_set_coarse(self._h, int(n_H), _ptr(P_rowptr), _ptr(P_col), _ptr(P_val)))
+        self.n_H = int(n_H)
+
+    def project_augmented(self, Ut, FA=None, FB=None):
+        import torch
+        N = Ut.shape[1]
+        D = self.n_H + N
+        if FA is None:
+            FA = torch.empty((D, D), dtype=torch.float64, device=Ut.device)
+        if FB is None:
+            FB = torch.empty((D, D), dtype=torch.float64, device=Ut.device)
+        self._call(self._L.ks_project_augmented(self._h, N, _ptr(Ut), _ptr(FA), _ptr(FB)))
+        return FA, FB
+
+    def memory_bytes(self) -> int:
+        v = C.c_size_t()
+        self._call(self._L.ks_memory_bytes(self._h, C.byref(v)))
+        return v.value
+
+    def launch_count(self) -> int:
+        v = C.c_int64()
+        self._call(self._L.ks_launch_count(self._h, C.byref(v)))
+        return v.value
+
+    def sync(self) -> int:
+        """ks_sync: returns the latched status (0 = OK) without raising."""
+        return self._L.ks_sync(self._h)
+
+    def last_error(self) -> str:
+        return self._L.ks_last_error(self._h).decode()
+
+
+def _raw_tensor(dptr: int, count: int, dtype, device):
+    """A torch tensor aliasing `count` elements at device address dptr (no copy, no ownership)."""
+    import torch
+
+    class _CAI:
+        pass
+
+    typestr = {torch.int32: "<i4", torch.float64: "<f8"}[dtype]
+    obj = _CAI()
+    obj.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (dptr, False), "version": 3,
+                                   "strides": None}
+    return torch.as_tensor(obj, device=device)
+
+
+def solve_step_host(ctx: Context, V_host, mu, lam_host, U_host, dev_bufs=None, tol=1e-10, max_iter=2000):
+    """One hot-path step from HOST buffers (pinned torch CPU tensors): H2D of V, lambda, U; assemble,
+    block solve, project on the device; D2H of F_A, F_B. Returns (FA, FB) host tensors and device bufs."""
+    import torch
+    N = U_host.shape[1]
+    if dev_bufs is None:
+        dev_bufs = dict(V=torch.empty_like(V_host, device="cuda"), lam=torch.empty_like(lam_host, device="cuda"),
+                        U=torch.empty_like(U_host, device="cuda"), Ut=torch.empty_like(U_host, device="cuda"),
+                        FA=torch.empty((ctx.n_H + N, ctx.n_H + N), dtype=torch.float64, device="cuda"),
+                        FB=torch.empty((ctx.n_H + N, ctx.n_H + N), dtype=torch.float64, device="cuda"),
+                        FA_h=torch.empty((ctx.n_H + N, ctx.n_H + N), dtype=torch.float64).pin_memory(),
+                        FB_h=torch.empty((ctx.n_H + N, ctx.n_H + N), dtype=torch.float64).pin_memory())
+    b = dev_bufs
+    with torch.cuda.stream(ctx.stream):
+        b["V"].copy_(V_host, non_blocking=True)
+        b["lam"].copy_(lam_host, non_blocking=True)
+        b["U"].copy_(U_host, non_blocking=True)
+        ctx.assemble_veff(b["V"], mu)
+        ctx.block_solve(b["lam"], b["U"], b["Ut"], tol=tol, max_iter=max_iter)
+        ctx.project_augmented(b["Ut"], b["FA"], b["FB"])
+        b["FA_h"].copy_(b["FA"], non_blocking=True)
+        b["FB_h"].copy_(b["FB"], non_blocking=True)
+    return b["FA_h"], b["FB_h"], dev_bufs

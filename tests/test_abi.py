@@ -1,0 +1,72 @@
+"""The C-ABI library loads and exports every symbol include/ks.h declares (no compute without a GPU),
+and the product package refuses to run without CUDA (no CPU fallback)."""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2404_19249_b200 import _build
+    _build.build()
+    import paper_2404_19249_b200 as pkg
+    return pkg.load_library()
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "ks.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ks_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_binding_list():
+    import paper_2404_19249_b200 as pkg
+    assert declared_symbols() == sorted(pkg.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", os.path.join(ROOT, "paper_2404_19249_b200", "libks.so")],
+                         capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r" T (ks_\w+)", out))
+    missing = [s for s in declared_symbols() if s not in exported]
+    assert not missing, missing
+    assert lib.ks_abi_version() == 1
+    assert b"sm_100a" in lib.ks_build_info()
+
+
+def test_library_is_sm100a_only():
+    so = os.path.join(ROOT, "paper_2404_19249_b200", "libks.so")
+    out = subprocess.run(["cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
+
+
+def test_null_context_arguments_rejected(lib):
+    import ctypes as C
+    h = C.c_void_p()
+    assert lib.ks_create(0, None, 0, None, None, None, C.byref(h)) == 1  # KS_E_ARG, no launch
+    assert b"KS_E_ARG" in lib.ks_last_error(None)
+    assert lib.ks_sync(None) == 1
+
+
+def test_no_cpu_fallback():
+    import torch
+    import paper_2404_19249_b200 as pkg
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import numpy as np
+    with pytest.raises(RuntimeError):
+        pkg.Context(np.zeros((4, 3)), np.zeros((1, 4), np.int32), np.zeros(4, np.uint8))
+
+
+def test_product_does_not_import_oracle():
+    pkg_dir = os.path.join(ROOT, "paper_2404_19249_b200")
+    for dirpath, _, files in os.walk(pkg_dir):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt and "oracle.c" not in txt, f
