@@ -60,10 +60,12 @@ static void free_all(ks_ctx *ctx) {
   void *ptrs[] = {ctx->tets, ctx->free_of_node, ctx->node_of_free, ctx->row_ptr, ctx->col, ctx->diag_pos,
                   ctx->emap, ctx->inv_ptr, ctx->inv_idx, ctx->vol, ctx->K, ctx->M, ctx->MV, ctx->H, ctx->A,
                   ctx->diag, ctx->w_tet, ctx->v_free, ctx->d_flags, ctx->d_block_iters, ctx->r, ctx->p, ctx->q,
-                  ctx->xpad, ctx->upad, ctx->partials, ctx->barrier, ctx->P_ptr, ctx->P_col, ctx->P_val,
-                  ctx->PT_ptr, ctx->PT_row, ctx->PT_val, ctx->G_ptr, ctx->G_col, ctx->G_val, ctx->B_H, ctx->Y_H,
-                  ctx->Y_M, ctx->gram_part};
+                  ctx->xpad, ctx->upad, ctx->partials, ctx->barrier};
   for (void *p : ptrs)
+    if (p) cudaFree(p);
+  ks_free_coarse(ctx);
+  void *proj[] = {ctx->Y_H, ctx->Y_M, ctx->proj_u, ctx->gram_part, ctx->bH_part, ctx->cH_part};
+  for (void *p : proj)
     if (p) cudaFree(p);
 }
 

@@ -56,19 +56,27 @@ struct ks_ctx {
   unsigned *barrier = nullptr;      // grid barrier counter
   int64_t partial_cap = 0;
 
-  // coarse space
+  // coarse space (ks_set_coarse) and projection workspace
   int64_t n_H = 0, p_nnz = 0;
-  int32_t *P_ptr = nullptr, *P_col = nullptr;   // [n_free+1], [p_nnz]
+  int32_t *P_ptr = nullptr, *P_col = nullptr;   // own copy, columns ascending within a row
   double *P_val = nullptr;
-  int32_t *PT_ptr = nullptr, *PT_row = nullptr; // coarse-major P^T: [n_H+1], [p_nnz] fine rows
-  double *PT_val = nullptr;
-  int32_t *G_ptr = nullptr, *G_col = nullptr;   // pattern of H P (n_free x n_H)
-  int64_t g_nnz = 0;
-  double *G_val = nullptr;                      // values of H P (scratch)
-  double *B_H = nullptr;                        // [n_H * n_H] cached P^T M P
-  double *Y_H = nullptr, *Y_M = nullptr;        // [n_free][N] projection scratch
+  int64_t n_items = 0, d_total = 0;
+  int d_max = 0;
+  int32_t *perm = nullptr;       // [n_free] fine rows grouped by parent set ("items" of <= ITEM_ROWS rows)
+  int32_t *item_ptr = nullptr;   // [n_items+1] ranges of perm
+  int32_t *item_S = nullptr;     // [4 n_items] parent coarse ids of the item (-1 padded)
+  int32_t *item_D_ptr = nullptr; // [n_items+1]
+  int32_t *item_D = nullptr;     // [d_total] sorted coarse ids touched by P rows of the item's neighbours
+  uint8_t *slotmap = nullptr;    // [4 nnz] slot of (entry k, parent t of col[k]) in its row's item D list
+  int32_t *CT_ptr = nullptr;     // [n_H+1] coarse node -> (item, local parent) list
+  int32_t *CT_val = nullptr;     // [4 n_items] entries 4 item + q
+  double *B_H = nullptr;         // [n_H n_H] cached P^T M P
+  double *AH_part = nullptr;     // [4 d_total] per-item partials of P^T Op P
+  double *bH_part = nullptr, *cH_part = nullptr;  // [4 n_items NP]
+  int64_t bc_cap = 0;
+  double *Y_H = nullptr, *Y_M = nullptr, *proj_u = nullptr;  // [n_free][NP]
   int64_t y_cap = 0;
-  double *gram_part = nullptr;                  // [grid][2 N N]
+  double *gram_part = nullptr;   // [blocks][2 N N]
   int64_t gram_cap = 0;
 
   std::string err;
@@ -124,3 +132,4 @@ ks_status ks_true_residual_impl(ks_ctx *ctx, int N, const double *lambda, const 
 ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, const int32_t *Pcol,
                              const double *Pval);
 ks_status ks_project_impl(ks_ctx *ctx, int N, const double *Ut, double *FA, double *FB);
+void ks_free_coarse(ks_ctx *ctx);

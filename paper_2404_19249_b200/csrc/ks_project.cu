@@ -2,12 +2,17 @@
 //   F_A = [[A_H, b_H], [b_H^T, beta]],  F_B = [[B_H, c_H], [c_H^T, gamma]]                (st1)-(st2)
 //   A_H = P^T H P (st5), b_H = P^T H U~ (st6), beta = U~^T H U~ (st7);
 //   B_H = P^T M P (cached per mesh pair), c_H = P^T M U~, gamma = U~^T M U~ (717-731).
-// Kernels (all deterministic: fixed partitions, fixed summation orders, no float atomics):
-//   K8  Y_H = H U~ and Y_M = M U~ in one pass over the shared column stream
-//   K8b beta, gamma: tall-skinny Gram products U~^T Y (register-tiled, per-block partials + fixed reduce)
-//   K9  b_H, c_H = P^T Y: coarse-major P^T lists, one block per coarse node
-//   K10 A_H = P^T (H P): G = H P per fine row on the precomputed pattern of H P, then one block per
-//       coarse row accumulating P^T G into per-warp dense rows in shared memory, combined in fixed order.
+//
+// Design (DESIGN.md §4 "projection"). Fine rows are grouped by their coarse parent set S (the <= 4
+// coarse nodes with P_ic != 0) and cut into "items" of <= ITEM_ROWS rows. Every contribution of a row
+// lands in coarse rows c in S, so one warp can accumulate an item's contributions privately:
+//   K8  k_proj_items  one pass over the item's rows: Y_H = H U~ and Y_M = M U~ (shared column stream),
+//                     the item partials sum_i P_ic Y_H[i] / Y_M[i] (for b_H, c_H) and
+//                     sum_i P_ic (H P)_i,d (for A_H) with d in the item's coarse window D (slot map
+//                     precomputed at setup). Per-row-slot private accumulators + fixed-order combine.
+//   K8b k_gram        beta, gamma = U~^T Y (register-tiled tall-skinny products, per-block partials)
+//   K9  k_proj_final  one block per coarse node c: fixed-order sums over the items containing c.
+// Everything is deterministic (fixed partitions and orders, no float atomics).
 #include <cub/cub.cuh>
 
 #include "ks_internal.cuh"
@@ -15,38 +20,181 @@
 
 namespace {
 
-constexpr int GROW_MAX = 512;  // max entries of a row of H P before dedup (row_len * 4)
+constexpr int ITEM_ROWS = 128;   // rows per item (chunk of a parent-set group)
+constexpr int DMAX = 255;        // max coarse window of an item (u8 slots; 255 = "no slot")
+constexpr int PROJ_WARPS = 8;
 
-__global__ void k_check_P(const int32_t *__restrict__ ptr, const int32_t *__restrict__ col, int64_t n_free,
-                          int64_t n_H, int64_t p_nnz, unsigned long long *bad) {
+// ---------------------------------------------------------------------------------------------
+// setup kernels
+// ---------------------------------------------------------------------------------------------
+// validate P rows (<= 4 entries, columns in range), sort each row by column, build the parent-set key
+__global__ void k_P_rows_keys(int32_t *__restrict__ ptr, int32_t *__restrict__ col, double *__restrict__ val,
+                              int64_t n_free, int64_t n_H, int64_t p_nnz, uint64_t *__restrict__ key,
+                              int32_t *__restrict__ rows, unsigned long long *bad) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n_free) return;
   int32_t a = ptr[i], b = ptr[i + 1];
   bool ok = a >= 0 && b >= a && b - a <= 4 && b <= p_nnz;
-  for (int32_t k = a; ok && k < b; k++) ok = col[k] >= 0 && col[k] < n_H;
-  if (!ok) atomicMin(bad, (unsigned long long)i);
+  int32_t c[4];
+  double v[4];
+  int m = ok ? b - a : 0;
+  for (int q = 0; q < m; q++) {
+    c[q] = col[a + q];
+    v[q] = val[a + q];
+    ok &= c[q] >= 0 && c[q] < n_H;
+  }
+  for (int x = 1; x < m; x++)
+    for (int y = x; y > 0 && c[y - 1] > c[y]; y--) {
+      int32_t tc = c[y]; c[y] = c[y - 1]; c[y - 1] = tc;
+      double tv = v[y]; v[y] = v[y - 1]; v[y - 1] = tv;
+    }
+  for (int x = 1; x < m; x++) ok &= c[x] != c[x - 1];
+  if (!ok) {
+    atomicMin(bad, (unsigned long long)i);
+    return;
+  }
+  uint64_t B = (uint64_t)n_H + 1, k = 0;
+  for (int q = 0; q < 4; q++) k = k * B + (uint64_t)(q < m ? c[q] : n_H);
+  for (int q = 0; q < m; q++) { col[a + q] = c[q]; val[a + q] = v[q]; }
+  key[i] = k;
+  rows[i] = (int32_t)i;
 }
 
-// expand P entries: key = coarse col, value = entry index (stable sort -> ascending fine row)
-__global__ void k_P_rows(const int32_t *__restrict__ ptr, int64_t n_free, int32_t *__restrict__ row_of) {
+__global__ void k_group_flags(const uint64_t *__restrict__ ks, int64_t n, int32_t *__restrict__ flag) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n_free) return;
-  for (int32_t k = ptr[i]; k < ptr[i + 1]; k++) row_of[k] = (int32_t)i;
+  if (i < n) flag[i] = (i == 0 || ks[i] != ks[i - 1]) ? 1 : 0;
 }
 
-__global__ void k_iota(int32_t *__restrict__ v, int64_t n) {
+__global__ void k_group_first(const int32_t *__restrict__ flag, const int32_t *__restrict__ gincl, int64_t n,
+                              int32_t *__restrict__ gfirst) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) v[i] = (int32_t)i;
+  if (i < n && flag[i]) gfirst[gincl[i] - 1] = (int32_t)i;
 }
 
-__global__ void k_PT_fill(const int32_t *__restrict__ order, const int32_t *__restrict__ row_of,
-                          const double *__restrict__ Pval, int64_t p_nnz, int32_t *__restrict__ PT_row,
-                          double *__restrict__ PT_val) {
-  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= p_nnz) return;
-  int32_t k = order[j];
-  PT_row[j] = row_of[k];
-  PT_val[j] = Pval[k];
+__global__ void k_item_flags(const int32_t *__restrict__ gincl, const int32_t *__restrict__ gfirst, int64_t n,
+                             int32_t *__restrict__ iflag) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) iflag[i] = ((i - gfirst[gincl[i] - 1]) % ITEM_ROWS) == 0 ? 1 : 0;
+}
+
+__global__ void k_item_ptr(const int32_t *__restrict__ iflag, const int32_t *__restrict__ iincl, int64_t n,
+                           int32_t *__restrict__ item_ptr, int32_t *__restrict__ item_of_pos) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  item_of_pos[i] = iincl[i] - 1;
+  if (iflag[i]) item_ptr[iincl[i] - 1] = (int32_t)i;
+}
+
+__global__ void k_item_S(const int32_t *__restrict__ item_ptr, const int32_t *__restrict__ perm,
+                         const int32_t *__restrict__ Pptr, const int32_t *__restrict__ Pcol, int64_t n_items,
+                         int32_t *__restrict__ item_S, int32_t *__restrict__ ct_key, int32_t *__restrict__ ct_val,
+                         int32_t n_H) {
+  int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (it >= n_items) return;
+  int32_t i = perm[item_ptr[it]];
+  int32_t a = Pptr[i], m = Pptr[i + 1] - a;
+  for (int q = 0; q < 4; q++) {
+    int32_t c = q < m ? Pcol[a + q] : -1;
+    item_S[4 * it + q] = c;
+    ct_key[4 * it + q] = c >= 0 ? c : n_H;
+    ct_val[4 * it + q] = (int32_t)(4 * it + q);
+  }
+}
+
+// Per item: the sorted set D of coarse columns of P rows of all neighbours of the item's rows.
+// Bitmap over coarse ids in shared memory (order-independent -> deterministic). pass 0: counts.
+__global__ void k_item_D(const int32_t *__restrict__ item_ptr, const int32_t *__restrict__ perm,
+                         const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                         const int32_t *__restrict__ Pptr, const int32_t *__restrict__ Pcol, int32_t n_H,
+                         int32_t *__restrict__ D_cnt, const int32_t *__restrict__ D_ptr, int32_t *__restrict__ D) {
+  extern __shared__ unsigned bits[];
+  __shared__ int32_t wsum[33];
+  const int64_t it = blockIdx.x;
+  const int nw = (n_H + 31) / 32;
+  for (int w = threadIdx.x; w < nw; w += blockDim.x) bits[w] = 0u;
+  __syncthreads();
+  const int32_t p0 = item_ptr[it], p1 = item_ptr[it + 1];
+  for (int32_t pos = p0 + threadIdx.x / 32; pos < p1; pos += blockDim.x / 32) {
+    const int32_t i = perm[pos];
+    for (int32_t k = row_ptr[i] + (threadIdx.x & 31); k < row_ptr[i + 1]; k += 32) {
+      const int32_t j = col[k];
+      for (int32_t t = Pptr[j]; t < Pptr[j + 1]; t++) {
+        const int32_t d = Pcol[t];
+        atomicOr(&bits[d >> 5], 1u << (d & 31));
+      }
+    }
+  }
+  __syncthreads();
+  // contiguous chunk of words per thread -> popcounts -> block exclusive scan (fixed)
+  const int per = (nw + blockDim.x - 1) / blockDim.x;
+  const int w0 = threadIdx.x * per, w1 = min(nw, w0 + per);
+  int cnt = 0;
+  for (int w = w0; w < w1; w++) cnt += __popc(bits[w]);
+  if (D_cnt) {
+    // block reduce
+    int v = cnt;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int s = 0;
+      for (int w = 0; w < (int)blockDim.x / 32; w++) s += wsum[w];
+      D_cnt[it] = s;
+    }
+    return;
+  }
+  // exclusive scan of cnt over threads
+  int v = cnt;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    int u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  if (lane == 31) wsum[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < (int)blockDim.x / 32; w++) { int t = wsum[w]; wsum[w] = s; s += t; }
+  }
+  __syncthreads();
+  int off = D_ptr[it] + wsum[warp] + v - cnt;
+  for (int w = w0; w < w1; w++) {
+    unsigned b = bits[w];
+    while (b) {
+      int l = __ffs(b) - 1;
+      D[off++] = w * 32 + l;
+      b &= b - 1;
+    }
+  }
+}
+
+// slot of each (entry k, parent t of col[k]) inside the D list of the row's item
+__global__ void k_slotmap(const int32_t *__restrict__ perm, const int32_t *__restrict__ item_of_pos,
+                          const int32_t *__restrict__ D_ptr, const int32_t *__restrict__ D,
+                          const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                          const int32_t *__restrict__ Pptr, const int32_t *__restrict__ Pcol, int64_t n_free,
+                          uint8_t *__restrict__ slotmap) {
+  int64_t pos = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (pos >= n_free) return;
+  const int32_t i = perm[pos], it = item_of_pos[pos];
+  const int32_t d0 = D_ptr[it], dn = D_ptr[it + 1] - d0;
+  for (int32_t k = row_ptr[i]; k < row_ptr[i + 1]; k++) {
+    const int32_t j = col[k];
+    const int32_t a = Pptr[j], m = Pptr[j + 1] - a;
+    for (int t = 0; t < 4; t++) {
+      uint8_t s = 255;
+      if (t < m) {
+        const int32_t c = Pcol[a + t];
+        int lo = 0, hi = dn;
+        while (lo < hi) {
+          int mid = (lo + hi) >> 1;
+          if (D[d0 + mid] < c) lo = mid + 1; else hi = mid;
+        }
+        s = (uint8_t)lo;
+      }
+      slotmap[4 * (int64_t)k + t] = s;
+    }
+  }
 }
 
 __global__ void k_lower_bound_ptr(const int32_t *__restrict__ keys, int64_t nk, int64_t nrows,
@@ -61,170 +209,209 @@ __global__ void k_lower_bound_ptr(const int32_t *__restrict__ keys, int64_t nk, 
   ptr[r] = (int32_t)lo;
 }
 
-// pattern of G = H P: row i = sorted unique coarse columns of the P rows of the columns of row i.
-// pass 0 counts, pass 1 fills.
-__global__ void k_G_pattern(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                            const int32_t *__restrict__ Pptr, const int32_t *__restrict__ Pcol, int64_t n_free,
-                            const int32_t *__restrict__ G_ptr, int32_t *__restrict__ G_cnt,
-                            int32_t *__restrict__ G_col, unsigned long long *bad) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n_free) return;
-  int32_t buf[GROW_MAX];
-  int m = 0;
-  for (int32_t k = row_ptr[i]; k < row_ptr[i + 1]; k++) {
-    int32_t j = col[k];
-    for (int32_t t = Pptr[j]; t < Pptr[j + 1]; t++) {
-      if (m >= GROW_MAX) { atomicMin(bad, (unsigned long long)i); return; }
-      buf[m++] = Pcol[t];
+// ---------------------------------------------------------------------------------------------
+// projection kernels
+// ---------------------------------------------------------------------------------------------
+struct ProjArgs {
+  const int32_t *row_ptr, *col;
+  const double *Aop;        // operator of the triple product (H, or M for the cached B_H)
+  const double *Mop;        // M (second operator of the Y pass)
+  const int32_t *Pptr;
+  const double *Pval;
+  const int32_t *perm, *item_ptr, *item_S, *D_ptr;
+  const uint8_t *slotmap;
+  const double *U;          // [n][NP]
+  double *YH, *YM;          // [n][NP]
+  double *AH_part, *bH_part, *cH_part;
+  int64_t n_items;
+  int d_max;
+};
+
+template <int NP, bool WITH_Y>
+__global__ void __launch_bounds__(PROJ_WARPS * 32) k_proj_items(ProjArgs a) {
+  constexpr int VEC = Lay<NP>::VEC;
+  constexpr int LPRY = Lay<NP>::LPR;             // lanes carrying Y columns
+  constexpr int LPR = LPRY < 8 ? 8 : LPRY;       // lanes per row in this kernel
+  constexpr int RPW = 32 / LPR;
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = lane / LPR, sub = lane % LPR;
+  const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (slot * LPR));
+  double *accA = smem + (int64_t)warp * RPW * 4 * a.d_max;
+  const int64_t gw = (int64_t)blockIdx.x * PROJ_WARPS + warp, nw = (int64_t)gridDim.x * PROJ_WARPS;
+
+  for (int64_t it = gw; it < a.n_items; it += nw) {
+    const int32_t p0 = __ldg(a.item_ptr + it), p1 = __ldg(a.item_ptr + it + 1);
+    int nS = 0;
+#pragma unroll
+    for (int q = 0; q < 4; q++) nS += __ldg(a.item_S + 4 * it + q) >= 0;
+    const int32_t dn = __ldg(a.D_ptr + it + 1) - __ldg(a.D_ptr + it);
+    for (int x = lane; x < RPW * 4 * dn; x += 32) accA[x] = 0.0;
+    __syncwarp();
+    double accB[4][VEC], accC[4][VEC];
+#pragma unroll
+    for (int c = 0; c < 4; c++)
+#pragma unroll
+      for (int v = 0; v < VEC; v++) accB[c][v] = accC[c][v] = 0.0;
+    double *myA = accA + slot * 4 * dn;
+
+    for (int32_t pos = p0 + slot; pos < p1; pos += RPW) {
+      const int32_t i = __ldg(a.perm + pos);
+      const int32_t pi = __ldg(a.Pptr + i);
+      double Pw[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) Pw[q] = q < nS ? __ldg(a.Pval + pi + q) : 0.0;
+      const int32_t k0 = __ldg(a.row_ptr + i), k1 = __ldg(a.row_ptr + i + 1);
+      Vec<VEC> yh, ym;
+      yh.zero();
+      ym.zero();
+      for (int32_t k = k0; k < k1; k++) {
+        const int32_t j = __ldg(a.col + k);
+        const double h = __ldg(a.Aop + k);
+        if (WITH_Y && sub < LPRY) {
+          const double m = __ldg(a.Mop + k);
+          Vec<VEC> x = Vec<VEC>::ldg(a.U + (int64_t)j * NP + sub * VEC);
+#pragma unroll
+          for (int v = 0; v < VEC; v++) {
+            yh.v[v] = fma(h, x.v[v], yh.v[v]);
+            ym.v[v] = fma(m, x.v[v], ym.v[v]);
+          }
+        }
+        const int32_t pj = __ldg(a.Pptr + j), cj = __ldg(a.Pptr + j + 1) - pj;
+        const uchar4 sl = __ldg(reinterpret_cast<const uchar4 *>(a.slotmap) + k);
+        const unsigned char s4[4] = {sl.x, sl.y, sl.z, sl.w};
+        for (int q = sub; q < 16; q += LPR) {
+          const int cl = q >> 2, t = q & 3;
+          if (cl < nS && t < cj) {
+            const int s = s4[t];
+            myA[cl * dn + s] = fma(Pw[cl] * h, __ldg(a.Pval + pj + t), myA[cl * dn + s]);
+          }
+        }
+        __syncwarp(gmask);
+      }
+      if (WITH_Y && sub < LPRY) {
+        yh.store(a.YH + (int64_t)i * NP + sub * VEC);
+        ym.store(a.YM + (int64_t)i * NP + sub * VEC);
+#pragma unroll
+        for (int c = 0; c < 4; c++)
+#pragma unroll
+          for (int v = 0; v < VEC; v++) {
+            accB[c][v] = fma(Pw[c], yh.v[v], accB[c][v]);
+            accC[c][v] = fma(Pw[c], ym.v[v], accC[c][v]);
+          }
+      }
     }
-  }
-  // insertion sort + unique
-  for (int x = 1; x < m; x++) {
-    int32_t v = buf[x];
-    int y = x - 1;
-    while (y >= 0 && buf[y] > v) { buf[y + 1] = buf[y]; y--; }
-    buf[y + 1] = v;
-  }
-  int u = 0;
-  for (int x = 0; x < m; x++)
-    if (u == 0 || buf[x] != buf[u - 1]) buf[u++] = buf[x];
-  if (G_cnt) G_cnt[i] = u;
-  if (G_col) {
-    int32_t g0 = G_ptr[i];
-    for (int x = 0; x < u; x++) G_col[g0 + x] = buf[x];
+    __syncwarp();
+    if (WITH_Y) {
+      // combine the row slots (lanes with equal sub) in butterfly order
+#pragma unroll
+      for (int c = 0; c < 4; c++)
+#pragma unroll
+        for (int v = 0; v < VEC; v++) {
+          double b = accB[c][v], cc = accC[c][v];
+#pragma unroll
+          for (int o = LPR; o < 32; o <<= 1) {
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+            cc += __shfl_xor_sync(0xffffffffu, cc, o);
+          }
+          if (slot == 0 && sub < LPRY) {
+            a.bH_part[(4 * it + c) * NP + sub * VEC + v] = b;
+            a.cH_part[(4 * it + c) * NP + sub * VEC + v] = cc;
+          }
+        }
+    }
+    // combine the row-slot copies of the A partial in slot order
+    double *out = a.AH_part + 4 * (int64_t)__ldg(a.D_ptr + it);
+    for (int x = lane; x < 4 * dn; x += 32) {
+      double s = 0.0;
+      for (int r = 0; r < RPW; r++) s += accA[r * 4 * dn + x];
+      out[x] = s;
+    }
+    __syncwarp();
   }
 }
 
-// G values: half-warp per fine row; lane s owns G slots s, s+16, ...; each slot sums the matching
-// (k, t) products in ascending (k, t) order.
-__global__ void __launch_bounds__(256) k_G_values(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                                                  const double *__restrict__ val, const int32_t *__restrict__ Pptr,
-                                                  const int32_t *__restrict__ Pcol, const double *__restrict__ Pval,
-                                                  const int32_t *__restrict__ G_ptr, const int32_t *__restrict__ G_col,
-                                                  int64_t n_free, double *__restrict__ G_val) {
-  int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 4;
-  int s = threadIdx.x & 15;
-  if (i >= n_free) return;
-  const int32_t g0 = G_ptr[i], g1 = G_ptr[i + 1];
-  const int32_t k0 = row_ptr[i], k1 = row_ptr[i + 1];
-  for (int32_t g = g0 + s; g < g1; g += 16) {
-    const int32_t d = G_col[g];
-    double acc = 0.0;
-    for (int32_t k = k0; k < k1; k++) {
-      const int32_t j = __ldg(col + k);
-      const double h = __ldg(val + k);
-      for (int32_t t = __ldg(Pptr + j); t < __ldg(Pptr + j + 1); t++)
-        if (__ldg(Pcol + t) == d) acc = fma(h, __ldg(Pval + t), acc);
-    }
-    G_val[g] = acc;
-  }
-}
-
-// out[c][d] (row stride ld) = sum_{j in P^T row c} P^T_val[j] * G[PT_row[j]][d]; RS warps each keep a
-// dense row of n_H partial sums in shared memory, combined in warp order.
-__global__ void k_PtG(const int32_t *__restrict__ PT_ptr, const int32_t *__restrict__ PT_row,
-                      const double *__restrict__ PT_val, const int32_t *__restrict__ G_ptr,
-                      const int32_t *__restrict__ G_col, const double *__restrict__ G_val, int64_t n_H,
-                      double *__restrict__ out, int64_t ld) {
-  extern __shared__ double acc[];  // [RS][n_H]
-  const int RS = blockDim.x >> 5;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// one block per coarse node c: A row from the item partials (dense rows per warp, combined in warp
+// order), and, with WITH_B, b_H / c_H entries (sums over the items in list order).
+template <bool WITH_B>
+__global__ void k_proj_final(const int32_t *__restrict__ CT_ptr, const int32_t *__restrict__ CT_val,
+                             const int32_t *__restrict__ D_ptr, const int32_t *__restrict__ D,
+                             const double *__restrict__ AH_part, const double *__restrict__ bH_part,
+                             const double *__restrict__ cH_part, int64_t n_H, int N, int NP, double *__restrict__ FA,
+                             double *__restrict__ FB, int64_t ldA, int64_t D2) {
+  extern __shared__ double acc[];  // [W][n_H]
+  const int W = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t c = blockIdx.x;
-  for (int64_t x = threadIdx.x; x < RS * n_H; x += blockDim.x) acc[x] = 0.0;
+  for (int64_t x = threadIdx.x; x < W * n_H; x += blockDim.x) acc[x] = 0.0;
   __syncthreads();
+  const int32_t e0 = CT_ptr[c], e1 = CT_ptr[c + 1];
   double *mine = acc + warp * n_H;
-  for (int32_t j = PT_ptr[c] + warp; j < PT_ptr[c + 1]; j += RS) {
-    const int32_t i = __ldg(PT_row + j);
-    const double wgt = __ldg(PT_val + j);
-    const int32_t g1 = __ldg(G_ptr + i + 1);
-    for (int32_t g = __ldg(G_ptr + i) + lane; g < g1; g += 32) {
-      const int32_t d = __ldg(G_col + g);
-      mine[d] = fma(wgt, __ldg(G_val + g), mine[d]);
-    }
+  for (int32_t e = e0 + warp; e < e1; e += W) {
+    const int32_t v = CT_val[e], it = v >> 2, cl = v & 3;
+    const int32_t d0 = D_ptr[it], dn = D_ptr[it + 1] - d0;
+    const double *src = AH_part + 4 * (int64_t)d0 + cl * dn;
+    for (int s = lane; s < dn; s += 32) mine[D[d0 + s]] += src[s];
     __syncwarp();
   }
   __syncthreads();
   for (int64_t d = threadIdx.x; d < n_H; d += blockDim.x) {
     double s = 0.0;
-    for (int w = 0; w < RS; w++) s += acc[w * n_H + d];
-    out[c * ld + d] = s;
+    for (int w = 0; w < W; w++) s += acc[w * n_H + d];
+    FA[c * ldA + d] = s;
   }
-}
-
-// Y_H = H U~, Y_M = M U~ (fast layout, N == NP)
-template <int NP>
-__global__ void __launch_bounds__(256) k_HM_times(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                                                  const double *__restrict__ H, const double *__restrict__ M,
-                                                  const double *__restrict__ X, double *__restrict__ YH,
-                                                  double *__restrict__ YM, int64_t n) {
-  constexpr int VEC = Lay<NP>::VEC, LPR = Lay<NP>::LPR;
-  const int64_t gl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t row = gl / LPR;
-  const int sub = (int)(gl % LPR);
-  if (row >= n) return;
-  Vec<VEC> yh, ym;
-  row_spmv2<NP>(col, H, M, __ldg(row_ptr + row), __ldg(row_ptr + row + 1), X, sub, yh, ym);
-  yh.store(YH + row * NP + sub * VEC);
-  ym.store(YM + row * NP + sub * VEC);
-}
-
-__global__ void k_HM_times_generic(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                                   const double *__restrict__ H, const double *__restrict__ M,
-                                   const double *__restrict__ X, double *__restrict__ YH, double *__restrict__ YM,
-                                   int64_t n, int N) {
-  const int64_t gl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (gl >= n * N) return;
-  const int64_t row = gl / N;
-  const int c = (int)(gl % N);
-  double sh = 0.0, sm = 0.0;
-  for (int32_t k = row_ptr[row]; k < row_ptr[row + 1]; k++) {
-    const double x = X[(int64_t)col[k] * N + c];
-    sh = fma(H[k], x, sh);
-    sm = fma(M[k], x, sm);
+  if (WITH_B) {
+    for (int a = threadIdx.x; a < 2 * N; a += blockDim.x) {
+      const int col = a % N;
+      const double *src = a < N ? bH_part : cH_part;
+      double s = 0.0;
+      for (int32_t e = e0; e < e1; e++) s += src[(int64_t)CT_val[e] * NP + col];
+      double *F = a < N ? FA : FB;
+      F[c * D2 + n_H + col] = s;
+      F[(n_H + col) * D2 + c] = s;
+    }
   }
-  YH[gl] = sh;
-  YM[gl] = sm;
 }
 
 // Gram partials: part[blk][m][a][b] = sum over the block's rows of U[i][a] * Y_m[i][b], m in {H, M}.
-// Outputs are tiled 4x4 per thread; threads beyond the tiles form row groups (rows r = g mod ngroups).
+// Inputs with row stride ld. Outputs tiled 4x4 per thread; spare threads form row groups.
 constexpr int GR_ROWS = 32;
 __global__ void __launch_bounds__(256) k_gram(const double *__restrict__ U, const double *__restrict__ YH,
-                                              const double *__restrict__ YM, int64_t n, int N, int64_t rows_per_blk,
-                                              double *__restrict__ part) {
+                                              const double *__restrict__ YM, int64_t n, int N, int ld,
+                                              int64_t rows_per_blk, double *__restrict__ part) {
   extern __shared__ double sm[];
   const int NT = (N + 3) / 4, NQ = NT * 4;
   double *sU = sm, *sH = sm + GR_ROWS * NQ, *sM = sm + 2 * GR_ROWS * NQ;
-  double *sRed = sm + 3 * GR_ROWS * NQ;  // [ngroups][2 N N] reduction scratch reuses after loop
+  double *sRed = sm + 3 * GR_ROWS * NQ;
   const int ntiles = 2 * NT * NT;
-  const int ngroups = max(1, (int)blockDim.x / ntiles);
+  const bool many = ntiles > (int)blockDim.x;
+  const int ngroups = many ? 1 : (int)blockDim.x / ntiles;
+  const int my_group = many ? 0 : (int)threadIdx.x / ntiles;
   const int64_t r0 = blockIdx.x * rows_per_blk;
   const int64_t r1 = min(n, r0 + rows_per_blk);
-  double acc[2][16];  // up to 2 tiles per thread when ntiles > blockDim
+  double acc[2][16];
+#pragma unroll
   for (int z = 0; z < 2; z++)
+#pragma unroll
     for (int k = 0; k < 16; k++) acc[z][k] = 0.0;
-  const int my_group = threadIdx.x / ntiles;
   for (int64_t rb = r0; rb < r1; rb += GR_ROWS) {
     const int nr = (int)min((int64_t)GR_ROWS, r1 - rb);
     __syncthreads();
     for (int x = threadIdx.x; x < GR_ROWS * NQ; x += blockDim.x) {
       const int rr = x / NQ, cc = x % NQ;
       const bool in = rr < nr && cc < N;
-      const int64_t g = (rb + rr) * N + cc;
+      const int64_t g = (rb + rr) * ld + cc;
       sU[x] = in ? U[g] : 0.0;
       sH[x] = in ? YH[g] : 0.0;
       sM[x] = in ? YM[g] : 0.0;
     }
     __syncthreads();
+#pragma unroll
     for (int z = 0; z < 2; z++) {
-      const int tile = (ntiles > (int)blockDim.x) ? threadIdx.x + z * blockDim.x : (z == 0 ? threadIdx.x % ntiles : -1);
-      if (tile < 0 || tile >= ntiles) continue;
-      if (ntiles <= (int)blockDim.x && my_group >= ngroups) continue;
+      const int tile = many ? (int)threadIdx.x + z * (int)blockDim.x : (z == 0 ? (int)threadIdx.x % ntiles : -1);
+      if (tile < 0 || tile >= ntiles || my_group >= ngroups) continue;
       const int m = tile / (NT * NT), ta = (tile % (NT * NT)) / NT, tb = tile % NT;
       const double *sY = m ? sM : sH;
-      const int rstart = (ntiles <= (int)blockDim.x) ? my_group : 0;
-      const int rstep = (ntiles <= (int)blockDim.x) ? ngroups : 1;
-      for (int rr = rstart; rr < nr; rr += rstep) {
+      for (int rr = my_group; rr < nr; rr += ngroups) {
         double ua[4], yb[4];
 #pragma unroll
         for (int k = 0; k < 4; k++) { ua[k] = sU[rr * NQ + ta * 4 + k]; yb[k] = sY[rr * NQ + tb * 4 + k]; }
@@ -236,20 +423,18 @@ __global__ void __launch_bounds__(256) k_gram(const double *__restrict__ U, cons
     }
   }
   __syncthreads();
-  // combine row groups in fixed order via shared memory, write 2 N N partial
   const int NN2 = 2 * N * N;
   for (int x = threadIdx.x; x < ngroups * NN2; x += blockDim.x) sRed[x] = 0.0;
   __syncthreads();
+#pragma unroll
   for (int z = 0; z < 2; z++) {
-    const int tile = (ntiles > (int)blockDim.x) ? threadIdx.x + z * blockDim.x : (z == 0 ? threadIdx.x % ntiles : -1);
-    if (tile < 0 || tile >= ntiles) continue;
-    const int grp = (ntiles > (int)blockDim.x) ? 0 : my_group;
-    if (grp >= ngroups) continue;
+    const int tile = many ? (int)threadIdx.x + z * (int)blockDim.x : (z == 0 ? (int)threadIdx.x % ntiles : -1);
+    if (tile < 0 || tile >= ntiles || my_group >= ngroups) continue;
     const int m = tile / (NT * NT), ta = (tile % (NT * NT)) / NT, tb = tile % NT;
     for (int x = 0; x < 4; x++)
       for (int y = 0; y < 4; y++) {
-        const int a = ta * 4 + x, b = tb * 4 + y;
-        if (a < N && b < N) sRed[grp * NN2 + m * N * N + a * N + b] = acc[z][x * 4 + y];
+        const int aa = ta * 4 + x, bb = tb * 4 + y;
+        if (aa < N && bb < N) sRed[my_group * NN2 + m * N * N + aa * N + bb] = acc[z][x * 4 + y];
       }
   }
   __syncthreads();
@@ -260,7 +445,6 @@ __global__ void __launch_bounds__(256) k_gram(const double *__restrict__ U, cons
   }
 }
 
-// beta / gamma = sum of block partials in block order -> bottom-right blocks of F_A / F_B
 __global__ void k_gram_final(const double *__restrict__ part, int nblk, int N, int64_t n_H, int64_t D,
                              double *__restrict__ FA, double *__restrict__ FB) {
   const int NN2 = 2 * N * N;
@@ -272,40 +456,18 @@ __global__ void k_gram_final(const double *__restrict__ part, int nblk, int N, i
   }
 }
 
-// b_H = P^T Y_H, c_H = P^T Y_M: block per coarse node c; thread (rs, a) sums entries j = rs mod RS.
-__global__ void k_PtY(const int32_t *__restrict__ PT_ptr, const int32_t *__restrict__ PT_row,
-                      const double *__restrict__ PT_val, const double *__restrict__ YH, const double *__restrict__ YM,
-                      int N, int64_t n_H, int64_t D, double *__restrict__ FA, double *__restrict__ FB) {
-  extern __shared__ double red[];  // [RS][2N]
-  const int RS = blockDim.x / N;
-  const int rs = threadIdx.x / N, a = threadIdx.x % N;
-  const int64_t c = blockIdx.x;
-  double sh = 0.0, sm = 0.0;
-  if (rs < RS) {
-    for (int32_t j = PT_ptr[c] + rs; j < PT_ptr[c + 1]; j += RS) {
-      const int64_t i = __ldg(PT_row + j);
-      const double w = __ldg(PT_val + j);
-      sh = fma(w, YH[i * N + a], sh);
-      sm = fma(w, YM[i * N + a], sm);
-    }
-    red[rs * 2 * N + a] = sh;
-    red[rs * 2 * N + N + a] = sm;
-  }
-  __syncthreads();
-  if (threadIdx.x < N) {
-    double th = 0.0, tm = 0.0;
-    for (int r = 0; r < RS; r++) { th += red[r * 2 * N + a]; tm += red[r * 2 * N + N + a]; }
-    FA[c * D + n_H + a] = th;
-    FA[(n_H + a) * D + c] = th;
-    FB[c * D + n_H + a] = tm;
-    FB[(n_H + a) * D + c] = tm;
-  }
-}
-
 __global__ void k_copy_block(const double *__restrict__ src, int64_t n_H, double *__restrict__ dst, int64_t D) {
   int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (x >= n_H * n_H) return;
   dst[(x / n_H) * D + x % n_H] = src[x];
+}
+
+__global__ void k_pad_proj(const double *__restrict__ src, int N, double *__restrict__ dst, int NP, int64_t n) {
+  const int64_t gl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gl >= n * NP) return;
+  const int64_t row = gl / NP;
+  const int c = (int)(gl % NP);
+  dst[gl] = c < N ? src[row * N + c] : 0.0;
 }
 
 int pow2_at_least(int N) {
@@ -314,43 +476,97 @@ int pow2_at_least(int N) {
   return np;
 }
 
-ks_status ptg_launch(ks_ctx *ctx, const double *Gv, double *out, int64_t ld) {
-  int RS = 4;
-  size_t sm = (size_t)RS * ctx->n_H * sizeof(double);
-  while (sm > 200 * 1024 && RS > 1) { RS >>= 1; sm = (size_t)RS * ctx->n_H * sizeof(double); }
-  if (sm > 200 * 1024) return ks_fail(ctx, KS_E_ARG, "n_H = %lld too large for the dense-row triple product", (long long)ctx->n_H);
-  KS_CUDA(ctx, cudaFuncSetAttribute(k_PtG, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  k_PtG<<<(unsigned)ctx->n_H, 32 * RS, sm, ctx->stream>>>(ctx->PT_ptr, ctx->PT_row, ctx->PT_val, ctx->G_ptr,
-                                                          ctx->G_col, Gv, ctx->n_H, out, ld);
+int proj_grid(ks_ctx *ctx, int64_t n_items) {
+  int64_t g = (n_items + PROJ_WARPS - 1) / PROJ_WARPS;
+  int64_t cap = (int64_t)ctx->sm_count * 8;
+  return (int)(g < cap ? (g < 1 ? 1 : g) : cap);
+}
+
+template <int NP, bool WITH_Y>
+ks_status launch_items(ks_ctx *ctx, ProjArgs &a) {
+  constexpr int LPRY = Lay<NP>::LPR;
+  constexpr int LPR = LPRY < 8 ? 8 : LPRY;
+  constexpr int RPW = 32 / LPR;
+  const size_t sm = sizeof(double) * (size_t)PROJ_WARPS * RPW * 4 * ctx->d_max;
+  KS_CUDA(ctx, cudaFuncSetAttribute(k_proj_items<NP, WITH_Y>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_proj_items<NP, WITH_Y><<<proj_grid(ctx, ctx->n_items), PROJ_WARPS * 32, sm, ctx->stream>>>(a);
   KS_LAUNCHED(ctx);
   return KS_OK;
 }
 
-ks_status g_values_launch(ks_ctx *ctx, const double *val) {
-  k_G_values<<<ks_blocks(16 * ctx->n_free, 256), 256, 0, ctx->stream>>>(
-      ctx->row_ptr, ctx->col, val, ctx->P_ptr, ctx->P_col, ctx->P_val, ctx->G_ptr, ctx->G_col, ctx->n_free,
-      ctx->G_val);
+template <bool WITH_B>
+ks_status launch_final(ks_ctx *ctx, int N, int NP, double *FA, double *FB, int64_t ldA, int64_t D2) {
+  int W = 4;
+  size_t sm = sizeof(double) * W * ctx->n_H;
+  while (sm > 200 * 1024 && W > 1) { W >>= 1; sm = sizeof(double) * W * ctx->n_H; }
+  if (sm > 200 * 1024) return ks_fail(ctx, KS_E_ARG, "n_H = %lld too large for the dense-row reduction", (long long)ctx->n_H);
+  KS_CUDA(ctx, cudaFuncSetAttribute(k_proj_final<WITH_B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_proj_final<WITH_B><<<(unsigned)ctx->n_H, 32 * W, sm, ctx->stream>>>(ctx->CT_ptr, ctx->CT_val, ctx->item_D_ptr,
+                                                                        ctx->item_D, ctx->AH_part, ctx->bH_part,
+                                                                        ctx->cH_part, ctx->n_H, N, NP, FA, FB, ldA, D2);
   KS_LAUNCHED(ctx);
   return KS_OK;
 }
+
+ProjArgs base_args(ks_ctx *ctx) {
+  ProjArgs a;
+  a.row_ptr = ctx->row_ptr;
+  a.col = ctx->col;
+  a.Aop = ctx->H;
+  a.Mop = ctx->M;
+  a.Pptr = ctx->P_ptr;
+  a.Pval = ctx->P_val;
+  a.perm = ctx->perm;
+  a.item_ptr = ctx->item_ptr;
+  a.item_S = ctx->item_S;
+  a.D_ptr = ctx->item_D_ptr;
+  a.slotmap = ctx->slotmap;
+  a.U = nullptr;
+  a.YH = a.YM = nullptr;
+  a.AH_part = ctx->AH_part;
+  a.bH_part = ctx->bH_part;
+  a.cH_part = ctx->cH_part;
+  a.n_items = ctx->n_items;
+  a.d_max = ctx->d_max;
+  return a;
+}
+
+struct TmpGuard {
+  std::vector<void *> p;
+  ~TmpGuard() { for (void *x : p) cudaFree(x); }
+};
+
+#define TMPA(ptr, count)                                                                       \
+  do {                                                                                         \
+    KS_CUDA(ctx, cudaMalloc((void **)&(ptr), sizeof(*(ptr)) * (size_t)((count) > 0 ? (count) : 1))); \
+    tg.p.push_back((void *)(ptr));                                                             \
+  } while (0)
 
 }  // namespace
+
+void ks_free_coarse(ks_ctx *ctx) {
+  void *ptrs[] = {ctx->P_ptr, ctx->P_col, ctx->P_val, ctx->perm, ctx->item_ptr, ctx->item_S, ctx->item_D_ptr,
+                  ctx->item_D, ctx->slotmap, ctx->CT_ptr, ctx->CT_val, ctx->B_H, ctx->AH_part};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+  ctx->P_ptr = ctx->P_col = nullptr;
+  ctx->P_val = nullptr;
+  ctx->perm = ctx->item_ptr = ctx->item_S = ctx->item_D_ptr = ctx->item_D = ctx->CT_ptr = ctx->CT_val = nullptr;
+  ctx->slotmap = nullptr;
+  ctx->B_H = ctx->AH_part = nullptr;
+  ctx->n_H = 0;
+}
 
 ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, const int32_t *Pcol, const double *Pval) {
   cudaStream_t s = ctx->stream;
   const int64_t nf = ctx->n_free;
-  // read p_nnz from the row pointer
+  if (n_H >= 55000) return ks_fail(ctx, KS_E_ARG, "n_H = %lld >= 55000 not supported (parent-set key)", (long long)n_H);
   int32_t h_pn = 0;
   KS_CUDA(ctx, cudaMemcpyAsync(&h_pn, Pptr + nf, 4, cudaMemcpyDeviceToHost, s));
   KS_CUDA(ctx, cudaStreamSynchronize(s));
   const int64_t pn = h_pn;
-  if (pn < 0) return ks_fail(ctx, KS_E_ARG, "P row_ptr[n_free] = %lld < 0", (long long)pn);
-  // drop a previous coarse space
-  for (void **b : {(void **)&ctx->P_ptr, (void **)&ctx->P_col, (void **)&ctx->P_val, (void **)&ctx->PT_ptr,
-                   (void **)&ctx->PT_row, (void **)&ctx->PT_val, (void **)&ctx->G_ptr, (void **)&ctx->G_col,
-                   (void **)&ctx->G_val, (void **)&ctx->B_H})
-    if (*b) { cudaFree(*b); *b = nullptr; }
-  ctx->n_H = n_H;
+  if (pn < 0 || pn > 4 * nf) return ks_fail(ctx, KS_E_ARG, "P row_ptr[n_free] = %lld out of range", (long long)pn);
+  ks_free_coarse(ctx);
   ctx->p_nnz = pn;
   KS_TRY(ks_alloc_t(ctx, &ctx->P_ptr, nf + 1, "P_ptr"));
   KS_TRY(ks_alloc_t(ctx, &ctx->P_col, pn, "P_col"));
@@ -359,84 +575,142 @@ ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, cons
   KS_CUDA(ctx, cudaMemcpyAsync(ctx->P_col, Pcol, 4 * pn, cudaMemcpyDeviceToDevice, s));
   KS_CUDA(ctx, cudaMemcpyAsync(ctx->P_val, Pval, 8 * pn, cudaMemcpyDeviceToDevice, s));
 
-  unsigned long long *bad = nullptr;
-  KS_CUDA(ctx, cudaMalloc((void **)&bad, 8));
-  struct Guard { void *p; ~Guard() { cudaFree(p); } } gbad{bad};
+  TmpGuard tg;
+  unsigned long long *bad;
+  uint64_t *key, *key_sorted;
+  int32_t *rows, *flag, *gincl, *gfirst, *iflag, *iincl, *item_of_pos, *dcnt, *ct_key, *ct_key_sorted, *ct_val;
+  TMPA(bad, 1);
+  TMPA(key, nf);
+  TMPA(key_sorted, nf);
+  TMPA(rows, nf);
+  KS_TRY(ks_alloc_t(ctx, &ctx->perm, nf, "perm"));
   KS_CUDA(ctx, cudaMemsetAsync(bad, 0xff, 8, s));
-  k_check_P<<<ks_blocks(nf, 256), 256, 0, s>>>(ctx->P_ptr, ctx->P_col, nf, n_H, pn, bad);
+  k_P_rows_keys<<<ks_blocks(nf, 256), 256, 0, s>>>(ctx->P_ptr, ctx->P_col, ctx->P_val, nf, n_H, pn, key, rows, bad);
   KS_LAUNCHED(ctx);
   unsigned long long h_bad = 0;
   KS_CUDA(ctx, cudaMemcpyAsync(&h_bad, bad, 8, cudaMemcpyDeviceToHost, s));
   KS_CUDA(ctx, cudaStreamSynchronize(s));
   if (h_bad != ~0ull)
-    return ks_fail(ctx, KS_E_ARG, "P row %llu invalid (more than 4 entries, or column outside [0, n_H))", h_bad);
+    return ks_fail(ctx, KS_E_ARG, "P row %llu invalid (more than 4 entries, repeated column, or column outside [0, n_H))", h_bad);
 
-  // ---- P^T (coarse-major) by a stable sort of the entries on their coarse column ----
-  int32_t *row_of, *keys_sorted, *idx, *idx_sorted;
-  KS_CUDA(ctx, cudaMalloc((void **)&row_of, 4 * (pn + 1)));
-  Guard g1{row_of};
-  KS_CUDA(ctx, cudaMalloc((void **)&keys_sorted, 4 * (pn + 1)));
-  Guard g2{keys_sorted};
-  KS_CUDA(ctx, cudaMalloc((void **)&idx, 4 * (pn + 1)));
-  Guard g3{idx};
-  KS_CUDA(ctx, cudaMalloc((void **)&idx_sorted, 4 * (pn + 1)));
-  Guard g4{idx_sorted};
-  k_P_rows<<<ks_blocks(nf, 256), 256, 0, s>>>(ctx->P_ptr, nf, row_of);
-  KS_LAUNCHED(ctx);
-  k_iota<<<ks_blocks(pn, 256), 256, 0, s>>>(idx, pn);
-  KS_LAUNCHED(ctx);
-  size_t tb = 0;
+  // ---- group rows by parent set (stable: ascending row inside a group), cut into items ----
   int end_bit = 1;
-  while ((1ll << end_bit) <= n_H) end_bit++;
-  KS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(nullptr, tb, ctx->P_col, keys_sorted, idx, idx_sorted, (int)pn, 0,
-                                               end_bit, s));
-  void *tmp;
-  KS_CUDA(ctx, cudaMalloc(&tmp, tb ? tb : 1));
-  Guard g5{tmp};
-  KS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(tmp, tb, ctx->P_col, keys_sorted, idx, idx_sorted, (int)pn, 0,
-                                               end_bit, s));
+  {
+    double bits = 4.0 * log2((double)n_H + 1.0);
+    end_bit = (int)ceil(bits) + 1;
+    if (end_bit > 64) end_bit = 64;
+  }
+  size_t tb = 0;
+  KS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key_sorted, rows, ctx->perm, (int)nf, 0, end_bit, s));
+  uint8_t *cub_tmp;
+  size_t cub_cap = tb;
+  TMPA(cub_tmp, cub_cap);
+  KS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(cub_tmp, tb, key, key_sorted, rows, ctx->perm, (int)nf, 0, end_bit, s));
   ctx->launches++;
-  KS_TRY(ks_alloc_t(ctx, &ctx->PT_ptr, n_H + 1, "PT_ptr"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->PT_row, pn, "PT_row"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->PT_val, pn, "PT_val"));
-  k_lower_bound_ptr<<<ks_blocks(n_H + 1, 256), 256, 0, s>>>(keys_sorted, pn, n_H, ctx->PT_ptr);
+  TMPA(flag, nf);
+  TMPA(gincl, nf);
+  TMPA(gfirst, nf);
+  TMPA(iflag, nf);
+  TMPA(iincl, nf);
+  TMPA(item_of_pos, nf);
+  k_group_flags<<<ks_blocks(nf, 256), 256, 0, s>>>(key_sorted, nf, flag);
   KS_LAUNCHED(ctx);
-  k_PT_fill<<<ks_blocks(pn, 256), 256, 0, s>>>(idx_sorted, row_of, ctx->P_val, pn, ctx->PT_row, ctx->PT_val);
-  KS_LAUNCHED(ctx);
-
-  // ---- pattern of G = H P ----
-  int32_t *cnt;
-  KS_CUDA(ctx, cudaMalloc((void **)&cnt, 4 * (nf + 1)));
-  Guard g6{cnt};
-  KS_CUDA(ctx, cudaMemsetAsync(bad, 0xff, 8, s));
-  k_G_pattern<<<ks_blocks(nf, 128), 128, 0, s>>>(ctx->row_ptr, ctx->col, ctx->P_ptr, ctx->P_col, nf, nullptr, cnt,
-                                                 nullptr, bad);
-  KS_LAUNCHED(ctx);
-  KS_TRY(ks_alloc_t(ctx, &ctx->G_ptr, nf + 1, "G_ptr"));
-  KS_CUDA(ctx, cudaMemsetAsync(cnt + nf, 0, 4, s));
-  size_t tb2 = 0;
-  KS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnt, ctx->G_ptr, (int)(nf + 1), s));
-  void *tmp2;
-  KS_CUDA(ctx, cudaMalloc(&tmp2, tb2 ? tb2 : 1));
-  Guard g7{tmp2};
-  KS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp2, tb2, cnt, ctx->G_ptr, (int)(nf + 1), s));
+  size_t need = 0;
+  KS_CUDA(ctx, cub::DeviceScan::InclusiveSum(nullptr, need, flag, gincl, (int)nf, s));
+  if (need > cub_cap) { cub_cap = need; TMPA(cub_tmp, cub_cap); }
+  tb = cub_cap;
+  KS_CUDA(ctx, cub::DeviceScan::InclusiveSum(cub_tmp, tb, flag, gincl, (int)nf, s));
   ctx->launches++;
-  int32_t h_g = 0;
-  KS_CUDA(ctx, cudaMemcpyAsync(&h_g, ctx->G_ptr + nf, 4, cudaMemcpyDeviceToHost, s));
-  KS_CUDA(ctx, cudaMemcpyAsync(&h_bad, bad, 8, cudaMemcpyDeviceToHost, s));
+  k_group_first<<<ks_blocks(nf, 256), 256, 0, s>>>(flag, gincl, nf, gfirst);
+  KS_LAUNCHED(ctx);
+  k_item_flags<<<ks_blocks(nf, 256), 256, 0, s>>>(gincl, gfirst, nf, iflag);
+  KS_LAUNCHED(ctx);
+  tb = cub_cap;
+  KS_CUDA(ctx, cub::DeviceScan::InclusiveSum(cub_tmp, tb, iflag, iincl, (int)nf, s));
+  ctx->launches++;
+  int32_t h_items = 0;
+  KS_CUDA(ctx, cudaMemcpyAsync(&h_items, iincl + nf - 1, 4, cudaMemcpyDeviceToHost, s));
   KS_CUDA(ctx, cudaStreamSynchronize(s));
-  if (h_bad != ~0ull) return ks_fail(ctx, KS_E_ARG, "row %llu of H P has more than %d entries", h_bad, GROW_MAX);
-  ctx->g_nnz = h_g;
-  KS_TRY(ks_alloc_t(ctx, &ctx->G_col, h_g, "G_col"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->G_val, h_g, "G_val"));
-  k_G_pattern<<<ks_blocks(nf, 128), 128, 0, s>>>(ctx->row_ptr, ctx->col, ctx->P_ptr, ctx->P_col, nf, ctx->G_ptr,
-                                                 nullptr, ctx->G_col, bad);
+  const int64_t ni = h_items;
+  ctx->n_items = ni;
+  KS_TRY(ks_alloc_t(ctx, &ctx->item_ptr, ni + 1, "item_ptr"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->item_S, 4 * ni, "item_S"));
+  int32_t h_nf = (int32_t)nf;
+  KS_CUDA(ctx, cudaMemcpyAsync(ctx->item_ptr + ni, &h_nf, 4, cudaMemcpyHostToDevice, s));
+  k_item_ptr<<<ks_blocks(nf, 256), 256, 0, s>>>(iflag, iincl, nf, ctx->item_ptr, item_of_pos);
+  KS_LAUNCHED(ctx);
+  TMPA(ct_key, 4 * ni);
+  TMPA(ct_key_sorted, 4 * ni);
+  TMPA(ct_val, 4 * ni);
+  KS_TRY(ks_alloc_t(ctx, &ctx->CT_val, 4 * ni, "CT_val"));
+  k_item_S<<<ks_blocks(ni, 256), 256, 0, s>>>(ctx->item_ptr, ctx->perm, ctx->P_ptr, ctx->P_col, ni, ctx->item_S,
+                                              ct_key, ct_val, (int32_t)n_H);
   KS_LAUNCHED(ctx);
 
-  // ---- cached B_H = P^T M P ----
+  // ---- coarse windows D per item ----
+  TMPA(dcnt, ni + 1);
+  KS_TRY(ks_alloc_t(ctx, &ctx->item_D_ptr, ni + 1, "item_D_ptr"));
+  const size_t bsm = sizeof(unsigned) * (size_t)((n_H + 31) / 32);
+  KS_CUDA(ctx, cudaFuncSetAttribute(k_item_D, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+  k_item_D<<<(unsigned)ni, 256, bsm, s>>>(ctx->item_ptr, ctx->perm, ctx->row_ptr, ctx->col, ctx->P_ptr, ctx->P_col,
+                                          (int32_t)n_H, dcnt, nullptr, nullptr);
+  KS_LAUNCHED(ctx);
+  KS_CUDA(ctx, cudaMemsetAsync(dcnt + ni, 0, 4, s));
+  need = 0;
+  KS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, need, dcnt, ctx->item_D_ptr, (int)(ni + 1), s));
+  if (need > cub_cap) { cub_cap = need; TMPA(cub_tmp, cub_cap); }
+  tb = cub_cap;
+  KS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(cub_tmp, tb, dcnt, ctx->item_D_ptr, (int)(ni + 1), s));
+  ctx->launches++;
+  int *dmax_d;
+  TMPA(dmax_d, 1);
+  need = 0;
+  KS_CUDA(ctx, cub::DeviceReduce::Max(nullptr, need, dcnt, dmax_d, (int)ni, s));
+  if (need > cub_cap) { cub_cap = need; TMPA(cub_tmp, cub_cap); }
+  tb = cub_cap;
+  KS_CUDA(ctx, cub::DeviceReduce::Max(cub_tmp, tb, dcnt, dmax_d, (int)ni, s));
+  ctx->launches++;
+  int32_t h_dtot = 0, h_dmax = 0;
+  KS_CUDA(ctx, cudaMemcpyAsync(&h_dtot, ctx->item_D_ptr + ni, 4, cudaMemcpyDeviceToHost, s));
+  KS_CUDA(ctx, cudaMemcpyAsync(&h_dmax, dmax_d, 4, cudaMemcpyDeviceToHost, s));
+  KS_CUDA(ctx, cudaStreamSynchronize(s));
+  if (h_dmax > DMAX - 1)
+    return ks_fail(ctx, KS_E_ARG, "an item touches %d coarse nodes (> %d): coarse mesh too fine for the fine mesh",
+                   h_dmax, DMAX - 1);
+  ctx->d_total = h_dtot;
+  ctx->d_max = h_dmax > 0 ? h_dmax : 1;
+  KS_TRY(ks_alloc_t(ctx, &ctx->item_D, h_dtot, "item_D"));
+  k_item_D<<<(unsigned)ni, 256, bsm, s>>>(ctx->item_ptr, ctx->perm, ctx->row_ptr, ctx->col, ctx->P_ptr, ctx->P_col,
+                                          (int32_t)n_H, nullptr, ctx->item_D_ptr, ctx->item_D);
+  KS_LAUNCHED(ctx);
+  KS_TRY(ks_alloc_t(ctx, &ctx->slotmap, 4 * ctx->nnz, "slotmap"));
+  k_slotmap<<<ks_blocks(nf, 128), 128, 0, s>>>(ctx->perm, item_of_pos, ctx->item_D_ptr, ctx->item_D, ctx->row_ptr,
+                                               ctx->col, ctx->P_ptr, ctx->P_col, nf, ctx->slotmap);
+  KS_LAUNCHED(ctx);
+
+  // ---- coarse node -> items list (stable sort on the coarse id; pads sort last) ----
+  int ct_bits = 1;
+  while ((1ll << ct_bits) <= n_H) ct_bits++;
+  need = 0;
+  KS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(nullptr, need, ct_key, ct_key_sorted, ct_val, ctx->CT_val, (int)(4 * ni),
+                                               0, ct_bits, s));
+  if (need > cub_cap) { cub_cap = need; TMPA(cub_tmp, cub_cap); }
+  tb = cub_cap;
+  KS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(cub_tmp, tb, ct_key, ct_key_sorted, ct_val, ctx->CT_val, (int)(4 * ni),
+                                               0, ct_bits, s));
+  ctx->launches++;
+  KS_TRY(ks_alloc_t(ctx, &ctx->CT_ptr, n_H + 1, "CT_ptr"));
+  k_lower_bound_ptr<<<ks_blocks(n_H + 1, 256), 256, 0, s>>>(ct_key_sorted, 4 * ni, n_H, ctx->CT_ptr);
+  KS_LAUNCHED(ctx);
+
+  // ---- cached B_H = P^T M P (A-part of the item pass with M) ----
+  KS_TRY(ks_alloc_t(ctx, &ctx->AH_part, 4 * ctx->d_total, "AH_part"));
   KS_TRY(ks_alloc_t(ctx, &ctx->B_H, n_H * n_H, "B_H"));
-  KS_TRY(g_values_launch(ctx, ctx->M));
-  KS_TRY(ptg_launch(ctx, ctx->G_val, ctx->B_H, n_H));
+  ctx->n_H = n_H;
+  ProjArgs a = base_args(ctx);
+  a.Aop = ctx->M;
+  KS_TRY((launch_items<16, false>(ctx, a)));
+  KS_TRY(launch_final<false>(ctx, 0, 16, ctx->B_H, nullptr, n_H, 0));
   KS_CUDA(ctx, cudaStreamSynchronize(s));
   return KS_OK;
 }
@@ -444,31 +718,44 @@ ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, cons
 ks_status ks_project_impl(ks_ctx *ctx, int N, const double *Ut, double *FA, double *FB) {
   cudaStream_t s = ctx->stream;
   const int64_t n = ctx->n_free, nH = ctx->n_H, D = nH + N;
-  if (ctx->y_cap < n * N) {
-    if (ctx->Y_H) { cudaFree(ctx->Y_H); ctx->Y_H = nullptr; }
-    if (ctx->Y_M) { cudaFree(ctx->Y_M); ctx->Y_M = nullptr; }
-    KS_TRY(ks_alloc_t(ctx, &ctx->Y_H, n * N, "Y_H"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->Y_M, n * N, "Y_M"));
-    ctx->y_cap = n * N;
+  const int np = pow2_at_least(N);
+  if (ctx->y_cap < n * np) {
+    for (double **b : {&ctx->Y_H, &ctx->Y_M, &ctx->proj_u})
+      if (*b) { cudaFree(*b); *b = nullptr; }
+    KS_TRY(ks_alloc_t(ctx, &ctx->Y_H, n * np, "Y_H"));
+    KS_TRY(ks_alloc_t(ctx, &ctx->Y_M, n * np, "Y_M"));
+    KS_TRY(ks_alloc_t(ctx, &ctx->proj_u, n * np, "proj U pad"));
+    ctx->y_cap = n * np;
   }
-  // K8: Y_H = H U~, Y_M = M U~
-  const bool fast = pow2_at_least(N) == N && ((uintptr_t)Ut & 15) == 0;
-  if (fast) {
-    switch (N) {
-#define KS_HM(NPV)                                                                                              \
-  case NPV:                                                                                                     \
-    k_HM_times<NPV><<<ks_blocks(n * Lay<NPV>::LPR, 256), 256, 0, s>>>(ctx->row_ptr, ctx->col, ctx->H, ctx->M, Ut, \
-                                                                      ctx->Y_H, ctx->Y_M, n);                    \
-    break;
-      KS_HM(1) KS_HM(2) KS_HM(4) KS_HM(8) KS_HM(16) KS_HM(32) KS_HM(64)
-#undef KS_HM
-    }
-  } else {
-    k_HM_times_generic<<<ks_blocks(n * N, 256), 256, 0, s>>>(ctx->row_ptr, ctx->col, ctx->H, ctx->M, Ut, ctx->Y_H,
-                                                             ctx->Y_M, n, N);
+  if (ctx->bc_cap < 4 * ctx->n_items * np) {
+    for (double **b : {&ctx->bH_part, &ctx->cH_part})
+      if (*b) { cudaFree(*b); *b = nullptr; }
+    KS_TRY(ks_alloc_t(ctx, &ctx->bH_part, 4 * ctx->n_items * np, "bH_part"));
+    KS_TRY(ks_alloc_t(ctx, &ctx->cH_part, 4 * ctx->n_items * np, "cH_part"));
+    ctx->bc_cap = 4 * ctx->n_items * np;
   }
-  KS_LAUNCHED(ctx);
-
+  const double *u = Ut;
+  if (np != N || ((uintptr_t)Ut & 15)) {
+    k_pad_proj<<<ks_blocks(n * np, 256), 256, 0, s>>>(Ut, N, ctx->proj_u, np, n);
+    KS_LAUNCHED(ctx);
+    u = ctx->proj_u;
+  }
+  // K8: item pass
+  ProjArgs a = base_args(ctx);
+  a.Aop = ctx->H;
+  a.U = u;
+  a.YH = ctx->Y_H;
+  a.YM = ctx->Y_M;
+  switch (np) {
+    case 1: KS_TRY((launch_items<1, true>(ctx, a))); break;
+    case 2: KS_TRY((launch_items<2, true>(ctx, a))); break;
+    case 4: KS_TRY((launch_items<4, true>(ctx, a))); break;
+    case 8: KS_TRY((launch_items<8, true>(ctx, a))); break;
+    case 16: KS_TRY((launch_items<16, true>(ctx, a))); break;
+    case 32: KS_TRY((launch_items<32, true>(ctx, a))); break;
+    case 64: KS_TRY((launch_items<64, true>(ctx, a))); break;
+    default: return ks_fail(ctx, KS_E_ARG, "N = %d unsupported", N);
+  }
   // K8b: beta, gamma
   const int nblk = 2 * ctx->sm_count;
   const int64_t rows_per_blk = ((n + nblk - 1) / nblk + GR_ROWS - 1) / GR_ROWS * GR_ROWS;
@@ -482,27 +769,17 @@ ks_status ks_project_impl(ks_ctx *ctx, int N, const double *Ut, double *FA, doub
   {
     const int NQ = (N + 3) / 4 * 4, NT = NQ / 4;
     const int ntiles = 2 * NT * NT;
-    const int ngroups = ntiles >= 256 ? 1 : 256 / ntiles;
+    if (ntiles > 512) return ks_fail(ctx, KS_E_ARG, "N = %d too large for the Gram kernel", N);
+    const int ngroups = ntiles > 256 ? 1 : 256 / ntiles;
     const size_t sm = sizeof(double) * (3 * GR_ROWS * NQ + (size_t)ngroups * 2 * N * N);
-    if (ntiles > 512) return ks_fail(ctx, KS_E_ARG, "N=%d too large for the Gram kernel", N);
     KS_CUDA(ctx, cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k_gram<<<nb, 256, sm, s>>>(Ut, ctx->Y_H, ctx->Y_M, n, N, rows_per_blk, ctx->gram_part);
+    k_gram<<<nb, 256, sm, s>>>(u, ctx->Y_H, ctx->Y_M, n, N, np, rows_per_blk, ctx->gram_part);
     KS_LAUNCHED(ctx);
     k_gram_final<<<ks_blocks(2 * N * N, 128), 128, 0, s>>>(ctx->gram_part, nb, N, nH, D, FA, FB);
     KS_LAUNCHED(ctx);
   }
-
-  // K9: b_H, c_H
-  {
-    const int T = N * (256 / N >= 1 ? 256 / N : 1);
-    k_PtY<<<(unsigned)nH, T, sizeof(double) * 2 * T, s>>>(ctx->PT_ptr, ctx->PT_row, ctx->PT_val, ctx->Y_H, ctx->Y_M,
-                                                          N, nH, D, FA, FB);
-    KS_LAUNCHED(ctx);
-  }
-
-  // K10: A_H = P^T (H P) into F_A, cached B_H into F_B
-  KS_TRY(g_values_launch(ctx, ctx->H));
-  KS_TRY(ptg_launch(ctx, ctx->G_val, FA, D));
+  // K9: A_H, b_H, c_H
+  KS_TRY(launch_final<true>(ctx, N, np, FA, FB, D, D));
   k_copy_block<<<ks_blocks(nH * nH, 256), 256, 0, s>>>(ctx->B_H, nH, FB, D);
   KS_LAUNCHED(ctx);
   return KS_OK;
