@@ -185,6 +185,25 @@ def cpu_baseline(p):
             "seconds": dt}
 
 
+def rank_seed(config, rank):
+    """Seed of the independent problem a rank solves (weak scaling)."""
+    return gen.SEED_BASE + config + 1000 * rank
+
+
+def combine_ranks(ms, units, world, dev):
+    """(max over ranks of a device time in ms, sum over ranks of work units). Plumbing only: no data of
+    the method crosses ranks."""
+    if world <= 1:
+        return float(ms), float(units)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    u = torch.tensor([float(units)], dtype=torch.float64, device=dev)
+    dist.all_reduce(u, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(u.item())
+
+
 def workload_config(p):
     return {"workload": f"{p.cfg['name']}: graded Kuhn tet mesh {p.n_cells}^3 cells on [-{p.L:g},{p.L:g}]^3, "
                         f"N={p.N} orbitals, block Jacobi-PCG tol {TOL:g}, coarse {p.nc}^3",
@@ -271,16 +290,7 @@ def run_ours(args, p, rank, world, local):
     k_last = ctx.last_iterations()
     units_rank = args.steps * p.N * p.n_free * k_last
 
-    # max over ranks of the device time; sum of units
-    if world > 1:
-        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms_max = float(tt.item())
-        uu = torch.tensor([float(units_rank)], dtype=torch.float64, device=dev)
-        dist.all_reduce(uu, op=dist.ReduceOp.SUM)
-        units_all = float(uu.item())
-    else:
-        total_ms_max, units_all = total_ms, float(units_rank)
+    total_ms_max, units_all = combine_ranks(total_ms, units_rank, world, dev)
     value = units_all / (total_ms_max * 1e-3)
 
     # ---- e2e through the public API with host (pinned) buffers ----
@@ -303,10 +313,7 @@ def run_ours(args, p, rank, world, local):
         h1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = h0.elapsed_time(h1)
-        if world > 1:
-            tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_ms = float(tt.item())
+        e2e_ms, _ = combine_ranks(e2e_ms, 0, world, dev)
         h2d = Vh.numel() * 8 + lamh.numel() * 8 + Uh.numel() * 8
         d2h = 2 * D * D * 8
         e2e = {"value": units_all / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
@@ -362,7 +369,7 @@ def main():
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     # independent problem per rank (weak scaling): seed offset by rank
-    p = gen.make_problem(args.config, seed=gen.SEED_BASE + args.config + 1000 * rank)
+    p = gen.make_problem(args.config, seed=rank_seed(args.config, rank))
     if args.impl == "reference":
         run_reference(args, p, rank, world)
     else:
