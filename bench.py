@@ -122,6 +122,38 @@ def bytes_solve_init(n, nnz, N):
     return 20 * nnz + 4 * (n + 1) + 8 * n + 8 * N * n * 4
 
 
+def phase_bytes(n, nnz, N):
+    """Algorithmic bytes of the three phases of one PCG iteration as the kernel runs them (10 vector
+    touches; z = r/d is never stored): S = SpMM q = A p (matrix + row_ptr, read p, write q),
+    U = r -= alpha q (read r, q, 1/d; write r), P = x += alpha p, p = z + beta p (read r, p, x, 1/d;
+    write x, p)."""
+    return {"S": 12 * nnz + 4 * (n + 1) + 16 * N * n,
+            "U": 24 * N * n + 8 * n,
+            "P": 40 * N * n + 8 * n}
+
+
+def traced_phases(ctx, solve, n, nnz, N, peak):
+    """One extra block solve with KS_PCG_TRACE=1: per-phase device time (mean over iterations, from the
+    kernel's own %globaltimer stamps at every grid barrier) and achieved GB/s against `peak`."""
+    os.environ["KS_PCG_TRACE"] = "1"
+    try:
+        solve()
+        ts = ctx.solve_trace()
+    finally:
+        os.environ.pop("KS_PCG_TRACE", None)
+    if len(ts) < 5:
+        return None
+    d = np.diff(ts.astype(np.int64)) * 1e-6  # ms
+    k = (len(d) - 1) // 3
+    out = {"init_ms": float(d[0]), "iterations": int(k)}
+    pb = phase_bytes(n, nnz, N)
+    for j, name in enumerate(("S", "U", "P")):
+        ms = float(np.mean(d[1 + j::3][:k]))
+        gbs = pb[name] / (ms * 1e-3) / 1e9
+        out[name] = {"ms": ms, "alg_bytes": int(pb[name]), "GB/s": gbs, "frac": gbs / peak}
+    return out
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -346,6 +378,8 @@ def run_ours(args, p, rank, world, local):
                      "alg_bytes_def": "init (20 nnz + 12 n + 32 N n) + k x textbook B_it (12 nnz + 20 n + 88 N n)"},
         "phases_ms": {"assemble_veff": t_asm, "block_solve": t_solve, "project_augmented": t_proj},
         "solve_only_value": N * n * k_last / (t_solve * 1e-3),
+        "pcg_phases": traced_phases(ctx, lambda: ctx.block_solve(lam, U, Ut, tol=TOL, max_iter=MAX_ITER, iters=iters,
+                                                                 relres=relres), n, nnz, N, peak),
         "gpu_launches": int(launches),
         "clocks": clk,
     }

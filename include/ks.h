@@ -133,6 +133,13 @@ ks_status ks_block_solve(ks_ctx *ctx, int32_t N, const double *d_lambda, const d
 /* Number of block iterations (max over columns) of the last ks_block_solve; synchronises the stream. */
 ks_status ks_last_iterations(ks_ctx *ctx, int32_t *h_block_iters);
 
+/* Phase timestamps of the last ks_block_solve, for profiling. Recorded only when the environment variable
+ * KS_PCG_TRACE=1 was set at that call: block 0 stamps %globaltimer (ns) at kernel start and after every
+ * grid barrier, i.e. [start, init, then per iteration: S (q = Ap), U (r update), P (x, p update)].
+ *   cap       capacity of h_ns;   h_ns [cap] u64 (host, output);   *h_count (host, output) = entries written
+ *             (0 when tracing was off). Synchronises the stream. */
+ks_status ks_solve_trace(ks_ctx *ctx, int32_t cap, uint64_t *h_ns, int32_t *h_count);
+
 /* True relative residual ||(lambda_i+mu) M u_i - A u~_i|| / ||(lambda_i+mu) M u_i|| per column into
  * d_relres [N] (parity helper, one extra SpMM pass). Asynchronous. */
 ks_status ks_true_residual(ks_ctx *ctx, int32_t N, const double *d_lambda, const double *d_U,

@@ -53,6 +53,9 @@ ks_status ks_alloc(ks_ctx *ctx, void **ptr, size_t bytes, const char *what) {
     return ks_fail(ctx, KS_E_NOMEM, "cudaMalloc(%zu bytes) for %s: %s", bytes, what, cudaGetErrorString(e));
   }
   ctx->bytes += bytes;
+  // zero-filled: padding tails past the logical ends (read by the bulk tile copies) stay defined
+  e = cudaMemsetAsync(*ptr, 0, bytes, ctx->stream);
+  if (e != cudaSuccess) return ks_cuda_check(ctx, e, "cudaMemsetAsync (new allocation)");
   return KS_OK;
 }
 
@@ -213,6 +216,22 @@ ks_status ks_last_iterations(ks_ctx *ctx, int32_t *h_block_iters) {
   if (!ctx || !h_block_iters) return KS_E_ARG;
   KS_CUDA(ctx, cudaMemcpyAsync(h_block_iters, ctx->d_block_iters, 4, cudaMemcpyDeviceToHost, ctx->stream));
   KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return KS_OK;
+}
+
+ks_status ks_solve_trace(ks_ctx *ctx, int32_t cap, uint64_t *h_ns, int32_t *h_count) {
+  if (!ctx || !h_count || (cap > 0 && !h_ns)) return KS_E_ARG;
+  *h_count = 0;
+  if (!ctx->trace) return KS_OK;
+  int n = 0;
+  KS_CUDA(ctx, cudaMemcpyAsync(&n, ctx->trace_count, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (n > cap) n = cap;
+  if (n > 0) {
+    KS_CUDA(ctx, cudaMemcpyAsync(h_ns, ctx->trace, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  *h_count = n;
   return KS_OK;
 }
 

@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
     const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col, const int32_t *__restrict__ inv_ptr,
     const int32_t *__restrict__ inv_idx, const double *__restrict__ w, const double *__restrict__ v_free,
     const double *__restrict__ K, const double *__restrict__ M, double mu, int64_t n_free, double *__restrict__ MV,
-    double *__restrict__ H, double *__restrict__ A, double *__restrict__ diag) {
+    double *__restrict__ H, double *__restrict__ A, double *__restrict__ diag, double *__restrict__ dinv) {
   int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 4;
   int j = threadIdx.x & 15;
   if (row >= n_free) return;
@@ -59,7 +59,10 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
     MV[e] = mv;
     H[e] = h;
     A[e] = a;
-    if (c == row) diag[row] = a;
+    if (c == row) {
+      diag[row] = a;
+      dinv[row] = 1.0 / a;
+    }
   }
 }
 
@@ -73,7 +76,7 @@ ks_status ks_assemble_impl(ks_ctx *ctx, const double *d_veff, double mu) {
   KS_LAUNCHED(ctx);
   k_assemble_rows<<<ks_blocks(16 * ctx->n_free, 256), 256, 0, s>>>(
       ctx->row_ptr, ctx->col, ctx->inv_ptr, ctx->inv_idx, ctx->w_tet, ctx->v_free, ctx->K, ctx->M, mu,
-      ctx->n_free, ctx->MV, ctx->H, ctx->A, ctx->diag);
+      ctx->n_free, ctx->MV, ctx->H, ctx->A, ctx->diag, ctx->dinv);
   KS_LAUNCHED(ctx);
   ctx->mu = mu;
   ctx->assembled = true;

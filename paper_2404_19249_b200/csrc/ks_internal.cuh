@@ -39,6 +39,7 @@ struct ks_ctx {
   double *vol = nullptr;            // [n_tets]
   double *K = nullptr, *M = nullptr, *MV = nullptr, *H = nullptr, *A = nullptr;  // [nnz]
   double *diag = nullptr;           // [n_free] diag(A)
+  double *dinv = nullptr;           // [n_free + 2] 1 / diag(A) (Jacobi preconditioner), zero padded
   double *w_tet = nullptr;          // [n_tets] |T| S_T (assembly scratch)
   double *v_free = nullptr;         // [n_free] V at free nodes (assembly scratch)
   double mu = 0.0;
@@ -47,6 +48,8 @@ struct ks_ctx {
   // device status
   unsigned *d_flags = nullptr;      // latched KSF_* bits
   int32_t *d_block_iters = nullptr; // [1] block iterations of the last solve
+  unsigned long long *trace = nullptr;  // [KS_TRACE_CAP] phase-end timestamps of the last traced solve
+  int *trace_count = nullptr;
 
   // solver workspace (grown on demand)
   int ws_np = 0;                    // padded N the workspace was sized for
@@ -55,6 +58,7 @@ struct ks_ctx {
   double *partials = nullptr;       // [grid][4 * 64]
   unsigned *barrier = nullptr;      // grid barrier counter
   int64_t partial_cap = 0;
+  std::vector<std::pair<int, int>> tile_nnz_cache;  // (tile rows, max nnz of such a tile)
 
   // coarse space (ks_set_coarse) and projection workspace
   int64_t n_H = 0, p_nnz = 0;
@@ -83,6 +87,10 @@ struct ks_ctx {
 };
 
 #define KS_MAX_N 64
+// elements of padding behind row_ptr, col and the value arrays: the bulk (TMA) tile copies round their
+// ranges out to 16-byte boundaries and may read up to this far past the logical end.
+#define KS_PAD 8
+#define KS_TRACE_CAP 8192
 
 const char *ks_status_name(ks_status s);
 ks_status ks_fail(ks_ctx *ctx, ks_status s, const char *fmt, ...);

@@ -285,8 +285,8 @@ ks_status ks_setup_mesh(ks_ctx *ctx, const double *h_xyz, const int32_t *h_tets,
   const int64_t nnz = (last_key == sentinel) ? h_nsel - 1 : h_nsel;
   ctx->nnz = nnz;
   if (nnz > 0x7fffffffLL) return ks_fail(ctx, KS_E_ARG, "nnz %lld exceeds int32 indexing", (long long)nnz);
-  KS_TRY(ks_alloc_t(ctx, &ctx->row_ptr, nf + 1, "row_ptr"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->col, nnz, "col"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->row_ptr, nf + 1 + KS_PAD, "row_ptr"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->col, nnz + KS_PAD, "col"));
   KS_TRY(ks_alloc_t(ctx, &ctx->diag_pos, nf, "diag_pos"));
   k_row_ptr<<<ks_blocks(nf + 1, T), T, 0, s>>>(uniq, nnz, nf, ctx->row_ptr);
   KS_LAUNCHED(ctx);
@@ -323,16 +323,17 @@ ks_status ks_setup_mesh(ks_ctx *ctx, const double *h_xyz, const int32_t *h_tets,
   KS_CUDA(ctx, cudaMemcpyAsync(ctx->inv_idx, iv_sorted, sizeof(int32_t) * h_nc, cudaMemcpyDeviceToDevice, s));
 
   // --- K and M ---
-  KS_TRY(ks_alloc_t(ctx, &ctx->K, nnz, "K"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->M, nnz, "M"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->K, nnz + KS_PAD, "K"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->M, nnz + KS_PAD, "M"));
   k_stiffness_mass<<<ks_blocks(nnz, T), T, 0, s>>>(ctx->inv_ptr, ctx->inv_idx, ctx->vol, grad, nnz, ctx->K, ctx->M);
   KS_LAUNCHED(ctx);
 
   // value arrays filled by assembly, scratch
-  KS_TRY(ks_alloc_t(ctx, &ctx->MV, nnz, "MV"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->H, nnz, "H"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->A, nnz, "A"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->MV, nnz + KS_PAD, "MV"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->H, nnz + KS_PAD, "H"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->A, nnz + KS_PAD, "A"));
   KS_TRY(ks_alloc_t(ctx, &ctx->diag, nf, "diag"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->dinv, nf + 2, "dinv"));  // +2: zero pad for the NP = 1 pairwise streams
   KS_TRY(ks_alloc_t(ctx, &ctx->w_tet, nt, "w_tet"));
   KS_TRY(ks_alloc_t(ctx, &ctx->v_free, nf, "v_free"));
   KS_CUDA(ctx, cudaStreamSynchronize(s));  // temporaries are freed by ~TempBuf after this point

@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libks.so")
+# KS_LIB overrides the library path (A/B builds of the same sources with other compile-time options)
+LIB_PATH = os.environ.get("KS_LIB") or os.path.join(_PKG, "libks.so")
 
 KS_OK, KS_E_ARG, KS_E_MESH, KS_E_NONFINITE, KS_E_NOT_SPD, KS_E_NOT_CONVERGED, KS_E_CUDA, KS_E_NOMEM, \
     KS_E_STATE = range(9)
@@ -22,7 +23,7 @@ OPS = {"K": 0, "M": 1, "MV": 2, "H": 3, "A": 4}
 
 # every symbol declared in include/ks.h (checked by tests/test_abi.py)
 EXPORTS = ["ks_abi_version", "ks_build_info", "ks_create", "ks_destroy", "ks_set_stream", "ks_pattern",
-           "ks_values", "ks_assemble_veff", "ks_spmm", "ks_block_solve", "ks_last_iterations",
+           "ks_values", "ks_assemble_veff", "ks_spmm", "ks_block_solve", "ks_last_iterations", "ks_solve_trace",
            "ks_true_residual", "ks_set_coarse", "ks_project_augmented", "ks_memory_bytes", "ks_launch_count",
            "ks_sync", "ks_last_error"]
 
@@ -58,6 +59,7 @@ def load_library(path: str = LIB_PATH):
         "ks_spmm": (st, [vp, C.c_int, i32, vp, vp]),
         "ks_block_solve": (st, [vp, i32, vp, vp, vp, dbl, i32, vp, vp]),
         "ks_last_iterations": (st, [vp, C.POINTER(i32)]),
+        "ks_solve_trace": (st, [vp, i32, vp, C.POINTER(i32)]),
         "ks_true_residual": (st, [vp, i32, vp, vp, vp, vp]),
         "ks_set_coarse": (st, [vp, i64, vp, vp, vp]),
         "ks_project_augmented": (st, [vp, i32, vp, vp, vp]),
@@ -204,6 +206,13 @@ class Context:
         v = C.c_int32()
         self._call(self._L.ks_last_iterations(self._h, C.byref(v)))
         return v.value
+
+    def solve_trace(self, cap: int = 8192) -> np.ndarray:
+        """Phase-end timestamps (ns) of the last block solve (KS_PCG_TRACE=1 at solve time), see ks.h."""
+        buf = np.zeros(cap, dtype=np.uint64)
+        cnt = C.c_int32()
+        self._call(self._L.ks_solve_trace(self._h, cap, buf.ctypes.data, C.byref(cnt)))
+        return buf[:cnt.value].copy()
 
     def true_residual(self, lam, U, Ut):
         import torch
