@@ -196,7 +196,7 @@ ks_status ks_spmm(ks_ctx *ctx, ks_op op, int32_t N, const double *d_X, double *d
   if (((uintptr_t)d_X & 7) || ((uintptr_t)d_Y & 7)) return ks_fail(ctx, KS_E_ARG, "ks_spmm: X, Y must be 8-byte aligned");
   const double *v = op_values(ctx, op);
   if (!v) return ks_fail(ctx, KS_E_STATE, "ks_spmm: operator %d not assembled", (int)op);
-  return ks_spmm_impl(ctx, v, N, d_X, d_Y);
+  return ks_spmm_impl(ctx, op, v, N, d_X, d_Y);
 }
 
 ks_status ks_block_solve(ks_ctx *ctx, int32_t N, const double *d_lambda, const double *d_U, double *d_Ut,

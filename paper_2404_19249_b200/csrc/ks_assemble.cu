@@ -39,12 +39,14 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
     const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col, const int32_t *__restrict__ inv_ptr,
     const int32_t *__restrict__ inv_idx, const double *__restrict__ w, const double *__restrict__ v_free,
     const double *__restrict__ K, const double *__restrict__ M, double mu, int64_t n_free, double *__restrict__ MV,
-    double *__restrict__ H, double *__restrict__ A, double *__restrict__ diag, double *__restrict__ dinv) {
+    double *__restrict__ H, double *__restrict__ A, double *__restrict__ diag, double *__restrict__ dinv,
+    const int32_t *__restrict__ sell_ptr, double *__restrict__ sell_A) {
   int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 4;
   int j = threadIdx.x & 15;
   if (row >= n_free) return;
   const double vi = __ldg(v_free + row);
-  const int32_t k1 = __ldg(row_ptr + row + 1);
+  const int32_t kr = __ldg(row_ptr + row), k1 = __ldg(row_ptr + row + 1);
+  const int64_t sbase = __ldg(sell_ptr + row / KS_SELL_C) + (row % KS_SELL_C) * 4;
   for (int32_t e = __ldg(row_ptr + row) + j; e < k1; e += 16) {
     const int32_t c = __ldg(col + e);
     double s = 0.0;
@@ -59,6 +61,8 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
     MV[e] = mv;
     H[e] = h;
     A[e] = a;
+    const int k = e - kr;   // slot of the entry in the sliced-ELL copy (ks_sell.cu)
+    sell_A[sbase + (k >> 2) * (4 * KS_SELL_C) + (k & 3)] = a;
     if (c == row) {
       diag[row] = a;
       dinv[row] = 1.0 / a;
@@ -76,7 +80,7 @@ ks_status ks_assemble_impl(ks_ctx *ctx, const double *d_veff, double mu) {
   KS_LAUNCHED(ctx);
   k_assemble_rows<<<ks_blocks(16 * ctx->n_free, 256), 256, 0, s>>>(
       ctx->row_ptr, ctx->col, ctx->inv_ptr, ctx->inv_idx, ctx->w_tet, ctx->v_free, ctx->K, ctx->M, mu,
-      ctx->n_free, ctx->MV, ctx->H, ctx->A, ctx->diag, ctx->dinv);
+      ctx->n_free, ctx->MV, ctx->H, ctx->A, ctx->diag, ctx->dinv, ctx->sell_ptr, ctx->sell_A);
   KS_LAUNCHED(ctx);
   ctx->mu = mu;
   ctx->assembled = true;

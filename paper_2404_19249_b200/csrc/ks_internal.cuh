@@ -41,6 +41,11 @@ struct ks_ctx {
   double *diag = nullptr;           // [n_free] diag(A)
   double *dinv = nullptr;           // [n_free + 2] 1 / diag(A) (Jacobi preconditioner), zero padded
   double *w_tet = nullptr;          // [n_tets] |T| S_T (assembly scratch)
+  // sliced-ELL copy of the pattern for the block-PCG SpMM (ks_sell.cu): A (per assembly) and M (fixed)
+  int64_t n_slices = 0, sell_total = 0;
+  int32_t *sell_ptr = nullptr;      // [n_slices+1] first entry of each 8-row slice
+  int32_t *sell_col = nullptr;      // [sell_total]
+  double *sell_A = nullptr, *sell_M = nullptr;  // [sell_total]
   double *v_free = nullptr;         // [n_free] V at free nodes (assembly scratch)
   double mu = 0.0;
   bool assembled = false;
@@ -91,6 +96,7 @@ struct ks_ctx {
 // ranges out to 16-byte boundaries and may read up to this far past the logical end.
 #define KS_PAD 8
 #define KS_TRACE_CAP 8192
+#define KS_SELL_C 8   // rows per slice of the sliced-ELL operator copy
 
 const char *ks_status_name(ks_status s);
 ks_status ks_fail(ks_ctx *ctx, ks_status s, const char *fmt, ...);
@@ -131,8 +137,9 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // internal entry points implemented in the .cu files
 ks_status ks_setup_mesh(ks_ctx *ctx, const double *h_xyz, const int32_t *h_tets, const uint8_t *h_dir);
+ks_status ks_sell_build(ks_ctx *ctx);
 ks_status ks_assemble_impl(ks_ctx *ctx, const double *d_veff, double mu);
-ks_status ks_spmm_impl(ks_ctx *ctx, const double *val, int N, const double *X, double *Y);
+ks_status ks_spmm_impl(ks_ctx *ctx, ks_op op, const double *val, int N, const double *X, double *Y);
 ks_status ks_solve_impl(ks_ctx *ctx, int N, const double *lambda, const double *U, double *Ut, double tol,
                         int max_iter, int32_t *iters, double *relres);
 ks_status ks_true_residual_impl(ks_ctx *ctx, int N, const double *lambda, const double *U,

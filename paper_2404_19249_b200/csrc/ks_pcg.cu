@@ -3,26 +3,22 @@
 // solved as ONE batched Jacobi-preconditioned CG over the [n][NP] orbital block by a persistent
 // cooperative kernel (one launch per solve, no host round trip). Per iteration, with per-column
 // alpha_i, beta_i and masks (DESIGN.md §4.3 "block PCG"):
-//   S  q = A p                      (multi-RHS CSR SpMM, fused p.q partials)          | grid barrier
-//   U  r -= alpha q, z = r / d      (fused r.z and r.r partials)                       | grid barrier
-//   P  x += alpha p, p = z + beta p (x update deferred to here so p is read once)      | grid barrier
-// Memory-level parallelism (the kernel is HBM-latency bound without it, profiles/r01_ncu_summary.md):
-//   * S stages each warp's rows of a tile (their slices of row_ptr / col / A values) into shared memory
-//     with bulk (TMA) copies, cp.async.bulk + one mbarrier per (warp, stage), STAGES tiles ahead; each
-//     warp runs its own pipeline (no block-wide sync per tile) and the next iteration's first tiles are
-//     prefetched while the U and P phases stream. The gathers of p then only wait on shared memory, and
-//     every lane issues 8 independent 16-byte gathers at a time (rows padded with the own row and a zero
-//     weight, so the loads are unconditional).
-//   * U and P stream UNR chunks per thread with all loads issued before any use.
-//   * The Jacobi preconditioner is applied as a product with 1/diag(A) (precomputed by the assembly).
+//   S  q = A p                      (multi-RHS SpMM on the sliced-ELL copy, fused p.q partials)  | barrier
+//   U  r -= alpha q, z = r / d      (fused r.z and r.r partials)                                  | barrier
+//   P  x += alpha p, p = z + beta p (x update deferred to here so p is read once)                 | barrier
+// Throughput design (profiles/r01_ncu_summary.md):
+//   * S reads the operator in SELL-8 (ks_sell.cu): per 4 nonzeros of a row one 16-byte col load and one
+//     32-byte value load, shared by the lanes of the row; the orbital rows are gathered with 32-byte
+//     loads (LDG.256), 4 lanes per 128-byte row at N = 16. The CSR form spent as many L1 wavefronts on
+//     broadcast col/val loads as on the gathers.
+//   * U and P stream 32-byte vectors (one row segment of 4 orbitals per thread).
+//   * The Jacobi preconditioner is a product with 1/diag(A) (precomputed by the assembly).
 // Reductions are deterministic: each block owns a fixed, interleaved set of row tiles, reduces in a fixed
 // order and writes one partial per column; after the barrier every block sums the partials in the same
 // fixed order, so all blocks hold bitwise-identical alpha/beta and the result is reproducible run to run.
 // Tiles are interleaved across blocks (tile t -> block t mod G) so that the gathered rows of p form a
-// sweeping front that stays L2-resident. The U/P chunk of 2*PCG_THREADS doubles is the
+// sweeping front that stays L2-resident. The U/P chunk (VEC doubles per thread) is the
 // same row range as the S tile, so U and P touch only rows the block itself produced in S.
-#include <cooperative_groups.h>
-
 #include "ks_internal.cuh"
 #include "ks_rowops.cuh"
 
@@ -32,27 +28,163 @@ namespace {
 #define KS_PCG_THREADS 512
 #endif
 #ifndef KS_PCG_MINB
-#define KS_PCG_MINB 2
+#define KS_PCG_MINB 1
 #endif
-constexpr int PCG_THREADS = KS_PCG_THREADS;   // 512 threads x 2 blocks/SM: 64 registers, no spills
+#ifndef KS_PCG_SUNR
+#define KS_PCG_SUNR 2
+#endif
+constexpr int PCG_THREADS = KS_PCG_THREADS;   // 512 threads x 1 block/SM: 128 registers, no spills
+constexpr int SUNR = KS_PCG_SUNR;             // slot groups (4 gathers each) in flight per lane
 constexpr int PCG_WARPS = PCG_THREADS / 32;
-constexpr int CHUNK = 2 * PCG_THREADS;   // doubles per streaming chunk (one double2 per thread)
-constexpr int STAGES = 3;                // bulk-copy pipeline depth of the S phase
-#ifndef KS_PCG_GATHER
-#define KS_PCG_GATHER 8
-#endif
-#ifndef KS_PCG_UNR_U
-#define KS_PCG_UNR_U 1
-#endif
-#ifndef KS_PCG_UNR_P
-#define KS_PCG_UNR_P 1
-#endif
-constexpr int GATHER = KS_PCG_GATHER;    // independent gathers per lane in flight
-constexpr int UNR_U = KS_PCG_UNR_U, UNR_P = KS_PCG_UNR_P;  // streaming chunks per thread per step (U, P)
+
+// Solver layout of an [n][NP] block: a row group of LPR lanes owns one row, lane `sub` owns the VEC
+// consecutive orbitals sub*VEC .. sub*VEC+VEC-1 (32-byte vectors for NP >= 4). Lane l therefore owns
+// columns (VEC*l) % NP + v, in the S phase (row groups) and in the U/P streams (element VEC*thread).
+template <int NP>
+struct SL {
+  static_assert(NP == 1 || NP == 2 || NP == 4 || NP == 8 || NP == 16 || NP == 32 || NP == 64, "NP");
+  static constexpr int VEC = NP >= 4 ? 4 : NP;
+  static constexpr int LPR = NP / VEC;
+  static constexpr int RPW = 32 / LPR;
+  static constexpr int TILE = PCG_WARPS * RPW;        // rows per tile
+  static constexpr int CHUNK = PCG_THREADS * VEC;     // doubles per U/P chunk (= TILE * NP)
+  static_assert(TILE * NP == CHUNK, "S tile and U/P chunk must cover the same rows");
+};
+
+template <int V>
+struct DV;  // V consecutive doubles
+template <>
+struct DV<1> {
+  double v[1];
+  __device__ __forceinline__ static DV ld(const double *p) { DV r; r.v[0] = *p; return r; }
+  __device__ __forceinline__ void st(double *p) const { *p = v[0]; }
+};
+template <>
+struct DV<2> {
+  double v[2];
+  __device__ __forceinline__ static DV ld(const double *p) {
+    double2 t = *reinterpret_cast<const double2 *>(p);
+    DV r; r.v[0] = t.x; r.v[1] = t.y; return r;
+  }
+  __device__ __forceinline__ void st(double *p) const { *reinterpret_cast<double2 *>(p) = make_double2(v[0], v[1]); }
+};
+template <>
+struct DV<4> {
+  double v[4];
+  __device__ __forceinline__ static DV ld(const double *p) {   // LDG.256 (32-byte aligned)
+    DV r;
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3]) : "l"(p) : "memory");
+    return r;
+  }
+  __device__ __forceinline__ void st(double *p) const {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+                 : "memory");
+  }
+};
+
+__device__ __forceinline__ void ldnc_v4(const double *p, double &a, double &b, double &c, double &d) {
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+
+// One row of Y = Op X on the sliced-ELL copy (ks_sell.cu): slot groups of 4, CSR order within the row,
+// padding slots gather the own row with weight 0. NV = 1 (ya = A x) or 2 (ya = A x, yb = B x on the
+// same col stream). The operator arrays are read-only for the kernel's lifetime (non-coherent path);
+// X may have been written by other blocks before a grid barrier and is read with coherent loads.
+template <int NP, int NV>
+__device__ __forceinline__ void sell_row(const int32_t *__restrict__ sell_ptr, const int32_t *__restrict__ scol,
+                                         const double *__restrict__ va, const double *__restrict__ vb, int64_t row,
+                                         const double *X, int sub, DV<SL<NP>::VEC> &ya, DV<SL<NP>::VEC> &yb) {
+  constexpr int VEC = SL<NP>::VEC;
+#pragma unroll
+  for (int v = 0; v < VEC; v++) ya.v[v] = yb.v[v] = 0.0;
+  const int64_t s = row / KS_SELL_C;
+  const int32_t b = __ldg(sell_ptr + s), e = __ldg(sell_ptr + s + 1);
+  const int groups = (e - b) / (4 * KS_SELL_C);
+  const int64_t base = b + (row % KS_SELL_C) * 4;
+  const double *xs = X + sub * VEC;
+  int g = 0;
+  if (SUNR == 2) {
+    for (; g + 2 <= groups; g += 2) {   // two slot groups: 8 gathers in flight per lane
+      const int64_t o = base + (int64_t)g * (4 * KS_SELL_C), o2 = o + 4 * KS_SELL_C;
+      const int4 c = __ldg(reinterpret_cast<const int4 *>(scol + o));
+      const int4 d = __ldg(reinterpret_cast<const int4 *>(scol + o2));
+      double a[8], bb[8];
+      ldnc_v4(va + o, a[0], a[1], a[2], a[3]);
+      ldnc_v4(va + o2, a[4], a[5], a[6], a[7]);
+      if (NV == 2) {
+        ldnc_v4(vb + o, bb[0], bb[1], bb[2], bb[3]);
+        ldnc_v4(vb + o2, bb[4], bb[5], bb[6], bb[7]);
+      }
+      DV<VEC> x[8];
+      x[0] = DV<VEC>::ld(xs + (int64_t)c.x * NP);
+      x[1] = DV<VEC>::ld(xs + (int64_t)c.y * NP);
+      x[2] = DV<VEC>::ld(xs + (int64_t)c.z * NP);
+      x[3] = DV<VEC>::ld(xs + (int64_t)c.w * NP);
+      x[4] = DV<VEC>::ld(xs + (int64_t)d.x * NP);
+      x[5] = DV<VEC>::ld(xs + (int64_t)d.y * NP);
+      x[6] = DV<VEC>::ld(xs + (int64_t)d.z * NP);
+      x[7] = DV<VEC>::ld(xs + (int64_t)d.w * NP);
+#pragma unroll
+      for (int j = 0; j < 8; j++)
+#pragma unroll
+        for (int v = 0; v < VEC; v++) {
+          ya.v[v] = fma(a[j], x[j].v[v], ya.v[v]);
+          if (NV == 2) yb.v[v] = fma(bb[j], x[j].v[v], yb.v[v]);
+        }
+    }
+  }
+  for (; g < groups; g++) {
+    const int64_t o = base + (int64_t)g * (4 * KS_SELL_C);
+    const int4 c = __ldg(reinterpret_cast<const int4 *>(scol + o));
+    double a0, a1, a2, a3, b0 = 0, b1 = 0, b2 = 0, b3 = 0;
+    ldnc_v4(va + o, a0, a1, a2, a3);
+    if (NV == 2) ldnc_v4(vb + o, b0, b1, b2, b3);
+    const DV<VEC> x0 = DV<VEC>::ld(xs + (int64_t)c.x * NP), x1 = DV<VEC>::ld(xs + (int64_t)c.y * NP);
+    const DV<VEC> x2 = DV<VEC>::ld(xs + (int64_t)c.z * NP), x3 = DV<VEC>::ld(xs + (int64_t)c.w * NP);
+#pragma unroll
+    for (int v = 0; v < VEC; v++) {
+      ya.v[v] = fma(a0, x0.v[v], ya.v[v]);
+      ya.v[v] = fma(a1, x1.v[v], ya.v[v]);
+      ya.v[v] = fma(a2, x2.v[v], ya.v[v]);
+      ya.v[v] = fma(a3, x3.v[v], ya.v[v]);
+      if (NV == 2) {
+        yb.v[v] = fma(b0, x0.v[v], yb.v[v]);
+        yb.v[v] = fma(b1, x1.v[v], yb.v[v]);
+        yb.v[v] = fma(b2, x2.v[v], yb.v[v]);
+        yb.v[v] = fma(b3, x3.v[v], yb.v[v]);
+      }
+    }
+  }
+}
+
+// Block-level column sums: acc[d][v] per lane (column (VEC*lane+v) % NP) -> out[d*NP + c], fixed order
+// (butterfly over the lanes of a column within the warp, then warps 0..W-1 in order).
+template <int NP, int ND>
+__device__ __forceinline__ void block_cols(double (&acc)[ND][SL<NP>::VEC], double *red, double *out) {
+  constexpr int VEC = SL<NP>::VEC, LPR = SL<NP>::LPR;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 0; d < ND; d++)
+#pragma unroll
+    for (int v = 0; v < VEC; v++) {
+      double s = acc[d][v];
+#pragma unroll
+      for (int o = LPR; o < 32; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane < LPR) red[(warp * ND + d) * NP + lane * VEC + v] = s;
+    }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ND * NP; i += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < PCG_WARPS; w++) s += red[w * ND * NP + i];
+    out[i] = s;
+  }
+  __syncthreads();
+}
 
 struct PcgArgs {
-  const int32_t *row_ptr, *col;
-  const double *A, *M, *dinv;
+  const int32_t *sell_ptr, *sell_col;
+  const double *A, *M, *dinv;   // A, M: sliced-ELL values
   const double *lambda;
   double mu, tol;
   const double *U;      // [n][NP] input (possibly padded copy)
@@ -64,12 +196,11 @@ struct PcgArgs {
   int32_t *iters_out;   // [N] or null
   double *relres_out;   // [N] or null
   int32_t *block_iters_out;
-  int64_t n;
-  int N, ntiles, max_iter;
-  int stage_nnz;        // capacity (elements) of one stage's col / value buffers (STAGED path)
   unsigned long long *trace;  // optional phase-end timestamps (%globaltimer, block 0), KS_PCG_TRACE=1
   int *trace_count;
   int trace_cap;
+  int64_t n;
+  int N, ntiles, max_iter;
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
@@ -105,135 +236,25 @@ __device__ __forceinline__ void reduce_partials(const double *part, int stride, 
   __syncthreads();
 }
 
-// ---- bulk (TMA) copies global -> shared, completion on an mbarrier ----
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred P1;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      " @!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-// Shared-memory layout of one warp's S-phase stage: row_ptr slice, col slice, value slice (16-byte aligned).
 template <int NP>
-struct Stage {
-  static constexpr int TR = Lay<NP>::RPW;               // rows of a warp tile
-  static constexpr int RP_CAP = (TR + 8 + 3) & ~3;     // row_ptr entries (aligned superset of TR + 1), x4
-  __host__ __device__ static size_t bytes(int cap) {    // cap: col / value elements (multiple of 4)
-    return sizeof(int32_t) * (RP_CAP + cap) + sizeof(double) * cap;
-  }
-};
-
-// Issue the bulk copies of the warp tile starting at row r0 (rows [r0, min(r0 + TR, n)), empty if r0 >= n)
-// into one stage's buffers (one thread).
-__device__ __forceinline__ void issue_tile(const PcgArgs &a, int TR, int64_t r0, int32_t *srp, int32_t *scol,
-                                           double *sval, uint64_t *bar) {
-  r0 = min(r0, a.n);
-  const int64_t r1 = min(r0 + TR, a.n);
-  const int32_t kb = __ldg(a.row_ptr + r0), ke = __ldg(a.row_ptr + r1);
-  const int64_t ra = r0 & ~3LL, re = (r1 + 1 + 3) & ~3LL;
-  const int32_t ca = kb & ~3, ce = (ke + 3) & ~3;
-  const int32_t va = kb & ~1, ve = (ke + 1) & ~1;
-  const unsigned b_rp = (unsigned)(re - ra) * 4u, b_col = (unsigned)(ce - ca) * 4u, b_val = (unsigned)(ve - va) * 8u;
-  mbar_expect_tx(bar, b_rp + b_col + b_val);
-  bulk_g2s(srp, a.row_ptr + ra, b_rp, bar);
-  if (b_col) bulk_g2s(scol, a.col + ca, b_col, bar);
-  if (b_val) bulk_g2s(sval, a.A + va, b_val, bar);
-}
-
-// y = sum_k val[k] X[col[k]] for one row, col/val from shared memory (already offset to the row's first
-// entry), GATHER unconditional gathers in flight (pad entries gather the own row with weight 0).
-template <int NP>
-__device__ __forceinline__ Vec<Lay<NP>::VEC> row_spmv_smem(const int32_t *scol, const double *sval, int len,
-                                                           int64_t row, const double *X, int sub) {
-  constexpr int VEC = Lay<NP>::VEC;
-  Vec<VEC> acc;
-  acc.zero();
-  for (int k = 0; k < len; k += GATHER) {
-    Vec<VEC> x[GATHER];
-    double w[GATHER];
-#pragma unroll
-    for (int j = 0; j < GATHER; j++) {
-      const bool in = k + j < len;
-      const int64_t c = in ? (int64_t)scol[k + j] : row;
-      w[j] = in ? sval[k + j] : 0.0;
-      x[j] = Vec<VEC>::load(X + c * NP + sub * VEC);
-    }
-#pragma unroll
-    for (int j = 0; j < GATHER; j++)
-#pragma unroll
-      for (int v = 0; v < VEC; v++) acc.v[v] = fma(w[j], x[j].v[v], acc.v[v]);
-  }
-  return acc;
-}
-
-template <int NP, bool STAGED>
 __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs a) {
-  constexpr int VEC = Lay<NP>::VEC, LPR = Lay<NP>::LPR, RPW = Lay<NP>::RPW;
-  constexpr int TILE = PCG_WARPS * RPW;              // rows per tile
+  constexpr int VEC = SL<NP>::VEC, LPR = SL<NP>::LPR, RPW = SL<NP>::RPW, TILE = SL<NP>::TILE;
+  constexpr int CHUNK = SL<NP>::CHUNK;
   constexpr int STRIDE = 4 * NP;                     // partial slots per block
-  static_assert(TILE * NP == CHUNK || NP == 1, "S tile and U/P chunk must cover the same rows");
 
   __shared__ double red[PCG_WARPS * 3 * NP];
   __shared__ double tot[3 * NP];
   __shared__ double s_alpha[NP], s_beta[NP], s_rho[NP], s_bnorm[NP], s_rr[NP];
   __shared__ int s_active[NP], s_conv[NP], s_iters[NP];
   __shared__ int s_any;
-  __shared__ __align__(8) uint64_t s_bar[PCG_WARPS][STAGES];
-  extern __shared__ __align__(16) unsigned char dyn[];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int slot = lane / LPR, sub = lane % LPR;
   const int G = gridDim.x;
   const int64_t n = a.n;
-  const int64_t nel = n * NP;
-  const int nchunks = (int)((nel + CHUNK - 1) / CHUNK);
   unsigned target = 0;
   double *part_init = a.partials;                      // region 0: 3 dots (init) / 2 dots (U)
   double *part_s = a.partials + (int64_t)G * STRIDE;   // region 1: 1 dot (S)
-
-  // ---- S-phase stage buffers and the per-warp tile pipelines ----
-  const int cap = a.stage_nnz;
-  const size_t stage_bytes = Stage<NP>::bytes(cap);
-  unsigned char *wdyn = dyn + (size_t)warp * STAGES * stage_bytes;
-  auto st_rp = [&](int s) { return reinterpret_cast<int32_t *>(wdyn + s * stage_bytes); };
-  auto st_col = [&](int s) { return reinterpret_cast<int32_t *>(wdyn + s * stage_bytes) + Stage<NP>::RP_CAP; };
-  auto st_val = [&](int s) {
-    return reinterpret_cast<double *>(wdyn + s * stage_bytes + sizeof(int32_t) * (Stage<NP>::RP_CAP + cap));
-  };
-  auto wtile_row = [&](int ti) { return (int64_t)(blockIdx.x + ti * G) * TILE + warp * RPW; };
-  const int my_tiles = a.ntiles > blockIdx.x ? (a.ntiles - blockIdx.x + G - 1) / G : 0;
-  unsigned seq = 0;  // tiles consumed so far (all phases); stage = seq % STAGES, parity = (seq / STAGES) & 1
-  if (STAGED) {
-    if (lane == 0) {
-      for (int s = 0; s < STAGES; s++) mbar_init(&s_bar[warp][s], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      // the S phases consume this block's tiles periodically: consumption number q is tile index
-      // q mod my_tiles; stage q mod STAGES always holds consumption q (prefetched STAGES ahead)
-      if (my_tiles > 0)
-        for (int q = 0; q < STAGES; q++)
-          issue_tile(a, RPW, wtile_row(q % my_tiles), st_rp(q), st_col(q), st_val(q), &s_bar[warp][q]);
-    }
-    __syncwarp();
-  }
   unsigned long long *trace = (a.trace && blockIdx.x == 0 && threadIdx.x == 0) ? a.trace : nullptr;
   int ntr = 0;
   auto stamp = [&]() {
@@ -261,12 +282,12 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
     for (int tile = blockIdx.x; tile < a.ntiles; tile += G) {
       int64_t row = (int64_t)tile * TILE + warp * RPW + slot;
       if (row < n) {
-        Vec<VEC> au, mu_;
-        row_spmv2<NP>(a.col, a.A, a.M, __ldg(a.row_ptr + row), __ldg(a.row_ptr + row + 1), a.U, sub, au, mu_);
+        DV<VEC> au, mu_;
+        sell_row<NP, 2>(a.sell_ptr, a.sell_col, a.A, a.M, row, a.U, sub, au, mu_);
         const int64_t off = row * NP + sub * VEC;
-        Vec<VEC> u = Vec<VEC>::load(a.U + off);
+        const DV<VEC> u = DV<VEC>::ld(a.U + off);
         const double dinv = __ldg(a.dinv + row);
-        Vec<VEC> r, z;
+        DV<VEC> r, z;
 #pragma unroll
         for (int v = 0; v < VEC; v++) {
           double b = sh[v] * mu_.v[v];
@@ -276,12 +297,12 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
           acc[1][v] += r.v[v] * z.v[v];
           acc[2][v] += r.v[v] * r.v[v];
         }
-        r.store(a.r + off);
-        z.store(a.p + off);
-        u.store(a.X + off);
+        r.st(a.r + off);
+        z.st(a.p + off);
+        u.st(a.X + off);
       }
     }
-    block_reduce_cols<NP, 3>(acc, red, tot);
+    block_cols<NP, 3>(acc, red, tot);
     for (int i = threadIdx.x; i < 3 * NP; i += blockDim.x) part_init[(int64_t)blockIdx.x * STRIDE + i] = tot[i];
     grid_barrier(a.bar, target);
     stamp();
@@ -304,9 +325,9 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
 
   // ---------------- iterations ----------------
   int it = 0;
-  // streaming layout: element e = chunk * CHUNK + 2 * threadIdx.x; columns c0, c0 + 1 (NP >= 2)
-  const int c0 = (2 * threadIdx.x) % NP;
-  const int c1 = NP == 1 ? 0 : c0 + 1;
+  const int64_t nel = n * NP;
+  const int nchunks = (int)((nel + CHUNK - 1) / CHUNK);
+  const int cb = (VEC * threadIdx.x) % NP;           // first column of this thread's stream vector
   for (;;) {
     if (threadIdx.x == 0) {
       int any = 0;
@@ -325,46 +346,19 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
       double acc[1][VEC];
 #pragma unroll
       for (int v = 0; v < VEC; v++) acc[0][v] = 0.0;
-      for (int i = 0; i < my_tiles; i++) {
-        const int tile = blockIdx.x + i * G;
-        const int64_t r0 = (int64_t)tile * TILE;
-        const int64_t row = r0 + warp * RPW + slot;
-        Vec<VEC> q;
-        if (STAGED) {
-          const int s = seq % STAGES;
-          mbar_wait(&s_bar[warp][s], (seq / STAGES) & 1u);
-          const int32_t *srp = st_rp(s);
-          const int64_t w0 = r0 + warp * RPW;   // first row of the warp tile
-          const int64_t ra = w0 & ~3LL;
-          const int32_t kb = srp[w0 - ra];       // first nnz of the warp tile; slices start at kb & ~3 / kb & ~1
-          if (row < n) {
-            const int32_t k0 = srp[row - ra], k1 = srp[row - ra + 1];
-            q = row_spmv_smem<NP>(st_col(s) + (k0 - (kb & ~3)), st_val(s) + (k0 - (kb & ~1)), k1 - k0, row, a.p,
-                                  sub);
-          }
-        } else if (row < n) {
-          q = row_spmv<NP>(a.col, a.A, __ldg(a.row_ptr + row), __ldg(a.row_ptr + row + 1), a.p, sub);
-        }
+      for (int tile = blockIdx.x; tile < a.ntiles; tile += G) {
+        const int64_t row = (int64_t)tile * TILE + warp * RPW + slot;
         if (row < n) {
+          DV<VEC> q, unused;
+          sell_row<NP, 1>(a.sell_ptr, a.sell_col, a.A, nullptr, row, a.p, sub, q, unused);
           const int64_t off = row * NP + sub * VEC;
-          Vec<VEC> pv = Vec<VEC>::load(a.p + off);
+          const DV<VEC> pv = DV<VEC>::ld(a.p + off);
 #pragma unroll
           for (int v = 0; v < VEC; v++) acc[0][v] += pv.v[v] * q.v[v];
-          q.store(a.q + off);
-        }
-        if (STAGED) {
-          __syncwarp();  // the warp is done with this stage's buffers
-          if (lane == 0) {
-            // refill the stage with consumption seq + STAGES (wrapping into the next iteration's S phase:
-            // the matrix never changes, so the prefetch overlaps the U and P phases)
-            const int s = seq % STAGES;
-            const int nxt = (int)((seq + STAGES) % (unsigned)my_tiles);
-            issue_tile(a, RPW, wtile_row(nxt), st_rp(s), st_col(s), st_val(s), &s_bar[warp][s]);
-          }
-          seq++;
+          q.st(a.q + off);
         }
       }
-      block_reduce_cols<NP, 1>(acc, red, tot);
+      block_cols<NP, 1>(acc, red, tot);
       for (int i = threadIdx.x; i < NP; i += blockDim.x) part_s[(int64_t)blockIdx.x * STRIDE + i] = tot[i];
       grid_barrier(a.bar, target);
       stamp();
@@ -388,40 +382,30 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
 
     // ---- U: r -= alpha q; r.z, r.r (z = r / d) ----
     {
-      const double al0 = s_alpha[c0], al1 = s_alpha[c1];
+      double al[VEC];
+#pragma unroll
+      for (int v = 0; v < VEC; v++) al[v] = s_alpha[cb + v];
       double acc[2][VEC];
 #pragma unroll
       for (int d = 0; d < 2; d++)
 #pragma unroll
         for (int v = 0; v < VEC; v++) acc[d][v] = 0.0;
-      for (int ch = blockIdx.x; ch < nchunks; ch += UNR_U * G) {
-        double2 r[UNR_U], q[UNR_U];
-        double d0[UNR_U], d1[UNR_U];
+      for (int ch = blockIdx.x; ch < nchunks; ch += G) {
+        const int64_t e = (int64_t)ch * CHUNK + VEC * threadIdx.x;
+        if (e < nel) {
+          DV<VEC> r = DV<VEC>::ld(a.r + e);
+          const DV<VEC> q = DV<VEC>::ld(a.q + e);
+          const double di = __ldg(a.dinv + e / NP);
 #pragma unroll
-        for (int u = 0; u < UNR_U; u++) {
-          const int64_t e = (int64_t)(ch + u * G) * CHUNK + 2 * threadIdx.x;
-          if (ch + u * G < nchunks && e < nel) {
-            r[u] = *reinterpret_cast<const double2 *>(a.r + e);
-            q[u] = *reinterpret_cast<const double2 *>(a.q + e);
-            if (NP == 1) { d0[u] = __ldg(a.dinv + e); d1[u] = __ldg(a.dinv + e + 1); }
-            else { d0[u] = d1[u] = __ldg(a.dinv + e / NP); }
+          for (int v = 0; v < VEC; v++) {
+            r.v[v] -= al[v] * q.v[v];
+            acc[0][v] += r.v[v] * (r.v[v] * di);
+            acc[1][v] += r.v[v] * r.v[v];
           }
-        }
-#pragma unroll
-        for (int u = 0; u < UNR_U; u++) {
-          const int64_t e = (int64_t)(ch + u * G) * CHUNK + 2 * threadIdx.x;
-          if (ch + u * G < nchunks && e < nel) {
-            r[u].x -= al0 * q[u].x;
-            r[u].y -= al1 * q[u].y;
-            acc[0][0] += r[u].x * (r[u].x * d0[u]);
-            acc[0][VEC - 1] += r[u].y * (r[u].y * d1[u]);
-            acc[1][0] += r[u].x * r[u].x;
-            acc[1][VEC - 1] += r[u].y * r[u].y;
-            *reinterpret_cast<double2 *>(a.r + e) = r[u];
-          }
+          r.st(a.r + e);
         }
       }
-      block_reduce_cols<NP, 2>(acc, red, tot);
+      block_cols<NP, 2>(acc, red, tot);
       for (int i = threadIdx.x; i < 2 * NP; i += blockDim.x) part_init[(int64_t)blockIdx.x * STRIDE + i] = tot[i];
       grid_barrier(a.bar, target);
       stamp();
@@ -452,33 +436,26 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
 
     // ---- P: x += alpha p; p = r/d + beta p ----
     {
-      const double al0 = s_alpha[c0], al1 = s_alpha[c1];
-      const double be0 = s_beta[c0], be1 = s_beta[c1];
-      for (int ch = blockIdx.x; ch < nchunks; ch += UNR_P * G) {
-        double2 r[UNR_P], p[UNR_P], x[UNR_P];
-        double d0[UNR_P], d1[UNR_P];
+      double al[VEC], be[VEC];
 #pragma unroll
-        for (int u = 0; u < UNR_P; u++) {
-          const int64_t e = (int64_t)(ch + u * G) * CHUNK + 2 * threadIdx.x;
-          if (ch + u * G < nchunks && e < nel) {
-            r[u] = *reinterpret_cast<const double2 *>(a.r + e);
-            p[u] = *reinterpret_cast<const double2 *>(a.p + e);
-            x[u] = *reinterpret_cast<const double2 *>(a.X + e);
-            if (NP == 1) { d0[u] = __ldg(a.dinv + e); d1[u] = __ldg(a.dinv + e + 1); }
-            else { d0[u] = d1[u] = __ldg(a.dinv + e / NP); }
-          }
-        }
+      for (int v = 0; v < VEC; v++) {
+        al[v] = s_alpha[cb + v];
+        be[v] = s_beta[cb + v];
+      }
+      for (int ch = blockIdx.x; ch < nchunks; ch += G) {
+        const int64_t e = (int64_t)ch * CHUNK + VEC * threadIdx.x;
+        if (e < nel) {
+          const DV<VEC> r = DV<VEC>::ld(a.r + e);
+          DV<VEC> p = DV<VEC>::ld(a.p + e);
+          DV<VEC> x = DV<VEC>::ld(a.X + e);
+          const double di = __ldg(a.dinv + e / NP);
 #pragma unroll
-        for (int u = 0; u < UNR_P; u++) {
-          const int64_t e = (int64_t)(ch + u * G) * CHUNK + 2 * threadIdx.x;
-          if (ch + u * G < nchunks && e < nel) {
-            x[u].x += al0 * p[u].x;
-            x[u].y += al1 * p[u].y;
-            p[u].x = r[u].x * d0[u] + be0 * p[u].x;
-            p[u].y = r[u].y * d1[u] + be1 * p[u].y;
-            *reinterpret_cast<double2 *>(a.X + e) = x[u];
-            *reinterpret_cast<double2 *>(a.p + e) = p[u];
+          for (int v = 0; v < VEC; v++) {
+            x.v[v] += al[v] * p.v[v];
+            p.v[v] = r.v[v] * di + be[v] * p.v[v];
           }
+          x.st(a.X + e);
+          p.st(a.p + e);
         }
       }
       if (threadIdx.x < NP && s_conv[threadIdx.x]) s_active[threadIdx.x] = 0;
@@ -498,19 +475,27 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
       if (a.trace_count) *a.trace_count = ntr;
     }
   }
-  if (STAGED) {
-    // drain the prefetches issued for an S phase that did not run, so no bulk copy outlives the block
-    const int pending = my_tiles > 0 ? STAGES : 0;
-    for (int i = 0; i < pending; i++) {
-      const unsigned q = seq + i;
-      mbar_wait(&s_bar[warp][q % STAGES], (q / STAGES) & 1u);
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------------------------
-// standalone multi-RHS SpMM (parity / benchmarking) and helpers
+// standalone multi-RHS SpMM on the sliced-ELL copy (A, M): parity helper and benchmark of phase S
 // ---------------------------------------------------------------------------------------------
+template <int NP>
+__global__ void __launch_bounds__(256) k_spmm_sell(const int32_t *__restrict__ sell_ptr,
+                                                   const int32_t *__restrict__ sell_col,
+                                                   const double *__restrict__ val, const double *__restrict__ X,
+                                                   double *__restrict__ Y, int64_t n) {
+  constexpr int VEC = SL<NP>::VEC, LPR = SL<NP>::LPR;
+  const int64_t gl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t row = gl / LPR;
+  const int sub = (int)(gl % LPR);
+  if (row >= n) return;
+  DV<VEC> y, unused;
+  sell_row<NP, 1>(sell_ptr, sell_col, val, nullptr, row, X, sub, y, unused);
+  y.st(Y + row * NP + sub * VEC);
+}
+
+// CSR multi-RHS SpMM for the operators without a sliced-ELL copy (K, M_V, H)
 template <int NP>
 __global__ void __launch_bounds__(256) k_spmm(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                                               const double *__restrict__ val, const double *__restrict__ X,
@@ -522,6 +507,41 @@ __global__ void __launch_bounds__(256) k_spmm(const int32_t *__restrict__ row_pt
   if (row >= n) return;
   Vec<VEC> y = row_spmv<NP>(col, val, __ldg(row_ptr + row), __ldg(row_ptr + row + 1), X, sub);
   y.store(Y + row * NP + sub * VEC);
+}
+
+template <int NP>
+ks_status launch_pcg(ks_ctx *ctx, PcgArgs &a) {
+  a.ntiles = (int)((a.n + SL<NP>::TILE - 1) / SL<NP>::TILE);
+  int per_sm = 0;
+  KS_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_pcg<NP>, PCG_THREADS, 0));
+  if (per_sm < 1) return ks_fail(ctx, KS_E_CUDA, "k_block_pcg<%d> cannot be resident", NP);
+  int G = per_sm * ctx->sm_count;
+  if (G > a.ntiles) G = a.ntiles;
+  if ((int64_t)G * 4 * NP * 2 > ctx->partial_cap) {
+    if (ctx->partials) { cudaFree(ctx->partials); ctx->partials = nullptr; }
+    ctx->partial_cap = (int64_t)G * 4 * NP * 2;
+    KS_TRY(ks_alloc_t(ctx, &ctx->partials, ctx->partial_cap, "pcg partials"));
+  }
+  a.partials = ctx->partials;
+  KS_CUDA(ctx, cudaMemsetAsync(ctx->barrier, 0, sizeof(unsigned), ctx->stream));
+  void *args[] = {&a};
+  KS_CUDA(ctx, cudaLaunchCooperativeKernel((const void *)k_block_pcg<NP>, dim3(G), dim3(PCG_THREADS), args, 0,
+                                           ctx->stream));
+  ctx->launches++;
+  return KS_OK;
+}
+
+template <int NP>
+void launch_spmm(ks_ctx *ctx, const double *sell_val, const double *csr_val, const double *X, double *Y) {
+  if (sell_val) {
+    const int64_t threads = ctx->n_free * SL<NP>::LPR;
+    k_spmm_sell<NP><<<ks_blocks(threads, 256), 256, 0, ctx->stream>>>(ctx->sell_ptr, ctx->sell_col, sell_val, X, Y,
+                                                                      ctx->n_free);
+  } else {
+    const int64_t threads = ctx->n_free * Lay<NP>::LPR;
+    k_spmm<NP><<<ks_blocks(threads, 256), 256, 0, ctx->stream>>>(ctx->row_ptr, ctx->col, csr_val, X, Y,
+                                                                 ctx->n_free);
+  }
 }
 
 __global__ void k_spmm_generic(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
@@ -603,99 +623,22 @@ int pad_np(int N) {
   return np;
 }
 
-// largest nnz count of a TR-row tile (sizes the S-phase stage buffers)
-__global__ void k_tile_max_nnz(const int32_t *__restrict__ row_ptr, int64_t n, int TR, int ntiles,
-                               int *__restrict__ out) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  int v = 0;
-  if (t < ntiles) {
-    const int64_t r0 = (int64_t)t * TR, r1 = min(r0 + TR, n);
-    v = row_ptr[r1] - row_ptr[r0];
-  }
-  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-  if ((threadIdx.x & 31) == 0 && v > 0) atomicMax(out, v);
-}
-
-static ks_status tile_max_nnz(ks_ctx *ctx, int TR, int ntiles, int *out) {
-  for (auto &e : ctx->tile_nnz_cache)
-    if (e.first == TR) { *out = e.second; return KS_OK; }
-  int *d = nullptr;
-  KS_TRY(ks_alloc_t(ctx, &d, 1, "tile nnz"));
-  k_tile_max_nnz<<<ks_blocks(ntiles, 256), 256, 0, ctx->stream>>>(ctx->row_ptr, ctx->n_free, TR, ntiles, d);
-  KS_LAUNCHED(ctx);
-  int h = 0;
-  KS_CUDA(ctx, cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  cudaFree(d);
-  ctx->bytes -= sizeof(int);
-  ctx->tile_nnz_cache.push_back({TR, h});
-  *out = h;
-  return KS_OK;
-}
-
-template <int NP, bool STAGED>
-ks_status launch_pcg_t(ks_ctx *ctx, PcgArgs &a, size_t dyn) {
-  auto kern = k_block_pcg<NP, STAGED>;
-  KS_CUDA(ctx, cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-  int per_sm = 0;
-  KS_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PCG_THREADS, dyn));
-  if (per_sm < 1) return ks_fail(ctx, KS_E_CUDA, "k_block_pcg<%d,%d> cannot be resident", NP, (int)STAGED);
-  int G = per_sm * ctx->sm_count;
-  if (G > a.ntiles) G = a.ntiles;
-  if ((int64_t)G * 4 * NP * 2 > ctx->partial_cap) {
-    if (ctx->partials) { cudaFree(ctx->partials); ctx->partials = nullptr; }
-    ctx->partial_cap = (int64_t)G * 4 * NP * 2;
-    KS_TRY(ks_alloc_t(ctx, &ctx->partials, ctx->partial_cap, "pcg partials"));
-  }
-  a.partials = ctx->partials;
-  KS_CUDA(ctx, cudaMemsetAsync(ctx->barrier, 0, sizeof(unsigned), ctx->stream));
-  void *args[] = {&a};
-  KS_CUDA(ctx, cudaLaunchCooperativeKernel((const void *)kern, dim3(G), dim3(PCG_THREADS), args, dyn, ctx->stream));
-  ctx->launches++;
-  return KS_OK;
-}
-
-// STAGED (bulk-copied matrix tiles) when STAGES stage buffers fit next to a second block on the SM;
-// KS_PCG_STAGED=0 in the environment forces the direct path (A/B measurements).
-constexpr size_t STAGE_SMEM_MAX = 96 * 1024;
-
-template <int NP>
-ks_status launch_pcg(ks_ctx *ctx, PcgArgs &a) {
-  constexpr int TILE = PCG_WARPS * Lay<NP>::RPW;
-  a.ntiles = (int)((a.n + TILE - 1) / TILE);
-  int mx = 0;
-  KS_TRY(tile_max_nnz(ctx, Lay<NP>::RPW, (int)((a.n + Lay<NP>::RPW - 1) / Lay<NP>::RPW), &mx));
-  const int cap = ((mx + 8) + 3) & ~3;   // + alignment slack of both slices
-  a.stage_nnz = cap;
-  const size_t dyn = (size_t)PCG_WARPS * STAGES * Stage<NP>::bytes(cap);
-  const char *env = getenv("KS_PCG_STAGED");
-  const bool want = !(env && env[0] == '0');
-  if (want && dyn <= STAGE_SMEM_MAX) return launch_pcg_t<NP, true>(ctx, a, dyn);
-  a.stage_nnz = 0;
-  return launch_pcg_t<NP, false>(ctx, a, 0);
-}
-
-template <int NP>
-void launch_spmm(ks_ctx *ctx, const double *val, const double *X, double *Y) {
-  const int64_t threads = ctx->n_free * Lay<NP>::LPR;
-  k_spmm<NP><<<ks_blocks(threads, 256), 256, 0, ctx->stream>>>(ctx->row_ptr, ctx->col, val, X, Y, ctx->n_free);
-}
-
 }  // namespace
 
-static bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+static bool aligned32(const void *p) { return ((uintptr_t)p & 31u) == 0; }
 
-ks_status ks_spmm_impl(ks_ctx *ctx, const double *val, int N, const double *X, double *Y) {
+ks_status ks_spmm_impl(ks_ctx *ctx, ks_op op, const double *val, int N, const double *X, double *Y) {
   const int np = pad_np(N);
-  if (np == N && aligned16(X) && aligned16(Y)) {
+  const double *sv = op == KS_OP_A ? ctx->sell_A : op == KS_OP_M ? ctx->sell_M : nullptr;
+  if (np == N && aligned32(X) && aligned32(Y)) {
     switch (N) {
-      case 1: launch_spmm<1>(ctx, val, X, Y); break;
-      case 2: launch_spmm<2>(ctx, val, X, Y); break;
-      case 4: launch_spmm<4>(ctx, val, X, Y); break;
-      case 8: launch_spmm<8>(ctx, val, X, Y); break;
-      case 16: launch_spmm<16>(ctx, val, X, Y); break;
-      case 32: launch_spmm<32>(ctx, val, X, Y); break;
-      case 64: launch_spmm<64>(ctx, val, X, Y); break;
+      case 1: launch_spmm<1>(ctx, sv, val, X, Y); break;
+      case 2: launch_spmm<2>(ctx, sv, val, X, Y); break;
+      case 4: launch_spmm<4>(ctx, sv, val, X, Y); break;
+      case 8: launch_spmm<8>(ctx, sv, val, X, Y); break;
+      case 16: launch_spmm<16>(ctx, sv, val, X, Y); break;
+      case 32: launch_spmm<32>(ctx, sv, val, X, Y); break;
+      case 64: launch_spmm<64>(ctx, sv, val, X, Y); break;
     }
   } else {
     k_spmm_generic<<<ks_blocks(ctx->n_free * N, 256), 256, 0, ctx->stream>>>(ctx->row_ptr, ctx->col, val, X, Y,
@@ -709,7 +652,7 @@ static ks_status ensure_solver_ws(ks_ctx *ctx, int np) {
   if (ctx->ws_np >= np && ctx->ws_rows == ctx->n_free) return KS_OK;
   for (double **b : {&ctx->r, &ctx->p, &ctx->q, &ctx->xpad, &ctx->upad})
     if (*b) { cudaFree(*b); *b = nullptr; }
-  const int64_t cnt = ctx->n_free * (int64_t)np + 2;  // +2: NP=1 streaming reads pairs
+  const int64_t cnt = ctx->n_free * (int64_t)np;
   KS_TRY(ks_alloc_t(ctx, &ctx->r, cnt, "pcg r"));
   KS_TRY(ks_alloc_t(ctx, &ctx->p, cnt, "pcg p"));
   KS_TRY(ks_alloc_t(ctx, &ctx->q, cnt, "pcg q"));
@@ -725,29 +668,20 @@ ks_status ks_solve_impl(ks_ctx *ctx, int N, const double *lambda, const double *
   const int np = pad_np(N);
   KS_TRY(ensure_solver_ws(ctx, np));
   const int64_t n = ctx->n_free;
-  // NP = 1 streams element pairs: pad to an even element count via the internal buffers
-  const bool direct = (np == N) && aligned16(U) && aligned16(Ut) && !(np == 1 && (n & 1));
+  const bool direct = (np == N) && aligned32(U) && aligned32(Ut);
   const double *u = U;
   double *x = Ut;
   if (!direct) {
-    KS_CUDA(ctx, cudaMemsetAsync(ctx->upad, 0, sizeof(double) * (n * np + 2), ctx->stream));
-    KS_CUDA(ctx, cudaMemsetAsync(ctx->xpad, 0, sizeof(double) * (n * np + 2), ctx->stream));
     k_pad<<<ks_blocks(n * np, 256), 256, 0, ctx->stream>>>(U, N, ctx->upad, np, n);
     KS_LAUNCHED(ctx);
     u = ctx->upad;
     x = ctx->xpad;
   }
-  if (np == 1) {
-    // keep the odd tail element finite for the pairwise streaming phases
-    KS_CUDA(ctx, cudaMemsetAsync(ctx->r + n, 0, sizeof(double) * 2, ctx->stream));
-    KS_CUDA(ctx, cudaMemsetAsync(ctx->q + n, 0, sizeof(double) * 2, ctx->stream));
-    KS_CUDA(ctx, cudaMemsetAsync(ctx->p + n, 0, sizeof(double) * 2, ctx->stream));
-  }
   PcgArgs a;
-  a.row_ptr = ctx->row_ptr;
-  a.col = ctx->col;
-  a.A = ctx->A;
-  a.M = ctx->M;
+  a.sell_ptr = ctx->sell_ptr;
+  a.sell_col = ctx->sell_col;
+  a.A = ctx->sell_A;
+  a.M = ctx->sell_M;
   a.dinv = ctx->dinv;
   a.lambda = lambda;
   a.mu = ctx->mu;

@@ -336,6 +336,7 @@ ks_status ks_setup_mesh(ks_ctx *ctx, const double *h_xyz, const int32_t *h_tets,
   KS_TRY(ks_alloc_t(ctx, &ctx->dinv, nf + 2, "dinv"));  // +2: zero pad for the NP = 1 pairwise streams
   KS_TRY(ks_alloc_t(ctx, &ctx->w_tet, nt, "w_tet"));
   KS_TRY(ks_alloc_t(ctx, &ctx->v_free, nf, "v_free"));
+  KS_TRY(ks_sell_build(ctx));
   KS_CUDA(ctx, cudaStreamSynchronize(s));  // temporaries are freed by ~TempBuf after this point
   return KS_OK;
 }
