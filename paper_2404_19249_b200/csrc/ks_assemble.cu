@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
     const int32_t *__restrict__ inv_idx, const double *__restrict__ w, const double *__restrict__ v_free,
     const double *__restrict__ K, const double *__restrict__ M, double mu, int64_t n_free, double *__restrict__ MV,
     double *__restrict__ H, double *__restrict__ A, double *__restrict__ diag, double *__restrict__ dinv,
-    const int32_t *__restrict__ sell_ptr, double *__restrict__ sell_A) {
+    const int32_t *__restrict__ sell_ptr, double *__restrict__ sell_A, double *__restrict__ sell_H) {
   int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 4;
   int j = threadIdx.x & 15;
   if (row >= n_free) return;
@@ -62,7 +62,9 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
     H[e] = h;
     A[e] = a;
     const int k = e - kr;   // slot of the entry in the sliced-ELL copy (ks_sell.cu)
-    sell_A[sbase + (k >> 2) * (4 * KS_SELL_C) + (k & 3)] = a;
+    const int64_t sp = sbase + (k >> 2) * (4 * KS_SELL_C) + (k & 3);
+    sell_A[sp] = a;
+    sell_H[sp] = h;
     if (c == row) {
       diag[row] = a;
       dinv[row] = 1.0 / a;
@@ -80,7 +82,7 @@ ks_status ks_assemble_impl(ks_ctx *ctx, const double *d_veff, double mu) {
   KS_LAUNCHED(ctx);
   k_assemble_rows<<<ks_blocks(16 * ctx->n_free, 256), 256, 0, s>>>(
       ctx->row_ptr, ctx->col, ctx->inv_ptr, ctx->inv_idx, ctx->w_tet, ctx->v_free, ctx->K, ctx->M, mu,
-      ctx->n_free, ctx->MV, ctx->H, ctx->A, ctx->diag, ctx->dinv, ctx->sell_ptr, ctx->sell_A);
+      ctx->n_free, ctx->MV, ctx->H, ctx->A, ctx->diag, ctx->dinv, ctx->sell_ptr, ctx->sell_A, ctx->sell_H);
   KS_LAUNCHED(ctx);
   ctx->mu = mu;
   ctx->assembled = true;

@@ -45,7 +45,7 @@ struct ks_ctx {
   int64_t n_slices = 0, sell_total = 0;
   int32_t *sell_ptr = nullptr;      // [n_slices+1] first entry of each 8-row slice
   int32_t *sell_col = nullptr;      // [sell_total]
-  double *sell_A = nullptr, *sell_M = nullptr;  // [sell_total]
+  double *sell_A = nullptr, *sell_M = nullptr, *sell_H = nullptr;  // [sell_total]
   double *v_free = nullptr;         // [n_free] V at free nodes (assembly scratch)
   double mu = 0.0;
   bool assembled = false;
@@ -69,6 +69,7 @@ struct ks_ctx {
   int64_t n_H = 0, p_nnz = 0;
   int32_t *P_ptr = nullptr, *P_col = nullptr;   // own copy, columns ascending within a row
   double *P_val = nullptr;
+  double *Pv4 = nullptr;         // [4 n_free] P rows as a zero-padded 4-wide table
   int64_t n_items = 0, d_total = 0;
   int d_max = 0;
   int32_t *perm = nullptr;       // [n_free] fine rows grouped by parent set ("items" of <= ITEM_ROWS rows)

@@ -3,26 +3,27 @@
 //   A_H = P^T H P (st5), b_H = P^T H U~ (st6), beta = U~^T H U~ (st7);
 //   B_H = P^T M P (cached per mesh pair), c_H = P^T M U~, gamma = U~^T M U~ (717-731).
 //
-// Design (DESIGN.md §4 "projection"). Fine rows are grouped by their coarse parent set S (the <= 4
+// Design (DESIGN.md §4.4 "projection"). Fine rows are grouped by their coarse parent set S (the <= 4
 // coarse nodes with P_ic != 0) and cut into "items" of <= ITEM_ROWS rows. Every contribution of a row
-// lands in coarse rows c in S, so one warp can accumulate an item's contributions privately:
-//   K8  k_proj_items  one pass over the item's rows: Y_H = H U~ and Y_M = M U~ (shared column stream),
-//                     the item partials sum_i P_ic Y_H[i] / Y_M[i] (for b_H, c_H) and
-//                     sum_i P_ic (H P)_i,d (for A_H) with d in the item's coarse window D (slot map
-//                     precomputed at setup). Per-row-slot private accumulators + fixed-order combine.
-//   K8b k_gram        beta, gamma = U~^T Y (register-tiled tall-skinny products, per-block partials)
-//   K9  k_proj_final  one block per coarse node c: fixed-order sums over the items containing c.
+// lands in coarse rows c in S, so one warp can accumulate an item privately:
+//   K8a k_proj_y      Y_H = H U~ and Y_M = M U~ on the sliced-ELL copies (one pass, shared col stream)
+//   K8b k_proj_a      item partials sum_i P_ic (Op P)_{i,d}, d in the item's coarse window D (slot map
+//                     and a 4-wide table of P rows precomputed in ks_set_coarse), Op = H (A_H) or M (B_H)
+//   K8c k_proj_bg     item partials sum_i P_ic Y_H[i] / Y_M[i] (b_H, c_H) and, per warp, the Gram
+//                     partials beta, gamma = U~^T Y (symmetric: upper 4x4 tiles), rows in item order
+//   K9  k_proj_final  one block per coarse node c: fixed-order sums over the items containing c;
+//       k_gram_fin    fixed-order sums of the Gram partials.
 // Everything is deterministic (fixed partitions and orders, no float atomics).
 #include <cub/cub.cuh>
 
 #include "ks_internal.cuh"
 #include "ks_rowops.cuh"
+#include "ks_sell.cuh"
 
 namespace {
 
 constexpr int ITEM_ROWS = 128;   // rows per item (chunk of a parent-set group)
 constexpr int DMAX = 255;        // max coarse window of an item (u8 slots; 255 = "no slot")
-constexpr int PROJ_WARPS = 8;
 
 // ---------------------------------------------------------------------------------------------
 // setup kernels
@@ -210,124 +211,253 @@ __global__ void k_lower_bound_ptr(const int32_t *__restrict__ keys, int64_t nk, 
 }
 
 // ---------------------------------------------------------------------------------------------
-// projection kernels
+// projection kernels (v2)
 // ---------------------------------------------------------------------------------------------
-struct ProjArgs {
-  const int32_t *row_ptr, *col;
-  const double *Aop;        // operator of the triple product (H, or M for the cached B_H)
-  const double *Mop;        // M (second operator of the Y pass)
-  const int32_t *Pptr;
-  const double *Pval;
-  const int32_t *perm, *item_ptr, *item_S, *D_ptr;
-  const uint8_t *slotmap;
-  const double *U;          // [n][NP]
-  double *YH, *YM;          // [n][NP]
-  double *AH_part, *bH_part, *cH_part;
-  int64_t n_items;
-  int d_max;
-};
+// K8a  k_proj_y   Y_H = H U~, Y_M = M U~ on the sliced-ELL copies (rows in natural order, coalesced)
+// K8b  k_proj_a   per item: sum_i P_ic (Op P)_{i,d} for c in S, d in the item window D  (A_H / B_H)
+// K8c  k_proj_bg  per item: b/c partials sum_i P_ic Y[i]; per warp: Gram partials U~^T Y (upper tiles)
+// K9   k_proj_final / k_gram_fin: fixed-order sums of the partials into F_A, F_B.
+constexpr int PA_WARPS = 4;      // warps per block of k_proj_a
+constexpr int PA_SLOTS = 8;      // rows of an item in flight per warp (4 lanes each: one per parent t)
+constexpr int PBG_WARPS = 8;     // warps per block of k_proj_bg
 
-template <int NP, bool WITH_Y>
-__global__ void __launch_bounds__(PROJ_WARPS * 32) k_proj_items(ProjArgs a) {
-  constexpr int VEC = Lay<NP>::VEC;
-  constexpr int LPRY = Lay<NP>::LPR;             // lanes carrying Y columns
-  constexpr int LPR = LPRY < 8 ? 8 : LPRY;       // lanes per row in this kernel
-  constexpr int RPW = 32 / LPR;
+template <int NP>
+__global__ void __launch_bounds__(256) k_proj_y(const int32_t *__restrict__ sell_ptr, const int32_t *__restrict__ sell_col,
+                                                const double *__restrict__ H, const double *__restrict__ M,
+                                                const double *__restrict__ U, double *__restrict__ YH,
+                                                double *__restrict__ YM, int64_t n) {
+  constexpr int VEC = SL<NP>::VEC, LPR = SL<NP>::LPR;
+  const int64_t gl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t row = gl / LPR;
+  const int sub = (int)(gl % LPR);
+  if (row >= n) return;
+  DV<VEC> yh, ym;
+  sell_row<NP, 2>(sell_ptr, sell_col, H, M, row, U, sub, yh, ym);
+  yh.st(YH + row * NP + sub * VEC);
+  ym.st(YM + row * NP + sub * VEC);
+}
+
+// Item partials of P^T Op P. Warp per item; lane = 4 * slot + t: row slot `slot` of PA_SLOTS, parent index t
+// of the neighbour's P row. Per nonzero k (row i, column j) the lane adds Op_k P_{j,t} P_{i,c} (c = 0..3) to
+// the row slot's private window copy W[slot][c][s], s = slotmap[4k + t] (distinct t of one k give distinct
+// coarse columns, so the 4 lanes of a slot never collide). Copies are combined in slot order.
+__global__ void __launch_bounds__(PA_WARPS * 32) k_proj_a(const int32_t *__restrict__ row_ptr,
+                                                          const int32_t *__restrict__ col,
+                                                          const double *__restrict__ val,
+                                                          const uint8_t *__restrict__ slotmap,
+                                                          const double *__restrict__ Pv4,
+                                                          const int32_t *__restrict__ perm,
+                                                          const int32_t *__restrict__ item_ptr,
+                                                          const int32_t *__restrict__ D_ptr, int64_t n_items, int wcap,
+                                                          double *__restrict__ AH_part) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int slot = lane / LPR, sub = lane % LPR;
-  const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (slot * LPR));
-  double *accA = smem + (int64_t)warp * RPW * 4 * a.d_max;
-  const int64_t gw = (int64_t)blockIdx.x * PROJ_WARPS + warp, nw = (int64_t)gridDim.x * PROJ_WARPS;
-
-  for (int64_t it = gw; it < a.n_items; it += nw) {
-    const int32_t p0 = __ldg(a.item_ptr + it), p1 = __ldg(a.item_ptr + it + 1);
-    int nS = 0;
+  const int slot = lane >> 2, t = lane & 3;
+  double *W = smem + (int64_t)warp * PA_SLOTS * 4 * wcap;   // [slot][c][wcap]
+  double *Wm = W + slot * 4 * wcap;
+  const int64_t gw = (int64_t)blockIdx.x * PA_WARPS + warp, nw = (int64_t)gridDim.x * PA_WARPS;
+  for (int x = lane; x < PA_SLOTS * 4 * wcap; x += 32) W[x] = 0.0;
+  __syncwarp();
+  for (int64_t it = gw; it < n_items; it += nw) {
+    const int32_t p0 = __ldg(item_ptr + it), p1 = __ldg(item_ptr + it + 1);
+    const int32_t d0 = __ldg(D_ptr + it), dn = __ldg(D_ptr + it + 1) - d0;
+    for (int32_t pos = p0 + slot; pos < p1; pos += PA_SLOTS) {
+      const int32_t i = __ldg(perm + pos);
+      double pi[4];
+      ldnc_v4(Pv4 + 4 * (int64_t)i, pi[0], pi[1], pi[2], pi[3]);
+      const int32_t k0 = __ldg(row_ptr + i), k1 = __ldg(row_ptr + i + 1);
+      int32_t k = k0;
+      for (; k + 4 <= k1; k += 4) {
+        int32_t j[4], s[4];
+        double h[4], pj[4];
 #pragma unroll
-    for (int q = 0; q < 4; q++) nS += __ldg(a.item_S + 4 * it + q) >= 0;
-    const int32_t dn = __ldg(a.D_ptr + it + 1) - __ldg(a.D_ptr + it);
-    for (int x = lane; x < RPW * 4 * dn; x += 32) accA[x] = 0.0;
-    __syncwarp();
-    double accB[4][VEC], accC[4][VEC];
-#pragma unroll
-    for (int c = 0; c < 4; c++)
-#pragma unroll
-      for (int v = 0; v < VEC; v++) accB[c][v] = accC[c][v] = 0.0;
-    double *myA = accA + slot * 4 * dn;
-
-    for (int32_t pos = p0 + slot; pos < p1; pos += RPW) {
-      const int32_t i = __ldg(a.perm + pos);
-      const int32_t pi = __ldg(a.Pptr + i);
-      double Pw[4];
-#pragma unroll
-      for (int q = 0; q < 4; q++) Pw[q] = q < nS ? __ldg(a.Pval + pi + q) : 0.0;
-      const int32_t k0 = __ldg(a.row_ptr + i), k1 = __ldg(a.row_ptr + i + 1);
-      Vec<VEC> yh, ym;
-      yh.zero();
-      ym.zero();
-      for (int32_t k = k0; k < k1; k++) {
-        const int32_t j = __ldg(a.col + k);
-        const double h = __ldg(a.Aop + k);
-        if (WITH_Y && sub < LPRY) {
-          const double m = __ldg(a.Mop + k);
-          Vec<VEC> x = Vec<VEC>::ldg(a.U + (int64_t)j * NP + sub * VEC);
-#pragma unroll
-          for (int v = 0; v < VEC; v++) {
-            yh.v[v] = fma(h, x.v[v], yh.v[v]);
-            ym.v[v] = fma(m, x.v[v], ym.v[v]);
-          }
+        for (int u = 0; u < 4; u++) {
+          j[u] = __ldg(col + k + u);
+          h[u] = __ldg(val + k + u);
+          s[u] = __ldg(slotmap + 4 * (int64_t)(k + u) + t);
         }
-        const int32_t pj = __ldg(a.Pptr + j), cj = __ldg(a.Pptr + j + 1) - pj;
-        const uchar4 sl = __ldg(reinterpret_cast<const uchar4 *>(a.slotmap) + k);
-        const unsigned char s4[4] = {sl.x, sl.y, sl.z, sl.w};
-        for (int q = sub; q < 16; q += LPR) {
-          const int cl = q >> 2, t = q & 3;
-          if (cl < nS && t < cj) {
-            const int s = s4[t];
-            myA[cl * dn + s] = fma(Pw[cl] * h, __ldg(a.Pval + pj + t), myA[cl * dn + s]);
+#pragma unroll
+        for (int u = 0; u < 4; u++) pj[u] = __ldg(Pv4 + 4 * (int64_t)j[u] + t);
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+          if (s[u] != 255) {
+            const double w = h[u] * pj[u];
+#pragma unroll
+            for (int c = 0; c < 4; c++) Wm[c * wcap + s[u]] = fma(pi[c], w, Wm[c * wcap + s[u]]);
           }
-        }
-        __syncwarp(gmask);
       }
-      if (WITH_Y && sub < LPRY) {
-        yh.store(a.YH + (int64_t)i * NP + sub * VEC);
-        ym.store(a.YM + (int64_t)i * NP + sub * VEC);
+      for (; k < k1; k++) {
+        const int32_t j0 = __ldg(col + k), s0 = __ldg(slotmap + 4 * (int64_t)k + t);
+        const double w = __ldg(val + k) * __ldg(Pv4 + 4 * (int64_t)j0 + t);
+        if (s0 != 255)
 #pragma unroll
-        for (int c = 0; c < 4; c++)
-#pragma unroll
-          for (int v = 0; v < VEC; v++) {
-            accB[c][v] = fma(Pw[c], yh.v[v], accB[c][v]);
-            accC[c][v] = fma(Pw[c], ym.v[v], accC[c][v]);
-          }
+          for (int c = 0; c < 4; c++) Wm[c * wcap + s0] = fma(pi[c], w, Wm[c * wcap + s0]);
       }
     }
     __syncwarp();
-    if (WITH_Y) {
-      // combine the row slots (lanes with equal sub) in butterfly order
-#pragma unroll
-      for (int c = 0; c < 4; c++)
-#pragma unroll
-        for (int v = 0; v < VEC; v++) {
-          double b = accB[c][v], cc = accC[c][v];
-#pragma unroll
-          for (int o = LPR; o < 32; o <<= 1) {
-            b += __shfl_xor_sync(0xffffffffu, b, o);
-            cc += __shfl_xor_sync(0xffffffffu, cc, o);
-          }
-          if (slot == 0 && sub < LPRY) {
-            a.bH_part[(4 * it + c) * NP + sub * VEC + v] = b;
-            a.cH_part[(4 * it + c) * NP + sub * VEC + v] = cc;
-          }
-        }
-    }
-    // combine the row-slot copies of the A partial in slot order
-    double *out = a.AH_part + 4 * (int64_t)__ldg(a.D_ptr + it);
+    double *out = AH_part + 4 * (int64_t)d0;
     for (int x = lane; x < 4 * dn; x += 32) {
-      double s = 0.0;
-      for (int r = 0; r < RPW; r++) s += accA[r * 4 * dn + x];
-      out[x] = s;
+      const int c = x / dn, d = x % dn;
+      double sum = 0.0;
+      for (int r = 0; r < PA_SLOTS; r++) {
+        sum += W[(r * 4 + c) * wcap + d];
+        W[(r * 4 + c) * wcap + d] = 0.0;
+      }
+      out[x] = sum;
     }
     __syncwarp();
+  }
+}
+
+// Item pass over the rows of each item (perm order): b/c partials per item and Gram partials per warp.
+// Rows are staged PBG_ROWS at a time in the warp's shared memory: U~, Y_H, Y_M rows and the P row.
+// Gram: 4x4 register tiles (op, ta, tb) with ta <= tb (the blocks are symmetric), lane l owns tiles
+// l, l + 32, ...; b/c: lane l owns (op, c) = l / 4 and the orbitals b in quarter l % 4.
+template <int NP, bool GRAM>
+__global__ void __launch_bounds__(PBG_WARPS * 32) k_proj_bg(const double *__restrict__ U, const double *__restrict__ YH,
+                                                            const double *__restrict__ YM,
+                                                            const double *__restrict__ Pv4,
+                                                            const int32_t *__restrict__ perm,
+                                                            const int32_t *__restrict__ item_ptr, int64_t n_items,
+                                                            double *__restrict__ bH_part, double *__restrict__ cH_part,
+                                                            double *__restrict__ gram_part) {
+  constexpr int T4 = NP >= 4 ? NP / 4 : 1;                 // 4-wide tiles per dimension
+  constexpr int NT2 = T4 * (T4 + 1) / 2;                   // upper tiles per operator
+  constexpr int MAXT = (2 * NT2 + 31) / 32;                // tiles per lane
+  constexpr int BQ = NP >= 4 ? NP / 4 : NP;                // b/c orbitals per lane (NP >= 4: a quarter)
+  constexpr int SEGS = (3 * NP + 4 + 3) / 4;               // 4-double segments staged per row
+  constexpr int RS = 4 * SEGS;                             // staged doubles per row (U~, Y_H, Y_M, P, pad)
+  constexpr int PBG_ROWS = NP <= 16 ? 8 : NP == 32 ? 4 : 2;  // rows staged per warp step
+  __shared__ __align__(16) double st[PBG_WARPS][PBG_ROWS * RS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double *S = st[warp];
+  const int64_t gw = (int64_t)blockIdx.x * PBG_WARPS + warp, nw = (int64_t)gridDim.x * PBG_WARPS;
+
+  // tile coordinates of this lane
+  int t_op[MAXT], t_a[MAXT], t_b[MAXT];
+#pragma unroll
+  for (int q = 0; q < MAXT; q++) {
+    int id = lane + 32 * q, op = 0, ta = 0, tb = 0;
+    if (id < 2 * NT2) {
+      op = id / NT2;
+      int r = id % NT2;
+      while (r >= T4 - ta) { r -= T4 - ta; ta++; }
+      tb = ta + r;
+    } else {
+      op = -1;
+    }
+    t_op[q] = op; t_a[q] = ta; t_b[q] = tb;
+  }
+  double g[MAXT][16];
+#pragma unroll
+  for (int q = 0; q < MAXT; q++)
+#pragma unroll
+    for (int e = 0; e < 16; e++) g[q][e] = 0.0;
+  const int bc_op = (lane >> 2) >> 2, bc_c = (lane >> 2) & 3, bc_b0 = (NP >= 4 ? (lane & 3) * BQ : 0);
+  const bool bc_on = NP >= 4 || (lane & 3) == 0;
+
+  for (int64_t it = gw; it < n_items; it += nw) {
+    const int32_t p0 = __ldg(item_ptr + it), p1 = __ldg(item_ptr + it + 1);
+    double bc[BQ];
+#pragma unroll
+    for (int v = 0; v < BQ; v++) bc[v] = 0.0;
+    for (int32_t pb = p0; pb < p1; pb += PBG_ROWS) {
+      const int nr = min(PBG_ROWS, p1 - pb);
+      __syncwarp();
+      // stage: per row 3 vectors of NP doubles + the P row (4 doubles), in 4-double segments
+      for (int x = lane; x < PBG_ROWS * SEGS; x += 32) {
+        const int r = x / SEGS, sg = x % SEGS;
+        double v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+        if (r < nr) {
+          const int64_t i = __ldg(perm + pb + r);
+          const int vec = (4 * sg) / NP, off = (4 * sg) % NP;
+          const double *src = vec == 0 ? U : vec == 1 ? YH : vec == 2 ? YM : Pv4;
+          const int64_t ld = vec < 3 ? NP : 4;
+          if (NP >= 4) {
+            ldnc_v4(src + i * ld + (vec < 3 ? off : 0), v0, v1, v2, v3);
+          } else {  // NP < 4: a segment spans several vectors of one row
+            double tmp[4];
+            for (int e = 0; e < 4; e++) {
+              const int fe = 4 * sg + e;
+              if (fe < 3 * NP) {
+                const int fv = fe / NP, fo = fe % NP;
+                tmp[e] = (fv == 0 ? U : fv == 1 ? YH : YM)[i * NP + fo];
+              } else {
+                tmp[e] = fe - 3 * NP < 4 ? Pv4[i * 4 + (fe - 3 * NP)] : 0.0;
+              }
+            }
+            v0 = tmp[0]; v1 = tmp[1]; v2 = tmp[2]; v3 = tmp[3];
+          }
+        }
+        double *d = S + r * RS + 4 * sg;
+        d[0] = v0; d[1] = v1; d[2] = v2; d[3] = v3;
+      }
+      __syncwarp();
+      for (int r = 0; r < nr; r++) {
+        const double *R = S + r * RS;
+        if (GRAM) {
+#pragma unroll
+          for (int q = 0; q < MAXT; q++) {
+            if (t_op[q] < 0) continue;
+            const double *ua = R + 4 * t_a[q];
+            const double *yb = R + NP * (1 + t_op[q]) + 4 * t_b[q];
+            double u4[4], y4[4];
+            if (NP >= 4) {
+              const double2 u01 = reinterpret_cast<const double2 *>(ua)[0], u23 = reinterpret_cast<const double2 *>(ua)[1];
+              const double2 y01 = reinterpret_cast<const double2 *>(yb)[0], y23 = reinterpret_cast<const double2 *>(yb)[1];
+              u4[0] = u01.x; u4[1] = u01.y; u4[2] = u23.x; u4[3] = u23.y;
+              y4[0] = y01.x; y4[1] = y01.y; y4[2] = y23.x; y4[3] = y23.y;
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; e++) { u4[e] = ua[e]; y4[e] = yb[e]; }
+            }
+#pragma unroll
+            for (int x = 0; x < 4; x++)
+#pragma unroll
+              for (int y = 0; y < 4; y++) g[q][x * 4 + y] = fma(u4[x], y4[y], g[q][x * 4 + y]);
+          }
+        }
+        if (bc_on) {
+          const double pc = R[3 * NP + bc_c];
+          const double *yv = R + NP * (1 + bc_op) + bc_b0;
+#pragma unroll
+          for (int v = 0; v < BQ; v++) bc[v] = fma(pc, yv[v], bc[v]);
+        }
+      }
+    }
+    if (bc_on) {
+      double *dst = (bc_op ? cH_part : bH_part) + (4 * it + bc_c) * NP + bc_b0;
+#pragma unroll
+      for (int v = 0; v < BQ; v++) dst[v] = bc[v];
+    }
+  }
+  if (GRAM) {
+    // per-warp partial [2][NP][NP], both triangles (the lower one mirrored from the upper tiles)
+    double *out = gram_part + gw * 2 * NP * NP;
+#pragma unroll
+    for (int q = 0; q < MAXT; q++) {
+      if (t_op[q] < 0) continue;
+      double *o = out + t_op[q] * NP * NP;
+      for (int x = 0; x < 4; x++)
+        for (int y = 0; y < 4; y++) {
+          const int a = 4 * t_a[q] + x, b = 4 * t_b[q] + y;
+          if (a < NP && b < NP) {
+            o[a * NP + b] = g[q][x * 4 + y];
+            if (t_a[q] != t_b[q]) o[b * NP + a] = g[q][x * 4 + y];
+          }
+        }
+    }
+  }
+}
+
+// beta / gamma blocks: fixed-order sum of the per-warp Gram partials
+__global__ void k_gram_fin(const double *__restrict__ part, int nparts, int N, int NP, int64_t n_H, int64_t D,
+                           double *__restrict__ FA, double *__restrict__ FB) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < 2 * N * N; x += gridDim.x * blockDim.x) {
+    const int m = x / (N * N), a = (x % (N * N)) / N, b = x % N;
+    double s = 0.0;
+    for (int w = 0; w < nparts; w++) s += part[(int64_t)w * 2 * NP * NP + m * NP * NP + a * NP + b];
+    (m ? FB : FA)[(n_H + a) * D + n_H + b] = s;
   }
 }
 
@@ -476,21 +606,79 @@ int pow2_at_least(int N) {
   return np;
 }
 
-int proj_grid(ks_ctx *ctx, int64_t n_items) {
-  int64_t g = (n_items + PROJ_WARPS - 1) / PROJ_WARPS;
+int proj_grid(ks_ctx *ctx, int64_t n_items, int warps_per_block) {
+  int64_t g = (n_items + warps_per_block - 1) / warps_per_block;
   int64_t cap = (int64_t)ctx->sm_count * 8;
   return (int)(g < cap ? (g < 1 ? 1 : g) : cap);
 }
 
-template <int NP, bool WITH_Y>
-ks_status launch_items(ks_ctx *ctx, ProjArgs &a) {
-  constexpr int LPRY = Lay<NP>::LPR;
-  constexpr int LPR = LPRY < 8 ? 8 : LPRY;
-  constexpr int RPW = 32 / LPR;
-  const size_t sm = sizeof(double) * (size_t)PROJ_WARPS * RPW * 4 * ctx->d_max;
-  KS_CUDA(ctx, cudaFuncSetAttribute(k_proj_items<NP, WITH_Y>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  k_proj_items<NP, WITH_Y><<<proj_grid(ctx, ctx->n_items), PROJ_WARPS * 32, sm, ctx->stream>>>(a);
+// P rows as a dense 4-wide table (columns ascending, zero padded): the gather of a neighbour's P row
+// is one 32-byte load instead of the row_ptr -> values chain
+__global__ void k_pv4(const int32_t *__restrict__ Pptr, const double *__restrict__ Pval, int64_t n,
+                      double *__restrict__ Pv4) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t a = Pptr[i], m = Pptr[i + 1] - a;
+  for (int t = 0; t < 4; t++) Pv4[4 * i + t] = t < m ? Pval[a + t] : 0.0;
+}
+
+ks_status launch_proj_a(ks_ctx *ctx, const double *op_vals) {
+  const int wcap = (ctx->d_max + 31) / 32 * 32;
+  const size_t sm = sizeof(double) * (size_t)PA_WARPS * PA_SLOTS * 4 * wcap;
+  KS_CUDA(ctx, cudaFuncSetAttribute(k_proj_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_proj_a<<<proj_grid(ctx, ctx->n_items, PA_WARPS), PA_WARPS * 32, sm, ctx->stream>>>(
+      ctx->row_ptr, ctx->col, op_vals, ctx->slotmap, ctx->Pv4, ctx->perm, ctx->item_ptr, ctx->item_D_ptr,
+      ctx->n_items, wcap, ctx->AH_part);
   KS_LAUNCHED(ctx);
+  return KS_OK;
+}
+
+template <int NP>
+ks_status launch_proj_yb(ks_ctx *ctx, int N, const double *u, double *FA, double *FB, int64_t D) {
+  cudaStream_t s = ctx->stream;
+  const int64_t n = ctx->n_free;
+  k_proj_y<NP><<<ks_blocks(n * SL<NP>::LPR, 256), 256, 0, s>>>(ctx->sell_ptr, ctx->sell_col, ctx->sell_H,
+                                                               ctx->sell_M, u, ctx->Y_H, ctx->Y_M, n);
+  KS_LAUNCHED(ctx);
+  constexpr bool GRAM = NP <= 32;
+  const int grid = 2 * ctx->sm_count;
+  const int nparts = grid * PBG_WARPS;
+  if (GRAM) {
+    const int64_t need = (int64_t)nparts * 2 * NP * NP;
+    if (ctx->gram_cap < need) {
+      if (ctx->gram_part) { cudaFree(ctx->gram_part); ctx->gram_part = nullptr; }
+      KS_TRY(ks_alloc_t(ctx, &ctx->gram_part, need, "gram partials"));
+      ctx->gram_cap = need;
+    }
+  }
+  k_proj_bg<NP, GRAM><<<grid, PBG_WARPS * 32, 0, s>>>(u, ctx->Y_H, ctx->Y_M, ctx->Pv4, ctx->perm, ctx->item_ptr,
+                                                       ctx->n_items, ctx->bH_part, ctx->cH_part, ctx->gram_part);
+  KS_LAUNCHED(ctx);
+  if (GRAM) {
+    k_gram_fin<<<ks_blocks(2 * N * N, 128), 128, 0, s>>>(ctx->gram_part, nparts, N, NP, ctx->n_H, D, FA, FB);
+    KS_LAUNCHED(ctx);
+  } else {
+    // NP = 64: register tiles of the fused pass would not fit; row-block Gram kernel (natural order)
+    const int nblk = 2 * ctx->sm_count;
+    const int64_t rows_per_blk = ((n + nblk - 1) / nblk + GR_ROWS - 1) / GR_ROWS * GR_ROWS;
+    const int nb = (int)((n + rows_per_blk - 1) / rows_per_blk);
+    const int64_t need = (int64_t)nb * 2 * N * N;
+    if (ctx->gram_cap < need) {
+      if (ctx->gram_part) { cudaFree(ctx->gram_part); ctx->gram_part = nullptr; }
+      KS_TRY(ks_alloc_t(ctx, &ctx->gram_part, need, "gram partials"));
+      ctx->gram_cap = need;
+    }
+    const int NQ = (N + 3) / 4 * 4, NT = NQ / 4;
+    const int ntiles = 2 * NT * NT;
+    if (ntiles > 512) return ks_fail(ctx, KS_E_ARG, "N = %d too large for the Gram kernel", N);
+    const int ngroups = ntiles > 256 ? 1 : 256 / ntiles;
+    const size_t sm = sizeof(double) * (3 * GR_ROWS * NQ + (size_t)ngroups * 2 * N * N);
+    KS_CUDA(ctx, cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_gram<<<nb, 256, sm, s>>>(u, ctx->Y_H, ctx->Y_M, n, N, NP, rows_per_blk, ctx->gram_part);
+    KS_LAUNCHED(ctx);
+    k_gram_final<<<ks_blocks(2 * N * N, 128), 128, 0, s>>>(ctx->gram_part, nb, N, ctx->n_H, D, FA, FB);
+    KS_LAUNCHED(ctx);
+  }
   return KS_OK;
 }
 
@@ -508,29 +696,6 @@ ks_status launch_final(ks_ctx *ctx, int N, int NP, double *FA, double *FB, int64
   return KS_OK;
 }
 
-ProjArgs base_args(ks_ctx *ctx) {
-  ProjArgs a;
-  a.row_ptr = ctx->row_ptr;
-  a.col = ctx->col;
-  a.Aop = ctx->H;
-  a.Mop = ctx->M;
-  a.Pptr = ctx->P_ptr;
-  a.Pval = ctx->P_val;
-  a.perm = ctx->perm;
-  a.item_ptr = ctx->item_ptr;
-  a.item_S = ctx->item_S;
-  a.D_ptr = ctx->item_D_ptr;
-  a.slotmap = ctx->slotmap;
-  a.U = nullptr;
-  a.YH = a.YM = nullptr;
-  a.AH_part = ctx->AH_part;
-  a.bH_part = ctx->bH_part;
-  a.cH_part = ctx->cH_part;
-  a.n_items = ctx->n_items;
-  a.d_max = ctx->d_max;
-  return a;
-}
-
 struct TmpGuard {
   std::vector<void *> p;
   ~TmpGuard() { for (void *x : p) cudaFree(x); }
@@ -545,12 +710,12 @@ struct TmpGuard {
 }  // namespace
 
 void ks_free_coarse(ks_ctx *ctx) {
-  void *ptrs[] = {ctx->P_ptr, ctx->P_col, ctx->P_val, ctx->perm, ctx->item_ptr, ctx->item_S, ctx->item_D_ptr,
+  void *ptrs[] = {ctx->P_ptr, ctx->P_col, ctx->P_val, ctx->Pv4, ctx->perm, ctx->item_ptr, ctx->item_S, ctx->item_D_ptr,
                   ctx->item_D, ctx->slotmap, ctx->CT_ptr, ctx->CT_val, ctx->B_H, ctx->AH_part};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   ctx->P_ptr = ctx->P_col = nullptr;
-  ctx->P_val = nullptr;
+  ctx->P_val = ctx->Pv4 = nullptr;
   ctx->perm = ctx->item_ptr = ctx->item_S = ctx->item_D_ptr = ctx->item_D = ctx->CT_ptr = ctx->CT_val = nullptr;
   ctx->slotmap = nullptr;
   ctx->B_H = ctx->AH_part = nullptr;
@@ -592,6 +757,9 @@ ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, cons
   KS_CUDA(ctx, cudaStreamSynchronize(s));
   if (h_bad != ~0ull)
     return ks_fail(ctx, KS_E_ARG, "P row %llu invalid (more than 4 entries, repeated column, or column outside [0, n_H))", h_bad);
+  KS_TRY(ks_alloc_t(ctx, &ctx->Pv4, 4 * nf, "Pv4"));
+  k_pv4<<<ks_blocks(nf, 256), 256, 0, s>>>(ctx->P_ptr, ctx->P_val, nf, ctx->Pv4);
+  KS_LAUNCHED(ctx);
 
   // ---- group rows by parent set (stable: ascending row inside a group), cut into items ----
   int end_bit = 1;
@@ -707,9 +875,7 @@ ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, cons
   KS_TRY(ks_alloc_t(ctx, &ctx->AH_part, 4 * ctx->d_total, "AH_part"));
   KS_TRY(ks_alloc_t(ctx, &ctx->B_H, n_H * n_H, "B_H"));
   ctx->n_H = n_H;
-  ProjArgs a = base_args(ctx);
-  a.Aop = ctx->M;
-  KS_TRY((launch_items<16, false>(ctx, a)));
+  KS_TRY(launch_proj_a(ctx, ctx->M));
   KS_TRY(launch_final<false>(ctx, 0, 16, ctx->B_H, nullptr, n_H, 0));
   KS_CUDA(ctx, cudaStreamSynchronize(s));
   return KS_OK;
@@ -735,49 +901,24 @@ ks_status ks_project_impl(ks_ctx *ctx, int N, const double *Ut, double *FA, doub
     ctx->bc_cap = 4 * ctx->n_items * np;
   }
   const double *u = Ut;
-  if (np != N || ((uintptr_t)Ut & 15)) {
+  if (np != N || ((uintptr_t)Ut & 31)) {
     k_pad_proj<<<ks_blocks(n * np, 256), 256, 0, s>>>(Ut, N, ctx->proj_u, np, n);
     KS_LAUNCHED(ctx);
     u = ctx->proj_u;
   }
-  // K8: item pass
-  ProjArgs a = base_args(ctx);
-  a.Aop = ctx->H;
-  a.U = u;
-  a.YH = ctx->Y_H;
-  a.YM = ctx->Y_M;
+  // K8a + K8c (+ Gram partials) for the orbital blocks
   switch (np) {
-    case 1: KS_TRY((launch_items<1, true>(ctx, a))); break;
-    case 2: KS_TRY((launch_items<2, true>(ctx, a))); break;
-    case 4: KS_TRY((launch_items<4, true>(ctx, a))); break;
-    case 8: KS_TRY((launch_items<8, true>(ctx, a))); break;
-    case 16: KS_TRY((launch_items<16, true>(ctx, a))); break;
-    case 32: KS_TRY((launch_items<32, true>(ctx, a))); break;
-    case 64: KS_TRY((launch_items<64, true>(ctx, a))); break;
+    case 1: KS_TRY(launch_proj_yb<1>(ctx, N, u, FA, FB, D)); break;
+    case 2: KS_TRY(launch_proj_yb<2>(ctx, N, u, FA, FB, D)); break;
+    case 4: KS_TRY(launch_proj_yb<4>(ctx, N, u, FA, FB, D)); break;
+    case 8: KS_TRY(launch_proj_yb<8>(ctx, N, u, FA, FB, D)); break;
+    case 16: KS_TRY(launch_proj_yb<16>(ctx, N, u, FA, FB, D)); break;
+    case 32: KS_TRY(launch_proj_yb<32>(ctx, N, u, FA, FB, D)); break;
+    case 64: KS_TRY(launch_proj_yb<64>(ctx, N, u, FA, FB, D)); break;
     default: return ks_fail(ctx, KS_E_ARG, "N = %d unsupported", N);
   }
-  // K8b: beta, gamma
-  const int nblk = 2 * ctx->sm_count;
-  const int64_t rows_per_blk = ((n + nblk - 1) / nblk + GR_ROWS - 1) / GR_ROWS * GR_ROWS;
-  const int nb = (int)((n + rows_per_blk - 1) / rows_per_blk);
-  const int64_t need = (int64_t)nb * 2 * N * N;
-  if (ctx->gram_cap < need) {
-    if (ctx->gram_part) { cudaFree(ctx->gram_part); ctx->gram_part = nullptr; }
-    KS_TRY(ks_alloc_t(ctx, &ctx->gram_part, need, "gram partials"));
-    ctx->gram_cap = need;
-  }
-  {
-    const int NQ = (N + 3) / 4 * 4, NT = NQ / 4;
-    const int ntiles = 2 * NT * NT;
-    if (ntiles > 512) return ks_fail(ctx, KS_E_ARG, "N = %d too large for the Gram kernel", N);
-    const int ngroups = ntiles > 256 ? 1 : 256 / ntiles;
-    const size_t sm = sizeof(double) * (3 * GR_ROWS * NQ + (size_t)ngroups * 2 * N * N);
-    KS_CUDA(ctx, cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k_gram<<<nb, 256, sm, s>>>(u, ctx->Y_H, ctx->Y_M, n, N, np, rows_per_blk, ctx->gram_part);
-    KS_LAUNCHED(ctx);
-    k_gram_final<<<ks_blocks(2 * N * N, 128), 128, 0, s>>>(ctx->gram_part, nb, N, nH, D, FA, FB);
-    KS_LAUNCHED(ctx);
-  }
+  // K8b: A_H item partials (unshifted H, reading Q1)
+  KS_TRY(launch_proj_a(ctx, ctx->H));
   // K9: A_H, b_H, c_H
   KS_TRY(launch_final<true>(ctx, N, np, FA, FB, D, D));
   k_copy_block<<<ks_blocks(nH * nH, 256), 256, 0, s>>>(ctx->B_H, nH, FB, D);

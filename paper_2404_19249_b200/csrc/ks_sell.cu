@@ -78,6 +78,7 @@ ks_status ks_sell_build(ks_ctx *ctx) {
   KS_TRY(ks_alloc_t(ctx, &ctx->sell_col, total, "sell col"));
   KS_TRY(ks_alloc_t(ctx, &ctx->sell_A, total, "sell A"));
   KS_TRY(ks_alloc_t(ctx, &ctx->sell_M, total, "sell M"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->sell_H, total, "sell H"));
   k_sell_fill_col<<<ks_blocks(n, 256), 256, 0, s>>>(ctx->row_ptr, ctx->col, n, ctx->sell_ptr, ctx->sell_col);
   KS_LAUNCHED(ctx);
   k_sell_fill_val<<<ks_blocks(n, 256), 256, 0, s>>>(ctx->row_ptr, ctx->M, n, ctx->sell_ptr, ctx->sell_M);

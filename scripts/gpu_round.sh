@@ -1,7 +1,6 @@
 #!/bin/bash
-# One gpurun call: GPU tests, bench, ncu launch list, ncu --set full of the top kernels.
+# One gpurun call: GPU tests, smoke, bench (full line), ncu launch list, ncu --set full of the top kernels.
 # usage (on the box): bash scripts/gpu_round.sh TAG [CONFIG]
-set -x
 TAG=${1:-r01}
 CFG=${2:-4}
 OUT=gpurun_out/$TAG
@@ -11,10 +10,11 @@ python -c 'import __graft_entry__ as g; g.build()' > $OUT/build.log 2>&1
 timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $OUT/pytest_gpu.log
 timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' > $OUT/smoke.log 2>&1; echo "smoke exit $?" >> $OUT/smoke.log
 timeout 600 python bench.py --config $CFG > $OUT/bench.json 2> $OUT/bench.err; echo "bench exit $?" >> $OUT/bench.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv \
-  python bench.py --config $CFG --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_launches.log 2>&1
-for K in k_block_pcg k_assemble k_proj; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 3 -c 1 -o $OUT/full_$K \
-    python bench.py --config $CFG --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_full_$K.log 2>&1
-done
+L="python bench.py --config $CFG --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
+$L > $OUT/plain_launches.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  --log-file $OUT/launches.csv $L > $OUT/ncu_launches.log 2>&1
+F="python bench.py --config $CFG --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
+$F > $OUT/plain_full.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on \
+  -k 'regex:k_block_pcg|k_proj_items|k_assemble_rows|k_gram' -s 6 -c 4 -o $OUT/full $F > $OUT/ncu_full.log 2>&1
+tail -2 $OUT/pytest_gpu.log $OUT/smoke.log; cat $OUT/bench.json
 ls -la $OUT
