@@ -53,23 +53,28 @@ ks_status ks_alloc(ks_ctx *ctx, void **ptr, size_t bytes, const char *what) {
     return ks_fail(ctx, KS_E_NOMEM, "cudaMalloc(%zu bytes) for %s: %s", bytes, what, cudaGetErrorString(e));
   }
   ctx->bytes += bytes;
+  ctx->allocs.push_back({*ptr, bytes});
   // zero-filled: padding tails past the logical ends (read by the bulk tile copies) stay defined
   e = cudaMemsetAsync(*ptr, 0, bytes, ctx->stream);
   if (e != cudaSuccess) return ks_cuda_check(ctx, e, "cudaMemsetAsync (new allocation)");
   return KS_OK;
 }
 
+void ks_free(ks_ctx *ctx, void *ptr) {
+  if (!ptr) return;
+  for (size_t k = 0; k < ctx->allocs.size(); k++)
+    if (ctx->allocs[k].first == ptr) {
+      ctx->bytes -= ctx->allocs[k].second;
+      ctx->allocs.erase(ctx->allocs.begin() + k);
+      break;
+    }
+  cudaFree(ptr);
+}
+
 static void free_all(ks_ctx *ctx) {
-  void *ptrs[] = {ctx->tets, ctx->free_of_node, ctx->node_of_free, ctx->row_ptr, ctx->col, ctx->diag_pos,
-                  ctx->emap, ctx->inv_ptr, ctx->inv_idx, ctx->vol, ctx->K, ctx->M, ctx->MV, ctx->H, ctx->A,
-                  ctx->diag, ctx->w_tet, ctx->v_free, ctx->d_flags, ctx->d_block_iters, ctx->r, ctx->p, ctx->q,
-                  ctx->xpad, ctx->upad, ctx->partials, ctx->barrier};
-  for (void *p : ptrs)
-    if (p) cudaFree(p);
-  ks_free_coarse(ctx);
-  void *proj[] = {ctx->Y_H, ctx->Y_M, ctx->proj_u, ctx->gram_part, ctx->bH_part, ctx->cH_part};
-  for (void *p : proj)
-    if (p) cudaFree(p);
+  for (auto &a : ctx->allocs) cudaFree(a.first);
+  ctx->allocs.clear();
+  ctx->bytes = 0;
 }
 
 extern "C" {

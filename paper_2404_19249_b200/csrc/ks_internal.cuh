@@ -24,7 +24,7 @@ struct ks_ctx {
   int64_t n_nodes = 0, n_tets = 0, n_free = 0, nnz = 0, n_contrib = 0;
   int64_t launches = 0;
   size_t bytes = 0;
-  std::vector<void *> allocs;
+  std::vector<std::pair<void *, size_t>> allocs;  // every library-owned device allocation (ks_alloc)
 
   // mesh / pattern (library-owned device memory)
   int32_t *tets = nullptr;          // [4 n_tets]
@@ -70,6 +70,8 @@ struct ks_ctx {
   int32_t *P_ptr = nullptr, *P_col = nullptr;   // own copy, columns ascending within a row
   double *P_val = nullptr;
   double *Pv4 = nullptr;         // [4 n_free] P rows as a zero-padded 4-wide table
+  double *Pv4p = nullptr;        // [4 n_free] the same in item order (position of the parent grouping)
+  int32_t *pos_of_row = nullptr; // [n_free] inverse of perm
   int64_t n_items = 0, d_total = 0;
   int d_max = 0;
   int32_t *perm = nullptr;       // [n_free] fine rows grouped by parent set ("items" of <= ITEM_ROWS rows)
@@ -78,13 +80,17 @@ struct ks_ctx {
   int32_t *item_D_ptr = nullptr; // [n_items+1]
   int32_t *item_D = nullptr;     // [d_total] sorted coarse ids touched by P rows of the item's neighbours
   uint8_t *slotmap = nullptr;    // [4 nnz] slot of (entry k, parent t of col[k]) in its row's item D list
+  uint8_t *lslot = nullptr;      // [16 n_free] a row's local window: its distinct item-window slots (255 pad)
+  uint16_t *lidx = nullptr;      // [nnz] local index of each parent t of col[k] (4 bits each, 15 = none)
+  uint8_t *item_tier = nullptr;  // [n_items] largest local window of the item's rows
   int32_t *CT_ptr = nullptr;     // [n_H+1] coarse node -> (item, local parent) list
   int32_t *CT_val = nullptr;     // [4 n_items] entries 4 item + q
   double *B_H = nullptr;         // [n_H n_H] cached P^T M P
   double *AH_part = nullptr;     // [4 d_total] per-item partials of P^T Op P
   double *bH_part = nullptr, *cH_part = nullptr;  // [4 n_items NP]
   int64_t bc_cap = 0;
-  double *Y_H = nullptr, *Y_M = nullptr, *proj_u = nullptr;  // [n_free][NP]
+  double *Y_H = nullptr, *Y_M = nullptr, *proj_u = nullptr;  // [n_free][NP] (Y_H, Y_M in item order)
+  double *proj_up = nullptr;     // [n_free][NP] U~ in item order
   int64_t y_cap = 0;
   double *gram_part = nullptr;   // [blocks][2 N N]
   int64_t gram_cap = 0;
@@ -103,6 +109,12 @@ const char *ks_status_name(ks_status s);
 ks_status ks_fail(ks_ctx *ctx, ks_status s, const char *fmt, ...);
 ks_status ks_cuda_check(ks_ctx *ctx, cudaError_t e, const char *what);
 ks_status ks_alloc(ks_ctx *ctx, void **ptr, size_t bytes, const char *what);
+void ks_free(ks_ctx *ctx, void *ptr);   // frees a ks_alloc'ed pointer (no-op on nullptr)
+template <typename T>
+static inline void ks_free_t(ks_ctx *ctx, T *&ptr) {
+  ks_free(ctx, (void *)ptr);
+  ptr = nullptr;
+}
 
 #define KS_TRY(expr)                      \
   do {                                    \

@@ -394,7 +394,7 @@ ks_status launch_pcg(ks_ctx *ctx, PcgArgs &a) {
   int G = per_sm * ctx->sm_count;
   if (G > a.ntiles) G = a.ntiles;
   if ((int64_t)G * 4 * NP * 2 > ctx->partial_cap) {
-    if (ctx->partials) { cudaFree(ctx->partials); ctx->partials = nullptr; }
+    ks_free_t(ctx, ctx->partials);
     ctx->partial_cap = (int64_t)G * 4 * NP * 2;
     KS_TRY(ks_alloc_t(ctx, &ctx->partials, ctx->partial_cap, "pcg partials"));
   }
@@ -527,7 +527,7 @@ ks_status ks_spmm_impl(ks_ctx *ctx, ks_op op, const double *val, int N, const do
 static ks_status ensure_solver_ws(ks_ctx *ctx, int np) {
   if (ctx->ws_np >= np && ctx->ws_rows == ctx->n_free) return KS_OK;
   for (double **b : {&ctx->r, &ctx->p, &ctx->q, &ctx->xpad, &ctx->upad})
-    if (*b) { cudaFree(*b); *b = nullptr; }
+    ks_free_t(ctx, *b);
   const int64_t cnt = ctx->n_free * (int64_t)np;
   KS_TRY(ks_alloc_t(ctx, &ctx->r, cnt, "pcg r"));
   KS_TRY(ks_alloc_t(ctx, &ctx->p, cnt, "pcg p"));

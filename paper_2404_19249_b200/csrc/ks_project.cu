@@ -217,15 +217,15 @@ __global__ void k_lower_bound_ptr(const int32_t *__restrict__ keys, int64_t nk, 
 // K8b  k_proj_a   per item: sum_i P_ic (Op P)_{i,d} for c in S, d in the item window D  (A_H / B_H)
 // K8c  k_proj_bg  per item: b/c partials sum_i P_ic Y[i]; per warp: Gram partials U~^T Y (upper tiles)
 // K9   k_proj_final / k_gram_fin: fixed-order sums of the partials into F_A, F_B.
-constexpr int PA_WARPS = 4;      // warps per block of k_proj_a
-constexpr int PA_SLOTS = 8;      // rows of an item in flight per warp (4 lanes each: one per parent t)
-constexpr int PBG_WARPS = 8;     // warps per block of k_proj_bg
 
 template <int NP>
 __global__ void __launch_bounds__(256) k_proj_y(const int32_t *__restrict__ sell_ptr, const int32_t *__restrict__ sell_col,
                                                 const double *__restrict__ H, const double *__restrict__ M,
-                                                const double *__restrict__ U, double *__restrict__ YH,
-                                                double *__restrict__ YM, int64_t n) {
+                                                const double *__restrict__ U, const int32_t *__restrict__ pos_of_row,
+                                                double *__restrict__ Up, double *__restrict__ YHp,
+                                                double *__restrict__ YMp, int64_t n) {
+  // rows in natural order (coalesced operator stream); outputs scattered, one full row each, into item
+  // order (position pos_of_row[row] of the coarse-parent grouping) for the item pass k_proj_bg
   constexpr int VEC = SL<NP>::VEC, LPR = SL<NP>::LPR;
   const int64_t gl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t row = gl / LPR;
@@ -233,18 +233,75 @@ __global__ void __launch_bounds__(256) k_proj_y(const int32_t *__restrict__ sell
   if (row >= n) return;
   DV<VEC> yh, ym;
   sell_row<NP, 2>(sell_ptr, sell_col, H, M, row, U, sub, yh, ym);
-  yh.st(YH + row * NP + sub * VEC);
-  ym.st(YM + row * NP + sub * VEC);
+  const int64_t o = (int64_t)__ldg(pos_of_row + row) * NP + sub * VEC;
+  DV<VEC>::ld(U + row * NP + sub * VEC).st(Up + o);
+  yh.st(YHp + o);
+  ym.st(YMp + o);
 }
 
-// Item partials of P^T Op P. Warp per item; lane = 4 * slot + t: row slot `slot` of PA_SLOTS, parent index t
-// of the neighbour's P row. Per nonzero k (row i, column j) the lane adds Op_k P_{j,t} P_{i,c} (c = 0..3) to
-// the row slot's private window copy W[slot][c][s], s = slotmap[4k + t] (distinct t of one k give distinct
-// coarse columns, so the 4 lanes of a slot never collide). Copies are combined in slot order.
+// Item partials of P^T Op P (A_H with Op = H, B_H with Op = M). One warp per item, in two phases per chunk
+// of 32 rows of the item (perm order):
+//   1. lane = row i: W_i over the row's LOCAL window (its <= 16 distinct item-window slots, precomputed in
+//      ks_set_coarse: lslot, and per nonzero the local index of each parent t: lidx, 4 bits each), in
+//      registers: W[m] += [l == m] Op_k P_{j_k, t} (branch-free, no shared-memory read-modify-write
+//      chains), then scattered once into the lane's row of a shared [32][wcap + 1] array;
+//   2. lane = window slot d: G[c][d] += P_ic W_i[d] over the chunk's rows in order (registers).
+// The register tier LT (4, 8 or 16 local slots) is chosen per item (max over its rows, warp-uniform).
+// No float atomics; the partition and all orders are fixed.
+constexpr int PA_WARPS = 4;      // warps per block of k_proj_a
+constexpr int PA_UNR = 4;        // nonzeros of a row in flight per lane
+
+template <int LT>
+__device__ __forceinline__ void proj_a_row(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                                           const double *__restrict__ val, const uint16_t *__restrict__ lidx,
+                                           const uint8_t *__restrict__ lslot, const double *__restrict__ Pv4,
+                                           int32_t i, double *Wl) {
+  double W[LT];
+#pragma unroll
+  for (int m = 0; m < LT; m++) W[m] = 0.0;
+  const int32_t k0 = __ldg(row_ptr + i), k1 = __ldg(row_ptr + i + 1);
+  for (int32_t kb = k0; kb < k1; kb += PA_UNR) {
+    int32_t j[PA_UNR];
+    double h[PA_UNR];
+    unsigned li[PA_UNR];
+#pragma unroll
+    for (int u = 0; u < PA_UNR; u++) {
+      const bool in = kb + u < k1;
+      const int32_t k = in ? kb + u : k0;
+      j[u] = __ldg(col + k);
+      h[u] = in ? __ldg(val + k) : 0.0;
+      li[u] = in ? __ldg(lidx + k) : 0xFFFFu;
+    }
+    double q[PA_UNR][4];
+#pragma unroll
+    for (int u = 0; u < PA_UNR; u++) ldnc_v4(Pv4 + 4 * (int64_t)j[u], q[u][0], q[u][1], q[u][2], q[u][3]);
+#pragma unroll
+    for (int u = 0; u < PA_UNR; u++)
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        const unsigned l = (li[u] >> (4 * t)) & 15u;
+        const double v = h[u] * q[u][t];
+#pragma unroll
+        for (int m = 0; m < LT; m++) W[m] += (l == (unsigned)m) ? v : 0.0;
+      }
+  }
+  // scatter the local window into the lane's row of the item window
+  const uint4 ls = __ldg(reinterpret_cast<const uint4 *>(lslot) + i);
+  const unsigned lw[4] = {ls.x, ls.y, ls.z, ls.w};
+#pragma unroll
+  for (int m = 0; m < LT; m++) {
+    const unsigned d = (lw[m >> 2] >> (8 * (m & 3))) & 255u;
+    if (d != 255u) Wl[d] = W[m];
+  }
+}
+
+template <int ND>                // window slots per lane in phase 2: ND * 32 >= wcap
 __global__ void __launch_bounds__(PA_WARPS * 32) k_proj_a(const int32_t *__restrict__ row_ptr,
                                                           const int32_t *__restrict__ col,
                                                           const double *__restrict__ val,
-                                                          const uint8_t *__restrict__ slotmap,
+                                                          const uint16_t *__restrict__ lidx,
+                                                          const uint8_t *__restrict__ lslot,
+                                                          const uint8_t *__restrict__ item_tier,
                                                           const double *__restrict__ Pv4,
                                                           const int32_t *__restrict__ perm,
                                                           const int32_t *__restrict__ item_ptr,
@@ -252,72 +309,128 @@ __global__ void __launch_bounds__(PA_WARPS * 32) k_proj_a(const int32_t *__restr
                                                           double *__restrict__ AH_part) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int slot = lane >> 2, t = lane & 3;
-  double *W = smem + (int64_t)warp * PA_SLOTS * 4 * wcap;   // [slot][c][wcap]
-  double *Wm = W + slot * 4 * wcap;
+  const int ws = wcap + 1;                                   // odd row stride: conflict-free column reads
+  double *W = smem + (int64_t)warp * 32 * (ws + 4);          // [32][ws] window rows, then [32][4] P rows
+  double *Ps = W + 32 * ws;
+  double *Wl = W + lane * ws;
   const int64_t gw = (int64_t)blockIdx.x * PA_WARPS + warp, nw = (int64_t)gridDim.x * PA_WARPS;
-  for (int x = lane; x < PA_SLOTS * 4 * wcap; x += 32) W[x] = 0.0;
-  __syncwarp();
   for (int64_t it = gw; it < n_items; it += nw) {
     const int32_t p0 = __ldg(item_ptr + it), p1 = __ldg(item_ptr + it + 1);
     const int32_t d0 = __ldg(D_ptr + it), dn = __ldg(D_ptr + it + 1) - d0;
-    for (int32_t pos = p0 + slot; pos < p1; pos += PA_SLOTS) {
-      const int32_t i = __ldg(perm + pos);
-      double pi[4];
-      ldnc_v4(Pv4 + 4 * (int64_t)i, pi[0], pi[1], pi[2], pi[3]);
-      const int32_t k0 = __ldg(row_ptr + i), k1 = __ldg(row_ptr + i + 1);
-      int32_t k = k0;
-      for (; k + 4 <= k1; k += 4) {
-        int32_t j[4], s[4];
-        double h[4], pj[4];
+    const int tier = __ldg(item_tier + it);
+    double G[ND][4];
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-          j[u] = __ldg(col + k + u);
-          h[u] = __ldg(val + k + u);
-          s[u] = __ldg(slotmap + 4 * (int64_t)(k + u) + t);
-        }
+    for (int q = 0; q < ND; q++)
 #pragma unroll
-        for (int u = 0; u < 4; u++) pj[u] = __ldg(Pv4 + 4 * (int64_t)j[u] + t);
+      for (int c = 0; c < 4; c++) G[q][c] = 0.0;
+    for (int32_t cb = p0; cb < p1; cb += 32) {
+      const int nr = min(32, p1 - cb);
+      // ---- phase 1: lane = row ----
+      for (int d = 0; d < dn; d++) Wl[d] = 0.0;
+      if (lane < nr) {
+        const int32_t i = __ldg(perm + cb + lane);
+        double pi0, pi1, pi2, pi3;
+        ldnc_v4(Pv4 + 4 * (int64_t)i, pi0, pi1, pi2, pi3);
+        Ps[lane * 4 + 0] = pi0; Ps[lane * 4 + 1] = pi1; Ps[lane * 4 + 2] = pi2; Ps[lane * 4 + 3] = pi3;
+        if (tier <= 4) proj_a_row<4>(row_ptr, col, val, lidx, lslot, Pv4, i, Wl);
+        else if (tier <= 8) proj_a_row<8>(row_ptr, col, val, lidx, lslot, Pv4, i, Wl);
+        else proj_a_row<16>(row_ptr, col, val, lidx, lslot, Pv4, i, Wl);
+      }
+      __syncwarp();
+      // ---- phase 2: lane = window slot ----
 #pragma unroll
-        for (int u = 0; u < 4; u++)
-          if (s[u] != 255) {
-            const double w = h[u] * pj[u];
+      for (int q = 0; q < ND; q++) {
+        const int d = lane + 32 * q;
+        if (d < dn) {
+          for (int r = 0; r < nr; r++) {
+            const double w = W[r * ws + d];
 #pragma unroll
-            for (int c = 0; c < 4; c++) Wm[c * wcap + s[u]] = fma(pi[c], w, Wm[c * wcap + s[u]]);
+            for (int c = 0; c < 4; c++) G[q][c] = fma(Ps[r * 4 + c], w, G[q][c]);
           }
+        }
       }
-      for (; k < k1; k++) {
-        const int32_t j0 = __ldg(col + k), s0 = __ldg(slotmap + 4 * (int64_t)k + t);
-        const double w = __ldg(val + k) * __ldg(Pv4 + 4 * (int64_t)j0 + t);
-        if (s0 != 255)
-#pragma unroll
-          for (int c = 0; c < 4; c++) Wm[c * wcap + s0] = fma(pi[c], w, Wm[c * wcap + s0]);
-      }
+      __syncwarp();
     }
-    __syncwarp();
     double *out = AH_part + 4 * (int64_t)d0;
-    for (int x = lane; x < 4 * dn; x += 32) {
-      const int c = x / dn, d = x % dn;
-      double sum = 0.0;
-      for (int r = 0; r < PA_SLOTS; r++) {
-        sum += W[(r * 4 + c) * wcap + d];
-        W[(r * 4 + c) * wcap + d] = 0.0;
-      }
-      out[x] = sum;
+#pragma unroll
+    for (int q = 0; q < ND; q++) {
+      const int d = lane + 32 * q;
+      if (d < dn)
+#pragma unroll
+        for (int c = 0; c < 4; c++) out[c * dn + d] = G[q][c];
     }
-    __syncwarp();
   }
 }
 
-// Item pass over the rows of each item (perm order): b/c partials per item and Gram partials per warp.
-// Rows are staged PBG_ROWS at a time in the warp's shared memory: U~, Y_H, Y_M rows and the P row.
-// Gram: 4x4 register tiles (op, ta, tb) with ta <= tb (the blocks are symmetric), lane l owns tiles
-// l, l + 32, ...; b/c: lane l owns (op, c) = l / 4 and the orbitals b in quarter l % 4.
+// Setup (ks_set_coarse): per row, its local window (sorted distinct item-window slots of its nonzeros'
+// parents, <= 16; 255-padded) and per nonzero the local index of each parent t (4 bits, 15 = none).
+// Returns the row's local window size in lsize.
+__global__ void k_local_windows(const int32_t *__restrict__ row_ptr, const uint8_t *__restrict__ slotmap,
+                                int64_t n, uint8_t *__restrict__ lslot, uint16_t *__restrict__ lidx,
+                                uint8_t *__restrict__ lsize, unsigned *__restrict__ overflow) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint8_t L[16];
+  int nl = 0;
+  bool over = false;
+  const int32_t k0 = row_ptr[i], k1 = row_ptr[i + 1];
+  for (int32_t k = k0; k < k1; k++)
+    for (int t = 0; t < 4; t++) {
+      const uint8_t s = slotmap[4 * (int64_t)k + t];
+      if (s == 255) continue;
+      int pos = 0;
+      while (pos < nl && L[pos] < s) pos++;
+      if (pos < nl && L[pos] == s) continue;
+      if (nl == 16) { over = true; continue; }
+      for (int m = nl; m > pos; m--) L[m] = L[m - 1];
+      L[pos] = s;
+      nl++;
+    }
+  if (over) atomicOr(overflow, 1u);
+  for (int m = 0; m < 16; m++) lslot[16 * i + m] = m < nl ? L[m] : 255;
+  lsize[i] = (uint8_t)nl;
+  for (int32_t k = k0; k < k1; k++) {
+    unsigned code = 0;
+    for (int t = 0; t < 4; t++) {
+      const uint8_t s = slotmap[4 * (int64_t)k + t];
+      unsigned l = 15;
+      if (s != 255)
+        for (int m = 0; m < nl; m++)
+          if (L[m] == s) l = m;
+      code |= l << (4 * t);
+    }
+    lidx[k] = (uint16_t)code;
+  }
+}
+
+// per item: the largest local window of its rows (register tier of k_proj_a)
+__global__ void k_item_tier(const int32_t *__restrict__ item_ptr, const int32_t *__restrict__ perm,
+                            const uint8_t *__restrict__ lsize, int64_t n_items, uint8_t *__restrict__ tier) {
+  const int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (it >= n_items) return;
+  int m = 0;
+  for (int32_t pos = item_ptr[it]; pos < item_ptr[it + 1]; pos++) m = max(m, (int)lsize[perm[pos]]);
+  tier[it] = (uint8_t)m;
+}
+
+// Item pass (item order: Up, YHp, YMp, Pv4p are stored by position, so every item's rows are contiguous):
+// b/c partials per item and Gram partials per warp. Each warp owns a contiguous range of items and streams
+// its rows through a 2-stage shared-memory ring with bulk (TMA) copies, lane 0 producing, all lanes
+// consuming. Gram: 4x4 register tiles (op, ta, tb), ta <= tb (the blocks are symmetric), lane l owns tiles
+// l, l + 32, ...; b/c: lane l owns (op, c) = l / 4 and the orbitals b of quarter l % 4.
+constexpr int PBG_WARPS = 4;     // warps per block of k_proj_bg
+constexpr int PBG_STAGES = 2;
+template <int NP>
+struct PbgLayout {
+  static constexpr int CH = NP <= 16 ? 32 : NP == 32 ? 16 : 8;          // rows per stage
+  static constexpr int STAGE = CH * (3 * NP + 4);                        // doubles per stage
+  static constexpr size_t WARP_BYTES = sizeof(double) * PBG_STAGES * STAGE;
+};
+
 template <int NP, bool GRAM>
-__global__ void __launch_bounds__(PBG_WARPS * 32) k_proj_bg(const double *__restrict__ U, const double *__restrict__ YH,
-                                                            const double *__restrict__ YM,
-                                                            const double *__restrict__ Pv4,
-                                                            const int32_t *__restrict__ perm,
+__global__ void __launch_bounds__(PBG_WARPS * 32) k_proj_bg(const double *__restrict__ Up, const double *__restrict__ YHp,
+                                                            const double *__restrict__ YMp,
+                                                            const double *__restrict__ Pv4p,
                                                             const int32_t *__restrict__ item_ptr, int64_t n_items,
                                                             double *__restrict__ bH_part, double *__restrict__ cH_part,
                                                             double *__restrict__ gram_part) {
@@ -325,26 +438,26 @@ __global__ void __launch_bounds__(PBG_WARPS * 32) k_proj_bg(const double *__rest
   constexpr int NT2 = T4 * (T4 + 1) / 2;                   // upper tiles per operator
   constexpr int MAXT = (2 * NT2 + 31) / 32;                // tiles per lane
   constexpr int BQ = NP >= 4 ? NP / 4 : NP;                // b/c orbitals per lane (NP >= 4: a quarter)
-  constexpr int SEGS = (3 * NP + 4 + 3) / 4;               // 4-double segments staged per row
-  constexpr int RS = 4 * SEGS;                             // staged doubles per row (U~, Y_H, Y_M, P, pad)
-  constexpr int PBG_ROWS = NP <= 16 ? 8 : NP == 32 ? 4 : 2;  // rows staged per warp step
-  __shared__ __align__(16) double st[PBG_WARPS][PBG_ROWS * RS];
+  constexpr int CH = PbgLayout<NP>::CH, STAGE = PbgLayout<NP>::STAGE;
+  extern __shared__ __align__(16) double dsm[];
+  __shared__ __align__(8) uint64_t bars[PBG_WARPS][PBG_STAGES];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double *S = st[warp];
+  double *ring = dsm + (size_t)warp * PBG_STAGES * STAGE;
   const int64_t gw = (int64_t)blockIdx.x * PBG_WARPS + warp, nw = (int64_t)gridDim.x * PBG_WARPS;
+  // contiguous item range of this warp, and its rows
+  const int64_t ia = n_items * gw / nw, ib = n_items * (gw + 1) / nw;
+  const int32_t ra = __ldg(item_ptr + ia), rb = __ldg(item_ptr + ib);
+  const int nchunks = (rb - ra + CH - 1) / CH;
 
-  // tile coordinates of this lane
   int t_op[MAXT], t_a[MAXT], t_b[MAXT];
 #pragma unroll
   for (int q = 0; q < MAXT; q++) {
-    int id = lane + 32 * q, op = 0, ta = 0, tb = 0;
+    int id = lane + 32 * q, op = -1, ta = 0, tb = 0;
     if (id < 2 * NT2) {
       op = id / NT2;
       int r = id % NT2;
       while (r >= T4 - ta) { r -= T4 - ta; ta++; }
       tb = ta + r;
-    } else {
-      op = -1;
     }
     t_op[q] = op; t_a[q] = ta; t_b[q] = tb;
   }
@@ -353,84 +466,87 @@ __global__ void __launch_bounds__(PBG_WARPS * 32) k_proj_bg(const double *__rest
   for (int q = 0; q < MAXT; q++)
 #pragma unroll
     for (int e = 0; e < 16; e++) g[q][e] = 0.0;
-  const int bc_op = (lane >> 2) >> 2, bc_c = (lane >> 2) & 3, bc_b0 = (NP >= 4 ? (lane & 3) * BQ : 0);
+  const int bc_op = lane >> 4, bc_c = (lane >> 2) & 3, bc_b0 = NP >= 4 ? (lane & 3) * BQ : 0;
   const bool bc_on = NP >= 4 || (lane & 3) == 0;
 
-  for (int64_t it = gw; it < n_items; it += nw) {
-    const int32_t p0 = __ldg(item_ptr + it), p1 = __ldg(item_ptr + it + 1);
-    double bc[BQ];
+  auto issue = [&](int c) {   // lane 0: chunk c of this warp's rows into stage c % PBG_STAGES
+    const int st = c % PBG_STAGES;
+    const int32_t r0 = ra + c * CH, cnt = min(CH, rb - r0);
+    double *S = ring + st * STAGE;
+    const unsigned bv = (unsigned)cnt * NP * 8u, bp = (unsigned)cnt * 32u;
+    mbar_expect_tx(&bars[warp][st], 3 * bv + bp);
+    bulk_g2s(S, Up + (int64_t)r0 * NP, bv, &bars[warp][st]);
+    bulk_g2s(S + CH * NP, YHp + (int64_t)r0 * NP, bv, &bars[warp][st]);
+    bulk_g2s(S + 2 * CH * NP, YMp + (int64_t)r0 * NP, bv, &bars[warp][st]);
+    bulk_g2s(S + 3 * CH * NP, Pv4p + 4 * (int64_t)r0, bp, &bars[warp][st]);
+  };
+  if (lane == 0) {
+    for (int st = 0; st < PBG_STAGES; st++) mbar_init(&bars[warp][st], 1);
+    mbar_fence_init();
+    for (int c = 0; c < PBG_STAGES && c < nchunks; c++) issue(c);
+  }
+  __syncwarp();
+
+  int64_t it = ia;
+  int32_t iend = __ldg(item_ptr + ia + 1);
+  double bc[BQ];
 #pragma unroll
-    for (int v = 0; v < BQ; v++) bc[v] = 0.0;
-    for (int32_t pb = p0; pb < p1; pb += PBG_ROWS) {
-      const int nr = min(PBG_ROWS, p1 - pb);
-      __syncwarp();
-      // stage: per row 3 vectors of NP doubles + the P row (4 doubles), in 4-double segments
-      for (int x = lane; x < PBG_ROWS * SEGS; x += 32) {
-        const int r = x / SEGS, sg = x % SEGS;
-        double v0 = 0, v1 = 0, v2 = 0, v3 = 0;
-        if (r < nr) {
-          const int64_t i = __ldg(perm + pb + r);
-          const int vec = (4 * sg) / NP, off = (4 * sg) % NP;
-          const double *src = vec == 0 ? U : vec == 1 ? YH : vec == 2 ? YM : Pv4;
-          const int64_t ld = vec < 3 ? NP : 4;
-          if (NP >= 4) {
-            ldnc_v4(src + i * ld + (vec < 3 ? off : 0), v0, v1, v2, v3);
-          } else {  // NP < 4: a segment spans several vectors of one row
-            double tmp[4];
-            for (int e = 0; e < 4; e++) {
-              const int fe = 4 * sg + e;
-              if (fe < 3 * NP) {
-                const int fv = fe / NP, fo = fe % NP;
-                tmp[e] = (fv == 0 ? U : fv == 1 ? YH : YM)[i * NP + fo];
-              } else {
-                tmp[e] = fe - 3 * NP < 4 ? Pv4[i * 4 + (fe - 3 * NP)] : 0.0;
-              }
-            }
-            v0 = tmp[0]; v1 = tmp[1]; v2 = tmp[2]; v3 = tmp[3];
-          }
-        }
-        double *d = S + r * RS + 4 * sg;
-        d[0] = v0; d[1] = v1; d[2] = v2; d[3] = v3;
-      }
-      __syncwarp();
-      for (int r = 0; r < nr; r++) {
-        const double *R = S + r * RS;
-        if (GRAM) {
-#pragma unroll
-          for (int q = 0; q < MAXT; q++) {
-            if (t_op[q] < 0) continue;
-            const double *ua = R + 4 * t_a[q];
-            const double *yb = R + NP * (1 + t_op[q]) + 4 * t_b[q];
-            double u4[4], y4[4];
-            if (NP >= 4) {
-              const double2 u01 = reinterpret_cast<const double2 *>(ua)[0], u23 = reinterpret_cast<const double2 *>(ua)[1];
-              const double2 y01 = reinterpret_cast<const double2 *>(yb)[0], y23 = reinterpret_cast<const double2 *>(yb)[1];
-              u4[0] = u01.x; u4[1] = u01.y; u4[2] = u23.x; u4[3] = u23.y;
-              y4[0] = y01.x; y4[1] = y01.y; y4[2] = y23.x; y4[3] = y23.y;
-            } else {
-#pragma unroll
-              for (int e = 0; e < 4; e++) { u4[e] = ua[e]; y4[e] = yb[e]; }
-            }
-#pragma unroll
-            for (int x = 0; x < 4; x++)
-#pragma unroll
-              for (int y = 0; y < 4; y++) g[q][x * 4 + y] = fma(u4[x], y4[y], g[q][x * 4 + y]);
-          }
-        }
-        if (bc_on) {
-          const double pc = R[3 * NP + bc_c];
-          const double *yv = R + NP * (1 + bc_op) + bc_b0;
-#pragma unroll
-          for (int v = 0; v < BQ; v++) bc[v] = fma(pc, yv[v], bc[v]);
-        }
-      }
-    }
+  for (int v = 0; v < BQ; v++) bc[v] = 0.0;
+  auto flush = [&]() {
     if (bc_on) {
       double *dst = (bc_op ? cH_part : bH_part) + (4 * it + bc_c) * NP + bc_b0;
 #pragma unroll
       for (int v = 0; v < BQ; v++) dst[v] = bc[v];
     }
+#pragma unroll
+    for (int v = 0; v < BQ; v++) bc[v] = 0.0;
+  };
+
+  for (int c = 0; c < nchunks; c++) {
+    const int st = c % PBG_STAGES;
+    mbar_wait(&bars[warp][st], (unsigned)(c / PBG_STAGES) & 1u);
+    const double *S = ring + st * STAGE;
+    const int32_t r0 = ra + c * CH, cnt = min(CH, rb - r0);
+    for (int rr = 0; rr < cnt; rr++) {
+      while (r0 + rr >= iend) {     // item boundary (warp-uniform)
+        flush();
+        it++;
+        iend = __ldg(item_ptr + it + 1);
+      }
+      const double *Ur = S + rr * NP, *Hr = S + CH * NP + rr * NP, *Mr = S + 2 * CH * NP + rr * NP;
+      const double *Pr = S + 3 * CH * NP + rr * 4;
+      if (GRAM) {
+#pragma unroll
+        for (int q = 0; q < MAXT; q++) {
+          if (t_op[q] < 0) continue;
+          const double *ua = Ur + 4 * t_a[q], *yb = (t_op[q] ? Mr : Hr) + 4 * t_b[q];
+          double u4[4], y4[4];
+          if (NP >= 4) {
+            const double2 u01 = reinterpret_cast<const double2 *>(ua)[0], u23 = reinterpret_cast<const double2 *>(ua)[1];
+            const double2 y01 = reinterpret_cast<const double2 *>(yb)[0], y23 = reinterpret_cast<const double2 *>(yb)[1];
+            u4[0] = u01.x; u4[1] = u01.y; u4[2] = u23.x; u4[3] = u23.y;
+            y4[0] = y01.x; y4[1] = y01.y; y4[2] = y23.x; y4[3] = y23.y;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; e++) { u4[e] = e < NP ? ua[e] : 0.0; y4[e] = e < NP ? yb[e] : 0.0; }
+          }
+#pragma unroll
+          for (int x = 0; x < 4; x++)
+#pragma unroll
+            for (int y = 0; y < 4; y++) g[q][x * 4 + y] = fma(u4[x], y4[y], g[q][x * 4 + y]);
+        }
+      }
+      if (bc_on) {
+        const double pc = Pr[bc_c];
+        const double *yv = (bc_op ? Mr : Hr) + bc_b0;
+#pragma unroll
+        for (int v = 0; v < BQ; v++) bc[v] = fma(pc, yv[v], bc[v]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && c + PBG_STAGES < nchunks) issue(c + PBG_STAGES);
   }
+  if (ib > ia) flush();   // the last item of the range
   if (GRAM) {
     // per-warp partial [2][NP][NP], both triangles (the lower one mirrored from the upper tiles)
     double *out = gram_part + gw * 2 * NP * NP;
@@ -450,15 +566,19 @@ __global__ void __launch_bounds__(PBG_WARPS * 32) k_proj_bg(const double *__rest
   }
 }
 
-// beta / gamma blocks: fixed-order sum of the per-warp Gram partials
+// beta / gamma blocks: one warp per entry sums the per-warp Gram partials (lane-strided, then a fixed
+// butterfly: deterministic)
 __global__ void k_gram_fin(const double *__restrict__ part, int nparts, int N, int NP, int64_t n_H, int64_t D,
                            double *__restrict__ FA, double *__restrict__ FB) {
-  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < 2 * N * N; x += gridDim.x * blockDim.x) {
-    const int m = x / (N * N), a = (x % (N * N)) / N, b = x % N;
-    double s = 0.0;
-    for (int w = 0; w < nparts; w++) s += part[(int64_t)w * 2 * NP * NP + m * NP * NP + a * NP + b];
-    (m ? FB : FA)[(n_H + a) * D + n_H + b] = s;
-  }
+  const int lane = threadIdx.x & 31;
+  const int64_t x = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (x >= 2 * N * N) return;
+  const int m = (int)(x / (N * N)), a = (int)((x % (N * N)) / N), b = (int)(x % N);
+  const double *src = part + m * NP * NP + a * NP + b;
+  double s = 0.0;
+  for (int w = lane; w < nparts; w += 32) s += __ldcg(src + (int64_t)w * 2 * NP * NP);
+  s = warp_sum(s);
+  if (lane == 0) (m ? FB : FA)[(n_H + a) * D + n_H + b] = s;
 }
 
 // one block per coarse node c: A row from the item partials (dense rows per warp, combined in warp
@@ -622,13 +742,25 @@ __global__ void k_pv4(const int32_t *__restrict__ Pptr, const double *__restrict
   for (int t = 0; t < 4; t++) Pv4[4 * i + t] = t < m ? Pval[a + t] : 0.0;
 }
 
+// item order: pos_of_row = inverse of perm, Pv4p[pos] = Pv4[perm[pos]]
+__global__ void k_item_order(const int32_t *__restrict__ perm, const double *__restrict__ Pv4, int64_t n,
+                             int32_t *__restrict__ pos_of_row, double *__restrict__ Pv4p) {
+  const int64_t pos = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (pos >= n) return;
+  const int32_t i = perm[pos];
+  pos_of_row[i] = (int32_t)pos;
+  for (int t = 0; t < 4; t++) Pv4p[4 * pos + t] = Pv4[4 * (int64_t)i + t];
+}
+
 ks_status launch_proj_a(ks_ctx *ctx, const double *op_vals) {
   const int wcap = (ctx->d_max + 31) / 32 * 32;
-  const size_t sm = sizeof(double) * (size_t)PA_WARPS * PA_SLOTS * 4 * wcap;
-  KS_CUDA(ctx, cudaFuncSetAttribute(k_proj_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  k_proj_a<<<proj_grid(ctx, ctx->n_items, PA_WARPS), PA_WARPS * 32, sm, ctx->stream>>>(
-      ctx->row_ptr, ctx->col, op_vals, ctx->slotmap, ctx->Pv4, ctx->perm, ctx->item_ptr, ctx->item_D_ptr,
-      ctx->n_items, wcap, ctx->AH_part);
+  if (wcap > 256) return ks_fail(ctx, KS_E_ARG, "coarse window %d > 256", ctx->d_max);
+  const size_t sm = sizeof(double) * (size_t)PA_WARPS * 32 * (wcap + 1 + 4);
+  auto kern = wcap <= 32 ? k_proj_a<1> : wcap <= 64 ? k_proj_a<2> : k_proj_a<8>;
+  KS_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  kern<<<proj_grid(ctx, ctx->n_items, PA_WARPS), PA_WARPS * 32, sm, ctx->stream>>>(
+      ctx->row_ptr, ctx->col, op_vals, ctx->lidx, ctx->lslot, ctx->item_tier, ctx->Pv4, ctx->perm, ctx->item_ptr,
+      ctx->item_D_ptr, ctx->n_items, wcap, ctx->AH_part);
   KS_LAUNCHED(ctx);
   return KS_OK;
 }
@@ -638,7 +770,8 @@ ks_status launch_proj_yb(ks_ctx *ctx, int N, const double *u, double *FA, double
   cudaStream_t s = ctx->stream;
   const int64_t n = ctx->n_free;
   k_proj_y<NP><<<ks_blocks(n * SL<NP>::LPR, 256), 256, 0, s>>>(ctx->sell_ptr, ctx->sell_col, ctx->sell_H,
-                                                               ctx->sell_M, u, ctx->Y_H, ctx->Y_M, n);
+                                                               ctx->sell_M, u, ctx->pos_of_row, ctx->proj_up,
+                                                               ctx->Y_H, ctx->Y_M, n);
   KS_LAUNCHED(ctx);
   constexpr bool GRAM = NP <= 32;
   const int grid = 2 * ctx->sm_count;
@@ -646,16 +779,18 @@ ks_status launch_proj_yb(ks_ctx *ctx, int N, const double *u, double *FA, double
   if (GRAM) {
     const int64_t need = (int64_t)nparts * 2 * NP * NP;
     if (ctx->gram_cap < need) {
-      if (ctx->gram_part) { cudaFree(ctx->gram_part); ctx->gram_part = nullptr; }
+      ks_free_t(ctx, ctx->gram_part);
       KS_TRY(ks_alloc_t(ctx, &ctx->gram_part, need, "gram partials"));
       ctx->gram_cap = need;
     }
   }
-  k_proj_bg<NP, GRAM><<<grid, PBG_WARPS * 32, 0, s>>>(u, ctx->Y_H, ctx->Y_M, ctx->Pv4, ctx->perm, ctx->item_ptr,
-                                                       ctx->n_items, ctx->bH_part, ctx->cH_part, ctx->gram_part);
+  const size_t bsm = PBG_WARPS * PbgLayout<NP>::WARP_BYTES;
+  KS_CUDA(ctx, cudaFuncSetAttribute(k_proj_bg<NP, GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+  k_proj_bg<NP, GRAM><<<grid, PBG_WARPS * 32, bsm, s>>>(ctx->proj_up, ctx->Y_H, ctx->Y_M, ctx->Pv4p, ctx->item_ptr,
+                                                         ctx->n_items, ctx->bH_part, ctx->cH_part, ctx->gram_part);
   KS_LAUNCHED(ctx);
   if (GRAM) {
-    k_gram_fin<<<ks_blocks(2 * N * N, 128), 128, 0, s>>>(ctx->gram_part, nparts, N, NP, ctx->n_H, D, FA, FB);
+    k_gram_fin<<<ks_blocks(2 * N * N * 32, 128), 128, 0, s>>>(ctx->gram_part, nparts, N, NP, ctx->n_H, D, FA, FB);
     KS_LAUNCHED(ctx);
   } else {
     // NP = 64: register tiles of the fused pass would not fit; row-block Gram kernel (natural order)
@@ -664,7 +799,7 @@ ks_status launch_proj_yb(ks_ctx *ctx, int N, const double *u, double *FA, double
     const int nb = (int)((n + rows_per_blk - 1) / rows_per_blk);
     const int64_t need = (int64_t)nb * 2 * N * N;
     if (ctx->gram_cap < need) {
-      if (ctx->gram_part) { cudaFree(ctx->gram_part); ctx->gram_part = nullptr; }
+      ks_free_t(ctx, ctx->gram_part);
       KS_TRY(ks_alloc_t(ctx, &ctx->gram_part, need, "gram partials"));
       ctx->gram_cap = need;
     }
@@ -674,7 +809,7 @@ ks_status launch_proj_yb(ks_ctx *ctx, int N, const double *u, double *FA, double
     const int ngroups = ntiles > 256 ? 1 : 256 / ntiles;
     const size_t sm = sizeof(double) * (3 * GR_ROWS * NQ + (size_t)ngroups * 2 * N * N);
     KS_CUDA(ctx, cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k_gram<<<nb, 256, sm, s>>>(u, ctx->Y_H, ctx->Y_M, n, N, NP, rows_per_blk, ctx->gram_part);
+    k_gram<<<nb, 256, sm, s>>>(ctx->proj_up, ctx->Y_H, ctx->Y_M, n, N, NP, rows_per_blk, ctx->gram_part);
     KS_LAUNCHED(ctx);
     k_gram_final<<<ks_blocks(2 * N * N, 128), 128, 0, s>>>(ctx->gram_part, nb, N, ctx->n_H, D, FA, FB);
     KS_LAUNCHED(ctx);
@@ -710,14 +845,17 @@ struct TmpGuard {
 }  // namespace
 
 void ks_free_coarse(ks_ctx *ctx) {
-  void *ptrs[] = {ctx->P_ptr, ctx->P_col, ctx->P_val, ctx->Pv4, ctx->perm, ctx->item_ptr, ctx->item_S, ctx->item_D_ptr,
-                  ctx->item_D, ctx->slotmap, ctx->CT_ptr, ctx->CT_val, ctx->B_H, ctx->AH_part};
-  for (void *p : ptrs)
-    if (p) cudaFree(p);
+  void *ptrs[] = {ctx->P_ptr, ctx->P_col, ctx->P_val, ctx->Pv4, ctx->Pv4p, ctx->pos_of_row, ctx->perm,
+                  ctx->lslot, ctx->lidx, ctx->item_tier,
+                  ctx->item_ptr, ctx->item_S, ctx->item_D_ptr, ctx->item_D, ctx->slotmap, ctx->CT_ptr,
+                  ctx->CT_val, ctx->B_H, ctx->AH_part};
+  for (void *p : ptrs) ks_free(ctx, p);
   ctx->P_ptr = ctx->P_col = nullptr;
-  ctx->P_val = ctx->Pv4 = nullptr;
+  ctx->P_val = ctx->Pv4 = ctx->Pv4p = nullptr;
+  ctx->pos_of_row = nullptr;
   ctx->perm = ctx->item_ptr = ctx->item_S = ctx->item_D_ptr = ctx->item_D = ctx->CT_ptr = ctx->CT_val = nullptr;
-  ctx->slotmap = nullptr;
+  ctx->slotmap = ctx->lslot = ctx->item_tier = nullptr;
+  ctx->lidx = nullptr;
   ctx->B_H = ctx->AH_part = nullptr;
   ctx->n_H = 0;
 }
@@ -775,6 +913,10 @@ ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, cons
   TMPA(cub_tmp, cub_cap);
   KS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(cub_tmp, tb, key, key_sorted, rows, ctx->perm, (int)nf, 0, end_bit, s));
   ctx->launches++;
+  KS_TRY(ks_alloc_t(ctx, &ctx->pos_of_row, nf, "pos_of_row"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->Pv4p, 4 * nf, "Pv4 (item order)"));
+  k_item_order<<<ks_blocks(nf, 256), 256, 0, s>>>(ctx->perm, ctx->Pv4, nf, ctx->pos_of_row, ctx->Pv4p);
+  KS_LAUNCHED(ctx);
   TMPA(flag, nf);
   TMPA(gincl, nf);
   TMPA(gfirst, nf);
@@ -855,6 +997,27 @@ ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, cons
   k_slotmap<<<ks_blocks(nf, 128), 128, 0, s>>>(ctx->perm, item_of_pos, ctx->item_D_ptr, ctx->item_D, ctx->row_ptr,
                                                ctx->col, ctx->P_ptr, ctx->P_col, nf, ctx->slotmap);
   KS_LAUNCHED(ctx);
+  // local windows of the rows and register tiers of the items (k_proj_a)
+  {
+    uint8_t *lsize;
+    unsigned *over;
+    TMPA(lsize, nf);
+    TMPA(over, 1);
+    KS_CUDA(ctx, cudaMemsetAsync(over, 0, sizeof(unsigned), s));
+    KS_TRY(ks_alloc_t(ctx, &ctx->lslot, 16 * nf, "lslot"));
+    KS_TRY(ks_alloc_t(ctx, &ctx->lidx, ctx->nnz, "lidx"));
+    KS_TRY(ks_alloc_t(ctx, &ctx->item_tier, ni, "item_tier"));
+    k_local_windows<<<ks_blocks(nf, 128), 128, 0, s>>>(ctx->row_ptr, ctx->slotmap, nf, ctx->lslot, ctx->lidx, lsize,
+                                                       over);
+    KS_LAUNCHED(ctx);
+    k_item_tier<<<ks_blocks(ni, 128), 128, 0, s>>>(ctx->item_ptr, ctx->perm, lsize, ni, ctx->item_tier);
+    KS_LAUNCHED(ctx);
+    unsigned h_over = 0;
+    KS_CUDA(ctx, cudaMemcpyAsync(&h_over, over, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    KS_CUDA(ctx, cudaStreamSynchronize(s));
+    if (h_over)
+      return ks_fail(ctx, KS_E_ARG, "a fine row touches more than 16 coarse nodes through its neighbours' P rows");
+  }
 
   // ---- coarse node -> items list (stable sort on the coarse id; pads sort last) ----
   int ct_bits = 1;
@@ -884,18 +1047,20 @@ ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, cons
 ks_status ks_project_impl(ks_ctx *ctx, int N, const double *Ut, double *FA, double *FB) {
   cudaStream_t s = ctx->stream;
   const int64_t n = ctx->n_free, nH = ctx->n_H, D = nH + N;
-  const int np = pow2_at_least(N);
+  // NP >= 2: item-ordered rows are then multiples of 16 bytes (bulk-copy granularity)
+  const int np = pow2_at_least(N) < 2 ? 2 : pow2_at_least(N);
   if (ctx->y_cap < n * np) {
-    for (double **b : {&ctx->Y_H, &ctx->Y_M, &ctx->proj_u})
-      if (*b) { cudaFree(*b); *b = nullptr; }
-    KS_TRY(ks_alloc_t(ctx, &ctx->Y_H, n * np, "Y_H"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->Y_M, n * np, "Y_M"));
+    for (double **b : {&ctx->Y_H, &ctx->Y_M, &ctx->proj_u, &ctx->proj_up})
+      ks_free_t(ctx, *b);
+    KS_TRY(ks_alloc_t(ctx, &ctx->Y_H, n * np, "Y_H (item order)"));
+    KS_TRY(ks_alloc_t(ctx, &ctx->Y_M, n * np, "Y_M (item order)"));
     KS_TRY(ks_alloc_t(ctx, &ctx->proj_u, n * np, "proj U pad"));
+    KS_TRY(ks_alloc_t(ctx, &ctx->proj_up, n * np, "proj U (item order)"));
     ctx->y_cap = n * np;
   }
   if (ctx->bc_cap < 4 * ctx->n_items * np) {
     for (double **b : {&ctx->bH_part, &ctx->cH_part})
-      if (*b) { cudaFree(*b); *b = nullptr; }
+      ks_free_t(ctx, *b);
     KS_TRY(ks_alloc_t(ctx, &ctx->bH_part, 4 * ctx->n_items * np, "bH_part"));
     KS_TRY(ks_alloc_t(ctx, &ctx->cH_part, 4 * ctx->n_items * np, "cH_part"));
     ctx->bc_cap = 4 * ctx->n_items * np;
@@ -908,7 +1073,6 @@ ks_status ks_project_impl(ks_ctx *ctx, int N, const double *Ut, double *FA, doub
   }
   // K8a + K8c (+ Gram partials) for the orbital blocks
   switch (np) {
-    case 1: KS_TRY(launch_proj_yb<1>(ctx, N, u, FA, FB, D)); break;
     case 2: KS_TRY(launch_proj_yb<2>(ctx, N, u, FA, FB, D)); break;
     case 4: KS_TRY(launch_proj_yb<4>(ctx, N, u, FA, FB, D)); break;
     case 8: KS_TRY(launch_proj_yb<8>(ctx, N, u, FA, FB, D)); break;
