@@ -97,8 +97,11 @@ ks_status ks_pattern(const ks_ctx *ctx, int64_t *n_free, int64_t *nnz, const int
                      const int32_t **d_col, const int32_t **d_emap, const int32_t **d_free_of_node,
                      const int32_t **d_inv_ptr, const int32_t **d_inv_idx);
 
-/* Device views of the value arrays [nnz] and the diagonal of A [n_free]. MV, H, A, diag are defined
- * after the first ks_assemble_veff (KS_E_STATE before). */
+/* Device views of the value arrays [nnz] (CSR order of ks_pattern) and the diagonal of A [n_free]. MV, H, A,
+ * diag are defined after the first ks_assemble_veff (KS_E_STATE before). The hot path keeps A and H in a
+ * sliced-ELL layout; the CSR arrays MV, H, A are recomputed from the last assembly's state on the
+ * context's stream when first requested after an assembly (one extra kernel; also by ks_spmm with
+ * KS_OP_MV / KS_OP_H and by ks_true_residual). Synchronise the stream before reading them. */
 ks_status ks_values(const ks_ctx *ctx, const double **d_K, const double **d_M, const double **d_MV,
                     const double **d_H, const double **d_A, const double **d_diag);
 

@@ -169,6 +169,10 @@ ks_status ks_values(const ks_ctx *ctx, const double **d_K, const double **d_M, c
   if (d_M) *d_M = ctx->M;
   if ((d_MV || d_H || d_A || d_diag) && !ctx->assembled)
     return ks_fail(const_cast<ks_ctx *>(ctx), KS_E_STATE, "ks_values: call ks_assemble_veff first");
+  if (d_MV || d_H || d_A) {
+    ks_status st = ks_materialize_views(const_cast<ks_ctx *>(ctx));
+    if (st != KS_OK) return st;
+  }
   if (d_MV) *d_MV = ctx->MV;
   if (d_H) *d_H = ctx->H;
   if (d_A) *d_A = ctx->A;
@@ -201,6 +205,7 @@ ks_status ks_spmm(ks_ctx *ctx, ks_op op, int32_t N, const double *d_X, double *d
   if (((uintptr_t)d_X & 7) || ((uintptr_t)d_Y & 7)) return ks_fail(ctx, KS_E_ARG, "ks_spmm: X, Y must be 8-byte aligned");
   const double *v = op_values(ctx, op);
   if (!v) return ks_fail(ctx, KS_E_STATE, "ks_spmm: operator %d not assembled", (int)op);
+  if (op == KS_OP_MV || op == KS_OP_H) KS_TRY(ks_materialize_views(ctx));
   return ks_spmm_impl(ctx, op, v, N, d_X, d_Y);
 }
 

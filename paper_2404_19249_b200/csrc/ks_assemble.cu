@@ -34,7 +34,13 @@ __global__ void k_tet_weights(const int32_t *__restrict__ tets, const double *__
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, KSF_NONFINITE);
 }
 
-// Half-warp per row: lane j of the half handles entries row_ptr[i] + j, + 16, ...
+// Half-warp per row: lane j of the half handles entries row_ptr[i] + j, + 16, ... The contributions of an
+// entry (its slice of the inverse map, ascending element) are loaded ASM_UNR at a time before their w_T
+// gathers, and summed in that order. VIEWS = false (the hot path) writes the operators the solver and the
+// projection read: the sliced-ELL copies of A and H, diag(A) and 1 / diag(A). VIEWS = true writes the CSR
+// value arrays M_V, H, A behind ks_values / ks_spmm (materialised on demand, same arithmetic).
+constexpr int ASM_UNR = 8;
+template <bool VIEWS>
 __global__ void __launch_bounds__(256) k_assemble_rows(
     const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col, const int32_t *__restrict__ inv_ptr,
     const int32_t *__restrict__ inv_idx, const double *__restrict__ w, const double *__restrict__ v_free,
@@ -46,28 +52,41 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
   if (row >= n_free) return;
   const double vi = __ldg(v_free + row);
   const int32_t kr = __ldg(row_ptr + row), k1 = __ldg(row_ptr + row + 1);
-  const int64_t sbase = __ldg(sell_ptr + row / KS_SELL_C) + (row % KS_SELL_C) * 4;
-  for (int32_t e = __ldg(row_ptr + row) + j; e < k1; e += 16) {
+  const int64_t sbase = VIEWS ? 0 : __ldg(sell_ptr + row / KS_SELL_C) + (row % KS_SELL_C) * 4;
+  for (int32_t e = kr + j; e < k1; e += 16) {
     const int32_t c = __ldg(col + e);
+    const double m = __ldg(M + e), kk = __ldg(K + e), vc = __ldg(v_free + c);
+    const int32_t q0 = __ldg(inv_ptr + e), q1 = __ldg(inv_ptr + e + 1);
     double s = 0.0;
-    const int32_t q1 = __ldg(inv_ptr + e + 1);
-    for (int32_t q = __ldg(inv_ptr + e); q < q1; q++) s += __ldg(w + (__ldg(inv_idx + q) >> 4));
-    const double m = __ldg(M + e);
+    for (int32_t qb = q0; qb < q1; qb += ASM_UNR) {
+      int32_t t[ASM_UNR];
+#pragma unroll
+      for (int u = 0; u < ASM_UNR; u++) t[u] = qb + u < q1 ? (__ldg(inv_idx + qb + u) >> 4) : -1;
+      double wt[ASM_UNR];
+#pragma unroll
+      for (int u = 0; u < ASM_UNR; u++) wt[u] = t[u] >= 0 ? __ldg(w + t[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < ASM_UNR; u++)
+        if (t[u] >= 0) s += wt[u];
+    }
     double mv;
     if (c == row) mv = vi * m / 3.0 + s / 60.0;
-    else mv = (vi + __ldg(v_free + c)) * m / 6.0 + s / 120.0;
-    const double h = 0.5 * __ldg(K + e) + mv;
+    else mv = (vi + vc) * m / 6.0 + s / 120.0;
+    const double h = 0.5 * kk + mv;
     const double a = h + mu * m;
-    MV[e] = mv;
-    H[e] = h;
-    A[e] = a;
-    const int k = e - kr;   // slot of the entry in the sliced-ELL copy (ks_sell.cu)
-    const int64_t sp = sbase + (k >> 2) * (4 * KS_SELL_C) + (k & 3);
-    sell_A[sp] = a;
-    sell_H[sp] = h;
-    if (c == row) {
-      diag[row] = a;
-      dinv[row] = 1.0 / a;
+    if (VIEWS) {
+      MV[e] = mv;
+      H[e] = h;
+      A[e] = a;
+    } else {
+      const int k = e - kr;   // slot of the entry in the sliced-ELL copy (ks_sell.cu)
+      const int64_t sp = sbase + (k >> 2) * (4 * KS_SELL_C) + (k & 3);
+      sell_A[sp] = a;
+      sell_H[sp] = h;
+      if (c == row) {
+        diag[row] = a;
+        dinv[row] = 1.0 / a;
+      }
     }
   }
 }
@@ -80,11 +99,23 @@ ks_status ks_assemble_impl(ks_ctx *ctx, const double *d_veff, double mu) {
   k_tet_weights<<<ks_blocks(n, 256), 256, 0, s>>>(ctx->tets, ctx->vol, d_veff, ctx->n_tets, ctx->node_of_free,
                                                   ctx->n_free, ctx->w_tet, ctx->v_free, ctx->d_flags);
   KS_LAUNCHED(ctx);
-  k_assemble_rows<<<ks_blocks(16 * ctx->n_free, 256), 256, 0, s>>>(
+  k_assemble_rows<false><<<ks_blocks(16 * ctx->n_free, 256), 256, 0, s>>>(
       ctx->row_ptr, ctx->col, ctx->inv_ptr, ctx->inv_idx, ctx->w_tet, ctx->v_free, ctx->K, ctx->M, mu,
-      ctx->n_free, ctx->MV, ctx->H, ctx->A, ctx->diag, ctx->dinv, ctx->sell_ptr, ctx->sell_A, ctx->sell_H);
+      ctx->n_free, nullptr, nullptr, nullptr, ctx->diag, ctx->dinv, ctx->sell_ptr, ctx->sell_A, ctx->sell_H);
   KS_LAUNCHED(ctx);
+  ctx->views_fresh = false;
   ctx->mu = mu;
   ctx->assembled = true;
+  return KS_OK;
+}
+
+// CSR value views (M_V, H, A) of the last assembly, recomputed from the kept per-tet weights and nodal V
+ks_status ks_materialize_views(ks_ctx *ctx) {
+  if (!ctx->assembled || ctx->views_fresh) return KS_OK;
+  k_assemble_rows<true><<<ks_blocks(16 * ctx->n_free, 256), 256, 0, ctx->stream>>>(
+      ctx->row_ptr, ctx->col, ctx->inv_ptr, ctx->inv_idx, ctx->w_tet, ctx->v_free, ctx->K, ctx->M, ctx->mu,
+      ctx->n_free, ctx->MV, ctx->H, ctx->A, nullptr, nullptr, nullptr, nullptr, nullptr);
+  KS_LAUNCHED(ctx);
+  ctx->views_fresh = true;
   return KS_OK;
 }

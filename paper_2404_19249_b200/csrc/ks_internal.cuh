@@ -49,6 +49,7 @@ struct ks_ctx {
   double *v_free = nullptr;         // [n_free] V at free nodes (assembly scratch)
   double mu = 0.0;
   bool assembled = false;
+  bool views_fresh = false;         // CSR views MV, H, A match the last assembly (ks_materialize_views)
 
   // device status
   unsigned *d_flags = nullptr;      // latched KSF_* bits
@@ -152,6 +153,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 ks_status ks_setup_mesh(ks_ctx *ctx, const double *h_xyz, const int32_t *h_tets, const uint8_t *h_dir);
 ks_status ks_sell_build(ks_ctx *ctx);
 ks_status ks_assemble_impl(ks_ctx *ctx, const double *d_veff, double mu);
+ks_status ks_materialize_views(ks_ctx *ctx);
 ks_status ks_spmm_impl(ks_ctx *ctx, ks_op op, const double *val, int N, const double *X, double *Y);
 ks_status ks_solve_impl(ks_ctx *ctx, int N, const double *lambda, const double *U, double *Ut, double tol,
                         int max_iter, int32_t *iters, double *relres);

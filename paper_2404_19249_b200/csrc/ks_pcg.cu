@@ -612,6 +612,7 @@ ks_status ks_true_residual_impl(ks_ctx *ctx, int N, const double *lambda, const 
   const int nblk = ks_blocks(total, T);
   double *part = nullptr;
   KS_CUDA(ctx, cudaMallocAsync((void **)&part, sizeof(double) * 2 * N * (size_t)nblk, ctx->stream));
+  KS_TRY(ks_materialize_views(ctx));
   k_true_residual<<<nblk, T, 2 * T * sizeof(double), ctx->stream>>>(ctx->row_ptr, ctx->col, ctx->A, ctx->M, lambda,
                                                                      ctx->mu, U, Ut, ctx->n_free, N, part);
   KS_LAUNCHED(ctx);

@@ -253,13 +253,15 @@ constexpr int PA_UNR = 4;        // nonzeros of a row in flight per lane
 
 template <int LT>
 __device__ __forceinline__ void proj_a_row(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                                           const double *__restrict__ val, const uint16_t *__restrict__ lidx,
+                                           const int32_t *__restrict__ sell_ptr, const double *__restrict__ sval,
+                                           const uint16_t *__restrict__ lidx,
                                            const uint8_t *__restrict__ lslot, const double *__restrict__ Pv4,
                                            int32_t i, double *Wl) {
   double W[LT];
 #pragma unroll
   for (int m = 0; m < LT; m++) W[m] = 0.0;
   const int32_t k0 = __ldg(row_ptr + i), k1 = __ldg(row_ptr + i + 1);
+  const int64_t sb = __ldg(sell_ptr + i / KS_SELL_C) + (i % KS_SELL_C) * 4;   // the row in the SELL copy
   for (int32_t kb = k0; kb < k1; kb += PA_UNR) {
     int32_t j[PA_UNR];
     double h[PA_UNR];
@@ -267,9 +269,9 @@ __device__ __forceinline__ void proj_a_row(const int32_t *__restrict__ row_ptr, 
 #pragma unroll
     for (int u = 0; u < PA_UNR; u++) {
       const bool in = kb + u < k1;
-      const int32_t k = in ? kb + u : k0;
+      const int32_t k = in ? kb + u : k0, sl = k - k0;
       j[u] = __ldg(col + k);
-      h[u] = in ? __ldg(val + k) : 0.0;
+      h[u] = in ? __ldg(sval + sb + (sl >> 2) * (4 * KS_SELL_C) + (sl & 3)) : 0.0;
       li[u] = in ? __ldg(lidx + k) : 0xFFFFu;
     }
     double q[PA_UNR][4];
@@ -298,7 +300,8 @@ __device__ __forceinline__ void proj_a_row(const int32_t *__restrict__ row_ptr, 
 template <int ND>                // window slots per lane in phase 2: ND * 32 >= wcap
 __global__ void __launch_bounds__(PA_WARPS * 32) k_proj_a(const int32_t *__restrict__ row_ptr,
                                                           const int32_t *__restrict__ col,
-                                                          const double *__restrict__ val,
+                                                          const int32_t *__restrict__ sell_ptr,
+                                                          const double *__restrict__ sval,
                                                           const uint16_t *__restrict__ lidx,
                                                           const uint8_t *__restrict__ lslot,
                                                           const uint8_t *__restrict__ item_tier,
@@ -332,9 +335,9 @@ __global__ void __launch_bounds__(PA_WARPS * 32) k_proj_a(const int32_t *__restr
         double pi0, pi1, pi2, pi3;
         ldnc_v4(Pv4 + 4 * (int64_t)i, pi0, pi1, pi2, pi3);
         Ps[lane * 4 + 0] = pi0; Ps[lane * 4 + 1] = pi1; Ps[lane * 4 + 2] = pi2; Ps[lane * 4 + 3] = pi3;
-        if (tier <= 4) proj_a_row<4>(row_ptr, col, val, lidx, lslot, Pv4, i, Wl);
-        else if (tier <= 8) proj_a_row<8>(row_ptr, col, val, lidx, lslot, Pv4, i, Wl);
-        else proj_a_row<16>(row_ptr, col, val, lidx, lslot, Pv4, i, Wl);
+        if (tier <= 4) proj_a_row<4>(row_ptr, col, sell_ptr, sval, lidx, lslot, Pv4, i, Wl);
+        else if (tier <= 8) proj_a_row<8>(row_ptr, col, sell_ptr, sval, lidx, lslot, Pv4, i, Wl);
+        else proj_a_row<16>(row_ptr, col, sell_ptr, sval, lidx, lslot, Pv4, i, Wl);
       }
       __syncwarp();
       // ---- phase 2: lane = window slot ----
@@ -752,14 +755,14 @@ __global__ void k_item_order(const int32_t *__restrict__ perm, const double *__r
   for (int t = 0; t < 4; t++) Pv4p[4 * pos + t] = Pv4[4 * (int64_t)i + t];
 }
 
-ks_status launch_proj_a(ks_ctx *ctx, const double *op_vals) {
+ks_status launch_proj_a(ks_ctx *ctx, const double *op_sell_vals) {   // Op in the sliced-ELL layout
   const int wcap = (ctx->d_max + 31) / 32 * 32;
   if (wcap > 256) return ks_fail(ctx, KS_E_ARG, "coarse window %d > 256", ctx->d_max);
   const size_t sm = sizeof(double) * (size_t)PA_WARPS * 32 * (wcap + 1 + 4);
   auto kern = wcap <= 32 ? k_proj_a<1> : wcap <= 64 ? k_proj_a<2> : k_proj_a<8>;
   KS_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   kern<<<proj_grid(ctx, ctx->n_items, PA_WARPS), PA_WARPS * 32, sm, ctx->stream>>>(
-      ctx->row_ptr, ctx->col, op_vals, ctx->lidx, ctx->lslot, ctx->item_tier, ctx->Pv4, ctx->perm, ctx->item_ptr,
+      ctx->row_ptr, ctx->col, ctx->sell_ptr, op_sell_vals, ctx->lidx, ctx->lslot, ctx->item_tier, ctx->Pv4, ctx->perm, ctx->item_ptr,
       ctx->item_D_ptr, ctx->n_items, wcap, ctx->AH_part);
   KS_LAUNCHED(ctx);
   return KS_OK;
@@ -1038,7 +1041,7 @@ ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, cons
   KS_TRY(ks_alloc_t(ctx, &ctx->AH_part, 4 * ctx->d_total, "AH_part"));
   KS_TRY(ks_alloc_t(ctx, &ctx->B_H, n_H * n_H, "B_H"));
   ctx->n_H = n_H;
-  KS_TRY(launch_proj_a(ctx, ctx->M));
+  KS_TRY(launch_proj_a(ctx, ctx->sell_M));
   KS_TRY(launch_final<false>(ctx, 0, 16, ctx->B_H, nullptr, n_H, 0));
   KS_CUDA(ctx, cudaStreamSynchronize(s));
   return KS_OK;
@@ -1082,7 +1085,7 @@ ks_status ks_project_impl(ks_ctx *ctx, int N, const double *Ut, double *FA, doub
     default: return ks_fail(ctx, KS_E_ARG, "N = %d unsupported", N);
   }
   // K8b: A_H item partials (unshifted H, reading Q1)
-  KS_TRY(launch_proj_a(ctx, ctx->H));
+  KS_TRY(launch_proj_a(ctx, ctx->sell_H));
   // K9: A_H, b_H, c_H
   KS_TRY(launch_final<true>(ctx, N, np, FA, FB, D, D));
   k_copy_block<<<ks_blocks(nH * nH, 256), 256, 0, s>>>(ctx->B_H, nH, FB, D);
