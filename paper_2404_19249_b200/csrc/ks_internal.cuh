@@ -81,9 +81,6 @@ struct ks_ctx {
   int32_t *item_D_ptr = nullptr; // [n_items+1]
   int32_t *item_D = nullptr;     // [d_total] sorted coarse ids touched by P rows of the item's neighbours
   uint8_t *slotmap = nullptr;    // [4 nnz] slot of (entry k, parent t of col[k]) in its row's item D list
-  uint8_t *lslot = nullptr;      // [16 n_free] a row's local window: its distinct item-window slots (255 pad)
-  uint16_t *lidx = nullptr;      // [nnz] local index of each parent t of col[k] (4 bits each, 15 = none)
-  uint8_t *item_tier = nullptr;  // [n_items] largest local window of the item's rows
   int32_t *CT_ptr = nullptr;     // [n_H+1] coarse node -> (item, local parent) list
   int32_t *CT_val = nullptr;     // [4 n_items] entries 4 item + q
   double *B_H = nullptr;         // [n_H n_H] cached P^T M P

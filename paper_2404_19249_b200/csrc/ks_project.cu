@@ -239,181 +239,93 @@ __global__ void __launch_bounds__(256) k_proj_y(const int32_t *__restrict__ sell
   ym.st(YMp + o);
 }
 
-// Item partials of P^T Op P (A_H with Op = H, B_H with Op = M). One warp per item, in two phases per chunk
-// of 32 rows of the item (perm order):
-//   1. lane = row i: W_i over the row's LOCAL window (its <= 16 distinct item-window slots, precomputed in
-//      ks_set_coarse: lslot, and per nonzero the local index of each parent t: lidx, 4 bits each), in
-//      registers: W[m] += [l == m] Op_k P_{j_k, t} (branch-free, no shared-memory read-modify-write
-//      chains), then scattered once into the lane's row of a shared [32][wcap + 1] array;
-//   2. lane = window slot d: G[c][d] += P_ic W_i[d] over the chunk's rows in order (registers).
-// The register tier LT (4, 8 or 16 local slots) is chosen per item (max over its rows, warp-uniform).
-// No float atomics; the partition and all orders are fixed.
-constexpr int PA_WARPS = 4;      // warps per block of k_proj_a
-constexpr int PA_UNR = 4;        // nonzeros of a row in flight per lane
+// Item partials of P^T Op P (A_H with Op = H, B_H with Op = M), G[c][d] = sum_{i in item} P_ic (Op P)_{i,d}
+// for the item's parents c and window slots d. No float atomics; the partition and all orders are fixed.
+constexpr int PA_UNR = 4;        // nonzeros of a row in flight per thread
 
-template <int LT>
-__device__ __forceinline__ void proj_a_row(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                                           const int32_t *__restrict__ sell_ptr, const double *__restrict__ sval,
-                                           const uint16_t *__restrict__ lidx,
-                                           const uint8_t *__restrict__ lslot, const double *__restrict__ Pv4,
-                                           int32_t i, double *Wl) {
-  double W[LT];
-#pragma unroll
-  for (int m = 0; m < LT; m++) W[m] = 0.0;
+// Row part: the row's contributions are added in place in its shared row of the item window. The 4 parents of one nonzero have distinct slots (distinct coarse nodes), so their 4
+// read-modify-writes are issued together (one shared-memory latency per nonzero); absent parents write
+// the pad column wcap. Nonzeros in CSR order, parents ascending: fixed order.
+__device__ __forceinline__ void proj_a_row_smem(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                                                const int32_t *__restrict__ sell_ptr, const double *__restrict__ sval,
+                                                const uint8_t *__restrict__ slotmap, const double *__restrict__ Pv4,
+                                                int32_t i, double *Wl, int wcap) {
   const int32_t k0 = __ldg(row_ptr + i), k1 = __ldg(row_ptr + i + 1);
-  const int64_t sb = __ldg(sell_ptr + i / KS_SELL_C) + (i % KS_SELL_C) * 4;   // the row in the SELL copy
+  const int64_t sb = __ldg(sell_ptr + i / KS_SELL_C) + (i % KS_SELL_C) * 4;
   for (int32_t kb = k0; kb < k1; kb += PA_UNR) {
     int32_t j[PA_UNR];
     double h[PA_UNR];
-    unsigned li[PA_UNR];
+    uchar4 sl[PA_UNR];
 #pragma unroll
     for (int u = 0; u < PA_UNR; u++) {
       const bool in = kb + u < k1;
-      const int32_t k = in ? kb + u : k0, sl = k - k0;
+      const int32_t k = in ? kb + u : k0, kl = k - k0;
       j[u] = __ldg(col + k);
-      h[u] = in ? __ldg(sval + sb + (sl >> 2) * (4 * KS_SELL_C) + (sl & 3)) : 0.0;
-      li[u] = in ? __ldg(lidx + k) : 0xFFFFu;
+      h[u] = in ? __ldg(sval + sb + (kl >> 2) * (4 * KS_SELL_C) + (kl & 3)) : 0.0;
+      sl[u] = in ? __ldg(reinterpret_cast<const uchar4 *>(slotmap) + k) : make_uchar4(255, 255, 255, 255);
     }
     double q[PA_UNR][4];
 #pragma unroll
     for (int u = 0; u < PA_UNR; u++) ldnc_v4(Pv4 + 4 * (int64_t)j[u], q[u][0], q[u][1], q[u][2], q[u][3]);
 #pragma unroll
-    for (int u = 0; u < PA_UNR; u++)
-#pragma unroll
-      for (int t = 0; t < 4; t++) {
-        const unsigned l = (li[u] >> (4 * t)) & 15u;
-        const double v = h[u] * q[u][t];
-#pragma unroll
-        for (int m = 0; m < LT; m++) W[m] += (l == (unsigned)m) ? v : 0.0;
-      }
-  }
-  // scatter the local window into the lane's row of the item window
-  const uint4 ls = __ldg(reinterpret_cast<const uint4 *>(lslot) + i);
-  const unsigned lw[4] = {ls.x, ls.y, ls.z, ls.w};
-#pragma unroll
-  for (int m = 0; m < LT; m++) {
-    const unsigned d = (lw[m >> 2] >> (8 * (m & 3))) & 255u;
-    if (d != 255u) Wl[d] = W[m];
+    for (int u = 0; u < PA_UNR; u++) {
+      const int s0 = sl[u].x == 255 ? wcap : sl[u].x, s1 = sl[u].y == 255 ? wcap : sl[u].y;
+      const int s2 = sl[u].z == 255 ? wcap : sl[u].z, s3 = sl[u].w == 255 ? wcap : sl[u].w;
+      const double w0 = Wl[s0], w1 = Wl[s1], w2 = Wl[s2], w3 = Wl[s3];
+      Wl[s0] = fma(h[u], q[u][0], w0);
+      Wl[s1] = fma(h[u], q[u][1], w1);
+      Wl[s2] = fma(h[u], q[u][2], w2);
+      Wl[s3] = fma(h[u], q[u][3], w3);
+    }
   }
 }
 
-template <int ND>                // window slots per lane in phase 2: ND * 32 >= wcap
-__global__ void __launch_bounds__(PA_WARPS * 32) k_proj_a(const int32_t *__restrict__ row_ptr,
-                                                          const int32_t *__restrict__ col,
-                                                          const int32_t *__restrict__ sell_ptr,
-                                                          const double *__restrict__ sval,
-                                                          const uint16_t *__restrict__ lidx,
-                                                          const uint8_t *__restrict__ lslot,
-                                                          const uint8_t *__restrict__ item_tier,
-                                                          const double *__restrict__ Pv4,
-                                                          const int32_t *__restrict__ perm,
-                                                          const int32_t *__restrict__ item_ptr,
-                                                          const int32_t *__restrict__ D_ptr, int64_t n_items, int wcap,
-                                                          double *__restrict__ AH_part) {
+// One block of ITEM_ROWS threads per item (all of its rows at once):
+//   1. thread = row r of the item: its row W[r][0..dn) of the item window (proj_a_row_smem), and P_r;
+//   2. thread = output (c, d): G[c][d] = sum_r P_rc W[r][d], r ascending (fixed order).
+__global__ void __launch_bounds__(ITEM_ROWS) k_proj_a(const int32_t *__restrict__ row_ptr,
+                                                     const int32_t *__restrict__ col,
+                                                     const int32_t *__restrict__ sell_ptr,
+                                                     const double *__restrict__ sval,
+                                                     const uint8_t *__restrict__ slotmap,
+                                                     const double *__restrict__ Pv4,
+                                                     const int32_t *__restrict__ perm,
+                                                     const int32_t *__restrict__ item_ptr,
+                                                     const int32_t *__restrict__ D_ptr, int64_t n_items, int wcap,
+                                                     double *__restrict__ AH_part) {
   extern __shared__ double smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int ws = wcap + 1;                                   // odd row stride: conflict-free column reads
-  double *W = smem + (int64_t)warp * 32 * (ws + 4);          // [32][ws] window rows, then [32][4] P rows
-  double *Ps = W + 32 * ws;
-  double *Wl = W + lane * ws;
-  const int64_t gw = (int64_t)blockIdx.x * PA_WARPS + warp, nw = (int64_t)gridDim.x * PA_WARPS;
-  for (int64_t it = gw; it < n_items; it += nw) {
+  const int ws = wcap + 1;                       // odd row stride; column wcap is the pad (absent parents)
+  double *W = smem;                              // [ITEM_ROWS][ws]
+  double *Ps = smem + ITEM_ROWS * ws;            // [ITEM_ROWS][4]
+  const int tid = threadIdx.x;
+  for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
     const int32_t p0 = __ldg(item_ptr + it), p1 = __ldg(item_ptr + it + 1);
     const int32_t d0 = __ldg(D_ptr + it), dn = __ldg(D_ptr + it + 1) - d0;
-    const int tier = __ldg(item_tier + it);
-    double G[ND][4];
-#pragma unroll
-    for (int q = 0; q < ND; q++)
-#pragma unroll
-      for (int c = 0; c < 4; c++) G[q][c] = 0.0;
-    for (int32_t cb = p0; cb < p1; cb += 32) {
-      const int nr = min(32, p1 - cb);
-      // ---- phase 1: lane = row ----
-      for (int d = 0; d < dn; d++) Wl[d] = 0.0;
-      if (lane < nr) {
-        const int32_t i = __ldg(perm + cb + lane);
-        double pi0, pi1, pi2, pi3;
-        ldnc_v4(Pv4 + 4 * (int64_t)i, pi0, pi1, pi2, pi3);
-        Ps[lane * 4 + 0] = pi0; Ps[lane * 4 + 1] = pi1; Ps[lane * 4 + 2] = pi2; Ps[lane * 4 + 3] = pi3;
-        if (tier <= 4) proj_a_row<4>(row_ptr, col, sell_ptr, sval, lidx, lslot, Pv4, i, Wl);
-        else if (tier <= 8) proj_a_row<8>(row_ptr, col, sell_ptr, sval, lidx, lslot, Pv4, i, Wl);
-        else proj_a_row<16>(row_ptr, col, sell_ptr, sval, lidx, lslot, Pv4, i, Wl);
-      }
-      __syncwarp();
-      // ---- phase 2: lane = window slot ----
-#pragma unroll
-      for (int q = 0; q < ND; q++) {
-        const int d = lane + 32 * q;
-        if (d < dn) {
-          for (int r = 0; r < nr; r++) {
-            const double w = W[r * ws + d];
-#pragma unroll
-            for (int c = 0; c < 4; c++) G[q][c] = fma(Ps[r * 4 + c], w, G[q][c]);
-          }
-        }
-      }
-      __syncwarp();
+    const int nr = p1 - p0;
+    double *Wl = W + tid * ws;
+    for (int d = 0; d < dn; d++) Wl[d] = 0.0;
+    if (tid < nr) {
+      const int32_t i = __ldg(perm + p0 + tid);
+      double pi0, pi1, pi2, pi3;
+      ldnc_v4(Pv4 + 4 * (int64_t)i, pi0, pi1, pi2, pi3);
+      Ps[tid * 4 + 0] = pi0; Ps[tid * 4 + 1] = pi1; Ps[tid * 4 + 2] = pi2; Ps[tid * 4 + 3] = pi3;
+      proj_a_row_smem(row_ptr, col, sell_ptr, sval, slotmap, Pv4, i, Wl, wcap);
     }
+    __syncthreads();
     double *out = AH_part + 4 * (int64_t)d0;
+    for (int x = tid; x < 4 * dn; x += ITEM_ROWS) {
+      const int c = x / dn, d = x % dn;
+      // four interleaved partial sums (rows r = 4m + q), combined in q order: fixed order, 4x the ILP
+      double g[4] = {0.0, 0.0, 0.0, 0.0};
+      int r = 0;
+      for (; r + 4 <= nr; r += 4)
 #pragma unroll
-    for (int q = 0; q < ND; q++) {
-      const int d = lane + 32 * q;
-      if (d < dn)
-#pragma unroll
-        for (int c = 0; c < 4; c++) out[c * dn + d] = G[q][c];
+        for (int q = 0; q < 4; q++) g[q] = fma(Ps[(r + q) * 4 + c], W[(r + q) * ws + d], g[q]);
+      for (int q = 0; r + q < nr; q++) g[q] = fma(Ps[(r + q) * 4 + c], W[(r + q) * ws + d], g[q]);
+      out[x] = (g[0] + g[1]) + (g[2] + g[3]);
     }
+    __syncthreads();
   }
-}
-
-// Setup (ks_set_coarse): per row, its local window (sorted distinct item-window slots of its nonzeros'
-// parents, <= 16; 255-padded) and per nonzero the local index of each parent t (4 bits, 15 = none).
-// Returns the row's local window size in lsize.
-__global__ void k_local_windows(const int32_t *__restrict__ row_ptr, const uint8_t *__restrict__ slotmap,
-                                int64_t n, uint8_t *__restrict__ lslot, uint16_t *__restrict__ lidx,
-                                uint8_t *__restrict__ lsize, unsigned *__restrict__ overflow) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  uint8_t L[16];
-  int nl = 0;
-  bool over = false;
-  const int32_t k0 = row_ptr[i], k1 = row_ptr[i + 1];
-  for (int32_t k = k0; k < k1; k++)
-    for (int t = 0; t < 4; t++) {
-      const uint8_t s = slotmap[4 * (int64_t)k + t];
-      if (s == 255) continue;
-      int pos = 0;
-      while (pos < nl && L[pos] < s) pos++;
-      if (pos < nl && L[pos] == s) continue;
-      if (nl == 16) { over = true; continue; }
-      for (int m = nl; m > pos; m--) L[m] = L[m - 1];
-      L[pos] = s;
-      nl++;
-    }
-  if (over) atomicOr(overflow, 1u);
-  for (int m = 0; m < 16; m++) lslot[16 * i + m] = m < nl ? L[m] : 255;
-  lsize[i] = (uint8_t)nl;
-  for (int32_t k = k0; k < k1; k++) {
-    unsigned code = 0;
-    for (int t = 0; t < 4; t++) {
-      const uint8_t s = slotmap[4 * (int64_t)k + t];
-      unsigned l = 15;
-      if (s != 255)
-        for (int m = 0; m < nl; m++)
-          if (L[m] == s) l = m;
-      code |= l << (4 * t);
-    }
-    lidx[k] = (uint16_t)code;
-  }
-}
-
-// per item: the largest local window of its rows (register tier of k_proj_a)
-__global__ void k_item_tier(const int32_t *__restrict__ item_ptr, const int32_t *__restrict__ perm,
-                            const uint8_t *__restrict__ lsize, int64_t n_items, uint8_t *__restrict__ tier) {
-  const int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (it >= n_items) return;
-  int m = 0;
-  for (int32_t pos = item_ptr[it]; pos < item_ptr[it + 1]; pos++) m = max(m, (int)lsize[perm[pos]]);
-  tier[it] = (uint8_t)m;
 }
 
 // Item pass (item order: Up, YHp, YMp, Pv4p are stored by position, so every item's rows are contiguous):
@@ -421,11 +333,11 @@ __global__ void k_item_tier(const int32_t *__restrict__ item_ptr, const int32_t 
 // its rows through a 2-stage shared-memory ring with bulk (TMA) copies, lane 0 producing, all lanes
 // consuming. Gram: 4x4 register tiles (op, ta, tb), ta <= tb (the blocks are symmetric), lane l owns tiles
 // l, l + 32, ...; b/c: lane l owns (op, c) = l / 4 and the orbitals b of quarter l % 4.
-constexpr int PBG_WARPS = 4;     // warps per block of k_proj_bg
+constexpr int PBG_WARPS = 8;     // warps per block of k_proj_bg
 constexpr int PBG_STAGES = 2;
 template <int NP>
 struct PbgLayout {
-  static constexpr int CH = NP <= 16 ? 32 : NP == 32 ? 16 : 8;          // rows per stage
+  static constexpr int CH = NP <= 16 ? 16 : NP == 32 ? 8 : 4;           // rows per stage
   static constexpr int STAGE = CH * (3 * NP + 4);                        // doubles per stage
   static constexpr size_t WARP_BYTES = sizeof(double) * PBG_STAGES * STAGE;
 };
@@ -756,13 +668,16 @@ __global__ void k_item_order(const int32_t *__restrict__ perm, const double *__r
 }
 
 ks_status launch_proj_a(ks_ctx *ctx, const double *op_sell_vals) {   // Op in the sliced-ELL layout
-  const int wcap = (ctx->d_max + 31) / 32 * 32;
-  if (wcap > 256) return ks_fail(ctx, KS_E_ARG, "coarse window %d > 256", ctx->d_max);
-  const size_t sm = sizeof(double) * (size_t)PA_WARPS * 32 * (wcap + 1 + 4);
-  auto kern = wcap <= 32 ? k_proj_a<1> : wcap <= 64 ? k_proj_a<2> : k_proj_a<8>;
-  KS_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  kern<<<proj_grid(ctx, ctx->n_items, PA_WARPS), PA_WARPS * 32, sm, ctx->stream>>>(
-      ctx->row_ptr, ctx->col, ctx->sell_ptr, op_sell_vals, ctx->lidx, ctx->lslot, ctx->item_tier, ctx->Pv4, ctx->perm, ctx->item_ptr,
+  const int wcap = ctx->d_max;
+  const size_t sm = sizeof(double) * (size_t)ITEM_ROWS * (wcap + 1 + 4);
+  if (sm > 200 * 1024) return ks_fail(ctx, KS_E_ARG, "coarse window %d too large", ctx->d_max);
+  KS_CUDA(ctx, cudaFuncSetAttribute(k_proj_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  int per_sm = 0;
+  KS_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_proj_a, ITEM_ROWS, sm));
+  int64_t grid = (int64_t)(per_sm > 0 ? per_sm : 1) * ctx->sm_count * 4;
+  if (grid > ctx->n_items) grid = ctx->n_items;
+  k_proj_a<<<(unsigned)(grid > 0 ? grid : 1), ITEM_ROWS, sm, ctx->stream>>>(
+      ctx->row_ptr, ctx->col, ctx->sell_ptr, op_sell_vals, ctx->slotmap, ctx->Pv4, ctx->perm, ctx->item_ptr,
       ctx->item_D_ptr, ctx->n_items, wcap, ctx->AH_part);
   KS_LAUNCHED(ctx);
   return KS_OK;
@@ -849,7 +764,7 @@ struct TmpGuard {
 
 void ks_free_coarse(ks_ctx *ctx) {
   void *ptrs[] = {ctx->P_ptr, ctx->P_col, ctx->P_val, ctx->Pv4, ctx->Pv4p, ctx->pos_of_row, ctx->perm,
-                  ctx->lslot, ctx->lidx, ctx->item_tier,
+
                   ctx->item_ptr, ctx->item_S, ctx->item_D_ptr, ctx->item_D, ctx->slotmap, ctx->CT_ptr,
                   ctx->CT_val, ctx->B_H, ctx->AH_part};
   for (void *p : ptrs) ks_free(ctx, p);
@@ -857,8 +772,7 @@ void ks_free_coarse(ks_ctx *ctx) {
   ctx->P_val = ctx->Pv4 = ctx->Pv4p = nullptr;
   ctx->pos_of_row = nullptr;
   ctx->perm = ctx->item_ptr = ctx->item_S = ctx->item_D_ptr = ctx->item_D = ctx->CT_ptr = ctx->CT_val = nullptr;
-  ctx->slotmap = ctx->lslot = ctx->item_tier = nullptr;
-  ctx->lidx = nullptr;
+  ctx->slotmap = nullptr;
   ctx->B_H = ctx->AH_part = nullptr;
   ctx->n_H = 0;
 }
@@ -1000,27 +914,7 @@ ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, cons
   k_slotmap<<<ks_blocks(nf, 128), 128, 0, s>>>(ctx->perm, item_of_pos, ctx->item_D_ptr, ctx->item_D, ctx->row_ptr,
                                                ctx->col, ctx->P_ptr, ctx->P_col, nf, ctx->slotmap);
   KS_LAUNCHED(ctx);
-  // local windows of the rows and register tiers of the items (k_proj_a)
-  {
-    uint8_t *lsize;
-    unsigned *over;
-    TMPA(lsize, nf);
-    TMPA(over, 1);
-    KS_CUDA(ctx, cudaMemsetAsync(over, 0, sizeof(unsigned), s));
-    KS_TRY(ks_alloc_t(ctx, &ctx->lslot, 16 * nf, "lslot"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->lidx, ctx->nnz, "lidx"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->item_tier, ni, "item_tier"));
-    k_local_windows<<<ks_blocks(nf, 128), 128, 0, s>>>(ctx->row_ptr, ctx->slotmap, nf, ctx->lslot, ctx->lidx, lsize,
-                                                       over);
-    KS_LAUNCHED(ctx);
-    k_item_tier<<<ks_blocks(ni, 128), 128, 0, s>>>(ctx->item_ptr, ctx->perm, lsize, ni, ctx->item_tier);
-    KS_LAUNCHED(ctx);
-    unsigned h_over = 0;
-    KS_CUDA(ctx, cudaMemcpyAsync(&h_over, over, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-    KS_CUDA(ctx, cudaStreamSynchronize(s));
-    if (h_over)
-      return ks_fail(ctx, KS_E_ARG, "a fine row touches more than 16 coarse nodes through its neighbours' P rows");
-  }
+
 
   // ---- coarse node -> items list (stable sort on the coarse id; pads sort last) ----
   int ct_bits = 1;
