@@ -55,6 +55,10 @@ def lib():
         L.or_block_pcg.argtypes = [vp, i32, vp, vp, vp, dbl, i32, vp, vp, vp]
         L.or_project.restype = i32
         L.or_project.argtypes = [vp, i64, vp, vp, vp, i32, vp, vp, vp]
+        L.or_pencil_eig.restype = i32
+        L.or_pencil_eig.argtypes = [i64, vp, vp, i32, vp, vp]
+        L.or_lift.restype = i32
+        L.or_lift.argtypes = [vp, i64, vp, vp, vp, i32, vp, i32, vp, vp]
         _lib = L
     return _lib
 
@@ -67,6 +71,36 @@ class OracleError(RuntimeError):
     def __init__(self, status, msg):
         super().__init__(f"oracle status {status}: {msg}")
         self.status = status
+
+
+def pencil_eig(FA, FB, k):
+    """Lowest k eigenpairs of F_A y = lambda F_B y (NEXT-1, oracle.c or_pencil_eig: Cholesky + cyclic
+    Jacobi). Returns (evals [k], evecs [D][k]); raises OracleError(OR_E_NOT_SPD) if F_B is not SPD."""
+    FA = np.ascontiguousarray(FA, dtype=np.float64)
+    FB = np.ascontiguousarray(FB, dtype=np.float64)
+    D = FA.shape[0]
+    ev = np.empty(k)
+    Y = np.empty((D, k))
+    st = lib().or_pencil_eig(D, _p(FA), _p(FB), int(k), _p(ev), _p(Y))
+    if st != OR_OK:
+        raise OracleError(st, "pencil_eig")
+    return ev, Y
+
+
+def augmented_step(mesh, n_H, P_rowptr, P_col, P_val, lam, U, tol=1e-10, max_iter=2000):
+    """One outer iteration of Algorithm 3 with a fixed potential, in the paper's order:
+    the N shifted BVPs (Aux_Linear_Problem) with the shift mu of the mesh's last
+    assemble_veff, the projection onto W = [P_H | U~] (st1-st7), the small eigenproblem
+    on W (Nonlinear_Eig_Hh) and the lift of its lowest N eigenvectors. Returns
+    (lambda_new [N], U_new [n_free][N], info)."""
+    N = U.shape[1]
+    r = mesh.block_pcg(lam, U, tol=tol, max_iter=max_iter)
+    if r["status"] != OR_OK:
+        raise OracleError(r["status"], "augmented_step: block_pcg")
+    FA, FB = mesh.project(n_H, P_rowptr, P_col, P_val, r["Ut"])
+    ev, Y = pencil_eig(FA, FB, N)
+    Unew = mesh.lift(n_H, P_rowptr, P_col, P_val, r["Ut"], Y)
+    return ev, Unew, dict(iters=r["iters"], FA=FA, FB=FB, Y=Y)
 
 
 class Mesh:
@@ -160,6 +194,20 @@ class Mesh:
         if st != OR_OK:
             raise OracleError(st, "project")
         return FA, FB
+
+    def lift(self, n_H, P_rowptr, P_col, P_val, Ut, Y):
+        """U_new = P Y[:n_H] + U~ Y[n_H:] (NEXT-1 lift, oracle.c or_lift)."""
+        Ut = np.ascontiguousarray(Ut, dtype=np.float64)
+        Y = np.ascontiguousarray(Y, dtype=np.float64)
+        N, k = Ut.shape[1], Y.shape[1]
+        Unew = np.empty((self.n_free, k))
+        pr = np.ascontiguousarray(P_rowptr, dtype=np.int32)
+        pc = np.ascontiguousarray(P_col, dtype=np.int32)
+        pv = np.ascontiguousarray(P_val, dtype=np.float64)
+        st = lib().or_lift(self._h, int(n_H), _p(pr), _p(pc), _p(pv), N, _p(Ut), k, _p(Y), _p(Unew))
+        if st != OR_OK:
+            raise OracleError(st, "lift")
+        return Unew
 
     def csr(self, which):
         """scipy CSR of one operator (for brute-force pins in tests)."""

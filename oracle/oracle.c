@@ -414,3 +414,124 @@ int or_project(const or_mesh *h, int64_t n_H, const int32_t *Pptr, const int32_t
   free(HU); free(MU);
   return OR_OK;
 }
+
+/*
+ * NEXT-1: the small eigenvalue problem of Algorithm 3 and the lift of its eigenvectors.
+ *
+ * or_pencil_eig: the generalized symmetric eigenproblem of (Nonlinear_Eig_Hh) restricted to W,
+ * F_A y = lambda F_B y, "a small-scale algebraic eigenvalue problem solved in
+ * serial". Textbook reduction: Cholesky F_B = L L^T (F_B must be SPD), C = L^-1 F_A L^-T,
+ * cyclic Jacobi rotations on C until every off-diagonal |c_pq| <= 1e-15 sqrt(|c_pp c_qq|) (or 100 sweeps),
+ * eigenvalues sorted ascending, eigenvectors y = L^-T z (then F_B-orthonormal). The lowest k are returned:
+ * evals [k], evecs [D][k] row-major (column j = eigenvector j).
+ * Returns OR_OK, OR_E_NOT_SPD when the Cholesky factorisation of F_B breaks down, OR_E_NOMEM.
+ */
+int or_pencil_eig(int64_t D, const double *FA, const double *FB, int k, double *evals, double *evecs) {
+  if (D < 1 || k < 1 || k > D) return OR_E_ARG;
+  double *L = (double *)calloc(D * D, sizeof(double));
+  double *C = (double *)calloc(D * D, sizeof(double));
+  double *Z = (double *)calloc(D * D, sizeof(double));
+  double *T = (double *)calloc(D * D, sizeof(double));
+  int64_t *ord = (int64_t *)calloc(D, sizeof(int64_t));
+  if (!L || !C || !Z || !T || !ord) { free(L); free(C); free(Z); free(T); free(ord); return OR_E_NOMEM; }
+  /* Cholesky (lower), F_B symmetric: use the lower triangle */
+  for (int64_t j = 0; j < D; j++) {
+    double s = FB[j * D + j];
+    for (int64_t m = 0; m < j; m++) s -= L[j * D + m] * L[j * D + m];
+    if (!(s > 0.0)) { free(L); free(C); free(Z); free(T); free(ord); return OR_E_NOT_SPD; }
+    L[j * D + j] = sqrt(s);
+    for (int64_t i = j + 1; i < D; i++) {
+      double t = FB[i * D + j];
+      for (int64_t m = 0; m < j; m++) t -= L[i * D + m] * L[j * D + m];
+      L[i * D + j] = t / L[j * D + j];
+    }
+  }
+  /* T = L^-1 F_A (forward substitution, column by column of F_A) */
+  for (int64_t c = 0; c < D; c++)
+    for (int64_t i = 0; i < D; i++) {
+      double t = FA[i * D + c];
+      for (int64_t m = 0; m < i; m++) t -= L[i * D + m] * T[m * D + c];
+      T[i * D + c] = t / L[i * D + i];
+    }
+  /* C = T L^-T, i.e. C^T = L^-1 T^T: row r of C solves L x = (row r of T)^T */
+  for (int64_t r = 0; r < D; r++)
+    for (int64_t i = 0; i < D; i++) {
+      double t = T[r * D + i];
+      for (int64_t m = 0; m < i; m++) t -= L[i * D + m] * C[r * D + m];
+      C[r * D + i] = t / L[i * D + i];
+    }
+  /* symmetrise (rounding) and run cyclic Jacobi: C = Z diag Z^T */
+  for (int64_t i = 0; i < D; i++)
+    for (int64_t j = i + 1; j < D; j++) {
+      double a = 0.5 * (C[i * D + j] + C[j * D + i]);
+      C[i * D + j] = C[j * D + i] = a;
+    }
+  for (int64_t i = 0; i < D; i++) Z[i * D + i] = 1.0;
+  for (int sweep = 0; sweep < 100; sweep++) {
+    int rotated = 0;
+    for (int64_t p = 0; p < D - 1; p++)
+      for (int64_t q = p + 1; q < D; q++) {
+        double apq = C[p * D + q], app = C[p * D + p], aqq = C[q * D + q];
+        if (fabs(apq) <= 1e-15 * sqrt(fabs(app * aqq)) || apq == 0.0) continue;
+        rotated = 1;
+        /* rotation angle: tan(2 theta) = 2 apq / (aqq - app), smaller root (Golub & Van Loan 8.5.2) */
+        double tau = (aqq - app) / (2.0 * apq);
+        double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+        double c = 1.0 / sqrt(1.0 + t * t), s = t * c;
+        for (int64_t r = 0; r < D; r++) {   /* columns p, q */
+          double crp = C[r * D + p], crq = C[r * D + q];
+          C[r * D + p] = c * crp - s * crq;
+          C[r * D + q] = s * crp + c * crq;
+        }
+        for (int64_t r = 0; r < D; r++) {   /* rows p, q */
+          double cpr = C[p * D + r], cqr = C[q * D + r];
+          C[p * D + r] = c * cpr - s * cqr;
+          C[q * D + r] = s * cpr + c * cqr;
+        }
+        C[p * D + q] = C[q * D + p] = 0.0;
+        for (int64_t r = 0; r < D; r++) {
+          double zrp = Z[r * D + p], zrq = Z[r * D + q];
+          Z[r * D + p] = c * zrp - s * zrq;
+          Z[r * D + q] = s * zrp + c * zrq;
+        }
+      }
+    if (!rotated) break;
+  }
+  /* ascending order (insertion sort of indices, ties by index) */
+  for (int64_t i = 0; i < D; i++) ord[i] = i;
+  for (int64_t i = 1; i < D; i++) {
+    int64_t x = ord[i], j = i;
+    while (j > 0 && C[ord[j - 1] * D + ord[j - 1]] > C[x * D + x]) { ord[j] = ord[j - 1]; j--; }
+    ord[j] = x;
+  }
+  /* y = L^-T z for the lowest k (back substitution with L^T) */
+  for (int j = 0; j < k; j++) {
+    int64_t e = ord[j];
+    evals[j] = C[e * D + e];
+    for (int64_t i = D - 1; i >= 0; i--) {
+      double t = Z[i * D + e];
+      for (int64_t m = i + 1; m < D; m++) t -= L[m * D + i] * evecs[m * k + j];
+      evecs[i * k + j] = t / L[i * D + i];
+    }
+  }
+  free(L); free(C); free(Z); free(T); free(ord);
+  return OR_OK;
+}
+
+/*
+ * or_lift: the new orbitals in W = [P_H | U~] (Algorithm 3: psi in S_H + span{psi~}):
+ *   U_new[i][j] = sum_c P_ic Y[c][j] + sum_m U~[i][m] Y[n_H + m][j],   Y [(n_H + N)][k] row-major.
+ * U_new [n_free][k].
+ */
+int or_lift(const or_mesh *h, int64_t n_H, const int32_t *Pptr, const int32_t *Pcol, const double *Pval, int N,
+            const double *Ut, int k, const double *Y, double *Unew) {
+  int64_t n = h->n_free;
+  for (int64_t i = 0; i < n; i++)
+    for (int j = 0; j < k; j++) {
+      double s = 0.0;
+      for (int32_t t = Pptr[i]; t < Pptr[i + 1]; t++) s += Pval[t] * Y[(int64_t)Pcol[t] * k + j];
+      for (int m = 0; m < N; m++) s += Ut[i * N + m] * Y[(n_H + m) * k + j];
+      Unew[i * k + j] = s;
+    }
+  return OR_OK;
+}
