@@ -154,6 +154,27 @@ def traced_phases(ctx, solve, n, nnz, N, peak):
     return out
 
 
+def next1_times(ctx, Ut, FA, FB, N, stream):
+    """NEXT-1 (not part of the timed step): the dense pencil eigensolve of the step's F_A, F_B (D = n_H + N,
+    cuSOLVER) and the lift U_new = P y_H + U~ y_t, each timed with CUDA events after one warm-up call."""
+    import torch
+    try:
+        out = {}
+        ev, Y = ctx.pencil_eig(FA, FB, N)
+        Un = ctx.lift(Ut, Y)
+        for name, fn in (("pencil_eig", lambda: ctx.pencil_eig(FA, FB, N)), ("lift", lambda: ctx.lift(Ut, Y, Un))):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            out[name] = a.elapsed_time(b)
+        out["D"] = int(FA.shape[0])
+        return out
+    except Exception as ex:  # reported, never fatal for the headline line
+        return {"error": str(ex)[:200]}
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -378,6 +399,7 @@ def run_ours(args, p, rank, world, local):
                      "alg_bytes_def": "init (20 nnz + 12 n + 32 N n) + k x textbook B_it (12 nnz + 20 n + 88 N n)"},
         "phases_ms": {"assemble_veff": t_asm, "block_solve": t_solve, "project_augmented": t_proj},
         "solve_only_value": N * n * k_last / (t_solve * 1e-3),
+        "next1_ms": next1_times(ctx, Ut, FA, FB, N, stream),
         "pcg_phases": traced_phases(ctx, lambda: ctx.block_solve(lam, U, Ut, tol=TOL, max_iter=MAX_ITER, iters=iters,
                                                                  relres=relres), n, nnz, N, peak),
         "gpu_launches": int(launches),

@@ -60,7 +60,8 @@ typedef enum {
   KS_E_NOT_CONVERGED = 5,  /* max_iter reached with some column above tolerance; last iterate written */
   KS_E_CUDA = 6,           /* CUDA runtime error (message has the CUDA error string) */
   KS_E_NOMEM = 7,          /* device allocation failed */
-  KS_E_STATE = 8           /* call order: e.g. solve before assemble, project before set_coarse */
+  KS_E_STATE = 8,          /* call order: e.g. solve before assemble, project before set_coarse */
+  KS_E_RANK = 9            /* F_B not positive definite: W = [P | U~] rank deficient (ks_pencil_eig) */
 } ks_status;
 
 /* Operator selector for ks_spmm / ks_values. */
@@ -164,6 +165,42 @@ ks_status ks_set_coarse(ks_ctx *ctx, int64_t n_H, const int32_t *d_P_row_ptr, co
  * Asynchronous, deterministic.
  */
 ks_status ks_project_augmented(ks_ctx *ctx, int32_t N, const double *d_Ut, double *d_FA, double *d_FB);
+
+/*
+ * NEXT-1: the small eigenvalue problem of Algorithm 3 and the linear outer loop.
+ *
+ * ks_pencil_eig: lowest k eigenpairs of F_A y = lambda F_B y (Nonlinear_Eig_Hh on W; "a
+ * small-scale algebraic eigenvalue problem solved in serial"), dense, by the cuSOLVER
+ * generalized symmetric eigensolver on the context's stream.
+ *   D = n_H + N >= 1, 1 <= k <= D; d_FA, d_FB [D][D] f64 symmetric (e.g. from ks_project_augmented), not
+ *   modified; d_evals [k] f64 ascending; d_evecs [D][k] f64 row-major, column j = eigenvector j, normalised
+ *   y^T F_B y = 1 (sign arbitrary). Synchronises the stream (reads the solver status).
+ *   Errors: KS_E_ARG, KS_E_RANK (F_B not SPD), KS_E_NONFINITE (no convergence), KS_E_CUDA.
+ */
+ks_status ks_pencil_eig(ks_ctx *ctx, int64_t D, int32_t k, const double *d_FA, const double *d_FB,
+                        double *d_evals, double *d_evecs);
+
+/*
+ * ks_lift: the new orbitals in W (Algorithm 3: psi in S_H + span{psi~}):
+ *   U_new[i][j] = sum_c P_ic Y[c][j] + sum_m U~[i][m] Y[n_H + m][j]
+ *   d_Ut [n_free][N], d_Y [(n_H + N)][k], d_Unew [n_free][k] (may not alias d_Ut). Requires ks_set_coarse.
+ *   Asynchronous.
+ */
+ks_status ks_lift(ks_ctx *ctx, int32_t N, const double *d_Ut, int32_t k, const double *d_Y, double *d_Unew);
+
+/*
+ * ks_augmented_solve: outer iterations of Algorithm 3 with the operators of the last ks_assemble_veff
+ * (a fixed potential): ks_block_solve (tol_bvp, max_iter_bvp) -> ks_project_augmented
+ * -> ks_pencil_eig (lowest N) -> ks_lift, repeated until max_j |lambda_j new - old| <= tol_eig max_j
+ * |lambda_j| or max_outer iterations.
+ *   d_lambda [N] (in: initial guesses, out: Ritz values), d_U [n_free][N] (in/out: orbitals), both updated
+ *   in place; h_outer (host, may be NULL): iterations done; h_history (host, may be NULL) [max_outer][N]:
+ *   the Ritz values of every iteration. Synchronises once per outer iteration.
+ *   Errors: as the four calls; KS_E_NOT_CONVERGED if max_outer is reached (last iterate kept).
+ */
+ks_status ks_augmented_solve(ks_ctx *ctx, int32_t N, double *d_lambda, double *d_U, double tol_eig,
+                             int32_t max_outer, double tol_bvp, int32_t max_iter_bvp, int32_t *h_outer,
+                             double *h_history);
 
 /* Device memory owned by the library (bytes). */
 ks_status ks_memory_bytes(const ks_ctx *ctx, size_t *bytes);

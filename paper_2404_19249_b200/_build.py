@@ -17,6 +17,9 @@ LIB = os.path.join(PKG, "libks.so")
 OBJ = os.path.join(PKG, "build")
 
 NVCC = os.environ.get("NVCC", "nvcc")
+# cuSOLVER (NEXT-1 dense pencil eigensolver) is linked dynamically from the toolkit the library was built with
+CUDA_LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.realpath(
+    __import__("shutil").which(NVCC) or "/usr/local/cuda/bin/nvcc"))), "lib64")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v",
          "-I" + os.path.join(ROOT, "include")]
@@ -55,7 +58,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(one, sources()))
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
+    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-lcusolver",
+           "-Xlinker", "-rpath," + CUDA_LIB]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

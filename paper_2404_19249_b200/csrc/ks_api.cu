@@ -20,6 +20,7 @@ const char *ks_status_name(ks_status s) {
     case KS_E_CUDA: return "KS_E_CUDA";
     case KS_E_NOMEM: return "KS_E_NOMEM";
     case KS_E_STATE: return "KS_E_STATE";
+    case KS_E_RANK: return "KS_E_RANK";
   }
   return "KS_E_?";
 }
@@ -72,6 +73,7 @@ void ks_free(ks_ctx *ctx, void *ptr) {
 }
 
 static void free_all(ks_ctx *ctx) {
+  ks_free_outer(ctx);
   for (auto &a : ctx->allocs) cudaFree(a.first);
   ctx->allocs.clear();
   ctx->bytes = 0;
@@ -227,6 +229,33 @@ ks_status ks_last_iterations(ks_ctx *ctx, int32_t *h_block_iters) {
   KS_CUDA(ctx, cudaMemcpyAsync(h_block_iters, ctx->d_block_iters, 4, cudaMemcpyDeviceToHost, ctx->stream));
   KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return KS_OK;
+}
+
+ks_status ks_pencil_eig(ks_ctx *ctx, int64_t D, int32_t k, const double *d_FA, const double *d_FB, double *d_evals,
+                        double *d_evecs) {
+  if (!ctx) return KS_E_ARG;
+  if (D < 1 || k < 1 || k > D || D > 65536) return ks_fail(ctx, KS_E_ARG, "ks_pencil_eig: need 1 <= k <= D <= 65536");
+  if (!d_FA || !d_FB || !d_evals || !d_evecs) return ks_fail(ctx, KS_E_ARG, "ks_pencil_eig: null pointer");
+  return ks_pencil_eig_impl(ctx, D, k, d_FA, d_FB, d_evals, d_evecs);
+}
+
+ks_status ks_lift(ks_ctx *ctx, int32_t N, const double *d_Ut, int32_t k, const double *d_Y, double *d_Unew) {
+  if (!ctx) return KS_E_ARG;
+  if (N < 1 || N > KS_MAX_N || k < 1 || !d_Ut || !d_Y || !d_Unew || d_Ut == d_Unew)
+    return ks_fail(ctx, KS_E_ARG, "ks_lift: bad arguments");
+  if (ctx->n_H < 1) return ks_fail(ctx, KS_E_STATE, "ks_lift: call ks_set_coarse first");
+  return ks_lift_impl(ctx, N, d_Ut, k, d_Y, d_Unew);
+}
+
+ks_status ks_augmented_solve(ks_ctx *ctx, int32_t N, double *d_lambda, double *d_U, double tol_eig, int32_t max_outer,
+                             double tol_bvp, int32_t max_iter_bvp, int32_t *h_outer, double *h_history) {
+  if (!ctx) return KS_E_ARG;
+  if (N < 1 || N > KS_MAX_N || !d_lambda || !d_U || !(tol_eig >= 0.0) || max_outer < 1 || !(tol_bvp > 0.0) ||
+      max_iter_bvp < 1)
+    return ks_fail(ctx, KS_E_ARG, "ks_augmented_solve: bad arguments");
+  if (!ctx->assembled) return ks_fail(ctx, KS_E_STATE, "ks_augmented_solve: call ks_assemble_veff first");
+  if (ctx->n_H < 1) return ks_fail(ctx, KS_E_STATE, "ks_augmented_solve: call ks_set_coarse first");
+  return ks_augmented_solve_impl(ctx, N, d_lambda, d_U, tol_eig, max_outer, tol_bvp, max_iter_bvp, h_outer, h_history);
 }
 
 ks_status ks_solve_trace(ks_ctx *ctx, int32_t cap, uint64_t *h_ns, int32_t *h_count) {

@@ -93,6 +93,15 @@ struct ks_ctx {
   double *gram_part = nullptr;   // [blocks][2 N N]
   int64_t gram_cap = 0;
 
+  // NEXT-1 (ks_outer.cu): cuSOLVER handle, pencil and outer-loop workspaces
+  void *cusolver = nullptr;
+  double *eig_A = nullptr, *eig_B = nullptr, *eig_w = nullptr, *eig_work = nullptr;
+  int *eig_info = nullptr;
+  int64_t eig_cap = 0;
+  int eig_work_cap = 0;
+  double *outer_Ut = nullptr, *outer_FA = nullptr, *outer_FB = nullptr, *outer_Y = nullptr, *outer_lam = nullptr;
+  int64_t outer_cap = 0, outer_D = 0;
+
   std::string err;
 };
 
@@ -160,3 +169,9 @@ ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, cons
                              const double *Pval);
 ks_status ks_project_impl(ks_ctx *ctx, int N, const double *Ut, double *FA, double *FB);
 void ks_free_coarse(ks_ctx *ctx);
+void ks_free_outer(ks_ctx *ctx);
+ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, const double *FB, double *evals,
+                             double *evecs);
+ks_status ks_lift_impl(ks_ctx *ctx, int N, const double *Ut, int k, const double *Y, double *Unew);
+ks_status ks_augmented_solve_impl(ks_ctx *ctx, int N, double *lambda, double *U, double tol_eig, int max_outer,
+                                  double tol_bvp, int32_t max_iter_bvp, int32_t *h_outer, double *h_history);

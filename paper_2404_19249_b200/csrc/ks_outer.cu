@@ -1,0 +1,156 @@
+// ks_outer.cu -- NEXT-1: close the linear Algorithm-3 loop.
+//   ks_pencil_eig       lowest k eigenpairs of F_A y = lambda F_B y, the "small-scale algebraic eigenvalue
+//                       problem" on W (Nonlinear_Eig_Hh); dense, D = n_H + N
+//                       <= ~1400, by the cuSOLVER generalized symmetric eigensolver (a plain library call,
+//                       like cuBLAS for a plain GEMM: Cholesky of F_B + tridiagonal divide and conquer).
+//   ks_lift             U_new = P y_H + U~ y_t (the new orbitals in S_H + span{psi~}), own kernel.
+//   ks_augmented_solve  outer iterations with a fixed potential: block solve -> projection -> pencil
+//                       eig -> lift, until max |lambda_new - lambda| <= tol_eig * max |lambda|.
+#include <cusolverDn.h>
+
+#include "ks_internal.cuh"
+#include "ks_sell.cuh"
+
+namespace {
+
+// eigenvectors: cuSOLVER leaves them column-major in A (column j = eigenvector j); out [D][k] row-major
+__global__ void k_take_evecs(const double *__restrict__ A, int64_t D, int k, double *__restrict__ out) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= D * k) return;
+  const int64_t i = x / k, j = x % k;
+  out[x] = A[j * D + i];
+}
+
+// U_new[i][j] = sum_t P_it Y[col_t][j] + sum_m U~[i][m] Y[n_H + m][j]; one thread per (row, output column)
+__global__ void k_lift(const int32_t *__restrict__ Pptr, const int32_t *__restrict__ Pcol,
+                       const double *__restrict__ Pval, const double *__restrict__ Ut, int N, int ldu,
+                       const double *__restrict__ Y, int k, int64_t n_H, int64_t n, double *__restrict__ Unew,
+                       int ldo) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= n * k) return;
+  const int64_t i = x / k;
+  const int j = (int)(x % k);
+  double s = 0.0;
+  for (int32_t t = __ldg(Pptr + i); t < __ldg(Pptr + i + 1); t++)
+    s = fma(__ldg(Pval + t), __ldg(Y + (int64_t)__ldg(Pcol + t) * k + j), s);
+  const double *u = Ut + i * ldu;
+  for (int m = 0; m < N; m++) s = fma(__ldg(u + m), __ldg(Y + (n_H + m) * k + j), s);
+  Unew[i * ldo + j] = s;
+}
+
+}  // namespace
+
+static ks_status ensure_solver_handle(ks_ctx *ctx) {
+  if (!ctx->cusolver) {
+    cusolverDnHandle_t h = nullptr;
+    if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) return ks_fail(ctx, KS_E_CUDA, "cusolverDnCreate failed");
+    ctx->cusolver = h;
+  }
+  if (cusolverDnSetStream((cusolverDnHandle_t)ctx->cusolver, ctx->stream) != CUSOLVER_STATUS_SUCCESS)
+    return ks_fail(ctx, KS_E_CUDA, "cusolverDnSetStream failed");
+  return KS_OK;
+}
+
+void ks_free_outer(ks_ctx *ctx) {
+  if (ctx->cusolver) cusolverDnDestroy((cusolverDnHandle_t)ctx->cusolver);
+  ctx->cusolver = nullptr;
+}
+
+ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, const double *FB, double *evals,
+                             double *evecs) {
+  KS_TRY(ensure_solver_handle(ctx));
+  cusolverDnHandle_t h = (cusolverDnHandle_t)ctx->cusolver;
+  if (ctx->eig_cap < D) {
+    ks_free_t(ctx, ctx->eig_A);
+    ks_free_t(ctx, ctx->eig_B);
+    ks_free_t(ctx, ctx->eig_w);
+    KS_TRY(ks_alloc_t(ctx, &ctx->eig_A, D * D, "pencil A"));
+    KS_TRY(ks_alloc_t(ctx, &ctx->eig_B, D * D, "pencil B"));
+    KS_TRY(ks_alloc_t(ctx, &ctx->eig_w, D, "pencil eigenvalues"));
+    ctx->eig_cap = D;
+  }
+  // symmetric matrices: row-major == column-major
+  KS_CUDA(ctx, cudaMemcpyAsync(ctx->eig_A, FA, sizeof(double) * D * D, cudaMemcpyDeviceToDevice, ctx->stream));
+  KS_CUDA(ctx, cudaMemcpyAsync(ctx->eig_B, FB, sizeof(double) * D * D, cudaMemcpyDeviceToDevice, ctx->stream));
+  int lwork = 0;
+  if (cusolverDnDsygvd_bufferSize(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)D,
+                                  ctx->eig_A, (int)D, ctx->eig_B, (int)D, ctx->eig_w, &lwork) != CUSOLVER_STATUS_SUCCESS)
+    return ks_fail(ctx, KS_E_CUDA, "cusolverDnDsygvd_bufferSize failed (D = %lld)", (long long)D);
+  if (ctx->eig_work_cap < lwork) {
+    ks_free_t(ctx, ctx->eig_work);
+    KS_TRY(ks_alloc_t(ctx, &ctx->eig_work, lwork, "pencil workspace"));
+    ctx->eig_work_cap = lwork;
+  }
+  if (!ctx->eig_info) KS_TRY(ks_alloc_t(ctx, &ctx->eig_info, 1, "pencil info"));
+  if (cusolverDnDsygvd(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)D, ctx->eig_A,
+                       (int)D, ctx->eig_B, (int)D, ctx->eig_w, ctx->eig_work, lwork, ctx->eig_info) !=
+      CUSOLVER_STATUS_SUCCESS)
+    return ks_fail(ctx, KS_E_CUDA, "cusolverDnDsygvd failed (D = %lld)", (long long)D);
+  ctx->launches++;
+  int info = 0;
+  KS_CUDA(ctx, cudaMemcpyAsync(&info, ctx->eig_info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (info > D)
+    return ks_fail(ctx, KS_E_RANK, "F_B is not positive definite (leading minor %d): W = [P | U~] is rank deficient",
+                   info - (int)D);
+  if (info != 0) return ks_fail(ctx, KS_E_NONFINITE, "pencil eigensolver did not converge (info %d)", info);
+  KS_CUDA(ctx, cudaMemcpyAsync(evals, ctx->eig_w, sizeof(double) * k, cudaMemcpyDeviceToDevice, ctx->stream));
+  k_take_evecs<<<ks_blocks(D * k, 256), 256, 0, ctx->stream>>>(ctx->eig_A, D, k, evecs);
+  KS_LAUNCHED(ctx);
+  return KS_OK;
+}
+
+ks_status ks_lift_impl(ks_ctx *ctx, int N, const double *Ut, int k, const double *Y, double *Unew) {
+  const int64_t n = ctx->n_free;
+  k_lift<<<ks_blocks(n * k, 256), 256, 0, ctx->stream>>>(ctx->P_ptr, ctx->P_col, ctx->P_val, Ut, N, N, Y, k, ctx->n_H,
+                                                          n, Unew, k);
+  KS_LAUNCHED(ctx);
+  return KS_OK;
+}
+
+ks_status ks_augmented_solve_impl(ks_ctx *ctx, int N, double *lambda, double *U, double tol_eig, int max_outer,
+                                  double tol_bvp, int32_t max_iter_bvp, int32_t *h_outer, double *h_history) {
+  const int64_t n = ctx->n_free, D = ctx->n_H + N;
+  if (ctx->outer_cap < n * N || ctx->outer_D < D) {
+    ks_free_t(ctx, ctx->outer_Ut);
+    ks_free_t(ctx, ctx->outer_FA);
+    ks_free_t(ctx, ctx->outer_FB);
+    ks_free_t(ctx, ctx->outer_Y);
+    ks_free_t(ctx, ctx->outer_lam);
+    KS_TRY(ks_alloc_t(ctx, &ctx->outer_Ut, n * N, "outer U~"));
+    KS_TRY(ks_alloc_t(ctx, &ctx->outer_FA, D * D, "outer F_A"));
+    KS_TRY(ks_alloc_t(ctx, &ctx->outer_FB, D * D, "outer F_B"));
+    KS_TRY(ks_alloc_t(ctx, &ctx->outer_Y, D * N, "outer Y"));
+    KS_TRY(ks_alloc_t(ctx, &ctx->outer_lam, N, "outer lambda"));
+    ctx->outer_cap = n * N;
+    ctx->outer_D = D;
+  }
+  std::vector<double> prev(N), cur(N);
+  KS_CUDA(ctx, cudaMemcpyAsync(prev.data(), lambda, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+  KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  int it = 0;
+  ks_status result = KS_E_NOT_CONVERGED;
+  while (it < max_outer) {
+    KS_TRY(ks_solve_impl(ctx, N, lambda, U, ctx->outer_Ut, tol_bvp, max_iter_bvp, nullptr, nullptr));
+    KS_TRY(ks_project_impl(ctx, N, ctx->outer_Ut, ctx->outer_FA, ctx->outer_FB));
+    KS_TRY(ks_pencil_eig_impl(ctx, D, N, ctx->outer_FA, ctx->outer_FB, ctx->outer_lam, ctx->outer_Y));
+    KS_TRY(ks_lift_impl(ctx, N, ctx->outer_Ut, N, ctx->outer_Y, U));
+    KS_CUDA(ctx, cudaMemcpyAsync(lambda, ctx->outer_lam, sizeof(double) * N, cudaMemcpyDeviceToDevice, ctx->stream));
+    KS_CUDA(ctx, cudaMemcpyAsync(cur.data(), ctx->outer_lam, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+    KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    double dmax = 0.0, lmax = 0.0;
+    for (int j = 0; j < N; j++) {
+      dmax = fmax(dmax, fabs(cur[j] - prev[j]));
+      lmax = fmax(lmax, fabs(cur[j]));
+      if (h_history) h_history[(int64_t)it * N + j] = cur[j];
+    }
+    it++;
+    prev = cur;
+    if (!(dmax == dmax)) { result = KS_E_NONFINITE; break; }
+    if (dmax <= tol_eig * lmax) { result = KS_OK; break; }
+  }
+  if (h_outer) *h_outer = it;
+  if (result != KS_OK)
+    return ks_fail(ctx, result, "ks_augmented_solve: %d outer iterations without reaching tol %g", it, tol_eig);
+  return KS_OK;
+}

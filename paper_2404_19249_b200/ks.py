@@ -16,16 +16,16 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("KS_LIB") or os.path.join(_PKG, "libks.so")
 
 KS_OK, KS_E_ARG, KS_E_MESH, KS_E_NONFINITE, KS_E_NOT_SPD, KS_E_NOT_CONVERGED, KS_E_CUDA, KS_E_NOMEM, \
-    KS_E_STATE = range(9)
+    KS_E_STATE, KS_E_RANK = range(10)
 STATUS_NAMES = {0: "KS_OK", 1: "KS_E_ARG", 2: "KS_E_MESH", 3: "KS_E_NONFINITE", 4: "KS_E_NOT_SPD",
-                5: "KS_E_NOT_CONVERGED", 6: "KS_E_CUDA", 7: "KS_E_NOMEM", 8: "KS_E_STATE"}
+                5: "KS_E_NOT_CONVERGED", 6: "KS_E_CUDA", 7: "KS_E_NOMEM", 8: "KS_E_STATE", 9: "KS_E_RANK"}
 OPS = {"K": 0, "M": 1, "MV": 2, "H": 3, "A": 4}
 
 # every symbol declared in include/ks.h (checked by tests/test_abi.py)
 EXPORTS = ["ks_abi_version", "ks_build_info", "ks_create", "ks_destroy", "ks_set_stream", "ks_pattern",
            "ks_values", "ks_assemble_veff", "ks_spmm", "ks_block_solve", "ks_last_iterations", "ks_solve_trace",
-           "ks_true_residual", "ks_set_coarse", "ks_project_augmented", "ks_memory_bytes", "ks_launch_count",
-           "ks_sync", "ks_last_error"]
+           "ks_true_residual", "ks_set_coarse", "ks_project_augmented", "ks_pencil_eig", "ks_lift",
+           "ks_augmented_solve", "ks_memory_bytes", "ks_launch_count", "ks_sync", "ks_last_error"]
 
 
 class KSError(RuntimeError):
@@ -63,6 +63,9 @@ def load_library(path: str = LIB_PATH):
         "ks_true_residual": (st, [vp, i32, vp, vp, vp, vp]),
         "ks_set_coarse": (st, [vp, i64, vp, vp, vp]),
         "ks_project_augmented": (st, [vp, i32, vp, vp, vp]),
+        "ks_pencil_eig": (st, [vp, i64, i32, vp, vp, vp, vp]),
+        "ks_lift": (st, [vp, i32, vp, i32, vp, vp]),
+        "ks_augmented_solve": (st, [vp, i32, vp, vp, dbl, i32, dbl, i32, C.POINTER(i32), vp]),
         "ks_memory_bytes": (st, [vp, C.POINTER(C.c_size_t)]),
         "ks_launch_count": (st, [vp, C.POINTER(i64)]),
         "ks_sync": (st, [vp]),
@@ -239,6 +242,42 @@ class Context:
             FB = torch.empty((D, D), dtype=torch.float64, device=Ut.device)
         self._call(self._L.ks_project_augmented(self._h, N, _ptr(Ut), _ptr(FA), _ptr(FB)))
         return FA, FB
+
+    def pencil_eig(self, FA, FB, k: int):
+        """ks_pencil_eig: lowest k eigenpairs of F_A y = lambda F_B y -> (evals [k], evecs [D][k])."""
+        import torch
+        D = FA.shape[0]
+        _check_cuda_tensor(FA, torch.float64, (D, D), "FA")
+        _check_cuda_tensor(FB, torch.float64, (D, D), "FB")
+        ev = torch.empty(k, dtype=torch.float64, device=FA.device)
+        Y = torch.empty((D, k), dtype=torch.float64, device=FA.device)
+        self._call(self._L.ks_pencil_eig(self._h, D, int(k), _ptr(FA), _ptr(FB), _ptr(ev), _ptr(Y)))
+        return ev, Y
+
+    def lift(self, Ut, Y, Unew=None):
+        """ks_lift: U_new = P Y[:n_H] + U~ Y[n_H:]."""
+        import torch
+        _check_cuda_tensor(Ut, torch.float64, None, "Ut")
+        _check_cuda_tensor(Y, torch.float64, None, "Y")
+        N, k = Ut.shape[1], Y.shape[1]
+        if Unew is None:
+            Unew = torch.empty((self.n_free, k), dtype=torch.float64, device=Ut.device)
+        self._call(self._L.ks_lift(self._h, N, _ptr(Ut), int(k), _ptr(Y), _ptr(Unew)))
+        return Unew
+
+    def augmented_solve(self, lam, U, tol_eig=1e-10, max_outer=50, tol_bvp=1e-10, max_iter_bvp=2000):
+        """ks_augmented_solve: outer iterations of Algorithm 3 with the current operators; lam and U are
+        updated in place. Returns (outer iterations, Ritz-value history [outer][N] as numpy)."""
+        import torch
+        _check_cuda_tensor(U, torch.float64, None, "U")
+        _check_cuda_tensor(lam, torch.float64, None, "lam")
+        N = U.shape[1]
+        hist = np.zeros((max_outer, N))
+        outer = C.c_int32()
+        self._call(self._L.ks_augmented_solve(self._h, N, _ptr(lam), _ptr(U), float(tol_eig), int(max_outer),
+                                              float(tol_bvp), int(max_iter_bvp), C.byref(outer),
+                                              hist.ctypes.data))
+        return outer.value, hist[:outer.value].copy()
 
     def memory_bytes(self) -> int:
         v = C.c_size_t()

@@ -1,0 +1,104 @@
+"""NEXT-1 on the GPU: the pencil eigensolver, the lift and the Algorithm-3 outer loop
+through the C ABI, against the oracle (tests/test_oracle_next1.py pins it) on the same inputs.
+Tolerances: eigenvalues |d lambda| <= 1e-9 max|lambda| (north_star's projected-eigenvalue bound);
+eigenvectors compared through the residual and F_B-orthonormality (signs are arbitrary, Q23); lift
+|d u| <= 1e-12 (|P||Y| + |U~||Y|) elementwise."""
+import numpy as np
+import pytest
+import scipy.linalg as sl
+
+import gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+DEV = "cuda"
+
+
+def dt(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def _ctx(p, mu):
+    import paper_2404_19249_b200 as ks
+    ctx = ks.Context(p.xyz, p.tets, p.dirichlet)
+    ctx.assemble_veff(dt(p.V), mu)
+    ctx.set_coarse(p.n_H, dt(p.P_rowptr), dt(p.P_col), dt(p.P_val))
+    return ctx
+
+
+@pytest.mark.parametrize("c", [2, 3])
+def test_pencil_eig_matches_oracle(c):
+    p = gen.make_problem(c)
+    ctx = _ctx(p, p.mu)
+    Ut, _, _ = ctx.block_solve(dt(p.lam), dt(p.U))
+    FA, FB = ctx.project_augmented(Ut)
+    ev, Y = ctx.pencil_eig(FA, FB, p.N)
+    assert ctx.sync() == 0
+    FAh, FBh = FA.cpu().numpy(), FB.cpu().numpy()
+    evo, Yo = oracle.pencil_eig(FAh, FBh, p.N)
+    ev, Y = ev.cpu().numpy(), Y.cpu().numpy()
+    assert np.all(np.abs(ev - evo) <= 1e-9 * np.abs(evo).max())
+    scale = np.abs(FAh).max() + np.abs(ev).max() * np.abs(FBh).max()
+    assert np.abs(FAh @ Y - (FBh @ Y) * ev).max() <= 1e-9 * scale
+    assert np.abs(Y.T @ FBh @ Y - np.eye(p.N)).max() <= 1e-9
+
+
+def test_pencil_eig_rank_deficient_is_reported():
+    import paper_2404_19249_b200 as ks
+    p = gen.make_problem(1)
+    ctx = _ctx(p, p.mu)
+    D = p.n_H + 2
+    FA = torch.eye(D, dtype=torch.float64, device=DEV)
+    FB = torch.eye(D, dtype=torch.float64, device=DEV)
+    FB[D - 1, D - 1] = -1.0
+    with pytest.raises(ks.KSError) as e:
+        ctx.pencil_eig(FA, FB, 2)
+    assert e.value.status == ks.KS_E_RANK
+
+
+@pytest.mark.parametrize("c,k", [(2, 4), (3, 8), (2, 3)])
+def test_lift_matches_oracle(c, k):
+    p = gen.make_problem(c)
+    ctx = _ctx(p, p.mu)
+    om = oracle.Mesh.from_problem(p)
+    rng = np.random.default_rng(c * 10 + k)
+    Ut = rng.standard_normal((p.n_free, p.N))
+    Y = rng.standard_normal((p.n_H + p.N, k))
+    Un = ctx.lift(dt(Ut), dt(Y)).cpu().numpy()
+    ref = om.lift(p.n_H, p.P_rowptr, p.P_col, p.P_val, Ut, Y)
+    import scipy.sparse as sp
+    P = sp.csr_matrix((p.P_val, p.P_col, p.P_rowptr), shape=(p.n_free, p.n_H))
+    bound = abs(P) @ np.abs(Y[:p.n_H]) + np.abs(Ut) @ np.abs(Y[p.n_H:])
+    assert np.all(np.abs(Un - ref) <= 1e-12 * bound)
+
+
+def test_augmented_solve_converges_like_the_oracle():
+    """The outer loop of Algorithm 3 on the harmonic oscillator (fixed potential): the GPU's Ritz values
+    converge to the brute-force fine eigenvalues, iterate by iterate within 1e-9 of the oracle's loop."""
+    p = gen.make_problem(dict(L=5.0, n=10, grading=None, jitter=0.15, nuclei=[((0.0, 0.0, 0.0), 1)],
+                              vnoise=0.0, N=4, orbitals="gauss", lam=("const", 2.0), nc=5, seed=9,
+                              potential="harmonic"))
+    mu = 0.0
+    xf = p.xyz[p.free_nodes]
+    ctr = np.array([[0.0, 0.0, 0.0], [1.0, 0.0, 0.0], [0.0, 1.0, 0.0], [0.0, 0.0, 1.0]])
+    U0 = np.ascontiguousarray(np.stack([np.exp(-0.5 * ((xf - c) ** 2).sum(1)) for c in ctr], axis=1))
+    ctx = _ctx(p, mu)
+    lam, U = dt(p.lam), dt(U0)
+    outer, hist = ctx.augmented_solve(lam, U, tol_eig=1e-12, max_outer=60, tol_bvp=1e-12)
+    assert ctx.sync() == 0
+    om = oracle.Mesh.from_problem(p)
+    om.assemble_veff(p.V, mu)
+    H, M = om.csr("H").toarray(), om.csr("M").toarray()
+    w = sl.eigh(H, M, eigvals_only=True)[:p.N]
+    lam_h = lam.cpu().numpy()
+    assert np.all(np.abs(lam_h - w) <= 1e-9 * np.abs(w).max()), (lam_h, w)
+    # the oracle's loop, iterate by iterate (same inputs; the Ritz values of the first iterations agree
+    # to the solver tolerance before rounding differences can matter)
+    lo, Uo = p.lam.copy(), U0.copy()
+    for it in range(min(outer, 8)):
+        lo, Uo, _ = oracle.augmented_step(om, p.n_H, p.P_rowptr, p.P_col, p.P_val, lo, Uo, tol=1e-12)
+        assert np.all(np.abs(hist[it] - lo) <= 1e-9 * np.abs(lo).max()), (it, hist[it], lo)
+    Uh = U.cpu().numpy()
+    assert np.abs(Uh.T @ M @ Uh - np.eye(p.N)).max() < 1e-8
