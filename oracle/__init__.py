@@ -57,6 +57,8 @@ def lib():
         L.or_project.argtypes = [vp, i64, vp, vp, vp, i32, vp, vp, vp]
         L.or_pencil_eig.restype = i32
         L.or_pencil_eig.argtypes = [i64, vp, vp, i32, vp, vp]
+        L.or_interpolation.restype = i32
+        L.or_interpolation.argtypes = [vp, i64, vp, i64, vp, i64, vp, vp, dbl, vp, vp, vp, C.POINTER(i64)]
         L.or_lift.restype = i32
         L.or_lift.argtypes = [vp, i64, vp, vp, vp, i32, vp, i32, vp, vp]
         _lib = L
@@ -85,6 +87,29 @@ def pencil_eig(FA, FB, k):
     if st != OR_OK:
         raise OracleError(st, "pencil_eig")
     return ev, Y
+
+
+INTERP_DROP = 1e-13  # |lambda| <= this is dropped from a P row (reading R4)
+
+
+def interpolation(xyz_f, free_nodes, xyz_c, tets_c, dirichlet_c, drop=INTERP_DROP):
+    """NEXT-3: the nonnested P1 interpolation operator of Algorithm 1 (oracle.c or_interpolation, brute-force
+    point location). Returns (rowptr [n_free+1] i32, col i32, val f64, n_H)."""
+    xyz_f = np.ascontiguousarray(xyz_f, dtype=np.float64)
+    fn = np.ascontiguousarray(free_nodes, dtype=np.int64)
+    xyz_c = np.ascontiguousarray(xyz_c, dtype=np.float64)
+    tets_c = np.ascontiguousarray(tets_c, dtype=np.int32)
+    dir_c = np.ascontiguousarray(dirichlet_c, dtype=np.uint8)
+    nf = fn.shape[0]
+    rp = np.zeros(nf + 1, np.int32)
+    col = np.zeros(4 * nf, np.int32)
+    val = np.zeros(4 * nf)
+    nH = C.c_int64()
+    st = lib().or_interpolation(_p(xyz_f), nf, _p(fn), xyz_c.shape[0], _p(xyz_c), tets_c.shape[0], _p(tets_c),
+                                _p(dir_c), float(drop), _p(rp), _p(col), _p(val), C.byref(nH))
+    if st != OR_OK:
+        raise OracleError(st, "interpolation")
+    return rp, col[:rp[-1]].copy(), val[:rp[-1]].copy(), nH.value
 
 
 def augmented_step(mesh, n_H, P_rowptr, P_col, P_val, lam, U, tol=1e-10, max_iter=2000):

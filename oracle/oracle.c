@@ -535,3 +535,84 @@ int or_lift(const or_mesh *h, int64_t n_H, const int32_t *Pptr, const int32_t *P
     }
   return OR_OK;
 }
+
+/*
+ * NEXT-3: the nonnested interpolation operator P = I_H^h of Algorithm 1
+ * (PAPER.md:499-548): for every vertex q of the fine mesh, the P1 interpolant of a coarse function at q,
+ * g(q) = sum_j lambda_j f(q_j), lambda = the barycentric coordinates of q in the coarse tet K that
+ * contains it. Plain definition (no quadtree, no walk): K = the coarse tet maximising min_j lambda_j(q; K)
+ * (the containing tet; on shared faces/edges every containing tet gives the same nonzero weights), first
+ * index on ties. Row i of P (fine FREE node i = free_nodes[i]) keeps the coarse FREE vertices (coarse
+ * Dirichlet vertices carry zero data) with |lambda| > drop (reading R4), sorted by
+ * coarse free index. O(n_free x n_coarse_tets): tiny meshes only.
+ *   xyz_f [*][3] fine coordinates, free_nodes [n_free] fine node ids of the rows; xyz_c [n_c][3],
+ *   tets_c [m_c][4], dir_c [n_c] (nonzero = Dirichlet); out: rowptr [n_free+1], col [4 n_free],
+ *   val [4 n_free]; *n_H = number of coarse free nodes. Returns OR_E_MESH if a tet is degenerate or a
+ *   point lies outside the coarse mesh (min lambda < -1e-10).
+ */
+int or_interpolation(const double *xyz_f, int64_t n_free, const int64_t *free_nodes, int64_t n_c,
+                     const double *xyz_c, int64_t m_c, const int32_t *tets_c, const uint8_t *dir_c, double drop,
+                     int32_t *rowptr, int32_t *col, double *val, int64_t *n_H) {
+  int32_t *cfree = (int32_t *)malloc(sizeof(int32_t) * (n_c > 0 ? n_c : 1));
+  double *Jinv = (double *)malloc(sizeof(double) * 9 * (m_c > 0 ? m_c : 1));
+  if (!cfree || !Jinv) { free(cfree); free(Jinv); return OR_E_NOMEM; }
+  int64_t nh = 0;
+  for (int64_t v = 0; v < n_c; v++) cfree[v] = dir_c[v] ? -1 : (int32_t)nh++;
+  *n_H = nh;
+  /* inverse of the edge matrix J = [x1-x0, x2-x0, x3-x0] (columns) per coarse tet: lambda_{1..3} = J^-1 (q - x0) */
+  for (int64_t t = 0; t < m_c; t++) {
+    const double *x0 = xyz_c + 3 * (int64_t)tets_c[4 * t];
+    double J[3][3];
+    for (int a = 0; a < 3; a++)
+      for (int r = 0; r < 3; r++) J[r][a] = xyz_c[3 * (int64_t)tets_c[4 * t + 1 + a] + r] - x0[r];
+    double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) - J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                 J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+    if (!(fabs(det) > 0.0)) { free(cfree); free(Jinv); return OR_E_MESH; }
+    double *Ji = Jinv + 9 * t;
+    Ji[0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) / det;
+    Ji[1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) / det;
+    Ji[2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) / det;
+    Ji[3] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) / det;
+    Ji[4] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) / det;
+    Ji[5] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) / det;
+    Ji[6] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) / det;
+    Ji[7] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / det;
+    Ji[8] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / det;
+  }
+  int64_t nnz = 0;
+  rowptr[0] = 0;
+  for (int64_t i = 0; i < n_free; i++) {
+    const double *q = xyz_f + 3 * free_nodes[i];
+    int64_t best = -1;
+    double best_min = -1e300, bl[4] = {0, 0, 0, 0};
+    for (int64_t t = 0; t < m_c; t++) {
+      const double *x0 = xyz_c + 3 * (int64_t)tets_c[4 * t];
+      const double d0 = q[0] - x0[0], d1 = q[1] - x0[1], d2 = q[2] - x0[2];
+      const double *Ji = Jinv + 9 * t;
+      double l1 = Ji[0] * d0 + Ji[1] * d1 + Ji[2] * d2;
+      double l2 = Ji[3] * d0 + Ji[4] * d1 + Ji[5] * d2;
+      double l3 = Ji[6] * d0 + Ji[7] * d1 + Ji[8] * d2;
+      double l0 = 1.0 - l1 - l2 - l3;
+      double m = fmin(fmin(l0, l1), fmin(l2, l3));
+      if (m > best_min) { best_min = m; best = t; bl[0] = l0; bl[1] = l1; bl[2] = l2; bl[3] = l3; }
+    }
+    if (best < 0 || best_min < -1e-10) { free(cfree); free(Jinv); return OR_E_MESH; }
+    /* keep free coarse vertices with |lambda| > drop, sorted by coarse free index */
+    int32_t cc[4];
+    double vv[4];
+    int m = 0;
+    for (int a = 0; a < 4; a++) {
+      int32_t cf = cfree[tets_c[4 * best + a]];
+      if (cf < 0 || !(fabs(bl[a]) > drop)) continue;
+      int pos = m;
+      while (pos > 0 && cc[pos - 1] > cf) { cc[pos] = cc[pos - 1]; vv[pos] = vv[pos - 1]; pos--; }
+      cc[pos] = cf;
+      vv[pos] = bl[a];
+      m++;
+    }
+    for (int a = 0; a < m; a++) { col[nnz] = cc[a]; val[nnz] = vv[a]; nnz++; }
+    rowptr[i + 1] = (int32_t)nnz;
+  }
+  free(cfree); free(Jinv);
+  return OR_OK;
+}
