@@ -202,6 +202,22 @@ ks_status ks_augmented_solve(ks_ctx *ctx, int32_t N, double *d_lambda, double *d
                              int32_t max_outer, double tol_bvp, int32_t max_iter_bvp, int32_t *h_outer,
                              double *h_history);
 
+/*
+ * NEXT-3: the nonnested interpolation operator P = I_H^h of Algorithm 1
+ * from an independent coarse tet mesh (nonnested, possibly unstructured, covering the
+ * fine mesh's domain): row i holds the barycentric coordinates of fine free node i in the coarse tet that
+ * contains it, restricted to coarse FREE vertices (Dirichlet vertices carry zero data) with |lambda| > 1e-13,
+ * sorted by coarse free index (coarse free index = rank of a non-Dirichlet coarse node, ascending id).
+ *   h_xyz_c [n_c][3] f64, h_tets_c [m_c][4] i32, h_dirichlet_c [n_c] u8 (host, read during the call);
+ *   d_P_row_ptr [n_free+1] i32, d_P_col [4 n_free] i32, d_P_val [4 n_free] f64 (device, caller-owned outputs,
+ *   ready for ks_set_coarse); *h_n_H = coarse free nodes, *h_p_nnz = entries written.
+ * Synchronises the stream. Errors: KS_E_ARG, KS_E_MESH (degenerate coarse tet, node id out of range, or a fine
+ * node outside the coarse mesh), KS_E_CUDA.
+ */
+ks_status ks_interpolation(ks_ctx *ctx, int64_t n_c, const double *h_xyz_c, int64_t m_c, const int32_t *h_tets_c,
+                           const uint8_t *h_dirichlet_c, int32_t *d_P_row_ptr, int32_t *d_P_col, double *d_P_val,
+                           int64_t *h_n_H, int64_t *h_p_nnz);
+
 /* Device memory owned by the library (bytes). */
 ks_status ks_memory_bytes(const ks_ctx *ctx, size_t *bytes);
 

@@ -258,6 +258,17 @@ ks_status ks_augmented_solve(ks_ctx *ctx, int32_t N, double *d_lambda, double *d
   return ks_augmented_solve_impl(ctx, N, d_lambda, d_U, tol_eig, max_outer, tol_bvp, max_iter_bvp, h_outer, h_history);
 }
 
+ks_status ks_interpolation(ks_ctx *ctx, int64_t n_c, const double *h_xyz_c, int64_t m_c, const int32_t *h_tets_c,
+                           const uint8_t *h_dirichlet_c, int32_t *d_P_row_ptr, int32_t *d_P_col, double *d_P_val,
+                           int64_t *h_n_H, int64_t *h_p_nnz) {
+  if (!ctx) return KS_E_ARG;
+  if (n_c < 4 || m_c < 1 || n_c > 0x7fffffffLL || m_c > 0x7fffffffLL || !h_xyz_c || !h_tets_c || !h_dirichlet_c ||
+      !d_P_row_ptr || !d_P_col || !d_P_val || !h_n_H || !h_p_nnz)
+    return ks_fail(ctx, KS_E_ARG, "ks_interpolation: bad arguments");
+  return ks_interpolation_impl(ctx, n_c, h_xyz_c, m_c, h_tets_c, h_dirichlet_c, d_P_row_ptr, d_P_col, d_P_val,
+                               h_n_H, h_p_nnz);
+}
+
 ks_status ks_solve_trace(ks_ctx *ctx, int32_t cap, uint64_t *h_ns, int32_t *h_count) {
   if (!ctx || !h_count || (cap > 0 && !h_ns)) return KS_E_ARG;
   *h_count = 0;

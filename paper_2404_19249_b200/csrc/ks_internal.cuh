@@ -28,6 +28,7 @@ struct ks_ctx {
 
   // mesh / pattern (library-owned device memory)
   int32_t *tets = nullptr;          // [4 n_tets]
+  double *xyz = nullptr;            // [3 n_nodes] node coordinates
   int32_t *free_of_node = nullptr;  // [n_nodes]
   int32_t *node_of_free = nullptr;  // [n_free]
   int32_t *row_ptr = nullptr;       // [n_free+1]
@@ -93,6 +94,7 @@ struct ks_ctx {
   double *gram_part = nullptr;   // [blocks][2 N N]
   int64_t gram_cap = 0;
 
+  int interp_fallbacks = 0;         // last ks_interpolation needed the scan fallback of the walk
   // NEXT-1 (ks_outer.cu): cuSOLVER handle, pencil and outer-loop workspaces
   void *cusolver = nullptr;
   double *eig_A = nullptr, *eig_B = nullptr, *eig_w = nullptr, *eig_work = nullptr;
@@ -170,6 +172,9 @@ ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, cons
 ks_status ks_project_impl(ks_ctx *ctx, int N, const double *Ut, double *FA, double *FB);
 void ks_free_coarse(ks_ctx *ctx);
 void ks_free_outer(ks_ctx *ctx);
+ks_status ks_interpolation_impl(ks_ctx *ctx, int64_t n_c, const double *h_xyz_c, int64_t m_c, const int32_t *h_tets_c,
+                                const uint8_t *h_dir_c, int32_t *d_rowptr, int32_t *d_col, double *d_val,
+                                int64_t *h_nH, int64_t *h_pnnz);
 ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, const double *FB, double *evals,
                              double *evecs);
 ks_status ks_lift_impl(ks_ctx *ctx, int N, const double *Ut, int k, const double *Y, double *Unew);

@@ -203,7 +203,8 @@ ks_status ks_setup_mesh(ks_ctx *ctx, const double *h_xyz, const int32_t *h_tets,
   uint8_t *dir;
   int32_t *flag, *scan;
   unsigned long long *bad;
-  TMP(ctx, tb, &xyz, 3 * nn);
+  KS_TRY(ks_alloc_t(ctx, &ctx->xyz, 3 * nn, "xyz"));   // kept: point location of NEXT-3 (ks_interpolation)
+  xyz = ctx->xyz;
   TMP(ctx, tb, &dir, nn);
   TMP(ctx, tb, &flag, nn);
   TMP(ctx, tb, &scan, nn);

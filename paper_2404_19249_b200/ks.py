@@ -25,7 +25,7 @@ OPS = {"K": 0, "M": 1, "MV": 2, "H": 3, "A": 4}
 EXPORTS = ["ks_abi_version", "ks_build_info", "ks_create", "ks_destroy", "ks_set_stream", "ks_pattern",
            "ks_values", "ks_assemble_veff", "ks_spmm", "ks_block_solve", "ks_last_iterations", "ks_solve_trace",
            "ks_true_residual", "ks_set_coarse", "ks_project_augmented", "ks_pencil_eig", "ks_lift",
-           "ks_augmented_solve", "ks_memory_bytes", "ks_launch_count", "ks_sync", "ks_last_error"]
+           "ks_augmented_solve", "ks_interpolation", "ks_memory_bytes", "ks_launch_count", "ks_sync", "ks_last_error"]
 
 
 class KSError(RuntimeError):
@@ -66,6 +66,7 @@ def load_library(path: str = LIB_PATH):
         "ks_pencil_eig": (st, [vp, i64, i32, vp, vp, vp, vp]),
         "ks_lift": (st, [vp, i32, vp, i32, vp, vp]),
         "ks_augmented_solve": (st, [vp, i32, vp, vp, dbl, i32, dbl, i32, C.POINTER(i32), vp]),
+        "ks_interpolation": (st, [vp, i64, vp, i64, vp, vp, vp, vp, vp, C.POINTER(i64), C.POINTER(i64)]),
         "ks_memory_bytes": (st, [vp, C.POINTER(C.c_size_t)]),
         "ks_launch_count": (st, [vp, C.POINTER(i64)]),
         "ks_sync": (st, [vp]),
@@ -278,6 +279,22 @@ class Context:
                                               float(tol_bvp), int(max_iter_bvp), C.byref(outer),
                                               hist.ctypes.data))
         return outer.value, hist[:outer.value].copy()
+
+    def interpolation(self, xyz_c, tets_c, dirichlet_c):
+        """ks_interpolation: P = I_H^h from an independent coarse mesh (host arrays) -> (row_ptr, col, val)
+        as CUDA tensors and n_H."""
+        import torch
+        xyz_c = np.ascontiguousarray(xyz_c, dtype=np.float64)
+        tets_c = np.ascontiguousarray(tets_c, dtype=np.int32)
+        dir_c = np.ascontiguousarray(dirichlet_c, dtype=np.uint8)
+        rp = torch.empty(self.n_free + 1, dtype=torch.int32, device=self.device)
+        col = torch.empty(4 * self.n_free, dtype=torch.int32, device=self.device)
+        val = torch.empty(4 * self.n_free, dtype=torch.float64, device=self.device)
+        nH, pn = C.c_int64(), C.c_int64()
+        self._call(self._L.ks_interpolation(self._h, xyz_c.shape[0], xyz_c.ctypes.data, tets_c.shape[0],
+                                            tets_c.ctypes.data, dir_c.ctypes.data, _ptr(rp), _ptr(col), _ptr(val),
+                                            C.byref(nH), C.byref(pn)))
+        return rp, col[:pn.value], val[:pn.value], nH.value
 
     def memory_bytes(self) -> int:
         v = C.c_size_t()
