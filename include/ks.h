@@ -218,6 +218,18 @@ ks_status ks_interpolation(ks_ctx *ctx, int64_t n_c, const double *h_xyz_c, int6
                            const uint8_t *h_dirichlet_c, int32_t *d_P_row_ptr, int32_t *d_P_col, double *d_P_val,
                            int64_t *h_n_H, int64_t *h_p_nnz);
 
+/*
+ * NEXT-2: the nonlinear terms of the Kohn-Sham operator, on all nodes.
+ * ks_density: rho(x_v) = f sum_j psi_j(x_v)^2 (f = occupation per orbital, 2 for the
+ *   paper's closed shells, reading R6); d_U [n_free][N]; d_rho [n_nodes] (0 on Dirichlet nodes).
+ * ks_vxc: LDA exchange -(3 rho / pi)^(1/3) + Perdew-Zunger correlation (Eqs. expot, copot,
+ *   PAPER.md:330-362) -> d_vxc [n_nodes]; d_eps [n_nodes] (may be NULL) = eps_x + eps_c, the
+ *   exchange-correlation energy per electron; rho <= 0 gives 0.
+ * Asynchronous.
+ */
+ks_status ks_density(ks_ctx *ctx, int32_t N, const double *d_U, double f, double *d_rho);
+ks_status ks_vxc(ks_ctx *ctx, const double *d_rho, double *d_vxc, double *d_eps);
+
 /* Device memory owned by the library (bytes). */
 ks_status ks_memory_bytes(const ks_ctx *ctx, size_t *bytes);
 

@@ -59,6 +59,12 @@ def lib():
         L.or_pencil_eig.argtypes = [i64, vp, vp, i32, vp, vp]
         L.or_interpolation.restype = i32
         L.or_interpolation.argtypes = [vp, i64, vp, i64, vp, i64, vp, vp, dbl, vp, vp, vp, C.POINTER(i64)]
+        L.or_density.restype = i32
+        L.or_density.argtypes = [vp, i32, vp, dbl, vp]
+        L.or_vxc.restype = i32
+        L.or_vxc.argtypes = [i64, vp, vp, vp]
+        L.or_hartree.restype = i32
+        L.or_hartree.argtypes = [vp, vp, vp, dbl, i32, vp, vp, C.POINTER(C.c_int)]
         L.or_lift.restype = i32
         L.or_lift.argtypes = [vp, i64, vp, vp, vp, i32, vp, i32, vp, vp]
         _lib = L
@@ -87,6 +93,16 @@ def pencil_eig(FA, FB, k):
     if st != OR_OK:
         raise OracleError(st, "pencil_eig")
     return ev, Y
+
+
+def vxc(rho):
+    """NEXT-2: LDA exchange + Perdew-Zunger correlation potential and energy per electron at nodal densities
+    (oracle.c or_vxc). Returns (v_xc, eps_xc)."""
+    rho = np.ascontiguousarray(rho, dtype=np.float64)
+    v = np.empty_like(rho)
+    e = np.empty_like(rho)
+    lib().or_vxc(rho.size, _p(rho), _p(v), _p(e))
+    return v, e
 
 
 INTERP_DROP = 1e-13  # |lambda| <= this is dropped from a P row (DESIGN.md reading R4)
@@ -233,6 +249,26 @@ class Mesh:
         if st != OR_OK:
             raise OracleError(st, "lift")
         return Unew
+
+    def density(self, U, f=2.0):
+        """NEXT-2: nodal density f sum_i psi_i^2 on all nodes (oracle.c or_density)."""
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        rho = np.empty(self.n_nodes)
+        lib().or_density(self._h, U.shape[1], _p(U), float(f), _p(rho))
+        return rho
+
+    def hartree(self, rho, tol=1e-12, max_iter=100000):
+        """NEXT-2: Hartree potential on all nodes (oracle.c or_hartree). Returns (vh [n_nodes], moments [10],
+        iterations)."""
+        rho = np.ascontiguousarray(rho, dtype=np.float64)
+        vh = np.empty(self.n_nodes)
+        mom = np.empty(10)
+        it = C.c_int()
+        st = lib().or_hartree(self._h, _p(self._keep[0]), _p(rho), float(tol), int(max_iter), _p(vh), _p(mom),
+                              C.byref(it))
+        if st != OR_OK:
+            raise OracleError(st, "hartree")
+        return vh, mom, it.value
 
     def csr(self, which):
         """scipy CSR of one operator (for brute-force pins in tests)."""

@@ -616,3 +616,186 @@ int or_interpolation(const double *xyz_f, int64_t n_free, const int64_t *free_no
   free(cfree); free(Jinv);
   return OR_OK;
 }
+
+/*
+ * NEXT-2: the nonlinear terms of the Kohn-Sham operator.
+ *
+ * or_density: nodal density rho(x_v) = f sum_i psi_i(x_v)^2 (rho_Psi = sum |psi_i|^2;
+ * occupation f per orbital: DESIGN.md reading R6 -- the paper's examples put 2 electrons in each orbital,
+ * He N = 1, HLi N = 2, CH4 N = 5, C6H6 N = 21), on ALL nodes (psi = 0 on Dirichlet nodes).
+ *   U [n_free][N], rho [n_nodes].
+ */
+int or_density(const or_mesh *h, int N, const double *U, double f, double *rho) {
+  for (int64_t v = 0; v < h->n_nodes; v++) {
+    int32_t i = h->free_of_node[v];
+    double s = 0.0;
+    if (i >= 0)
+      for (int j = 0; j < N; j++) s += U[(int64_t)i * N + j] * U[(int64_t)i * N + j];
+    rho[v] = f * s;
+  }
+  return OR_OK;
+}
+
+/*
+ * or_vxc: LDA exchange V_x = -(3 rho / pi)^(1/3) (Eq. expot) plus Perdew-Zunger correlation
+ * (Eq. copot) with r_s = (3 / (4 pi rho))^(1/3), A = 0.0311, B = -0.048, C = 0.0020,
+ * D = -0.0116, gamma = -0.1423, beta1 = 1.0529, beta2 = 0.3334:
+ *   r_s < 1:  V_c = A ln r_s + (B - A/3) + (2/3) C r_s ln r_s + (1/3)(2D - C) r_s
+ *   r_s >= 1: V_c = eps_c (1 + 7/6 beta1 sqrt(r_s) + 4/3 beta2 r_s) / (1 + beta1 sqrt(r_s) + beta2 r_s),
+ *             eps_c = gamma / (1 + beta1 sqrt(r_s) + beta2 r_s).
+ * rho <= 0 gives V_xc = 0 (no electrons). Also returns eps_xc = eps_x + eps_c per node when eps != NULL
+ * (eps_x = -(3/4)(3 rho / pi)^(1/3), the energy per electron of E_x^LDA).
+ */
+int or_vxc(int64_t n, const double *rho, double *vxc, double *eps) {
+  const double A = 0.0311, B = -0.048, C = 0.0020, D = -0.0116, G = -0.1423, B1 = 1.0529, B2 = 0.3334;
+  const double PI = 3.14159265358979323846;
+  for (int64_t v = 0; v < n; v++) {
+    double r = rho[v];
+    if (!(r > 0.0)) { vxc[v] = 0.0; if (eps) eps[v] = 0.0; continue; }
+    double vx = -cbrt(3.0 * r / PI);
+    double rs = cbrt(3.0 / (4.0 * PI * r));
+    double vc, ec;
+    if (rs < 1.0) {
+      double l = log(rs);
+      ec = A * l + B + C * rs * l + D * rs;
+      vc = A * l + (B - A / 3.0) + (2.0 / 3.0) * C * rs * l + (1.0 / 3.0) * (2.0 * D - C) * rs;
+    } else {
+      double sq = sqrt(rs), den = 1.0 + B1 * sq + B2 * rs;
+      ec = G / den;
+      vc = ec * (1.0 + (7.0 / 6.0) * B1 * sq + (4.0 / 3.0) * B2 * rs) / den;
+    }
+    vxc[v] = vx + vc;
+    if (eps) eps[v] = 0.75 * vx + ec;
+  }
+  return OR_OK;
+}
+
+/*
+ * or_hartree: the Hartree potential: -Lap V = 4 pi rho in Omega, V = w_D on dOmega, with
+ * w_D the multipole expansion (Eq. bd) about the centre of charge x'' = int x rho / int rho:
+ *   w_D(x) = Q/|d| + sum_i p_i d_i/|d|^3 + 1/2 sum_ij q_ij (3 d_i d_j - delta_ij |d|^2)/|d|^5,  d = x - x'',
+ *   Q = int rho, p_i = int rho (x'-x'')_i, q_ij = int rho (x'-x'')_i (x'-x'')_j.
+ * (reading R5: the factor 1/2 of the second-order Taylor term of 1/|x - x'|, missing in the printed
+ * Eq. bd.) Moments are exact integrals of the P1 density: int_T lambda^alpha = 3! alpha! |T| / (3+|alpha|)!.
+ * P1 Galerkin with the Dirichlet lift: for free i, sum_j K_ij V_j = 4 pi sum_{all b} M_ib rho_b
+ *   - sum_{Dirichlet b} K_ib w_D(x_b), accumulated element by element (t ascending); the free values by Jacobi-PCG
+ * on K from zero to ||r|| <= tol ||b||. vh [n_nodes] = the free values and w_D on Dirichlet nodes.
+ * mom [10] (may be NULL) = Q, x''_0..2, p_0..2, q_00, q_11, q_22 (diagonal). Returns OR_E_NOT_CONVERGED if
+ * max_iter is reached (vh still written), *iters = iterations.
+ */
+int or_hartree(const or_mesh *h, const double *xyz, const double *rho, double tol, int max_iter, double *vh,
+               double *mom, int *iters) {
+  const double PI = 3.14159265358979323846;
+  int64_t nt = h->n_tets, n = h->n_free, nn = h->n_nodes;
+  /* moments */
+  double Q = 0.0, m1[3] = {0, 0, 0};
+  for (int64_t t = 0; t < nt; t++) {
+    const int32_t *v = h->tets + 4 * t;
+    double V = h->vol[t], sr = 0.0;
+    for (int a = 0; a < 4; a++) sr += rho[v[a]];
+    Q += V * sr / 4.0;
+    for (int a = 0; a < 4; a++)
+      for (int b = 0; b < 4; b++)
+        for (int i = 0; i < 3; i++) m1[i] += rho[v[a]] * xyz[3 * (int64_t)v[b] + i] * V * (a == b ? 2.0 : 1.0) / 20.0;
+  }
+  double c[3] = {0, 0, 0}, p[3] = {0, 0, 0}, q[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  if (Q != 0.0)
+    for (int i = 0; i < 3; i++) c[i] = m1[i] / Q;
+  for (int64_t t = 0; t < nt; t++) {
+    const int32_t *v = h->tets + 4 * t;
+    double V = h->vol[t];
+    double y[4][3];
+    for (int a = 0; a < 4; a++)
+      for (int i = 0; i < 3; i++) y[a][i] = xyz[3 * (int64_t)v[a] + i] - c[i];
+    for (int a = 0; a < 4; a++)
+      for (int b = 0; b < 4; b++) {
+        double w2 = V * (a == b ? 2.0 : 1.0) / 20.0;
+        for (int i = 0; i < 3; i++) p[i] += rho[v[a]] * y[b][i] * w2;
+        for (int cc = 0; cc < 4; cc++) {
+          /* int lambda_a lambda_b lambda_c = alpha! |T| / 120 */
+          double al = (a == b && b == cc) ? 6.0 : ((a == b || b == cc || a == cc) ? 2.0 : 1.0);
+          double w3 = V * al / 120.0;
+          for (int i = 0; i < 3; i++)
+            for (int j = 0; j < 3; j++) q[i][j] += rho[v[a]] * y[b][i] * y[cc][j] * w3;
+        }
+      }
+  }
+  if (mom) {
+    mom[0] = Q;
+    for (int i = 0; i < 3; i++) { mom[1 + i] = c[i]; mom[4 + i] = p[i]; mom[7 + i] = q[i][i]; }
+  }
+  /* boundary values */
+  double *w = (double *)calloc(nn, sizeof(double));
+  double *bvec = (double *)calloc(n > 0 ? n : 1, sizeof(double));
+  if (!w || !bvec) { free(w); free(bvec); return OR_E_NOMEM; }
+  for (int64_t vtx = 0; vtx < nn; vtx++) {
+    if (h->free_of_node[vtx] >= 0) continue;
+    double d[3], r2 = 0.0;
+    for (int i = 0; i < 3; i++) { d[i] = xyz[3 * vtx + i] - c[i]; r2 += d[i] * d[i]; }
+    double r = sqrt(r2);
+    double s = Q / r;
+    for (int i = 0; i < 3; i++) s += p[i] * d[i] / (r2 * r);
+    for (int i = 0; i < 3; i++)
+      for (int j = 0; j < 3; j++) s += 0.5 * q[i][j] * (3.0 * d[i] * d[j] - (i == j ? r2 : 0.0)) / (r2 * r2 * r);
+    w[vtx] = s;
+  }
+  /* load vector with the Dirichlet lift, element by element */
+  for (int64_t t = 0; t < nt; t++) {
+    const int32_t *v = h->tets + 4 * t;
+    const double *g = h->grad + 12 * t;
+    double V = h->vol[t];
+    for (int a = 0; a < 4; a++) {
+      int32_t ia = h->free_of_node[v[a]];
+      if (ia < 0) continue;
+      double s = 0.0;
+      for (int b = 0; b < 4; b++) {
+        s += 4.0 * PI * V * (a == b ? 2.0 : 1.0) / 20.0 * rho[v[b]];
+        if (h->free_of_node[v[b]] < 0) {
+          double kab = V * (g[3 * a] * g[3 * b] + g[3 * a + 1] * g[3 * b + 1] + g[3 * a + 2] * g[3 * b + 2]);
+          s -= kab * w[v[b]];
+        }
+      }
+      bvec[ia] += s;
+    }
+  }
+  /* Jacobi-PCG on K from x0 = 0 */
+  double *x = (double *)calloc(n > 0 ? n : 1, sizeof(double));
+  double *r = (double *)malloc(sizeof(double) * (n > 0 ? n : 1));
+  double *z = (double *)malloc(sizeof(double) * (n > 0 ? n : 1));
+  double *pp = (double *)malloc(sizeof(double) * (n > 0 ? n : 1));
+  double *qq = (double *)malloc(sizeof(double) * (n > 0 ? n : 1));
+  double *dK = (double *)malloc(sizeof(double) * (n > 0 ? n : 1));
+  for (int64_t i = 0; i < n; i++)
+    for (int64_t k = h->row_ptr[i]; k < h->row_ptr[i + 1]; k++)
+      if (h->col[k] == i) dK[i] = h->K[k];
+  double bn = 0.0;
+  for (int64_t i = 0; i < n; i++) { r[i] = bvec[i]; z[i] = r[i] / dK[i]; pp[i] = z[i]; bn += bvec[i] * bvec[i]; }
+  bn = sqrt(bn);
+  double rz = 0.0;
+  for (int64_t i = 0; i < n; i++) rz += r[i] * z[i];
+  int it = 0, st = OR_OK;
+  for (;;) {
+    double rr = 0.0;
+    for (int64_t i = 0; i < n; i++) rr += r[i] * r[i];
+    if (sqrt(rr) <= tol * bn) break;
+    if (it >= max_iter) { st = OR_E_NOT_CONVERGED; break; }
+    matvec(h, h->K, pp, qq);
+    double pq = 0.0;
+    for (int64_t i = 0; i < n; i++) pq += pp[i] * qq[i];
+    double al = rz / pq;
+    for (int64_t i = 0; i < n; i++) { x[i] += al * pp[i]; r[i] -= al * qq[i]; z[i] = r[i] / dK[i]; }
+    double rz2 = 0.0;
+    for (int64_t i = 0; i < n; i++) rz2 += r[i] * z[i];
+    double be = rz2 / rz;
+    rz = rz2;
+    for (int64_t i = 0; i < n; i++) pp[i] = z[i] + be * pp[i];
+    it++;
+  }
+  for (int64_t vtx = 0; vtx < nn; vtx++) {
+    int32_t i = h->free_of_node[vtx];
+    vh[vtx] = i >= 0 ? x[i] : w[vtx];
+  }
+  if (iters) *iters = it;
+  free(w); free(bvec); free(x); free(r); free(z); free(pp); free(qq); free(dK);
+  return st;
+}

@@ -269,6 +269,18 @@ ks_status ks_interpolation(ks_ctx *ctx, int64_t n_c, const double *h_xyz_c, int6
                                h_n_H, h_p_nnz);
 }
 
+ks_status ks_density(ks_ctx *ctx, int32_t N, const double *d_U, double f, double *d_rho) {
+  if (!ctx) return KS_E_ARG;
+  if (N < 1 || N > KS_MAX_N || !d_U || !d_rho || !(f >= 0.0)) return ks_fail(ctx, KS_E_ARG, "ks_density: bad arguments");
+  return ks_density_impl(ctx, N, d_U, f, d_rho);
+}
+
+ks_status ks_vxc(ks_ctx *ctx, const double *d_rho, double *d_vxc, double *d_eps) {
+  if (!ctx) return KS_E_ARG;
+  if (!d_rho || !d_vxc) return ks_fail(ctx, KS_E_ARG, "ks_vxc: null pointer");
+  return ks_vxc_impl(ctx, d_rho, d_vxc, d_eps);
+}
+
 ks_status ks_solve_trace(ks_ctx *ctx, int32_t cap, uint64_t *h_ns, int32_t *h_count) {
   if (!ctx || !h_count || (cap > 0 && !h_ns)) return KS_E_ARG;
   *h_count = 0;

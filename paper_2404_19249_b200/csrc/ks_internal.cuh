@@ -2,6 +2,7 @@
 // Not part of the ABI; see include/ks.h.
 #pragma once
 #include <cuda_runtime.h>
+#include <math_constants.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <string>
@@ -172,6 +173,8 @@ ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, cons
 ks_status ks_project_impl(ks_ctx *ctx, int N, const double *Ut, double *FA, double *FB);
 void ks_free_coarse(ks_ctx *ctx);
 void ks_free_outer(ks_ctx *ctx);
+ks_status ks_density_impl(ks_ctx *ctx, int N, const double *U, double f, double *rho);
+ks_status ks_vxc_impl(ks_ctx *ctx, const double *rho, double *vxc, double *eps);
 ks_status ks_interpolation_impl(ks_ctx *ctx, int64_t n_c, const double *h_xyz_c, int64_t m_c, const int32_t *h_tets_c,
                                 const uint8_t *h_dir_c, int32_t *d_rowptr, int32_t *d_col, double *d_val,
                                 int64_t *h_nH, int64_t *h_pnnz);

@@ -25,7 +25,7 @@ OPS = {"K": 0, "M": 1, "MV": 2, "H": 3, "A": 4}
 EXPORTS = ["ks_abi_version", "ks_build_info", "ks_create", "ks_destroy", "ks_set_stream", "ks_pattern",
            "ks_values", "ks_assemble_veff", "ks_spmm", "ks_block_solve", "ks_last_iterations", "ks_solve_trace",
            "ks_true_residual", "ks_set_coarse", "ks_project_augmented", "ks_pencil_eig", "ks_lift",
-           "ks_augmented_solve", "ks_interpolation", "ks_memory_bytes", "ks_launch_count", "ks_sync", "ks_last_error"]
+           "ks_augmented_solve", "ks_interpolation", "ks_density", "ks_vxc", "ks_memory_bytes", "ks_launch_count", "ks_sync", "ks_last_error"]
 
 
 class KSError(RuntimeError):
@@ -67,6 +67,8 @@ def load_library(path: str = LIB_PATH):
         "ks_lift": (st, [vp, i32, vp, i32, vp, vp]),
         "ks_augmented_solve": (st, [vp, i32, vp, vp, dbl, i32, dbl, i32, C.POINTER(i32), vp]),
         "ks_interpolation": (st, [vp, i64, vp, i64, vp, vp, vp, vp, vp, C.POINTER(i64), C.POINTER(i64)]),
+        "ks_density": (st, [vp, i32, vp, dbl, vp]),
+        "ks_vxc": (st, [vp, vp, vp, vp]),
         "ks_memory_bytes": (st, [vp, C.POINTER(C.c_size_t)]),
         "ks_launch_count": (st, [vp, C.POINTER(i64)]),
         "ks_sync": (st, [vp]),
@@ -295,6 +297,26 @@ class Context:
                                             tets_c.ctypes.data, dir_c.ctypes.data, _ptr(rp), _ptr(col), _ptr(val),
                                             C.byref(nH), C.byref(pn)))
         return rp, col[:pn.value], val[:pn.value], nH.value
+
+    def density(self, U, f=2.0, rho=None):
+        """ks_density: nodal density on all nodes."""
+        import torch
+        _check_cuda_tensor(U, torch.float64, None, "U")
+        if rho is None:
+            rho = torch.empty(self.n_nodes, dtype=torch.float64, device=U.device)
+        self._call(self._L.ks_density(self._h, U.shape[1], _ptr(U), float(f), _ptr(rho)))
+        return rho
+
+    def vxc(self, rho, vxc=None, eps=None):
+        """ks_vxc: LDA/PZ exchange-correlation potential (and energy per electron) on all nodes."""
+        import torch
+        _check_cuda_tensor(rho, torch.float64, (self.n_nodes,), "rho")
+        if vxc is None:
+            vxc = torch.empty_like(rho)
+        if eps is None:
+            eps = torch.empty_like(rho)
+        self._call(self._L.ks_vxc(self._h, _ptr(rho), _ptr(vxc), _ptr(eps)))
+        return vxc, eps
 
     def memory_bytes(self) -> int:
         v = C.c_size_t()
