@@ -230,6 +230,19 @@ ks_status ks_interpolation(ks_ctx *ctx, int64_t n_c, const double *h_xyz_c, int6
 ks_status ks_density(ks_ctx *ctx, int32_t N, const double *d_U, double f, double *d_rho);
 ks_status ks_vxc(ks_ctx *ctx, const double *d_rho, double *d_vxc, double *d_eps);
 
+/*
+ * ks_hartree: the Hartree potential: -Lap V = 4 pi rho, V = w_D on the boundary with the
+ * multipole expansion of Eq. bd about the centre of charge (monopole, dipole, quadrupole with the 1/2 of the
+ * Taylor term, reading R5; moments exact for the P1 density); P1 Galerkin with the Dirichlet lift,
+ * the free values by the batched Jacobi-PCG (N = 1) on the stiffness matrix to ||r|| <= tol ||b||.
+ *   d_rho [n_nodes]; d_vh [n_nodes] (out: free values and w_D; in when warm != 0: the warm start);
+ *   h_mom [10] (host, may be NULL): Q, centre (3), dipole (3), diagonal of the second moment (3);
+ *   h_iters (host, may be NULL): PCG iterations. Synchronises the stream when h_mom or h_iters is given.
+ *   Latches KS_E_NOT_CONVERGED (ks_sync) when max_iter is reached.
+ */
+ks_status ks_hartree(ks_ctx *ctx, const double *d_rho, double tol, int32_t max_iter, double *d_vh, int32_t warm,
+                     double *h_mom, int32_t *h_iters);
+
 /* Device memory owned by the library (bytes). */
 ks_status ks_memory_bytes(const ks_ctx *ctx, size_t *bytes);
 

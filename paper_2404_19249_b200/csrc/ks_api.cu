@@ -281,6 +281,13 @@ ks_status ks_vxc(ks_ctx *ctx, const double *d_rho, double *d_vxc, double *d_eps)
   return ks_vxc_impl(ctx, d_rho, d_vxc, d_eps);
 }
 
+ks_status ks_hartree(ks_ctx *ctx, const double *d_rho, double tol, int32_t max_iter, double *d_vh, int32_t warm,
+                     double *h_mom, int32_t *h_iters) {
+  if (!ctx) return KS_E_ARG;
+  if (!d_rho || !d_vh || !(tol > 0.0) || max_iter < 1) return ks_fail(ctx, KS_E_ARG, "ks_hartree: bad arguments");
+  return ks_hartree_impl(ctx, d_rho, tol, max_iter, d_vh, warm, h_mom, h_iters);
+}
+
 ks_status ks_solve_trace(ks_ctx *ctx, int32_t cap, uint64_t *h_ns, int32_t *h_count) {
   if (!ctx || !h_count || (cap > 0 && !h_ns)) return KS_E_ARG;
   *h_count = 0;

@@ -48,6 +48,8 @@ struct ks_ctx {
   int32_t *sell_ptr = nullptr;      // [n_slices+1] first entry of each 8-row slice
   int32_t *sell_col = nullptr;      // [sell_total]
   double *sell_A = nullptr, *sell_M = nullptr, *sell_H = nullptr;  // [sell_total]
+  double *sell_K = nullptr;         // [sell_total] stiffness (Poisson operator of the Hartree solve)
+  double *dinvK = nullptr;          // [n_free + 2] 1 / diag(K)
   double *v_free = nullptr;         // [n_free] V at free nodes (assembly scratch)
   double mu = 0.0;
   bool assembled = false;
@@ -62,7 +64,7 @@ struct ks_ctx {
   // solver workspace (grown on demand)
   int ws_np = 0;                    // padded N the workspace was sized for
   int64_t ws_rows = 0;
-  double *r = nullptr, *p = nullptr, *q = nullptr, *xpad = nullptr, *upad = nullptr;
+  double *r = nullptr, *p = nullptr, *q = nullptr, *xpad = nullptr, *upad = nullptr, *bpad = nullptr;
   double *partials = nullptr;       // [grid][4 * 64]
   unsigned *barrier = nullptr;      // grid barrier counter
   int64_t partial_cap = 0;
@@ -95,6 +97,10 @@ struct ks_ctx {
   double *gram_part = nullptr;   // [blocks][2 N N]
   int64_t gram_cap = 0;
 
+  // NEXT-2 Hartree workspace (ks_scf.cu)
+  double *har_w = nullptr, *har_c = nullptr, *har_b = nullptr, *har_x0 = nullptr, *har_x = nullptr;
+  double *har_mom = nullptr, *har_part = nullptr;
+  int32_t *har_iters = nullptr;
   int interp_fallbacks = 0;         // last ks_interpolation needed the scan fallback of the walk
   // NEXT-1 (ks_outer.cu): cuSOLVER handle, pencil and outer-loop workspaces
   void *cusolver = nullptr;
@@ -166,6 +172,9 @@ ks_status ks_materialize_views(ks_ctx *ctx);
 ks_status ks_spmm_impl(ks_ctx *ctx, ks_op op, const double *val, int N, const double *X, double *Y);
 ks_status ks_solve_impl(ks_ctx *ctx, int N, const double *lambda, const double *U, double *Ut, double tol,
                         int max_iter, int32_t *iters, double *relres);
+ks_status ks_pcg_run(ks_ctx *ctx, const double *sell_vals, const double *dinv, double mu, int N,
+                     const double *lambda, const double *B, const double *U, double *Ut, double tol, int max_iter,
+                     int32_t *iters, double *relres);
 ks_status ks_true_residual_impl(ks_ctx *ctx, int N, const double *lambda, const double *U,
                                 const double *Ut, double *relres);
 ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, const int32_t *Pcol,
@@ -175,6 +184,8 @@ void ks_free_coarse(ks_ctx *ctx);
 void ks_free_outer(ks_ctx *ctx);
 ks_status ks_density_impl(ks_ctx *ctx, int N, const double *U, double f, double *rho);
 ks_status ks_vxc_impl(ks_ctx *ctx, const double *rho, double *vxc, double *eps);
+ks_status ks_hartree_impl(ks_ctx *ctx, const double *rho, double tol, int max_iter, double *vh, int warm,
+                          double *h_mom, int32_t *h_iters);
 ks_status ks_interpolation_impl(ks_ctx *ctx, int64_t n_c, const double *h_xyz_c, int64_t m_c, const int32_t *h_tets_c,
                                 const uint8_t *h_dir_c, int32_t *d_rowptr, int32_t *d_col, double *d_val,
                                 int64_t *h_nH, int64_t *h_pnnz);

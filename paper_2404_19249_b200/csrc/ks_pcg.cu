@@ -63,7 +63,8 @@ struct PcgArgs {
   const double *A, *M, *dinv;   // A, M: sliced-ELL values
   const double *lambda;
   double mu, tol;
-  const double *U;      // [n][NP] input (possibly padded copy)
+  const double *U;      // [n][NP] input (possibly padded copy): u_i, and x0 (warm start)
+  const double *B;      // [n][NP] given right-hand side (Poisson mode), or null: b = (lambda + mu) M u
   double *X;            // [n][NP] solution
   double *r, *p, *q;    // [n][NP] workspace
   double *partials;     // [G][4*NP]
@@ -153,14 +154,21 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
 #pragma unroll
     for (int v = 0; v < VEC; v++) {
       int c = sub * VEC + v;
-      sh[v] = (c < a.N ? __ldg(a.lambda + c) : 0.0) + a.mu;
+      sh[v] = (c < a.N && a.lambda ? __ldg(a.lambda + c) : 0.0) + a.mu;
     }
     for (int tile = blockIdx.x; tile < a.ntiles; tile += G) {
       int64_t row = (int64_t)tile * TILE + warp * RPW + slot;
       if (row < n) {
         DV<VEC> au, mu_;
-        sell_row<NP, 2>(a.sell_ptr, a.sell_col, a.A, a.M, row, a.U, sub, au, mu_);
         const int64_t off = row * NP + sub * VEC;
+        if (a.B) {   // Poisson mode: the right-hand side is given (grid-uniform branch)
+          sell_row<NP, 1>(a.sell_ptr, a.sell_col, a.A, nullptr, row, a.U, sub, au, mu_);
+          mu_ = DV<VEC>::ld(a.B + off);
+#pragma unroll
+          for (int v = 0; v < VEC; v++) sh[v] = 1.0;
+        } else {
+          sell_row<NP, 2>(a.sell_ptr, a.sell_col, a.A, a.M, row, a.U, sub, au, mu_);
+        }
         const DV<VEC> u = DV<VEC>::ld(a.U + off);
         const double dinv = __ldg(a.dinv + row);
         DV<VEC> r, z;
@@ -526,7 +534,7 @@ ks_status ks_spmm_impl(ks_ctx *ctx, ks_op op, const double *val, int N, const do
 
 static ks_status ensure_solver_ws(ks_ctx *ctx, int np) {
   if (ctx->ws_np >= np && ctx->ws_rows == ctx->n_free) return KS_OK;
-  for (double **b : {&ctx->r, &ctx->p, &ctx->q, &ctx->xpad, &ctx->upad})
+  for (double **b : {&ctx->r, &ctx->p, &ctx->q, &ctx->xpad, &ctx->upad, &ctx->bpad})
     ks_free_t(ctx, *b);
   const int64_t cnt = ctx->n_free * (int64_t)np;
   KS_TRY(ks_alloc_t(ctx, &ctx->r, cnt, "pcg r"));
@@ -534,6 +542,7 @@ static ks_status ensure_solver_ws(ks_ctx *ctx, int np) {
   KS_TRY(ks_alloc_t(ctx, &ctx->q, cnt, "pcg q"));
   KS_TRY(ks_alloc_t(ctx, &ctx->xpad, cnt, "pcg x pad"));
   KS_TRY(ks_alloc_t(ctx, &ctx->upad, cnt, "pcg u pad"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->bpad, cnt, "pcg b pad"));
   ctx->ws_np = np;
   ctx->ws_rows = ctx->n_free;
   return KS_OK;
@@ -541,28 +550,42 @@ static ks_status ensure_solver_ws(ks_ctx *ctx, int np) {
 
 ks_status ks_solve_impl(ks_ctx *ctx, int N, const double *lambda, const double *U, double *Ut, double tol,
                         int max_iter, int32_t *iters, double *relres) {
+  return ks_pcg_run(ctx, ctx->sell_A, ctx->dinv, ctx->mu, N, lambda, nullptr, U, Ut, tol, max_iter, iters, relres);
+}
+
+// General batched Jacobi-PCG on a sliced-ELL operator: A x = b with b = (lambda + mu) M u (B == null, the BVPs)
+// or b = B (given, [n][N]; the Poisson solve of the Hartree potential), x0 = U.
+ks_status ks_pcg_run(ks_ctx *ctx, const double *sell_vals, const double *dinv, double mu, int N,
+                     const double *lambda, const double *B, const double *U, double *Ut, double tol, int max_iter,
+                     int32_t *iters, double *relres) {
   const int np = pad_np(N);
   KS_TRY(ensure_solver_ws(ctx, np));
   const int64_t n = ctx->n_free;
-  const bool direct = (np == N) && aligned32(U) && aligned32(Ut);
-  const double *u = U;
+  const bool direct = (np == N) && aligned32(U) && aligned32(Ut) && (!B || aligned32(B));
+  const double *u = U, *bb = B;
   double *x = Ut;
   if (!direct) {
     k_pad<<<ks_blocks(n * np, 256), 256, 0, ctx->stream>>>(U, N, ctx->upad, np, n);
     KS_LAUNCHED(ctx);
     u = ctx->upad;
     x = ctx->xpad;
+    if (B) {   // the given right-hand side is padded into the (not yet used) q buffer
+      k_pad<<<ks_blocks(n * np, 256), 256, 0, ctx->stream>>>(B, N, ctx->bpad, np, n);
+      KS_LAUNCHED(ctx);
+      bb = ctx->bpad;
+    }
   }
   PcgArgs a;
   a.sell_ptr = ctx->sell_ptr;
   a.sell_col = ctx->sell_col;
-  a.A = ctx->sell_A;
+  a.A = sell_vals;
   a.M = ctx->sell_M;
-  a.dinv = ctx->dinv;
+  a.dinv = dinv;
   a.lambda = lambda;
-  a.mu = ctx->mu;
+  a.mu = mu;
   a.tol = tol;
   a.U = u;
+  a.B = bb;
   a.X = x;
   a.r = ctx->r;
   a.p = ctx->p;

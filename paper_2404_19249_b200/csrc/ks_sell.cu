@@ -50,6 +50,14 @@ __global__ void k_sell_fill_val(const int32_t *__restrict__ row_ptr, const doubl
   for (int k = 0; k < K; k++) sval[base + (k >> 2) * (4 * KS_SELL_C) + (k & 3)] = k < len ? val[k0 + k] : 0.0;
 }
 
+__global__ void k_inv_diag(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                           const double *__restrict__ val, int64_t n, double *__restrict__ dinv) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int32_t k = row_ptr[i]; k < row_ptr[i + 1]; k++)
+    if (col[k] == i) dinv[i] = 1.0 / val[k];
+}
+
 }  // namespace
 
 ks_status ks_sell_build(ks_ctx *ctx) {
@@ -82,6 +90,12 @@ ks_status ks_sell_build(ks_ctx *ctx) {
   k_sell_fill_col<<<ks_blocks(n, 256), 256, 0, s>>>(ctx->row_ptr, ctx->col, n, ctx->sell_ptr, ctx->sell_col);
   KS_LAUNCHED(ctx);
   k_sell_fill_val<<<ks_blocks(n, 256), 256, 0, s>>>(ctx->row_ptr, ctx->M, n, ctx->sell_ptr, ctx->sell_M);
+  KS_LAUNCHED(ctx);
+  KS_TRY(ks_alloc_t(ctx, &ctx->sell_K, total, "sell K"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->dinvK, n + 2, "1/diag K"));
+  k_sell_fill_val<<<ks_blocks(n, 256), 256, 0, s>>>(ctx->row_ptr, ctx->K, n, ctx->sell_ptr, ctx->sell_K);
+  KS_LAUNCHED(ctx);
+  k_inv_diag<<<ks_blocks(n, 256), 256, 0, s>>>(ctx->row_ptr, ctx->col, ctx->K, n, ctx->dinvK);
   KS_LAUNCHED(ctx);
   return KS_OK;
 }

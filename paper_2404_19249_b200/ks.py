@@ -25,7 +25,7 @@ OPS = {"K": 0, "M": 1, "MV": 2, "H": 3, "A": 4}
 EXPORTS = ["ks_abi_version", "ks_build_info", "ks_create", "ks_destroy", "ks_set_stream", "ks_pattern",
            "ks_values", "ks_assemble_veff", "ks_spmm", "ks_block_solve", "ks_last_iterations", "ks_solve_trace",
            "ks_true_residual", "ks_set_coarse", "ks_project_augmented", "ks_pencil_eig", "ks_lift",
-           "ks_augmented_solve", "ks_interpolation", "ks_density", "ks_vxc", "ks_memory_bytes", "ks_launch_count", "ks_sync", "ks_last_error"]
+           "ks_augmented_solve", "ks_interpolation", "ks_density", "ks_vxc", "ks_hartree", "ks_memory_bytes", "ks_launch_count", "ks_sync", "ks_last_error"]
 
 
 class KSError(RuntimeError):
@@ -69,6 +69,7 @@ def load_library(path: str = LIB_PATH):
         "ks_interpolation": (st, [vp, i64, vp, i64, vp, vp, vp, vp, vp, C.POINTER(i64), C.POINTER(i64)]),
         "ks_density": (st, [vp, i32, vp, dbl, vp]),
         "ks_vxc": (st, [vp, vp, vp, vp]),
+        "ks_hartree": (st, [vp, vp, dbl, i32, vp, i32, vp, C.POINTER(i32)]),
         "ks_memory_bytes": (st, [vp, C.POINTER(C.c_size_t)]),
         "ks_launch_count": (st, [vp, C.POINTER(i64)]),
         "ks_sync": (st, [vp]),
@@ -317,6 +318,18 @@ class Context:
             eps = torch.empty_like(rho)
         self._call(self._L.ks_vxc(self._h, _ptr(rho), _ptr(vxc), _ptr(eps)))
         return vxc, eps
+
+    def hartree(self, rho, tol=1e-12, max_iter=100000, vh=None, warm=False):
+        """ks_hartree: Hartree potential on all nodes -> (vh, moments [10] numpy, PCG iterations)."""
+        import torch
+        _check_cuda_tensor(rho, torch.float64, (self.n_nodes,), "rho")
+        if vh is None:
+            vh = torch.zeros_like(rho)
+        mom = np.zeros(10)
+        it = C.c_int32()
+        self._call(self._L.ks_hartree(self._h, _ptr(rho), float(tol), int(max_iter), _ptr(vh), int(bool(warm)),
+                                      mom.ctypes.data, C.byref(it)))
+        return vh, mom, it.value
 
     def memory_bytes(self) -> int:
         v = C.c_size_t()

@@ -1,0 +1,78 @@
+"""NEXT-2 on the GPU: nodal density, LDA/PZ exchange-correlation potential and the Hartree
+potential through the C ABI against the oracle (tests/test_oracle_next2.py pins it).
+Tolerances: density and V_xc |d| <= 1e-14 relative (the same pointwise formulas; libdevice vs libm
+cbrt/log differ by an ulp); Hartree moments 1e-12 relative, potential max |d| <= 1e-9 max |V_H| (both PCGs
+to 1e-12)."""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+DEV = "cuda"
+
+
+def dt(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def _ctx(p):
+    import paper_2404_19249_b200 as ks
+    return ks.Context(p.xyz, p.tets, p.dirichlet)
+
+
+@pytest.mark.parametrize("c", [1, 2])
+def test_density_and_vxc_match_oracle(c):
+    p = gen.make_problem(c)
+    ctx = _ctx(p)
+    om = oracle.Mesh.from_problem(p)
+    rho = ctx.density(dt(p.U), f=2.0)
+    v, e = ctx.vxc(rho)
+    rho_o = om.density(p.U, f=2.0)
+    assert np.all(np.abs(rho.cpu().numpy() - rho_o) <= 1e-14 * np.abs(rho_o))
+    v_o, e_o = oracle.vxc(rho_o)
+    assert np.all(np.abs(v.cpu().numpy() - v_o) <= 1e-14 * np.abs(v_o) + 1e-300)
+    assert np.all(np.abs(e.cpu().numpy() - e_o) <= 1e-14 * np.abs(e_o) + 1e-300)
+    # a density sweep across the r_s = 1 switch and tiny / zero densities
+    rs = np.concatenate([np.geomspace(1e-3, 0.999, 40), np.geomspace(1.0, 50.0, 40)])
+    r = np.zeros(p.n_nodes)
+    r[:rs.size] = 3.0 / (4.0 * np.pi * rs ** 3)
+    v, e = ctx.vxc(dt(r))
+    v_o, e_o = oracle.vxc(r)
+    assert np.all(np.abs(v.cpu().numpy() - v_o) <= 1e-14 * np.abs(v_o) + 1e-300)
+
+
+@pytest.mark.parametrize("n,centre", [(16, (0.3, -0.2, 0.1)), (24, (1.0, 0.5, -0.7))])
+def test_hartree_matches_oracle(n, centre):
+    from scipy.special import erf
+    p = gen.make_problem(dict(L=8.0, n=n, grading=None, jitter=0.1, nuclei=[((0.0, 0.0, 0.0), 1)], vnoise=0.0, N=1,
+                              orbitals="exp", lam=("const", -0.5), nc=2, seed=4))
+    r = np.sqrt(((p.xyz - np.asarray(centre)) ** 2).sum(1))
+    rho = 2.0 * (2 * np.pi) ** -1.5 * np.exp(-r ** 2 / 2)
+    ctx = _ctx(p)
+    vh, mom, it = ctx.hartree(dt(rho), tol=1e-12)
+    assert ctx.sync() == 0
+    om = oracle.Mesh.from_problem(p)
+    vh_o, mom_o, it_o = om.hartree(rho, tol=1e-12)
+    assert np.all(np.abs(mom[:4] - mom_o[:4]) <= 1e-12 * (1 + np.abs(mom_o[:4])))
+    assert np.all(np.abs(mom[4:] - mom_o[4:]) <= 1e-12 * (1 + np.abs(mom_o[7:]).max()))
+    vg = vh.cpu().numpy()
+    assert np.abs(vg - vh_o).max() <= 1e-9 * np.abs(vh_o).max()
+    assert abs(it - it_o) <= 3
+    # and the physics: close to the exact potential of the Gaussian charge
+    exact = 2.0 * erf(r / np.sqrt(2)) / np.maximum(r, 1e-300)
+    assert np.abs(vg - exact).max() < 0.2
+
+
+def test_hartree_warm_start_reaches_the_same_potential():
+    p = gen.make_problem(1)
+    ctx = _ctx(p)
+    rho = ctx.density(dt(p.U), f=2.0)
+    vh, _, it_cold = ctx.hartree(rho, tol=1e-12)
+    vh2 = vh.clone()
+    vh2, _, it_warm = ctx.hartree(rho, tol=1e-12, vh=vh2, warm=True)
+    assert it_warm <= 1
+    assert torch.allclose(vh, vh2, rtol=1e-10, atol=0)
