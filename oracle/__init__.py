@@ -105,6 +105,90 @@ def vxc(rho):
     return v, e
 
 
+def anderson_mix(rho_in_hist, rho_out_hist, beta=0.7, depth=5):
+    """NEXT-2: Anderson mixing (Eqs. mix2-mix6) with the histories of input and output
+    densities (oldest first, newest last; only the last `depth` are used). With m the newest index and
+    F^(j) = rho_out^(j) - rho_in^(j), the coefficients alpha_j (j = m0..m-1) solve
+        sum_k (F^m - F^j, F^m - F^k) alpha_k = (F^m - F^j, F^m)                               (mix6)
+    (discrete l2 inner product of the nodal vectors, reading R7), then
+        rho~ = rho^m + sum_j alpha_j (rho^j - rho^m)   for in and out                        (mix4)
+        rho_in^(m+1) = beta rho~_out + (1 - beta) rho~_in.                                    (mix1)"""
+    hin = [np.asarray(x, dtype=np.float64) for x in rho_in_hist[-depth:]]
+    hout = [np.asarray(x, dtype=np.float64) for x in rho_out_hist[-depth:]]
+    F = [o - i for i, o in zip(hin, hout)]
+    m = len(F) - 1
+    alpha = np.zeros(m)
+    if m > 0:
+        G = np.empty((m, m))
+        r = np.empty(m)
+        for j in range(m):
+            dj = F[m] - F[j]
+            r[j] = dj @ F[m]
+            for k in range(m):
+                G[j, k] = dj @ (F[m] - F[k])
+        alpha = np.linalg.solve(G, r)
+    t_in = hin[m] + sum(alpha[j] * (hin[j] - hin[m]) for j in range(m))
+    t_out = hout[m] + sum(alpha[j] * (hout[j] - hout[m]) for j in range(m))
+    return beta * t_out + (1.0 - beta) * t_in
+
+
+def scf_solve(mesh, n_H, P_rowptr, P_col, P_val, V_ext, lam, U, mu, f=2.0, tol=1e-8, max_outer=60, inner=20,
+              inner_tol=None, beta=0.7, depth=5, bvp_tol=1e-12, hartree_tol=1e-12):
+    """NEXT-2: Algorithm 3 for the Kohn-Sham equation, in the paper's order (DESIGN.md
+    reading R8 for the inner loop):
+      outer: V_eff = V_ext + V_Har[rho] + V_xc[rho] -> assemble (st4) -> the N
+             BVPs from (lambda, Psi) (Aux_Linear_Problem) -> Psi~;
+      inner (the small KS equation Nonlinear_Eig_Hh on S_H + span{Psi~}, solved self-consistently with Psi~
+             fixed, at most `inner` steps): project (st1-st7) -> small eigenproblem ->
+             lift -> rho_out = f sum psi^2 -> stop when ||rho_out - rho_in||_M <= inner_tol ||rho_out||_M, else
+             Anderson-mix (depth, beta; PAPER.md:1074-1109) and reassemble st4 with the mixed density;
+      stop when the outer density change ||rho^(l) - rho^(l-1)||_M <= tol ||rho^(l)||_M.
+    Returns dict(lam, U, rho, outer, inner steps per outer, outer density changes, lam history)."""
+    inner_tol = tol if inner_tol is None else inner_tol
+    fr = mesh.free_of_node()
+    order = np.argsort(fr[fr >= 0])
+    Mf = mesh.csr("M")
+
+    def mnorm(x):
+        xf = x[fr >= 0][order]
+        return np.sqrt(xf @ (Mf @ xf))
+
+    def veff(rho):
+        vh, _, _ = mesh.hartree(rho, tol=hartree_tol)
+        return V_ext + vh + vxc(rho)[0]
+
+    rho = mesh.density(U, f)
+    steps, dres, lams = [], [], []
+    for it in range(max_outer):
+        mesh.assemble_veff(veff(rho), mu)
+        r = mesh.block_pcg(lam, U, tol=bvp_tol)
+        if r["status"] != OR_OK:
+            raise OracleError(r["status"], "scf_solve: block_pcg")
+        Ut = r["Ut"]
+        rho_in, hin, hout = rho, [], []
+        for k in range(inner):
+            FA, FB = mesh.project(n_H, P_rowptr, P_col, P_val, Ut)
+            lam, Y = pencil_eig(FA, FB, U.shape[1])
+            U = mesh.lift(n_H, P_rowptr, P_col, P_val, Ut, Y)
+            rho_out = mesh.density(U, f)
+            res = mnorm(rho_out - rho_in) / mnorm(rho_out)
+            if res <= inner_tol or k == inner - 1:
+                break
+            hin.append(rho_in)
+            hout.append(rho_out)
+            rho_in = anderson_mix(hin, hout, beta, depth)
+            mesh.assemble_veff(veff(rho_in), mu)
+        steps.append(k + 1)
+        change = mnorm(rho_out - rho) / mnorm(rho_out)
+        dres.append(change)
+        lams.append(lam.copy())
+        rho = rho_out
+        if change <= tol:
+            break
+    return dict(lam=lam, U=U, rho=rho, outer=len(dres), inner=np.array(steps), dres=np.array(dres),
+                lams=np.array(lams))
+
+
 INTERP_DROP = 1e-13  # |lambda| <= this is dropped from a P row (DESIGN.md reading R4)
 
 
@@ -269,6 +353,9 @@ class Mesh:
         if st != OR_OK:
             raise OracleError(st, "hartree")
         return vh, mom, it.value
+
+    def free_of_node(self):
+        return self.pattern()[3]
 
     def csr(self, which):
         """scipy CSR of one operator (for brute-force pins in tests)."""

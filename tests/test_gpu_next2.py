@@ -1,8 +1,8 @@
 """NEXT-2 on the GPU: nodal density, LDA/PZ exchange-correlation potential and the Hartree
 potential through the C ABI against the oracle (tests/test_oracle_next2.py pins it).
 Tolerances: density and V_xc |d| <= 1e-14 relative (the same pointwise formulas; libdevice vs libm
-cbrt/log differ by an ulp); Hartree moments 1e-12 relative, potential max |d| <= 1e-9 max |V_H| (both PCGs
-to 1e-12)."""
+cbrt/log differ by an ulp); Hartree moments 1e-10 relative (element sums in different orders), potential
+max |d| <= 1e-9 max |V_H| (both PCGs to 1e-12)."""
 import numpy as np
 import pytest
 
@@ -57,8 +57,9 @@ def test_hartree_matches_oracle(n, centre):
     assert ctx.sync() == 0
     om = oracle.Mesh.from_problem(p)
     vh_o, mom_o, it_o = om.hartree(rho, tol=1e-12)
-    assert np.all(np.abs(mom[:4] - mom_o[:4]) <= 1e-12 * (1 + np.abs(mom_o[:4])))
-    assert np.all(np.abs(mom[4:] - mom_o[4:]) <= 1e-12 * (1 + np.abs(mom_o[7:]).max()))
+    # sums over ~10^5..10^6 element terms in different orders (block tree vs sequential): 1e-10 relative
+    assert np.all(np.abs(mom[:4] - mom_o[:4]) <= 1e-10 * (1 + np.abs(mom_o[:4])))
+    assert np.all(np.abs(mom[4:] - mom_o[4:]) <= 1e-10 * (1 + np.abs(mom_o[7:]).max()))
     vg = vh.cpu().numpy()
     assert np.abs(vg - vh_o).max() <= 1e-9 * np.abs(vh_o).max()
     assert abs(it - it_o) <= 3

@@ -112,3 +112,49 @@ def test_hartree_boundary_multipoles_capture_the_quadrupole():
     quad_size = np.abs(exact[bd] - mono).max()
     assert quad_size > 1e-3
     assert np.abs(vh[bd] - exact[bd]).max() < 0.1 * quad_size
+
+
+def test_anderson_depth_one_is_linear_mixing():
+    rng = np.random.default_rng(0)
+    a, b = rng.standard_normal(50), rng.standard_normal(50)
+    assert np.allclose(oracle.anderson_mix([a], [b], beta=0.7, depth=5), 0.7 * b + (1.0 - 0.7) * a, rtol=0, atol=1e-15)
+
+
+def test_anderson_solves_a_linear_fixed_point_like_gmres():
+    """For a linear map rho_out = G rho_in + c (contractive), Anderson mixing with beta = 1 and enough depth
+    reaches the fixed point (I - G)^-1 c in at most dim + 1 steps (its equivalence with GMRES)."""
+    rng = np.random.default_rng(1)
+    d = 4
+    G = 0.5 * rng.standard_normal((d, d)) / np.sqrt(d)
+    c = rng.standard_normal(d)
+    exact = np.linalg.solve(np.eye(d) - G, c)
+    x = np.zeros(d)
+    hin, hout = [], []
+    for _ in range(d + 1):
+        hin.append(x)
+        hout.append(G @ x + c)
+        x = oracle.anderson_mix(hin, hout, beta=1.0, depth=d + 1)
+    assert np.abs(x - exact).max() < 1e-10
+
+
+def test_scf_converges_to_the_fine_kohn_sham_solution():
+    """Algorithm 3 (nonlinear, He-like: Z = 2, one doubly occupied orbital) on a graded fine mesh with a
+    nonnested graded coarse mesh: at convergence the Ritz value is the lowest eigenvalue of the fine-mesh
+    Kohn-Sham operator H[rho] assembled from the converged density (brute-force dense eigensolve), and the
+    outer density change decays linearly."""
+    import scipy.linalg as sl
+    nuc = [((0.0, 0.0, 0.0), 2)]
+    mk = lambda n: gen.make_problem(dict(L=8.0, n=n, grading=("power", 1.8), jitter=0.0, nuclei=nuc, vnoise=0.0,
+                                         N=1, orbitals="gauss", lam=("const", -0.9), nc=2, seed=2))
+    p, c = mk(12), mk(6)
+    rp, col, val, nH = oracle.interpolation(p.xyz, p.free_nodes, c.xyz, c.tets, c.dirichlet)
+    m = oracle.Mesh.from_problem(p)
+    r = oracle.scf_solve(m, nH, rp, col, val, p.V, p.lam.copy(), p.U.copy(), mu=2.0, tol=1e-9, max_outer=60,
+                         inner=30)
+    assert r["dres"][-1] <= 1e-9 and r["outer"] < 60
+    vh, _, _ = m.hartree(r["rho"], tol=1e-13)
+    m.assemble_veff(p.V + vh + oracle.vxc(r["rho"])[0], 2.0)
+    w = sl.eigh(m.csr("H").toarray(), m.csr("M").toarray(), eigvals_only=True)[0]
+    assert abs(r["lam"][0] - w) < 1e-7 * abs(w), (r["lam"], w)
+    tail = r["dres"][-6:]
+    assert np.all(tail[1:] < tail[:-1])
