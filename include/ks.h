@@ -243,6 +243,26 @@ ks_status ks_vxc(ks_ctx *ctx, const double *d_rho, double *d_vxc, double *d_eps)
 ks_status ks_hartree(ks_ctx *ctx, const double *d_rho, double tol, int32_t max_iter, double *d_vh, int32_t warm,
                      double *h_mom, int32_t *h_iters);
 
+/*
+ * ks_scf_solve: Algorithm 3 for the Kohn-Sham equation on the context's mesh and coarse
+ * space (ks_set_coarse), with Anderson mixing:
+ *   outer: V_eff = V_ext + V_Har[rho] + V_xc[rho] -> ks_assemble_veff(V_eff, mu) -> the N BVPs from
+ *          (lambda, Psi) -> Psi~;
+ *   inner (the small Kohn-Sham equation on S_H + span{Psi~}, self-consistent with Psi~ fixed, at most `inner`
+ *          steps; reading R8): projection -> pencil eig -> lift -> rho_out = f sum psi^2; stop when
+ *          ||rho_out - rho_in||_M <= inner_tol ||rho_out||_M, else Anderson-mix (depth <= 7, beta) and
+ *          reassemble with the mixed density;
+ *   stop when the outer density change ||rho^(l) - rho^(l-1)||_M <= tol ||rho^(l)||_M.
+ *   d_vext [n_nodes] (the external potential, e.g. smoothed Coulomb); f occupation per orbital; mu shift;
+ *   d_lambda [N], d_U [n_free][N] (in: initial, out: converged); host outputs (may be NULL): h_outer,
+ *   h_inner [max_outer] inner steps, h_dres [max_outer] outer density changes, h_lams [max_outer][N].
+ *   Synchronises. Errors: as the calls it makes; KS_E_NOT_CONVERGED after max_outer (last iterate kept).
+ */
+ks_status ks_scf_solve(ks_ctx *ctx, int32_t N, const double *d_vext, double f, double mu, double *d_lambda,
+                       double *d_U, double tol, int32_t max_outer, int32_t inner, double inner_tol, double beta,
+                       int32_t depth, double bvp_tol, double hartree_tol, int32_t *h_outer, int32_t *h_inner,
+                       double *h_dres, double *h_lams);
+
 /* Device memory owned by the library (bytes). */
 ks_status ks_memory_bytes(const ks_ctx *ctx, size_t *bytes);
 

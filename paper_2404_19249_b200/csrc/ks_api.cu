@@ -288,6 +288,20 @@ ks_status ks_hartree(ks_ctx *ctx, const double *d_rho, double tol, int32_t max_i
   return ks_hartree_impl(ctx, d_rho, tol, max_iter, d_vh, warm, h_mom, h_iters);
 }
 
+ks_status ks_scf_solve(ks_ctx *ctx, int32_t N, const double *d_vext, double f, double mu, double *d_lambda,
+                       double *d_U, double tol, int32_t max_outer, int32_t inner, double inner_tol, double beta,
+                       int32_t depth, double bvp_tol, double hartree_tol, int32_t *h_outer, int32_t *h_inner,
+                       double *h_dres, double *h_lams) {
+  if (!ctx) return KS_E_ARG;
+  if (N < 1 || N > KS_MAX_N || !d_vext || !d_lambda || !d_U || !(f >= 0.0) || !(mu >= 0.0) || !(tol > 0.0) ||
+      max_outer < 1 || inner < 1 || !(inner_tol > 0.0) || !(beta > 0.0 && beta <= 1.0) || depth < 1 || depth > 7 ||
+      !(bvp_tol > 0.0) || !(hartree_tol > 0.0))
+    return ks_fail(ctx, KS_E_ARG, "ks_scf_solve: bad arguments");
+  if (ctx->n_H < 1) return ks_fail(ctx, KS_E_STATE, "ks_scf_solve: call ks_set_coarse first");
+  return ks_scf_solve_impl(ctx, N, d_vext, f, mu, d_lambda, d_U, tol, max_outer, inner, inner_tol, beta, depth,
+                           bvp_tol, hartree_tol, h_outer, h_inner, h_dres, h_lams);
+}
+
 ks_status ks_solve_trace(ks_ctx *ctx, int32_t cap, uint64_t *h_ns, int32_t *h_count) {
   if (!ctx || !h_count || (cap > 0 && !h_ns)) return KS_E_ARG;
   *h_count = 0;

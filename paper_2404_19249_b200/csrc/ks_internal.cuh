@@ -101,6 +101,13 @@ struct ks_ctx {
   double *har_w = nullptr, *har_c = nullptr, *har_b = nullptr, *har_x0 = nullptr, *har_x = nullptr;
   double *har_mom = nullptr, *har_part = nullptr;
   int32_t *har_iters = nullptr;
+  // NEXT-2 SCF driver workspace
+  double *scf_rho = nullptr, *scf_in = nullptr, *scf_out = nullptr, *scf_vh = nullptr, *scf_vxc = nullptr;
+  double *scf_veff = nullptr, *scf_Ut = nullptr, *scf_FA = nullptr, *scf_FB = nullptr, *scf_Y = nullptr;
+  double *scf_hin = nullptr, *scf_hout = nullptr, *scf_part = nullptr, *scf_red = nullptr, *scf_alpha = nullptr;
+  int *scf_slot = nullptr;
+  int64_t scf_nn = 0, scf_D = 0;
+  int scf_N = 0, scf_depth = 0;
   int interp_fallbacks = 0;         // last ks_interpolation needed the scan fallback of the walk
   // NEXT-1 (ks_outer.cu): cuSOLVER handle, pencil and outer-loop workspaces
   void *cusolver = nullptr;
@@ -184,6 +191,10 @@ void ks_free_coarse(ks_ctx *ctx);
 void ks_free_outer(ks_ctx *ctx);
 ks_status ks_density_impl(ks_ctx *ctx, int N, const double *U, double f, double *rho);
 ks_status ks_vxc_impl(ks_ctx *ctx, const double *rho, double *vxc, double *eps);
+ks_status ks_scf_solve_impl(ks_ctx *ctx, int N, const double *vext, double f, double mu, double *lambda, double *U,
+                            double tol, int max_outer, int inner, double inner_tol, double beta, int depth,
+                            double bvp_tol, double hartree_tol, int32_t *h_outer, int32_t *h_inner, double *h_dres,
+                            double *h_lams);
 ks_status ks_hartree_impl(ks_ctx *ctx, const double *rho, double tol, int max_iter, double *vh, int warm,
                           double *h_mom, int32_t *h_iters);
 ks_status ks_interpolation_impl(ks_ctx *ctx, int64_t n_c, const double *h_xyz_c, int64_t m_c, const int32_t *h_tets_c,

@@ -2,6 +2,9 @@
 //   ks_density   nodal density rho = f sum_i psi_i^2 (occupation f, reading R6)
 //   ks_vxc       LDA exchange + Perdew-Zunger correlation potential (Eqs. expot, copot)
 // Pointwise over all nodes, fp64 (libdevice cbrt / log / sqrt).
+#include <cmath>
+#include <vector>
+
 #include "ks_internal.cuh"
 
 namespace {
@@ -300,5 +303,280 @@ ks_status ks_hartree_impl(ks_ctx *ctx, const double *rho, double tol, int max_it
     }
     if (h_iters) *h_iters = it;
   }
+  return KS_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Algorithm 3 for the Kohn-Sham equation with Anderson mixing
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+constexpr int SB = 256;
+constexpr int AMAX = 8;   // largest Anderson depth
+
+__global__ void k_veff(const double *__restrict__ vext, const double *__restrict__ vh, const double *__restrict__ vxc,
+                       int64_t n, double *__restrict__ veff) {
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v < n) veff[v] = vext[v] + vh[v] + vxc[v];
+}
+
+// partials of x_f^T (M x_f) for the free part of a nodal vector x = a - b (b may be null): one SELL row per
+// thread, fixed-order block tree
+__global__ void __launch_bounds__(SB) k_mnorm2(const int32_t *__restrict__ sell_ptr, const int32_t *__restrict__ sell_col,
+                                               const double *__restrict__ M, const int32_t *__restrict__ node_of_free,
+                                               const double *__restrict__ a, const double *__restrict__ b, int64_t n,
+                                               double *__restrict__ part) {
+  __shared__ double sm[SB];
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)SB + threadIdx.x; i < n; i += (int64_t)gridDim.x * SB) {
+    const int64_t s = i / KS_SELL_C;
+    const int32_t bs = __ldg(sell_ptr + s), e = __ldg(sell_ptr + s + 1);
+    const int K = (e - bs) / KS_SELL_C;
+    const int64_t base = bs + (i % KS_SELL_C) * 4;
+    const int64_t vi = __ldg(node_of_free + i);
+    const double xi = __ldg(a + vi) - (b ? __ldg(b + vi) : 0.0);
+    double mx = 0.0;
+    for (int k = 0; k < K; k++) {
+      const int64_t o = base + (k >> 2) * (4 * KS_SELL_C) + (k & 3);
+      const int64_t vj = __ldg(node_of_free + __ldg(sell_col + o));
+      const double xj = __ldg(a + vj) - (b ? __ldg(b + vj) : 0.0);
+      mx = fma(__ldg(M + o), xj, mx);
+    }
+    acc = fma(xi, mx, acc);
+  }
+  sm[threadIdx.x] = acc;
+  __syncthreads();
+  for (int st = SB / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) sm[threadIdx.x] += sm[threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sm[0];
+}
+
+// Anderson Gram: with F_j = out_j - in_j (slots in age order, m = newest), D_j = F_m - F_j (j < m):
+// G[j][k] = (D_j, D_k), r[j] = (D_j, F_m); partials [nblk][m*m + m]
+__global__ void __launch_bounds__(SB) k_anderson_gram(const double *__restrict__ hin, const double *__restrict__ hout,
+                                                      const int *__restrict__ slot, int m, int64_t n,
+                                                      double *__restrict__ part) {
+  __shared__ double sm[(AMAX * AMAX + AMAX) * 32];
+  const int nv = m * m + m;
+  double acc[AMAX * AMAX + AMAX];
+  for (int k = 0; k < nv; k++) acc[k] = 0.0;
+  const int64_t sm_ = slot[m];
+  for (int64_t v = blockIdx.x * (int64_t)SB + threadIdx.x; v < n; v += (int64_t)gridDim.x * SB) {
+    const double Fm = hout[sm_ * n + v] - hin[sm_ * n + v];
+    double D[AMAX];
+    for (int j = 0; j < m; j++) D[j] = Fm - (hout[(int64_t)slot[j] * n + v] - hin[(int64_t)slot[j] * n + v]);
+    for (int j = 0; j < m; j++) {
+      for (int k = 0; k < m; k++) acc[j * m + k] += D[j] * D[k];
+      acc[m * m + j] += D[j] * Fm;
+    }
+  }
+  // fixed-order: warp butterflies, then warps in order
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = 0; k < nv; k++) {
+    double s = acc[k];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) sm[k * 32 + warp] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < nv) {
+    double s = 0.0;
+    for (int w = 0; w < SB / 32; w++) s += sm[threadIdx.x * 32 + w];
+    part[(int64_t)blockIdx.x * nv + threadIdx.x] = s;
+  }
+}
+
+__global__ void k_sum_partials(const double *__restrict__ part, int nblk, int nv, double *__restrict__ out) {
+  const int k = threadIdx.x;
+  if (k >= nv) return;
+  double s = 0.0;
+  for (int b = 0; b < nblk; b++) s += part[(int64_t)b * nv + k];
+  out[k] = s;
+}
+
+// rho = beta (out_m + sum a_j (out_j - out_m)) + (1 - beta)(in_m + sum a_j (in_j - in_m))
+__global__ void k_anderson_combine(const double *__restrict__ hin, const double *__restrict__ hout,
+                                   const int *__restrict__ slot, const double *__restrict__ alpha, int m,
+                                   double beta, int64_t n, double *__restrict__ rho) {
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const int64_t sm_ = slot[m];
+  const double im = hin[sm_ * n + v], om = hout[sm_ * n + v];
+  double ti = im, to = om;
+  for (int j = 0; j < m; j++) {
+    ti += alpha[j] * (hin[(int64_t)slot[j] * n + v] - im);
+    to += alpha[j] * (hout[(int64_t)slot[j] * n + v] - om);
+  }
+  rho[v] = beta * to + (1.0 - beta) * ti;
+}
+
+}  // namespace
+
+static ks_status scf_alloc(ks_ctx *ctx, int N, int depth) {
+  const int64_t nn = ctx->n_nodes, n = ctx->n_free, D = ctx->n_H + N;
+  if (ctx->scf_nn == nn && ctx->scf_N >= N && ctx->scf_depth >= depth && ctx->scf_D >= D) return KS_OK;
+  for (double **b : {&ctx->scf_rho, &ctx->scf_in, &ctx->scf_out, &ctx->scf_vh, &ctx->scf_vxc, &ctx->scf_veff,
+                     &ctx->scf_Ut, &ctx->scf_FA, &ctx->scf_FB, &ctx->scf_Y, &ctx->scf_hin, &ctx->scf_hout,
+                     &ctx->scf_part, &ctx->scf_red, &ctx->scf_alpha})
+    ks_free_t(ctx, *b);
+  ks_free_t(ctx, ctx->scf_slot);
+  KS_TRY(ks_alloc_t(ctx, &ctx->scf_rho, nn, "scf rho"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->scf_in, nn, "scf rho_in"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->scf_out, nn, "scf rho_out"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->scf_vh, nn, "scf V_H"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->scf_vxc, nn, "scf V_xc"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->scf_veff, nn, "scf V_eff"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->scf_Ut, n * N, "scf U~"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->scf_FA, D * D, "scf F_A"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->scf_FB, D * D, "scf F_B"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->scf_Y, D * N, "scf Y"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->scf_hin, (int64_t)depth * nn, "anderson in"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->scf_hout, (int64_t)depth * nn, "anderson out"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->scf_part, (int64_t)4 * ctx->sm_count * (AMAX * AMAX + AMAX), "scf partials"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->scf_red, AMAX * AMAX + AMAX, "scf reductions"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->scf_alpha, AMAX, "anderson alpha"));
+  KS_TRY(ks_alloc_t(ctx, &ctx->scf_slot, AMAX + 1, "anderson slots"));
+  ctx->scf_nn = nn;
+  ctx->scf_N = N;
+  ctx->scf_depth = depth;
+  ctx->scf_D = D;
+  return KS_OK;
+}
+
+// ||a - b||_M over the free nodes (b may be null), synchronises
+static ks_status mnorm(ks_ctx *ctx, const double *a, const double *b, double *out) {
+  const int nblk = 4 * ctx->sm_count;
+  k_mnorm2<<<nblk, SB, 0, ctx->stream>>>(ctx->sell_ptr, ctx->sell_col, ctx->sell_M, ctx->node_of_free, a, b,
+                                          ctx->n_free, ctx->scf_part);
+  KS_LAUNCHED(ctx);
+  k_sum_partials<<<1, 32, 0, ctx->stream>>>(ctx->scf_part, nblk, 1, ctx->scf_red);
+  KS_LAUNCHED(ctx);
+  double v = 0.0;
+  KS_CUDA(ctx, cudaMemcpyAsync(&v, ctx->scf_red, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  *out = std::sqrt(v > 0.0 ? v : 0.0);
+  return KS_OK;
+}
+
+static ks_status make_veff(ks_ctx *ctx, const double *vext, const double *rho, double hartree_tol, bool warm) {
+  KS_TRY(ks_hartree_impl(ctx, rho, hartree_tol, 100000, ctx->scf_vh, warm ? 1 : 0, nullptr, nullptr));
+  KS_TRY(ks_vxc_impl(ctx, rho, ctx->scf_vxc, nullptr));
+  k_veff<<<ks_blocks(ctx->n_nodes, 256), 256, 0, ctx->stream>>>(vext, ctx->scf_vh, ctx->scf_vxc, ctx->n_nodes,
+                                                                ctx->scf_veff);
+  KS_LAUNCHED(ctx);
+  return KS_OK;
+}
+
+// Anderson step over the history slots (age order in `order`, newest last): rho_next into ctx->scf_in
+static ks_status anderson(ks_ctx *ctx, const std::vector<int> &order, double beta) {
+  const int m = (int)order.size() - 1;
+  const int64_t nn = ctx->n_nodes;
+  std::vector<int> slot(order);
+  KS_CUDA(ctx, cudaMemcpyAsync(ctx->scf_slot, slot.data(), sizeof(int) * slot.size(), cudaMemcpyHostToDevice, ctx->stream));
+  std::vector<double> alpha(AMAX, 0.0);
+  if (m > 0) {
+    const int nv = m * m + m, nblk = 4 * ctx->sm_count;
+    k_anderson_gram<<<nblk, SB, 0, ctx->stream>>>(ctx->scf_hin, ctx->scf_hout, ctx->scf_slot, m, nn, ctx->scf_part);
+    KS_LAUNCHED(ctx);
+    k_sum_partials<<<1, 128, 0, ctx->stream>>>(ctx->scf_part, nblk, nv, ctx->scf_red);
+    KS_LAUNCHED(ctx);
+    std::vector<double> g(nv);
+    KS_CUDA(ctx, cudaMemcpyAsync(g.data(), ctx->scf_red, sizeof(double) * nv, cudaMemcpyDeviceToHost, ctx->stream));
+    KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    // (mix6): G alpha = r by Gaussian elimination with partial pivoting (m <= AMAX - 1)
+    std::vector<double> A(m * m), r(m);
+    for (int j = 0; j < m; j++) {
+      r[j] = g[m * m + j];
+      for (int k = 0; k < m; k++) A[j * m + k] = g[j * m + k];
+    }
+    for (int c = 0; c < m; c++) {
+      int piv = c;
+      for (int q = c + 1; q < m; q++)
+        if (std::fabs(A[q * m + c]) > std::fabs(A[piv * m + c])) piv = q;
+      if (!(std::fabs(A[piv * m + c]) > 0.0)) return ks_fail(ctx, KS_E_NONFINITE, "Anderson mixing: singular system");
+      if (piv != c) {
+        for (int k = 0; k < m; k++) std::swap(A[c * m + k], A[piv * m + k]);
+        std::swap(r[c], r[piv]);
+      }
+      for (int q = c + 1; q < m; q++) {
+        const double l = A[q * m + c] / A[c * m + c];
+        for (int k = c; k < m; k++) A[q * m + k] -= l * A[c * m + k];
+        r[q] -= l * r[c];
+      }
+    }
+    for (int c = m - 1; c >= 0; c--) {
+      double s = r[c];
+      for (int k = c + 1; k < m; k++) s -= A[c * m + k] * alpha[k];
+      alpha[c] = s / A[c * m + c];
+    }
+  }
+  KS_CUDA(ctx, cudaMemcpyAsync(ctx->scf_alpha, alpha.data(), sizeof(double) * AMAX, cudaMemcpyHostToDevice, ctx->stream));
+  k_anderson_combine<<<ks_blocks(nn, 256), 256, 0, ctx->stream>>>(ctx->scf_hin, ctx->scf_hout, ctx->scf_slot,
+                                                                   ctx->scf_alpha, m, beta, nn, ctx->scf_in);
+  KS_LAUNCHED(ctx);
+  KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));   // the host vectors above must outlive the copies
+  return KS_OK;
+}
+
+ks_status ks_scf_solve_impl(ks_ctx *ctx, int N, const double *vext, double f, double mu, double *lambda, double *U,
+                            double tol, int max_outer, int inner, double inner_tol, double beta, int depth,
+                            double bvp_tol, double hartree_tol, int32_t *h_outer, int32_t *h_inner, double *h_dres,
+                            double *h_lams) {
+  KS_TRY(scf_alloc(ctx, N, depth));
+  const int64_t nn = ctx->n_nodes, D = ctx->n_H + N;
+  cudaStream_t s = ctx->stream;
+  KS_TRY(ks_density_impl(ctx, N, U, f, ctx->scf_rho));
+  bool warm = false;
+  int it = 0;
+  ks_status result = KS_E_NOT_CONVERGED;
+  while (it < max_outer) {
+    KS_TRY(make_veff(ctx, vext, ctx->scf_rho, hartree_tol, warm));
+    warm = true;
+    KS_TRY(ks_assemble_impl(ctx, ctx->scf_veff, mu));
+    KS_TRY(ks_solve_impl(ctx, N, lambda, U, ctx->scf_Ut, bvp_tol, 100000, nullptr, nullptr));
+    KS_CUDA(ctx, cudaMemcpyAsync(ctx->scf_in, ctx->scf_rho, sizeof(double) * nn, cudaMemcpyDeviceToDevice, s));
+    std::vector<int> order;   // Anderson history slots, oldest first
+    int next_slot = 0, k = 0;
+    for (k = 0; k < inner; k++) {
+      KS_TRY(ks_project_impl(ctx, N, ctx->scf_Ut, ctx->scf_FA, ctx->scf_FB));
+      KS_TRY(ks_pencil_eig_impl(ctx, D, N, ctx->scf_FA, ctx->scf_FB, lambda, ctx->scf_Y));
+      KS_TRY(ks_lift_impl(ctx, N, ctx->scf_Ut, N, ctx->scf_Y, U));
+      KS_TRY(ks_density_impl(ctx, N, U, f, ctx->scf_out));
+      double dn = 0.0, on = 0.0;
+      KS_TRY(mnorm(ctx, ctx->scf_out, ctx->scf_in, &dn));
+      KS_TRY(mnorm(ctx, ctx->scf_out, nullptr, &on));
+      if (dn <= inner_tol * on || k == inner - 1) break;
+      // push (rho_in, rho_out) into the history ring, then mix
+      const int sl = next_slot;
+      next_slot = (next_slot + 1) % depth;
+      if ((int)order.size() == depth) order.erase(order.begin());
+      order.push_back(sl);
+      KS_CUDA(ctx, cudaMemcpyAsync(ctx->scf_hin + (int64_t)sl * nn, ctx->scf_in, sizeof(double) * nn,
+                                   cudaMemcpyDeviceToDevice, s));
+      KS_CUDA(ctx, cudaMemcpyAsync(ctx->scf_hout + (int64_t)sl * nn, ctx->scf_out, sizeof(double) * nn,
+                                   cudaMemcpyDeviceToDevice, s));
+      KS_TRY(anderson(ctx, order, beta));
+      KS_TRY(make_veff(ctx, vext, ctx->scf_in, hartree_tol, true));
+      KS_TRY(ks_assemble_impl(ctx, ctx->scf_veff, mu));
+    }
+    double ch = 0.0, on = 0.0;
+    KS_TRY(mnorm(ctx, ctx->scf_out, ctx->scf_rho, &ch));
+    KS_TRY(mnorm(ctx, ctx->scf_out, nullptr, &on));
+    const double change = on > 0.0 ? ch / on : ch;
+    if (h_dres) h_dres[it] = change;
+    if (h_inner) h_inner[it] = k + 1;
+    if (h_lams) {
+      KS_CUDA(ctx, cudaMemcpyAsync(h_lams + (int64_t)it * N, lambda, sizeof(double) * N, cudaMemcpyDeviceToHost, s));
+      KS_CUDA(ctx, cudaStreamSynchronize(s));
+    }
+    KS_CUDA(ctx, cudaMemcpyAsync(ctx->scf_rho, ctx->scf_out, sizeof(double) * nn, cudaMemcpyDeviceToDevice, s));
+    it++;
+    if (!(change == change)) { result = KS_E_NONFINITE; break; }
+    if (change <= tol) { result = KS_OK; break; }
+  }
+  if (h_outer) *h_outer = it;
+  KS_CUDA(ctx, cudaStreamSynchronize(s));
+  if (result != KS_OK) return ks_fail(ctx, result, "ks_scf_solve: %d outer iterations without reaching tol %g", it, tol);
   return KS_OK;
 }

@@ -25,7 +25,7 @@ OPS = {"K": 0, "M": 1, "MV": 2, "H": 3, "A": 4}
 EXPORTS = ["ks_abi_version", "ks_build_info", "ks_create", "ks_destroy", "ks_set_stream", "ks_pattern",
            "ks_values", "ks_assemble_veff", "ks_spmm", "ks_block_solve", "ks_last_iterations", "ks_solve_trace",
            "ks_true_residual", "ks_set_coarse", "ks_project_augmented", "ks_pencil_eig", "ks_lift",
-           "ks_augmented_solve", "ks_interpolation", "ks_density", "ks_vxc", "ks_hartree", "ks_memory_bytes", "ks_launch_count", "ks_sync", "ks_last_error"]
+           "ks_augmented_solve", "ks_interpolation", "ks_density", "ks_vxc", "ks_hartree", "ks_scf_solve", "ks_memory_bytes", "ks_launch_count", "ks_sync", "ks_last_error"]
 
 
 class KSError(RuntimeError):
@@ -70,6 +70,8 @@ def load_library(path: str = LIB_PATH):
         "ks_density": (st, [vp, i32, vp, dbl, vp]),
         "ks_vxc": (st, [vp, vp, vp, vp]),
         "ks_hartree": (st, [vp, vp, dbl, i32, vp, i32, vp, C.POINTER(i32)]),
+        "ks_scf_solve": (st, [vp, i32, vp, dbl, dbl, vp, vp, dbl, i32, i32, dbl, dbl, i32, dbl, dbl,
+                              C.POINTER(i32), vp, vp, vp]),
         "ks_memory_bytes": (st, [vp, C.POINTER(C.c_size_t)]),
         "ks_launch_count": (st, [vp, C.POINTER(i64)]),
         "ks_sync": (st, [vp]),
@@ -330,6 +332,24 @@ class Context:
         self._call(self._L.ks_hartree(self._h, _ptr(rho), float(tol), int(max_iter), _ptr(vh), int(bool(warm)),
                                       mom.ctypes.data, C.byref(it)))
         return vh, mom, it.value
+
+    def scf_solve(self, vext, lam, U, mu, f=2.0, tol=1e-8, max_outer=60, inner=20, inner_tol=None, beta=0.7,
+                  depth=5, bvp_tol=1e-12, hartree_tol=1e-12):
+        """ks_scf_solve: Algorithm 3 for the Kohn-Sham equation; lam and U updated in place. Returns dict(outer,
+        inner steps, outer density changes, Ritz-value history) as numpy."""
+        import torch
+        _check_cuda_tensor(vext, torch.float64, (self.n_nodes,), "vext")
+        N = U.shape[1]
+        outer = C.c_int32()
+        inner_steps = np.zeros(max_outer, np.int32)
+        dres = np.zeros(max_outer)
+        lams = np.zeros((max_outer, N))
+        self._call(self._L.ks_scf_solve(self._h, N, _ptr(vext), float(f), float(mu), _ptr(lam), _ptr(U), float(tol),
+                                        int(max_outer), int(inner), float(tol if inner_tol is None else inner_tol),
+                                        float(beta), int(depth), float(bvp_tol), float(hartree_tol), C.byref(outer),
+                                        inner_steps.ctypes.data, dres.ctypes.data, lams.ctypes.data))
+        k = outer.value
+        return dict(outer=k, inner=inner_steps[:k], dres=dres[:k], lams=lams[:k])
 
     def memory_bytes(self) -> int:
         v = C.c_size_t()

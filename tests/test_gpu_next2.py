@@ -77,3 +77,28 @@ def test_hartree_warm_start_reaches_the_same_potential():
     vh2, _, it_warm = ctx.hartree(rho, tol=1e-12, vh=vh2, warm=True)
     assert it_warm <= 1
     assert torch.allclose(vh, vh2, rtol=1e-10, atol=0)
+
+
+def test_scf_solve_matches_the_oracle_loop():
+    """Algorithm 3 for a He-like system (Z = 2, one doubly occupied orbital) with a nonnested graded coarse
+    mesh: the GPU driver (ks_scf_solve, with P from ks_interpolation) against oracle.scf_solve (P from the
+    oracle's point location), outer iteration by outer iteration."""
+    nuc = [((0.0, 0.0, 0.0), 2)]
+    mk = lambda n: gen.make_problem(dict(L=8.0, n=n, grading=("power", 1.8), jitter=0.0, nuclei=nuc, vnoise=0.0,
+                                         N=1, orbitals="gauss", lam=("const", -0.9), nc=2, seed=2))
+    p, c = mk(12), mk(6)
+    ctx = _ctx(p)
+    rp, col, val, nH = ctx.interpolation(c.xyz, c.tets, c.dirichlet)
+    ctx.set_coarse(nH, rp, col, val)
+    lam, U = dt(p.lam), dt(p.U)
+    out = ctx.scf_solve(dt(p.V), lam, U, mu=2.0, tol=1e-9, max_outer=60, inner=30)
+    assert ctx.sync() == 0
+    om = oracle.Mesh.from_problem(p)
+    orp, ocol, oval, onH = oracle.interpolation(p.xyz, p.free_nodes, c.xyz, c.tets, c.dirichlet)
+    ref = oracle.scf_solve(om, onH, orp, ocol, oval, p.V, p.lam.copy(), p.U.copy(), mu=2.0, tol=1e-9, max_outer=60,
+                           inner=30)
+    assert abs(out["outer"] - ref["outer"]) <= 1
+    k = min(out["outer"], ref["outer"])
+    assert np.all(np.abs(out["lams"][:3] - ref["lams"][:3]) <= 1e-8 * np.abs(ref["lams"][:3]))
+    assert abs(lam.cpu().numpy()[0] - ref["lam"][0]) <= 1e-8 * abs(ref["lam"][0])
+    assert out["dres"][-1] <= 1e-9
