@@ -334,9 +334,10 @@ class Context:
         return vh, mom, it.value
 
     def scf_solve(self, vext, lam, U, mu, f=2.0, tol=1e-8, max_outer=60, inner=20, inner_tol=None, beta=0.7,
-                  depth=5, bvp_tol=1e-12, hartree_tol=1e-12):
+                  depth=5, bvp_tol=1e-12, hartree_tol=1e-12, allow_unconverged=False):
         """ks_scf_solve: Algorithm 3 for the Kohn-Sham equation; lam and U updated in place. Returns dict(outer,
-        inner steps, outer density changes, Ritz-value history) as numpy."""
+        inner steps, outer density changes, Ritz-value history, converged) as numpy; KS_E_NOT_CONVERGED raises
+        unless allow_unconverged."""
         import torch
         _check_cuda_tensor(vext, torch.float64, (self.n_nodes,), "vext")
         N = U.shape[1]
@@ -344,12 +345,14 @@ class Context:
         inner_steps = np.zeros(max_outer, np.int32)
         dres = np.zeros(max_outer)
         lams = np.zeros((max_outer, N))
-        self._call(self._L.ks_scf_solve(self._h, N, _ptr(vext), float(f), float(mu), _ptr(lam), _ptr(U), float(tol),
-                                        int(max_outer), int(inner), float(tol if inner_tol is None else inner_tol),
-                                        float(beta), int(depth), float(bvp_tol), float(hartree_tol), C.byref(outer),
-                                        inner_steps.ctypes.data, dres.ctypes.data, lams.ctypes.data))
+        st = self._L.ks_scf_solve(self._h, N, _ptr(vext), float(f), float(mu), _ptr(lam), _ptr(U), float(tol),
+                                  int(max_outer), int(inner), float(tol if inner_tol is None else inner_tol),
+                                  float(beta), int(depth), float(bvp_tol), float(hartree_tol), C.byref(outer),
+                                  inner_steps.ctypes.data, dres.ctypes.data, lams.ctypes.data)
+        if st not in (KS_OK, KS_E_NOT_CONVERGED) or (st == KS_E_NOT_CONVERGED and not allow_unconverged):
+            self._call(st)
         k = outer.value
-        return dict(outer=k, inner=inner_steps[:k], dres=dres[:k], lams=lams[:k])
+        return dict(outer=k, inner=inner_steps[:k], dres=dres[:k], lams=lams[:k], converged=st == KS_OK)
 
     def memory_bytes(self) -> int:
         v = C.c_size_t()
