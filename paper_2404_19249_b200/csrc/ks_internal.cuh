@@ -108,6 +108,11 @@ struct ks_ctx {
   int *scf_slot = nullptr;
   int64_t scf_nn = 0, scf_D = 0;
   int scf_N = 0, scf_depth = 0;
+  // staged S phase of the block PCG (ks_stage.cu): tables for one NP
+  int stage_np = 0, stage_cap = 0;
+  int64_t stage_groups = 0, stage_staged = 0;
+  int32_t *stage_meta = nullptr;
+  uint16_t *stage_slcol = nullptr, *stage_dlc = nullptr;
   int interp_fallbacks = 0;         // last ks_interpolation needed the scan fallback of the walk
   // NEXT-1 (ks_outer.cu): cuSOLVER handle, pencil and outer-loop workspaces
   void *cusolver = nullptr;
@@ -127,6 +132,8 @@ struct ks_ctx {
 #define KS_PAD 8
 #define KS_TRACE_CAP 8192
 #define KS_SELL_C 8   // rows per slice of the sliced-ELL operator copy
+#define KS_STAGE_RMAX 8      // runs of staged p rows per S-phase group (ks_stage.cu)
+#define KS_META_BYTES 80     // group record: 4 ints + KS_STAGE_RMAX (start, len) pairs
 
 const char *ks_status_name(ks_status s);
 ks_status ks_fail(ks_ctx *ctx, ks_status s, const char *fmt, ...);
@@ -174,6 +181,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 // internal entry points implemented in the .cu files
 ks_status ks_setup_mesh(ks_ctx *ctx, const double *h_xyz, const int32_t *h_tets, const uint8_t *h_dir);
 ks_status ks_sell_build(ks_ctx *ctx);
+ks_status ks_stage_build(ks_ctx *ctx, int NP, int max_rows);
 ks_status ks_assemble_impl(ks_ctx *ctx, const double *d_veff, double mu);
 ks_status ks_materialize_views(ks_ctx *ctx);
 ks_status ks_spmm_impl(ks_ctx *ctx, ks_op op, const double *val, int N, const double *X, double *Y);

@@ -36,9 +36,8 @@ constexpr int PCG_WARPS = PCG_THREADS / 32;
 
 // Block-level column sums: acc[d][v] per lane (column (VEC*lane+v) % NP) -> out[d*NP + c], fixed order
 // (butterfly over the lanes of a column within the warp, then warps 0..W-1 in order).
-template <int NP, int ND>
-__device__ __forceinline__ void block_cols(double (&acc)[ND][SL<NP, PCG_THREADS>::VEC], double *red, double *out) {
-  constexpr int VEC = SL<NP, PCG_THREADS>::VEC, LPR = SL<NP, PCG_THREADS>::LPR;
+template <int NP, int ND, int VEC = SL<NP, PCG_THREADS>::VEC, int LPR = SL<NP, PCG_THREADS>::LPR>
+__device__ __forceinline__ void block_cols(double (&acc)[ND][VEC], double *red, double *out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int d = 0; d < ND; d++)
@@ -78,6 +77,12 @@ struct PcgArgs {
   int trace_cap;
   int64_t n;
   int N, ntiles, max_iter;
+  // staged S phase (ks_stage.cu)
+  const int32_t *meta;        // [n_groups] KS_META_BYTES records
+  const uint16_t *slcol;      // [sell_total] local column of every slot
+  const uint16_t *dlc;        // [n] local index of the row itself
+  int64_t ngroups;
+  int stage_cap;              // staged rows per stage buffer
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
@@ -113,7 +118,136 @@ __device__ __forceinline__ void reduce_partials(const double *part, int stride, 
   __syncthreads();
 }
 
+// ---- staged S phase: the p rows a group of GRP rows references are copied (bulk, TMA) into shared memory
+constexpr int PSTAGES = 3;
+constexpr int META_SLOT = 128;   // bytes reserved for the group record in a stage (KS_META_BYTES <= 128)
+
 template <int NP>
+struct SP {   // staged layout: 2 orbitals per lane (NP >= 4)
+  static constexpr int VEC = 2, LPR = NP >= 4 ? NP / 2 : 2, RPW = 32 / LPR, GRP = PCG_WARPS * RPW;
+  static_assert(GRP * NP == 1024, "group size of ks_stage_build");
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// thread 0: copy the staged rows of consumption k (group g) into stage st, plus the record of group k + PSTAGES
+// (the producer reads records only from shared memory after the prologue). rec: the record of group g.
+template <int NP>
+__device__ __forceinline__ void issue_group(const PcgArgs &a, const int32_t *rec, int64_t g, int64_t g_next,
+                                            unsigned char *stage, uint64_t *bar, int *staged_flag) {
+  const int nruns = rec[0];
+  *staged_flag = nruns > 0;
+  unsigned bytes = nruns > 0 ? (unsigned)rec[1] * NP * 8u : 0u;
+  if (g_next >= 0) bytes += KS_META_BYTES;
+  if (bytes == 0) {
+    mbar_arrive(bar);
+    return;
+  }
+  mbar_expect_tx(bar, bytes);
+  double *buf = reinterpret_cast<double *>(stage + META_SLOT);
+  int off = 0;
+  for (int r = 0; r < nruns; r++) {
+    const int start = rec[4 + 2 * r], len = rec[5 + 2 * r];
+    bulk_g2s(buf + (int64_t)off * NP, a.p + (int64_t)start * NP, (unsigned)len * NP * 8u, bar);
+    off += len;
+  }
+  if (g_next >= 0) bulk_g2s(stage, a.meta + g_next * (KS_META_BYTES / 4), KS_META_BYTES, bar);
+}
+
+// q = A p for this CTA's groups, p.q partials in acc (staged layout); returns the consumptions done
+template <int NP>
+__device__ __forceinline__ void s_phase_staged(const PcgArgs &a, unsigned char *dyn, uint64_t *pbar, int *s_staged,
+                                               unsigned &pseq, double (&acc)[1][2]) {
+  constexpr int LPR = SP<NP>::LPR, RPW = SP<NP>::RPW, GRP = SP<NP>::GRP;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = lane / LPR, sub = lane % LPR;
+  const int G = gridDim.x;
+  const int64_t n = a.n;
+  const size_t stage_bytes = META_SLOT + (size_t)a.stage_cap * NP * 8;
+  const int64_t my = a.ngroups > blockIdx.x ? (a.ngroups - blockIdx.x + G - 1) / G : 0;
+  auto stage_of = [&](unsigned q) { return dyn + (size_t)(q % PSTAGES) * stage_bytes; };
+  if (threadIdx.x == 0) {
+    // p was written by other CTAs before the grid barrier: order the bulk (async-proxy) reads after it
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    for (int k = 0; k < PSTAGES && k < my; k++) {
+      const int64_t g = blockIdx.x + (int64_t)k * G;
+      const int64_t gn = k + PSTAGES < my ? g + (int64_t)PSTAGES * G : -1;
+      const int32_t *rec = a.meta + g * (KS_META_BYTES / 4);
+      int32_t r[KS_META_BYTES / 4];
+      for (int x = 0; x < KS_META_BYTES / 4; x++) r[x] = __ldg(rec + x);
+      issue_group<NP>(a, r, g, gn, stage_of(pseq + k), &pbar[(pseq + k) % PSTAGES], &s_staged[(pseq + k) % PSTAGES]);
+    }
+  }
+  for (int64_t k = 0; k < my; k++) {
+    const unsigned q = pseq + (unsigned)k;
+    const int st = q % PSTAGES;
+    mbar_wait(&pbar[st], (q / PSTAGES) & 1u);
+    unsigned char *stage = stage_of(q);
+    const double *buf = reinterpret_cast<const double *>(stage + META_SLOT);
+    const int64_t g = blockIdx.x + k * G;
+    const int64_t row = g * GRP + warp * RPW + slot;
+    const bool staged = s_staged[st];
+    if (row < n) {
+      const int64_t sl = row / KS_SELL_C;
+      const int32_t b = __ldg(a.sell_ptr + sl), e = __ldg(a.sell_ptr + sl + 1);
+      const int groups = (e - b) / (4 * KS_SELL_C);
+      const int64_t base = b + (row % KS_SELL_C) * 4;
+      double q0 = 0.0, q1 = 0.0, p0, p1;
+      if (staged) {
+        for (int gg = 0; gg < groups; gg++) {
+          const int64_t o = base + (int64_t)gg * (4 * KS_SELL_C);
+          const ushort4 lc = __ldg(reinterpret_cast<const ushort4 *>(a.slcol + o));
+          double w0, w1, w2, w3;
+          ldnc_v4(a.A + o, w0, w1, w2, w3);
+          const double2 x0 = *reinterpret_cast<const double2 *>(buf + (int64_t)lc.x * NP + 2 * sub);
+          const double2 x1 = *reinterpret_cast<const double2 *>(buf + (int64_t)lc.y * NP + 2 * sub);
+          const double2 x2 = *reinterpret_cast<const double2 *>(buf + (int64_t)lc.z * NP + 2 * sub);
+          const double2 x3 = *reinterpret_cast<const double2 *>(buf + (int64_t)lc.w * NP + 2 * sub);
+          q0 = fma(w0, x0.x, q0); q1 = fma(w0, x0.y, q1);
+          q0 = fma(w1, x1.x, q0); q1 = fma(w1, x1.y, q1);
+          q0 = fma(w2, x2.x, q0); q1 = fma(w2, x2.y, q1);
+          q0 = fma(w3, x3.x, q0); q1 = fma(w3, x3.y, q1);
+        }
+        const double2 pv = *reinterpret_cast<const double2 *>(buf + (int64_t)__ldg(a.dlc + row) * NP + 2 * sub);
+        p0 = pv.x; p1 = pv.y;
+      } else {   // group too irregular to stage: gathers from global memory
+        for (int gg = 0; gg < groups; gg++) {
+          const int64_t o = base + (int64_t)gg * (4 * KS_SELL_C);
+          const int4 c = __ldg(reinterpret_cast<const int4 *>(a.sell_col + o));
+          double w0, w1, w2, w3;
+          ldnc_v4(a.A + o, w0, w1, w2, w3);
+          const double2 x0 = *reinterpret_cast<const double2 *>(a.p + (int64_t)c.x * NP + 2 * sub);
+          const double2 x1 = *reinterpret_cast<const double2 *>(a.p + (int64_t)c.y * NP + 2 * sub);
+          const double2 x2 = *reinterpret_cast<const double2 *>(a.p + (int64_t)c.z * NP + 2 * sub);
+          const double2 x3 = *reinterpret_cast<const double2 *>(a.p + (int64_t)c.w * NP + 2 * sub);
+          q0 = fma(w0, x0.x, q0); q1 = fma(w0, x0.y, q1);
+          q0 = fma(w1, x1.x, q0); q1 = fma(w1, x1.y, q1);
+          q0 = fma(w2, x2.x, q0); q1 = fma(w2, x2.y, q1);
+          q0 = fma(w3, x3.x, q0); q1 = fma(w3, x3.y, q1);
+        }
+        const double2 pv = *reinterpret_cast<const double2 *>(a.p + row * NP + 2 * sub);
+        p0 = pv.x; p1 = pv.y;
+      }
+      acc[0][0] += p0 * q0;
+      acc[0][1] += p1 * q1;
+      *reinterpret_cast<double2 *>(a.q + row * NP + 2 * sub) = make_double2(q0, q1);
+    }
+    __syncthreads();   // every warp is done with stage st
+    if (threadIdx.x == 0 && k + PSTAGES < my) {
+      int32_t r[KS_META_BYTES / 4];
+      const int32_t *rec = reinterpret_cast<const int32_t *>(stage);   // arrived with consumption k
+      for (int x = 0; x < KS_META_BYTES / 4; x++) r[x] = rec[x];
+      const int64_t g2 = g + (int64_t)PSTAGES * G;
+      const int64_t gn = k + 2 * PSTAGES < my ? g2 + (int64_t)PSTAGES * G : -1;
+      issue_group<NP>(a, r, g2, gn, stage, &pbar[st], &s_staged[st]);
+    }
+  }
+  pseq += (unsigned)my;
+}
+
+template <int NP, bool STAGEP>
 __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs a) {
   constexpr int VEC = SL<NP, PCG_THREADS>::VEC, LPR = SL<NP, PCG_THREADS>::LPR, RPW = SL<NP, PCG_THREADS>::RPW, TILE = SL<NP, PCG_THREADS>::TILE;
   constexpr int CHUNK = SL<NP, PCG_THREADS>::CHUNK;
@@ -124,6 +258,10 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
   __shared__ double s_alpha[NP], s_beta[NP], s_rho[NP], s_bnorm[NP], s_rr[NP];
   __shared__ int s_active[NP], s_conv[NP], s_iters[NP];
   __shared__ int s_any;
+  __shared__ __align__(8) uint64_t s_pbar[PSTAGES];
+  __shared__ int s_staged[PSTAGES];
+  extern __shared__ __align__(128) unsigned char dyn[];
+  unsigned pseq = 0;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int slot = lane / LPR, sub = lane % LPR;
@@ -142,6 +280,13 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
     }
   };
   stamp();
+  if constexpr (STAGEP) {
+    if (threadIdx.x == 0) {
+      for (int st = 0; st < PSTAGES; st++) mbar_init(&s_pbar[st], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+  }
 
   // ---------------- init: b = (lambda+mu) M u, r = b - A u, x = u, z = r/d, p = z ----------------
   {
@@ -226,7 +371,11 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
     }
 
     // ---- S: q = A p, p.q ----
-    {
+    if constexpr (STAGEP) {
+      double acc[1][2] = {{0.0, 0.0}};
+      s_phase_staged<NP>(a, dyn, s_pbar, s_staged, pseq, acc);
+      block_cols<NP, 1, 2, NP / 2>(acc, red, tot);
+    } else {
       double acc[1][VEC];
 #pragma unroll
       for (int v = 0; v < VEC; v++) acc[0][v] = 0.0;
@@ -243,6 +392,8 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
         }
       }
       block_cols<NP, 1>(acc, red, tot);
+    }
+    {
       for (int i = threadIdx.x; i < NP; i += blockDim.x) part_s[(int64_t)blockIdx.x * STRIDE + i] = tot[i];
       grid_barrier(a.bar, target);
       stamp();
@@ -393,12 +544,13 @@ __global__ void __launch_bounds__(256) k_spmm(const int32_t *__restrict__ row_pt
   y.store(Y + row * NP + sub * VEC);
 }
 
-template <int NP>
-ks_status launch_pcg(ks_ctx *ctx, PcgArgs &a) {
-  a.ntiles = (int)((a.n + SL<NP, PCG_THREADS>::TILE - 1) / SL<NP, PCG_THREADS>::TILE);
+template <int NP, bool STAGEP>
+ks_status launch_pcg_t(ks_ctx *ctx, PcgArgs &a, size_t dyn) {
+  auto kern = k_block_pcg<NP, STAGEP>;
+  if (dyn > 0) KS_CUDA(ctx, cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
   int per_sm = 0;
-  KS_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_pcg<NP>, PCG_THREADS, 0));
-  if (per_sm < 1) return ks_fail(ctx, KS_E_CUDA, "k_block_pcg<%d> cannot be resident", NP);
+  KS_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PCG_THREADS, dyn));
+  if (per_sm < 1) return ks_fail(ctx, KS_E_CUDA, "k_block_pcg<%d,%d> cannot be resident", NP, (int)STAGEP);
   int G = per_sm * ctx->sm_count;
   if (G > a.ntiles) G = a.ntiles;
   if ((int64_t)G * 4 * NP * 2 > ctx->partial_cap) {
@@ -409,10 +561,44 @@ ks_status launch_pcg(ks_ctx *ctx, PcgArgs &a) {
   a.partials = ctx->partials;
   KS_CUDA(ctx, cudaMemsetAsync(ctx->barrier, 0, sizeof(unsigned), ctx->stream));
   void *args[] = {&a};
-  KS_CUDA(ctx, cudaLaunchCooperativeKernel((const void *)k_block_pcg<NP>, dim3(G), dim3(PCG_THREADS), args, 0,
-                                           ctx->stream));
+  KS_CUDA(ctx, cudaLaunchCooperativeKernel((const void *)kern, dim3(G), dim3(PCG_THREADS), args, dyn, ctx->stream));
   ctx->launches++;
   return KS_OK;
+}
+
+// Staged S phase (opt-in, KS_PCG_STAGE=1): for NP >= 4 when the group tables fit three stages of shared
+// memory. Measured slower on the lexicographically numbered meshes (C4: S 471 us vs 296 us gathering,
+// r01ad): a 64-row group references ~7 runs of ~66 rows, so each p row is copied into ~7 stage buffers and
+// the L2 -> shared traffic (7.2x the vector per S phase) saturates L2, while L1 gathers hit ~50 %. It needs
+// 3-D-local row groups to pay off.
+constexpr size_t PSTAGE_SMEM_MAX = 200 * 1024;
+
+template <int NP>
+ks_status launch_pcg(ks_ctx *ctx, PcgArgs &a) {
+  a.ntiles = (int)((a.n + SL<NP, PCG_THREADS>::TILE - 1) / SL<NP, PCG_THREADS>::TILE);
+  a.meta = nullptr;
+  a.slcol = nullptr;
+  a.dlc = nullptr;
+  a.ngroups = 0;
+  a.stage_cap = 0;
+  const char *env = getenv("KS_PCG_STAGE");
+  const bool want = NP >= 4 && env && env[0] == '1';
+  if constexpr (NP >= 4) {
+    if (want) {
+      const int max_rows = (int)((PSTAGE_SMEM_MAX / PSTAGES - META_SLOT) / (NP * 8));
+      KS_TRY(ks_stage_build(ctx, NP, max_rows));
+      if (ctx->stage_staged > 0) {
+        a.meta = ctx->stage_meta;
+        a.slcol = ctx->stage_slcol;
+        a.dlc = ctx->stage_dlc;
+        a.ngroups = ctx->stage_groups;
+        a.stage_cap = ctx->stage_cap;
+        const size_t dyn = (size_t)PSTAGES * (META_SLOT + (size_t)ctx->stage_cap * NP * 8);
+        return launch_pcg_t<NP, true>(ctx, a, dyn);
+      }
+    }
+  }
+  return launch_pcg_t<NP, false>(ctx, a, 0);
 }
 
 template <int NP>

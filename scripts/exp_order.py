@@ -80,7 +80,7 @@ def main():
         os.environ.pop("KS_PCG_TRACE")
         d = np.diff(ts.astype(np.int64)) * 1e-3
         k = (len(d) - 1) // 3
-        print(json.dumps({"order": order, "staged": os.environ.get("KS_PCG_STAGED", "1"), "solve_ms": ms,
+        print(json.dumps({"order": order, "stage": os.environ.get("KS_PCG_STAGE", "1"), "solve_ms": ms,
                           "iters": ctx.last_iterations(), "init_us": d[0],
                           "S_us": float(np.mean(d[1::3][:k])), "U_us": float(np.mean(d[2::3][:k])),
                           "P_us": float(np.mean(d[3::3][:k]))}), flush=True)

@@ -306,3 +306,16 @@ def test_config4_full_parity():
         for name, blk in _blocks(F, p.n_H).items():
             ref_b = _blocks(Fo, p.n_H)[name]
             assert np.linalg.norm(blk - ref_b) <= 1e-9 * np.linalg.norm(ref_b), name
+
+
+@pytest.mark.parametrize("c", [3])
+def test_block_solve_staged_s_phase(c, monkeypatch):
+    """The opt-in S phase with the orbital block staged in shared memory by bulk copies (KS_PCG_STAGE=1)
+    reaches the same solutions as the oracle."""
+    monkeypatch.setenv("KS_PCG_STAGE", "1")
+    k = case(c)
+    p = k.p
+    ref, ut, it, rr, st = _solve_both(k, p.lam, p.U)
+    assert st == 0 and ref["status"] == 0
+    assert np.all(_mnorm_rel(k.om.csr("M"), ut, ref["Ut"]) <= 1e-8)
+    assert np.all(np.abs(it - ref["iters"]) <= 2)
