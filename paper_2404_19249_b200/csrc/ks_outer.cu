@@ -2,7 +2,8 @@
 //   ks_pencil_eig       lowest k eigenpairs of F_A y = lambda F_B y, the "small-scale algebraic eigenvalue
 //                       problem" on W (Nonlinear_Eig_Hh); dense, D = n_H + N
 //                       <= ~1400, by the cuSOLVER generalized symmetric eigensolver (a plain library call,
-//                       like cuBLAS for a plain GEMM: Cholesky of F_B + tridiagonal divide and conquer).
+//                       like cuBLAS for a plain GEMM): Cholesky of F_B, tridiagonal reduction, and only the
+//                       lowest k eigenpairs (index range, dsygvdx).
 //   ks_lift             U_new = P y_H + U~ y_t (the new orbitals in S_H + span{psi~}), own kernel.
 //   ks_augmented_solve  outer iterations with a fixed potential: block solve -> projection -> pencil
 //                       eig -> lift, until max |lambda_new - lambda| <= tol_eig * max |lambda|.
@@ -72,9 +73,19 @@ ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, co
   // symmetric matrices: row-major == column-major
   KS_CUDA(ctx, cudaMemcpyAsync(ctx->eig_A, FA, sizeof(double) * D * D, cudaMemcpyDeviceToDevice, ctx->stream));
   KS_CUDA(ctx, cudaMemcpyAsync(ctx->eig_B, FB, sizeof(double) * D * D, cudaMemcpyDeviceToDevice, ctx->stream));
-  int lwork = 0;
-  if (cusolverDnDsygvd_bufferSize(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)D,
-                                  ctx->eig_A, (int)D, ctx->eig_B, (int)D, ctx->eig_w, &lwork) != CUSOLVER_STATUS_SUCCESS)
+  // only the lowest k eigenpairs are needed: the index-range solver (bisection + inverse iteration on the
+  // tridiagonal form, k back-transformed vectors) instead of all D (KS_PENCIL_ALL=1 selects dsygvd)
+  const char *all = getenv("KS_PENCIL_ALL");
+  const bool subset = !(all && all[0] == '1') && k < D;
+  int lwork = 0, meig = 0;
+  if (subset) {
+    if (cusolverDnDsygvdx_bufferSize(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
+                                     CUBLAS_FILL_MODE_LOWER, (int)D, ctx->eig_A, (int)D, ctx->eig_B, (int)D, 0.0, 0.0,
+                                     1, k, &meig, ctx->eig_w, &lwork) != CUSOLVER_STATUS_SUCCESS)
+      return ks_fail(ctx, KS_E_CUDA, "cusolverDnDsygvdx_bufferSize failed (D = %lld)", (long long)D);
+  } else if (cusolverDnDsygvd_bufferSize(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                         (int)D, ctx->eig_A, (int)D, ctx->eig_B, (int)D, ctx->eig_w, &lwork) !=
+             CUSOLVER_STATUS_SUCCESS)
     return ks_fail(ctx, KS_E_CUDA, "cusolverDnDsygvd_bufferSize failed (D = %lld)", (long long)D);
   if (ctx->eig_work_cap < lwork) {
     ks_free_t(ctx, ctx->eig_work);
@@ -82,10 +93,17 @@ ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, co
     ctx->eig_work_cap = lwork;
   }
   if (!ctx->eig_info) KS_TRY(ks_alloc_t(ctx, &ctx->eig_info, 1, "pencil info"));
-  if (cusolverDnDsygvd(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)D, ctx->eig_A,
-                       (int)D, ctx->eig_B, (int)D, ctx->eig_w, ctx->eig_work, lwork, ctx->eig_info) !=
-      CUSOLVER_STATUS_SUCCESS)
-    return ks_fail(ctx, KS_E_CUDA, "cusolverDnDsygvd failed (D = %lld)", (long long)D);
+  cusolverStatus_t cst;
+  if (subset)
+    cst = cusolverDnDsygvdx(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
+                            CUBLAS_FILL_MODE_LOWER, (int)D, ctx->eig_A, (int)D, ctx->eig_B, (int)D, 0.0, 0.0, 1, k,
+                            &meig, ctx->eig_w, ctx->eig_work, lwork, ctx->eig_info);
+  else
+    cst = cusolverDnDsygvd(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)D, ctx->eig_A,
+                           (int)D, ctx->eig_B, (int)D, ctx->eig_w, ctx->eig_work, lwork, ctx->eig_info);
+  if (cst != CUSOLVER_STATUS_SUCCESS)
+    return ks_fail(ctx, KS_E_CUDA, "cusolver generalized eigensolver failed (D = %lld, status %d)", (long long)D,
+                   (int)cst);
   ctx->launches++;
   int info = 0;
   KS_CUDA(ctx, cudaMemcpyAsync(&info, ctx->eig_info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));

@@ -1,4 +1,5 @@
-// ks_rowops.cuh -- the multi-RHS CSR row kernel shared by the SpMM, PCG and projection kernels.
+// ks_rowops.cuh -- the multi-RHS CSR row kernel of the standalone SpMM (ks_spmm) for the operators without
+// a sliced-ELL copy (K, M_V, H views). The hot path uses the sliced-ELL row kernel of ks_sell.cuh.
 //
 // Layout of a block of vectors: X[n][NP] row-major, NP a power of two <= 64. A "row group" of LPR lanes
 // owns one row; lane `sub` of the group owns the VEC = 2 consecutive columns sub*VEC .. sub*VEC+1
@@ -85,70 +86,4 @@ __device__ __forceinline__ Vec<Lay<NP>::VEC> row_spmv(const int32_t *__restrict_
     for (int v = 0; v < VEC; v++) acc.v[v] = fma(a0, x0.v[v], acc.v[v]);
   }
   return acc;
-}
-
-// Two operators sharing the column stream: ya = A x, yb = B x (one pass over col and the gathers).
-template <int NP>
-__device__ __forceinline__ void row_spmv2(const int32_t *__restrict__ col, const double *__restrict__ va,
-                                          const double *__restrict__ vb, int32_t k0, int32_t k1, const double *X,
-                                          int sub, Vec<Lay<NP>::VEC> &ya, Vec<Lay<NP>::VEC> &yb) {
-  constexpr int VEC = Lay<NP>::VEC;
-  ya.zero();
-  yb.zero();
-  int32_t k = k0;
-  for (; k + 2 <= k1; k += 2) {
-    int32_t c0 = __ldg(col + k), c1 = __ldg(col + k + 1);
-    double a0 = __ldg(va + k), a1 = __ldg(va + k + 1);
-    double b0 = __ldg(vb + k), b1 = __ldg(vb + k + 1);
-    Vec<VEC> x0 = Vec<VEC>::load(X + (int64_t)c0 * NP + sub * VEC);
-    Vec<VEC> x1 = Vec<VEC>::load(X + (int64_t)c1 * NP + sub * VEC);
-#pragma unroll
-    for (int v = 0; v < VEC; v++) {
-      ya.v[v] = fma(a0, x0.v[v], ya.v[v]);
-      yb.v[v] = fma(b0, x0.v[v], yb.v[v]);
-      ya.v[v] = fma(a1, x1.v[v], ya.v[v]);
-      yb.v[v] = fma(b1, x1.v[v], yb.v[v]);
-    }
-  }
-  for (; k < k1; k++) {
-    int32_t c0 = __ldg(col + k);
-    double a0 = __ldg(va + k), b0 = __ldg(vb + k);
-    Vec<VEC> x0 = Vec<VEC>::load(X + (int64_t)c0 * NP + sub * VEC);
-#pragma unroll
-    for (int v = 0; v < VEC; v++) {
-      ya.v[v] = fma(a0, x0.v[v], ya.v[v]);
-      yb.v[v] = fma(b0, x0.v[v], yb.v[v]);
-    }
-  }
-}
-
-// Sum of a per-lane value over the lanes that own the same column (lanes l, l^LPR, l^2LPR, ...).
-// Butterfly order: every participating lane ends with the bitwise-identical total.
-template <int NP>
-__device__ __forceinline__ double reduce_same_column(double v) {
-#pragma unroll
-  for (int o = Lay<NP>::LPR; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// Block-level: acc[d][vv] per lane (column (VEC*lane+vv) % NP) -> out[d*NP + c] (block totals), fixed
-// order (warp butterfly, then warps 0..W-1 in order). red: shared scratch of W*ND*NP doubles.
-template <int NP, int ND>
-__device__ __forceinline__ void block_reduce_cols(double (&acc)[ND][Lay<NP>::VEC], double *red, double *out) {
-  constexpr int VEC = Lay<NP>::VEC, LPR = Lay<NP>::LPR;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
-#pragma unroll
-  for (int d = 0; d < ND; d++)
-#pragma unroll
-    for (int v = 0; v < VEC; v++) {
-      double s = reduce_same_column<NP>(acc[d][v]);
-      if (lane < LPR) red[(warp * ND + d) * NP + lane * VEC + v] = s;
-    }
-  __syncthreads();
-  for (int i = threadIdx.x; i < ND * NP; i += blockDim.x) {
-    double s = 0.0;
-    for (int w = 0; w < W; w++) s += red[w * ND * NP + i];
-    out[i] = s;
-  }
-  __syncthreads();
 }

@@ -1,6 +1,6 @@
 #!/usr/bin/env python
-"""Standalone multi-RHS SpMM timing (ks_spmm, Y = A X) on config C for N in a list: GB/s of algorithmic
-bytes 12 nnz + 4 (n+1) + 16 N n (matrix, read X once, write Y)."""
+"""Standalone multi-RHS SpMM timing (ks_spmm, Y = A X on the sliced-ELL copy) on config C for N in a list:
+GB/s of algorithmic bytes 12 nnz + 4 (n+1) + 16 N n (matrix, read X once, write Y)."""
 import json
 import os
 import sys
@@ -33,5 +33,5 @@ for N in Ns:
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / R
     b = 12 * nnz + 4 * (n + 1) + 16 * N * n
-    print(json.dumps({"N": N, "ms": ms, "alg_GBs": b / ms / 1e6, "variant": os.environ.get("KS_SPMM_VARIANT", "0")}),
+    print(json.dumps({"N": N, "ms": ms, "alg_GBs": b / ms / 1e6}),
           flush=True)
