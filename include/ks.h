@@ -263,6 +263,20 @@ ks_status ks_scf_solve(ks_ctx *ctx, int32_t N, const double *d_vext, double f, d
                        int32_t depth, double bvp_tol, double hartree_tol, int32_t *h_outer, int32_t *h_inner,
                        double *h_dres, double *h_lams);
 
+/*
+ * The hot-path step from HOST buffers, pipelined. ks_step_submit enqueues one step: copy V_eff [n_nodes],
+ * lambda [N], U [n_free][N] from host memory (pinned for asynchronous copies), ks_assemble_veff(V_eff, mu),
+ * ks_block_solve(tol, max_iter), ks_project_augmented, and copy F_A, F_B [(n_H+N)^2] to host memory. It
+ * returns without waiting. Consecutive steps alternate between two device slots; input copies run on an
+ * internal host-to-device stream and result copies on an internal device-to-host stream, ordered against the
+ * context's stream by events, so the input copy of one step overlaps the compute of the previous one.
+ * The caller must not modify a step's host inputs, or read its outputs, before ks_step_wait returns.
+ * ks_step_wait waits for every submitted step. Device-detected conditions are reported by ks_sync.
+ */
+ks_status ks_step_submit(ks_ctx *ctx, int32_t N, const double *h_V, double mu, const double *h_lambda,
+                         const double *h_U, double tol, int32_t max_iter, double *h_FA, double *h_FB);
+ks_status ks_step_wait(ks_ctx *ctx);
+
 /* Device memory owned by the library (bytes). */
 ks_status ks_memory_bytes(const ks_ctx *ctx, size_t *bytes);
 

@@ -73,6 +73,7 @@ void ks_free(ks_ctx *ctx, void *ptr) {
 }
 
 static void free_all(ks_ctx *ctx) {
+  ks_free_stream(ctx);
   ks_free_outer(ctx);
   for (auto &a : ctx->allocs) cudaFree(a.first);
   ctx->allocs.clear();
@@ -300,6 +301,21 @@ ks_status ks_scf_solve(ks_ctx *ctx, int32_t N, const double *d_vext, double f, d
   if (ctx->n_H < 1) return ks_fail(ctx, KS_E_STATE, "ks_scf_solve: call ks_set_coarse first");
   return ks_scf_solve_impl(ctx, N, d_vext, f, mu, d_lambda, d_U, tol, max_outer, inner, inner_tol, beta, depth,
                            bvp_tol, hartree_tol, h_outer, h_inner, h_dres, h_lams);
+}
+
+ks_status ks_step_submit(ks_ctx *ctx, int32_t N, const double *h_V, double mu, const double *h_lambda,
+                         const double *h_U, double tol, int32_t max_iter, double *h_FA, double *h_FB) {
+  if (!ctx) return KS_E_ARG;
+  if (N < 1 || N > KS_MAX_N || !h_V || !h_lambda || !h_U || !h_FA || !h_FB || !(tol > 0.0) || max_iter < 1 ||
+      !(mu >= 0.0))
+    return ks_fail(ctx, KS_E_ARG, "ks_step_submit: bad arguments");
+  if (ctx->n_H < 1) return ks_fail(ctx, KS_E_STATE, "ks_step_submit: call ks_set_coarse first");
+  return ks_step_submit_impl(ctx, N, h_V, mu, h_lambda, h_U, tol, max_iter, h_FA, h_FB);
+}
+
+ks_status ks_step_wait(ks_ctx *ctx) {
+  if (!ctx) return KS_E_ARG;
+  return ks_step_wait_impl(ctx);
 }
 
 ks_status ks_solve_trace(ks_ctx *ctx, int32_t cap, uint64_t *h_ns, int32_t *h_count) {

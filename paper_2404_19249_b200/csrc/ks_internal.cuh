@@ -113,6 +113,13 @@ struct ks_ctx {
   int64_t stage_groups = 0, stage_staged = 0;
   int32_t *stage_meta = nullptr;
   uint16_t *stage_slcol = nullptr, *stage_dlc = nullptr;
+  // pipelined host-buffer steps (ks_stream.cu)
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
+  double *st_V[2] = {nullptr, nullptr}, *st_lam[2] = {nullptr, nullptr}, *st_U[2] = {nullptr, nullptr};
+  double *st_Ut[2] = {nullptr, nullptr}, *st_FA[2] = {nullptr, nullptr}, *st_FB[2] = {nullptr, nullptr};
+  int step_N = 0;
+  int64_t step_D = 0, step_count = 0;
   int interp_fallbacks = 0;         // last ks_interpolation needed the scan fallback of the walk
   // NEXT-1 (ks_outer.cu): cuSOLVER handle, pencil and outer-loop workspaces
   void *cusolver = nullptr;
@@ -197,6 +204,10 @@ ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, cons
 ks_status ks_project_impl(ks_ctx *ctx, int N, const double *Ut, double *FA, double *FB);
 void ks_free_coarse(ks_ctx *ctx);
 void ks_free_outer(ks_ctx *ctx);
+void ks_free_stream(ks_ctx *ctx);
+ks_status ks_step_submit_impl(ks_ctx *ctx, int N, const double *h_V, double mu, const double *h_lambda,
+                              const double *h_U, double tol, int max_iter, double *h_FA, double *h_FB);
+ks_status ks_step_wait_impl(ks_ctx *ctx);
 ks_status ks_density_impl(ks_ctx *ctx, int N, const double *U, double f, double *rho);
 ks_status ks_vxc_impl(ks_ctx *ctx, const double *rho, double *vxc, double *eps);
 ks_status ks_scf_solve_impl(ks_ctx *ctx, int N, const double *vext, double f, double mu, double *lambda, double *U,

@@ -25,7 +25,8 @@ OPS = {"K": 0, "M": 1, "MV": 2, "H": 3, "A": 4}
 EXPORTS = ["ks_abi_version", "ks_build_info", "ks_create", "ks_destroy", "ks_set_stream", "ks_pattern",
            "ks_values", "ks_assemble_veff", "ks_spmm", "ks_block_solve", "ks_last_iterations", "ks_solve_trace",
            "ks_true_residual", "ks_set_coarse", "ks_project_augmented", "ks_pencil_eig", "ks_lift",
-           "ks_augmented_solve", "ks_interpolation", "ks_density", "ks_vxc", "ks_hartree", "ks_scf_solve", "ks_memory_bytes", "ks_launch_count", "ks_sync", "ks_last_error"]
+           "ks_augmented_solve", "ks_interpolation", "ks_density", "ks_vxc", "ks_hartree", "ks_scf_solve",
+           "ks_step_submit", "ks_step_wait", "ks_memory_bytes", "ks_launch_count", "ks_sync", "ks_last_error"]
 
 
 class KSError(RuntimeError):
@@ -72,6 +73,8 @@ def load_library(path: str = LIB_PATH):
         "ks_hartree": (st, [vp, vp, dbl, i32, vp, i32, vp, C.POINTER(i32)]),
         "ks_scf_solve": (st, [vp, i32, vp, dbl, dbl, vp, vp, dbl, i32, i32, dbl, dbl, i32, dbl, dbl,
                               C.POINTER(i32), vp, vp, vp]),
+        "ks_step_submit": (st, [vp, i32, vp, dbl, vp, vp, dbl, i32, vp, vp]),
+        "ks_step_wait": (st, [vp]),
         "ks_memory_bytes": (st, [vp, C.POINTER(C.c_size_t)]),
         "ks_launch_count": (st, [vp, C.POINTER(i64)]),
         "ks_sync": (st, [vp]),
@@ -354,6 +357,16 @@ class Context:
         k = outer.value
         return dict(outer=k, inner=inner_steps[:k], dres=dres[:k], lams=lams[:k], converged=st == KS_OK)
 
+    def step_submit(self, V_host, mu, lam_host, U_host, FA_host, FB_host, tol=1e-10, max_iter=2000):
+        """ks_step_submit: one pipelined hot-path step from host buffers (pinned torch CPU tensors)."""
+        N = U_host.shape[1]
+        self._call(self._L.ks_step_submit(self._h, N, V_host.data_ptr(), float(mu), lam_host.data_ptr(),
+                                          U_host.data_ptr(), float(tol), int(max_iter), FA_host.data_ptr(),
+                                          FB_host.data_ptr()))
+
+    def step_wait(self):
+        self._call(self._L.ks_step_wait(self._h))
+
     def memory_bytes(self) -> int:
         v = C.c_size_t()
         self._call(self._L.ks_memory_bytes(self._h, C.byref(v)))
@@ -386,26 +399,16 @@ def _raw_tensor(dptr: int, count: int, dtype, device):
     return torch.as_tensor(obj, device=device)
 
 
-def solve_step_host(ctx: Context, V_host, mu, lam_host, U_host, dev_bufs=None, tol=1e-10, max_iter=2000):
-    """One hot-path step from HOST buffers (pinned torch CPU tensors): H2D of V, lambda, U; assemble,
-    block solve, project on the device; D2H of F_A, F_B. Returns (FA, FB) host tensors and device bufs."""
+def solve_step_host(ctx: Context, V_host, mu, lam_host, U_host, out=None, tol=1e-10, max_iter=2000, wait=True):
+    """One hot-path step from HOST buffers (pinned torch CPU tensors) through ks_step_submit: H2D of V, lambda,
+    U; assemble, block solve, project on the device; D2H of F_A, F_B into `out` (a pair of pinned host
+    tensors, allocated when None). With wait=False consecutive calls pipeline (ks_step_wait completes them)."""
     import torch
     N = U_host.shape[1]
-    if dev_bufs is None:
-        dev_bufs = dict(V=torch.empty_like(V_host, device="cuda"), lam=torch.empty_like(lam_host, device="cuda"),
-                        U=torch.empty_like(U_host, device="cuda"), Ut=torch.empty_like(U_host, device="cuda"),
-                        FA=torch.empty((ctx.n_H + N, ctx.n_H + N), dtype=torch.float64, device="cuda"),
-                        FB=torch.empty((ctx.n_H + N, ctx.n_H + N), dtype=torch.float64, device="cuda"),
-                        FA_h=torch.empty((ctx.n_H + N, ctx.n_H + N), dtype=torch.float64).pin_memory(),
-                        FB_h=torch.empty((ctx.n_H + N, ctx.n_H + N), dtype=torch.float64).pin_memory())
-    b = dev_bufs
-    with torch.cuda.stream(ctx.stream):
-        b["V"].copy_(V_host, non_blocking=True)
-        b["lam"].copy_(lam_host, non_blocking=True)
-        b["U"].copy_(U_host, non_blocking=True)
-        ctx.assemble_veff(b["V"], mu)
-        ctx.block_solve(b["lam"], b["U"], b["Ut"], tol=tol, max_iter=max_iter)
-        ctx.project_augmented(b["Ut"], b["FA"], b["FB"])
-        b["FA_h"].copy_(b["FA"], non_blocking=True)
-        b["FB_h"].copy_(b["FB"], non_blocking=True)
-    return b["FA_h"], b["FB_h"], dev_bufs
+    D = ctx.n_H + N
+    if out is None:
+        out = (torch.empty((D, D), dtype=torch.float64).pin_memory(), torch.empty((D, D), dtype=torch.float64).pin_memory())
+    ctx.step_submit(V_host, mu, lam_host, U_host, out[0], out[1], tol=tol, max_iter=max_iter)
+    if wait:
+        ctx.step_wait()
+    return out

@@ -319,3 +319,28 @@ def test_block_solve_staged_s_phase(c, monkeypatch):
     assert st == 0 and ref["status"] == 0
     assert np.all(_mnorm_rel(k.om.csr("M"), ut, ref["Ut"]) <= 1e-8)
     assert np.all(np.abs(it - ref["iters"]) <= 2)
+
+
+def test_pipelined_host_steps_equal_the_device_path():
+    """ks_step_submit / ks_step_wait (two device slots, copy streams) give bitwise the same F_A, F_B as the
+    device-resident calls on the same inputs, for several pipelined steps with alternating inputs."""
+    import paper_2404_19249_b200 as ks
+    k = case(2)
+    p = k.p
+    rng = np.random.default_rng(5)
+    Us = [p.U, p.U + 1e-3 * rng.standard_normal(p.U.shape), p.U]
+    ref = []
+    for U in Us:
+        Ut, _, _ = k.ctx.block_solve(dt(p.lam), dt(U))
+        FA, FB = k.ctx.project_augmented(Ut)
+        ref.append((FA.cpu().numpy(), FB.cpu().numpy()))
+    Vh = torch.from_numpy(p.V).pin_memory()
+    lamh = torch.from_numpy(p.lam).pin_memory()
+    Uhs = [torch.from_numpy(np.ascontiguousarray(U)).pin_memory() for U in Us]
+    outs = []
+    for Uh in Uhs:
+        outs.append(ks.solve_step_host(k.ctx, Vh, p.mu, lamh, Uh, None, wait=False))
+    k.ctx.step_wait()
+    assert k.ctx.sync() == 0
+    for (FA, FB), (FAr, FBr) in zip(outs, ref):
+        assert np.array_equal(FA.numpy(), FAr) and np.array_equal(FB.numpy(), FBr)
