@@ -481,6 +481,152 @@ __global__ void __launch_bounds__(PBG_WARPS * 32) k_proj_bg(const double *__rest
   }
 }
 
+// The same item pass on the FP64 tensor cores (NP = 8, 16, 32): both products are dense
+// contractions over the warp's rows, taken 4 rows (one k-step) at a time with mma.m8n8k4.f64:
+//   Gram   G_op[8ta.., 8tb..] += U~[rows, 8ta..]^T Y_op[rows, 8tb..]      (upper tiles ta <= tb)
+//   b / c  bc_op[c, 8tb..]    += P_item[rows, c]^T  Y_op[rows, 8tb..]      (A rows 0..3 = the 4 parent
+//                                                                          slots, rows 4..7 zero)
+// Fragments (PTX m8n8k4 .f64): A[m = lane/4][k = lane%4], B[k = lane%4][n = lane/4], C[m = lane/4][n =
+// 2(lane%4) + v]. The Y fragments serve both products, so every staged double is read from shared memory
+// once per lane group instead of once per register tile. A k-step that crosses an item boundary is split
+// into masked segments (P = 0 outside the segment); rows past the chunk are zeroed by select (never by a
+// multiply: stale shared memory may hold NaN patterns).
+template <int NP>
+__global__ void __launch_bounds__(PBG_WARPS * 32, NP == 32 ? 1 : 2) k_proj_bg_mma(const double *__restrict__ Up,
+                                                                const double *__restrict__ YHp,
+                                                                const double *__restrict__ YMp,
+                                                                const double *__restrict__ Pv4p,
+                                                                const int32_t *__restrict__ item_ptr, int64_t n_items,
+                                                                double *__restrict__ bH_part,
+                                                                double *__restrict__ cH_part,
+                                                                double *__restrict__ gram_part) {
+  static_assert(NP == 8 || NP == 16 || NP == 32, "mma item pass: NP in {8, 16, 32}");
+  constexpr int TT = NP / 8;                       // 8-wide tiles per dimension
+  constexpr int NU = TT * (TT + 1) / 2;            // upper tiles per operator
+  constexpr int CH = PbgLayout<NP>::CH, STAGE = PbgLayout<NP>::STAGE;
+  static_assert(CH % 4 == 0, "chunks of whole k-steps");
+  extern __shared__ __align__(16) double dsm[];
+  __shared__ __align__(8) uint64_t bars[PBG_WARPS][PBG_STAGES];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, grp = lane >> 2, tig = lane & 3;
+  double *ring = dsm + (size_t)warp * PBG_STAGES * STAGE;
+  const int64_t gw = (int64_t)blockIdx.x * PBG_WARPS + warp, nw = (int64_t)gridDim.x * PBG_WARPS;
+  const int64_t ia = n_items * gw / nw, ib = n_items * (gw + 1) / nw;
+  const int32_t ra = __ldg(item_ptr + ia), rb = __ldg(item_ptr + ib);
+  const int nchunks = (rb - ra + CH - 1) / CH;
+
+  double g[2][NU][2], bc[2][TT][2];
+#pragma unroll
+  for (int op = 0; op < 2; op++) {
+#pragma unroll
+    for (int t = 0; t < NU; t++) g[op][t][0] = g[op][t][1] = 0.0;
+#pragma unroll
+    for (int t = 0; t < TT; t++) bc[op][t][0] = bc[op][t][1] = 0.0;
+  }
+
+  auto issue = [&](int c) {
+    const int st = c % PBG_STAGES;
+    const int32_t r0 = ra + c * CH, cnt = min(CH, rb - r0);
+    double *S = ring + st * STAGE;
+    const unsigned bv = (unsigned)cnt * NP * 8u, bp = (unsigned)cnt * 32u;
+    mbar_expect_tx(&bars[warp][st], 3 * bv + bp);
+    bulk_g2s(S, Up + (int64_t)r0 * NP, bv, &bars[warp][st]);
+    bulk_g2s(S + CH * NP, YHp + (int64_t)r0 * NP, bv, &bars[warp][st]);
+    bulk_g2s(S + 2 * CH * NP, YMp + (int64_t)r0 * NP, bv, &bars[warp][st]);
+    bulk_g2s(S + 3 * CH * NP, Pv4p + 4 * (int64_t)r0, bp, &bars[warp][st]);
+  };
+  if (lane == 0) {
+    for (int st = 0; st < PBG_STAGES; st++) mbar_init(&bars[warp][st], 1);
+    mbar_fence_init();
+    for (int c = 0; c < PBG_STAGES && c < nchunks; c++) issue(c);
+  }
+  __syncwarp();
+
+  int64_t it = ia;
+  int32_t iend = __ldg(item_ptr + ia + 1);
+  auto flush = [&]() {
+    if (grp < 4) {
+#pragma unroll
+      for (int op = 0; op < 2; op++) {
+        double *dst = (op ? cH_part : bH_part) + (4 * it + grp) * NP + 2 * tig;
+#pragma unroll
+        for (int t = 0; t < TT; t++) *reinterpret_cast<double2 *>(dst + 8 * t) = make_double2(bc[op][t][0], bc[op][t][1]);
+      }
+    }
+#pragma unroll
+    for (int op = 0; op < 2; op++)
+#pragma unroll
+      for (int t = 0; t < TT; t++) bc[op][t][0] = bc[op][t][1] = 0.0;
+  };
+
+  for (int c = 0; c < nchunks; c++) {
+    const int st = c % PBG_STAGES;
+    mbar_wait(&bars[warp][st], (unsigned)(c / PBG_STAGES) & 1u);
+    const double *S = ring + st * STAGE;
+    const int32_t r0 = ra + c * CH, cnt = min(CH, rb - r0);
+    for (int kk = 0; kk < cnt; kk += 4) {
+      const bool rv = kk + tig < cnt;
+      const int so = (kk + tig) * NP + grp;
+      double fu[TT], fh[TT], fm[TT];
+#pragma unroll
+      for (int t = 0; t < TT; t++) {
+        fu[t] = rv ? S[so + 8 * t] : 0.0;
+        fh[t] = rv ? S[CH * NP + so + 8 * t] : 0.0;
+        fm[t] = rv ? S[2 * CH * NP + so + 8 * t] : 0.0;
+      }
+      int u = 0;
+#pragma unroll
+      for (int ta = 0; ta < TT; ta++)
+#pragma unroll
+        for (int tb = ta; tb < TT; tb++, u++) {
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(g[0][u][0]), "+d"(g[0][u][1]) : "d"(fu[ta]), "d"(fh[tb]));
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(g[1][u][0]), "+d"(g[1][u][1]) : "d"(fu[ta]), "d"(fm[tb]));
+        }
+      const double pv = (rv && grp < 4) ? S[3 * CH * NP + (kk + tig) * 4 + grp] : 0.0;
+      const int32_t kb = r0 + kk, ke = min(kb + 4, r0 + cnt), r = kb + tig;
+      int32_t lo = kb;
+      while (true) {                       // segments of the k-step by item (warp-uniform)
+        while (lo >= iend) {
+          flush();
+          it++;
+          iend = __ldg(item_ptr + it + 1);
+        }
+        const int32_t hi = min(ke, iend);
+        const double pa = (r >= lo && r < hi) ? pv : 0.0;
+#pragma unroll
+        for (int t = 0; t < TT; t++) {
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(bc[0][t][0]), "+d"(bc[0][t][1]) : "d"(pa), "d"(fh[t]));
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(bc[1][t][0]), "+d"(bc[1][t][1]) : "d"(pa), "d"(fm[t]));
+        }
+        lo = hi;
+        if (lo >= ke) break;
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && c + PBG_STAGES < nchunks) issue(c + PBG_STAGES);
+  }
+  if (ib > ia) flush();
+  // per-warp partial [2][NP][NP], both triangles
+  double *out = gram_part + gw * 2 * NP * NP;
+#pragma unroll
+  for (int op = 0; op < 2; op++) {
+    int u = 0;
+#pragma unroll
+    for (int ta = 0; ta < TT; ta++)
+#pragma unroll
+      for (int tb = ta; tb < TT; tb++, u++)
+#pragma unroll
+        for (int v = 0; v < 2; v++) {
+          const int a = 8 * ta + grp, b = 8 * tb + 2 * tig + v;
+          out[op * NP * NP + a * NP + b] = g[op][u][v];
+          if (ta != tb) out[op * NP * NP + b * NP + a] = g[op][u][v];
+        }
+  }
+}
+
 // beta / gamma blocks: one warp per entry sums the per-warp Gram partials (lane-strided, then a fixed
 // butterfly: deterministic)
 __global__ void k_gram_fin(const double *__restrict__ part, int nparts, int N, int NP, int64_t n_H, int64_t D,
@@ -683,6 +829,15 @@ ks_status launch_proj_a(ks_ctx *ctx, const double *op_sell_vals) {   // Op in th
   return KS_OK;
 }
 
+// KS_PROJ_MMA=0 selects the FFMA item pass (A/B knob); default: tensor cores
+bool proj_mma_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("KS_PROJ_MMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int NP>
 ks_status launch_proj_yb(ks_ctx *ctx, int N, const double *u, double *FA, double *FB, int64_t D) {
   cudaStream_t s = ctx->stream;
@@ -703,9 +858,22 @@ ks_status launch_proj_yb(ks_ctx *ctx, int N, const double *u, double *FA, double
     }
   }
   const size_t bsm = PBG_WARPS * PbgLayout<NP>::WARP_BYTES;
-  KS_CUDA(ctx, cudaFuncSetAttribute(k_proj_bg<NP, GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
-  k_proj_bg<NP, GRAM><<<grid, PBG_WARPS * 32, bsm, s>>>(ctx->proj_up, ctx->Y_H, ctx->Y_M, ctx->Pv4p, ctx->item_ptr,
-                                                         ctx->n_items, ctx->bH_part, ctx->cH_part, ctx->gram_part);
+  if constexpr (NP == 8 || NP == 16 || NP == 32) {
+    if (proj_mma_enabled()) {
+      KS_CUDA(ctx, cudaFuncSetAttribute(k_proj_bg_mma<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+      k_proj_bg_mma<NP><<<grid, PBG_WARPS * 32, bsm, s>>>(ctx->proj_up, ctx->Y_H, ctx->Y_M, ctx->Pv4p, ctx->item_ptr,
+                                                          ctx->n_items, ctx->bH_part, ctx->cH_part, ctx->gram_part);
+    } else {
+      KS_CUDA(ctx, cudaFuncSetAttribute(k_proj_bg<NP, GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+      k_proj_bg<NP, GRAM><<<grid, PBG_WARPS * 32, bsm, s>>>(ctx->proj_up, ctx->Y_H, ctx->Y_M, ctx->Pv4p,
+                                                             ctx->item_ptr, ctx->n_items, ctx->bH_part, ctx->cH_part,
+                                                             ctx->gram_part);
+    }
+  } else {
+    KS_CUDA(ctx, cudaFuncSetAttribute(k_proj_bg<NP, GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+    k_proj_bg<NP, GRAM><<<grid, PBG_WARPS * 32, bsm, s>>>(ctx->proj_up, ctx->Y_H, ctx->Y_M, ctx->Pv4p, ctx->item_ptr,
+                                                           ctx->n_items, ctx->bH_part, ctx->cH_part, ctx->gram_part);
+  }
   KS_LAUNCHED(ctx);
   if (GRAM) {
     k_gram_fin<<<ks_blocks(2 * N * N * 32, 128), 128, 0, s>>>(ctx->gram_part, nparts, N, NP, ctx->n_H, D, FA, FB);
