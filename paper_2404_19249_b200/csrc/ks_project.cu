@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(256) k_proj_y(const int32_t *__restrict__ sell
 
 // Item partials of P^T Op P (A_H with Op = H, B_H with Op = M), G[c][d] = sum_{i in item} P_ic (Op P)_{i,d}
 // for the item's parents c and window slots d. No float atomics; the partition and all orders are fixed.
-constexpr int PA_UNR = 4;        // nonzeros of a row in flight per thread
+constexpr int PA_UNR = 8;        // nonzeros of a row in flight per thread
 
 // Row part: the row's contributions are added in place in its shared row of the item window. The 4 parents of one nonzero have distinct slots (distinct coarse nodes), so their 4
 // read-modify-writes are issued together (one shared-memory latency per nonzero); absent parents write
@@ -282,7 +282,7 @@ __device__ __forceinline__ void proj_a_row_smem(const int32_t *__restrict__ row_
 
 // One block of ITEM_ROWS threads per item (all of its rows at once):
 //   1. thread = row r of the item: its row W[r][0..dn) of the item window (proj_a_row_smem), and P_r;
-//   2. thread = output (c, d): G[c][d] = sum_r P_rc W[r][d], r ascending (fixed order).
+//   2. G = P_item^T W on the FP64 tensor cores (mma.m8n8k4.f64), one warp per 8-column tile of the window.
 __global__ void __launch_bounds__(ITEM_ROWS) k_proj_a(const int32_t *__restrict__ row_ptr,
                                                      const int32_t *__restrict__ col,
                                                      const int32_t *__restrict__ sell_ptr,
@@ -312,17 +312,26 @@ __global__ void __launch_bounds__(ITEM_ROWS) k_proj_a(const int32_t *__restrict_
       proj_a_row_smem(row_ptr, col, sell_ptr, sval, slotmap, Pv4, i, Wl, wcap);
     }
     __syncthreads();
+    // G = P_item^T W on the FP64 tensor cores: warp w takes the 8-column tiles w, w + 4, ... of the window;
+    // k-steps of 4 rows; A[m = c][k = r] = P_rc (rows 4..7 zero), B[k = r][n = d] = W[r][d]. Rows past nr
+    // and columns past dn are zeroed by select (stale shared memory).
+    const int lane = tid & 31, warp = tid >> 5, grp = lane >> 2, tig = lane & 3;
     double *out = AH_part + 4 * (int64_t)d0;
-    for (int x = tid; x < 4 * dn; x += ITEM_ROWS) {
-      const int c = x / dn, d = x % dn;
-      // four interleaved partial sums (rows r = 4m + q), combined in q order: fixed order, 4x the ILP
-      double g[4] = {0.0, 0.0, 0.0, 0.0};
-      int r = 0;
-      for (; r + 4 <= nr; r += 4)
-#pragma unroll
-        for (int q = 0; q < 4; q++) g[q] = fma(Ps[(r + q) * 4 + c], W[(r + q) * ws + d], g[q]);
-      for (int q = 0; r + q < nr; q++) g[q] = fma(Ps[(r + q) * 4 + c], W[(r + q) * ws + d], g[q]);
-      out[x] = (g[0] + g[1]) + (g[2] + g[3]);
+    for (int t = warp; 8 * t < dn; t += ITEM_ROWS / 32) {
+      const int d = 8 * t + grp;
+      double c0 = 0.0, c1 = 0.0;
+      for (int r0 = 0; r0 < nr; r0 += 4) {
+        const int r = r0 + tig;
+        const double av = (grp < 4 && r < nr) ? Ps[r * 4 + grp] : 0.0;
+        const double bv = (r < nr && d < dn) ? W[r * ws + d] : 0.0;
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(c0), "+d"(c1) : "d"(av), "d"(bv));
+      }
+      if (grp < 4) {
+        const int dd = 8 * t + 2 * tig;
+        if (dd < dn) out[grp * dn + dd] = c0;
+        if (dd + 1 < dn) out[grp * dn + dd + 1] = c1;
+      }
     }
     __syncthreads();
   }
