@@ -652,26 +652,60 @@ __global__ void k_gram_fin(const double *__restrict__ part, int nparts, int N, i
 }
 
 // one block per coarse node c: A row from the item partials (dense rows per warp, combined in warp
-// order), and, with WITH_B, b_H / c_H entries (sums over the items in list order).
+// order), and, with WITH_B, b_H / c_H entries (per-warp register sums over the warp's items, combined in
+// warp order). Items are visited 4 at a time per warp so their metadata loads overlap. Fixed order.
+constexpr int PF_BATCH = 4;
 template <bool WITH_B>
 __global__ void k_proj_final(const int32_t *__restrict__ CT_ptr, const int32_t *__restrict__ CT_val,
                              const int32_t *__restrict__ D_ptr, const int32_t *__restrict__ D,
                              const double *__restrict__ AH_part, const double *__restrict__ bH_part,
                              const double *__restrict__ cH_part, int64_t n_H, int N, int NP, double *__restrict__ FA,
                              double *__restrict__ FB, int64_t ldA, int64_t D2) {
-  extern __shared__ double acc[];  // [W][n_H]
+  extern __shared__ double acc[];  // [W][n_H], then (WITH_B) [W][2N]
   const int W = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t c = blockIdx.x;
   for (int64_t x = threadIdx.x; x < W * n_H; x += blockDim.x) acc[x] = 0.0;
   __syncthreads();
-  const int32_t e0 = CT_ptr[c], e1 = CT_ptr[c + 1];
+  const int32_t e0 = __ldg(CT_ptr + c), e1 = __ldg(CT_ptr + c + 1);
   double *mine = acc + warp * n_H;
-  for (int32_t e = e0 + warp; e < e1; e += W) {
-    const int32_t v = CT_val[e], it = v >> 2, cl = v & 3;
-    const int32_t d0 = D_ptr[it], dn = D_ptr[it + 1] - d0;
-    const double *src = AH_part + 4 * (int64_t)d0 + cl * dn;
-    for (int s = lane; s < dn; s += 32) mine[D[d0 + s]] += src[s];
-    __syncwarp();
+  constexpr int BQ = 4;                  // b/c columns per lane: 2N <= 128
+  double bacc[BQ] = {0.0, 0.0, 0.0, 0.0};
+  for (int32_t eb = e0 + warp; eb < e1; eb += PF_BATCH * W) {
+    int32_t v[PF_BATCH], d0[PF_BATCH], dn[PF_BATCH];
+#pragma unroll
+    for (int k = 0; k < PF_BATCH; k++) {
+      const int32_t e = eb + k * W;
+      v[k] = e < e1 ? __ldg(CT_val + e) : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < PF_BATCH; k++) {
+      d0[k] = 0;
+      dn[k] = 0;
+      if (v[k] >= 0) {
+        d0[k] = __ldg(D_ptr + (v[k] >> 2));
+        dn[k] = __ldg(D_ptr + (v[k] >> 2) + 1) - d0[k];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < PF_BATCH; k++) {
+      if (v[k] < 0) continue;
+      const double *src = AH_part + 4 * (int64_t)d0[k] + (v[k] & 3) * dn[k];
+      for (int s = lane; s < dn[k]; s += 32) mine[__ldg(D + d0[k] + s)] += __ldcg(src + s);
+      __syncwarp();
+      if (WITH_B) {
+#pragma unroll
+        for (int q = 0; q < BQ; q++) {
+          const int a = lane + 32 * q;
+          if (a < 2 * N) bacc[q] += __ldcg((a < N ? bH_part : cH_part) + (int64_t)v[k] * NP + (a < N ? a : a - N));
+        }
+      }
+    }
+  }
+  if (WITH_B) {
+    double *bs = acc + W * n_H;
+#pragma unroll
+    for (int q = 0; q < BQ; q++)
+      if (lane + 32 * q < 2 * N) bs[warp * 2 * N + lane + 32 * q] = bacc[q];
   }
   __syncthreads();
   for (int64_t d = threadIdx.x; d < n_H; d += blockDim.x) {
@@ -680,11 +714,11 @@ __global__ void k_proj_final(const int32_t *__restrict__ CT_ptr, const int32_t *
     FA[c * ldA + d] = s;
   }
   if (WITH_B) {
+    const double *bs = acc + W * n_H;
     for (int a = threadIdx.x; a < 2 * N; a += blockDim.x) {
       const int col = a % N;
-      const double *src = a < N ? bH_part : cH_part;
       double s = 0.0;
-      for (int32_t e = e0; e < e1; e++) s += src[(int64_t)CT_val[e] * NP + col];
+      for (int w = 0; w < W; w++) s += bs[w * 2 * N + a];
       double *F = a < N ? FA : FB;
       F[c * D2 + n_H + col] = s;
       F[(n_H + col) * D2 + c] = s;
@@ -914,9 +948,9 @@ ks_status launch_proj_yb(ks_ctx *ctx, int N, const double *u, double *FA, double
 
 template <bool WITH_B>
 ks_status launch_final(ks_ctx *ctx, int N, int NP, double *FA, double *FB, int64_t ldA, int64_t D2) {
-  int W = 4;
-  size_t sm = sizeof(double) * W * ctx->n_H;
-  while (sm > 200 * 1024 && W > 1) { W >>= 1; sm = sizeof(double) * W * ctx->n_H; }
+  int W = 8;
+  size_t sm = sizeof(double) * W * (ctx->n_H + 2 * N);
+  while (sm > 200 * 1024 && W > 1) { W >>= 1; sm = sizeof(double) * W * (ctx->n_H + 2 * N); }
   if (sm > 200 * 1024) return ks_fail(ctx, KS_E_ARG, "n_H = %lld too large for the dense-row reduction", (long long)ctx->n_H);
   KS_CUDA(ctx, cudaFuncSetAttribute(k_proj_final<WITH_B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   k_proj_final<WITH_B><<<(unsigned)ctx->n_H, 32 * W, sm, ctx->stream>>>(ctx->CT_ptr, ctx->CT_val, ctx->item_D_ptr,
