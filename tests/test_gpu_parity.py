@@ -242,8 +242,10 @@ def test_projection_matches_oracle(c):
     assert np.all(np.abs(w - wo) <= 1e-9 * np.abs(wo).max())
 
 
-@pytest.mark.parametrize("N", [1, 3, 5, 16])
+@pytest.mark.parametrize("N", [1, 3, 5, 8, 16, 20, 32, 33, 64])
 def test_projection_ragged_N(N):
+    """Every item-pass variant: NP = 2, 4 (FFMA), 8, 16, 32 (FP64 tensor cores), 64 (row-block Gram), with
+    ragged N and small items (many item boundaries inside a 4-row k-step)."""
     p = small(n=8, N=N, nc=3)
     k = Case(p)
     rng = np.random.default_rng(N)
