@@ -219,7 +219,10 @@ __global__ void k_lower_bound_ptr(const int32_t *__restrict__ keys, int64_t nk, 
 // K9   k_proj_final / k_gram_fin: fixed-order sums of the partials into F_A, F_B.
 
 template <int NP>
-__global__ void __launch_bounds__(256) k_proj_y(const int32_t *__restrict__ sell_ptr, const int32_t *__restrict__ sell_col,
+#ifndef KS_PY_MINB
+#define KS_PY_MINB 4   // <= 64 registers: 4 blocks/SM (A/B: 436 vs 468 us at C4, same box)
+#endif
+__global__ void __launch_bounds__(256, KS_PY_MINB) k_proj_y(const int32_t *__restrict__ sell_ptr, const int32_t *__restrict__ sell_col,
                                                 const double *__restrict__ H, const double *__restrict__ M,
                                                 const double *__restrict__ U, const int32_t *__restrict__ pos_of_row,
                                                 double *__restrict__ Up, double *__restrict__ YHp,
@@ -283,7 +286,10 @@ __device__ __forceinline__ void proj_a_row_smem(const int32_t *__restrict__ row_
 // One block of ITEM_ROWS threads per item (all of its rows at once):
 //   1. thread = row r of the item: its row W[r][0..dn) of the item window (proj_a_row_smem), and P_r;
 //   2. G = P_item^T W on the FP64 tensor cores (mma.m8n8k4.f64), one warp per 8-column tile of the window.
-__global__ void __launch_bounds__(ITEM_ROWS) k_proj_a(const int32_t *__restrict__ row_ptr,
+#ifndef KS_PA_MINB
+#define KS_PA_MINB 1
+#endif
+__global__ void __launch_bounds__(ITEM_ROWS, KS_PA_MINB) k_proj_a(const int32_t *__restrict__ row_ptr,
                                                      const int32_t *__restrict__ col,
                                                      const int32_t *__restrict__ sell_ptr,
                                                      const double *__restrict__ sval,
