@@ -175,6 +175,60 @@ def next1_times(ctx, Ut, FA, FB, N, stream):
         return {"error": str(ex)[:200]}
 
 
+def next_rows(ctx, p, U, stream, peak):
+    """NEXT-2 / NEXT-3 rows (not part of the timed step), each timed with CUDA events after one warm-up call,
+    with its algorithmic bytes against the measured HBM peak:
+      density  rho = f sum_i u_i^2 at the nodes: read U, free map, write rho;
+      vxc      LDA/PZ potential and energy density: read rho, write v_xc, eps;
+      hartree  multipole boundary data + element loads + Jacobi-PCG on K (N = 1, tol 1e-10): counted as the
+               PCG's init + k textbook iterations at N = 1 (the element and boundary passes are extra);
+      interpolation  Algorithm 1 on an independent jittered coarse Kuhn mesh of nc^3 cells: host setup (bucket
+               grid, face adjacency) + the GPU walk, wall clock around the call (synchronised)."""
+    import torch
+    import gen
+    out = {}
+    try:
+        n, nn, nnz, N = p.n_free, p.n_nodes, int(ctx.nnz), p.N
+
+        def timed(fn):
+            fn()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            r = fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b), r
+
+        def bw(ms, nbytes):
+            g = nbytes / (ms * 1e-3) / 1e9
+            return {"ms": ms, "alg_bytes": int(nbytes), "GB/s": g, "frac": g / peak}
+
+        rho = ctx.density(U, 2.0)
+        ms, _ = timed(lambda: ctx.density(U, 2.0, rho))
+        out["density"] = bw(ms, 8 * N * n + 4 * nn + 8 * nn)
+        vx, ex = ctx.vxc(rho)
+        ms, _ = timed(lambda: ctx.vxc(rho, vx, ex))
+        out["vxc"] = bw(ms, 24 * nn)
+        vh = torch.zeros_like(rho)
+        ms, r = timed(lambda: ctx.hartree(rho, tol=1e-10, vh=vh))
+        k = int(r[2])
+        out["hartree"] = dict(bw(ms, bytes_solve_init(n, nnz, 1) + k * bytes_per_iteration(n, nnz, 1)),
+                              iterations=k)
+        c = gen.make_problem(dict(L=p.L, n=p.nc, grading=None, jitter=0.2, nuclei=[((0.0, 0.0, 0.0), 1)],
+                                  vnoise=0.0, N=1, orbitals="exp", lam=("const", -0.5), nc=1, seed=11))
+        ctx.interpolation(c.xyz, c.tets, c.dirichlet)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, _, _, nH = ctx.interpolation(c.xyz, c.tets, c.dirichlet)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        out["interpolation"] = {"ms_wall": 1e3 * dt, "fine_points": n, "coarse_tets": int(c.tets.shape[0]),
+                                "n_H": int(nH), "points_per_s": n / dt}
+    except Exception as ex:  # reported, never fatal for the headline line
+        out["error"] = str(ex)[:200]
+    return out
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -400,6 +454,7 @@ def run_ours(args, p, rank, world, local):
         "phases_ms": {"assemble_veff": t_asm, "block_solve": t_solve, "project_augmented": t_proj},
         "solve_only_value": N * n * k_last / (t_solve * 1e-3),
         "next1_ms": next1_times(ctx, Ut, FA, FB, N, stream),
+        "next23": next_rows(ctx, p, U, stream, peak),
         "pcg_phases": traced_phases(ctx, lambda: ctx.block_solve(lam, U, Ut, tol=TOL, max_iter=MAX_ITER, iters=iters,
                                                                  relres=relres), n, nnz, N, peak),
         "gpu_launches": int(launches),

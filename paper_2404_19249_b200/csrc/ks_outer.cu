@@ -9,6 +9,8 @@
 //                       eig -> lift, until max |lambda_new - lambda| <= tol_eig * max |lambda|.
 #include <cusolverDn.h>
 
+#include <algorithm>
+
 #include "ks_internal.cuh"
 #include "ks_sell.cuh"
 
@@ -23,20 +25,94 @@ __global__ void k_take_evecs(const double *__restrict__ A, int64_t D, int k, dou
 }
 
 // U_new[i][j] = sum_t P_it Y[col_t][j] + sum_m U~[i][m] Y[n_H + m][j]; one thread per (row, output column)
-__global__ void k_lift(const int32_t *__restrict__ Pptr, const int32_t *__restrict__ Pcol,
-                       const double *__restrict__ Pval, const double *__restrict__ Ut, int N, int ldu,
-                       const double *__restrict__ Y, int k, int64_t n_H, int64_t n, double *__restrict__ Unew,
-                       int ldo) {
-  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (x >= n * k) return;
-  const int64_t i = x / k;
-  const int j = (int)(x % k);
-  double s = 0.0;
-  for (int32_t t = __ldg(Pptr + i); t < __ldg(Pptr + i + 1); t++)
-    s = fma(__ldg(Pval + t), __ldg(Y + (int64_t)__ldg(Pcol + t) * k + j), s);
-  const double *u = Ut + i * ldu;
-  for (int m = 0; m < N; m++) s = fma(__ldg(u + m), __ldg(Y + (n_H + m) * k + j), s);
-  Unew[i * ldo + j] = s;
+// U_new = P y_H + U~ y_t (the lift of the Ritz vectors). One warp per 8 rows: the dense
+// part U~[8 rows][N] x y_t[N][k] on the FP64 tensor cores (mma.m8n8k4.f64, k-steps of 4 orbitals; A[m = row]
+// [k = orbital] from global, B = y_t staged in shared memory per block), then the <= 4 coarse parents of
+// each row added from y_H in the epilogue (fragment C[m = lane/4][n = 2(lane%4) + v]). Ragged N and k are
+// masked by select.
+constexpr int LIFT_WARPS = 8;
+// row stride of the staged y_t: S = 4 (mod 16) doubles, so the B-fragment loads of a half-warp (rows tig,
+// columns grp: addresses tig*S + grp) hit 16 distinct 8-byte bank pairs (K8 = 32 would be 4-way conflicted)
+__host__ __device__ inline int lift_stride(int k) {
+  const int K8 = (k + 7) & ~7;
+  return K8 + ((4 - K8) % 16 + 16) % 16;
+}
+__global__ void __launch_bounds__(LIFT_WARPS * 32) k_lift(const int32_t *__restrict__ Pptr,
+                                                          const int32_t *__restrict__ Pcol,
+                                                          const double *__restrict__ Pval,
+                                                          const double *__restrict__ Ut, int N, int ldu,
+                                                          const double *__restrict__ Y, int k, int64_t n_H, int64_t n,
+                                                          double *__restrict__ Unew, int ldo) {
+  extern __shared__ double yt[];   // [N4][S] zero-padded y_t
+  const int N4 = (N + 3) & ~3, K8 = (k + 7) & ~7, S = lift_stride(k);
+  for (int x = threadIdx.x; x < N4 * S; x += blockDim.x) {
+    const int m = x / S, j = x % S;
+    yt[x] = (m < N && j < k) ? __ldg(Y + (n_H + m) * k + j) : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, grp = lane >> 2, tig = lane & 3;
+  const int64_t ntile = (n + 7) / 8;     // 8-row warp tiles, strided over the (persistent) grid
+  for (int64_t tile = (int64_t)blockIdx.x * LIFT_WARPS + (threadIdx.x >> 5); tile < ntile;
+       tile += (int64_t)gridDim.x * LIFT_WARPS) {
+  const int64_t i = tile * 8 + grp;      // this lane's row (A fragments and outputs)
+  const bool rv = i < n;
+  // the row's coarse parents (<= 4), loaded ahead of the MMA loop so their latency overlaps it
+  int32_t pc[4] = {0, 0, 0, 0};
+  double pw[4] = {0.0, 0.0, 0.0, 0.0};
+  int np = 0;
+  if (rv) {
+    const int32_t p0 = __ldg(Pptr + i);
+    np = min(__ldg(Pptr + i + 1) - p0, 4);
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+      if (q < np) {
+        pc[q] = __ldg(Pcol + p0 + q);
+        pw[q] = __ldg(Pval + p0 + q);
+      }
+  }
+  for (int t0 = 0; t0 < K8; t0 += 32) {  // up to 4 column tiles of 8 per pass
+    double c[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    for (int k0 = 0; k0 < N4; k0 += 16) {  // 4 k-steps per batch: independent A loads in flight
+      double a[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int m = k0 + 4 * u + tig;
+        a[u] = (rv && m < N) ? __ldg(Ut + i * ldu + m) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int m = k0 + 4 * u + tig;
+        if (k0 + 4 * u >= N4) break;
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+          if (t0 + 8 * t >= K8) break;
+          const double b = yt[m * S + t0 + 8 * t + grp];
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(c[t][0]), "+d"(c[t][1]) : "d"(a[u]), "d"(b));
+        }
+      }
+    }
+    if (rv) {
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        if (q >= np) break;
+        const double *yh = Y + (int64_t)pc[q] * k;
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+          const int j = t0 + 8 * t + 2 * tig;
+          if (j < k) c[t][0] = fma(pw[q], __ldg(yh + j), c[t][0]);
+          if (j + 1 < k) c[t][1] = fma(pw[q], __ldg(yh + j + 1), c[t][1]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        const int j = t0 + 8 * t + 2 * tig;
+        if (j < k) Unew[i * ldo + j] = c[t][0];
+        if (j + 1 < k) Unew[i * ldo + j + 1] = c[t][1];
+      }
+    }
+  }
+  }
 }
 
 }  // namespace
@@ -120,8 +196,12 @@ ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, co
 
 ks_status ks_lift_impl(ks_ctx *ctx, int N, const double *Ut, int k, const double *Y, double *Unew) {
   const int64_t n = ctx->n_free;
-  k_lift<<<ks_blocks(n * k, 256), 256, 0, ctx->stream>>>(ctx->P_ptr, ctx->P_col, ctx->P_val, Ut, N, N, Y, k, ctx->n_H,
-                                                          n, Unew, k);
+  const size_t sm = sizeof(double) * (size_t)((N + 3) & ~3) * lift_stride(k);
+  if (sm > 200 * 1024) return ks_fail(ctx, KS_E_ARG, "lift: N = %d, k = %d too large for the staged y_t", N, k);
+  if (sm > 48 * 1024) KS_CUDA(ctx, cudaFuncSetAttribute(k_lift, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_lift<<<(unsigned)std::min<int64_t>(ks_blocks(n, 8 * LIFT_WARPS), 8 * (int64_t)ctx->sm_count), LIFT_WARPS * 32, sm,
+           ctx->stream>>>(ctx->P_ptr, ctx->P_col, ctx->P_val, Ut, N, N,
+                                                                              Y, k, ctx->n_H, n, Unew, k);
   KS_LAUNCHED(ctx);
   return KS_OK;
 }

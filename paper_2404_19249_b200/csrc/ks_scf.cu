@@ -9,18 +9,24 @@
 
 namespace {
 
+// 4 lanes per node: lane q sums u_ij^2 over j = q, q + 4, ... (each warp load covers 8 full 32-byte row
+// segments), then a fixed 2-step butterfly; Dirichlet nodes get 0.
 __global__ void k_density(const int32_t *__restrict__ free_of_node, const double *__restrict__ U, int N, double f,
                           int64_t n_nodes, double *__restrict__ rho) {
-  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (v >= n_nodes) return;
-  const int32_t i = __ldg(free_of_node + v);
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t v = g >> 2;
+  const int q = (int)(g & 3);
+  const bool valid = v < n_nodes;   // no early return: the butterfly needs all 4 lanes
+  const int32_t i = valid ? __ldg(free_of_node + v) : -1;
   double s = 0.0;
   if (i >= 0)
-    for (int j = 0; j < N; j++) {
+    for (int j = q; j < N; j += 4) {
       const double u = __ldg(U + (int64_t)i * N + j);
-      s += u * u;
+      s = fma(u, u, s);
     }
-  rho[v] = f * s;
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  if (valid && q == 0) rho[v] = f * s;
 }
 
 __global__ void k_vxc(const double *__restrict__ rho, int64_t n, double *__restrict__ vxc, double *__restrict__ eps) {
@@ -52,7 +58,7 @@ __global__ void k_vxc(const double *__restrict__ rho, int64_t n, double *__restr
 }  // namespace
 
 ks_status ks_density_impl(ks_ctx *ctx, int N, const double *U, double f, double *rho) {
-  k_density<<<ks_blocks(ctx->n_nodes, 256), 256, 0, ctx->stream>>>(ctx->free_of_node, U, N, f, ctx->n_nodes, rho);
+  k_density<<<ks_blocks(4 * ctx->n_nodes, 256), 256, 0, ctx->stream>>>(ctx->free_of_node, U, N, f, ctx->n_nodes, rho);
   KS_LAUNCHED(ctx);
   return KS_OK;
 }
