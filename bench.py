@@ -180,8 +180,10 @@ def next_rows(ctx, p, U, stream, peak):
     with its algorithmic bytes against the measured HBM peak:
       density  rho = f sum_i u_i^2 at the nodes: read U, free map, write rho;
       vxc      LDA/PZ potential and energy density: read rho, write v_xc, eps;
-      hartree  multipole boundary data + element loads + Jacobi-PCG on K (N = 1, tol 1e-10): counted as the
-               PCG's init + k textbook iterations at N = 1 (the element and boundary passes are extra);
+      hartree  multipole boundary data + element loads + the PCG on K (N = 1, tol 1e-10; two-level with the
+               coarse space set above, KS_HARTREE_2L=0: Jacobi): counted as the PCG's init + k textbook
+               iterations at N = 1 plus the two-level restriction/prolongation/coarse bytes (the element and
+               boundary passes are extra);
       interpolation  Algorithm 1 on an independent jittered coarse Kuhn mesh of nc^3 cells: host setup (bucket
                grid, face adjacency) + the GPU walk, wall clock around the call (synchronised)."""
     import torch
@@ -212,8 +214,13 @@ def next_rows(ctx, p, U, stream, peak):
         vh = torch.zeros_like(rho)
         ms, r = timed(lambda: ctx.hartree(rho, tol=1e-10, vh=vh))
         k = int(r[2])
-        out["hartree"] = dict(bw(ms, bytes_solve_init(n, nnz, 1) + k * bytes_per_iteration(n, nnz, 1)),
-                              iterations=k)
+        two_level = os.environ.get("KS_HARTREE_2L", "1") != "0"   # a coarse space is set above
+        nH = int(p.n_H)
+        # two-level (ks_pcg2l.cu): + restriction (perm, r, q, 4-wide P in item order: 52 B/row), prolongation
+        # (4-wide P columns and values: 48 B/row) and the dense K_H^-1 (8 n_H^2) per iteration and in the init
+        extra = (100 * n + 8 * nH * nH) if two_level else 0
+        out["hartree"] = dict(bw(ms, bytes_solve_init(n, nnz, 1) + extra + k * (bytes_per_iteration(n, nnz, 1) + extra)),
+                              iterations=k, preconditioner="two-level (Jacobi + P K_H^-1 P^T)" if two_level else "Jacobi")
         c = gen.make_problem(dict(L=p.L, n=p.nc, grading=None, jitter=0.2, nuclei=[((0.0, 0.0, 0.0), 1)],
                                   vnoise=0.0, N=1, orbitals="exp", lam=("const", -0.5), nc=1, seed=11))
         ctx.interpolation(c.xyz, c.tets, c.dirichlet)

@@ -101,6 +101,14 @@ struct ks_ctx {
   double *har_w = nullptr, *har_c = nullptr, *har_b = nullptr, *har_x0 = nullptr, *har_x = nullptr;
   double *har_mom = nullptr, *har_part = nullptr;
   int32_t *har_iters = nullptr;
+  // two-level preconditioner of the Hartree solve (ks_pcg2l.cu): K_H^-1 = (P^T K P)^-1 on the coarse space
+  int har2l_state = 0;              // 0: not built for the current coarse space, 1: built, -1: unusable
+  double *har2l_KHinv = nullptr;    // [n_H n_H]
+  double *har2l_rpart = nullptr;    // [4 n_items] item restriction partials
+  double *har2l_rH = nullptr, *har2l_y = nullptr;                       // [n_H]
+  double *har2l_r = nullptr, *har2l_r2 = nullptr, *har2l_p = nullptr, *har2l_q = nullptr;  // [n_free]
+  double *har2l_part = nullptr;     // [grid][8] block partials
+  int32_t *har2l_Pc4 = nullptr;     // [4 n_free] P columns as a 4-wide table (pairs with Pv4)
   // NEXT-2 SCF driver workspace
   double *scf_rho = nullptr, *scf_in = nullptr, *scf_out = nullptr, *scf_vh = nullptr, *scf_vxc = nullptr;
   double *scf_veff = nullptr, *scf_Ut = nullptr, *scf_FA = nullptr, *scf_FB = nullptr, *scf_Y = nullptr;
@@ -189,6 +197,11 @@ __device__ __forceinline__ double warp_sum(double v) {
 ks_status ks_setup_mesh(ks_ctx *ctx, const double *h_xyz, const int32_t *h_tets, const uint8_t *h_dir);
 ks_status ks_sell_build(ks_ctx *ctx);
 ks_status ks_stage_build(ks_ctx *ctx, int NP, int max_rows);
+ks_status ks_coarse_galerkin(ks_ctx *ctx, const double *op_sell_vals, double *out);   // P^T Op P, dense [n_H][n_H]
+ks_status ks_spd_inverse(ks_ctx *ctx, double *A, int64_t n, bool *spd);              // A <- A^-1 (Cholesky)
+ks_status ks_pcg2l_run(ks_ctx *ctx, const double *b, const double *x0, double *x, double tol, int max_iter,
+                       int32_t *d_iters);
+void ks_free_pcg2l(ks_ctx *ctx);
 ks_status ks_assemble_impl(ks_ctx *ctx, const double *d_veff, double mu);
 ks_status ks_materialize_views(ks_ctx *ctx);
 ks_status ks_spmm_impl(ks_ctx *ctx, ks_op op, const double *val, int N, const double *X, double *Y);

@@ -133,6 +133,52 @@ void ks_free_outer(ks_ctx *ctx) {
   ctx->cusolver = nullptr;
 }
 
+__global__ void k_mirror_lower(double *A, int64_t n) {   // column-major lower -> full symmetric
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= n * n) return;
+  const int64_t i = x % n, j = x / n;   // A(i, j) = A[i + j n]
+  if (i < j) A[i + j * n] = A[j + i * n];
+}
+
+// A <- A^-1 for a symmetric positive definite [n][n] (Cholesky: potrf + potri, then mirrored); *spd = false
+// (A left unusable) when the factorisation finds a non-positive pivot.
+ks_status ks_spd_inverse(ks_ctx *ctx, double *A, int64_t n, bool *spd) {
+  KS_TRY(ensure_solver_handle(ctx));
+  cusolverDnHandle_t h = (cusolverDnHandle_t)ctx->cusolver;
+  int lw1 = 0, lw2 = 0;
+  if (cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, (int)n, A, (int)n, &lw1) != CUSOLVER_STATUS_SUCCESS ||
+      cusolverDnDpotri_bufferSize(h, CUBLAS_FILL_MODE_LOWER, (int)n, A, (int)n, &lw2) != CUSOLVER_STATUS_SUCCESS)
+    return ks_fail(ctx, KS_E_CUDA, "potrf/potri bufferSize failed");
+  const int lw = lw1 > lw2 ? lw1 : lw2;
+  double *work = nullptr;
+  int *info = nullptr;
+  KS_CUDA(ctx, cudaMallocAsync((void **)&work, sizeof(double) * (size_t)(lw > 0 ? lw : 1), ctx->stream));
+  KS_CUDA(ctx, cudaMallocAsync((void **)&info, sizeof(int), ctx->stream));
+  int hinfo = 0;
+  bool ok = cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, (int)n, A, (int)n, work, lw, info) == CUSOLVER_STATUS_SUCCESS;
+  if (ok) {
+    KS_CUDA(ctx, cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    ok = hinfo == 0;
+  }
+  if (ok) {
+    ok = cusolverDnDpotri(h, CUBLAS_FILL_MODE_LOWER, (int)n, A, (int)n, work, lw, info) == CUSOLVER_STATUS_SUCCESS;
+    if (ok) {
+      KS_CUDA(ctx, cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+      ok = hinfo == 0;
+    }
+  }
+  KS_CUDA(ctx, cudaFreeAsync(work, ctx->stream));
+  KS_CUDA(ctx, cudaFreeAsync(info, ctx->stream));
+  if (ok) {
+    k_mirror_lower<<<ks_blocks(n * n, 256), 256, 0, ctx->stream>>>(A, n);
+    KS_LAUNCHED(ctx);
+  }
+  *spd = ok;
+  return KS_OK;
+}
+
 ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, const double *FB, double *evals,
                              double *evecs) {
   KS_TRY(ensure_solver_handle(ctx));

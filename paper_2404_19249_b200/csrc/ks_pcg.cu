@@ -22,6 +22,7 @@
 #include "ks_internal.cuh"
 #include "ks_rowops.cuh"
 #include "ks_sell.cuh"
+#include "ks_grid.cuh"
 
 namespace {
 
@@ -84,27 +85,6 @@ struct PcgArgs {
   int64_t ngroups;
   int stage_cap;              // staged rows per stage buffer
 };
-
-__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Grid-wide barrier for a cooperative launch (all blocks co-resident). Monotonic counter, reset to 0
-// before the launch; `target` advances by gridDim.x per barrier in every block. The gpu-scope fences
-// make the other blocks' writes visible (and invalidate this SM's L1 lines read before the barrier).
-__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &target) {
-  __syncthreads();
-  target += gridDim.x;
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
-    while (ld_acquire(bar) < target) __nanosleep(20);
-    __threadfence();
-  }
-  __syncthreads();
-}
 
 // out[j] = sum_{g < G} part[g*stride + j] for j < nv, fixed order, one warp per value.
 __device__ __forceinline__ void reduce_partials(const double *part, int stride, int nv, double *out) {

@@ -979,7 +979,15 @@ struct TmpGuard {
 
 }  // namespace
 
+// dense P^T Op P [n_H][n_H] for an operator in the sliced-ELL layout (the A-part of the item pass)
+ks_status ks_coarse_galerkin(ks_ctx *ctx, const double *op_sell_vals, double *out) {
+  if (ctx->n_H <= 0) return ks_fail(ctx, KS_E_STATE, "no coarse space");
+  KS_TRY(launch_proj_a(ctx, op_sell_vals));
+  return launch_final<false>(ctx, 0, 16, out, nullptr, ctx->n_H, 0);
+}
+
 void ks_free_coarse(ks_ctx *ctx) {
+  ks_free_pcg2l(ctx);
   void *ptrs[] = {ctx->P_ptr, ctx->P_col, ctx->P_val, ctx->Pv4, ctx->Pv4p, ctx->pos_of_row, ctx->perm,
 
                   ctx->item_ptr, ctx->item_S, ctx->item_D_ptr, ctx->item_D, ctx->slotmap, ctx->CT_ptr,

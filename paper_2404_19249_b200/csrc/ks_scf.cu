@@ -3,6 +3,7 @@
 //   ks_vxc       LDA exchange + Perdew-Zunger correlation potential (Eqs. expot, copot)
 // Pointwise over all nodes, fp64 (libdevice cbrt / log / sqrt).
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "ks_internal.cuh"
@@ -294,8 +295,17 @@ ks_status ks_hartree_impl(ks_ctx *ctx, const double *rho, double tol, int max_it
   } else {
     KS_CUDA(ctx, cudaMemsetAsync(ctx->har_x0, 0, sizeof(double) * n, s));
   }
-  KS_TRY(ks_pcg_run(ctx, ctx->sell_K, ctx->dinvK, 0.0, 1, nullptr, ctx->har_b, ctx->har_x0, ctx->har_x, tol, max_iter,
-                    ctx->har_iters, nullptr));
+  // two-level preconditioner on the coarse space of ks_set_coarse when one is set (ks_pcg2l.cu, DESIGN.md
+  // §8.4); KS_HARTREE_2L=0 or no coarse space: the Jacobi-PCG of ks_pcg.cu
+  const char *e2l = getenv("KS_HARTREE_2L");
+  ks_status st2 = KS_E_STATE;
+  if (!(e2l && e2l[0] == '0')) {
+    st2 = ks_pcg2l_run(ctx, ctx->har_b, ctx->har_x0, ctx->har_x, tol, max_iter, ctx->har_iters);
+    if (st2 != KS_OK && st2 != KS_E_STATE) return st2;
+  }
+  if (st2 != KS_OK)
+    KS_TRY(ks_pcg_run(ctx, ctx->sell_K, ctx->dinvK, 0.0, 1, nullptr, ctx->har_b, ctx->har_x0, ctx->har_x, tol,
+                      max_iter, ctx->har_iters, nullptr));
   k_hartree_out<<<ks_blocks(nn, 256), 256, 0, s>>>(ctx->free_of_node, ctx->har_x, ctx->har_w, nn, vh);
   KS_LAUNCHED(ctx);
   if (h_mom || h_iters) {

@@ -68,6 +68,31 @@ def test_hartree_matches_oracle(n, centre):
     assert np.abs(vg - exact).max() < 0.2
 
 
+@pytest.mark.parametrize("c", [1, 2])
+def test_hartree_two_level_matches_oracle(c, monkeypatch):
+    """With a coarse space set, ks_hartree runs the two-level preconditioned CG (Jacobi + coarse correction
+    P (P^T K P)^-1 P^T, ks_pcg2l.cu): the same potential as the oracle's Jacobi-PCG within the solve
+    tolerance, in fewer iterations, bitwise reproducible; KS_HARTREE_2L=0 falls back to Jacobi."""
+    p = gen.make_problem(c)
+    ctx = _ctx(p)
+    ctx.set_coarse(p.n_H, dt(p.P_rowptr), dt(p.P_col), dt(p.P_val))
+    xf = p.xyz
+    r = np.sqrt(((xf - np.array([0.3, -0.2, 0.1])) ** 2).sum(1))
+    rho = 2.0 * (2 * np.pi) ** -1.5 * np.exp(-r ** 2 / 2)
+    vh, mom, it2 = ctx.hartree(dt(rho), tol=1e-12)
+    vh_b, _, it2b = ctx.hartree(dt(rho), tol=1e-12)
+    assert ctx.sync() == 0
+    assert torch.equal(vh, vh_b) and it2 == it2b
+    om = oracle.Mesh.from_problem(p)
+    vh_o, _, it_o = om.hartree(rho, tol=1e-12)
+    assert np.abs(vh.cpu().numpy() - vh_o).max() <= 1e-9 * np.abs(vh_o).max()
+    assert it2 < it_o
+    monkeypatch.setenv("KS_HARTREE_2L", "0")
+    vh_j, _, it_j = ctx.hartree(dt(rho), tol=1e-12)
+    assert abs(it_j - it_o) <= 3
+    assert np.abs(vh_j.cpu().numpy() - vh_o).max() <= 1e-9 * np.abs(vh_o).max()
+
+
 def test_hartree_warm_start_reaches_the_same_potential():
     p = gen.make_problem(1)
     ctx = _ctx(p)
