@@ -234,7 +234,11 @@ ks_status ks_vxc(ks_ctx *ctx, const double *d_rho, double *d_vxc, double *d_eps)
  * ks_hartree: the Hartree potential: -Lap V = 4 pi rho, V = w_D on the boundary with the
  * multipole expansion of Eq. bd about the centre of charge (monopole, dipole, quadrupole with the 1/2 of the
  * Taylor term, reading R5; moments exact for the P1 density); P1 Galerkin with the Dirichlet lift,
- * the free values by the batched Jacobi-PCG (N = 1) on the stiffness matrix to ||r|| <= tol ||b||.
+ * the free values by a preconditioned CG on the stiffness matrix to ||r|| <= tol ||b||. When a coarse
+ * space is set (ks_set_coarse), the preconditioner is two-level: Jacobi + P (P^T K P)^-1 P^T, with the
+ * coarse operator built and Cholesky-inverted on the first call after ks_set_coarse. That is NEXT-4
+ * (DESIGN.md §8.4); it falls back to Jacobi if P^T K P is not SPD. Without a coarse space, or with the
+ * environment variable KS_HARTREE_2L=0, it is the batched Jacobi-PCG (N = 1).
  *   d_rho [n_nodes]; d_vh [n_nodes] (out: free values and w_D; in when warm != 0: the warm start);
  *   h_mom [10] (host, may be NULL): Q, centre (3), dipole (3), diagonal of the second moment (3);
  *   h_iters (host, may be NULL): PCG iterations. Synchronises the stream when h_mom or h_iters is given.
