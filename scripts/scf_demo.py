@@ -4,7 +4,7 @@ hot path): a CH4-like molecule (config C3 geometry: C Z=6 at the origin, 4 H at 
 N = 5 doubly occupied orbitals, smoothed Coulomb V_ext), graded fine mesh, an independent graded coarse mesh
 (nonnested) interpolated by ks_interpolation (Algorithm 1), and ks_scf_solve (Algorithm 3 with Anderson
 mixing). Prints one JSON line: sizes, timings, outer/inner iterations, density-change history, Ritz values.
-usage: python scripts/scf_demo.py [fine_cells] [coarse_cells] [mu]"""
+usage: python scripts/scf_demo.py [fine_cells] [coarse_cells] [mu] [max_outer]"""
 import json
 import os
 import sys
@@ -22,6 +22,7 @@ def main():
     nf = int(sys.argv[1]) if len(sys.argv) > 1 else 48
     ncs = int(sys.argv[2]) if len(sys.argv) > 2 else 10
     mu = float(sys.argv[3]) if len(sys.argv) > 3 else 20.0
+    max_outer = int(sys.argv[4]) if len(sys.argv) > 4 else 150
     base = gen.make_config(3)
     nuc = base["nuclei"]
 
@@ -42,7 +43,7 @@ def main():
     U = torch.from_numpy(p.U).to(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    out = ctx.scf_solve(torch.from_numpy(p.V).to(dev), lam, U, mu=mu, f=2.0, tol=1e-7, max_outer=80, inner=30,
+    out = ctx.scf_solve(torch.from_numpy(p.V).to(dev), lam, U, mu=mu, f=2.0, tol=1e-7, max_outer=max_outer, inner=30,
                         inner_tol=1e-7, allow_unconverged=True)
     status = "converged" if out["converged"] else "not converged (max_outer)"
     e1.record()
@@ -59,6 +60,7 @@ def main():
         "lowest_ritz_history": [float("%.8f" % x) for x in out["lams"][:, 0]],
         "ritz_values": lam.cpu().numpy().tolist(), "electrons": float(mom[0]),
         "time_ms": {"scf_total": ms, "per_outer": ms / max(1, out["outer"])},
+        "hartree_preconditioner": "Jacobi" if os.environ.get("KS_HARTREE_2L", "1") == "0" else "two-level",
         "setup_s": {"gen": t1 - t0, "interpolation_and_coarse": t2 - t1},
     }), flush=True)
 
