@@ -83,3 +83,23 @@ def test_next_entry_points_on_a_small_mesh():
     evo, _ = oracle.pencil_eig(FA.cpu().numpy(), FB.cpu().numpy(), p.N)
     assert np.allclose(ev.cpu().numpy(), evo, rtol=1e-9, atol=1e-12)
     assert np.all(np.isfinite(Un.cpu().numpy()))
+
+
+def test_zero_inputs_stop_before_the_first_iteration(monkeypatch):
+    """U = 0 (b = 0 in every column) and rho = 0 (no charge): the solvers stop at the initial check with exact
+    zeros and no 0/0 -- the block PCG, and both Hartree paths (two-level with a coarse space, and Jacobi)."""
+    import paper_2404_19249_b200 as ks
+    p = box(6, L=2.0, N=3, nc=3)
+    ctx = ks.Context(p.xyz, p.tets, p.dirichlet)
+    ctx.assemble_veff(dt(p.V), 5.0)
+    U = torch.zeros((p.n_free, 3), dtype=torch.float64, device=DEV)
+    Ut, iters, relres = ctx.block_solve(dt(p.lam), U)
+    assert ctx.sync() == 0
+    assert torch.count_nonzero(Ut) == 0 and torch.all(iters == 0) and torch.all(relres == 0)
+    ctx.set_coarse(p.n_H, dt(p.P_rowptr), dt(p.P_col), dt(p.P_val))
+    rho = torch.zeros(p.n_nodes, dtype=torch.float64, device=DEV)
+    for env in ("1", "0"):
+        monkeypatch.setenv("KS_HARTREE_2L", env)
+        vh, mom, it = ctx.hartree(rho)
+        assert ctx.sync() == 0
+        assert it == 0 and torch.count_nonzero(vh) == 0 and np.all(mom == 0)

@@ -152,7 +152,7 @@ def test_block_solve_matches_oracle(c):
     assert np.all(tr <= 1e-9)
 
 
-@pytest.mark.parametrize("N", [1, 2, 3, 5, 7, 13, 20, 33])
+@pytest.mark.parametrize("N", [1, 2, 3, 5, 7, 13, 20, 33, 64])
 def test_block_solve_ragged_N(N):
     """Non-power-of-two N (padded internally), ragged tail tiles, N = 1 with odd n."""
     p = small(n=7, N=N)
