@@ -294,7 +294,6 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
         } else {
           sell_row<NP, 2>(a.sell_ptr, a.sell_col, a.A, a.M, row, a.U, sub, au, mu_);
         }
-        const DV<VEC> u = DV<VEC>::ld(a.U + off);
         const double dinv = __ldg(a.dinv + row);
         DV<VEC> r, z;
 #pragma unroll
@@ -307,8 +306,7 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
           acc[2][v] += r.v[v] * r.v[v];
         }
         r.st(a.r + off);
-        z.st(a.p + off);
-        u.st(a.X + off);
+        z.st(a.p + off);   // x0 = u is not copied: the first P phase reads it from U (saves a vector write)
       }
     }
     block_cols<NP, 3>(acc, red, tot);
@@ -462,7 +460,7 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
         if (e < nel) {
           const DV<VEC> r = DV<VEC>::ld(a.r + e);
           DV<VEC> p = DV<VEC>::ld(a.p + e);
-          DV<VEC> x = DV<VEC>::ld(a.X + e);
+          DV<VEC> x = DV<VEC>::ld((it == 0 ? a.U : a.X) + e);   // x0 = u
           const double di = __ldg(a.dinv + e / NP);
 #pragma unroll
           for (int v = 0; v < VEC; v++) {
@@ -480,6 +478,12 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
     }
   }
 
+  if (it == 0) {   // no P phase ran (converged at the initial check, or stopped before it): x = x0 = u
+    for (int ch = blockIdx.x; ch < nchunks; ch += G) {
+      const int64_t e = (int64_t)ch * CHUNK + VEC * threadIdx.x;
+      if (e < nel) DV<VEC>::ld(a.U + e).st(a.X + e);
+    }
+  }
   if (blockIdx.x == 0) {
     for (int c = threadIdx.x; c < a.N; c += blockDim.x) {
       if (a.iters_out) a.iters_out[c] = s_iters[c];
