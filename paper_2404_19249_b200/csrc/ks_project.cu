@@ -226,9 +226,10 @@ __global__ void __launch_bounds__(256, KS_PY_MINB) k_proj_y(const int32_t *__res
                                                 const double *__restrict__ H, const double *__restrict__ M,
                                                 const double *__restrict__ U, const int32_t *__restrict__ pos_of_row,
                                                 double *__restrict__ Up, double *__restrict__ YHp,
-                                                double *__restrict__ YMp, int64_t n) {
+                                                double *__restrict__ YMp, int64_t n, bool write_up) {
   // rows in natural order (coalesced operator stream); outputs scattered, one full row each, into item
-  // order (position pos_of_row[row] of the coarse-parent grouping) for the item pass k_proj_bg
+  // order (position pos_of_row[row] of the coarse-parent grouping) for the item pass k_proj_bg; the
+  // item-ordered copy of U~ only for the FFMA pass (write_up; the tensor-core pass copies U~ rows itself)
   constexpr int VEC = SL<NP>::VEC, LPR = SL<NP>::LPR;
   const int64_t gl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t row = gl / LPR;
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(256, KS_PY_MINB) k_proj_y(const int32_t *__res
   DV<VEC> yh, ym;
   sell_row<NP, 2>(sell_ptr, sell_col, H, M, row, U, sub, yh, ym);
   const int64_t o = (int64_t)__ldg(pos_of_row + row) * NP + sub * VEC;
-  DV<VEC>::ld(U + row * NP + sub * VEC).st(Up + o);
+  if (write_up) DV<VEC>::ld(U + row * NP + sub * VEC).st(Up + o);
   yh.st(YHp + o);
   ym.st(YMp + o);
 }
@@ -506,8 +507,15 @@ __global__ void __launch_bounds__(PBG_WARPS * 32) k_proj_bg(const double *__rest
 // once per lane group instead of once per register tile. A k-step that crosses an item boundary is split
 // into masked segments (P = 0 outside the segment); rows past the chunk are zeroed by select (never by a
 // multiply: stale shared memory may hold NaN patterns).
+// U~ rows: NP <= 16 copied per row from the natural-order block through perm (no item-ordered copy of U~ is
+// written by the Y pass: C4 net -33 us); NP = 32 from the item-ordered copy (1 block/SM: the per-row copies
+// put the perm loads on the pipeline's critical path, C5 +0.3 ms).
 template <int NP>
-__global__ void __launch_bounds__(PBG_WARPS * 32, NP == 32 ? 1 : 2) k_proj_bg_mma(const double *__restrict__ Up,
+__host__ __device__ constexpr bool pbg_gather_u() { return NP <= 16; }
+
+template <int NP>
+__global__ void __launch_bounds__(PBG_WARPS * 32, NP == 32 ? 1 : 2) k_proj_bg_mma(const double *__restrict__ U,
+                                                                const int32_t *__restrict__ perm,
                                                                 const double *__restrict__ YHp,
                                                                 const double *__restrict__ YMp,
                                                                 const double *__restrict__ Pv4p,
@@ -538,23 +546,32 @@ __global__ void __launch_bounds__(PBG_WARPS * 32, NP == 32 ? 1 : 2) k_proj_bg_mm
     for (int t = 0; t < TT; t++) bc[op][t][0] = bc[op][t][1] = 0.0;
   }
 
+  // all lanes: lane 0 registers the stage's bytes and copies the contiguous item-ordered Y_H, Y_M and P
+  // rows; the U~ rows come either per row (lane l < cnt: natural-order row perm[r0 + l], pbg_gather_u) or
+  // as one contiguous copy of the item-ordered block (U = that copy)
   auto issue = [&](int c) {
     const int st = c % PBG_STAGES;
     const int32_t r0 = ra + c * CH, cnt = min(CH, rb - r0);
     double *S = ring + st * STAGE;
     const unsigned bv = (unsigned)cnt * NP * 8u, bp = (unsigned)cnt * 32u;
-    mbar_expect_tx(&bars[warp][st], 3 * bv + bp);
-    bulk_g2s(S, Up + (int64_t)r0 * NP, bv, &bars[warp][st]);
-    bulk_g2s(S + CH * NP, YHp + (int64_t)r0 * NP, bv, &bars[warp][st]);
-    bulk_g2s(S + 2 * CH * NP, YMp + (int64_t)r0 * NP, bv, &bars[warp][st]);
-    bulk_g2s(S + 3 * CH * NP, Pv4p + 4 * (int64_t)r0, bp, &bars[warp][st]);
+    if (lane == 0) {
+      mbar_expect_tx(&bars[warp][st], 3 * bv + bp);
+      if constexpr (!pbg_gather_u<NP>()) bulk_g2s(S, U + (int64_t)r0 * NP, bv, &bars[warp][st]);
+      bulk_g2s(S + CH * NP, YHp + (int64_t)r0 * NP, bv, &bars[warp][st]);
+      bulk_g2s(S + 2 * CH * NP, YMp + (int64_t)r0 * NP, bv, &bars[warp][st]);
+      bulk_g2s(S + 3 * CH * NP, Pv4p + 4 * (int64_t)r0, bp, &bars[warp][st]);
+    }
+    if constexpr (pbg_gather_u<NP>()) {
+      __syncwarp();
+      if (lane < cnt) bulk_g2s(S + lane * NP, U + (int64_t)__ldg(perm + r0 + lane) * NP, NP * 8u, &bars[warp][st]);
+    }
   };
   if (lane == 0) {
     for (int st = 0; st < PBG_STAGES; st++) mbar_init(&bars[warp][st], 1);
     mbar_fence_init();
-    for (int c = 0; c < PBG_STAGES && c < nchunks; c++) issue(c);
   }
   __syncwarp();
+  for (int c = 0; c < PBG_STAGES && c < nchunks; c++) issue(c);
 
   int64_t it = ia;
   int32_t iend = __ldg(item_ptr + ia + 1);
@@ -621,7 +638,7 @@ __global__ void __launch_bounds__(PBG_WARPS * 32, NP == 32 ? 1 : 2) k_proj_bg_mm
       }
     }
     __syncwarp();
-    if (lane == 0 && c + PBG_STAGES < nchunks) issue(c + PBG_STAGES);
+    if (c + PBG_STAGES < nchunks) issue(c + PBG_STAGES);
   }
   if (ib > ia) flush();
   // per-warp partial [2][NP][NP], both triangles
@@ -836,12 +853,6 @@ int pow2_at_least(int N) {
   return np;
 }
 
-int proj_grid(ks_ctx *ctx, int64_t n_items, int warps_per_block) {
-  int64_t g = (n_items + warps_per_block - 1) / warps_per_block;
-  int64_t cap = (int64_t)ctx->sm_count * 8;
-  return (int)(g < cap ? (g < 1 ? 1 : g) : cap);
-}
-
 // P rows as a dense 4-wide table (columns ascending, zero padded): the gather of a neighbour's P row
 // is one 32-byte load instead of the row_ptr -> values chain
 __global__ void k_pv4(const int32_t *__restrict__ Pptr, const double *__restrict__ Pval, int64_t n,
@@ -891,9 +902,12 @@ template <int NP>
 ks_status launch_proj_yb(ks_ctx *ctx, int N, const double *u, double *FA, double *FB, int64_t D) {
   cudaStream_t s = ctx->stream;
   const int64_t n = ctx->n_free;
+  constexpr bool MMA_NP = NP == 8 || NP == 16 || NP == 32;
+  const bool mma = MMA_NP && proj_mma_enabled();
+  const bool gather_u = mma && pbg_gather_u<NP>();
   k_proj_y<NP><<<ks_blocks(n * SL<NP>::LPR, 256), 256, 0, s>>>(ctx->sell_ptr, ctx->sell_col, ctx->sell_H,
                                                                ctx->sell_M, u, ctx->pos_of_row, ctx->proj_up,
-                                                               ctx->Y_H, ctx->Y_M, n);
+                                                               ctx->Y_H, ctx->Y_M, n, !gather_u);
   KS_LAUNCHED(ctx);
   constexpr bool GRAM = NP <= 32;
   const int grid = 2 * ctx->sm_count;
@@ -908,9 +922,10 @@ ks_status launch_proj_yb(ks_ctx *ctx, int N, const double *u, double *FA, double
   }
   const size_t bsm = PBG_WARPS * PbgLayout<NP>::WARP_BYTES;
   if constexpr (NP == 8 || NP == 16 || NP == 32) {
-    if (proj_mma_enabled()) {
+    if (mma) {
       KS_CUDA(ctx, cudaFuncSetAttribute(k_proj_bg_mma<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
-      k_proj_bg_mma<NP><<<grid, PBG_WARPS * 32, bsm, s>>>(ctx->proj_up, ctx->Y_H, ctx->Y_M, ctx->Pv4p, ctx->item_ptr,
+      k_proj_bg_mma<NP><<<grid, PBG_WARPS * 32, bsm, s>>>(gather_u ? u : ctx->proj_up, ctx->perm, ctx->Y_H, ctx->Y_M,
+                                                          ctx->Pv4p, ctx->item_ptr,
                                                           ctx->n_items, ctx->bH_part, ctx->cH_part, ctx->gram_part);
     } else {
       KS_CUDA(ctx, cudaFuncSetAttribute(k_proj_bg<NP, GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
