@@ -14,6 +14,8 @@
 //   order); padding slots hold col = i (own row, a valid gather) and value 0.
 #include <cub/cub.cuh>
 
+#include <vector>
+
 #include "ks_internal.cuh"
 
 namespace {
@@ -71,6 +73,17 @@ ks_status ks_sell_build(ks_ctx *ctx) {
   KS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (ns + 1), s));
   k_sell_count<<<ks_blocks(ns, 256), 256, 0, s>>>(ctx->row_ptr, n, ns, cnt);
   KS_LAUNCHED(ctx);
+  {   // the slice offsets are int32: check the padded total in 64 bits before the scan
+    std::vector<int32_t> hc(ns);
+    KS_CUDA(ctx, cudaMemcpyAsync(hc.data(), cnt, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost, s));
+    KS_CUDA(ctx, cudaStreamSynchronize(s));
+    int64_t tot = 0;
+    for (int32_t c : hc) tot += c;
+    if (tot > 0x7fffffffLL) {
+      KS_CUDA(ctx, cudaFreeAsync(cnt, s));
+      return ks_fail(ctx, KS_E_ARG, "sliced-ELL copy of %lld entries exceeds int32 indexing", (long long)tot);
+    }
+  }
   size_t tmp_bytes = 0;
   KS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, ctx->sell_ptr, (int)(ns + 1), s));
   void *tmp = nullptr;
