@@ -45,10 +45,19 @@ def parse():
     return ap.parse_args()
 
 
+# KS_BENCH_SHARE_GPU=1: smoke test of the multi-rank path on a one-GPU box (tests/test_gpu_bench_multirank.py):
+# ranks share the box's GPUs (local rank mod device count) and the timing plumbing runs on gloo. The ranks'
+# kernels never wait on one another (independent problems); never used for a measurement.
+SHARE_GPU = os.environ.get("KS_BENCH_SHARE_GPU", "0") == "1"
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if SHARE_GPU:
+        import torch
+        local = local % max(1, torch.cuda.device_count())
     return rank, world, local
 
 
@@ -311,6 +320,7 @@ def combine_ranks(ms, units, world, dev):
         return float(ms), float(units)
     import torch
     import torch.distributed as dist
+    dev = "cpu" if SHARE_GPU else dev
     t = torch.tensor([float(ms)], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     u = torch.tensor([float(units)], dtype=torch.float64, device=dev)
@@ -485,7 +495,10 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if SHARE_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     # independent problem per rank (weak scaling): seed offset by rank
     p = gen.make_problem(args.config, seed=rank_seed(args.config, rank))
     if args.impl == "reference":
