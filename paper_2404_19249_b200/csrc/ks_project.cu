@@ -508,8 +508,8 @@ __global__ void __launch_bounds__(PBG_WARPS * 32) k_proj_bg(const double *__rest
 // into masked segments (P = 0 outside the segment); rows past the chunk are zeroed by select (never by a
 // multiply: stale shared memory may hold NaN patterns).
 // U~ rows: NP <= 16 copied per row from the natural-order block through perm (no item-ordered copy of U~ is
-// written by the Y pass: C4 net -33 us); NP = 32 from the item-ordered copy (1 block/SM: the per-row copies
-// put the perm loads on the pipeline's critical path, C5 +0.3 ms).
+// written by the Y pass: C4 net -33 us); NP = 32 from the item-ordered copy (the per-row 256-byte bulk
+// copies cost the item pass +0.3 ms at C5, more than the Y pass saves; prefetching perm did not help).
 template <int NP>
 __host__ __device__ constexpr bool pbg_gather_u() { return NP <= 16; }
 
