@@ -131,6 +131,10 @@ struct ks_ctx {
   int interp_fallbacks = 0;         // last ks_interpolation needed the scan fallback of the walk
   // NEXT-1 (ks_outer.cu): cuSOLVER handle, pencil and outer-loop workspaces
   void *cusolver = nullptr;
+  void *cublas = nullptr;           // cuBLAS handle of the filtered pencil eigensolver (ks_outer.cu)
+  double *ef_buf = nullptr;         // [4][D][m] work blocks of the filtered eigensolver
+  double *ef_small = nullptr;       // [m][m] device staging of the small Rayleigh-Ritz / SVQB matrices
+  int64_t ef_cap = 0, ef_small_cap = 0;
   double *eig_A = nullptr, *eig_B = nullptr, *eig_w = nullptr, *eig_work = nullptr;
   int *eig_info = nullptr;
   int64_t eig_cap = 0;

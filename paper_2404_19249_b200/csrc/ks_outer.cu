@@ -11,6 +11,12 @@
 
 #include <algorithm>
 
+#include <cublas_v2.h>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "ks_internal.cuh"
 #include "ks_sell.cuh"
 
@@ -24,7 +30,6 @@ __global__ void k_take_evecs(const double *__restrict__ A, int64_t D, int k, dou
   out[x] = A[j * D + i];
 }
 
-// U_new[i][j] = sum_t P_it Y[col_t][j] + sum_m U~[i][m] Y[n_H + m][j]; one thread per (row, output column)
 // U_new = P y_H + U~ y_t (the lift of the Ritz vectors). One warp per 8 rows: the dense
 // part U~[8 rows][N] x y_t[N][k] on the FP64 tensor cores (mma.m8n8k4.f64, k-steps of 4 orbitals; A[m = row]
 // [k = orbital] from global, B = y_t staged in shared memory per block), then the <= 4 coarse parents of
@@ -131,6 +136,8 @@ static ks_status ensure_solver_handle(ks_ctx *ctx) {
 void ks_free_outer(ks_ctx *ctx) {
   if (ctx->cusolver) cusolverDnDestroy((cusolverDnHandle_t)ctx->cusolver);
   ctx->cusolver = nullptr;
+  if (ctx->cublas) cublasDestroy((cublasHandle_t)ctx->cublas);
+  ctx->cublas = nullptr;
 }
 
 __global__ void k_mirror_lower(double *A, int64_t n) {   // column-major lower -> full symmetric
@@ -179,6 +186,301 @@ ks_status ks_spd_inverse(ks_ctx *ctx, double *A, int64_t n, bool *spd) {
   return KS_OK;
 }
 
+// ------------------------------------------------------------------------------------------------------
+// Filtered eigensolver for the lowest k eigenpairs of the pencil. After the reduction to
+// standard form, B = L L^T (potrf) and C = L^-1 A L^-T (two trsm), it runs a Chebyshev-filtered subspace
+// iteration on a block of m = k + g vectors.
+//   start   X = L^T Y0, Y0 = [unit vectors on the last k coordinates | g seeded random columns]: the Ritz
+//           vectors of W = [P | U~] lie mostly on the U~ block.
+//   repeat  SVQB-orthonormalise X; Rayleigh-Ritz (X^T C X, m x m, host Jacobi); stop when every wanted
+//           residual ||C x_j - lambda_j x_j|| <= tol * (Gershgorin bound of C); otherwise a degree-DEG
+//           Chebyshev filter damping [lambda_m, bound] (3-term recurrence, one GEMM per degree).
+//   end     y_j = L^-T x_j, F_B-orthonormal by construction.
+// The small dense problems (m <= k + 8 <= 72) are solved on the host by cyclic Jacobi. It falls back to the
+// dense cuSOLVER path if it does not converge.
+namespace {
+
+constexpr int EF_GUARD = 8, EF_DEG = 20, EF_MAXIT = 40;
+
+// cyclic Jacobi for a symmetric n x n (column-major, overwritten): ascending eigenvalues w, eigenvectors V
+void host_jacobi_eig(std::vector<double> &A, int n, std::vector<double> &w, std::vector<double> &V) {
+  V.assign((size_t)n * n, 0.0);
+  for (int i = 0; i < n; i++) V[(size_t)i * n + i] = 1.0;
+  for (int sweep = 0; sweep < 60; sweep++) {
+    int rotated = 0;
+    for (int p = 0; p < n - 1; p++)
+      for (int q = p + 1; q < n; q++) {
+        const double apq = A[(size_t)q * n + p];
+        const double app = A[(size_t)p * n + p], aqq = A[(size_t)q * n + q];
+        // negligible against both diagonal entries (at working precision): no rotation
+        if (std::fabs(apq) <= 1e-18 * std::sqrt(std::fabs(app * aqq)) || apq == 0.0) continue;
+        rotated++;
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), sn = t * c;
+        for (int r = 0; r < n; r++) {   // columns p, q
+          const double arp = A[(size_t)p * n + r], arq = A[(size_t)q * n + r];
+          A[(size_t)p * n + r] = c * arp - sn * arq;
+          A[(size_t)q * n + r] = sn * arp + c * arq;
+        }
+        for (int r = 0; r < n; r++) {   // rows p, q
+          const double apr = A[(size_t)r * n + p], aqr = A[(size_t)r * n + q];
+          A[(size_t)r * n + p] = c * apr - sn * aqr;
+          A[(size_t)r * n + q] = sn * apr + c * aqr;
+        }
+        for (int r = 0; r < n; r++) {
+          const double vp = V[(size_t)p * n + r], vq = V[(size_t)q * n + r];
+          V[(size_t)p * n + r] = c * vp - sn * vq;
+          V[(size_t)q * n + r] = sn * vp + c * vq;
+        }
+      }
+    if (rotated == 0) break;
+  }
+  std::vector<int> idx(n);
+  for (int i = 0; i < n; i++) idx[i] = i;
+  std::sort(idx.begin(), idx.end(), [&](int a, int b) { return A[(size_t)a * n + a] < A[(size_t)b * n + b]; });
+  std::vector<double> V2((size_t)n * n);
+  w.resize(n);
+  for (int j = 0; j < n; j++) {
+    w[j] = A[(size_t)idx[j] * n + idx[j]];
+    for (int r = 0; r < n; r++) V2[(size_t)j * n + r] = V[(size_t)idx[j] * n + r];
+  }
+  V.swap(V2);
+}
+
+__global__ void k_row_abs_max(const double *__restrict__ C, int64_t D, double *__restrict__ out) {
+  // one block: max over rows of sum_j |C_ij| (column-major, symmetric: column sums)
+  __shared__ double red[256];
+  double m = 0.0;
+  for (int64_t j = threadIdx.x; j < D; j += blockDim.x) {
+    double s = 0.0;
+    for (int64_t i = 0; i < D; i++) s += fabs(C[j * D + i]);
+    m = fmax(m, s);
+  }
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+// Yn = alpha (CY - c Y) + beta Xp  (element-wise on D x m blocks)
+__global__ void k_cheb(const double *__restrict__ CY, const double *__restrict__ Y, const double *__restrict__ Xp,
+                       int64_t len, double alpha, double c, double beta, double *__restrict__ Yn) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= len) return;
+  Yn[x] = alpha * (CY[x] - c * Y[x]) + (Xp ? beta * Xp[x] : 0.0);
+}
+
+// squared residual norms of the first k columns: sum_i (CX_ij - lam_j X_ij)^2 (one warp per column)
+__global__ void k_resid(const double *__restrict__ CX, const double *__restrict__ X, const double *__restrict__ lam,
+                        int64_t D, int k, double *__restrict__ out) {
+  const int j = blockIdx.x;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < D; i += blockDim.x) {
+    const double r = CX[j * D + i] - lam[j] * X[j * D + i];
+    s += r * r;
+  }
+  s = warp_sum(s);
+  if (threadIdx.x == 0) out[j] = s;
+}
+
+}  // namespace
+
+static ks_status ensure_blas(ks_ctx *ctx) {
+  if (!ctx->cublas) {
+    cublasHandle_t b = nullptr;
+    if (cublasCreate(&b) != CUBLAS_STATUS_SUCCESS) return ks_fail(ctx, KS_E_CUDA, "cublasCreate failed");
+    ctx->cublas = b;
+  }
+  if (cublasSetStream((cublasHandle_t)ctx->cublas, ctx->stream) != CUBLAS_STATUS_SUCCESS)
+    return ks_fail(ctx, KS_E_CUDA, "cublasSetStream failed");
+  return KS_OK;
+}
+
+#define KS_BLAS(ctx, call)                                                                         \
+  do {                                                                                             \
+    if ((call) != CUBLAS_STATUS_SUCCESS) return ks_fail(ctx, KS_E_CUDA, "cuBLAS call failed: " #call); \
+  } while (0)
+
+// the filtered path on ctx->eig_A (A, overwritten by C) and ctx->eig_B (B, overwritten by L), after potrf.
+// *done = false: not converged (the caller runs the dense path on fresh copies)
+static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *evals, double *evecs, bool *done) {
+  *done = false;
+  KS_TRY(ensure_blas(ctx));
+  cublasHandle_t hb = (cublasHandle_t)ctx->cublas;
+  cudaStream_t st = ctx->stream;
+  const int m = k + EF_GUARD;
+  const double one = 1.0, zero = 0.0;
+  double *A = ctx->eig_A, *L = ctx->eig_B;
+  // C = L^-1 A L^-T (in A)
+  KS_BLAS(ctx, cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)D,
+                           (int)D, &one, L, (int)D, A, (int)D));
+  KS_BLAS(ctx, cublasDtrsm(hb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)D,
+                           (int)D, &one, L, (int)D, A, (int)D));
+  if (ctx->ef_cap < 4 * D * m) {
+    ks_free_t(ctx, ctx->ef_buf);
+    KS_TRY(ks_alloc_t(ctx, &ctx->ef_buf, 4 * D * m, "filtered eig blocks"));
+    ctx->ef_cap = 4 * D * m;
+  }
+  if (ctx->ef_small_cap < (int64_t)m * m + m + 1) {
+    ks_free_t(ctx, ctx->ef_small);
+    KS_TRY(ks_alloc_t(ctx, &ctx->ef_small, (int64_t)m * m + m + 1, "filtered eig small"));
+    ctx->ef_small_cap = (int64_t)m * m + m + 1;
+  }
+  double *X = ctx->ef_buf, *CX = X + D * m, *T1 = CX + D * m, *T2 = T1 + D * m, *sm = ctx->ef_small;
+  // start block: Y0 in T1, X = L^T Y0
+  {
+    std::vector<double> y0((size_t)D * m, 0.0);
+    uint64_t sd = 0x9E3779B97F4A7C15ull;
+    for (int j = 0; j < m; j++) {
+      if (j < k) {
+        y0[(size_t)j * D + (D - k + j)] = 1.0;
+      } else {
+        for (int64_t i = 0; i < D; i++) {
+          sd = sd * 6364136223846793005ull + 1442695040888963407ull;
+          y0[(size_t)j * D + i] = (double)(sd >> 11) * 0x1.0p-53 - 0.5;
+        }
+      }
+    }
+    KS_CUDA(ctx, cudaMemcpyAsync(T1, y0.data(), sizeof(double) * D * m, cudaMemcpyHostToDevice, st));
+    KS_CUDA(ctx, cudaStreamSynchronize(st));
+    KS_BLAS(ctx, cublasDtrmm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)D, m,
+                             &one, L, (int)D, T1, (int)D, X, (int)D));
+  }
+  double bound = 0.0;
+  k_row_abs_max<<<1, 256, 0, st>>>(A, D, sm);
+  KS_LAUNCHED(ctx);
+  KS_CUDA(ctx, cudaMemcpyAsync(&bound, sm, sizeof(double), cudaMemcpyDeviceToHost, st));
+  KS_CUDA(ctx, cudaStreamSynchronize(st));
+  const double tol = 1e-12;
+  std::vector<double> G((size_t)m * m), w, V, Tm, lam(m), res(k);
+  for (int it = 0; it < EF_MAXIT; it++) {
+    // orthonormalise X into T1: CholQR2 (two passes of G = X^T X = R^T R, X <- X R^-1, on the column-scaled
+    // Gram), SVQB (eigen-decomposition of the Gram) when a Cholesky pivot collapses
+    {
+      const double *src = X;
+      bool ok = true;
+      for (int pass = 0; pass < 2 && ok; pass++) {
+        KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, (int)D, &one, src, (int)D, src, (int)D, &zero, sm,
+                                 m));
+        KS_CUDA(ctx, cudaMemcpyAsync(G.data(), sm, sizeof(double) * m * m, cudaMemcpyDeviceToHost, st));
+        KS_CUDA(ctx, cudaStreamSynchronize(st));
+        std::vector<double> dsc(m);
+        for (int j = 0; j < m; j++) dsc[j] = std::sqrt(G[(size_t)j * m + j]);
+        if (!(dsc[0] > 0.0)) return KS_OK;
+        for (int j = 0; j < m; j++)
+          for (int i = 0; i < m; i++) G[(size_t)j * m + i] /= dsc[i] * dsc[j];
+        // Cholesky G = R^T R (upper R, column-major), then Tm = D^-1 R^-1
+        std::vector<double> R((size_t)m * m, 0.0);
+        for (int j = 0; j < m && ok; j++) {
+          for (int i = 0; i <= j; i++) {
+            double v = G[(size_t)j * m + i];
+            for (int l = 0; l < i; l++) v -= R[(size_t)i * m + l] * R[(size_t)j * m + l];
+            if (i == j) {
+              if (!(v > 1e-12)) { ok = false; break; }
+              R[(size_t)j * m + j] = std::sqrt(v);
+            } else {
+              R[(size_t)j * m + i] = v / R[(size_t)i * m + i];
+            }
+          }
+        }
+        if (!ok) break;
+        Tm.assign((size_t)m * m, 0.0);   // R^-1 (upper), by columns
+        for (int j = 0; j < m; j++) {
+          Tm[(size_t)j * m + j] = 1.0 / R[(size_t)j * m + j];
+          for (int i = j - 1; i >= 0; i--) {
+            double v = 0.0;
+            for (int l = i + 1; l <= j; l++) v += R[(size_t)l * m + i] * Tm[(size_t)j * m + l];
+            Tm[(size_t)j * m + i] = -v / R[(size_t)i * m + i];
+          }
+        }
+        for (int j = 0; j < m; j++)
+          for (int i = 0; i < m; i++) Tm[(size_t)j * m + i] /= dsc[i];
+        KS_CUDA(ctx, cudaMemcpyAsync(sm, Tm.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice, st));
+        double *dst = pass == 0 ? T2 : T1;
+        KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, m, &one, src, (int)D, sm, m, &zero, dst,
+                                 (int)D));
+        src = dst;
+      }
+      if (!ok) {   // SVQB of X (rank loss -> dense path)
+        KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, (int)D, &one, X, (int)D, X, (int)D, &zero, sm, m));
+        KS_CUDA(ctx, cudaMemcpyAsync(G.data(), sm, sizeof(double) * m * m, cudaMemcpyDeviceToHost, st));
+        KS_CUDA(ctx, cudaStreamSynchronize(st));
+        std::vector<double> dsc(m);
+        for (int j = 0; j < m; j++) dsc[j] = std::sqrt(G[(size_t)j * m + j]);
+        for (int j = 0; j < m; j++)
+          for (int i = 0; i < m; i++) G[(size_t)j * m + i] /= dsc[i] * dsc[j];
+        host_jacobi_eig(G, m, w, V);
+        if (!(w[0] > 1e-13 * w[m - 1])) return KS_OK;
+        Tm.assign((size_t)m * m, 0.0);
+        for (int j = 0; j < m; j++)
+          for (int i = 0; i < m; i++) Tm[(size_t)j * m + i] = V[(size_t)j * m + i] / (dsc[i] * std::sqrt(w[j]));
+        KS_CUDA(ctx, cudaMemcpyAsync(sm, Tm.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice, st));
+        KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, m, &one, X, (int)D, sm, m, &zero, T1,
+                                 (int)D));
+      }
+    }
+    // Rayleigh-Ritz: H = X^T C X
+    KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, (int)D, &one, A, (int)D, T1, (int)D, &zero, T2,
+                             (int)D));
+    KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, (int)D, &one, T1, (int)D, T2, (int)D, &zero, sm, m));
+    KS_CUDA(ctx, cudaMemcpyAsync(G.data(), sm, sizeof(double) * m * m, cudaMemcpyDeviceToHost, st));
+    KS_CUDA(ctx, cudaStreamSynchronize(st));
+    for (int j = 0; j < m; j++)
+      for (int i = 0; i < j; i++) G[(size_t)j * m + i] = G[(size_t)i * m + j] = 0.5 * (G[(size_t)j * m + i] + G[(size_t)i * m + j]);
+    host_jacobi_eig(G, m, w, V);
+    lam = w;
+    KS_CUDA(ctx, cudaMemcpyAsync(sm, V.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice, st));
+    KS_CUDA(ctx, cudaMemcpyAsync(sm + (int64_t)m * m, lam.data(), sizeof(double) * m, cudaMemcpyHostToDevice, st));
+    KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, m, &one, T1, (int)D, sm, m, &zero, X, (int)D));
+    KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, m, &one, T2, (int)D, sm, m, &zero, CX, (int)D));
+    // wanted residuals
+    k_resid<<<k, 32, 0, st>>>(CX, X, sm + (int64_t)m * m, D, k, T2);
+    KS_LAUNCHED(ctx);
+    KS_CUDA(ctx, cudaMemcpyAsync(res.data(), T2, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+    KS_CUDA(ctx, cudaStreamSynchronize(st));
+    double rmax = 0.0;
+    for (int j = 0; j < k; j++) rmax = std::fmax(rmax, std::sqrt(res[j]));
+    if (!std::isfinite(rmax)) return KS_OK;
+    if (rmax <= tol * bound) {
+      // y = L^-T x for the wanted block, evals
+      KS_BLAS(ctx, cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)D, k,
+                               &one, L, (int)D, X, (int)D));
+      KS_CUDA(ctx, cudaMemcpyAsync(evals, sm + (int64_t)m * m, sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
+      k_take_evecs<<<ks_blocks(D * k, 256), 256, 0, st>>>(X, D, k, evecs);
+      KS_LAUNCHED(ctx);
+      *done = true;
+      return KS_OK;
+    }
+    // Chebyshev filter of degree EF_DEG damping [lam_m, bound]; X_prev = X, Y = sigma/e (C X - c X)
+    const double a = lam[m - 1], b = bound, e = 0.5 * (b - a), c = 0.5 * (b + a);
+    if (!(e > 0.0)) return KS_OK;
+    double sigma = e / (lam[0] - c);
+    const double s1 = 2.0 / sigma;
+    const int64_t len = D * m;
+    double *Xp = X, *Y = T1, *Yn = T2;
+    k_cheb<<<ks_blocks(len, 256), 256, 0, st>>>(CX, X, nullptr, len, sigma / e, c, 0.0, Y);
+    KS_LAUNCHED(ctx);
+    for (int d = 2; d <= EF_DEG; d++) {
+      const double s2 = 1.0 / (s1 - sigma);
+      KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, (int)D, &one, A, (int)D, Y, (int)D, &zero, CX,
+                               (int)D));
+      k_cheb<<<ks_blocks(len, 256), 256, 0, st>>>(CX, Y, Xp, len, 2.0 * s2 / e, c, -sigma * s2, Yn);
+      KS_LAUNCHED(ctx);
+      double *t = Xp;
+      Xp = Y;
+      Y = Yn;
+      Yn = t;
+      sigma = s2;
+    }
+    if (Y != X) KS_CUDA(ctx, cudaMemcpyAsync(X, Y, sizeof(double) * len, cudaMemcpyDeviceToDevice, st));
+  }
+  return KS_OK;
+}
+
 ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, const double *FB, double *evals,
                              double *evecs) {
   KS_TRY(ensure_solver_handle(ctx));
@@ -195,6 +497,37 @@ ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, co
   // symmetric matrices: row-major == column-major
   KS_CUDA(ctx, cudaMemcpyAsync(ctx->eig_A, FA, sizeof(double) * D * D, cudaMemcpyDeviceToDevice, ctx->stream));
   KS_CUDA(ctx, cudaMemcpyAsync(ctx->eig_B, FB, sizeof(double) * D * D, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (!ctx->eig_info) KS_TRY(ks_alloc_t(ctx, &ctx->eig_info, 1, "pencil info"));
+  // the filtered subspace iteration for the lowest k when the block is small against D (KS_PENCIL_DENSE=1:
+  // always the dense cuSOLVER path below; it is also the fallback)
+  const char *dense = getenv("KS_PENCIL_DENSE");
+  if (!(dense && dense[0] == '1') && k <= 64 && k + EF_GUARD <= D / 2) {
+    int lw = 0;
+    if (cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, (int)D, ctx->eig_B, (int)D, &lw) !=
+        CUSOLVER_STATUS_SUCCESS)
+      return ks_fail(ctx, KS_E_CUDA, "cusolverDnDpotrf_bufferSize failed");
+    if (ctx->eig_work_cap < lw) {
+      ks_free_t(ctx, ctx->eig_work);
+      KS_TRY(ks_alloc_t(ctx, &ctx->eig_work, lw, "pencil workspace"));
+      ctx->eig_work_cap = lw;
+    }
+    if (cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, (int)D, ctx->eig_B, (int)D, ctx->eig_work, lw, ctx->eig_info) !=
+        CUSOLVER_STATUS_SUCCESS)
+      return ks_fail(ctx, KS_E_CUDA, "cusolverDnDpotrf failed");
+    ctx->launches++;
+    int pinfo = 0;
+    KS_CUDA(ctx, cudaMemcpyAsync(&pinfo, ctx->eig_info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (pinfo > 0)
+      return ks_fail(ctx, KS_E_RANK, "F_B is not positive definite (leading minor %d): W = [P | U~] is rank deficient",
+                     pinfo);
+    bool done = false;
+    KS_TRY(pencil_eig_filtered(ctx, D, k, evals, evecs, &done));
+    if (done) return KS_OK;
+    // not converged: the dense path on fresh copies
+    KS_CUDA(ctx, cudaMemcpyAsync(ctx->eig_A, FA, sizeof(double) * D * D, cudaMemcpyDeviceToDevice, ctx->stream));
+    KS_CUDA(ctx, cudaMemcpyAsync(ctx->eig_B, FB, sizeof(double) * D * D, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
   // only the lowest k eigenpairs are needed: the index-range solver (bisection + inverse iteration on the
   // tridiagonal form, k back-transformed vectors) instead of all D (KS_PENCIL_ALL=1 selects dsygvd)
   const char *all = getenv("KS_PENCIL_ALL");
