@@ -102,3 +102,45 @@ def test_augmented_solve_converges_like_the_oracle():
         assert np.all(np.abs(hist[it] - lo) <= 1e-9 * np.abs(lo).max()), (it, hist[it], lo)
     Uh = U.cpu().numpy()
     assert np.abs(Uh.T @ M @ Uh - np.eye(p.N)).max() < 1e-8
+
+
+@pytest.mark.parametrize("c", [2, 3])
+def test_filtered_and_dense_pencil_solvers_agree(c, monkeypatch):
+    """ks_pencil_eig's Chebyshev-filtered subspace iteration (default when k + 8 <= D / 2) and the dense
+    cuSOLVER path (KS_PENCIL_DENSE=1) give the same eigenvalues and the same eigenvectors up to sign."""
+    p = gen.make_problem(c)
+    ctx = _ctx(p, p.mu)
+    Ut, _, _ = ctx.block_solve(dt(p.lam), dt(p.U))
+    FA, FB = ctx.project_augmented(Ut)
+    ev_f, Y_f = ctx.pencil_eig(FA, FB, p.N)
+    monkeypatch.setenv("KS_PENCIL_DENSE", "1")
+    ev_d, Y_d = ctx.pencil_eig(FA, FB, p.N)
+    assert ctx.sync() == 0
+    ev_f, ev_d = ev_f.cpu().numpy(), ev_d.cpu().numpy()
+    assert np.all(np.abs(ev_f - ev_d) <= 1e-10 * np.abs(ev_d).max())
+    O = Y_f.cpu().numpy().T @ FB.cpu().numpy() @ Y_d.cpu().numpy()
+    gaps = np.diff(ev_d)
+    simple = np.ones(p.N, bool)
+    simple[1:] &= gaps > 1e-6 * np.abs(ev_d).max()
+    simple[:-1] &= gaps > 1e-6 * np.abs(ev_d).max()
+    assert np.all(np.abs(np.abs(np.diag(O))[simple] - 1.0) <= 1e-8)
+
+
+def test_pencil_eig_random_pencil_any_start():
+    """A random SPD pencil, where the start block (unit vectors on the last k coordinates) carries no
+    information: the filtered iteration still converges (or falls back to the dense path) to scipy's answer."""
+    rng = np.random.default_rng(3)
+    D, k = 300, 8
+    Q = rng.standard_normal((D, D))
+    FA = Q @ np.diag(np.linspace(-5.0, 5.0, D)) @ Q.T / D
+    Bm = rng.standard_normal((D, D))
+    FB = Bm @ Bm.T / D + np.eye(D)
+    p = gen.make_problem(1)
+    ctx = _ctx(p, p.mu)
+    ev, Y = ctx.pencil_eig(dt(FA), dt(FB), k)
+    assert ctx.sync() == 0
+    ref = sl.eigh(FA, FB, eigvals_only=True)[:k]
+    ev, Y = ev.cpu().numpy(), Y.cpu().numpy()
+    assert np.all(np.abs(ev - ref) <= 1e-9 * np.abs(ref).max())
+    assert np.abs(Y.T @ FB @ Y - np.eye(k)).max() <= 1e-9
+    assert np.abs(FA @ Y - (FB @ Y) * ev).max() <= 1e-9 * (np.abs(FA).max() + np.abs(ev).max() * np.abs(FB).max())
