@@ -164,8 +164,9 @@ def traced_phases(ctx, solve, n, nnz, N, peak):
 
 
 def next1_times(ctx, Ut, FA, FB, N, stream):
-    """NEXT-1 (not part of the timed step): the dense pencil eigensolve of the step's F_A, F_B (D = n_H + N,
-    cuSOLVER) and the lift U_new = P y_H + U~ y_t, each timed with CUDA events after one warm-up call."""
+    """NEXT-1 (not part of the timed step): the pencil eigensolve of the step's F_A, F_B (D = n_H + N; the
+    Chebyshev-filtered subspace iteration, dense cuSOLVER with KS_PENCIL_DENSE=1) and the lift
+    U_new = P y_H + U~ y_t, each timed with CUDA events after one warm-up call."""
     import torch
     try:
         out = {}
