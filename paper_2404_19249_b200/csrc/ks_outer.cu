@@ -248,22 +248,16 @@ void host_jacobi_eig(std::vector<double> &A, int n, std::vector<double> &w, std:
   V.swap(V2);
 }
 
-__global__ void k_row_abs_max(const double *__restrict__ C, int64_t D, double *__restrict__ out) {
-  // one block: max over rows of sum_j |C_ij| (column-major, symmetric: column sums)
-  __shared__ double red[256];
-  double m = 0.0;
-  for (int64_t j = threadIdx.x; j < D; j += blockDim.x) {
-    double s = 0.0;
-    for (int64_t i = 0; i < D; i++) s += fabs(C[j * D + i]);
-    m = fmax(m, s);
-  }
-  red[threadIdx.x] = m;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *out = red[0];
+// Gershgorin bound max_j sum_i |C_ij| (symmetric, column-major): one warp per column, the maximum through
+// an integer atomicMax on the bits of the non-negative column sums (order-independent). *out must be 0.
+__global__ void k_row_abs_max(const double *__restrict__ C, int64_t D, unsigned long long *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (j >= D) return;
+  double s = 0.0;
+  for (int64_t i = lane; i < D; i += 32) s += fabs(C[j * D + i]);
+  s = warp_sum(s);
+  if (lane == 0) atomicMax(out, (unsigned long long)__double_as_longlong(s));
 }
 
 // Yn = alpha (CY - c Y) + beta Xp  (element-wise on D x m blocks)
@@ -351,7 +345,8 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
                              &one, L, (int)D, T1, (int)D, X, (int)D));
   }
   double bound = 0.0;
-  k_row_abs_max<<<1, 256, 0, st>>>(A, D, sm);
+  KS_CUDA(ctx, cudaMemsetAsync(sm, 0, sizeof(double), st));
+  k_row_abs_max<<<ks_blocks(32 * D, 256), 256, 0, st>>>(A, D, reinterpret_cast<unsigned long long *>(sm));
   KS_LAUNCHED(ctx);
   KS_CUDA(ctx, cudaMemcpyAsync(&bound, sm, sizeof(double), cudaMemcpyDeviceToHost, st));
   KS_CUDA(ctx, cudaStreamSynchronize(st));

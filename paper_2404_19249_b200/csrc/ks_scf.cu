@@ -167,17 +167,24 @@ __global__ void __launch_bounds__(HB) k_moments2(const int32_t *__restrict__ tet
   block_sum<9>(v, sm, part);
 }
 
-// fixed-order sum of block partials; pass 1 also forms the centre of charge
+// fixed-order sum of block partials (warp k sums value k: lane-strided, then a butterfly); pass 1 also forms
+// the centre of charge. Launch with 32 * nv threads.
 __global__ void k_moments_final(const double *__restrict__ part, int nblk, int nv, int pass, double *__restrict__ mom) {
+  __shared__ double s[9];
+  const int lane = threadIdx.x & 31, k = threadIdx.x >> 5;
+  if (k < nv) {
+    double v = 0.0;
+    for (int b = lane; b < nblk; b += 32) v += part[(int64_t)b * nv + k];
+    v = warp_sum(v);
+    if (lane == 0) s[k] = v;
+  }
+  __syncthreads();
   if (threadIdx.x != 0) return;
-  double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  for (int b = 0; b < nblk; b++)
-    for (int k = 0; k < nv; k++) s[k] += part[(int64_t)b * nv + k];
   if (pass == 1) {
     mom[0] = s[0];
     for (int i = 0; i < 3; i++) mom[1 + i] = s[0] != 0.0 ? s[1 + i] / s[0] : 0.0;
   } else {
-    for (int k = 0; k < 9; k++) mom[4 + k] = s[k];
+    for (int kk = 0; kk < 9; kk++) mom[4 + kk] = s[kk];
   }
 }
 
@@ -269,17 +276,17 @@ ks_status ks_hartree_impl(ks_ctx *ctx, const double *rho, double tol, int max_it
     KS_TRY(ks_alloc_t(ctx, &ctx->har_x0, n, "hartree x0"));
     KS_TRY(ks_alloc_t(ctx, &ctx->har_x, n, "hartree x"));
     KS_TRY(ks_alloc_t(ctx, &ctx->har_mom, 16, "hartree moments"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->har_part, 9 * 2 * (int64_t)ctx->sm_count, "hartree partials"));
+    KS_TRY(ks_alloc_t(ctx, &ctx->har_part, 9 * 8 * (int64_t)ctx->sm_count, "hartree partials"));
     KS_TRY(ks_alloc_t(ctx, &ctx->har_iters, 1, "hartree iterations"));
   }
-  const int nblk = 2 * ctx->sm_count;
+  const int nblk = 8 * ctx->sm_count;   // latency-bound gathers over the tets: 8 blocks per SM
   k_moments1<<<nblk, HB, 0, s>>>(ctx->tets, ctx->vol, ctx->xyz, rho, nt, ctx->har_part);
   KS_LAUNCHED(ctx);
-  k_moments_final<<<1, 32, 0, s>>>(ctx->har_part, nblk, 4, 1, ctx->har_mom);
+  k_moments_final<<<1, 32 * 4, 0, s>>>(ctx->har_part, nblk, 4, 1, ctx->har_mom);
   KS_LAUNCHED(ctx);
   k_moments2<<<nblk, HB, 0, s>>>(ctx->tets, ctx->vol, ctx->xyz, rho, ctx->har_mom, nt, ctx->har_part);
   KS_LAUNCHED(ctx);
-  k_moments_final<<<1, 32, 0, s>>>(ctx->har_part, nblk, 9, 2, ctx->har_mom);
+  k_moments_final<<<1, 32 * 9, 0, s>>>(ctx->har_part, nblk, 9, 2, ctx->har_mom);
   KS_LAUNCHED(ctx);
   k_hartree_boundary<<<ks_blocks(nn, 256), 256, 0, s>>>(ctx->free_of_node, ctx->xyz, ctx->har_mom, nn, ctx->har_w);
   KS_LAUNCHED(ctx);
