@@ -135,6 +135,7 @@ struct ks_ctx {
   double *ef_buf = nullptr;         // [4][D][m] work blocks of the filtered eigensolver
   double *ef_small = nullptr;       // [m][m] device staging of the small Rayleigh-Ritz / SVQB matrices
   int64_t ef_cap = 0, ef_small_cap = 0;
+  int64_t ef_L_D = 0;                // D of the Cholesky factor held in eig_B (0: none)
   double *eig_A = nullptr, *eig_B = nullptr, *eig_w = nullptr, *eig_work = nullptr;
   int *eig_info = nullptr;
   int64_t eig_cap = 0;
@@ -237,7 +238,9 @@ ks_status ks_interpolation_impl(ks_ctx *ctx, int64_t n_c, const double *h_xyz_c,
                                 const uint8_t *h_dir_c, int32_t *d_rowptr, int32_t *d_col, double *d_val,
                                 int64_t *h_nH, int64_t *h_pnnz);
 ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, const double *FB, double *evals,
-                             double *evecs);
+                             double *evecs, const double *Ywarm = nullptr, bool same_B = false);
+// Ywarm [D][k] (device, may alias evecs): start block of the filtered path (e.g. the previous inner step's
+// eigenvectors); same_B: F_B equals the previous call's (its Cholesky factor is reused)
 ks_status ks_lift_impl(ks_ctx *ctx, int N, const double *Ut, int k, const double *Y, double *Unew);
 ks_status ks_augmented_solve_impl(ks_ctx *ctx, int N, double *lambda, double *U, double tol_eig, int max_outer,
                                   double tol_bvp, int32_t max_iter_bvp, int32_t *h_outer, double *h_history);

@@ -268,6 +268,14 @@ __global__ void k_cheb(const double *__restrict__ CY, const double *__restrict__
   Yn[x] = alpha * (CY[x] - c * Y[x]) + (Xp ? beta * Xp[x] : 0.0);
 }
 
+// T[j * D + i] = Y[i * k + j] for the first k columns of a column-major D x m block (Y row-major D x k)
+__global__ void k_put_cols(const double *__restrict__ Y, int64_t D, int k, double *__restrict__ T) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= D * k) return;
+  const int64_t i = x / k, j = x % k;
+  T[j * D + i] = Y[x];
+}
+
 // squared residual norms of the first k columns: sum_i (CX_ij - lam_j X_ij)^2 (one warp per column)
 __global__ void k_resid(const double *__restrict__ CX, const double *__restrict__ X, const double *__restrict__ lam,
                         int64_t D, int k, double *__restrict__ out) {
@@ -301,7 +309,8 @@ static ks_status ensure_blas(ks_ctx *ctx) {
 
 // the filtered path on ctx->eig_A (A, overwritten by C) and ctx->eig_B (B, overwritten by L), after potrf.
 // *done = false: not converged (the caller runs the dense path on fresh copies)
-static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *evals, double *evecs, bool *done) {
+static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *evals, double *evecs, bool *done,
+                                     const double *Ywarm) {
   *done = false;
   KS_TRY(ensure_blas(ctx));
   cublasHandle_t hb = (cublasHandle_t)ctx->cublas;
@@ -340,6 +349,10 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
       }
     }
     KS_CUDA(ctx, cudaMemcpyAsync(T1, y0.data(), sizeof(double) * D * m, cudaMemcpyHostToDevice, st));
+    if (Ywarm) {   // the caller's start vectors replace the unit vectors
+      k_put_cols<<<ks_blocks(D * k, 256), 256, 0, st>>>(Ywarm, D, k, T1);
+      KS_LAUNCHED(ctx);
+    }
     KS_CUDA(ctx, cudaStreamSynchronize(st));
     KS_BLAS(ctx, cublasDtrmm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)D, m,
                              &one, L, (int)D, T1, (int)D, X, (int)D));
@@ -477,7 +490,7 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
 }
 
 ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, const double *FB, double *evals,
-                             double *evecs) {
+                             double *evecs, const double *Ywarm, bool same_B) {
   KS_TRY(ensure_solver_handle(ctx));
   cusolverDnHandle_t h = (cusolverDnHandle_t)ctx->cusolver;
   if (ctx->eig_cap < D) {
@@ -490,13 +503,18 @@ ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, co
     ctx->eig_cap = D;
   }
   // symmetric matrices: row-major == column-major
+  const char *dense = getenv("KS_PENCIL_DENSE");
+  const bool filtered = !(dense && dense[0] == '1') && k <= 64 && k + EF_GUARD <= D / 2;
+  const bool have_L = filtered && same_B && ctx->ef_L_D == D;
   KS_CUDA(ctx, cudaMemcpyAsync(ctx->eig_A, FA, sizeof(double) * D * D, cudaMemcpyDeviceToDevice, ctx->stream));
-  KS_CUDA(ctx, cudaMemcpyAsync(ctx->eig_B, FB, sizeof(double) * D * D, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (!have_L)
+    KS_CUDA(ctx, cudaMemcpyAsync(ctx->eig_B, FB, sizeof(double) * D * D, cudaMemcpyDeviceToDevice, ctx->stream));
+  ctx->ef_L_D = 0;   // eig_B holds F_B (or L below)
   if (!ctx->eig_info) KS_TRY(ks_alloc_t(ctx, &ctx->eig_info, 1, "pencil info"));
   // the filtered subspace iteration for the lowest k when the block is small against D (KS_PENCIL_DENSE=1:
   // always the dense cuSOLVER path below; it is also the fallback)
-  const char *dense = getenv("KS_PENCIL_DENSE");
-  if (!(dense && dense[0] == '1') && k <= 64 && k + EF_GUARD <= D / 2) {
+  if (filtered) {
+    if (!have_L) {
     int lw = 0;
     if (cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, (int)D, ctx->eig_B, (int)D, &lw) !=
         CUSOLVER_STATUS_SUCCESS)
@@ -516,9 +534,12 @@ ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, co
     if (pinfo > 0)
       return ks_fail(ctx, KS_E_RANK, "F_B is not positive definite (leading minor %d): W = [P | U~] is rank deficient",
                      pinfo);
+    }
+    ctx->ef_L_D = D;   // eig_B = L
     bool done = false;
-    KS_TRY(pencil_eig_filtered(ctx, D, k, evals, evecs, &done));
+    KS_TRY(pencil_eig_filtered(ctx, D, k, evals, evecs, &done, Ywarm));
     if (done) return KS_OK;
+    ctx->ef_L_D = 0;
     // not converged: the dense path on fresh copies
     KS_CUDA(ctx, cudaMemcpyAsync(ctx->eig_A, FA, sizeof(double) * D * D, cudaMemcpyDeviceToDevice, ctx->stream));
     KS_CUDA(ctx, cudaMemcpyAsync(ctx->eig_B, FB, sizeof(double) * D * D, cudaMemcpyDeviceToDevice, ctx->stream));

@@ -563,7 +563,10 @@ ks_status ks_scf_solve_impl(ks_ctx *ctx, int N, const double *vext, double f, do
     int next_slot = 0, k = 0;
     for (k = 0; k < inner; k++) {
       KS_TRY(ks_project_impl(ctx, N, ctx->scf_Ut, ctx->scf_FA, ctx->scf_FB));
-      KS_TRY(ks_pencil_eig_impl(ctx, D, N, ctx->scf_FA, ctx->scf_FB, lambda, ctx->scf_Y));
+      // within the inner loop U~ (hence F_B) is fixed: reuse its Cholesky factor and start the filtered
+      // eigensolver from the previous inner step's eigenvectors
+      KS_TRY(ks_pencil_eig_impl(ctx, D, N, ctx->scf_FA, ctx->scf_FB, lambda, ctx->scf_Y, k > 0 ? ctx->scf_Y : nullptr,
+                                k > 0));
       KS_TRY(ks_lift_impl(ctx, N, ctx->scf_Ut, N, ctx->scf_Y, U));
       KS_TRY(ks_density_impl(ctx, N, U, f, ctx->scf_out));
       double dn = 0.0, on = 0.0;
