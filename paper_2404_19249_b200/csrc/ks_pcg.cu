@@ -567,7 +567,7 @@ ks_status launch_pcg(ks_ctx *ctx, PcgArgs &a) {
   a.stage_cap = 0;
   const char *env = getenv("KS_PCG_STAGE");
   const bool want = NP >= 4 && env && env[0] == '1';
-  if constexpr (NP >= 4) {
+  if constexpr (NP >= 4 && PCG_THREADS == 512) {   // the staged layout assumes 512 threads (SP<NP>)
     if (want) {
       const int max_rows = (int)((PSTAGE_SMEM_MAX / PSTAGES - META_SLOT) / (NP * 8));
       KS_TRY(ks_stage_build(ctx, NP, max_rows));
