@@ -365,7 +365,9 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
   KS_CUDA(ctx, cudaStreamSynchronize(st));
   const double tol = 1e-12;
   std::vector<double> G((size_t)m * m), w, V, Tm, lam(m), res(k);
-  for (int it = 0; it < EF_MAXIT; it++) {
+  int maxit = EF_MAXIT;   // KS_PENCIL_EF_MAXIT: test hook to exercise the dense fallback
+  if (const char *e = getenv("KS_PENCIL_EF_MAXIT")) maxit = atoi(e);
+  for (int it = 0; it < maxit; it++) {
     // orthonormalise X into T1: CholQR2 (two passes of G = X^T X = R^T R, X <- X R^-1, on the column-scaled
     // Gram), SVQB (eigen-decomposition of the Gram) when a Cholesky pivot collapses
     {

@@ -144,3 +144,19 @@ def test_pencil_eig_random_pencil_any_start():
     assert np.all(np.abs(ev - ref) <= 1e-9 * np.abs(ref).max())
     assert np.abs(Y.T @ FB @ Y - np.eye(k)).max() <= 1e-9
     assert np.abs(FA @ Y - (FB @ Y) * ev).max() <= 1e-9 * (np.abs(FA).max() + np.abs(ev).max() * np.abs(FB).max())
+
+
+def test_pencil_eig_falls_back_to_the_dense_path(monkeypatch):
+    """A filtered iteration stopped before convergence (KS_PENCIL_EF_MAXIT=1) falls back to the dense
+    cuSOLVER path on fresh copies of F_A, F_B: the same eigenpairs as KS_PENCIL_DENSE=1."""
+    p = gen.make_problem(2)
+    ctx = _ctx(p, p.mu)
+    Ut, _, _ = ctx.block_solve(dt(p.lam), dt(p.U))
+    FA, FB = ctx.project_augmented(Ut)
+    monkeypatch.setenv("KS_PENCIL_EF_MAXIT", "1")
+    ev_f, Y_f = ctx.pencil_eig(FA, FB, p.N)
+    monkeypatch.delenv("KS_PENCIL_EF_MAXIT")
+    monkeypatch.setenv("KS_PENCIL_DENSE", "1")
+    ev_d, Y_d = ctx.pencil_eig(FA, FB, p.N)
+    assert ctx.sync() == 0
+    assert torch.equal(ev_f, ev_d) and torch.equal(Y_f, Y_d)
