@@ -15,6 +15,8 @@
 //       k_gram_fin    fixed-order sums of the Gram partials.
 // Everything is deterministic (fixed partitions and orders, no float atomics).
 #include <cub/cub.cuh>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "ks_internal.cuh"
 #include "ks_rowops.cuh"
@@ -510,11 +512,28 @@ __global__ void __launch_bounds__(PBG_WARPS * 32) k_proj_bg(const double *__rest
 // once per lane group instead of once per register tile. A k-step that crosses an item boundary is split
 // into masked segments (P = 0 outside the segment); rows past the chunk are zeroed by select (never by a
 // multiply: stale shared memory may hold NaN patterns).
-// U~ rows: NP <= 16 copied per row from the natural-order block through perm (no item-ordered copy of U~ is
-// written by the Y pass: C4 net -33 us); NP = 32 from the item-ordered copy (the per-row 256-byte bulk
-// copies cost the item pass +0.3 ms at C5, more than the Y pass saves; prefetching perm did not help).
+// U~ rows: NP <= 16 gathered from the natural-order block through perm with TMA tile::gather4 (4 rows per
+// copy; no item-ordered copy of U~ is written by the Y pass: C4 net -45 us); NP = 32 from the item-ordered
+// copy (per-row bulk copies cost the item pass +0.3 ms at C5, gather4 +0.22 ms: no net gain over the 0.24 ms
+// the Y pass saves).
+#ifndef KS_PBG_GATHER_MAXNP
+#define KS_PBG_GATHER_MAXNP 16
+#endif
+#ifndef KS_PBG_G4
+#define KS_PBG_G4 1   // the per-row U~ copies as TMA tile::gather4 (4 rows per copy, tensor map of U~): C4 item pass 165 -> 156 us
+#endif
 template <int NP>
-__host__ __device__ constexpr bool pbg_gather_u() { return NP <= 16; }
+__host__ __device__ constexpr bool pbg_gather_u() { return NP <= KS_PBG_GATHER_MAXNP; }
+
+// TMA gather of 4 rows (row indices r0..r3, columns [0, box width)) of a 2-D tensor into shared memory
+__device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *map, int32_t r0, int32_t r1, int32_t r2,
+                                            int32_t r3, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
 
 template <int NP>
 __global__ void __launch_bounds__(PBG_WARPS * 32, NP == 32 ? 1 : 2) k_proj_bg_mma(const double *__restrict__ U,
@@ -525,7 +544,8 @@ __global__ void __launch_bounds__(PBG_WARPS * 32, NP == 32 ? 1 : 2) k_proj_bg_mm
                                                                 const int32_t *__restrict__ item_ptr, int64_t n_items,
                                                                 double *__restrict__ bH_part,
                                                                 double *__restrict__ cH_part,
-                                                                double *__restrict__ gram_part) {
+                                                                double *__restrict__ gram_part,
+                                                                const __grid_constant__ CUtensorMap tmapU) {
   static_assert(NP == 8 || NP == 16 || NP == 32, "mma item pass: NP in {8, 16, 32}");
   constexpr int TT = NP / 8;                       // 8-wide tiles per dimension
   constexpr int NU = TT * (TT + 1) / 2;            // upper tiles per operator
@@ -557,8 +577,9 @@ __global__ void __launch_bounds__(PBG_WARPS * 32, NP == 32 ? 1 : 2) k_proj_bg_mm
     const int32_t r0 = ra + c * CH, cnt = min(CH, rb - r0);
     double *S = ring + st * STAGE;
     const unsigned bv = (unsigned)cnt * NP * 8u, bp = (unsigned)cnt * 32u;
+    const unsigned bu = (pbg_gather_u<NP>() && KS_PBG_G4) ? (unsigned)((cnt + 3) / 4) * 4u * NP * 8u : bv;
     if (lane == 0) {
-      mbar_expect_tx(&bars[warp][st], 3 * bv + bp);
+      mbar_expect_tx(&bars[warp][st], bu + 2 * bv + bp);
       if constexpr (!pbg_gather_u<NP>()) bulk_g2s(S, U + (int64_t)r0 * NP, bv, &bars[warp][st]);
       bulk_g2s(S + CH * NP, YHp + (int64_t)r0 * NP, bv, &bars[warp][st]);
       bulk_g2s(S + 2 * CH * NP, YMp + (int64_t)r0 * NP, bv, &bars[warp][st]);
@@ -566,7 +587,16 @@ __global__ void __launch_bounds__(PBG_WARPS * 32, NP == 32 ? 1 : 2) k_proj_bg_mm
     }
     if constexpr (pbg_gather_u<NP>()) {
       __syncwarp();
+#if KS_PBG_G4
+      if (lane < (cnt + 3) / 4) {   // rows past cnt repeat the last valid row (masked in the fragments)
+        int32_t rr[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) rr[q] = __ldg(perm + r0 + min(4 * lane + q, cnt - 1));
+        tma_gather4(S + 4 * lane * NP, &tmapU, rr[0], rr[1], rr[2], rr[3], &bars[warp][st]);
+      }
+#else
       if (lane < cnt) bulk_g2s(S + lane * NP, U + (int64_t)__ldg(perm + r0 + lane) * NP, NP * 8u, &bars[warp][st]);
+#endif
     }
   };
   if (lane == 0) {
@@ -901,6 +931,26 @@ bool proj_mma_enabled() {
   return on;
 }
 
+// tensor map of a row-major [n][np] f64 block for TMA row gathers: box = one full row (gather4 takes 4)
+ks_status make_row_map(ks_ctx *ctx, const double *base, int64_t n, int np, CUtensorMap *map) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return ks_fail(ctx, KS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)np, (cuuint64_t)n};
+  const cuuint64_t strides[1] = {(cuuint64_t)np * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)np, 1u}, estr[2] = {1u, 1u};
+  if (encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return ks_fail(ctx, KS_E_CUDA, "cuTensorMapEncodeTiled failed (n = %lld, np = %d)", (long long)n, np);
+  return KS_OK;
+}
+
 template <int NP>
 ks_status launch_proj_yb(ks_ctx *ctx, int N, const double *u, double *FA, double *FB, int64_t D) {
   cudaStream_t s = ctx->stream;
@@ -927,9 +977,13 @@ ks_status launch_proj_yb(ks_ctx *ctx, int N, const double *u, double *FA, double
   if constexpr (NP == 8 || NP == 16 || NP == 32) {
     if (mma) {
       KS_CUDA(ctx, cudaFuncSetAttribute(k_proj_bg_mma<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+      CUtensorMap tmapU;
+      memset(&tmapU, 0, sizeof(tmapU));
+      if (gather_u && KS_PBG_G4) KS_TRY(make_row_map(ctx, u, n, NP, &tmapU));
       k_proj_bg_mma<NP><<<grid, PBG_WARPS * 32, bsm, s>>>(gather_u ? u : ctx->proj_up, ctx->perm, ctx->Y_H, ctx->Y_M,
                                                           ctx->Pv4p, ctx->item_ptr,
-                                                          ctx->n_items, ctx->bH_part, ctx->cH_part, ctx->gram_part);
+                                                          ctx->n_items, ctx->bH_part, ctx->cH_part, ctx->gram_part,
+                                                          tmapU);
     } else {
       KS_CUDA(ctx, cudaFuncSetAttribute(k_proj_bg<NP, GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
       k_proj_bg<NP, GRAM><<<grid, PBG_WARPS * 32, bsm, s>>>(ctx->proj_up, ctx->Y_H, ctx->Y_M, ctx->Pv4p,
