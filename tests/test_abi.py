@@ -70,3 +70,20 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "oracle.c" not in txt, f
+
+
+def c_consumer_build(out):
+    """Compile tests/c_abi/c_consumer.c (strict C99, -Werror) against include/ks.h and link it with libks.so
+    and the CUDA runtime: the ABI is usable from plain C, without Python or torch."""
+    lib_dir = os.path.join(ROOT, "paper_2404_19249_b200")
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    cmd = ["gcc", "-std=c99", "-Wall", "-Wextra", "-Werror", "-I" + os.path.join(ROOT, "include"),
+           "-I" + os.path.join(cuda, "include"), os.path.join(ROOT, "tests", "c_abi", "c_consumer.c"), "-o", out,
+           "-L" + lib_dir, "-lks", "-L" + os.path.join(cuda, "lib64"), "-lcudart", "-Wl,-rpath," + lib_dir,
+           "-Wl,-rpath," + os.path.join(cuda, "lib64"), "-lm"]
+    return subprocess.run(cmd, capture_output=True, text=True)
+
+
+def test_c_consumer_compiles_and_links(lib, tmp_path):
+    r = c_consumer_build(str(tmp_path / "c_consumer"))
+    assert r.returncode == 0, r.stderr
