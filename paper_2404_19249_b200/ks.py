@@ -253,7 +253,9 @@ class Context:
         return FA, FB
 
     def pencil_eig(self, FA, FB, k: int):
-        """ks_pencil_eig: lowest k eigenpairs of F_A y = lambda F_B y -> (evals [k], evecs [D][k])."""
+        """ks_pencil_eig: lowest k eigenpairs of F_A y = lambda F_B y -> (evals [k], evecs [D][k]), evecs
+        F_B-orthonormal. Chebyshev-filtered subspace iteration after the Cholesky reduction when k + 8 <= D / 2,
+        dense cuSOLVER otherwise or with KS_PENCIL_DENSE=1 (include/ks.h)."""
         import torch
         D = FA.shape[0]
         _check_cuda_tensor(FA, torch.float64, (D, D), "FA")
@@ -325,7 +327,9 @@ class Context:
         return vxc, eps
 
     def hartree(self, rho, tol=1e-12, max_iter=100000, vh=None, warm=False):
-        """ks_hartree: Hartree potential on all nodes -> (vh, moments [10] numpy, PCG iterations)."""
+        """ks_hartree: Hartree potential on all nodes -> (vh, moments [10] numpy, PCG iterations). With a coarse
+        space set (set_coarse) the solve is the two-level preconditioned CG (Jacobi + P (P^T K P)^-1 P^T),
+        else (or with KS_HARTREE_2L=0) Jacobi-PCG (include/ks.h)."""
         import torch
         _check_cuda_tensor(rho, torch.float64, (self.n_nodes,), "rho")
         if vh is None:
