@@ -163,10 +163,11 @@ def traced_phases(ctx, solve, n, nnz, N, peak):
     return out
 
 
-def next1_times(ctx, Ut, FA, FB, N, stream):
+def next1_times(ctx, Ut, FA, FB, N, stream, p_lam=None, U0=None):
     """NEXT-1 (not part of the timed step): the pencil eigensolve of the step's F_A, F_B (D = n_H + N; the
     Chebyshev-filtered subspace iteration, dense cuSOLVER with KS_PENCIL_DENSE=1) and the lift
-    U_new = P y_H + U~ y_t, each timed with CUDA events after one warm-up call."""
+    U_new = P y_H + U~ y_t, each timed with CUDA events after one warm-up call; and one whole outer iteration
+    of the linear Algorithm 3 (ks_augmented_solve) from the step's inputs."""
     import torch
     try:
         out = {}
@@ -180,6 +181,17 @@ def next1_times(ctx, Ut, FA, FB, N, stream):
             torch.cuda.synchronize()
             out[name] = a.elapsed_time(b)
         out["D"] = int(FA.shape[0])
+        # one outer iteration of the linear Algorithm 3 (block solve -> projection -> pencil eigensolve ->
+        # lift, ks_augmented_solve with tol_eig = inf: it stops after the first iteration), on copies
+        lam0 = torch.from_numpy(np.asarray(p_lam)).to(FA.device)
+        for rep in range(2):
+            lam_c, U_c = lam0.clone(), U0.clone()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ctx.augmented_solve(lam_c, U_c, tol_eig=float("inf"), max_outer=1, tol_bvp=TOL, max_iter_bvp=MAX_ITER)
+            b.record(stream)
+            torch.cuda.synchronize()
+        out["outer_iteration"] = a.elapsed_time(b)
         return out
     except Exception as ex:  # reported, never fatal for the headline line
         return {"error": str(ex)[:200]}
@@ -471,7 +483,7 @@ def run_ours(args, p, rank, world, local):
                      "alg_bytes_def": "init (20 nnz + 12 n + 32 N n) + k x textbook B_it (12 nnz + 20 n + 88 N n)"},
         "phases_ms": {"assemble_veff": t_asm, "block_solve": t_solve, "project_augmented": t_proj},
         "solve_only_value": N * n * k_last / (t_solve * 1e-3),
-        "next1_ms": next1_times(ctx, Ut, FA, FB, N, stream),
+        "next1_ms": next1_times(ctx, Ut, FA, FB, N, stream, p.lam, U),
         "next23": next_rows(ctx, p, U, stream, peak),
         "pcg_phases": traced_phases(ctx, lambda: ctx.block_solve(lam, U, Ut, tol=TOL, max_iter=MAX_ITER, iters=iters,
                                                                  relres=relres), n, nnz, N, peak),
