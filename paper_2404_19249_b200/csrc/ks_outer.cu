@@ -328,10 +328,10 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
     KS_TRY(ks_alloc_t(ctx, &ctx->ef_buf, 4 * D * m, "filtered eig blocks"));
     ctx->ef_cap = 4 * D * m;
   }
-  if (ctx->ef_small_cap < (int64_t)m * m + m + 1) {
+  if (ctx->ef_small_cap < 2 * (int64_t)m * m + m + 1) {   // two m x m Grams, then V and lambda
     ks_free_t(ctx, ctx->ef_small);
-    KS_TRY(ks_alloc_t(ctx, &ctx->ef_small, (int64_t)m * m + m + 1, "filtered eig small"));
-    ctx->ef_small_cap = (int64_t)m * m + m + 1;
+    KS_TRY(ks_alloc_t(ctx, &ctx->ef_small, 2 * (int64_t)m * m + m + 1, "filtered eig small"));
+    ctx->ef_small_cap = 2 * (int64_t)m * m + m + 1;
   }
   double *X = ctx->ef_buf, *CX = X + D * m, *T1 = CX + D * m, *T2 = T1 + D * m, *sm = ctx->ef_small;
   // start block: Y0 in T1, X = L^T Y0
@@ -367,86 +367,81 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
   std::vector<double> G((size_t)m * m), w, V, Tm, lam(m), res(k);
   int maxit = EF_MAXIT;   // KS_PENCIL_EF_MAXIT: test hook to exercise the dense fallback
   if (const char *e = getenv("KS_PENCIL_EF_MAXIT")) maxit = atoi(e);
-  for (int it = 0; it < maxit; it++) {
-    // orthonormalise X into T1: CholQR2 (two passes of G = X^T X = R^T R, X <- X R^-1, on the column-scaled
-    // Gram), SVQB (eigen-decomposition of the Gram) when a Cholesky pivot collapses
-    {
-      const double *src = X;
-      bool ok = true;
-      for (int pass = 0; pass < 2 && ok; pass++) {
-        KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, (int)D, &one, src, (int)D, src, (int)D, &zero, sm,
-                                 m));
-        KS_CUDA(ctx, cudaMemcpyAsync(G.data(), sm, sizeof(double) * m * m, cudaMemcpyDeviceToHost, st));
-        KS_CUDA(ctx, cudaStreamSynchronize(st));
-        std::vector<double> dsc(m);
-        for (int j = 0; j < m; j++) dsc[j] = std::sqrt(G[(size_t)j * m + j]);
-        if (!(dsc[0] > 0.0)) return KS_OK;
-        for (int j = 0; j < m; j++)
-          for (int i = 0; i < m; i++) G[(size_t)j * m + i] /= dsc[i] * dsc[j];
-        // Cholesky G = R^T R (upper R, column-major), then Tm = D^-1 R^-1
-        std::vector<double> R((size_t)m * m, 0.0);
-        for (int j = 0; j < m && ok; j++) {
-          for (int i = 0; i <= j; i++) {
-            double v = G[(size_t)j * m + i];
-            for (int l = 0; l < i; l++) v -= R[(size_t)i * m + l] * R[(size_t)j * m + l];
-            if (i == j) {
-              if (!(v > 1e-12)) { ok = false; break; }
-              R[(size_t)j * m + j] = std::sqrt(v);
-            } else {
-              R[(size_t)j * m + i] = v / R[(size_t)i * m + i];
-            }
-          }
+  // host: Cholesky of the column-scaled Gram G = D R^T R D (upper R, column-major); false on a collapsed pivot
+  auto host_chol = [&](const std::vector<double> &Gm, std::vector<double> &dsc, std::vector<double> &Rinv) -> bool {
+    dsc.resize(m);
+    for (int j = 0; j < m; j++) dsc[j] = std::sqrt(Gm[(size_t)j * m + j]);
+    if (!(dsc[0] > 0.0)) return false;
+    std::vector<double> R((size_t)m * m, 0.0);
+    for (int j = 0; j < m; j++)
+      for (int i = 0; i <= j; i++) {
+        double v = Gm[(size_t)j * m + i] / (dsc[i] * dsc[j]);
+        for (int l = 0; l < i; l++) v -= R[(size_t)i * m + l] * R[(size_t)j * m + l];
+        if (i == j) {
+          if (!(v > 1e-12)) return false;
+          R[(size_t)j * m + j] = std::sqrt(v);
+        } else {
+          R[(size_t)j * m + i] = v / R[(size_t)i * m + i];
         }
-        if (!ok) break;
-        Tm.assign((size_t)m * m, 0.0);   // R^-1 (upper), by columns
-        for (int j = 0; j < m; j++) {
-          Tm[(size_t)j * m + j] = 1.0 / R[(size_t)j * m + j];
-          for (int i = j - 1; i >= 0; i--) {
-            double v = 0.0;
-            for (int l = i + 1; l <= j; l++) v += R[(size_t)l * m + i] * Tm[(size_t)j * m + l];
-            Tm[(size_t)j * m + i] = -v / R[(size_t)i * m + i];
-          }
-        }
-        for (int j = 0; j < m; j++)
-          for (int i = 0; i < m; i++) Tm[(size_t)j * m + i] /= dsc[i];
-        KS_CUDA(ctx, cudaMemcpyAsync(sm, Tm.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice, st));
-        double *dst = pass == 0 ? T2 : T1;
-        KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, m, &one, src, (int)D, sm, m, &zero, dst,
-                                 (int)D));
-        src = dst;
       }
-      if (!ok) {   // SVQB of X (rank loss -> dense path)
-        KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, (int)D, &one, X, (int)D, X, (int)D, &zero, sm, m));
-        KS_CUDA(ctx, cudaMemcpyAsync(G.data(), sm, sizeof(double) * m * m, cudaMemcpyDeviceToHost, st));
-        KS_CUDA(ctx, cudaStreamSynchronize(st));
-        std::vector<double> dsc(m);
-        for (int j = 0; j < m; j++) dsc[j] = std::sqrt(G[(size_t)j * m + j]);
-        for (int j = 0; j < m; j++)
-          for (int i = 0; i < m; i++) G[(size_t)j * m + i] /= dsc[i] * dsc[j];
-        host_jacobi_eig(G, m, w, V);
-        if (!(w[0] > 1e-13 * w[m - 1])) return KS_OK;
-        Tm.assign((size_t)m * m, 0.0);
-        for (int j = 0; j < m; j++)
-          for (int i = 0; i < m; i++) Tm[(size_t)j * m + i] = V[(size_t)j * m + i] / (dsc[i] * std::sqrt(w[j]));
-        KS_CUDA(ctx, cudaMemcpyAsync(sm, Tm.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice, st));
-        KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, m, &one, X, (int)D, sm, m, &zero, T1,
-                                 (int)D));
+    Rinv.assign((size_t)m * m, 0.0);   // R^-1 (upper), by columns
+    for (int j = 0; j < m; j++) {
+      Rinv[(size_t)j * m + j] = 1.0 / R[(size_t)j * m + j];
+      for (int i = j - 1; i >= 0; i--) {
+        double v = 0.0;
+        for (int l = i + 1; l <= j; l++) v += R[(size_t)l * m + i] * Rinv[(size_t)j * m + l];
+        Rinv[(size_t)j * m + i] = -v / R[(size_t)i * m + i];
       }
     }
-    // Rayleigh-Ritz: H = X^T C X
-    KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, (int)D, &one, A, (int)D, T1, (int)D, &zero, T2,
+    return true;
+  };
+  std::vector<double> G2((size_t)m * m), dsc, Rinv, Hs((size_t)m * m);
+  for (int it = 0; it < maxit; it++) {
+    // Rayleigh-Ritz on span(X) with the orthonormalisation folded in: T2 = C X, G = X^T X and H = X^T C X in
+    // one round trip; on the host the small pencil (H, G) is reduced by the Cholesky factor of the scaled G
+    // and diagonalised by Jacobi: V = D^-1 R^-1 W, X <- X V (orthonormal), CX <- (C X) V
+    KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, (int)D, &one, A, (int)D, X, (int)D, &zero, T2,
                              (int)D));
-    KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, (int)D, &one, T1, (int)D, T2, (int)D, &zero, sm, m));
+    KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, (int)D, &one, X, (int)D, X, (int)D, &zero, sm, m));
+    KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, (int)D, &one, X, (int)D, T2, (int)D, &zero,
+                             sm + (int64_t)m * m, m));
     KS_CUDA(ctx, cudaMemcpyAsync(G.data(), sm, sizeof(double) * m * m, cudaMemcpyDeviceToHost, st));
+    KS_CUDA(ctx, cudaMemcpyAsync(G2.data(), sm + (int64_t)m * m, sizeof(double) * m * m, cudaMemcpyDeviceToHost, st));
     KS_CUDA(ctx, cudaStreamSynchronize(st));
+    if (!host_chol(G, dsc, Rinv)) return KS_OK;   // the block lost rank: dense path
+    // Hs = R^-T (D^-1 H D^-1) R^-1
     for (int j = 0; j < m; j++)
-      for (int i = 0; i < j; i++) G[(size_t)j * m + i] = G[(size_t)i * m + j] = 0.5 * (G[(size_t)j * m + i] + G[(size_t)i * m + j]);
-    host_jacobi_eig(G, m, w, V);
+      for (int i = 0; i < m; i++) G2[(size_t)j * m + i] /= dsc[i] * dsc[j];
+    {
+      std::vector<double> HR((size_t)m * m, 0.0);   // (D^-1 H D^-1) R^-1
+      for (int j = 0; j < m; j++)
+        for (int l = 0; l <= j; l++) {
+          const double r = Rinv[(size_t)j * m + l];
+          for (int i = 0; i < m; i++) HR[(size_t)j * m + i] += G2[(size_t)l * m + i] * r;
+        }
+      for (int j = 0; j < m; j++)
+        for (int i = 0; i < m; i++) {
+          double v = 0.0;
+          for (int l = 0; l <= i; l++) v += Rinv[(size_t)i * m + l] * HR[(size_t)j * m + l];
+          Hs[(size_t)j * m + i] = v;
+        }
+      for (int j = 0; j < m; j++)
+        for (int i = 0; i < j; i++) Hs[(size_t)j * m + i] = Hs[(size_t)i * m + j] = 0.5 * (Hs[(size_t)j * m + i] + Hs[(size_t)i * m + j]);
+    }
+    host_jacobi_eig(Hs, m, w, V);
     lam = w;
-    KS_CUDA(ctx, cudaMemcpyAsync(sm, V.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice, st));
+    Tm.assign((size_t)m * m, 0.0);   // D^-1 R^-1 W
+    for (int j = 0; j < m; j++)
+      for (int i = 0; i < m; i++) {
+        double v = 0.0;
+        for (int l = i; l < m; l++) v += Rinv[(size_t)l * m + i] * V[(size_t)j * m + l];
+        Tm[(size_t)j * m + i] = v / dsc[i];
+      }
+    KS_CUDA(ctx, cudaMemcpyAsync(sm, Tm.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice, st));
     KS_CUDA(ctx, cudaMemcpyAsync(sm + (int64_t)m * m, lam.data(), sizeof(double) * m, cudaMemcpyHostToDevice, st));
-    KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, m, &one, T1, (int)D, sm, m, &zero, X, (int)D));
+    KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, m, &one, X, (int)D, sm, m, &zero, T1, (int)D));
     KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, m, &one, T2, (int)D, sm, m, &zero, CX, (int)D));
+    std::swap(X, T1);
     // wanted residuals
     k_resid<<<k, 32, 0, st>>>(CX, X, sm + (int64_t)m * m, D, k, T2);
     KS_LAUNCHED(ctx);
@@ -456,11 +451,20 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
     for (int j = 0; j < k; j++) rmax = std::fmax(rmax, std::sqrt(res[j]));
     if (!std::isfinite(rmax)) return KS_OK;
     if (rmax <= tol * bound) {
-      // y = L^-T x for the wanted block, evals
+      // one more Cholesky-QR pass (X V is orthonormal only up to cond(X)^2 eps), then y = L^-T x, evals
+      KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, (int)D, &one, X, (int)D, X, (int)D, &zero, sm, m));
+      KS_CUDA(ctx, cudaMemcpyAsync(G.data(), sm, sizeof(double) * m * m, cudaMemcpyDeviceToHost, st));
+      KS_CUDA(ctx, cudaStreamSynchronize(st));
+      if (!host_chol(G, dsc, Rinv)) return KS_OK;
+      for (int j = 0; j < m; j++)
+        for (int i = 0; i < m; i++) Tm[(size_t)j * m + i] = Rinv[(size_t)j * m + i] / dsc[i];
+      KS_CUDA(ctx, cudaMemcpyAsync(sm, Tm.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice, st));
+      KS_CUDA(ctx, cudaMemcpyAsync(sm + (int64_t)m * m, lam.data(), sizeof(double) * m, cudaMemcpyHostToDevice, st));
+      KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, m, &one, X, (int)D, sm, m, &zero, T1, (int)D));
       KS_BLAS(ctx, cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)D, k,
-                               &one, L, (int)D, X, (int)D));
+                               &one, L, (int)D, T1, (int)D));
       KS_CUDA(ctx, cudaMemcpyAsync(evals, sm + (int64_t)m * m, sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
-      k_take_evecs<<<ks_blocks(D * k, 256), 256, 0, st>>>(X, D, k, evecs);
+      k_take_evecs<<<ks_blocks(D * k, 256), 256, 0, st>>>(T1, D, k, evecs);
       KS_LAUNCHED(ctx);
       *done = true;
       return KS_OK;
