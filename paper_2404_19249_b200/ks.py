@@ -105,6 +105,22 @@ def _check_cuda_tensor(t, dtype, shape=None, name="tensor"):
     return t
 
 
+def _n_cols(t) -> int:
+    if t.dim() != 2:
+        raise ValueError(f"expected a 2-D [rows][N] block, got shape {tuple(t.shape)}")
+    return int(t.shape[1])
+
+
+def _check_host_tensor(t, dtype, shape, name):
+    import torch
+    if not isinstance(t, torch.Tensor) or t.is_cuda:
+        raise TypeError(f"{name} must be a host (CPU) torch.Tensor")
+    if t.dtype != dtype or not t.is_contiguous() or tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must be a contiguous {dtype} tensor of shape {tuple(shape)}, "
+                         f"got {t.dtype} {tuple(t.shape)}")
+    return t
+
+
 class Context:
     """ks_create .. ks_destroy. Host mesh arrays are numpy; everything else lives in torch CUDA tensors."""
 
@@ -192,17 +208,19 @@ class Context:
 
     def spmm(self, op: str, X, Y=None):
         import torch
-        _check_cuda_tensor(X, torch.float64, None, "X")
         N = X.shape[1] if X.dim() == 2 else 1
+        shape = (self.n_free, N) if X.dim() == 2 else (self.n_free,)
+        _check_cuda_tensor(X, torch.float64, shape, "X")
         if Y is None:
             Y = torch.empty_like(X)
+        _check_cuda_tensor(Y, torch.float64, shape, "Y")
         self._call(self._L.ks_spmm(self._h, OPS[op], N, _ptr(X), _ptr(Y)))
         return Y
 
     def block_solve(self, lam, U, Ut=None, tol=1e-10, max_iter=2000, iters=None, relres=None):
         import torch
-        _check_cuda_tensor(U, torch.float64, None, "U")
-        N = U.shape[1]
+        N = _n_cols(U)
+        _check_cuda_tensor(U, torch.float64, (self.n_free, N), "U")
         _check_cuda_tensor(lam, torch.float64, (N,), "lambda")
         if Ut is None:
             Ut = torch.empty_like(U)
@@ -210,6 +228,9 @@ class Context:
             iters = torch.zeros(N, dtype=torch.int32, device=U.device)
         if relres is None:
             relres = torch.zeros(N, dtype=torch.float64, device=U.device)
+        _check_cuda_tensor(Ut, torch.float64, (self.n_free, N), "Ut")
+        _check_cuda_tensor(iters, torch.int32, (N,), "iters")
+        _check_cuda_tensor(relres, torch.float64, (N,), "relres")
         self._call(self._L.ks_block_solve(self._h, N, _ptr(lam), _ptr(U), _ptr(Ut), float(tol), int(max_iter),
                                           _ptr(iters), _ptr(relres)))
         return Ut, iters, relres
@@ -228,7 +249,10 @@ class Context:
 
     def true_residual(self, lam, U, Ut):
         import torch
-        N = U.shape[1]
+        N = _n_cols(U)
+        _check_cuda_tensor(lam, torch.float64, (N,), "lambda")
+        _check_cuda_tensor(U, torch.float64, (self.n_free, N), "U")
+        _check_cuda_tensor(Ut, torch.float64, (self.n_free, N), "Ut")
         out = torch.empty(N, dtype=torch.float64, device=U.device)
         self._call(self._L.ks_true_residual(self._h, N, _ptr(lam), _ptr(U), _ptr(Ut), _ptr(out)))
         return out
@@ -237,18 +261,25 @@ class Context:
         import torch
         _check_cuda_tensor(P_rowptr, torch.int32, (self.n_free + 1,), "P_rowptr")
         _check_cuda_tensor(P_col, torch.int32, None, "P_col")
-        _check_cuda_tensor(P_val, torch.float64, None, "P_val")
+        _check_cuda_tensor(P_val, torch.float64, tuple(P_col.shape), "P_val")
+        if P_col.dim() != 1:
+            raise ValueError("P_col must be 1-D")
         self._call(self._L.ks_set_coarse(self._h, int(n_H), _ptr(P_rowptr), _ptr(P_col), _ptr(P_val)))
         self.n_H = int(n_H)
 
     def project_augmented(self, Ut, FA=None, FB=None):
         import torch
-        N = Ut.shape[1]
+        if self.n_H is None:
+            raise KSError(KS_E_STATE, "project_augmented: call set_coarse first")
+        N = _n_cols(Ut)
+        _check_cuda_tensor(Ut, torch.float64, (self.n_free, N), "Ut")
         D = self.n_H + N
         if FA is None:
             FA = torch.empty((D, D), dtype=torch.float64, device=Ut.device)
         if FB is None:
             FB = torch.empty((D, D), dtype=torch.float64, device=Ut.device)
+        _check_cuda_tensor(FA, torch.float64, (D, D), "FA")
+        _check_cuda_tensor(FB, torch.float64, (D, D), "FB")
         self._call(self._L.ks_project_augmented(self._h, N, _ptr(Ut), _ptr(FA), _ptr(FB)))
         return FA, FB
 
@@ -268,11 +299,14 @@ class Context:
     def lift(self, Ut, Y, Unew=None):
         """ks_lift: U_new = P Y[:n_H] + U~ Y[n_H:]."""
         import torch
-        _check_cuda_tensor(Ut, torch.float64, None, "Ut")
-        _check_cuda_tensor(Y, torch.float64, None, "Y")
-        N, k = Ut.shape[1], Y.shape[1]
+        if self.n_H is None:
+            raise KSError(KS_E_STATE, "lift: call set_coarse first")
+        N, k = _n_cols(Ut), _n_cols(Y)
+        _check_cuda_tensor(Ut, torch.float64, (self.n_free, N), "Ut")
+        _check_cuda_tensor(Y, torch.float64, (self.n_H + N, k), "Y")
         if Unew is None:
             Unew = torch.empty((self.n_free, k), dtype=torch.float64, device=Ut.device)
+        _check_cuda_tensor(Unew, torch.float64, (self.n_free, k), "Unew")
         self._call(self._L.ks_lift(self._h, N, _ptr(Ut), int(k), _ptr(Y), _ptr(Unew)))
         return Unew
 
@@ -280,9 +314,9 @@ class Context:
         """ks_augmented_solve: outer iterations of Algorithm 3 with the current operators; lam and U are
         updated in place. Returns (outer iterations, Ritz-value history [outer][N] as numpy)."""
         import torch
-        _check_cuda_tensor(U, torch.float64, None, "U")
-        _check_cuda_tensor(lam, torch.float64, None, "lam")
-        N = U.shape[1]
+        N = _n_cols(U)
+        _check_cuda_tensor(U, torch.float64, (self.n_free, N), "U")
+        _check_cuda_tensor(lam, torch.float64, (N,), "lam")
         hist = np.zeros((max_outer, N))
         outer = C.c_int32()
         self._call(self._L.ks_augmented_solve(self._h, N, _ptr(lam), _ptr(U), float(tol_eig), int(max_outer),
@@ -309,9 +343,10 @@ class Context:
     def density(self, U, f=2.0, rho=None):
         """ks_density: nodal density on all nodes."""
         import torch
-        _check_cuda_tensor(U, torch.float64, None, "U")
+        _check_cuda_tensor(U, torch.float64, (self.n_free, _n_cols(U)), "U")
         if rho is None:
             rho = torch.empty(self.n_nodes, dtype=torch.float64, device=U.device)
+        _check_cuda_tensor(rho, torch.float64, (self.n_nodes,), "rho")
         self._call(self._L.ks_density(self._h, U.shape[1], _ptr(U), float(f), _ptr(rho)))
         return rho
 
@@ -323,6 +358,8 @@ class Context:
             vxc = torch.empty_like(rho)
         if eps is None:
             eps = torch.empty_like(rho)
+        _check_cuda_tensor(vxc, torch.float64, (self.n_nodes,), "vxc")
+        _check_cuda_tensor(eps, torch.float64, (self.n_nodes,), "eps")
         self._call(self._L.ks_vxc(self._h, _ptr(rho), _ptr(vxc), _ptr(eps)))
         return vxc, eps
 
@@ -334,6 +371,7 @@ class Context:
         _check_cuda_tensor(rho, torch.float64, (self.n_nodes,), "rho")
         if vh is None:
             vh = torch.zeros_like(rho)
+        _check_cuda_tensor(vh, torch.float64, (self.n_nodes,), "vh")
         mom = np.zeros(10)
         it = C.c_int32()
         self._call(self._L.ks_hartree(self._h, _ptr(rho), float(tol), int(max_iter), _ptr(vh), int(bool(warm)),
@@ -347,7 +385,9 @@ class Context:
         unless allow_unconverged."""
         import torch
         _check_cuda_tensor(vext, torch.float64, (self.n_nodes,), "vext")
-        N = U.shape[1]
+        N = _n_cols(U)
+        _check_cuda_tensor(U, torch.float64, (self.n_free, N), "U")
+        _check_cuda_tensor(lam, torch.float64, (N,), "lam")
         outer = C.c_int32()
         inner_steps = np.zeros(max_outer, np.int32)
         dres = np.zeros(max_outer)
@@ -363,7 +403,13 @@ class Context:
 
     def step_submit(self, V_host, mu, lam_host, U_host, FA_host, FB_host, tol=1e-10, max_iter=2000):
         """ks_step_submit: one pipelined hot-path step from host buffers (pinned torch CPU tensors)."""
-        N = U_host.shape[1]
+        import torch
+        N = _n_cols(U_host)
+        D = (self.n_H or 0) + N
+        for t, shape, name in ((V_host, (self.n_nodes,), "V_host"), (lam_host, (N,), "lam_host"),
+                               (U_host, (self.n_free, N), "U_host"), (FA_host, (D, D), "FA_host"),
+                               (FB_host, (D, D), "FB_host")):
+            _check_host_tensor(t, torch.float64, shape, name)
         self._call(self._L.ks_step_submit(self._h, N, V_host.data_ptr(), float(mu), lam_host.data_ptr(),
                                           U_host.data_ptr(), float(tol), int(max_iter), FA_host.data_ptr(),
                                           FB_host.data_ptr()))

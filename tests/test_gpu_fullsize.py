@@ -4,21 +4,22 @@
   - the block solve of all 32 columns on the GPU; the TRUE relative residual of every column
     (a property that holds at any size) and two sampled columns solved by the oracle one by one
     (M-norm difference <= 1e-8, iterations within +-2);
-  - the projection of the GPU's U~ by both sides (Frobenius-relative <= 1e-9 per block).
+  - the projection of the GPU's U~ by both sides, every entry within 1e-9 (|W|^T |Op| |W|)_ij
+    (tests/fbounds.py), and the lowest N pencil eigenvalues (GPU eigensolver on the GPU's F against
+    LAPACK on the oracle's F) within 1e-9 max|lambda|.
 The oracle's share is ~3 minutes of one CPU core; the test is marked slow."""
 import numpy as np
 import pytest
 
+import scipy.linalg as sl
+
 import gen
 import oracle
+from fbounds import assert_entrywise, projection_bounds
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 torch = pytest.importorskip("torch")
-
-
-def _blocks(F, nH):
-    return {"coarse": F[:nH, :nH], "cross": F[:nH, nH:], "orbital": F[nH:, nH:]}
 
 
 def test_config5_sampled_parity():
@@ -34,7 +35,9 @@ def test_config5_sampled_parity():
     Ut, iters, relres = ctx.block_solve(lam, U, tol=1e-10, max_iter=2000)
     true_rel = ctx.true_residual(lam, U, Ut)
     FA, FB = ctx.project_augmented(Ut)
+    ev, _ = ctx.pencil_eig(FA, FB, p.N)
     assert ctx.sync() == 0, ctx.last_error()
+    ev = ev.cpu().numpy()
     A_gpu = ctx.values()["A"].cpu().numpy()
     ut = Ut.cpu().numpy()
     it = iters.cpu().numpy()
@@ -71,7 +74,8 @@ def test_config5_sampled_parity():
 
     # projection of the same U~ by both sides
     FAo, FBo = om.project(p.n_H, p.P_rowptr, p.P_col, p.P_val, ut)
-    for F, Fo in ((FA, FAo), (FB, FBo)):
-        for name, blk in _blocks(F, p.n_H).items():
-            ref_b = _blocks(Fo, p.n_H)[name]
-            assert np.linalg.norm(blk - ref_b) <= 1e-9 * np.linalg.norm(ref_b), name
+    bA, bB = projection_bounds(om, p.n_H, p.P_rowptr, p.P_col, p.P_val, ut)
+    assert_entrywise(FA, FAo, bA, what="F_A")
+    assert_entrywise(FB, FBo, bB, what="F_B")
+    wo = sl.eigh(FAo, FBo, eigvals_only=True, subset_by_index=[0, p.N - 1])
+    assert np.all(np.abs(ev - wo) <= 1e-9 * np.abs(wo).max()), (ev, wo)

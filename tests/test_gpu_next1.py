@@ -28,8 +28,10 @@ def _ctx(p, mu):
     return ctx
 
 
-@pytest.mark.parametrize("c", [2, 3])
+@pytest.mark.parametrize("c", [2, 3, pytest.param(4, marks=pytest.mark.slow)])
 def test_pencil_eig_matches_oracle(c):
+    """C4 (D = 745) is the pencil bench.py times after the step (next1_ms); C5 (D = 1363) is checked in
+    tests/test_gpu_fullsize.py."""
     p = gen.make_problem(c)
     ctx = _ctx(p, p.mu)
     Ut, _, _ = ctx.block_solve(dt(p.lam), dt(p.U))

@@ -1,8 +1,9 @@
 """NEXT-2 on the GPU: nodal density, LDA/PZ exchange-correlation potential and the Hartree
 potential through the C ABI against the oracle (tests/test_oracle_next2.py pins it).
 Tolerances: density and V_xc |d| <= 1e-14 relative (the same pointwise formulas; libdevice vs libm
-cbrt/log differ by an ulp); Hartree moments 1e-10 relative (element sums in different orders), potential
-max |d| <= 1e-9 max |V_H| (both PCGs to 1e-12)."""
+cbrt/log differ by an ulp); Hartree moments 1e-10 x (1 + |m|): the a-priori bound of a sum of ~3e5 element
+terms in two different orders (reading R9); potential max |d| <= 1e-9 max |V_H| (both PCGs to
+1e-12); the SCF loop Ritz values 1e-9 relative, outer iteration by outer iteration."""
 import numpy as np
 import pytest
 
@@ -57,7 +58,8 @@ def test_hartree_matches_oracle(n, centre):
     assert ctx.sync() == 0
     om = oracle.Mesh.from_problem(p)
     vh_o, mom_o, it_o = om.hartree(rho, tol=1e-12)
-    # sums over ~10^5..10^6 element terms in different orders (block tree vs sequential): 1e-10 relative
+    # sums over ~10^5..10^6 element terms in different orders (block tree vs sequential): the worst-case
+    # rounding bound (n_terms - 1) u sum|terms| ~ 3.7e-11 (1 + |m|) at n = 24 (reading R9)
     assert np.all(np.abs(mom[:4] - mom_o[:4]) <= 1e-10 * (1 + np.abs(mom_o[:4])))
     assert np.all(np.abs(mom[4:] - mom_o[4:]) <= 1e-10 * (1 + np.abs(mom_o[7:]).max()))
     vg = vh.cpu().numpy()
@@ -127,3 +129,37 @@ def test_scf_solve_matches_the_oracle_loop():
     assert np.all(np.abs(out["lams"][:3] - ref["lams"][:3]) <= 1e-8 * np.abs(ref["lams"][:3]))
     assert abs(lam.cpu().numpy()[0] - ref["lam"][0]) <= 1e-8 * abs(ref["lam"][0])
     assert out["dres"][-1] <= 1e-9
+
+
+@pytest.mark.slow
+def test_scf_solve_four_orbitals_matches_the_oracle_loop():
+    """Algorithm 3 with N = 4 doubly occupied orbitals (four Z = 2 centres, no symmetry) on a graded 24^3 fine
+    mesh with an independent graded 8^3 coarse mesh: GPU (ks_scf_solve, P from ks_interpolation) against
+    oracle.scf_solve, every outer iteration's Ritz values within 1e-9 relative."""
+    nuc = [((1.1, 0.3, -0.2), 2), ((-1.2, 0.2, 0.4), 2), ((0.2, 1.3, 0.1), 2), ((0.1, -1.0, -0.9), 2)]
+    mk = lambda n: gen.make_problem(dict(L=9.0, n=n, grading=("power", 1.5), jitter=0.0, nuclei=nuc, vnoise=0.0,
+                                         N=4, orbitals="gauss", lam=("uniform", -2.0, -0.5), nc=2, seed=9))
+    p, c = mk(24), mk(8)
+    assert p.n_free >= 23 ** 3
+    ctx = _ctx(p)
+    rp, col, val, nH = ctx.interpolation(c.xyz, c.tets, c.dirichlet)
+    ctx.set_coarse(nH, rp, col, val)
+    lam, U = dt(p.lam), dt(p.U)
+    out = ctx.scf_solve(dt(p.V), lam, U, mu=4.0, tol=1e-10, max_outer=120, inner=30)
+    assert ctx.sync() == 0
+    om = oracle.Mesh.from_problem(p)
+    orp, ocol, oval, onH = oracle.interpolation(p.xyz, p.free_nodes, c.xyz, c.tets, c.dirichlet)
+    assert onH == nH
+    ref = oracle.scf_solve(om, onH, orp, ocol, oval, p.V, p.lam.copy(), p.U.copy(), mu=4.0, tol=1e-10,
+                           max_outer=120, inner=30)
+    assert abs(out["outer"] - ref["outer"]) <= 1
+    # outer iteration by outer iteration while both took the same inner steps (the same path up to rounding)
+    k = 0
+    while k < min(out["outer"], ref["outer"]) and out["inner"][k] == ref["inner"][k]:
+        k += 1
+    assert k >= 3
+    scale = np.abs(ref["lams"][:k]).max()
+    assert np.all(np.abs(out["lams"][:k] - ref["lams"][:k]) <= 1e-9 * scale)
+    # the converged Ritz values
+    assert np.all(np.abs(lam.cpu().numpy() - ref["lam"]) <= 1e-9 * np.abs(ref["lam"]).max())
+    assert out["dres"][-1] <= 1e-10

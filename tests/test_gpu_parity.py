@@ -5,7 +5,8 @@ seeded inputs. Tolerances (reading Q12, BASELINE.json north_star)
   SpMM: |delta_ij| <= 1e-12 * (|Op| |X|)_ij
   block solve: ||u~_gpu - u~_oracle||_M / ||u~_oracle||_M <= 1e-8 per column at tol 1e-10,
                iteration counts within +-2
-  projection: Frobenius-relative difference per block <= 1e-9; pencil eigenvalues within 1e-9 max|lambda|.
+  projection: every entry |dF_ij| <= 1e-9 (|W|^T |Op| |W|)_ij, W = [P | U~] (tests/fbounds.py, DESIGN.md Q12');
+              pencil eigenvalues within 1e-9 max|lambda|.
 """
 import numpy as np
 import pytest
@@ -14,6 +15,7 @@ import scipy.sparse as sp
 
 import gen
 import oracle
+from fbounds import assert_entrywise, projection_bounds
 
 pytestmark = pytest.mark.gpu
 
@@ -127,6 +129,22 @@ def test_spmm(c, N):
         assert np.all(np.abs(Y - ref) <= 1e-12 * bound + 1e-300), op
 
 
+@pytest.mark.parametrize("N", [3, 16])
+def test_spmm_A_fresh_after_each_assembly(N):
+    """spmm('A') right after assemble_veff (no earlier MV/H call) and after a re-assembly with another mu:
+    the generic CSR path (ragged N) reads the CSR view of A, which must follow the last assembly."""
+    p = small(n=6, N=N)
+    k = Case(p, assemble=False, coarse=False)
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((p.n_free, N))
+    for mu in (p.mu, 3.0 * p.mu + 1.0):
+        k.ctx.assemble_veff(dt(p.V), mu)
+        k.om.assemble_veff(p.V, mu)
+        Y = k.ctx.spmm("A", dt(X)).cpu().numpy()
+        ref = k.om.spmm("A", X)
+        assert np.all(np.abs(Y - ref) <= 1e-12 * (abs(k.om.csr("A")) @ np.abs(X)) + 1e-300), mu
+
+
 def _mnorm_rel(M, a, b):
     d = a - b
     return np.sqrt(np.einsum("ij,ij->j", d, M @ d)) / np.sqrt(np.einsum("ij,ij->j", b, M @ b))
@@ -219,10 +237,6 @@ def test_argument_errors():
         k.ctx.block_solve(dt(k.p.lam), U, max_iter=0)
 
 
-def _blocks(F, nH):
-    return {"A_H": F[:nH, :nH], "b_H": F[:nH, nH:], "b_H^T": F[nH:, :nH], "beta": F[nH:, nH:]}
-
-
 @pytest.mark.parametrize("c", [1, 2, 3])
 def test_projection_matches_oracle(c):
     k = case(c)
@@ -233,10 +247,9 @@ def test_projection_matches_oracle(c):
     assert k.ctx.sync() == 0
     FA, FB = FA.cpu().numpy(), FB.cpu().numpy()
     FAo, FBo = k.om.project(p.n_H, p.P_rowptr, p.P_col, p.P_val, Ut)
-    for F, Fo in ((FA, FAo), (FB, FBo)):
-        for name, blk in _blocks(F, p.n_H).items():
-            ref = _blocks(Fo, p.n_H)[name]
-            assert np.linalg.norm(blk - ref) <= 1e-9 * np.linalg.norm(ref), name
+    bA, bB = projection_bounds(k.om, p.n_H, p.P_rowptr, p.P_col, p.P_val, Ut)
+    assert_entrywise(FA, FAo, bA, what="F_A")
+    assert_entrywise(FB, FBo, bB, what="F_B")
     w = sl.eigh(FA, FB, eigvals_only=True)[:p.N]
     wo = sl.eigh(FAo, FBo, eigvals_only=True)[:p.N]
     assert np.all(np.abs(w - wo) <= 1e-9 * np.abs(wo).max())
@@ -252,8 +265,9 @@ def test_projection_ragged_N(N):
     Ut = rng.standard_normal((p.n_free, N))
     FA, FB = k.ctx.project_augmented(dt(Ut))
     FAo, FBo = k.om.project(p.n_H, p.P_rowptr, p.P_col, p.P_val, Ut)
-    for F, Fo in ((FA.cpu().numpy(), FAo), (FB.cpu().numpy(), FBo)):
-        assert np.linalg.norm(F - Fo) <= 1e-9 * np.linalg.norm(Fo)
+    bA, bB = projection_bounds(k.om, p.n_H, p.P_rowptr, p.P_col, p.P_val, Ut)
+    assert_entrywise(FA.cpu().numpy(), FAo, bA, what="F_A")
+    assert_entrywise(FB.cpu().numpy(), FBo, bB, what="F_B")
 
 
 def test_whole_step_deterministic():
@@ -304,10 +318,14 @@ def test_config4_full_parity():
     assert np.all(np.abs(it - ref["iters"]) <= 2)
     FA, FB = k.ctx.project_augmented(dt(ut))
     FAo, FBo = k.om.project(p.n_H, p.P_rowptr, p.P_col, p.P_val, ut)
-    for F, Fo in ((FA.cpu().numpy(), FAo), (FB.cpu().numpy(), FBo)):
-        for name, blk in _blocks(F, p.n_H).items():
-            ref_b = _blocks(Fo, p.n_H)[name]
-            assert np.linalg.norm(blk - ref_b) <= 1e-9 * np.linalg.norm(ref_b), name
+    bA, bB = projection_bounds(k.om, p.n_H, p.P_rowptr, p.P_col, p.P_val, ut)
+    assert_entrywise(FA.cpu().numpy(), FAo, bA, what="F_A")
+    assert_entrywise(FB.cpu().numpy(), FBo, bB, what="F_B")
+    # the pencil's lowest N eigenvalues: the GPU eigensolver on the GPU's F against LAPACK on the oracle's F
+    ev, _ = k.ctx.pencil_eig(FA, FB, p.N)
+    assert k.ctx.sync() == 0
+    wo = sl.eigh(FAo, FBo, eigvals_only=True, subset_by_index=[0, p.N - 1])
+    assert np.all(np.abs(ev.cpu().numpy() - wo) <= 1e-9 * np.abs(wo).max())
 
 
 @pytest.mark.parametrize("c", [3])
