@@ -131,11 +131,20 @@ def bytes_solve_init(n, nnz, N):
     return 20 * nnz + 4 * (n + 1) + 8 * n + 8 * N * n * 4
 
 
-def phase_bytes(n, nnz, N):
-    """Algorithmic bytes of the three phases of one PCG iteration as the kernel runs them (10 vector
-    touches; z = r/d is never stored): S = SpMM q = A p (matrix + row_ptr, read p, write q),
-    U = r -= alpha q (read r, q, 1/d; write r), P = x += alpha p, p = z + beta p (read r, p, x, 1/d;
-    write x, p)."""
+def fused_kernel() -> bool:
+    """The BVPs run the fused two-phase PCG kernel unless KS_PCG_FUSED=0."""
+    return os.environ.get("KS_PCG_FUSED", "1") != "0"
+
+
+def phase_bytes(n, nnz, N, fused=True):
+    """Algorithmic bytes of the phases of one PCG iteration as the kernel runs them (10 vector touches).
+    Fused (default): S = w = A z (matrix + row_ptr, gather z) with q = w + beta q, p = z + beta p,
+    x += alpha p on the same rows (read q, p, x; write q, p, x); U = z -= alpha q / d (read z, q, d, 1/d;
+    write z). Three-phase (KS_PCG_FUSED=0): S = q = A p (read p, write q), U = r -= alpha q (read r, q,
+    1/d; write r), P = x += alpha p, p = z + beta p (read r, p, x, 1/d; write x, p)."""
+    if fused:
+        return {"S": 12 * nnz + 4 * (n + 1) + 56 * N * n,
+                "U": 24 * N * n + 16 * n}
     return {"S": 12 * nnz + 4 * (n + 1) + 16 * N * n,
             "U": 24 * N * n + 8 * n,
             "P": 40 * N * n + 8 * n}
@@ -150,14 +159,23 @@ def traced_phases(ctx, solve, n, nnz, N, peak):
         ts = ctx.solve_trace()
     finally:
         os.environ.pop("KS_PCG_TRACE", None)
-    if len(ts) < 5:
+    fused = fused_kernel()
+    names = ("S", "U") if fused else ("S", "U", "P")
+    if len(ts) < 2 + 2 * len(names):
         return None
     d = np.diff(ts.astype(np.int64)) * 1e-6  # ms
-    k = (len(d) - 1) // 3
-    out = {"init_ms": float(d[0]), "iterations": int(k)}
-    pb = phase_bytes(n, nnz, N)
-    for j, name in enumerate(("S", "U", "P")):
-        ms = float(np.mean(d[1 + j::3][:k]))
+    out = {"kernel": "fused S+P, U" if fused else "S, U, P", "init_ms": float(d[0])}
+    if fused:   # [init, S0 (q = A p only), then per iteration U_k, S_{k+1}, ... ]: S0 is reported apart
+        out["S0_ms"] = float(d[1])
+        d = d[2:]
+        names = ("U", "S")
+    else:
+        d = d[1:]
+    k = len(d) // len(names)
+    out["iterations"] = int(k)
+    pb = phase_bytes(n, nnz, N, fused)
+    for j, name in enumerate(names):
+        ms = float(np.mean(d[j::len(names)][:k]))
         gbs = pb[name] / (ms * 1e-3) / 1e9
         out[name] = {"ms": ms, "alg_bytes": int(pb[name]), "GB/s": gbs, "frac": gbs / peak}
     return out
@@ -363,7 +381,7 @@ def run_ours(args, p, rank, world, local):
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
-    ctx = ks.Context(p.xyz, p.tets, p.dirichlet, stream=stream)
+    ctx = ks.Context(p.xyz, p.tets, p.dirichlet, stream=stream, max_N=p.N)
     V = torch.from_numpy(p.V).to(dev)
     lam = torch.from_numpy(p.lam).to(dev)
     U = torch.from_numpy(p.U).to(dev)

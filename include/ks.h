@@ -21,9 +21,19 @@
  *   - Pointers named d_* are DEVICE pointers on the context's device; h_* are HOST pointers. The caller
  *     owns every pointer it passes; the library never frees them and never keeps host pointers past the
  *     call. Device inputs/outputs must stay valid until the stream work that uses them completes.
- *   - Internal structures (pattern, maps, values, solver workspace) are allocated by the library with
- *     cudaMalloc on the context's device in ks_create / ks_set_coarse / on first use of a block size N,
- *     and freed by ks_destroy. ks_memory_bytes reports the total.
+ *   - Memory: the caller owns ALL device memory. libks never allocates or frees device memory (no cudaMalloc,
+ *     cudaMallocAsync or cudaFree anywhere in the library); it carves every buffer it uses out of regions
+ *     the caller allocates from the sizes the plan calls return:
+ *       ks_plan(mesh, max_N)          -> persistent, workspace, setup bytes      -> ks_create
+ *       ks_coarse_plan(ctx, n_H, P)   -> coarse bytes                            -> ks_set_coarse
+ *       ks_ext_plan(ctx, features, .) -> extension bytes (NEXT rows, host steps) -> ks_attach_ext
+ *       ks_interpolation_plan(...)    -> scratch bytes of one ks_interpolation call
+ *     Regions are device memory on the context's device, 256-byte aligned (torch's allocator gives 512),
+ *     borrowed by the context: they must stay valid until ks_destroy (persistent, workspace), the next
+ *     ks_set_coarse (coarse, extension) or the end of the call (setup, interpolation scratch), and until the
+ *     stream work that uses them has completed. A region smaller than its plan returns KS_E_WORKSPACE.
+ *     The cuSOLVER / cuBLAS handles of NEXT-1 are the libraries' own host objects; cuBLAS is given its GEMM
+ *     workspace from the extension region (cublasSetWorkspace).
  *   - Every compute call is asynchronous on the context's stream (a cudaStream_t passed as void*).
  *     Device-detected conditions (non-finite values, NOT_SPD columns, non-convergence) are latched in a
  *     device flag word and returned by the next ks_sync. Argument errors are returned immediately and
@@ -46,7 +56,7 @@
 extern "C" {
 #endif
 
-#define KS_ABI_VERSION 1
+#define KS_ABI_VERSION 2
 
 typedef struct ks_ctx ks_ctx;
 
@@ -61,8 +71,16 @@ typedef enum {
   KS_E_CUDA = 6,           /* CUDA runtime error (message has the CUDA error string) */
   KS_E_NOMEM = 7,          /* device allocation failed */
   KS_E_STATE = 8,          /* call order: e.g. solve before assemble, project before set_coarse */
-  KS_E_RANK = 9            /* F_B not positive definite: W = [P | U~] rank deficient (ks_pencil_eig) */
+  KS_E_RANK = 9,           /* F_B not positive definite: W = [P | U~] rank deficient (ks_pencil_eig) */
+  KS_E_WORKSPACE = 10      /* a caller-provided region is smaller than its plan (see "Memory") */
 } ks_status;
+
+/* Features of the extension workspace (ks_ext_plan / ks_attach_ext). */
+enum {
+  KS_EXT_EIG = 1u,   /* ks_pencil_eig, ks_augmented_solve (NEXT-1) */
+  KS_EXT_SCF = 2u,   /* ks_hartree, ks_scf_solve (NEXT-2; implies KS_EXT_EIG) */
+  KS_EXT_STEP = 4u   /* ks_step_submit / ks_step_wait (the hot-path step from host buffers) */
+};
 
 /* Operator selector for ks_spmm / ks_values. */
 typedef enum { KS_OP_K = 0, KS_OP_M = 1, KS_OP_MV = 2, KS_OP_H = 3, KS_OP_A = 4 } ks_op;
@@ -72,22 +90,46 @@ int ks_abi_version(void);
 const char *ks_build_info(void);
 
 /*
+ * Memory plan of one fine mesh: the three region sizes ks_create needs (see "Memory").
+ *   h_xyz, h_tets, h_dirichlet: as ks_create (host, read during the call); max_N: largest block of orbitals
+ *   (1 <= max_N <= 64) any later call will use.
+ *   *persistent_bytes: mesh, CSR pattern, scatter map and inverse, K, M, M_V, H, A values, sliced-ELL copies
+ *                      (the context's lifetime);
+ *   *workspace_bytes:  the block solver's vectors for N <= max_N plus call scratch (the context's lifetime);
+ *   *setup_bytes:      temporaries of ks_create only (sort keys, geometry); may be freed after it returns.
+ * The sizes come from a host count of the pattern (the definitions of SURVEY.md §8(c) items 1-3). Needs a CUDA
+ * device (CUB temporary sizes). Errors: KS_E_ARG, KS_E_MESH (node index out of range, no free node), KS_E_CUDA;
+ * the message is ks_last_error(NULL).
+ */
+ks_status ks_plan(int64_t n_nodes, const double *h_xyz, int64_t n_tets, const int32_t *h_tets,
+                  const uint8_t *h_dirichlet, int32_t max_N, size_t *persistent_bytes, size_t *workspace_bytes,
+                  size_t *setup_bytes);
+
+/*
  * Setup of one fine mesh (section 2 of the paper; st3 PAPER.md:733-738).
  *   h_xyz       [n_nodes][3] f64 node coordinates (host)
  *   h_tets      [n_tets][4]  i32 node ids, positively oriented (host)
  *   h_dirichlet [n_nodes]    u8, nonzero = Dirichlet node (psi = 0 on dOmega)
+ *   max_N       as passed to ks_plan
+ *   d_persistent, d_workspace: caller-owned device regions of at least the planned sizes (context lifetime)
+ *   d_setup     caller-owned region of setup_bytes, used only during this call; NULL = the workspace serves
+ *               (then workspace_bytes >= setup_bytes is required)
  *   stream      cudaStream_t (NULL = legacy default stream) on the current device
- * On success *out is a new context; the call synchronises the stream once (setup is not async).
- * Errors: KS_E_ARG, KS_E_MESH (first bad tet id in ks_last_error(NULL) and in the ctx message),
- * KS_E_NOMEM, KS_E_CUDA. On error *out is NULL.
+ * On success *out is a new context; the call synchronises the stream (setup is not async).
+ * Errors: KS_E_ARG, KS_E_MESH (first bad tet id in ks_last_error(NULL)), KS_E_WORKSPACE, KS_E_CUDA.
+ * On error *out is NULL.
  */
 ks_status ks_create(int64_t n_nodes, const double *h_xyz, int64_t n_tets, const int32_t *h_tets,
-                    const uint8_t *h_dirichlet, void *stream, ks_ctx **out);
+                    const uint8_t *h_dirichlet, int32_t max_N, void *d_persistent, size_t persistent_bytes,
+                    void *d_workspace, size_t workspace_bytes, void *d_setup, size_t setup_bytes, void *stream,
+                    ks_ctx **out);
 
-/* Frees the library-owned device memory and the host struct. Safe on NULL. */
+/* Synchronises the stream and frees the host struct (the caller frees its regions afterwards). Safe on NULL. */
 void ks_destroy(ks_ctx *ctx);
 
-/* Re-targets the context to another stream (same device). */
+/* Re-targets the context to another stream (same device). Ordering: the new stream waits (event) for all
+ * work already enqueued on the old stream, because both share the context's workspaces; work enqueued on
+ * the new stream after this call therefore runs after it. */
 ks_status ks_set_stream(ks_ctx *ctx, void *stream);
 
 /* Sizes and read-only device views of the setup products (owned by the library). Any out-pointer may
@@ -125,7 +167,7 @@ ks_status ks_spmm(ks_ctx *ctx, ks_op op, int32_t N, const double *d_X, double *d
  * by Jacobi-preconditioned CG from x0 = u_i, batched over the N columns in one persistent kernel:
  * per-column alpha/beta, a column stops when ||r||_2 <= tol ||b||_2 (recursive residual) and is frozen.
  *   d_lambda [N] f64, d_U [n_free][N] f64 (input), d_Ut [n_free][N] f64 (output, may not alias d_U)
- *   tol > 0, max_iter >= 1, 1 <= N <= 64
+ *   tol > 0, max_iter >= 1, 1 <= N <= max_N (ks_plan)
  *   d_iters [N] i32 (output, may be NULL): iterations applied to each column
  *   d_relres [N] f64 (output, may be NULL): recursive ||r||/||b|| at exit
  * Asynchronous; the status (NOT_SPD, NONFINITE, NOT_CONVERGED) is latched for ks_sync. The last iterate
@@ -152,11 +194,24 @@ ks_status ks_true_residual(ks_ctx *ctx, int32_t N, const double *d_lambda, const
 /*
  * The interpolation operator P = I_H^h from the coarse space (Alg. 1, 747-753 st5):
  *   n_H coarse free nodes; d_P_row_ptr [n_free+1] i32, d_P_col [p_nnz] i32 (< n_H), d_P_val [p_nnz] f64.
- * The library copies P and builds P^T (coarse-major), the pattern of H P, and caches B_H = P^T M P.
- * Synchronises the stream once. Requires n_H >= 1, at most 4 entries per row.
+ * ks_coarse_plan groups the fine rows by parent set (in the workspace's call scratch) and returns the size of
+ * the coarse region; ks_set_coarse builds, in the caller's d_coarse region: the copy of P, the item tables,
+ * the pattern of H P, cached B_H = P^T M P and the projection workspace for N <= max_N. Both synchronise the
+ * stream. Requires n_H >= 1, at most 4 entries per row. A new coarse space detaches the extension workspace.
  */
+ks_status ks_coarse_plan(ks_ctx *ctx, int64_t n_H, const int32_t *d_P_row_ptr, const int32_t *d_P_col,
+                         const double *d_P_val, size_t *coarse_bytes);
 ks_status ks_set_coarse(ks_ctx *ctx, int64_t n_H, const int32_t *d_P_row_ptr, const int32_t *d_P_col,
-                        const double *d_P_val);
+                        const double *d_P_val, void *d_coarse, size_t coarse_bytes);
+
+/*
+ * Extension workspace of the NEXT rows and the host-buffer steps: features = KS_EXT_* mask; max_D = largest
+ * pencil dimension ks_pencil_eig will see (0: n_H + max_N, the projected pencil). Plan after ks_set_coarse
+ * (the sizes depend on n_H); ks_attach_ext binds the caller's region (valid until the next ks_set_coarse or
+ * ks_destroy). Calls that need a feature that is not attached return KS_E_STATE.
+ */
+ks_status ks_ext_plan(ks_ctx *ctx, uint32_t features, int64_t max_D, size_t *ext_bytes);
+ks_status ks_attach_ext(ks_ctx *ctx, uint32_t features, int64_t max_D, void *d_ext, size_t ext_bytes);
 
 /*
  * Projection onto W = [P | U~] (st1-st7), unshifted H (reading Q1):
@@ -211,14 +266,16 @@ ks_status ks_augmented_solve(ks_ctx *ctx, int32_t N, double *d_lambda, double *d
  * contains it, restricted to coarse FREE vertices (Dirichlet vertices carry zero data) with |lambda| > 1e-13,
  * sorted by coarse free index (coarse free index = rank of a non-Dirichlet coarse node, ascending id).
  *   h_xyz_c [n_c][3] f64, h_tets_c [m_c][4] i32, h_dirichlet_c [n_c] u8 (host, read during the call);
+ *   d_work: caller-owned device scratch of at least ks_interpolation_plan's bytes (used during the call only);
  *   d_P_row_ptr [n_free+1] i32, d_P_col [4 n_free] i32, d_P_val [4 n_free] f64 (device, caller-owned outputs,
  *   ready for ks_set_coarse); *h_n_H = coarse free nodes, *h_p_nnz = entries written.
  * Synchronises the stream. Errors: KS_E_ARG, KS_E_MESH (degenerate coarse tet, node id out of range, or a fine
- * node outside the coarse mesh), KS_E_CUDA.
+ * node outside the coarse mesh), KS_E_WORKSPACE, KS_E_CUDA.
  */
+ks_status ks_interpolation_plan(ks_ctx *ctx, int64_t n_c, const double *h_xyz_c, int64_t m_c, size_t *work_bytes);
 ks_status ks_interpolation(ks_ctx *ctx, int64_t n_c, const double *h_xyz_c, int64_t m_c, const int32_t *h_tets_c,
-                           const uint8_t *h_dirichlet_c, int32_t *d_P_row_ptr, int32_t *d_P_col, double *d_P_val,
-                           int64_t *h_n_H, int64_t *h_p_nnz);
+                           const uint8_t *h_dirichlet_c, void *d_work, size_t work_bytes, int32_t *d_P_row_ptr,
+                           int32_t *d_P_col, double *d_P_val, int64_t *h_n_H, int64_t *h_p_nnz);
 
 /*
  * NEXT-2: the nonlinear terms of the Kohn-Sham operator, on all nodes.
@@ -283,8 +340,11 @@ ks_status ks_step_submit(ks_ctx *ctx, int32_t N, const double *h_V, double mu, c
                          const double *h_U, double tol, int32_t max_iter, double *h_FA, double *h_FB);
 ks_status ks_step_wait(ks_ctx *ctx);
 
-/* Device memory owned by the library (bytes). */
+/* Bytes of caller memory the context currently references (sum of the bound regions' sizes). */
 ks_status ks_memory_bytes(const ks_ctx *ctx, size_t *bytes);
+/* Capacity, bytes in use and peak use of one region: 0 persistent, 1 workspace, 3 coarse, 4 extension
+ * (2 setup and 5 call scratch are unbound after their call). Any out-pointer may be NULL. */
+ks_status ks_memory_usage(const ks_ctx *ctx, int32_t region, size_t *capacity, size_t *used, size_t *peak);
 
 /* Number of kernel launches issued by this context since creation (for the bench's gpu_launches). */
 ks_status ks_launch_count(const ks_ctx *ctx, int64_t *count);

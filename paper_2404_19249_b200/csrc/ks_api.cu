@@ -5,6 +5,7 @@
 #include <mutex>
 
 #include "ks_internal.cuh"
+#include "ks_layout.cuh"
 
 static std::mutex g_err_mu;
 static std::string g_create_err;
@@ -21,6 +22,7 @@ const char *ks_status_name(ks_status s) {
     case KS_E_NOMEM: return "KS_E_NOMEM";
     case KS_E_STATE: return "KS_E_STATE";
     case KS_E_RANK: return "KS_E_RANK";
+    case KS_E_WORKSPACE: return "KS_E_WORKSPACE";
   }
   return "KS_E_?";
 }
@@ -45,39 +47,40 @@ ks_status ks_cuda_check(ks_ctx *ctx, cudaError_t e, const char *what) {
   return ks_fail(ctx, KS_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
+static const char *region_name(int r) {
+  static const char *names[KS_R_N] = {"persistent", "workspace", "setup", "coarse", "ext", "call"};
+  return (r >= 0 && r < KS_R_N) ? names[r] : "?";
+}
+
 ks_status ks_alloc(ks_ctx *ctx, void **ptr, size_t bytes, const char *what) {
   *ptr = nullptr;
-  cudaError_t e = cudaMalloc(ptr, bytes);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    *ptr = nullptr;
-    return ks_fail(ctx, KS_E_NOMEM, "cudaMalloc(%zu bytes) for %s: %s", bytes, what, cudaGetErrorString(e));
-  }
-  ctx->bytes += bytes;
-  ctx->allocs.push_back({*ptr, bytes});
-  // zero-filled: padding tails past the logical ends (read by the bulk tile copies) stay defined
-  e = cudaMemsetAsync(*ptr, 0, bytes, ctx->stream);
+  ks_region &g = ctx->reg[ctx->region];
+  const size_t need = ks_round(bytes > 0 ? bytes : 1);
+  if (!g.base || g.off + need > g.cap)
+    return ks_fail(ctx, KS_E_WORKSPACE, "%s region: %s needs %zu bytes at offset %zu of %zu (plan it with the "
+                   "matching ks_*_plan call)", region_name(ctx->region), what, need, g.off, g.cap);
+  *ptr = g.base + g.off;
+  g.off += need;
+  if (g.off > g.peak) g.peak = g.off;
+  // zero-filled: padding tails past the logical ends (read by the vector and bulk copies) stay defined
+  cudaError_t e = cudaMemsetAsync(*ptr, 0, bytes > 0 ? bytes : 1, ctx->stream);
   if (e != cudaSuccess) return ks_cuda_check(ctx, e, "cudaMemsetAsync (new allocation)");
   return KS_OK;
 }
 
-void ks_free(ks_ctx *ctx, void *ptr) {
-  if (!ptr) return;
-  for (size_t k = 0; k < ctx->allocs.size(); k++)
-    if (ctx->allocs[k].first == ptr) {
-      ctx->bytes -= ctx->allocs[k].second;
-      ctx->allocs.erase(ctx->allocs.begin() + k);
-      break;
-    }
-  cudaFree(ptr);
+static ks_status bind_region(ks_ctx *ctx, int r, void *base, size_t bytes, const char *what) {
+  if (((uintptr_t)base & (KS_ALIGN - 1)) != 0)
+    return ks_fail(ctx, KS_E_ARG, "%s: device pointer must be %d-byte aligned", what, KS_ALIGN);
+  ctx->reg[r].base = (uint8_t *)base;
+  ctx->reg[r].cap = base ? bytes : 0;
+  ctx->reg[r].off = 0;
+  ctx->reg[r].peak = 0;
+  return KS_OK;
 }
 
 static void free_all(ks_ctx *ctx) {
   ks_free_stream(ctx);
   ks_free_outer(ctx);
-  for (auto &a : ctx->allocs) cudaFree(a.first);
-  ctx->allocs.clear();
-  ctx->bytes = 0;
 }
 
 extern "C" {
@@ -90,26 +93,76 @@ const char *ks_build_info(void) {
   return "libks sm_100a fp64 (nvcc " KS_STR(__CUDACC_VER_MAJOR__) "." KS_STR(__CUDACC_VER_MINOR__) ") " __DATE__;
 }
 
-ks_status ks_create(int64_t n_nodes, const double *h_xyz, int64_t n_tets, const int32_t *h_tets,
-                    const uint8_t *h_dirichlet, void *stream, ks_ctx **out) {
-  if (!out) return KS_E_ARG;
-  *out = nullptr;
-  auto set_err = [](const std::string &m) {
-    std::lock_guard<std::mutex> g(g_err_mu);
-    g_create_err = m;
-  };
+static void set_create_err(const std::string &m) {
+  std::lock_guard<std::mutex> g(g_err_mu);
+  g_create_err = m;
+}
+
+static ks_status check_mesh_args(int64_t n_nodes, const double *h_xyz, int64_t n_tets, const int32_t *h_tets,
+                                 const uint8_t *h_dirichlet, int32_t max_N) {
   if (n_nodes < 4 || n_tets < 1 || !h_xyz || !h_tets || !h_dirichlet) {
-    set_err("KS_E_ARG: ks_create needs n_nodes >= 4, n_tets >= 1 and non-null host arrays");
+    set_create_err("KS_E_ARG: needs n_nodes >= 4, n_tets >= 1 and non-null host arrays");
     return KS_E_ARG;
   }
   if (n_nodes > 0x7fffffffLL || 16 * n_tets > 0x7fffffffLL) {
-    set_err("KS_E_ARG: mesh too large for int32 indexing (n_nodes < 2^31, 16 n_tets < 2^31)");
+    set_create_err("KS_E_ARG: mesh too large for int32 indexing (n_nodes < 2^31, 16 n_tets < 2^31)");
+    return KS_E_ARG;
+  }
+  if (max_N < 1 || max_N > KS_MAX_N) {
+    set_create_err("KS_E_ARG: max_N must be in [1, 64]");
+    return KS_E_ARG;
+  }
+  return KS_OK;
+}
+
+static int device_sm_count() {
+  int dev = 0, sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  return sm;
+}
+
+ks_status ks_plan(int64_t n_nodes, const double *h_xyz, int64_t n_tets, const int32_t *h_tets,
+                  const uint8_t *h_dirichlet, int32_t max_N, size_t *persistent_bytes, size_t *workspace_bytes,
+                  size_t *setup_bytes) {
+  KS_TRY(check_mesh_args(n_nodes, h_xyz, n_tets, h_tets, h_dirichlet, max_N));
+  if (!persistent_bytes || !workspace_bytes || !setup_bytes) {
+    set_create_err("KS_E_ARG: ks_plan needs non-null size outputs");
+    return KS_E_ARG;
+  }
+  KsMeshSizes z;
+  std::string err;
+  ks_status st = ks_count_mesh(n_nodes, h_tets, n_tets, h_dirichlet, &z, &err);
+  if (st != KS_OK) {
+    set_create_err(err);
+    return st;
+  }
+  const int sm = device_sm_count();
+  if (sm < 1) {
+    set_create_err("KS_E_CUDA: no CUDA device");
+    return KS_E_CUDA;
+  }
+  st = ks_plan_sizes(z, max_N, sm, persistent_bytes, workspace_bytes, setup_bytes);
+  if (st != KS_OK) set_create_err("KS_E_CUDA: CUB temporary-size query failed");
+  return st;
+}
+
+ks_status ks_create(int64_t n_nodes, const double *h_xyz, int64_t n_tets, const int32_t *h_tets,
+                    const uint8_t *h_dirichlet, int32_t max_N, void *d_persistent, size_t persistent_bytes,
+                    void *d_workspace, size_t workspace_bytes, void *d_setup, size_t setup_bytes, void *stream,
+                    ks_ctx **out) {
+  if (!out) return KS_E_ARG;
+  *out = nullptr;
+  KS_TRY(check_mesh_args(n_nodes, h_xyz, n_tets, h_tets, h_dirichlet, max_N));
+  if (!d_persistent || !d_workspace) {
+    set_create_err("KS_E_ARG: ks_create needs the persistent and workspace regions (sizes from ks_plan)");
     return KS_E_ARG;
   }
   ks_ctx *ctx = new ks_ctx();
   ctx->stream = (cudaStream_t)stream;
   ctx->n_nodes = n_nodes;
   ctx->n_tets = n_tets;
+  ctx->max_N = max_N;
   ks_status st = KS_OK;
   do {
     if ((st = ks_cuda_check(ctx, cudaGetDevice(&ctx->device), "cudaGetDevice")) != KS_OK) break;
@@ -119,15 +172,23 @@ ks_status ks_create(int64_t n_nodes, const double *h_xyz, int64_t n_tets, const 
     int coop = 0;
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
     if (!coop) { st = ks_fail(ctx, KS_E_CUDA, "device does not support cooperative launch"); break; }
-    if ((st = ks_alloc_t(ctx, &ctx->d_flags, 1, "flags")) != KS_OK) break;
-    if ((st = ks_alloc_t(ctx, &ctx->d_block_iters, 1, "block iters")) != KS_OK) break;
-    if ((st = ks_alloc_t(ctx, &ctx->barrier, 1, "barrier")) != KS_OK) break;
-    if ((st = ks_cuda_check(ctx, cudaMemsetAsync(ctx->d_flags, 0, 4, ctx->stream), "memset")) != KS_OK) break;
-    if ((st = ks_cuda_check(ctx, cudaMemsetAsync(ctx->d_block_iters, 0, 4, ctx->stream), "memset")) != KS_OK) break;
+    if ((st = bind_region(ctx, KS_R_PERSIST, d_persistent, persistent_bytes, "d_persistent")) != KS_OK) break;
+    if ((st = bind_region(ctx, KS_R_WORK, d_workspace, workspace_bytes, "d_workspace")) != KS_OK) break;
+    // setup temporaries: the caller's setup region, or the workspace (free until the solver carves it)
+    if ((st = d_setup ? bind_region(ctx, KS_R_SETUP, d_setup, setup_bytes, "d_setup")
+                      : bind_region(ctx, KS_R_SETUP, d_workspace, workspace_bytes, "d_workspace")) != KS_OK)
+      break;
     st = ks_setup_mesh(ctx, h_xyz, h_tets, h_dirichlet);
+    ctx->reg[KS_R_SETUP] = ks_region();   // the setup region is not referenced after ks_create returns
+    if (st != KS_OK) break;
+    KsRegion rg(ctx, KS_R_WORK);
+    KsCarver cv(ctx);
+    ks_layout_work(cv, ctx, ctx->n_free, max_N, ctx->sm_count);
+    if ((st = cv.st) != KS_OK) break;
+    st = ks_cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize (ks_create)");
   } while (0);
   if (st != KS_OK) {
-    set_err(ctx->err);
+    set_create_err(ctx->err);
     free_all(ctx);
     delete ctx;
     return st;
@@ -146,7 +207,17 @@ void ks_destroy(ks_ctx *ctx) {
 
 ks_status ks_set_stream(ks_ctx *ctx, void *stream) {
   if (!ctx) return KS_E_ARG;
-  ctx->stream = (cudaStream_t)stream;
+  cudaStream_t ns = (cudaStream_t)stream;
+  if (ns == ctx->stream) return KS_OK;
+  // Work still queued on the old stream shares the context's workspaces (grid-barrier counter, solver
+  // vectors, status flags): the new stream waits for it before anything enqueued after this call runs.
+  cudaEvent_t ev;
+  KS_CUDA(ctx, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  cudaError_t e = cudaEventRecord(ev, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(ns, ev, 0);
+  cudaEventDestroy(ev);
+  KS_CUDA(ctx, e);
+  ctx->stream = ns;
   return KS_OK;
 }
 
@@ -208,7 +279,9 @@ ks_status ks_spmm(ks_ctx *ctx, ks_op op, int32_t N, const double *d_X, double *d
   if (((uintptr_t)d_X & 7) || ((uintptr_t)d_Y & 7)) return ks_fail(ctx, KS_E_ARG, "ks_spmm: X, Y must be 8-byte aligned");
   const double *v = op_values(ctx, op);
   if (!v) return ks_fail(ctx, KS_E_STATE, "ks_spmm: operator %d not assembled", (int)op);
-  if (op == KS_OP_MV || op == KS_OP_H) KS_TRY(ks_materialize_views(ctx));
+  // the CSR views M_V, H, A are recomputed after an assembly on first use (the generic CSR kernel reads A
+  // for ragged N or unaligned blocks, so A is refreshed as well)
+  if (op == KS_OP_MV || op == KS_OP_H || op == KS_OP_A) KS_TRY(ks_materialize_views(ctx));
   return ks_spmm_impl(ctx, op, v, N, d_X, d_Y);
 }
 
@@ -259,15 +332,23 @@ ks_status ks_augmented_solve(ks_ctx *ctx, int32_t N, double *d_lambda, double *d
   return ks_augmented_solve_impl(ctx, N, d_lambda, d_U, tol_eig, max_outer, tol_bvp, max_iter_bvp, h_outer, h_history);
 }
 
+ks_status ks_interpolation_plan(ks_ctx *ctx, int64_t n_c, const double *h_xyz_c, int64_t m_c,
+                                size_t *work_bytes) {
+  if (!ctx) return KS_E_ARG;
+  if (n_c < 4 || m_c < 1 || n_c > 0x7fffffffLL || m_c > 0x7fffffffLL || !h_xyz_c || !work_bytes)
+    return ks_fail(ctx, KS_E_ARG, "ks_interpolation_plan: bad arguments");
+  return ks_interpolation_plan_impl(ctx, n_c, h_xyz_c, m_c, work_bytes);
+}
+
 ks_status ks_interpolation(ks_ctx *ctx, int64_t n_c, const double *h_xyz_c, int64_t m_c, const int32_t *h_tets_c,
-                           const uint8_t *h_dirichlet_c, int32_t *d_P_row_ptr, int32_t *d_P_col, double *d_P_val,
-                           int64_t *h_n_H, int64_t *h_p_nnz) {
+                           const uint8_t *h_dirichlet_c, void *d_work, size_t work_bytes, int32_t *d_P_row_ptr,
+                           int32_t *d_P_col, double *d_P_val, int64_t *h_n_H, int64_t *h_p_nnz) {
   if (!ctx) return KS_E_ARG;
   if (n_c < 4 || m_c < 1 || n_c > 0x7fffffffLL || m_c > 0x7fffffffLL || !h_xyz_c || !h_tets_c || !h_dirichlet_c ||
-      !d_P_row_ptr || !d_P_col || !d_P_val || !h_n_H || !h_p_nnz)
+      !d_work || !d_P_row_ptr || !d_P_col || !d_P_val || !h_n_H || !h_p_nnz)
     return ks_fail(ctx, KS_E_ARG, "ks_interpolation: bad arguments");
-  return ks_interpolation_impl(ctx, n_c, h_xyz_c, m_c, h_tets_c, h_dirichlet_c, d_P_row_ptr, d_P_col, d_P_val,
-                               h_n_H, h_p_nnz);
+  return ks_interpolation_impl(ctx, n_c, h_xyz_c, m_c, h_tets_c, h_dirichlet_c, d_work, work_bytes, d_P_row_ptr,
+                               d_P_col, d_P_val, h_n_H, h_p_nnz);
 }
 
 ks_status ks_density(ks_ctx *ctx, int32_t N, const double *d_U, double f, double *d_rho) {
@@ -343,14 +424,95 @@ ks_status ks_true_residual(ks_ctx *ctx, int32_t N, const double *d_lambda, const
   return ks_true_residual_impl(ctx, N, d_lambda, d_U, d_Ut, d_relres);
 }
 
+static ks_status check_coarse_args(ks_ctx *ctx, int64_t n_H, const int32_t *d_P_row_ptr, const int32_t *d_P_col,
+                                   const double *d_P_val) {
+  if (n_H < 1 || n_H > 0x7fffffffLL) return ks_fail(ctx, KS_E_ARG, "coarse space: n_H = %lld", (long long)n_H);
+  if (!d_P_row_ptr || !d_P_col || !d_P_val) return ks_fail(ctx, KS_E_ARG, "coarse space: null P arrays");
+  return KS_OK;
+}
+
+ks_status ks_coarse_plan(ks_ctx *ctx, int64_t n_H, const int32_t *d_P_row_ptr, const int32_t *d_P_col,
+                         const double *d_P_val, size_t *coarse_bytes) {
+  if (!ctx || !coarse_bytes) return KS_E_ARG;
+  KS_TRY(check_coarse_args(ctx, n_H, d_P_row_ptr, d_P_col, d_P_val));
+  return ks_set_coarse_impl(ctx, n_H, d_P_row_ptr, d_P_col, d_P_val, true, coarse_bytes);
+}
+
 ks_status ks_set_coarse(ks_ctx *ctx, int64_t n_H, const int32_t *d_P_row_ptr, const int32_t *d_P_col,
-                        const double *d_P_val) {
+                        const double *d_P_val, void *d_coarse, size_t coarse_bytes) {
   if (!ctx) return KS_E_ARG;
-  if (n_H < 1 || n_H > 0x7fffffffLL) return ks_fail(ctx, KS_E_ARG, "ks_set_coarse: n_H = %lld", (long long)n_H);
-  if (!d_P_row_ptr || !d_P_col || !d_P_val) return ks_fail(ctx, KS_E_ARG, "ks_set_coarse: null P arrays");
-  ks_status st = ks_set_coarse_impl(ctx, n_H, d_P_row_ptr, d_P_col, d_P_val);
-  if (st != KS_OK) ctx->n_H = 0;
+  KS_TRY(check_coarse_args(ctx, n_H, d_P_row_ptr, d_P_col, d_P_val));
+  if (!d_coarse) return ks_fail(ctx, KS_E_ARG, "ks_set_coarse: null coarse region (size from ks_coarse_plan)");
+  // a new coarse space invalidates the old one and the extension workspace planned for it
+  KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  ks_free_coarse(ctx);
+  ctx->ext_features = 0;
+  ctx->reg[KS_R_EXT] = ks_region();
+  KS_TRY(bind_region(ctx, KS_R_COARSE, d_coarse, coarse_bytes, "d_coarse"));
+  ks_status st = ks_set_coarse_impl(ctx, n_H, d_P_row_ptr, d_P_col, d_P_val, false, nullptr);
+  if (st != KS_OK) {
+    ks_free_coarse(ctx);
+    ctx->reg[KS_R_COARSE] = ks_region();
+  }
   return st;
+}
+
+static ks_status ext_sizes(ks_ctx *ctx, uint32_t features, int64_t max_D, KsExtSizes *e) {
+  if (features & KS_EXT_SCF) features |= KS_EXT_EIG;
+  e->features = features;
+  e->nn = ctx->n_nodes;
+  e->nt = ctx->n_tets;
+  e->nf = ctx->n_free;
+  e->nH = ctx->n_H;
+  e->ni = ctx->n_items;
+  e->N = ctx->max_N;
+  e->sm_count = ctx->sm_count;
+  e->D = ctx->n_H + ctx->max_N;
+  if (max_D > e->D) e->D = max_D;
+  e->lwork = 1;
+  if (features & KS_EXT_EIG) KS_TRY(ks_cusolver_lwork(ctx, e->D, ctx->n_H, &e->lwork));
+  return KS_OK;
+}
+
+ks_status ks_ext_plan(ks_ctx *ctx, uint32_t features, int64_t max_D, size_t *ext_bytes) {
+  if (!ctx || !ext_bytes) return KS_E_ARG;
+  if (features == 0 || (features & ~(uint32_t)(KS_EXT_EIG | KS_EXT_SCF | KS_EXT_STEP)))
+    return ks_fail(ctx, KS_E_ARG, "ks_ext_plan: features must be a nonempty KS_EXT_* mask");
+  if (max_D < 0 || max_D > 65536) return ks_fail(ctx, KS_E_ARG, "ks_ext_plan: max_D = %lld", (long long)max_D);
+  KsExtSizes e;
+  KS_TRY(ext_sizes(ctx, features, max_D, &e));
+  KsSizer sz;
+  ks_ctx tmp;
+  ks_layout_ext(sz, &tmp, e);
+  *ext_bytes = sz.bytes;
+  return KS_OK;
+}
+
+ks_status ks_attach_ext(ks_ctx *ctx, uint32_t features, int64_t max_D, void *d_ext, size_t ext_bytes) {
+  if (!ctx) return KS_E_ARG;
+  if (features == 0 || (features & ~(uint32_t)(KS_EXT_EIG | KS_EXT_SCF | KS_EXT_STEP)) || !d_ext || max_D < 0 ||
+      max_D > 65536)
+    return ks_fail(ctx, KS_E_ARG, "ks_attach_ext: bad arguments");
+  KsExtSizes e;
+  KS_TRY(ext_sizes(ctx, features, max_D, &e));
+  KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->ext_features = 0;
+  ctx->har2l_state = 0;
+  KS_TRY(bind_region(ctx, KS_R_EXT, d_ext, ext_bytes, "d_ext"));
+  {
+    KsRegion rg(ctx, KS_R_EXT);
+    KsCarver cv(ctx);
+    ks_layout_ext(cv, ctx, e);
+    if (cv.st != KS_OK) {
+      ctx->reg[KS_R_EXT] = ks_region();
+      return cv.st;
+    }
+  }
+  ctx->ext_features = e.features;
+  ctx->ext_nH = ctx->n_H;
+  ctx->ext_D = e.D;
+  ctx->ext_lwork = e.lwork;
+  return KS_OK;
 }
 
 ks_status ks_project_augmented(ks_ctx *ctx, int32_t N, const double *d_Ut, double *d_FA, double *d_FB) {
@@ -364,7 +526,17 @@ ks_status ks_project_augmented(ks_ctx *ctx, int32_t N, const double *d_Ut, doubl
 
 ks_status ks_memory_bytes(const ks_ctx *ctx, size_t *bytes) {
   if (!ctx || !bytes) return KS_E_ARG;
-  *bytes = ctx->bytes;
+  size_t b = 0;
+  for (int r = 0; r < KS_R_N; r++) b += ctx->reg[r].cap;
+  *bytes = b;
+  return KS_OK;
+}
+
+ks_status ks_memory_usage(const ks_ctx *ctx, int32_t region, size_t *capacity, size_t *used, size_t *peak) {
+  if (!ctx || region < 0 || region >= KS_R_N) return KS_E_ARG;
+  if (capacity) *capacity = ctx->reg[region].cap;
+  if (used) *used = ctx->reg[region].off;
+  if (peak) *peak = ctx->reg[region].peak;
   return KS_OK;
 }
 
@@ -379,8 +551,10 @@ ks_status ks_sync(ks_ctx *ctx) {
   cudaError_t e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) return ks_cuda_check(ctx, e, "cudaStreamSynchronize");
   unsigned f = 0;
-  KS_CUDA(ctx, cudaMemcpy(&f, ctx->d_flags, 4, cudaMemcpyDeviceToHost));
-  KS_CUDA(ctx, cudaMemset(ctx->d_flags, 0, 4));
+  // read and clear on the context's stream, so the clear is ordered before work enqueued afterwards
+  KS_CUDA(ctx, cudaMemcpyAsync(&f, ctx->d_flags, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  KS_CUDA(ctx, cudaMemsetAsync(ctx->d_flags, 0, 4, ctx->stream));
+  KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   if (f & KSF_NONFINITE) return ks_fail(ctx, KS_E_NONFINITE, "non-finite value met (V_eff or a solver reduction)");
   if (f & KSF_NOT_SPD) return ks_fail(ctx, KS_E_NOT_SPD, "p.Ap <= 0 in some column: A = H + mu M not SPD (mu too small)");
   if (f & KSF_NOT_CONVERGED) return ks_fail(ctx, KS_E_NOT_CONVERGED, "max_iter reached with columns above tolerance");

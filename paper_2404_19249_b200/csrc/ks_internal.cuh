@@ -18,14 +18,38 @@ enum : unsigned {
   KSF_MESH = 8u,
 };
 
+// Device memory is owned by the caller (include/ks.h, "Memory"): the library carves every buffer out of
+// caller-provided regions with a bump allocator (ks_alloc); it never calls cudaMalloc / cudaFree.
+enum : int {
+  KS_R_PERSIST = 0,   // ks_create: mesh, pattern, maps, values, sliced-ELL copies (ctx lifetime)
+  KS_R_WORK = 1,      // ks_create: solver workspace for N <= max_N + call scratch (ctx lifetime)
+  KS_R_SETUP = 2,     // ks_create only: setup temporaries (may be the workspace)
+  KS_R_COARSE = 3,    // ks_set_coarse: P, item tables, B_H, projection workspace (until the next set_coarse)
+  KS_R_EXT = 4,       // ks_attach_ext: NEXT-1/2 and host-step workspaces
+  KS_R_CALL = 5,      // one call's caller-provided scratch (ks_interpolation)
+  KS_R_N = 6
+};
+struct ks_region {
+  uint8_t *base = nullptr;
+  size_t cap = 0, off = 0, peak = 0;
+};
+#define KS_ALIGN 256
+static inline size_t ks_round(size_t b) { return (b + KS_ALIGN - 1) / KS_ALIGN * KS_ALIGN; }
+
 struct ks_ctx {
   int device = 0;
   int sm_count = 0;
   cudaStream_t stream = nullptr;
   int64_t n_nodes = 0, n_tets = 0, n_free = 0, nnz = 0, n_contrib = 0;
   int64_t launches = 0;
-  size_t bytes = 0;
-  std::vector<std::pair<void *, size_t>> allocs;  // every library-owned device allocation (ks_alloc)
+  int max_N = 0;                    // largest N the workspace was planned for (ks_plan / ks_create)
+  ks_region reg[KS_R_N];
+  int region = KS_R_PERSIST;        // region ks_alloc carves from
+  unsigned ext_features = 0;        // KS_EXT_* of the attached extension workspace (0: none attached)
+  int64_t ext_nH = -1;              // n_H it was planned for (a new coarse space detaches it)
+  int64_t ext_D = 0;                // largest pencil dimension it holds
+  int64_t ext_lwork = 0;            // cuSOLVER workspace (doubles) it holds
+  uint8_t *blas_ws = nullptr;       // cuBLAS workspace (KS_EXT_BLAS_WS bytes)
 
   // mesh / pattern (library-owned device memory)
   int32_t *tets = nullptr;          // [4 n_tets]
@@ -61,14 +85,10 @@ struct ks_ctx {
   unsigned long long *trace = nullptr;  // [KS_TRACE_CAP] phase-end timestamps of the last traced solve
   int *trace_count = nullptr;
 
-  // solver workspace (grown on demand)
-  int ws_np = 0;                    // padded N the workspace was sized for
-  int64_t ws_rows = 0;
+  // solver workspace (KS_R_WORK, carved at ks_create for N <= max_N)
   double *r = nullptr, *p = nullptr, *q = nullptr, *xpad = nullptr, *upad = nullptr, *bpad = nullptr;
   double *partials = nullptr;       // [grid][4 * 64]
   unsigned *barrier = nullptr;      // grid barrier counter
-  int64_t partial_cap = 0;
-  std::vector<std::pair<int, int>> tile_nnz_cache;  // (tile rows, max nnz of such a tile)
 
   // coarse space (ks_set_coarse) and projection workspace
   int64_t n_H = 0, p_nnz = 0;
@@ -90,10 +110,8 @@ struct ks_ctx {
   double *B_H = nullptr;         // [n_H n_H] cached P^T M P
   double *AH_part = nullptr;     // [4 d_total] per-item partials of P^T Op P
   double *bH_part = nullptr, *cH_part = nullptr;  // [4 n_items NP]
-  int64_t bc_cap = 0;
   double *Y_H = nullptr, *Y_M = nullptr, *proj_u = nullptr;  // [n_free][NP] (Y_H, Y_M in item order)
   double *proj_up = nullptr;     // [n_free][NP] U~ in item order
-  int64_t y_cap = 0;
   double *gram_part = nullptr;   // [blocks][2 N N]
   int64_t gram_cap = 0;
 
@@ -114,34 +132,22 @@ struct ks_ctx {
   double *scf_veff = nullptr, *scf_Ut = nullptr, *scf_FA = nullptr, *scf_FB = nullptr, *scf_Y = nullptr;
   double *scf_hin = nullptr, *scf_hout = nullptr, *scf_part = nullptr, *scf_red = nullptr, *scf_alpha = nullptr;
   int *scf_slot = nullptr;
-  int64_t scf_nn = 0, scf_D = 0;
-  int scf_N = 0, scf_depth = 0;
-  // staged S phase of the block PCG (ks_stage.cu): tables for one NP
-  int stage_np = 0, stage_cap = 0;
-  int64_t stage_groups = 0, stage_staged = 0;
-  int32_t *stage_meta = nullptr;
-  uint16_t *stage_slcol = nullptr, *stage_dlc = nullptr;
   // pipelined host-buffer steps (ks_stream.cu)
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
   double *st_V[2] = {nullptr, nullptr}, *st_lam[2] = {nullptr, nullptr}, *st_U[2] = {nullptr, nullptr};
   double *st_Ut[2] = {nullptr, nullptr}, *st_FA[2] = {nullptr, nullptr}, *st_FB[2] = {nullptr, nullptr};
-  int step_N = 0;
-  int64_t step_D = 0, step_count = 0;
+  int64_t step_count = 0;
   int interp_fallbacks = 0;         // last ks_interpolation needed the scan fallback of the walk
   // NEXT-1 (ks_outer.cu): cuSOLVER handle, pencil and outer-loop workspaces
   void *cusolver = nullptr;
   void *cublas = nullptr;           // cuBLAS handle of the filtered pencil eigensolver (ks_outer.cu)
   double *ef_buf = nullptr;         // [4][D][m] work blocks of the filtered eigensolver
   double *ef_small = nullptr;       // [m][m] device staging of the small Rayleigh-Ritz / SVQB matrices
-  int64_t ef_cap = 0, ef_small_cap = 0;
   int64_t ef_L_D = 0;                // D of the Cholesky factor held in eig_B (0: none)
   double *eig_A = nullptr, *eig_B = nullptr, *eig_w = nullptr, *eig_work = nullptr;
   int *eig_info = nullptr;
-  int64_t eig_cap = 0;
-  int eig_work_cap = 0;
   double *outer_Ut = nullptr, *outer_FA = nullptr, *outer_FB = nullptr, *outer_Y = nullptr, *outer_lam = nullptr;
-  int64_t outer_cap = 0, outer_D = 0;
 
   std::string err;
 };
@@ -152,19 +158,41 @@ struct ks_ctx {
 #define KS_PAD 8
 #define KS_TRACE_CAP 8192
 #define KS_SELL_C 8   // rows per slice of the sliced-ELL operator copy
-#define KS_STAGE_RMAX 8      // runs of staged p rows per S-phase group (ks_stage.cu)
-#define KS_META_BYTES 80     // group record: 4 ints + KS_STAGE_RMAX (start, len) pairs
 
 const char *ks_status_name(ks_status s);
 ks_status ks_fail(ks_ctx *ctx, ks_status s, const char *fmt, ...);
 ks_status ks_cuda_check(ks_ctx *ctx, cudaError_t e, const char *what);
+// carves `bytes` (KS_ALIGN-aligned, zero-filled on the stream) from region ctx->region; KS_E_WORKSPACE when
+// the caller's region is smaller than its plan said
 ks_status ks_alloc(ks_ctx *ctx, void **ptr, size_t bytes, const char *what);
-void ks_free(ks_ctx *ctx, void *ptr);   // frees a ks_alloc'ed pointer (no-op on nullptr)
-template <typename T>
-static inline void ks_free_t(ks_ctx *ctx, T *&ptr) {
-  ks_free(ctx, (void *)ptr);
-  ptr = nullptr;
-}
+
+// the allocation region for a scope
+struct KsRegion {
+  ks_ctx *c;
+  int prev;
+  KsRegion(ks_ctx *c_, int r) : c(c_), prev(c_->region) { c->region = r; }
+  ~KsRegion() { c->region = prev; }
+};
+// temporaries of one call: allocations from region r inside the scope are released at its end
+struct KsScratch {
+  ks_ctx *c;
+  int r, prev;
+  size_t mark;
+  KsScratch(ks_ctx *c_, int r_) : c(c_), r(r_), prev(c_->region), mark(c_->reg[r_].off) { c->region = r_; }
+  ~KsScratch() {
+    c->reg[r].off = mark;
+    c->region = prev;
+  }
+};
+
+// byte counter with the allocator's rounding: plans add exactly what the allocation sites carve
+struct KsSizer {
+  size_t bytes = 0;
+  template <typename T>
+  void add(T **, int64_t count, const char * = nullptr) {
+    bytes += ks_round(sizeof(T) * (size_t)(count > 0 ? count : 1));
+  }
+};
 
 #define KS_TRY(expr)                      \
   do {                                    \
@@ -200,10 +228,10 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // internal entry points implemented in the .cu files
 ks_status ks_setup_mesh(ks_ctx *ctx, const double *h_xyz, const int32_t *h_tets, const uint8_t *h_dir);
-ks_status ks_sell_build(ks_ctx *ctx);
-ks_status ks_stage_build(ks_ctx *ctx, int NP, int max_rows);
+ks_status ks_sell_build(ks_ctx *ctx, int32_t *cnt, void *cub, size_t cub_bytes, int64_t planned_total);
 ks_status ks_coarse_galerkin(ks_ctx *ctx, const double *op_sell_vals, double *out);   // P^T Op P, dense [n_H][n_H]
 ks_status ks_spd_inverse(ks_ctx *ctx, double *A, int64_t n, bool *spd);              // A <- A^-1 (Cholesky)
+ks_status ks_cusolver_lwork(ks_ctx *ctx, int64_t D, int64_t nH, int64_t *lwork);
 ks_status ks_pcg2l_run(ks_ctx *ctx, const double *b, const double *x0, double *x, double tol, int max_iter,
                        int32_t *d_iters);
 void ks_free_pcg2l(ks_ctx *ctx);
@@ -218,7 +246,7 @@ ks_status ks_pcg_run(ks_ctx *ctx, const double *sell_vals, const double *dinv, d
 ks_status ks_true_residual_impl(ks_ctx *ctx, int N, const double *lambda, const double *U,
                                 const double *Ut, double *relres);
 ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, const int32_t *Pcol,
-                             const double *Pval);
+                             const double *Pval, bool plan_only, size_t *coarse_bytes);
 ks_status ks_project_impl(ks_ctx *ctx, int N, const double *Ut, double *FA, double *FB);
 void ks_free_coarse(ks_ctx *ctx);
 void ks_free_outer(ks_ctx *ctx);
@@ -235,8 +263,9 @@ ks_status ks_scf_solve_impl(ks_ctx *ctx, int N, const double *vext, double f, do
 ks_status ks_hartree_impl(ks_ctx *ctx, const double *rho, double tol, int max_iter, double *vh, int warm,
                           double *h_mom, int32_t *h_iters);
 ks_status ks_interpolation_impl(ks_ctx *ctx, int64_t n_c, const double *h_xyz_c, int64_t m_c, const int32_t *h_tets_c,
-                                const uint8_t *h_dir_c, int32_t *d_rowptr, int32_t *d_col, double *d_val,
-                                int64_t *h_nH, int64_t *h_pnnz);
+                                const uint8_t *h_dir_c, void *d_work, size_t work_bytes, int32_t *d_rowptr,
+                                int32_t *d_col, double *d_val, int64_t *h_nH, int64_t *h_pnnz);
+ks_status ks_interpolation_plan_impl(ks_ctx *ctx, int64_t n_c, const double *h_xyz_c, int64_t m_c, size_t *bytes);
 ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, const double *FB, double *evals,
                              double *evecs, const double *Ywarm = nullptr, bool same_B = false);
 // Ywarm [D][k] (device, may alias evecs): start block of the filtered path (e.g. the previous inner step's

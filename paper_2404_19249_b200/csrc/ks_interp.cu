@@ -20,6 +20,7 @@
 #include <cub/cub.cuh>
 
 #include "ks_internal.cuh"
+#include "ks_layout.cuh"
 
 #define KS_INTERP_DROP 1e-13
 #define KS_INTERP_ACCEPT (-1e-12)
@@ -147,24 +148,70 @@ __global__ void k_compact_rows(const int32_t *__restrict__ rowptr, const int32_t
   }
 }
 
-struct DevBuf {
-  std::vector<void *> p;
-  ~DevBuf() { for (void *x : p) cudaFree(x); }
-  template <typename T>
-  cudaError_t get(T **ptr, size_t count) {
-    cudaError_t e = cudaMalloc((void **)ptr, sizeof(T) * (count ? count : 1));
-    if (e == cudaSuccess) p.push_back(*ptr);
-    return e;
-  }
+struct InterpBufs {
+  double *xc = nullptr, *J = nullptr, *val4 = nullptr;
+  int32_t *tc = nullptr, *nbr = nullptr, *vtet = nullptr, *cptr = nullptr, *cv = nullptr, *cfree = nullptr;
+  int32_t *cnt = nullptr, *col4 = nullptr;
+  unsigned *flags = nullptr;
+  uint8_t *cub = nullptr;
 };
+
+// the call's device buffers (caller-provided scratch, ks_interpolation_plan sizes it with the same list)
+template <class A>
+void interp_layout(A &a, InterpBufs &b, int64_t n_c, int64_t m_c, int64_t ncell, int64_t nf, size_t cub) {
+  a.add(&b.xc, 3 * n_c, "coarse xyz");
+  a.add(&b.J, 9 * m_c, "coarse inverse Jacobians");
+  a.add(&b.tc, 4 * m_c, "coarse tets");
+  a.add(&b.nbr, 4 * m_c, "coarse face neighbours");
+  a.add(&b.vtet, n_c, "vertex tet");
+  a.add(&b.cptr, ncell + 1, "bucket ptr");
+  a.add(&b.cv, n_c, "bucket vertices");
+  a.add(&b.cfree, n_c, "coarse free numbering");
+  a.add(&b.cnt, nf + 1, "row counts");
+  a.add(&b.col4, 4 * nf, "4-wide columns");
+  a.add(&b.val4, 4 * nf, "4-wide values");
+  a.add(&b.flags, 1, "flags");
+  a.add(&b.cub, (int64_t)cub, "scan temporary");
+}
+
+// bucket grid over the coarse vertices: cell ~ the mean vertex spacing, <= 1024 cells per axis
+void interp_grid(const double *xc, int64_t n_c, double bmin[3], double bmax[3], double *h, int g[3]) {
+  for (int d = 0; d < 3; d++) { bmin[d] = 1e300; bmax[d] = -1e300; }
+  for (int64_t v = 0; v < n_c; v++)
+    for (int d = 0; d < 3; d++) {
+      bmin[d] = std::min(bmin[d], xc[3 * v + d]);
+      bmax[d] = std::max(bmax[d], xc[3 * v + d]);
+    }
+  double vol = 1.0;
+  for (int d = 0; d < 3; d++) vol *= std::max(bmax[d] - bmin[d], 1e-300);
+  *h = std::cbrt(vol / (double)std::max<int64_t>(n_c, 1));
+  for (int d = 0; d < 3; d++) g[d] = std::max(1, std::min(1024, (int)std::ceil((bmax[d] - bmin[d]) / *h)));
+}
 
 }  // namespace
 
-#define DB(ptr, n) KS_CUDA(ctx, db.get(&(ptr), (size_t)(n)))
+static ks_status interp_cub_bytes(int64_t nf, size_t *bytes) {
+  int32_t *p = nullptr;
+  *bytes = 0;
+  return cub::DeviceScan::ExclusiveSum(nullptr, *bytes, p, p, (int)(nf + 1)) == cudaSuccess ? KS_OK : KS_E_CUDA;
+}
+
+ks_status ks_interpolation_plan_impl(ks_ctx *ctx, int64_t n_c, const double *xc, int64_t m_c, size_t *bytes) {
+  double bmin[3], bmax[3], h;
+  int g[3];
+  interp_grid(xc, n_c, bmin, bmax, &h, g);
+  size_t cub = 0;
+  if (interp_cub_bytes(ctx->n_free, &cub) != KS_OK) return ks_fail(ctx, KS_E_CUDA, "CUB temporary-size query failed");
+  KsSizer sz;
+  InterpBufs b;
+  interp_layout(sz, b, n_c, m_c, (int64_t)g[0] * g[1] * g[2], ctx->n_free, cub);
+  *bytes = sz.bytes;
+  return KS_OK;
+}
 
 ks_status ks_interpolation_impl(ks_ctx *ctx, int64_t n_c, const double *xc, int64_t m_c, const int32_t *tc,
-                                const uint8_t *dc, int32_t *d_rowptr, int32_t *d_col, double *d_val, int64_t *h_nH,
-                                int64_t *h_pnnz) {
+                                const uint8_t *dc, void *d_work, size_t work_bytes, int32_t *d_rowptr, int32_t *d_col,
+                                double *d_val, int64_t *h_nH, int64_t *h_pnnz) {
   cudaStream_t s = ctx->stream;
   // ---- host: coarse structures (free numbering, inverse Jacobians, face adjacency, vertex -> tet, buckets)
   std::vector<int32_t> cfree(n_c);
@@ -215,17 +262,9 @@ ks_status ks_interpolation_impl(ks_ctx *ctx, int64_t n_c, const double *xc, int6
   std::vector<int32_t> vtet(n_c, -1);
   for (int64_t t = m_c - 1; t >= 0; t--)
     for (int a = 0; a < 4; a++) vtet[tc[4 * t + a]] = (int32_t)t;   // smallest incident tet id
-  double bmin[3] = {1e300, 1e300, 1e300}, bmax[3] = {-1e300, -1e300, -1e300};
-  for (int64_t v = 0; v < n_c; v++)
-    for (int d = 0; d < 3; d++) {
-      bmin[d] = std::min(bmin[d], xc[3 * v + d]);
-      bmax[d] = std::max(bmax[d], xc[3 * v + d]);
-    }
-  double vol = 1.0;
-  for (int d = 0; d < 3; d++) vol *= std::max(bmax[d] - bmin[d], 1e-300);
-  const double h = std::cbrt(vol / (double)std::max<int64_t>(n_c, 1));
+  double bmin[3], bmax[3], h;
   int g[3];
-  for (int d = 0; d < 3; d++) g[d] = std::max(1, std::min(1024, (int)std::ceil((bmax[d] - bmin[d]) / h)));
+  interp_grid(xc, n_c, bmin, bmax, &h, g);
   const int64_t ncell = (int64_t)g[0] * g[1] * g[2];
   std::vector<int32_t> cell_of(n_c), cell_ptr(ncell + 1, 0), cell_v(n_c);
   for (int64_t v = 0; v < n_c; v++) {
@@ -239,24 +278,29 @@ ks_status ks_interpolation_impl(ks_ctx *ctx, int64_t n_c, const double *xc, int6
     std::vector<int32_t> fill(cell_ptr.begin(), cell_ptr.end() - 1);
     for (int64_t v = 0; v < n_c; v++) cell_v[fill[cell_of[v]]++] = (int32_t)v;   // ascending ids per cell
   }
-  // ---- device
-  DevBuf db;
-  double *d_xc, *d_J, *d_val4;
-  int32_t *d_tc, *d_nbr, *d_vtet, *d_cptr, *d_cv, *d_cfree, *d_cnt, *d_col4;
-  unsigned *d_flags;
+  // ---- device: the call's buffers carved from the caller's scratch
   const int64_t nf = ctx->n_free;
-  DB(d_xc, 3 * n_c);
-  DB(d_J, 9 * m_c);
-  DB(d_tc, 4 * m_c);
-  DB(d_nbr, 4 * m_c);
-  DB(d_vtet, n_c);
-  DB(d_cptr, ncell + 1);
-  DB(d_cv, n_c);
-  DB(d_cfree, n_c);
-  DB(d_cnt, nf + 1);
-  DB(d_col4, 4 * nf);
-  DB(d_val4, 4 * nf);
-  DB(d_flags, 1);
+  size_t cub_bytes = 0;
+  if (interp_cub_bytes(nf, &cub_bytes) != KS_OK) return ks_fail(ctx, KS_E_CUDA, "CUB temporary-size query failed");
+  if (((uintptr_t)d_work & (KS_ALIGN - 1)) != 0) return ks_fail(ctx, KS_E_ARG, "ks_interpolation: d_work not aligned");
+  struct CallRegion {
+    ks_ctx *c;
+    ~CallRegion() { c->reg[KS_R_CALL] = ks_region(); }
+  } unbind{ctx};
+  ctx->reg[KS_R_CALL].base = (uint8_t *)d_work;
+  ctx->reg[KS_R_CALL].cap = work_bytes;
+  ctx->reg[KS_R_CALL].off = 0;
+  InterpBufs bf;
+  {
+    KsRegion rg(ctx, KS_R_CALL);
+    KsCarver cv(ctx);
+    interp_layout(cv, bf, n_c, m_c, ncell, nf, cub_bytes);
+    KS_TRY(cv.st);
+  }
+  double *d_xc = bf.xc, *d_J = bf.J, *d_val4 = bf.val4;
+  int32_t *d_tc = bf.tc, *d_nbr = bf.nbr, *d_vtet = bf.vtet, *d_cptr = bf.cptr, *d_cv = bf.cv, *d_cfree = bf.cfree;
+  int32_t *d_cnt = bf.cnt, *d_col4 = bf.col4;
+  unsigned *d_flags = bf.flags;
   KS_CUDA(ctx, cudaMemcpyAsync(d_xc, xc, sizeof(double) * 3 * n_c, cudaMemcpyHostToDevice, s));
   KS_CUDA(ctx, cudaMemcpyAsync(d_J, Jinv.data(), sizeof(double) * 9 * m_c, cudaMemcpyHostToDevice, s));
   KS_CUDA(ctx, cudaMemcpyAsync(d_tc, tc, sizeof(int32_t) * 4 * m_c, cudaMemcpyHostToDevice, s));
@@ -289,11 +333,8 @@ ks_status ks_interpolation_impl(ks_ctx *ctx, int64_t n_c, const double *xc, int6
   a.flags = d_flags;
   k_locate<<<ks_blocks(nf, 128), 128, 0, s>>>(a);
   KS_LAUNCHED(ctx);
-  size_t tmp_bytes = 0;
-  KS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_cnt, d_rowptr, (int)(nf + 1), s));
-  void *tmp = nullptr;
-  KS_CUDA(ctx, db.get((uint8_t **)&tmp, tmp_bytes));
-  KS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, d_cnt, d_rowptr, (int)(nf + 1), s));
+  size_t tmp_bytes = cub_bytes;
+  KS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(bf.cub, tmp_bytes, d_cnt, d_rowptr, (int)(nf + 1), s));
   ctx->launches++;
   k_compact_rows<<<ks_blocks(nf, 256), 256, 0, s>>>(d_rowptr, d_col4, d_val4, nf, d_col, d_val);
   KS_LAUNCHED(ctx);

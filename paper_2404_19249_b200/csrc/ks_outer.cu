@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "ks_internal.cuh"
+#include "ks_layout.cuh"
 #include "ks_sell.cuh"
 
 namespace {
@@ -157,10 +158,9 @@ ks_status ks_spd_inverse(ks_ctx *ctx, double *A, int64_t n, bool *spd) {
       cusolverDnDpotri_bufferSize(h, CUBLAS_FILL_MODE_LOWER, (int)n, A, (int)n, &lw2) != CUSOLVER_STATUS_SUCCESS)
     return ks_fail(ctx, KS_E_CUDA, "potrf/potri bufferSize failed");
   const int lw = lw1 > lw2 ? lw1 : lw2;
-  double *work = nullptr;
-  int *info = nullptr;
-  KS_CUDA(ctx, cudaMallocAsync((void **)&work, sizeof(double) * (size_t)(lw > 0 ? lw : 1), ctx->stream));
-  KS_CUDA(ctx, cudaMallocAsync((void **)&info, sizeof(int), ctx->stream));
+  if (lw > ctx->ext_lwork) return ks_fail(ctx, KS_E_WORKSPACE, "Cholesky workspace %d exceeds the ext plan", lw);
+  double *work = ctx->eig_work;
+  int *info = ctx->eig_info;
   int hinfo = 0;
   bool ok = cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, (int)n, A, (int)n, work, lw, info) == CUSOLVER_STATUS_SUCCESS;
   if (ok) {
@@ -176,13 +176,41 @@ ks_status ks_spd_inverse(ks_ctx *ctx, double *A, int64_t n, bool *spd) {
       ok = hinfo == 0;
     }
   }
-  KS_CUDA(ctx, cudaFreeAsync(work, ctx->stream));
-  KS_CUDA(ctx, cudaFreeAsync(info, ctx->stream));
   if (ok) {
     k_mirror_lower<<<ks_blocks(n * n, 256), 256, 0, ctx->stream>>>(A, n);
     KS_LAUNCHED(ctx);
   }
   *spd = ok;
+  return KS_OK;
+}
+
+// cuSOLVER workspace (doubles) of the pencil routes for dimension D (k = 1..D) and of the Cholesky inverse of
+// the n_H x n_H coarse stiffness (two-level Hartree solve)
+ks_status ks_cusolver_lwork(ks_ctx *ctx, int64_t D, int64_t nH, int64_t *lwork) {
+  KS_TRY(ensure_solver_handle(ctx));
+  cusolverDnHandle_t h = (cusolverDnHandle_t)ctx->cusolver;
+  int lw = 1, x = 0, meig = 0;
+  double *p = nullptr, *w = nullptr;
+  auto mx = [&](cusolverStatus_t st) {
+    if (st != CUSOLVER_STATUS_SUCCESS) return false;
+    lw = lw > x ? lw : x;
+    return true;
+  };
+  const int d = (int)D;
+  bool ok = mx(cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, d, p, d, &x)) &&
+            mx(cusolverDnDsygvd_bufferSize(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, d,
+                                           p, d, p, d, w, &x));
+  for (int k : {1, d}) {
+    ok = ok && mx(cusolverDnDsygvdx_bufferSize(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
+                                               CUBLAS_FILL_MODE_LOWER, d, p, d, p, d, 0.0, 0.0, 1, k, &meig, w, &x));
+  }
+  if (nH > 0) {
+    const int c = (int)nH;
+    ok = ok && mx(cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, c, p, c, &x)) &&
+         mx(cusolverDnDpotri_bufferSize(h, CUBLAS_FILL_MODE_LOWER, c, p, c, &x));
+  }
+  if (!ok) return ks_fail(ctx, KS_E_CUDA, "cuSOLVER bufferSize query failed (D = %lld)", (long long)D);
+  *lwork = lw;
   return KS_OK;
 }
 
@@ -299,6 +327,9 @@ static ks_status ensure_blas(ks_ctx *ctx) {
   }
   if (cublasSetStream((cublasHandle_t)ctx->cublas, ctx->stream) != CUBLAS_STATUS_SUCCESS)
     return ks_fail(ctx, KS_E_CUDA, "cublasSetStream failed");
+  // the GEMM workspace comes from the caller's extension region (cuBLAS allocates none of its own)
+  if (cublasSetWorkspace((cublasHandle_t)ctx->cublas, ctx->blas_ws, KS_EXT_BLAS_WS) != CUBLAS_STATUS_SUCCESS)
+    return ks_fail(ctx, KS_E_CUDA, "cublasSetWorkspace failed");
   return KS_OK;
 }
 
@@ -323,16 +354,8 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
                            (int)D, &one, L, (int)D, A, (int)D));
   KS_BLAS(ctx, cublasDtrsm(hb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)D,
                            (int)D, &one, L, (int)D, A, (int)D));
-  if (ctx->ef_cap < 4 * D * m) {
-    ks_free_t(ctx, ctx->ef_buf);
-    KS_TRY(ks_alloc_t(ctx, &ctx->ef_buf, 4 * D * m, "filtered eig blocks"));
-    ctx->ef_cap = 4 * D * m;
-  }
-  if (ctx->ef_small_cap < 2 * (int64_t)m * m + m + 1) {   // two m x m Grams, then V and lambda
-    ks_free_t(ctx, ctx->ef_small);
-    KS_TRY(ks_alloc_t(ctx, &ctx->ef_small, 2 * (int64_t)m * m + m + 1, "filtered eig small"));
-    ctx->ef_small_cap = 2 * (int64_t)m * m + m + 1;
-  }
+  // ef_buf [4][D][m], ef_small [2 m m + m + 1] (two m x m Grams, then V and lambda): the extension workspace
+  // holds them for m <= max_N + EF_GUARD and D <= ext_D (ks_pencil_eig_impl routes larger k to the dense path)
   double *X = ctx->ef_buf, *CX = X + D * m, *T1 = CX + D * m, *T2 = T1 + D * m, *sm = ctx->ef_small;
   // start block: Y0 in T1, X = L^T Y0
   {
@@ -499,24 +522,19 @@ ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, co
                              double *evecs, const double *Ywarm, bool same_B) {
   KS_TRY(ensure_solver_handle(ctx));
   cusolverDnHandle_t h = (cusolverDnHandle_t)ctx->cusolver;
-  if (ctx->eig_cap < D) {
-    ks_free_t(ctx, ctx->eig_A);
-    ks_free_t(ctx, ctx->eig_B);
-    ks_free_t(ctx, ctx->eig_w);
-    KS_TRY(ks_alloc_t(ctx, &ctx->eig_A, D * D, "pencil A"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->eig_B, D * D, "pencil B"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->eig_w, D, "pencil eigenvalues"));
-    ctx->eig_cap = D;
-  }
+  if (!(ctx->ext_features & (KS_EXT_EIG | KS_EXT_SCF)))
+    return ks_fail(ctx, KS_E_STATE, "ks_pencil_eig: attach an extension workspace planned with KS_EXT_EIG");
+  if (D > ctx->ext_D)
+    return ks_fail(ctx, KS_E_WORKSPACE, "ks_pencil_eig: D = %lld exceeds the ext plan's %lld", (long long)D,
+                   (long long)ctx->ext_D);
   // symmetric matrices: row-major == column-major
   const char *dense = getenv("KS_PENCIL_DENSE");
-  const bool filtered = !(dense && dense[0] == '1') && k <= 64 && k + EF_GUARD <= D / 2;
+  const bool filtered = !(dense && dense[0] == '1') && k <= ctx->max_N && k + EF_GUARD <= D / 2;
   const bool have_L = filtered && same_B && ctx->ef_L_D == D;
   KS_CUDA(ctx, cudaMemcpyAsync(ctx->eig_A, FA, sizeof(double) * D * D, cudaMemcpyDeviceToDevice, ctx->stream));
   if (!have_L)
     KS_CUDA(ctx, cudaMemcpyAsync(ctx->eig_B, FB, sizeof(double) * D * D, cudaMemcpyDeviceToDevice, ctx->stream));
   ctx->ef_L_D = 0;   // eig_B holds F_B (or L below)
-  if (!ctx->eig_info) KS_TRY(ks_alloc_t(ctx, &ctx->eig_info, 1, "pencil info"));
   // the filtered subspace iteration for the lowest k when the block is small against D (KS_PENCIL_DENSE=1:
   // always the dense cuSOLVER path below; it is also the fallback)
   if (filtered) {
@@ -525,11 +543,7 @@ ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, co
     if (cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, (int)D, ctx->eig_B, (int)D, &lw) !=
         CUSOLVER_STATUS_SUCCESS)
       return ks_fail(ctx, KS_E_CUDA, "cusolverDnDpotrf_bufferSize failed");
-    if (ctx->eig_work_cap < lw) {
-      ks_free_t(ctx, ctx->eig_work);
-      KS_TRY(ks_alloc_t(ctx, &ctx->eig_work, lw, "pencil workspace"));
-      ctx->eig_work_cap = lw;
-    }
+    if (lw > ctx->ext_lwork) return ks_fail(ctx, KS_E_WORKSPACE, "potrf workspace %d exceeds the ext plan", lw);
     if (cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, (int)D, ctx->eig_B, (int)D, ctx->eig_work, lw, ctx->eig_info) !=
         CUSOLVER_STATUS_SUCCESS)
       return ks_fail(ctx, KS_E_CUDA, "cusolverDnDpotrf failed");
@@ -564,12 +578,8 @@ ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, co
                                          (int)D, ctx->eig_A, (int)D, ctx->eig_B, (int)D, ctx->eig_w, &lwork) !=
              CUSOLVER_STATUS_SUCCESS)
     return ks_fail(ctx, KS_E_CUDA, "cusolverDnDsygvd_bufferSize failed (D = %lld)", (long long)D);
-  if (ctx->eig_work_cap < lwork) {
-    ks_free_t(ctx, ctx->eig_work);
-    KS_TRY(ks_alloc_t(ctx, &ctx->eig_work, lwork, "pencil workspace"));
-    ctx->eig_work_cap = lwork;
-  }
-  if (!ctx->eig_info) KS_TRY(ks_alloc_t(ctx, &ctx->eig_info, 1, "pencil info"));
+  if (lwork > ctx->ext_lwork)
+    return ks_fail(ctx, KS_E_WORKSPACE, "eigensolver workspace %d exceeds the ext plan", lwork);
   cusolverStatus_t cst;
   if (subset)
     cst = cusolverDnDsygvdx(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
@@ -609,21 +619,9 @@ ks_status ks_lift_impl(ks_ctx *ctx, int N, const double *Ut, int k, const double
 
 ks_status ks_augmented_solve_impl(ks_ctx *ctx, int N, double *lambda, double *U, double tol_eig, int max_outer,
                                   double tol_bvp, int32_t max_iter_bvp, int32_t *h_outer, double *h_history) {
-  const int64_t n = ctx->n_free, D = ctx->n_H + N;
-  if (ctx->outer_cap < n * N || ctx->outer_D < D) {
-    ks_free_t(ctx, ctx->outer_Ut);
-    ks_free_t(ctx, ctx->outer_FA);
-    ks_free_t(ctx, ctx->outer_FB);
-    ks_free_t(ctx, ctx->outer_Y);
-    ks_free_t(ctx, ctx->outer_lam);
-    KS_TRY(ks_alloc_t(ctx, &ctx->outer_Ut, n * N, "outer U~"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->outer_FA, D * D, "outer F_A"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->outer_FB, D * D, "outer F_B"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->outer_Y, D * N, "outer Y"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->outer_lam, N, "outer lambda"));
-    ctx->outer_cap = n * N;
-    ctx->outer_D = D;
-  }
+  const int64_t D = ctx->n_H + N;
+  if (!(ctx->ext_features & (KS_EXT_EIG | KS_EXT_SCF)) || N > ctx->max_N)
+    return ks_fail(ctx, KS_E_STATE, "ks_augmented_solve: attach an extension workspace planned with KS_EXT_EIG");
   std::vector<double> prev(N), cur(N);
   KS_CUDA(ctx, cudaMemcpyAsync(prev.data(), lambda, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
   KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));

@@ -20,6 +20,7 @@
 // sweeping front that stays L2-resident. The U/P chunk (VEC doubles per thread) is the
 // same row range as the S tile, so U and P touch only rows the block itself produced in S.
 #include "ks_internal.cuh"
+#include "ks_layout.cuh"
 #include "ks_rowops.cuh"
 #include "ks_sell.cuh"
 #include "ks_grid.cuh"
@@ -61,6 +62,7 @@ __device__ __forceinline__ void block_cols(double (&acc)[ND][VEC], double *red, 
 struct PcgArgs {
   const int32_t *sell_ptr, *sell_col;
   const double *A, *M, *dinv;   // A, M: sliced-ELL values
+  const double *dg;             // diag(A) [n] (fused kernel: r = d z)
   const double *lambda;
   double mu, tol;
   const double *U;      // [n][NP] input (possibly padded copy): u_i, and x0 (warm start)
@@ -78,12 +80,6 @@ struct PcgArgs {
   int trace_cap;
   int64_t n;
   int N, ntiles, max_iter;
-  // staged S phase (ks_stage.cu)
-  const int32_t *meta;        // [n_groups] KS_META_BYTES records
-  const uint16_t *slcol;      // [sell_total] local column of every slot
-  const uint16_t *dlc;        // [n] local index of the row itself
-  int64_t ngroups;
-  int stage_cap;              // staged rows per stage buffer
 };
 
 // out[j] = sum_{g < G} part[g*stride + j] for j < nv, fixed order, one warp per value.
@@ -98,136 +94,7 @@ __device__ __forceinline__ void reduce_partials(const double *part, int stride, 
   __syncthreads();
 }
 
-// ---- staged S phase: the p rows a group of GRP rows references are copied (bulk, TMA) into shared memory
-constexpr int PSTAGES = 3;
-constexpr int META_SLOT = 128;   // bytes reserved for the group record in a stage (KS_META_BYTES <= 128)
-
 template <int NP>
-struct SP {   // staged layout: 2 orbitals per lane (NP >= 4)
-  static constexpr int VEC = 2, LPR = NP >= 4 ? NP / 2 : 2, RPW = 32 / LPR, GRP = PCG_WARPS * RPW;
-  static_assert(GRP * NP == 1024, "group size of ks_stage_build");
-};
-
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// thread 0: copy the staged rows of consumption k (group g) into stage st, plus the record of group k + PSTAGES
-// (the producer reads records only from shared memory after the prologue). rec: the record of group g.
-template <int NP>
-__device__ __forceinline__ void issue_group(const PcgArgs &a, const int32_t *rec, int64_t g, int64_t g_next,
-                                            unsigned char *stage, uint64_t *bar, int *staged_flag) {
-  const int nruns = rec[0];
-  *staged_flag = nruns > 0;
-  unsigned bytes = nruns > 0 ? (unsigned)rec[1] * NP * 8u : 0u;
-  if (g_next >= 0) bytes += KS_META_BYTES;
-  if (bytes == 0) {
-    mbar_arrive(bar);
-    return;
-  }
-  mbar_expect_tx(bar, bytes);
-  double *buf = reinterpret_cast<double *>(stage + META_SLOT);
-  int off = 0;
-  for (int r = 0; r < nruns; r++) {
-    const int start = rec[4 + 2 * r], len = rec[5 + 2 * r];
-    bulk_g2s(buf + (int64_t)off * NP, a.p + (int64_t)start * NP, (unsigned)len * NP * 8u, bar);
-    off += len;
-  }
-  if (g_next >= 0) bulk_g2s(stage, a.meta + g_next * (KS_META_BYTES / 4), KS_META_BYTES, bar);
-}
-
-// q = A p for this CTA's groups, p.q partials in acc (staged layout); returns the consumptions done
-template <int NP>
-__device__ __forceinline__ void s_phase_staged(const PcgArgs &a, unsigned char *dyn, uint64_t *pbar, int *s_staged,
-                                               unsigned &pseq, double (&acc)[1][2]) {
-  constexpr int LPR = SP<NP>::LPR, RPW = SP<NP>::RPW, GRP = SP<NP>::GRP;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int slot = lane / LPR, sub = lane % LPR;
-  const int G = gridDim.x;
-  const int64_t n = a.n;
-  const size_t stage_bytes = META_SLOT + (size_t)a.stage_cap * NP * 8;
-  const int64_t my = a.ngroups > blockIdx.x ? (a.ngroups - blockIdx.x + G - 1) / G : 0;
-  auto stage_of = [&](unsigned q) { return dyn + (size_t)(q % PSTAGES) * stage_bytes; };
-  if (threadIdx.x == 0) {
-    // p was written by other CTAs before the grid barrier: order the bulk (async-proxy) reads after it
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    for (int k = 0; k < PSTAGES && k < my; k++) {
-      const int64_t g = blockIdx.x + (int64_t)k * G;
-      const int64_t gn = k + PSTAGES < my ? g + (int64_t)PSTAGES * G : -1;
-      const int32_t *rec = a.meta + g * (KS_META_BYTES / 4);
-      int32_t r[KS_META_BYTES / 4];
-      for (int x = 0; x < KS_META_BYTES / 4; x++) r[x] = __ldg(rec + x);
-      issue_group<NP>(a, r, g, gn, stage_of(pseq + k), &pbar[(pseq + k) % PSTAGES], &s_staged[(pseq + k) % PSTAGES]);
-    }
-  }
-  for (int64_t k = 0; k < my; k++) {
-    const unsigned q = pseq + (unsigned)k;
-    const int st = q % PSTAGES;
-    mbar_wait(&pbar[st], (q / PSTAGES) & 1u);
-    unsigned char *stage = stage_of(q);
-    const double *buf = reinterpret_cast<const double *>(stage + META_SLOT);
-    const int64_t g = blockIdx.x + k * G;
-    const int64_t row = g * GRP + warp * RPW + slot;
-    const bool staged = s_staged[st];
-    if (row < n) {
-      const int64_t sl = row / KS_SELL_C;
-      const int32_t b = __ldg(a.sell_ptr + sl), e = __ldg(a.sell_ptr + sl + 1);
-      const int groups = (e - b) / (4 * KS_SELL_C);
-      const int64_t base = b + (row % KS_SELL_C) * 4;
-      double q0 = 0.0, q1 = 0.0, p0, p1;
-      if (staged) {
-        for (int gg = 0; gg < groups; gg++) {
-          const int64_t o = base + (int64_t)gg * (4 * KS_SELL_C);
-          const ushort4 lc = __ldg(reinterpret_cast<const ushort4 *>(a.slcol + o));
-          double w0, w1, w2, w3;
-          ldnc_v4(a.A + o, w0, w1, w2, w3);
-          const double2 x0 = *reinterpret_cast<const double2 *>(buf + (int64_t)lc.x * NP + 2 * sub);
-          const double2 x1 = *reinterpret_cast<const double2 *>(buf + (int64_t)lc.y * NP + 2 * sub);
-          const double2 x2 = *reinterpret_cast<const double2 *>(buf + (int64_t)lc.z * NP + 2 * sub);
-          const double2 x3 = *reinterpret_cast<const double2 *>(buf + (int64_t)lc.w * NP + 2 * sub);
-          q0 = fma(w0, x0.x, q0); q1 = fma(w0, x0.y, q1);
-          q0 = fma(w1, x1.x, q0); q1 = fma(w1, x1.y, q1);
-          q0 = fma(w2, x2.x, q0); q1 = fma(w2, x2.y, q1);
-          q0 = fma(w3, x3.x, q0); q1 = fma(w3, x3.y, q1);
-        }
-        const double2 pv = *reinterpret_cast<const double2 *>(buf + (int64_t)__ldg(a.dlc + row) * NP + 2 * sub);
-        p0 = pv.x; p1 = pv.y;
-      } else {   // group too irregular to stage: gathers from global memory
-        for (int gg = 0; gg < groups; gg++) {
-          const int64_t o = base + (int64_t)gg * (4 * KS_SELL_C);
-          const int4 c = __ldg(reinterpret_cast<const int4 *>(a.sell_col + o));
-          double w0, w1, w2, w3;
-          ldnc_v4(a.A + o, w0, w1, w2, w3);
-          const double2 x0 = *reinterpret_cast<const double2 *>(a.p + (int64_t)c.x * NP + 2 * sub);
-          const double2 x1 = *reinterpret_cast<const double2 *>(a.p + (int64_t)c.y * NP + 2 * sub);
-          const double2 x2 = *reinterpret_cast<const double2 *>(a.p + (int64_t)c.z * NP + 2 * sub);
-          const double2 x3 = *reinterpret_cast<const double2 *>(a.p + (int64_t)c.w * NP + 2 * sub);
-          q0 = fma(w0, x0.x, q0); q1 = fma(w0, x0.y, q1);
-          q0 = fma(w1, x1.x, q0); q1 = fma(w1, x1.y, q1);
-          q0 = fma(w2, x2.x, q0); q1 = fma(w2, x2.y, q1);
-          q0 = fma(w3, x3.x, q0); q1 = fma(w3, x3.y, q1);
-        }
-        const double2 pv = *reinterpret_cast<const double2 *>(a.p + row * NP + 2 * sub);
-        p0 = pv.x; p1 = pv.y;
-      }
-      acc[0][0] += p0 * q0;
-      acc[0][1] += p1 * q1;
-      *reinterpret_cast<double2 *>(a.q + row * NP + 2 * sub) = make_double2(q0, q1);
-    }
-    __syncthreads();   // every warp is done with stage st
-    if (threadIdx.x == 0 && k + PSTAGES < my) {
-      int32_t r[KS_META_BYTES / 4];
-      const int32_t *rec = reinterpret_cast<const int32_t *>(stage);   // arrived with consumption k
-      for (int x = 0; x < KS_META_BYTES / 4; x++) r[x] = rec[x];
-      const int64_t g2 = g + (int64_t)PSTAGES * G;
-      const int64_t gn = k + 2 * PSTAGES < my ? g2 + (int64_t)PSTAGES * G : -1;
-      issue_group<NP>(a, r, g2, gn, stage, &pbar[st], &s_staged[st]);
-    }
-  }
-  pseq += (unsigned)my;
-}
-
-template <int NP, bool STAGEP>
 __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs a) {
   constexpr int VEC = SL<NP, PCG_THREADS>::VEC, LPR = SL<NP, PCG_THREADS>::LPR, RPW = SL<NP, PCG_THREADS>::RPW, TILE = SL<NP, PCG_THREADS>::TILE;
   constexpr int CHUNK = SL<NP, PCG_THREADS>::CHUNK;
@@ -238,10 +105,6 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
   __shared__ double s_alpha[NP], s_beta[NP], s_rho[NP], s_bnorm[NP], s_rr[NP];
   __shared__ int s_active[NP], s_conv[NP], s_iters[NP];
   __shared__ int s_any;
-  __shared__ __align__(8) uint64_t s_pbar[PSTAGES];
-  __shared__ int s_staged[PSTAGES];
-  extern __shared__ __align__(128) unsigned char dyn[];
-  unsigned pseq = 0;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int slot = lane / LPR, sub = lane % LPR;
@@ -260,13 +123,6 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
     }
   };
   stamp();
-  if constexpr (STAGEP) {
-    if (threadIdx.x == 0) {
-      for (int st = 0; st < PSTAGES; st++) mbar_init(&s_pbar[st], 1);
-      mbar_fence_init();
-    }
-    __syncthreads();
-  }
 
   // ---------------- init: b = (lambda+mu) M u, r = b - A u, x = u, z = r/d, p = z ----------------
   {
@@ -349,11 +205,7 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
     }
 
     // ---- S: q = A p, p.q ----
-    if constexpr (STAGEP) {
-      double acc[1][2] = {{0.0, 0.0}};
-      s_phase_staged<NP>(a, dyn, s_pbar, s_staged, pseq, acc);
-      block_cols<NP, 1, 2, NP / 2>(acc, red, tot);
-    } else {
+    {
       double acc[1][VEC];
 #pragma unroll
       for (int v = 0; v < VEC; v++) acc[0][v] = 0.0;
@@ -496,6 +348,308 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
   }
 }
 
+
+// L2 prefetch of the streamed operands of a warp's rows one tile ahead (cp.async.bulk.prefetch: no register,
+// no L1 wavefront; the later loads hit L2): the sliced-ELL values and columns of its slice and, in the fused S
+// phase, its row segments of q, p and x. Sizes are multiples of 16 bytes for NP >= 4 (KS_PCG_PREFETCH=0: off).
+#ifndef KS_PCG_PREFETCH
+#define KS_PCG_PREFETCH 1
+#endif
+__device__ __forceinline__ void l2_prefetch(const void *ptr, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
+}
+template <int NP, int RPW>
+__device__ __forceinline__ void prefetch_rows(const PcgArgs &a, int64_t row0, const double *xin, bool streams) {
+  if (row0 >= a.n) return;
+  const int64_t rows = min((int64_t)RPW, a.n - row0);
+  const int32_t e0 = __ldg(a.sell_ptr + row0 / KS_SELL_C), e1 = __ldg(a.sell_ptr + (row0 + rows - 1) / KS_SELL_C + 1);
+  l2_prefetch(a.A + e0, (unsigned)(e1 - e0) * 8u);
+  l2_prefetch(a.sell_col + e0, (unsigned)(e1 - e0) * 4u);
+  if (streams) {
+    const unsigned vb = (unsigned)(rows * NP * 8);
+    l2_prefetch(a.q + row0 * NP, vb);
+    l2_prefetch(a.p + row0 * NP, vb);
+    l2_prefetch(xin + row0 * NP, vb);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Fused two-phase iteration (the default for the BVPs, KS_PCG_FUSED=0 selects the three-phase kernel above).
+// z = D^-1 r is stored instead of r, and q = A p is carried by the recurrence
+//     q_{k+1} = A z_{k+1} + beta_k q_k        (p_{k+1} = z_{k+1} + beta_k p_k, exact-arithmetic identical)
+// so that neither the p update nor the x update needs its own pass: both run inside the SpMM pass, on the rows
+// the pass produces, while the gathers of z keep the load/store unit busy:
+//   S  w = A z (gathered), q = w + beta q, p' = z + beta p, x += alpha_prev p, partials p'.q     | barrier
+//   U  z -= alpha D^-1 q, partials d z^2 (= r.z) and d^2 z^2 (= r.r)                            | barrier
+// The same 10 vector touches per iteration as the three-phase form, one grid barrier fewer. The deferred
+// x_{k+1} = x_k + alpha_k p_k of the last iteration runs in a final streaming pass. Per-column freezing,
+// NOT_SPD / NONFINITE / NOT_CONVERGED semantics and the fixed reduction order are those of k_block_pcg.
+template <int NP>
+__global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(PcgArgs a) {
+  constexpr int VEC = SL<NP, PCG_THREADS>::VEC, LPR = SL<NP, PCG_THREADS>::LPR, RPW = SL<NP, PCG_THREADS>::RPW,
+                TILE = SL<NP, PCG_THREADS>::TILE, CHUNK = SL<NP, PCG_THREADS>::CHUNK;
+  constexpr int STRIDE = 4 * NP;
+
+  __shared__ double red[PCG_WARPS * 3 * NP];
+  __shared__ double tot[3 * NP];
+  __shared__ double s_alpha[NP], s_xalpha[NP], s_beta[NP], s_rho[NP], s_bnorm[NP], s_rr[NP];
+  __shared__ int s_active[NP], s_iters[NP];
+  __shared__ int s_any;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = lane / LPR, sub = lane % LPR;
+  const int G = gridDim.x;
+  const int64_t n = a.n;
+  unsigned target = 0;
+  double *part_a = a.partials;                        // region 0: init (3 dots) / U (2 dots)
+  double *part_s = a.partials + (int64_t)G * STRIDE;  // region 1: S (1 dot)
+  double *Z = a.r;                                    // the r buffer holds z = D^-1 r
+  unsigned long long *trace = (a.trace && blockIdx.x == 0 && threadIdx.x == 0) ? a.trace : nullptr;
+  int ntr = 0;
+  auto stamp = [&]() {
+    if (trace && ntr < a.trace_cap) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[ntr++] = t;
+    }
+  };
+  stamp();
+
+  // ---------------- init: b = (lambda+mu) M u, r = b - A u, z = r / d, p = z (x = u stays implicit) ------------
+  {
+    double acc[3][VEC];
+#pragma unroll
+    for (int d = 0; d < 3; d++)
+#pragma unroll
+      for (int v = 0; v < VEC; v++) acc[d][v] = 0.0;
+    double sh[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; v++) {
+      const int c = sub * VEC + v;
+      sh[v] = (c < a.N ? __ldg(a.lambda + c) : 0.0) + a.mu;
+    }
+    for (int tile = blockIdx.x; tile < a.ntiles; tile += G) {
+      const int64_t row = (int64_t)tile * TILE + warp * RPW + slot;
+      if (row < n) {
+        DV<VEC> au, mu_;
+        sell_row<NP, 2>(a.sell_ptr, a.sell_col, a.A, a.M, row, a.U, sub, au, mu_);
+        const int64_t off = row * NP + sub * VEC;
+        const double dinv = __ldg(a.dinv + row);
+        DV<VEC> z;
+#pragma unroll
+        for (int v = 0; v < VEC; v++) {
+          const double b = sh[v] * mu_.v[v];
+          const double r = b - au.v[v];
+          z.v[v] = r * dinv;
+          acc[0][v] += b * b;
+          acc[1][v] += r * z.v[v];
+          acc[2][v] += r * r;
+        }
+        z.st(Z + off);
+        z.st(a.p + off);
+      }
+    }
+    block_cols<NP, 3>(acc, red, tot);
+    for (int i = threadIdx.x; i < 3 * NP; i += blockDim.x) part_a[(int64_t)blockIdx.x * STRIDE + i] = tot[i];
+    grid_barrier(a.bar, target);
+    stamp();
+    reduce_partials(part_a, STRIDE, 3 * NP, tot);
+    if (threadIdx.x < NP) {
+      const int c = threadIdx.x;
+      const double bn = sqrt(tot[c]), rz = tot[NP + c], rr = tot[2 * NP + c];
+      s_bnorm[c] = bn;
+      s_rho[c] = rz;
+      s_rr[c] = rr;
+      s_iters[c] = 0;
+      s_alpha[c] = 0.0;
+      s_xalpha[c] = 0.0;
+      s_beta[c] = 0.0;
+      const bool real = c < a.N;
+      const bool finite = isfinite(bn) && isfinite(rr) && isfinite(rz);
+      if (real && !finite && blockIdx.x == 0) atomicOr(a.flags, KSF_NONFINITE);
+      s_active[c] = real && finite && !(sqrt(rr) <= a.tol * bn);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int any = 0;
+      for (int c = 0; c < NP; c++) any |= s_active[c];
+      s_any = any;
+    }
+    __syncthreads();
+  }
+
+  int it = 0;
+  bool xwritten = false;   // x = u until the first deferred x update
+  const int64_t nel = n * NP;
+  const int nchunks = (int)((nel + CHUNK - 1) / CHUNK);
+  const int cb = (VEC * threadIdx.x) % NP;
+  if (s_any) {
+    for (bool first = true;; first = false) {
+      // ---- S: w = A z; q = w + beta q; p' = z + beta p; x += alpha_prev p; p'.q ----
+      {
+        double be[VEC], xa[VEC], acc[1][VEC];
+#pragma unroll
+        for (int v = 0; v < VEC; v++) {
+          be[v] = s_beta[sub * VEC + v];
+          xa[v] = s_xalpha[sub * VEC + v];
+          acc[0][v] = 0.0;
+        }
+        const double *xin = xwritten ? a.X : a.U;
+        constexpr bool PF = KS_PCG_PREFETCH && NP >= 4;
+        if (PF && lane == 0) prefetch_rows<NP, RPW>(a, (int64_t)blockIdx.x * TILE + warp * RPW, xin, !first);
+        for (int tile = blockIdx.x; tile < a.ntiles; tile += G) {
+          const int64_t row = (int64_t)tile * TILE + warp * RPW + slot;
+          if (PF && lane == 0) prefetch_rows<NP, RPW>(a, (int64_t)(tile + G) * TILE + warp * RPW, xin, !first);
+          if (row < n) {
+            DV<VEC> w, unused;
+            sell_row<NP, 1>(a.sell_ptr, a.sell_col, a.A, nullptr, row, Z, sub, w, unused);
+            const int64_t off = row * NP + sub * VEC;
+            if (first) {   // p = z (init), q = A p
+              const DV<VEC> pv = DV<VEC>::ld(a.p + off);
+#pragma unroll
+              for (int v = 0; v < VEC; v++) acc[0][v] += pv.v[v] * w.v[v];
+              w.st(a.q + off);
+            } else {
+              DV<VEC> qv = DV<VEC>::ld(a.q + off), pv = DV<VEC>::ld(a.p + off);
+              const DV<VEC> zv = DV<VEC>::ld(Z + off);
+              DV<VEC> xv = DV<VEC>::ld(xin + off);
+#pragma unroll
+              for (int v = 0; v < VEC; v++) {
+                xv.v[v] += xa[v] * pv.v[v];
+                pv.v[v] = zv.v[v] + be[v] * pv.v[v];
+                qv.v[v] = w.v[v] + be[v] * qv.v[v];
+                acc[0][v] += pv.v[v] * qv.v[v];
+              }
+              qv.st(a.q + off);
+              pv.st(a.p + off);
+              xv.st(a.X + off);
+            }
+          }
+        }
+        if (!first) xwritten = true;
+        block_cols<NP, 1>(acc, red, tot);
+        for (int i = threadIdx.x; i < NP; i += blockDim.x) part_s[(int64_t)blockIdx.x * STRIDE + i] = tot[i];
+        grid_barrier(a.bar, target);
+        stamp();
+        reduce_partials(part_s, STRIDE, NP, tot);
+        if (threadIdx.x < NP) {
+          const int c = threadIdx.x;
+          double al = 0.0;
+          if (s_active[c]) {
+            const double pq = tot[c];
+            if (!(pq > 0.0)) {
+              if (blockIdx.x == 0) atomicOr(a.flags, isfinite(pq) ? KSF_NOT_SPD : KSF_NONFINITE);
+              s_active[c] = 0;
+            } else {
+              al = s_rho[c] / pq;
+            }
+          }
+          s_alpha[c] = al;
+          s_xalpha[c] = al;   // applied to x with this p in the next S pass (or the final pass)
+        }
+        __syncthreads();
+      }
+
+      // ---- U: z -= alpha D^-1 q; r.z = d z^2, r.r = (d z)^2 ----
+      {
+        double al[VEC], acc[2][VEC];
+#pragma unroll
+        for (int v = 0; v < VEC; v++) {
+          al[v] = s_alpha[cb + v];
+          acc[0][v] = acc[1][v] = 0.0;
+        }
+        for (int ch = blockIdx.x; ch < nchunks; ch += G) {
+          const int64_t e = (int64_t)ch * CHUNK + VEC * threadIdx.x;
+          if (e < nel) {
+            DV<VEC> z = DV<VEC>::ld(Z + e);
+            const DV<VEC> q = DV<VEC>::ld(a.q + e);
+            const double di = __ldg(a.dinv + e / NP), dd = __ldg(a.dg + e / NP);
+#pragma unroll
+            for (int v = 0; v < VEC; v++) {
+              z.v[v] -= al[v] * (q.v[v] * di);
+              const double r = dd * z.v[v];
+              acc[0][v] += r * z.v[v];
+              acc[1][v] += r * r;
+            }
+            z.st(Z + e);
+          }
+        }
+        block_cols<NP, 2>(acc, red, tot);
+        for (int i = threadIdx.x; i < 2 * NP; i += blockDim.x) part_a[(int64_t)blockIdx.x * STRIDE + i] = tot[i];
+        grid_barrier(a.bar, target);
+        stamp();
+        reduce_partials(part_a, STRIDE, 2 * NP, tot);
+        if (threadIdx.x < NP) {
+          const int c = threadIdx.x;
+          double be = 0.0;
+          if (s_active[c]) {
+            const double rz = tot[c], rr = tot[NP + c];
+            s_iters[c] += 1;
+            bool conv;
+            if (!isfinite(rz) || !isfinite(rr)) {
+              if (blockIdx.x == 0) atomicOr(a.flags, KSF_NONFINITE);
+              conv = true;
+            } else {
+              be = rz / s_rho[c];
+              s_rho[c] = rz;
+              s_rr[c] = rr;
+              conv = sqrt(rr) <= a.tol * s_bnorm[c];
+            }
+            if (conv) {
+              be = 0.0;
+              s_active[c] = 0;
+            }
+          }
+          s_beta[c] = be;
+        }
+        __syncthreads();
+        it++;
+        if (threadIdx.x == 0) {
+          int any = 0;
+          for (int c = 0; c < NP; c++) any |= s_active[c];
+          s_any = any;
+        }
+        __syncthreads();
+        if (!s_any) break;
+        if (it >= a.max_iter) {
+          if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(a.flags, KSF_NOT_CONVERGED);
+          break;
+        }
+      }
+    }
+  }
+
+  // ---- final: the deferred x_{k+1} = x_k + alpha_k p_k (x = u when no iteration ran) ----
+  {
+    double xa[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; v++) xa[v] = s_xalpha[cb + v];
+    const double *xin = xwritten ? a.X : a.U;
+    for (int ch = blockIdx.x; ch < nchunks; ch += G) {
+      const int64_t e = (int64_t)ch * CHUNK + VEC * threadIdx.x;
+      if (e < nel) {
+        DV<VEC> x = DV<VEC>::ld(xin + e);
+        if (it > 0) {
+          const DV<VEC> pv = DV<VEC>::ld(a.p + e);
+#pragma unroll
+          for (int v = 0; v < VEC; v++) x.v[v] += xa[v] * pv.v[v];
+        }
+        x.st(a.X + e);
+      }
+    }
+  }
+  if (blockIdx.x == 0) {
+    for (int c = threadIdx.x; c < a.N; c += blockDim.x) {
+      if (a.iters_out) a.iters_out[c] = s_iters[c];
+      if (a.relres_out) a.relres_out[c] = s_bnorm[c] > 0.0 ? sqrt(s_rr[c]) / s_bnorm[c] : sqrt(s_rr[c]);
+    }
+    if (threadIdx.x == 0) {
+      *a.block_iters_out = it;
+      if (a.trace_count) *a.trace_count = ntr;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------------------------
 // standalone multi-RHS SpMM on the sliced-ELL copy (A, M): parity helper and benchmark of phase S
 // ---------------------------------------------------------------------------------------------
@@ -528,61 +682,31 @@ __global__ void __launch_bounds__(256) k_spmm(const int32_t *__restrict__ row_pt
   y.store(Y + row * NP + sub * VEC);
 }
 
-template <int NP, bool STAGEP>
-ks_status launch_pcg_t(ks_ctx *ctx, PcgArgs &a, size_t dyn) {
-  auto kern = k_block_pcg<NP, STAGEP>;
-  if (dyn > 0) KS_CUDA(ctx, cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+template <int NP, bool FUSED>
+ks_status launch_pcg_t(ks_ctx *ctx, PcgArgs &a) {
+  auto kern = FUSED ? k_block_pcg_fused<NP> : k_block_pcg<NP>;
   int per_sm = 0;
-  KS_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PCG_THREADS, dyn));
-  if (per_sm < 1) return ks_fail(ctx, KS_E_CUDA, "k_block_pcg<%d,%d> cannot be resident", NP, (int)STAGEP);
+  KS_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PCG_THREADS, 0));
+  if (per_sm < 1) return ks_fail(ctx, KS_E_CUDA, "k_block_pcg<%d> cannot be resident", NP);
+  if (per_sm > KS_PCG_GMAX_PER_SM) per_sm = KS_PCG_GMAX_PER_SM;   // the partials are planned for this many
   int G = per_sm * ctx->sm_count;
   if (G > a.ntiles) G = a.ntiles;
-  if ((int64_t)G * 4 * NP * 2 > ctx->partial_cap) {
-    ks_free_t(ctx, ctx->partials);
-    ctx->partial_cap = (int64_t)G * 4 * NP * 2;
-    KS_TRY(ks_alloc_t(ctx, &ctx->partials, ctx->partial_cap, "pcg partials"));
-  }
   a.partials = ctx->partials;
   KS_CUDA(ctx, cudaMemsetAsync(ctx->barrier, 0, sizeof(unsigned), ctx->stream));
   void *args[] = {&a};
-  KS_CUDA(ctx, cudaLaunchCooperativeKernel((const void *)kern, dim3(G), dim3(PCG_THREADS), args, dyn, ctx->stream));
+  KS_CUDA(ctx, cudaLaunchCooperativeKernel((const void *)kern, dim3(G), dim3(PCG_THREADS), args, 0, ctx->stream));
   ctx->launches++;
   return KS_OK;
 }
 
-// Staged S phase (opt-in, KS_PCG_STAGE=1): for NP >= 4 when the group tables fit three stages of shared
-// memory. Measured slower on the lexicographically numbered meshes (C4: S 471 us vs 296 us gathering,
-// r01ad): a 64-row group references ~7 runs of ~66 rows, so each p row is copied into ~7 stage buffers and
-// the L2 -> shared traffic (7.2x the vector per S phase) saturates L2, while L1 gathers hit ~50 %. It needs
-// 3-D-local row groups to pay off.
-constexpr size_t PSTAGE_SMEM_MAX = 200 * 1024;
-
 template <int NP>
 ks_status launch_pcg(ks_ctx *ctx, PcgArgs &a) {
   a.ntiles = (int)((a.n + SL<NP, PCG_THREADS>::TILE - 1) / SL<NP, PCG_THREADS>::TILE);
-  a.meta = nullptr;
-  a.slcol = nullptr;
-  a.dlc = nullptr;
-  a.ngroups = 0;
-  a.stage_cap = 0;
-  const char *env = getenv("KS_PCG_STAGE");
-  const bool want = NP >= 4 && env && env[0] == '1';
-  if constexpr (NP >= 4 && PCG_THREADS == 512) {   // the staged layout assumes 512 threads (SP<NP>)
-    if (want) {
-      const int max_rows = (int)((PSTAGE_SMEM_MAX / PSTAGES - META_SLOT) / (NP * 8));
-      KS_TRY(ks_stage_build(ctx, NP, max_rows));
-      if (ctx->stage_staged > 0) {
-        a.meta = ctx->stage_meta;
-        a.slcol = ctx->stage_slcol;
-        a.dlc = ctx->stage_dlc;
-        a.ngroups = ctx->stage_groups;
-        a.stage_cap = ctx->stage_cap;
-        const size_t dyn = (size_t)PSTAGES * (META_SLOT + (size_t)ctx->stage_cap * NP * 8);
-        return launch_pcg_t<NP, true>(ctx, a, dyn);
-      }
-    }
-  }
-  return launch_pcg_t<NP, false>(ctx, a, 0);
+  // the fused two-phase kernel serves the BVPs (right-hand side (lambda + mu) M u); the Poisson mode of the
+  // Hartree solve (given B, up to ~10^3 iterations to 1e-12) keeps the three-phase recurrences
+  const char *fz = getenv("KS_PCG_FUSED");
+  if (!a.B && !(fz && fz[0] == '0')) return launch_pcg_t<NP, true>(ctx, a);
+  return launch_pcg_t<NP, false>(ctx, a);
 }
 
 template <int NP>
@@ -625,41 +749,41 @@ __global__ void k_unpad(const double *__restrict__ src, int NP, double *__restri
   dst[gl] = src[(gl / N) * NP + gl % N];
 }
 
-// true residual partials: per block sums of b^2 and (b - A ut)^2 per column (generic layout)
+// true residual partials: per block sums of b^2 and (b - A ut)^2 per column (generic layout). A block of
+// R * N threads covers a contiguous row range; thread t owns column t % N and every R-th row; the per-column
+// sums are combined in a fixed order (deterministic, no atomics).
 __global__ void k_true_residual(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                                 const double *__restrict__ A, const double *__restrict__ M,
                                 const double *__restrict__ lambda, double mu, const double *__restrict__ U,
                                 const double *__restrict__ Ut, int64_t n, int N, double *__restrict__ part) {
-  // one thread per (row, column); block handles a contiguous range; partial per block per column
-  extern __shared__ double sh[];  // [2][blockDim]
-  const int64_t gl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  __shared__ double sb[256], sr[256];
+  const int R = blockDim.x / N;
+  const int c = threadIdx.x % N, rs = threadIdx.x / N;
+  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = blockIdx.x * chunk, r1 = min(n, r0 + chunk);
   double bb = 0.0, rr = 0.0;
-  int c = -1;
-  if (gl < n * N) {
-    const int64_t row = gl / N;
-    c = (int)(gl % N);
-    double mu_ = 0.0, au = 0.0;
-    for (int32_t k = row_ptr[row]; k < row_ptr[row + 1]; k++) {
-      mu_ = fma(M[k], U[(int64_t)col[k] * N + c], mu_);
-      au = fma(A[k], Ut[(int64_t)col[k] * N + c], au);
+  if (rs < R)
+    for (int64_t row = r0 + rs; row < r1; row += R) {
+      double mu_ = 0.0, au = 0.0;
+      for (int32_t k = row_ptr[row]; k < row_ptr[row + 1]; k++) {
+        mu_ = fma(M[k], U[(int64_t)col[k] * N + c], mu_);
+        au = fma(A[k], Ut[(int64_t)col[k] * N + c], au);
+      }
+      const double b = (lambda[c] + mu) * mu_;
+      bb += b * b;
+      rr += (b - au) * (b - au);
     }
-    double b = (lambda[c] + mu) * mu_;
-    bb = b * b;
-    rr = (b - au) * (b - au);
-  }
-  sh[threadIdx.x] = bb;
-  sh[blockDim.x + threadIdx.x] = rr;
+  sb[threadIdx.x] = bb;
+  sr[threadIdx.x] = rr;
   __syncthreads();
-  // column-wise sums in fixed order by thread 0..N-1
-  for (int cc = threadIdx.x; cc < N; cc += blockDim.x) {
-    double sb = 0.0, sr = 0.0;
-    const int64_t first = blockIdx.x * (int64_t)blockDim.x;
-    for (int t = 0; t < (int)blockDim.x; t++) {
-      const int64_t g = first + t;
-      if (g < n * N && (int)(g % N) == cc) { sb += sh[t]; sr += sh[blockDim.x + t]; }
+  if (threadIdx.x < N) {
+    double tb = 0.0, tr = 0.0;
+    for (int q = 0; q < R; q++) {
+      tb += sb[q * N + threadIdx.x];
+      tr += sr[q * N + threadIdx.x];
     }
-    part[(int64_t)blockIdx.x * 2 * N + cc] = sb;
-    part[(int64_t)blockIdx.x * 2 * N + N + cc] = sr;
+    part[(int64_t)blockIdx.x * 2 * N + threadIdx.x] = tb;
+    part[(int64_t)blockIdx.x * 2 * N + N + threadIdx.x] = tr;
   }
 }
 
@@ -702,22 +826,6 @@ ks_status ks_spmm_impl(ks_ctx *ctx, ks_op op, const double *val, int N, const do
   return KS_OK;
 }
 
-static ks_status ensure_solver_ws(ks_ctx *ctx, int np) {
-  if (ctx->ws_np >= np && ctx->ws_rows == ctx->n_free) return KS_OK;
-  for (double **b : {&ctx->r, &ctx->p, &ctx->q, &ctx->xpad, &ctx->upad, &ctx->bpad})
-    ks_free_t(ctx, *b);
-  const int64_t cnt = ctx->n_free * (int64_t)np;
-  KS_TRY(ks_alloc_t(ctx, &ctx->r, cnt, "pcg r"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->p, cnt, "pcg p"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->q, cnt, "pcg q"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->xpad, cnt, "pcg x pad"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->upad, cnt, "pcg u pad"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->bpad, cnt, "pcg b pad"));
-  ctx->ws_np = np;
-  ctx->ws_rows = ctx->n_free;
-  return KS_OK;
-}
-
 ks_status ks_solve_impl(ks_ctx *ctx, int N, const double *lambda, const double *U, double *Ut, double tol,
                         int max_iter, int32_t *iters, double *relres) {
   return ks_pcg_run(ctx, ctx->sell_A, ctx->dinv, ctx->mu, N, lambda, nullptr, U, Ut, tol, max_iter, iters, relres);
@@ -729,7 +837,8 @@ ks_status ks_pcg_run(ks_ctx *ctx, const double *sell_vals, const double *dinv, d
                      const double *lambda, const double *B, const double *U, double *Ut, double tol, int max_iter,
                      int32_t *iters, double *relres) {
   const int np = pad_np(N);
-  KS_TRY(ensure_solver_ws(ctx, np));
+  if (N > ctx->max_N)
+    return ks_fail(ctx, KS_E_ARG, "N = %d exceeds the max_N = %d the workspace was planned for", N, ctx->max_N);
   const int64_t n = ctx->n_free;
   const bool direct = (np == N) && aligned32(U) && aligned32(Ut) && (!B || aligned32(B));
   const double *u = U, *bb = B;
@@ -751,6 +860,7 @@ ks_status ks_pcg_run(ks_ctx *ctx, const double *sell_vals, const double *dinv, d
   a.A = sell_vals;
   a.M = ctx->sell_M;
   a.dinv = dinv;
+  a.dg = ctx->diag;
   a.lambda = lambda;
   a.mu = mu;
   a.tol = tol;
@@ -770,10 +880,6 @@ ks_status ks_pcg_run(ks_ctx *ctx, const double *sell_vals, const double *dinv, d
   a.trace_cap = 0;
   const char *tr = getenv("KS_PCG_TRACE");
   if (tr && tr[0] == '1') {
-    if (!ctx->trace) {
-      KS_TRY(ks_alloc_t(ctx, &ctx->trace, KS_TRACE_CAP, "pcg trace"));
-      KS_TRY(ks_alloc_t(ctx, &ctx->trace_count, 1, "pcg trace count"));
-    }
     a.trace = ctx->trace;
     a.trace_count = ctx->trace_count;
     a.trace_cap = KS_TRACE_CAP;
@@ -800,17 +906,17 @@ ks_status ks_pcg_run(ks_ctx *ctx, const double *sell_vals, const double *dinv, d
 
 ks_status ks_true_residual_impl(ks_ctx *ctx, int N, const double *lambda, const double *U, const double *Ut,
                                 double *relres) {
-  const int64_t total = ctx->n_free * N;
-  const int T = 256;
-  const int nblk = ks_blocks(total, T);
+  if (N > ctx->max_N) return ks_fail(ctx, KS_E_ARG, "N = %d exceeds max_N = %d", N, ctx->max_N);
+  const int T = (256 / N) * N;
+  const int nblk = 4 * ctx->sm_count;
+  KsScratch scratch(ctx, KS_R_WORK);
   double *part = nullptr;
-  KS_CUDA(ctx, cudaMallocAsync((void **)&part, sizeof(double) * 2 * N * (size_t)nblk, ctx->stream));
+  KS_TRY(ks_alloc_t(ctx, &part, (int64_t)2 * N * nblk, "true residual partials"));
   KS_TRY(ks_materialize_views(ctx));
-  k_true_residual<<<nblk, T, 2 * T * sizeof(double), ctx->stream>>>(ctx->row_ptr, ctx->col, ctx->A, ctx->M, lambda,
-                                                                     ctx->mu, U, Ut, ctx->n_free, N, part);
+  k_true_residual<<<nblk, T, 0, ctx->stream>>>(ctx->row_ptr, ctx->col, ctx->A, ctx->M, lambda, ctx->mu, U, Ut,
+                                                ctx->n_free, N, part);
   KS_LAUNCHED(ctx);
   k_true_residual_final<<<1, 64, 0, ctx->stream>>>(part, nblk, N, relres);
   KS_LAUNCHED(ctx);
-  KS_CUDA(ctx, cudaFreeAsync(part, ctx->stream));
   return KS_OK;
 }

@@ -16,12 +16,13 @@
 
 #include "ks_grid.cuh"
 #include "ks_internal.cuh"
+#include "ks_layout.cuh"
 #include "ks_sell.cuh"
 
 namespace {
 
 constexpr int T2 = 512, W2 = T2 / 32;
-constexpr int NSLOT = 8;   // block partial slots: 0 S, 1-2 U, 3 C2, 4-6 init
+constexpr int NSLOT = KS_EXT_NSLOT2L;   // block partial slots: 0 S, 1-2 U, 3 C2, 4-6 init
 
 struct P2Args {
   const int32_t *sell_ptr, *sell_col;
@@ -319,28 +320,17 @@ __global__ void __launch_bounds__(T2, KS_P2_MINB) k_pcg2l(P2Args a) {
 
 }  // namespace
 
-void ks_free_pcg2l(ks_ctx *ctx) {
-  for (double **b : {&ctx->har2l_KHinv, &ctx->har2l_rpart, &ctx->har2l_rH, &ctx->har2l_y, &ctx->har2l_r,
-                     &ctx->har2l_r2, &ctx->har2l_p, &ctx->har2l_q, &ctx->har2l_part})
-    ks_free_t(ctx, *b);
-  ks_free_t(ctx, ctx->har2l_Pc4);
-  ctx->har2l_state = 0;
-}
+void ks_free_pcg2l(ks_ctx *ctx) { ctx->har2l_state = 0; }
 
 // K_H^-1 and the work vectors for the current coarse space (once per ks_set_coarse)
 static ks_status pcg2l_setup(ks_ctx *ctx) {
   if (ctx->har2l_state != 0) return KS_OK;
+  // the tables live in the extension workspace (ks_layout_ext), planned for the current coarse space
+  if (ctx->ext_nH != ctx->n_H || !ctx->har2l_KHinv) {
+    ctx->har2l_state = -1;
+    return KS_OK;
+  }
   const int64_t n = ctx->n_free, nH = ctx->n_H;
-  KS_TRY(ks_alloc_t(ctx, &ctx->har2l_KHinv, nH * nH, "K_H^-1"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->har2l_rpart, 4 * ctx->n_items, "restriction partials"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->har2l_rH, nH, "r_H"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->har2l_y, nH, "y_H"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->har2l_r, n, "2l r"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->har2l_r2, n, "2l r'"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->har2l_p, n, "2l p"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->har2l_q, n, "2l q"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->har2l_part, (int64_t)NSLOT * 4 * ctx->sm_count, "2l partials"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->har2l_Pc4, 4 * n, "P columns 4-wide"));
   k_pc4<<<ks_blocks(n, 256), 256, 0, ctx->stream>>>(ctx->P_ptr, ctx->P_col, n, ctx->har2l_Pc4);
   KS_LAUNCHED(ctx);
   KS_TRY(ks_coarse_galerkin(ctx, ctx->sell_K, ctx->har2l_KHinv));

@@ -19,6 +19,7 @@
 #include <cudaTypedefs.h>
 
 #include "ks_internal.cuh"
+#include "ks_layout.cuh"
 #include "ks_rowops.cuh"
 #include "ks_sell.cuh"
 
@@ -965,14 +966,8 @@ ks_status launch_proj_yb(ks_ctx *ctx, int N, const double *u, double *FA, double
   constexpr bool GRAM = NP <= 32;
   const int grid = 2 * ctx->sm_count;
   const int nparts = grid * PBG_WARPS;
-  if (GRAM) {
-    const int64_t need = (int64_t)nparts * 2 * NP * NP;
-    if (ctx->gram_cap < need) {
-      ks_free_t(ctx, ctx->gram_part);
-      KS_TRY(ks_alloc_t(ctx, &ctx->gram_part, need, "gram partials"));
-      ctx->gram_cap = need;
-    }
-  }
+  if (GRAM && (int64_t)nparts * 2 * NP * NP > ctx->gram_cap)
+    return ks_fail(ctx, KS_E_WORKSPACE, "gram partials exceed the coarse plan");
   const size_t bsm = PBG_WARPS * PbgLayout<NP>::WARP_BYTES;
   if constexpr (NP == 8 || NP == 16 || NP == 32) {
     if (mma) {
@@ -1004,12 +999,8 @@ ks_status launch_proj_yb(ks_ctx *ctx, int N, const double *u, double *FA, double
     const int nblk = 2 * ctx->sm_count;
     const int64_t rows_per_blk = ((n + nblk - 1) / nblk + GR_ROWS - 1) / GR_ROWS * GR_ROWS;
     const int nb = (int)((n + rows_per_blk - 1) / rows_per_blk);
-    const int64_t need = (int64_t)nb * 2 * N * N;
-    if (ctx->gram_cap < need) {
-      ks_free_t(ctx, ctx->gram_part);
-      KS_TRY(ks_alloc_t(ctx, &ctx->gram_part, need, "gram partials"));
-      ctx->gram_cap = need;
-    }
+    if ((int64_t)nb * 2 * N * N > ctx->gram_cap)
+      return ks_fail(ctx, KS_E_WORKSPACE, "gram partials exceed the coarse plan");
     const int NQ = (N + 3) / 4 * 4, NT = NQ / 4;
     const int ntiles = 2 * NT * NT;
     if (ntiles > 512) return ks_fail(ctx, KS_E_ARG, "N = %d too large for the Gram kernel", N);
@@ -1038,16 +1029,16 @@ ks_status launch_final(ks_ctx *ctx, int N, int NP, double *FA, double *FB, int64
   return KS_OK;
 }
 
-struct TmpGuard {
-  std::vector<void *> p;
-  ~TmpGuard() { for (void *x : p) cudaFree(x); }
-};
-
-#define TMPA(ptr, count)                                                                       \
-  do {                                                                                         \
-    KS_CUDA(ctx, cudaMalloc((void **)&(ptr), sizeof(*(ptr)) * (size_t)((count) > 0 ? (count) : 1))); \
-    tg.p.push_back((void *)(ptr));                                                             \
-  } while (0)
+// gram partial slots of launch_proj_yb for any block width up to np_max (NP <= 32: one N x N pair per warp of
+// the item pass; NP = 64: one per row block of k_gram)
+int64_t proj_gram_cap(int sm_count, int np_max) {
+  int64_t cap = 0;
+  for (int np = 2; np <= np_max; np <<= 1) {
+    const int64_t c = np <= 32 ? (int64_t)2 * sm_count * PBG_WARPS * 2 * np * np : (int64_t)2 * sm_count * 2 * np * np;
+    cap = c > cap ? c : cap;
+  }
+  return cap;
+}
 
 }  // namespace
 
@@ -1060,21 +1051,28 @@ ks_status ks_coarse_galerkin(ks_ctx *ctx, const double *op_sell_vals, double *ou
 
 void ks_free_coarse(ks_ctx *ctx) {
   ks_free_pcg2l(ctx);
-  void *ptrs[] = {ctx->P_ptr, ctx->P_col, ctx->P_val, ctx->Pv4, ctx->Pv4p, ctx->pos_of_row, ctx->perm,
-
-                  ctx->item_ptr, ctx->item_S, ctx->item_D_ptr, ctx->item_D, ctx->slotmap, ctx->CT_ptr,
-                  ctx->CT_val, ctx->B_H, ctx->AH_part};
-  for (void *p : ptrs) ks_free(ctx, p);
   ctx->P_ptr = ctx->P_col = nullptr;
   ctx->P_val = ctx->Pv4 = ctx->Pv4p = nullptr;
   ctx->pos_of_row = nullptr;
   ctx->perm = ctx->item_ptr = ctx->item_S = ctx->item_D_ptr = ctx->item_D = ctx->CT_ptr = ctx->CT_val = nullptr;
   ctx->slotmap = nullptr;
   ctx->B_H = ctx->AH_part = nullptr;
+  ctx->Y_H = ctx->Y_M = ctx->proj_u = ctx->proj_up = ctx->bH_part = ctx->cH_part = ctx->gram_part = nullptr;
+  ctx->gram_cap = 0;
   ctx->n_H = 0;
 }
 
-ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, const int32_t *Pcol, const double *Pval) {
+static int proj_np(int max_N) {
+  const int np = ks_pow2_at_least(max_N);
+  return np < 2 ? 2 : np;
+}
+
+// The coarse space of (st5)-(st7): P copied, fine rows grouped by parent set into items, coarse windows,
+// slot map, coarse node -> item lists, cached B_H = P^T M P. The grouping runs in call scratch of the
+// workspace; plan_only stops once the item count and window total are known and returns the coarse region
+// size (ks_coarse_plan); otherwise the coarse layout is carved from the caller's coarse region.
+ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, const int32_t *Pcol, const double *Pval,
+                             bool plan_only, size_t *coarse_bytes) {
   cudaStream_t s = ctx->stream;
   const int64_t nf = ctx->n_free;
   if (n_H >= 55000) return ks_fail(ctx, KS_E_ARG, "n_H = %lld >= 55000 not supported (parent-set key)", (long long)n_H);
@@ -1083,34 +1081,27 @@ ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, cons
   KS_CUDA(ctx, cudaStreamSynchronize(s));
   const int64_t pn = h_pn;
   if (pn < 0 || pn > 4 * nf) return ks_fail(ctx, KS_E_ARG, "P row_ptr[n_free] = %lld out of range", (long long)pn);
-  ks_free_coarse(ctx);
-  ctx->p_nnz = pn;
-  KS_TRY(ks_alloc_t(ctx, &ctx->P_ptr, nf + 1, "P_ptr"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->P_col, pn, "P_col"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->P_val, pn, "P_val"));
-  KS_CUDA(ctx, cudaMemcpyAsync(ctx->P_ptr, Pptr, 4 * (nf + 1), cudaMemcpyDeviceToDevice, s));
-  KS_CUDA(ctx, cudaMemcpyAsync(ctx->P_col, Pcol, 4 * pn, cudaMemcpyDeviceToDevice, s));
-  KS_CUDA(ctx, cudaMemcpyAsync(ctx->P_val, Pval, 8 * pn, cudaMemcpyDeviceToDevice, s));
+  size_t cub_cap = 0;
+  if (ks_coarse_cub_bytes(nf, &cub_cap) != KS_OK) return ks_fail(ctx, KS_E_CUDA, "CUB temporary-size query failed");
 
-  TmpGuard tg;
-  unsigned long long *bad;
-  uint64_t *key, *key_sorted;
-  int32_t *rows, *flag, *gincl, *gfirst, *iflag, *iincl, *item_of_pos, *dcnt, *ct_key, *ct_key_sorted, *ct_val;
-  TMPA(bad, 1);
-  TMPA(key, nf);
-  TMPA(key_sorted, nf);
-  TMPA(rows, nf);
-  KS_TRY(ks_alloc_t(ctx, &ctx->perm, nf, "perm"));
-  KS_CUDA(ctx, cudaMemsetAsync(bad, 0xff, 8, s));
-  k_P_rows_keys<<<ks_blocks(nf, 256), 256, 0, s>>>(ctx->P_ptr, ctx->P_col, ctx->P_val, nf, n_H, pn, key, rows, bad);
+  KsScratch scratch(ctx, KS_R_WORK);
+  KsCoarseTemps t;
+  KsCarver cv(ctx);
+  ks_layout_coarse_temps_rows(cv, t, nf, pn, cub_cap);
+  KS_TRY(cv.st);
+  uint8_t *cub_tmp = t.cub;
+  KS_CUDA(ctx, cudaMemcpyAsync(t.P_ptr, Pptr, 4 * (nf + 1), cudaMemcpyDeviceToDevice, s));
+  KS_CUDA(ctx, cudaMemcpyAsync(t.P_col, Pcol, 4 * pn, cudaMemcpyDeviceToDevice, s));
+  KS_CUDA(ctx, cudaMemcpyAsync(t.P_val, Pval, 8 * pn, cudaMemcpyDeviceToDevice, s));
+  KS_CUDA(ctx, cudaMemsetAsync(t.bad, 0xff, 8, s));
+  k_P_rows_keys<<<ks_blocks(nf, 256), 256, 0, s>>>(t.P_ptr, t.P_col, t.P_val, nf, n_H, pn, t.key, t.rows, t.bad);
   KS_LAUNCHED(ctx);
   unsigned long long h_bad = 0;
-  KS_CUDA(ctx, cudaMemcpyAsync(&h_bad, bad, 8, cudaMemcpyDeviceToHost, s));
+  KS_CUDA(ctx, cudaMemcpyAsync(&h_bad, t.bad, 8, cudaMemcpyDeviceToHost, s));
   KS_CUDA(ctx, cudaStreamSynchronize(s));
   if (h_bad != ~0ull)
     return ks_fail(ctx, KS_E_ARG, "P row %llu invalid (more than 4 entries, repeated column, or column outside [0, n_H))", h_bad);
-  KS_TRY(ks_alloc_t(ctx, &ctx->Pv4, 4 * nf, "Pv4"));
-  k_pv4<<<ks_blocks(nf, 256), 256, 0, s>>>(ctx->P_ptr, ctx->P_val, nf, ctx->Pv4);
+  k_pv4<<<ks_blocks(nf, 256), 256, 0, s>>>(t.P_ptr, t.P_val, nf, t.Pv4);
   KS_LAUNCHED(ctx);
 
   // ---- group rows by parent set (stable: ascending row inside a group), cut into items ----
@@ -1120,121 +1111,119 @@ ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, cons
     end_bit = (int)ceil(bits) + 1;
     if (end_bit > 64) end_bit = 64;
   }
-  size_t tb = 0;
-  KS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key_sorted, rows, ctx->perm, (int)nf, 0, end_bit, s));
-  uint8_t *cub_tmp;
-  size_t cub_cap = tb;
-  TMPA(cub_tmp, cub_cap);
-  KS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(cub_tmp, tb, key, key_sorted, rows, ctx->perm, (int)nf, 0, end_bit, s));
+  size_t tb = cub_cap;
+  KS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(cub_tmp, tb, t.key, t.key_sorted, t.rows, t.perm, (int)nf, 0, end_bit, s));
   ctx->launches++;
-  KS_TRY(ks_alloc_t(ctx, &ctx->pos_of_row, nf, "pos_of_row"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->Pv4p, 4 * nf, "Pv4 (item order)"));
-  k_item_order<<<ks_blocks(nf, 256), 256, 0, s>>>(ctx->perm, ctx->Pv4, nf, ctx->pos_of_row, ctx->Pv4p);
+  k_item_order<<<ks_blocks(nf, 256), 256, 0, s>>>(t.perm, t.Pv4, nf, t.pos_of_row, t.Pv4p);
   KS_LAUNCHED(ctx);
-  TMPA(flag, nf);
-  TMPA(gincl, nf);
-  TMPA(gfirst, nf);
-  TMPA(iflag, nf);
-  TMPA(iincl, nf);
-  TMPA(item_of_pos, nf);
-  k_group_flags<<<ks_blocks(nf, 256), 256, 0, s>>>(key_sorted, nf, flag);
-  KS_LAUNCHED(ctx);
-  size_t need = 0;
-  KS_CUDA(ctx, cub::DeviceScan::InclusiveSum(nullptr, need, flag, gincl, (int)nf, s));
-  if (need > cub_cap) { cub_cap = need; TMPA(cub_tmp, cub_cap); }
-  tb = cub_cap;
-  KS_CUDA(ctx, cub::DeviceScan::InclusiveSum(cub_tmp, tb, flag, gincl, (int)nf, s));
-  ctx->launches++;
-  k_group_first<<<ks_blocks(nf, 256), 256, 0, s>>>(flag, gincl, nf, gfirst);
-  KS_LAUNCHED(ctx);
-  k_item_flags<<<ks_blocks(nf, 256), 256, 0, s>>>(gincl, gfirst, nf, iflag);
+  k_group_flags<<<ks_blocks(nf, 256), 256, 0, s>>>(t.key_sorted, nf, t.flag);
   KS_LAUNCHED(ctx);
   tb = cub_cap;
-  KS_CUDA(ctx, cub::DeviceScan::InclusiveSum(cub_tmp, tb, iflag, iincl, (int)nf, s));
+  KS_CUDA(ctx, cub::DeviceScan::InclusiveSum(cub_tmp, tb, t.flag, t.gincl, (int)nf, s));
+  ctx->launches++;
+  k_group_first<<<ks_blocks(nf, 256), 256, 0, s>>>(t.flag, t.gincl, nf, t.gfirst);
+  KS_LAUNCHED(ctx);
+  k_item_flags<<<ks_blocks(nf, 256), 256, 0, s>>>(t.gincl, t.gfirst, nf, t.iflag);
+  KS_LAUNCHED(ctx);
+  tb = cub_cap;
+  KS_CUDA(ctx, cub::DeviceScan::InclusiveSum(cub_tmp, tb, t.iflag, t.iincl, (int)nf, s));
   ctx->launches++;
   int32_t h_items = 0;
-  KS_CUDA(ctx, cudaMemcpyAsync(&h_items, iincl + nf - 1, 4, cudaMemcpyDeviceToHost, s));
+  KS_CUDA(ctx, cudaMemcpyAsync(&h_items, t.iincl + nf - 1, 4, cudaMemcpyDeviceToHost, s));
   KS_CUDA(ctx, cudaStreamSynchronize(s));
   const int64_t ni = h_items;
-  ctx->n_items = ni;
-  KS_TRY(ks_alloc_t(ctx, &ctx->item_ptr, ni + 1, "item_ptr"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->item_S, 4 * ni, "item_S"));
+  ks_layout_coarse_temps_items(cv, t, ni);
+  KS_TRY(cv.st);
   int32_t h_nf = (int32_t)nf;
-  KS_CUDA(ctx, cudaMemcpyAsync(ctx->item_ptr + ni, &h_nf, 4, cudaMemcpyHostToDevice, s));
-  k_item_ptr<<<ks_blocks(nf, 256), 256, 0, s>>>(iflag, iincl, nf, ctx->item_ptr, item_of_pos);
+  KS_CUDA(ctx, cudaMemcpyAsync(t.item_ptr + ni, &h_nf, 4, cudaMemcpyHostToDevice, s));
+  k_item_ptr<<<ks_blocks(nf, 256), 256, 0, s>>>(t.iflag, t.iincl, nf, t.item_ptr, t.item_of_pos);
   KS_LAUNCHED(ctx);
-  TMPA(ct_key, 4 * ni);
-  TMPA(ct_key_sorted, 4 * ni);
-  TMPA(ct_val, 4 * ni);
-  KS_TRY(ks_alloc_t(ctx, &ctx->CT_val, 4 * ni, "CT_val"));
-  k_item_S<<<ks_blocks(ni, 256), 256, 0, s>>>(ctx->item_ptr, ctx->perm, ctx->P_ptr, ctx->P_col, ni, ctx->item_S,
-                                              ct_key, ct_val, (int32_t)n_H);
+  k_item_S<<<ks_blocks(ni, 256), 256, 0, s>>>(t.item_ptr, t.perm, t.P_ptr, t.P_col, ni, t.item_S, t.ct_key, t.ct_val,
+                                              (int32_t)n_H);
   KS_LAUNCHED(ctx);
 
-  // ---- coarse windows D per item ----
-  TMPA(dcnt, ni + 1);
-  KS_TRY(ks_alloc_t(ctx, &ctx->item_D_ptr, ni + 1, "item_D_ptr"));
+  // ---- coarse windows D per item: sizes ----
   const size_t bsm = sizeof(unsigned) * (size_t)((n_H + 31) / 32);
   KS_CUDA(ctx, cudaFuncSetAttribute(k_item_D, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
-  k_item_D<<<(unsigned)ni, 256, bsm, s>>>(ctx->item_ptr, ctx->perm, ctx->row_ptr, ctx->col, ctx->P_ptr, ctx->P_col,
-                                          (int32_t)n_H, dcnt, nullptr, nullptr);
+  k_item_D<<<(unsigned)ni, 256, bsm, s>>>(t.item_ptr, t.perm, ctx->row_ptr, ctx->col, t.P_ptr, t.P_col, (int32_t)n_H,
+                                          t.dcnt, nullptr, nullptr);
   KS_LAUNCHED(ctx);
-  KS_CUDA(ctx, cudaMemsetAsync(dcnt + ni, 0, 4, s));
-  need = 0;
-  KS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, need, dcnt, ctx->item_D_ptr, (int)(ni + 1), s));
-  if (need > cub_cap) { cub_cap = need; TMPA(cub_tmp, cub_cap); }
+  KS_CUDA(ctx, cudaMemsetAsync(t.dcnt + ni, 0, 4, s));
   tb = cub_cap;
-  KS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(cub_tmp, tb, dcnt, ctx->item_D_ptr, (int)(ni + 1), s));
+  KS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(cub_tmp, tb, t.dcnt, t.item_D_ptr, (int)(ni + 1), s));
   ctx->launches++;
-  int *dmax_d;
-  TMPA(dmax_d, 1);
-  need = 0;
-  KS_CUDA(ctx, cub::DeviceReduce::Max(nullptr, need, dcnt, dmax_d, (int)ni, s));
-  if (need > cub_cap) { cub_cap = need; TMPA(cub_tmp, cub_cap); }
   tb = cub_cap;
-  KS_CUDA(ctx, cub::DeviceReduce::Max(cub_tmp, tb, dcnt, dmax_d, (int)ni, s));
+  KS_CUDA(ctx, cub::DeviceReduce::Max(cub_tmp, tb, t.dcnt, t.dmax, (int)ni, s));
   ctx->launches++;
   int32_t h_dtot = 0, h_dmax = 0;
-  KS_CUDA(ctx, cudaMemcpyAsync(&h_dtot, ctx->item_D_ptr + ni, 4, cudaMemcpyDeviceToHost, s));
-  KS_CUDA(ctx, cudaMemcpyAsync(&h_dmax, dmax_d, 4, cudaMemcpyDeviceToHost, s));
+  KS_CUDA(ctx, cudaMemcpyAsync(&h_dtot, t.item_D_ptr + ni, 4, cudaMemcpyDeviceToHost, s));
+  KS_CUDA(ctx, cudaMemcpyAsync(&h_dmax, t.dmax, 4, cudaMemcpyDeviceToHost, s));
   KS_CUDA(ctx, cudaStreamSynchronize(s));
   if (h_dmax > DMAX - 1)
     return ks_fail(ctx, KS_E_ARG, "an item touches %d coarse nodes (> %d): coarse mesh too fine for the fine mesh",
                    h_dmax, DMAX - 1);
+  KsCoarseSizes cs;
+  cs.nf = nf;
+  cs.nnz = ctx->nnz;
+  cs.pn = pn;
+  cs.ni = ni;
+  cs.dtot = h_dtot;
+  cs.nH = n_H;
+  cs.np = proj_np(ctx->max_N);
+  cs.gram = proj_gram_cap(ctx->sm_count, cs.np);
+  if (plan_only) {
+    KsSizer sz;
+    ks_layout_coarse(sz, ctx, cs);
+    *coarse_bytes = sz.bytes;
+    return KS_OK;
+  }
+
+  // ---- the coarse region: carve the layout, move the grouping arrays in, build the rest ----
+  ks_free_coarse(ctx);
+  ctx->reg[KS_R_COARSE].off = 0;
+  {
+    KsRegion rg(ctx, KS_R_COARSE);
+    KsCarver cc(ctx);
+    ks_layout_coarse(cc, ctx, cs);
+    KS_TRY(cc.st);
+  }
+  ctx->p_nnz = pn;
+  ctx->n_items = ni;
   ctx->d_total = h_dtot;
   ctx->d_max = h_dmax > 0 ? h_dmax : 1;
-  KS_TRY(ks_alloc_t(ctx, &ctx->item_D, h_dtot, "item_D"));
+  ctx->gram_cap = cs.gram;
+  KS_CUDA(ctx, cudaMemcpyAsync(ctx->P_ptr, t.P_ptr, 4 * (nf + 1), cudaMemcpyDeviceToDevice, s));
+  KS_CUDA(ctx, cudaMemcpyAsync(ctx->P_col, t.P_col, 4 * pn, cudaMemcpyDeviceToDevice, s));
+  KS_CUDA(ctx, cudaMemcpyAsync(ctx->P_val, t.P_val, 8 * pn, cudaMemcpyDeviceToDevice, s));
+  KS_CUDA(ctx, cudaMemcpyAsync(ctx->perm, t.perm, 4 * nf, cudaMemcpyDeviceToDevice, s));
+  KS_CUDA(ctx, cudaMemcpyAsync(ctx->Pv4, t.Pv4, 32 * nf, cudaMemcpyDeviceToDevice, s));
+  KS_CUDA(ctx, cudaMemcpyAsync(ctx->pos_of_row, t.pos_of_row, 4 * nf, cudaMemcpyDeviceToDevice, s));
+  KS_CUDA(ctx, cudaMemcpyAsync(ctx->Pv4p, t.Pv4p, 32 * nf, cudaMemcpyDeviceToDevice, s));
+  KS_CUDA(ctx, cudaMemcpyAsync(ctx->item_ptr, t.item_ptr, 4 * (ni + 1), cudaMemcpyDeviceToDevice, s));
+  KS_CUDA(ctx, cudaMemcpyAsync(ctx->item_S, t.item_S, 16 * ni, cudaMemcpyDeviceToDevice, s));
+  KS_CUDA(ctx, cudaMemcpyAsync(ctx->item_D_ptr, t.item_D_ptr, 4 * (ni + 1), cudaMemcpyDeviceToDevice, s));
   k_item_D<<<(unsigned)ni, 256, bsm, s>>>(ctx->item_ptr, ctx->perm, ctx->row_ptr, ctx->col, ctx->P_ptr, ctx->P_col,
                                           (int32_t)n_H, nullptr, ctx->item_D_ptr, ctx->item_D);
   KS_LAUNCHED(ctx);
-  KS_TRY(ks_alloc_t(ctx, &ctx->slotmap, 4 * ctx->nnz, "slotmap"));
-  k_slotmap<<<ks_blocks(nf, 128), 128, 0, s>>>(ctx->perm, item_of_pos, ctx->item_D_ptr, ctx->item_D, ctx->row_ptr,
+  k_slotmap<<<ks_blocks(nf, 128), 128, 0, s>>>(ctx->perm, t.item_of_pos, ctx->item_D_ptr, ctx->item_D, ctx->row_ptr,
                                                ctx->col, ctx->P_ptr, ctx->P_col, nf, ctx->slotmap);
   KS_LAUNCHED(ctx);
-
 
   // ---- coarse node -> items list (stable sort on the coarse id; pads sort last) ----
   int ct_bits = 1;
   while ((1ll << ct_bits) <= n_H) ct_bits++;
-  need = 0;
-  KS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(nullptr, need, ct_key, ct_key_sorted, ct_val, ctx->CT_val, (int)(4 * ni),
-                                               0, ct_bits, s));
-  if (need > cub_cap) { cub_cap = need; TMPA(cub_tmp, cub_cap); }
   tb = cub_cap;
-  KS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(cub_tmp, tb, ct_key, ct_key_sorted, ct_val, ctx->CT_val, (int)(4 * ni),
-                                               0, ct_bits, s));
+  KS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(cub_tmp, tb, t.ct_key, t.ct_key_sorted, t.ct_val, ctx->CT_val,
+                                               (int)(4 * ni), 0, ct_bits, s));
   ctx->launches++;
-  KS_TRY(ks_alloc_t(ctx, &ctx->CT_ptr, n_H + 1, "CT_ptr"));
-  k_lower_bound_ptr<<<ks_blocks(n_H + 1, 256), 256, 0, s>>>(ct_key_sorted, 4 * ni, n_H, ctx->CT_ptr);
+  k_lower_bound_ptr<<<ks_blocks(n_H + 1, 256), 256, 0, s>>>(t.ct_key_sorted, 4 * ni, n_H, ctx->CT_ptr);
   KS_LAUNCHED(ctx);
 
   // ---- cached B_H = P^T M P (A-part of the item pass with M) ----
-  KS_TRY(ks_alloc_t(ctx, &ctx->AH_part, 4 * ctx->d_total, "AH_part"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->B_H, n_H * n_H, "B_H"));
   ctx->n_H = n_H;
   KS_TRY(launch_proj_a(ctx, ctx->sell_M));
   KS_TRY(launch_final<false>(ctx, 0, 16, ctx->B_H, nullptr, n_H, 0));
-  KS_CUDA(ctx, cudaStreamSynchronize(s));
+  KS_CUDA(ctx, cudaStreamSynchronize(s));   // the call scratch is released at return
   return KS_OK;
 }
 
@@ -1243,22 +1232,7 @@ ks_status ks_project_impl(ks_ctx *ctx, int N, const double *Ut, double *FA, doub
   const int64_t n = ctx->n_free, nH = ctx->n_H, D = nH + N;
   // NP >= 2: item-ordered rows are then multiples of 16 bytes (bulk-copy granularity)
   const int np = pow2_at_least(N) < 2 ? 2 : pow2_at_least(N);
-  if (ctx->y_cap < n * np) {
-    for (double **b : {&ctx->Y_H, &ctx->Y_M, &ctx->proj_u, &ctx->proj_up})
-      ks_free_t(ctx, *b);
-    KS_TRY(ks_alloc_t(ctx, &ctx->Y_H, n * np, "Y_H (item order)"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->Y_M, n * np, "Y_M (item order)"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->proj_u, n * np, "proj U pad"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->proj_up, n * np, "proj U (item order)"));
-    ctx->y_cap = n * np;
-  }
-  if (ctx->bc_cap < 4 * ctx->n_items * np) {
-    for (double **b : {&ctx->bH_part, &ctx->cH_part})
-      ks_free_t(ctx, *b);
-    KS_TRY(ks_alloc_t(ctx, &ctx->bH_part, 4 * ctx->n_items * np, "bH_part"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->cH_part, 4 * ctx->n_items * np, "cH_part"));
-    ctx->bc_cap = 4 * ctx->n_items * np;
-  }
+  if (N > ctx->max_N) return ks_fail(ctx, KS_E_ARG, "N = %d exceeds max_N = %d", N, ctx->max_N);
   const double *u = Ut;
   if (np != N || ((uintptr_t)Ut & 31)) {
     k_pad_proj<<<ks_blocks(n * np, 256), 256, 0, s>>>(Ut, N, ctx->proj_u, np, n);

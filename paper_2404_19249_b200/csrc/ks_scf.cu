@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "ks_internal.cuh"
+#include "ks_layout.cuh"
 
 namespace {
 
@@ -269,16 +270,8 @@ ks_status ks_hartree_impl(ks_ctx *ctx, const double *rho, double tol, int max_it
                           double *h_mom, int32_t *h_iters) {
   cudaStream_t s = ctx->stream;
   const int64_t nn = ctx->n_nodes, nt = ctx->n_tets, n = ctx->n_free;
-  if (!ctx->har_w) {
-    KS_TRY(ks_alloc_t(ctx, &ctx->har_w, nn, "hartree w"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->har_c, 4 * nt, "hartree element loads"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->har_b, n, "hartree rhs"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->har_x0, n, "hartree x0"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->har_x, n, "hartree x"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->har_mom, 16, "hartree moments"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->har_part, 9 * 8 * (int64_t)ctx->sm_count, "hartree partials"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->har_iters, 1, "hartree iterations"));
-  }
+  if (!(ctx->ext_features & KS_EXT_SCF))
+    return ks_fail(ctx, KS_E_STATE, "ks_hartree: attach an extension workspace planned with KS_EXT_SCF");
   const int nblk = 8 * ctx->sm_count;   // latency-bound gathers over the tets: 8 blocks per SM
   k_moments1<<<nblk, HB, 0, s>>>(ctx->tets, ctx->vol, ctx->xyz, rho, nt, ctx->har_part);
   KS_LAUNCHED(ctx);
@@ -437,33 +430,11 @@ __global__ void k_anderson_combine(const double *__restrict__ hin, const double 
 }  // namespace
 
 static ks_status scf_alloc(ks_ctx *ctx, int N, int depth) {
-  const int64_t nn = ctx->n_nodes, n = ctx->n_free, D = ctx->n_H + N;
-  if (ctx->scf_nn == nn && ctx->scf_N >= N && ctx->scf_depth >= depth && ctx->scf_D >= D) return KS_OK;
-  for (double **b : {&ctx->scf_rho, &ctx->scf_in, &ctx->scf_out, &ctx->scf_vh, &ctx->scf_vxc, &ctx->scf_veff,
-                     &ctx->scf_Ut, &ctx->scf_FA, &ctx->scf_FB, &ctx->scf_Y, &ctx->scf_hin, &ctx->scf_hout,
-                     &ctx->scf_part, &ctx->scf_red, &ctx->scf_alpha})
-    ks_free_t(ctx, *b);
-  ks_free_t(ctx, ctx->scf_slot);
-  KS_TRY(ks_alloc_t(ctx, &ctx->scf_rho, nn, "scf rho"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->scf_in, nn, "scf rho_in"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->scf_out, nn, "scf rho_out"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->scf_vh, nn, "scf V_H"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->scf_vxc, nn, "scf V_xc"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->scf_veff, nn, "scf V_eff"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->scf_Ut, n * N, "scf U~"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->scf_FA, D * D, "scf F_A"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->scf_FB, D * D, "scf F_B"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->scf_Y, D * N, "scf Y"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->scf_hin, (int64_t)depth * nn, "anderson in"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->scf_hout, (int64_t)depth * nn, "anderson out"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->scf_part, (int64_t)4 * ctx->sm_count * (AMAX * AMAX + AMAX), "scf partials"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->scf_red, AMAX * AMAX + AMAX, "scf reductions"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->scf_alpha, AMAX, "anderson alpha"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->scf_slot, AMAX + 1, "anderson slots"));
-  ctx->scf_nn = nn;
-  ctx->scf_N = N;
-  ctx->scf_depth = depth;
-  ctx->scf_D = D;
+  if (!(ctx->ext_features & KS_EXT_SCF) || ctx->ext_nH != ctx->n_H)
+    return ks_fail(ctx, KS_E_STATE, "ks_scf_solve: attach an extension workspace planned with KS_EXT_SCF for this "
+                   "coarse space");
+  if (N > ctx->max_N || depth > KS_EXT_DEPTH_MAX || ctx->n_H + N > ctx->ext_D)
+    return ks_fail(ctx, KS_E_WORKSPACE, "ks_scf_solve: N = %d / depth = %d exceed the extension plan", N, depth);
   return KS_OK;
 }
 

@@ -14,8 +14,6 @@
 //   order); padding slots hold col = i (own row, a valid gather) and value 0.
 #include <cub/cub.cuh>
 
-#include <vector>
-
 #include "ks_internal.cuh"
 
 namespace {
@@ -62,50 +60,28 @@ __global__ void k_inv_diag(const int32_t *__restrict__ row_ptr, const int32_t *_
 
 }  // namespace
 
-ks_status ks_sell_build(ks_ctx *ctx) {
+// cnt [n_slices + 1] and cub (cub_bytes) are setup temporaries; total = the plan's entry count (checked)
+ks_status ks_sell_build(ks_ctx *ctx, int32_t *cnt, void *cub, size_t cub_bytes, int64_t planned_total) {
   cudaStream_t s = ctx->stream;
   const int64_t n = ctx->n_free;
   const int64_t ns = (n + KS_SELL_C - 1) / KS_SELL_C;
   ctx->n_slices = ns;
-  KS_TRY(ks_alloc_t(ctx, &ctx->sell_ptr, ns + 1, "sell_ptr"));
-  int32_t *cnt = nullptr;
-  KS_CUDA(ctx, cudaMallocAsync((void **)&cnt, sizeof(int32_t) * (ns + 1), s));
   KS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (ns + 1), s));
   k_sell_count<<<ks_blocks(ns, 256), 256, 0, s>>>(ctx->row_ptr, n, ns, cnt);
   KS_LAUNCHED(ctx);
-  {   // the slice offsets are int32: check the padded total in 64 bits before the scan
-    std::vector<int32_t> hc(ns);
-    KS_CUDA(ctx, cudaMemcpyAsync(hc.data(), cnt, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost, s));
-    KS_CUDA(ctx, cudaStreamSynchronize(s));
-    int64_t tot = 0;
-    for (int32_t c : hc) tot += c;
-    if (tot > 0x7fffffffLL) {
-      KS_CUDA(ctx, cudaFreeAsync(cnt, s));
-      return ks_fail(ctx, KS_E_ARG, "sliced-ELL copy of %lld entries exceeds int32 indexing", (long long)tot);
-    }
-  }
-  size_t tmp_bytes = 0;
-  KS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, ctx->sell_ptr, (int)(ns + 1), s));
-  void *tmp = nullptr;
-  KS_CUDA(ctx, cudaMallocAsync(&tmp, tmp_bytes, s));
-  KS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, ctx->sell_ptr, (int)(ns + 1), s));
+  size_t tmp_bytes = cub_bytes;
+  KS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(cub, tmp_bytes, cnt, ctx->sell_ptr, (int)(ns + 1), s));
   ctx->launches++;
   int32_t total = 0;
   KS_CUDA(ctx, cudaMemcpyAsync(&total, ctx->sell_ptr + ns, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   KS_CUDA(ctx, cudaStreamSynchronize(s));
-  KS_CUDA(ctx, cudaFreeAsync(tmp, s));
-  KS_CUDA(ctx, cudaFreeAsync(cnt, s));
+  if (total != planned_total)
+    return ks_fail(ctx, KS_E_CUDA, "sliced-ELL entries %d differ from the plan's %lld", total, (long long)planned_total);
   ctx->sell_total = total;
-  KS_TRY(ks_alloc_t(ctx, &ctx->sell_col, total, "sell col"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->sell_A, total, "sell A"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->sell_M, total, "sell M"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->sell_H, total, "sell H"));
   k_sell_fill_col<<<ks_blocks(n, 256), 256, 0, s>>>(ctx->row_ptr, ctx->col, n, ctx->sell_ptr, ctx->sell_col);
   KS_LAUNCHED(ctx);
   k_sell_fill_val<<<ks_blocks(n, 256), 256, 0, s>>>(ctx->row_ptr, ctx->M, n, ctx->sell_ptr, ctx->sell_M);
   KS_LAUNCHED(ctx);
-  KS_TRY(ks_alloc_t(ctx, &ctx->sell_K, total, "sell K"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->dinvK, n + 2, "1/diag K"));
   k_sell_fill_val<<<ks_blocks(n, 256), 256, 0, s>>>(ctx->row_ptr, ctx->K, n, ctx->sell_ptr, ctx->sell_K);
   KS_LAUNCHED(ctx);
   k_inv_diag<<<ks_blocks(n, 256), 256, 0, s>>>(ctx->row_ptr, ctx->col, ctx->K, n, ctx->dinvK);

@@ -7,6 +7,7 @@
 #include <cub/cub.cuh>
 
 #include "ks_internal.cuh"
+#include "ks_layout.cuh"
 
 namespace {
 
@@ -179,38 +180,37 @@ int bitlen(uint64_t x) {
   return b;
 }
 
-struct TempBuf {
-  std::vector<void *> ptrs;
-  ~TempBuf() { for (void *p : ptrs) cudaFree(p); }
-  template <typename T>
-  cudaError_t get(T **p, size_t count) {
-    cudaError_t e = cudaMalloc((void **)p, sizeof(T) * (count ? count : 1));
-    if (e == cudaSuccess) ptrs.push_back(*p);
-    return e;
-  }
-};
-
 }  // namespace
 
-#define TMP(ctx, tb, ptr, n) KS_TRY(ks_cuda_check((ctx), (tb).get((ptr), (size_t)(n)), "cudaMalloc(setup temp)"))
 
 ks_status ks_setup_mesh(ks_ctx *ctx, const double *h_xyz, const int32_t *h_tets, const uint8_t *h_dir) {
   cudaStream_t s = ctx->stream;
   const int64_t nn = ctx->n_nodes, nt = ctx->n_tets;
   const int T = 256;
-  TempBuf tb;
-  double *xyz;
-  uint8_t *dir;
-  int32_t *flag, *scan;
-  unsigned long long *bad;
-  KS_TRY(ks_alloc_t(ctx, &ctx->xyz, 3 * nn, "xyz"));   // kept: point location of NEXT-3 (ks_interpolation)
-  xyz = ctx->xyz;
-  TMP(ctx, tb, &dir, nn);
-  TMP(ctx, tb, &flag, nn);
-  TMP(ctx, tb, &scan, nn);
-  TMP(ctx, tb, &bad, 1);
-  KS_TRY(ks_alloc_t(ctx, &ctx->tets, 4 * nt, "tets"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->free_of_node, nn, "free_of_node"));
+  // sizes of the setup products counted on the host (the plan's count), then every buffer carved up front:
+  // the persistent layout from the caller's persistent region, the temporaries from the setup region
+  KsMeshSizes z;
+  KS_TRY(ks_count_mesh(nn, h_tets, nt, h_dir, &z, &ctx->err));
+  size_t cub_cap = 0;
+  if (ks_setup_cub_bytes(z, &cub_cap) != KS_OK) return ks_fail(ctx, KS_E_CUDA, "CUB temporary-size query failed");
+  {
+    KsRegion rg(ctx, KS_R_PERSIST);
+    KsCarver cv(ctx);
+    ks_layout_persist(cv, ctx, z);
+    KS_TRY(cv.st);
+  }
+  KsSetupTemps tp;
+  {
+    KsRegion rg(ctx, KS_R_SETUP);
+    KsCarver cv(ctx);
+    ks_layout_setup(cv, tp, z, cub_cap);
+    KS_TRY(cv.st);
+  }
+  double *xyz = ctx->xyz;
+  uint8_t *dir = tp.dir;
+  int32_t *flag = tp.flag, *scan = tp.scan;
+  unsigned long long *bad = tp.bad;
+  void *cub_tmp = tp.cub;
   KS_CUDA(ctx, cudaMemcpyAsync(xyz, h_xyz, sizeof(double) * 3 * nn, cudaMemcpyHostToDevice, s));
   KS_CUDA(ctx, cudaMemcpyAsync(dir, h_dir, nn, cudaMemcpyHostToDevice, s));
   KS_CUDA(ctx, cudaMemcpyAsync(ctx->tets, h_tets, sizeof(int32_t) * 4 * nt, cudaMemcpyHostToDevice, s));
@@ -226,11 +226,7 @@ ks_status ks_setup_mesh(ks_ctx *ctx, const double *h_xyz, const int32_t *h_tets,
   // --- free numbering (exclusive scan of non-Dirichlet flags) ---
   k_notdir<<<ks_blocks(nn, T), T, 0, s>>>(dir, nn, flag);
   KS_LAUNCHED(ctx);
-  size_t tmp_bytes = 0;
-  KS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, flag, scan, (int)nn, s));
-  void *cub_tmp = nullptr;
-  size_t cub_cap = tmp_bytes;
-  TMP(ctx, tb, (uint8_t **)&cub_tmp, cub_cap);
+  size_t tmp_bytes = cub_cap;
   KS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(cub_tmp, tmp_bytes, flag, scan, (int)nn, s));
   ctx->launches++;
   int32_t last_scan = 0, last_flag = 0;
@@ -239,15 +235,12 @@ ks_status ks_setup_mesh(ks_ctx *ctx, const double *h_xyz, const int32_t *h_tets,
   KS_CUDA(ctx, cudaStreamSynchronize(s));
   const int64_t nf = (int64_t)last_scan + last_flag;
   ctx->n_free = nf;
-  if (nf < 1) return ks_fail(ctx, KS_E_MESH, "mesh has no free (non-Dirichlet) node");
-  KS_TRY(ks_alloc_t(ctx, &ctx->node_of_free, nf, "node_of_free"));
+  if (nf != z.nf) return ks_fail(ctx, KS_E_CUDA, "free count %lld differs from the plan's %lld", (long long)nf, (long long)z.nf);
   k_free_numbering<<<ks_blocks(nn, T), T, 0, s>>>(dir, scan, nn, ctx->free_of_node, ctx->node_of_free);
   KS_LAUNCHED(ctx);
 
   // --- geometry ---
-  double *grad;
-  TMP(ctx, tb, &grad, 12 * nt);
-  KS_TRY(ks_alloc_t(ctx, &ctx->vol, nt, "vol"));
+  double *grad = tp.grad;
   k_geometry<<<ks_blocks(nt, T), T, 0, s>>>(xyz, ctx->tets, nt, ctx->vol, grad, bad);
   KS_LAUNCHED(ctx);
   KS_CUDA(ctx, cudaMemcpyAsync(&h_bad, bad, sizeof h_bad, cudaMemcpyDeviceToHost, s));
@@ -256,20 +249,12 @@ ks_status ks_setup_mesh(ks_ctx *ctx, const double *h_xyz, const int32_t *h_tets,
 
   // --- pattern: sort + unique of (free row, free col) keys ---
   const int64_t nk = 16 * nt;
-  uint64_t *keys, *keys_sorted, *uniq;
-  int *n_sel;
-  TMP(ctx, tb, &keys, nk);
-  TMP(ctx, tb, &keys_sorted, nk);
-  TMP(ctx, tb, &n_sel, 1);
+  uint64_t *keys = tp.keys, *keys_sorted = tp.keys_sorted, *uniq;
+  int *n_sel = tp.n_sel;
   const uint64_t sentinel = (uint64_t)nf << 32;
   k_pair_keys<<<ks_blocks(nk, T), T, 0, s>>>(ctx->tets, ctx->free_of_node, nt, sentinel, keys);
   KS_LAUNCHED(ctx);
   const int end_bit = 32 + bitlen((uint64_t)nf);
-  KS_CUDA(ctx, cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys, keys_sorted, (int)nk, 0, end_bit, s));
-  size_t need2 = 0;
-  KS_CUDA(ctx, cub::DeviceSelect::Unique(nullptr, need2, keys_sorted, keys, n_sel, (int)nk, s));
-  if (need2 > tmp_bytes) tmp_bytes = need2;
-  if (tmp_bytes > cub_cap) { cub_cap = tmp_bytes; TMP(ctx, tb, (uint8_t **)&cub_tmp, cub_cap); }
   tmp_bytes = cub_cap;
   KS_CUDA(ctx, cub::DeviceRadixSort::SortKeys(cub_tmp, tmp_bytes, keys, keys_sorted, (int)nk, 0, end_bit, s));
   ctx->launches++;
@@ -285,10 +270,7 @@ ks_status ks_setup_mesh(ks_ctx *ctx, const double *h_xyz, const int32_t *h_tets,
   KS_CUDA(ctx, cudaStreamSynchronize(s));
   const int64_t nnz = (last_key == sentinel) ? h_nsel - 1 : h_nsel;
   ctx->nnz = nnz;
-  if (nnz > 0x7fffffffLL) return ks_fail(ctx, KS_E_ARG, "nnz %lld exceeds int32 indexing", (long long)nnz);
-  KS_TRY(ks_alloc_t(ctx, &ctx->row_ptr, nf + 1 + KS_PAD, "row_ptr"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->col, nnz + KS_PAD, "col"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->diag_pos, nf, "diag_pos"));
+  if (nnz != z.nnz) return ks_fail(ctx, KS_E_CUDA, "nnz %lld differs from the plan's %lld", (long long)nnz, (long long)z.nnz);
   k_row_ptr<<<ks_blocks(nf + 1, T), T, 0, s>>>(uniq, nnz, nf, ctx->row_ptr);
   KS_LAUNCHED(ctx);
   k_cols<<<ks_blocks(nnz, T), T, 0, s>>>(uniq, nnz, ctx->col);
@@ -297,7 +279,6 @@ ks_status ks_setup_mesh(ks_ctx *ctx, const double *h_xyz, const int32_t *h_tets,
   KS_LAUNCHED(ctx);
 
   // --- scatter map and its inverse (stable sort of emap targets keeps ascending index order) ---
-  KS_TRY(ks_alloc_t(ctx, &ctx->emap, nk, "emap"));
   uint32_t *ik = reinterpret_cast<uint32_t *>(keys_sorted);          // reuse 8-byte buffers as 2 x 4-byte
   uint32_t *ik_sorted = ik + nk;
   int32_t *iv = reinterpret_cast<int32_t *>(keys);
@@ -306,38 +287,23 @@ ks_status ks_setup_mesh(ks_ctx *ctx, const double *h_xyz, const int32_t *h_tets,
                                         ik, iv);
   KS_LAUNCHED(ctx);
   const int end_bit2 = bitlen((uint64_t)nnz);
-  size_t need3 = 0;
-  KS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(nullptr, need3, ik, ik_sorted, iv, iv_sorted, (int)nk, 0, end_bit2, s));
-  if (need3 > cub_cap) { cub_cap = need3; TMP(ctx, tb, (uint8_t **)&cub_tmp, cub_cap); }
   tmp_bytes = cub_cap;
   KS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(cub_tmp, tmp_bytes, ik, ik_sorted, iv, iv_sorted, (int)nk, 0,
                                                end_bit2, s));
   ctx->launches++;
-  KS_TRY(ks_alloc_t(ctx, &ctx->inv_ptr, nnz + 1, "inv_ptr"));
   k_inv_ptr<<<ks_blocks(nnz + 1, T), T, 0, s>>>(ik_sorted, nk, nnz, ctx->inv_ptr);
   KS_LAUNCHED(ctx);
   int32_t h_nc = 0;
   KS_CUDA(ctx, cudaMemcpyAsync(&h_nc, ctx->inv_ptr + nnz, 4, cudaMemcpyDeviceToHost, s));
   KS_CUDA(ctx, cudaStreamSynchronize(s));
   ctx->n_contrib = h_nc;
-  KS_TRY(ks_alloc_t(ctx, &ctx->inv_idx, h_nc, "inv_idx"));
+  if (h_nc != z.nc) return ks_fail(ctx, KS_E_CUDA, "contributions %d differ from the plan's %lld", h_nc, (long long)z.nc);
   KS_CUDA(ctx, cudaMemcpyAsync(ctx->inv_idx, iv_sorted, sizeof(int32_t) * h_nc, cudaMemcpyDeviceToDevice, s));
 
   // --- K and M ---
-  KS_TRY(ks_alloc_t(ctx, &ctx->K, nnz + KS_PAD, "K"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->M, nnz + KS_PAD, "M"));
   k_stiffness_mass<<<ks_blocks(nnz, T), T, 0, s>>>(ctx->inv_ptr, ctx->inv_idx, ctx->vol, grad, nnz, ctx->K, ctx->M);
   KS_LAUNCHED(ctx);
-
-  // value arrays filled by assembly, scratch
-  KS_TRY(ks_alloc_t(ctx, &ctx->MV, nnz + KS_PAD, "MV"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->H, nnz + KS_PAD, "H"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->A, nnz + KS_PAD, "A"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->diag, nf, "diag"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->dinv, nf + 2, "dinv"));  // +2: zero pad for the NP = 1 pairwise streams
-  KS_TRY(ks_alloc_t(ctx, &ctx->w_tet, nt, "w_tet"));
-  KS_TRY(ks_alloc_t(ctx, &ctx->v_free, nf, "v_free"));
-  KS_TRY(ks_sell_build(ctx));
-  KS_CUDA(ctx, cudaStreamSynchronize(s));  // temporaries are freed by ~TempBuf after this point
+  KS_TRY(ks_sell_build(ctx, tp.sell_cnt, cub_tmp, cub_cap, z.sell_total));
+  KS_CUDA(ctx, cudaStreamSynchronize(s));  // the setup temporaries are not referenced after this point
   return KS_OK;
 }

@@ -7,9 +7,13 @@
 // s+1 overlaps the compute of step s (B200: separate H2D and D2H copy engines).
 #include "ks_internal.cuh"
 
+// the two device slots live in the extension workspace (KS_EXT_STEP, planned for N <= max_N); the copy streams
+// and events are created on first use
 static ks_status ensure_step_slots(ks_ctx *ctx, int N) {
-  const int64_t n = ctx->n_free, nn = ctx->n_nodes, D = ctx->n_H + N;
-  if (ctx->step_N == N && ctx->step_D == D) return KS_OK;
+  if (!(ctx->ext_features & KS_EXT_STEP) || ctx->ext_nH != ctx->n_H)
+    return ks_fail(ctx, KS_E_STATE, "ks_step_submit: attach an extension workspace planned with KS_EXT_STEP for this "
+                   "coarse space");
+  if (N > ctx->max_N) return ks_fail(ctx, KS_E_ARG, "ks_step_submit: N = %d exceeds max_N = %d", N, ctx->max_N);
   if (!ctx->s_h2d) {
     KS_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->s_h2d, cudaStreamNonBlocking));
     KS_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking));
@@ -19,19 +23,6 @@ static ks_status ensure_step_slots(ks_ctx *ctx, int N) {
       KS_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_d2h[s], cudaEventDisableTiming));
     }
   }
-  for (int s = 0; s < 2; s++) {
-    for (double **b : {&ctx->st_V[s], &ctx->st_lam[s], &ctx->st_U[s], &ctx->st_Ut[s], &ctx->st_FA[s], &ctx->st_FB[s]})
-      ks_free_t(ctx, *b);
-    KS_TRY(ks_alloc_t(ctx, &ctx->st_V[s], nn, "step V"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->st_lam[s], N, "step lambda"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->st_U[s], n * N, "step U"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->st_Ut[s], n * N, "step U~"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->st_FA[s], D * D, "step F_A"));
-    KS_TRY(ks_alloc_t(ctx, &ctx->st_FB[s], D * D, "step F_B"));
-  }
-  KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));   // the zero-fills of the new slots
-  ctx->step_N = N;
-  ctx->step_D = D;
   return KS_OK;
 }
 

@@ -16,17 +16,22 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("KS_LIB") or os.path.join(_PKG, "libks.so")
 
 KS_OK, KS_E_ARG, KS_E_MESH, KS_E_NONFINITE, KS_E_NOT_SPD, KS_E_NOT_CONVERGED, KS_E_CUDA, KS_E_NOMEM, \
-    KS_E_STATE, KS_E_RANK = range(10)
+    KS_E_STATE, KS_E_RANK, KS_E_WORKSPACE = range(11)
 STATUS_NAMES = {0: "KS_OK", 1: "KS_E_ARG", 2: "KS_E_MESH", 3: "KS_E_NONFINITE", 4: "KS_E_NOT_SPD",
-                5: "KS_E_NOT_CONVERGED", 6: "KS_E_CUDA", 7: "KS_E_NOMEM", 8: "KS_E_STATE", 9: "KS_E_RANK"}
+                5: "KS_E_NOT_CONVERGED", 6: "KS_E_CUDA", 7: "KS_E_NOMEM", 8: "KS_E_STATE", 9: "KS_E_RANK",
+                10: "KS_E_WORKSPACE"}
+KS_EXT_EIG, KS_EXT_SCF, KS_EXT_STEP = 1, 2, 4
+KS_EXT_ALL = KS_EXT_EIG | KS_EXT_SCF | KS_EXT_STEP
+REGIONS = {"persistent": 0, "workspace": 1, "coarse": 3, "ext": 4}
 OPS = {"K": 0, "M": 1, "MV": 2, "H": 3, "A": 4}
 
 # every symbol declared in include/ks.h (checked by tests/test_abi.py)
-EXPORTS = ["ks_abi_version", "ks_build_info", "ks_create", "ks_destroy", "ks_set_stream", "ks_pattern",
+EXPORTS = ["ks_abi_version", "ks_build_info", "ks_plan", "ks_create", "ks_destroy", "ks_set_stream", "ks_pattern",
            "ks_values", "ks_assemble_veff", "ks_spmm", "ks_block_solve", "ks_last_iterations", "ks_solve_trace",
-           "ks_true_residual", "ks_set_coarse", "ks_project_augmented", "ks_pencil_eig", "ks_lift",
-           "ks_augmented_solve", "ks_interpolation", "ks_density", "ks_vxc", "ks_hartree", "ks_scf_solve",
-           "ks_step_submit", "ks_step_wait", "ks_memory_bytes", "ks_launch_count", "ks_sync", "ks_last_error"]
+           "ks_true_residual", "ks_coarse_plan", "ks_set_coarse", "ks_ext_plan", "ks_attach_ext",
+           "ks_project_augmented", "ks_pencil_eig", "ks_lift", "ks_augmented_solve", "ks_interpolation_plan",
+           "ks_interpolation", "ks_density", "ks_vxc", "ks_hartree", "ks_scf_solve", "ks_step_submit",
+           "ks_step_wait", "ks_memory_bytes", "ks_memory_usage", "ks_launch_count", "ks_sync", "ks_last_error"]
 
 
 class KSError(RuntimeError):
@@ -51,7 +56,10 @@ def load_library(path: str = LIB_PATH):
     sig = {
         "ks_abi_version": (C.c_int, []),
         "ks_build_info": (C.c_char_p, []),
-        "ks_create": (st, [i64, vp, i64, vp, vp, vp, C.POINTER(vp)]),
+        "ks_plan": (st, [i64, vp, i64, vp, vp, i32, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
+                         C.POINTER(C.c_size_t)]),
+        "ks_create": (st, [i64, vp, i64, vp, vp, i32, vp, C.c_size_t, vp, C.c_size_t, vp, C.c_size_t, vp,
+                           C.POINTER(vp)]),
         "ks_destroy": (None, [vp]),
         "ks_set_stream": (st, [vp, vp]),
         "ks_pattern": (st, [vp, C.POINTER(i64), C.POINTER(i64)] + [C.POINTER(vp)] * 6),
@@ -62,12 +70,17 @@ def load_library(path: str = LIB_PATH):
         "ks_last_iterations": (st, [vp, C.POINTER(i32)]),
         "ks_solve_trace": (st, [vp, i32, vp, C.POINTER(i32)]),
         "ks_true_residual": (st, [vp, i32, vp, vp, vp, vp]),
-        "ks_set_coarse": (st, [vp, i64, vp, vp, vp]),
+        "ks_coarse_plan": (st, [vp, i64, vp, vp, vp, C.POINTER(C.c_size_t)]),
+        "ks_set_coarse": (st, [vp, i64, vp, vp, vp, vp, C.c_size_t]),
+        "ks_ext_plan": (st, [vp, C.c_uint32, i64, C.POINTER(C.c_size_t)]),
+        "ks_attach_ext": (st, [vp, C.c_uint32, i64, vp, C.c_size_t]),
         "ks_project_augmented": (st, [vp, i32, vp, vp, vp]),
         "ks_pencil_eig": (st, [vp, i64, i32, vp, vp, vp, vp]),
         "ks_lift": (st, [vp, i32, vp, i32, vp, vp]),
         "ks_augmented_solve": (st, [vp, i32, vp, vp, dbl, i32, dbl, i32, C.POINTER(i32), vp]),
-        "ks_interpolation": (st, [vp, i64, vp, i64, vp, vp, vp, vp, vp, C.POINTER(i64), C.POINTER(i64)]),
+        "ks_interpolation_plan": (st, [vp, i64, vp, i64, C.POINTER(C.c_size_t)]),
+        "ks_interpolation": (st, [vp, i64, vp, i64, vp, vp, vp, C.c_size_t, vp, vp, vp, C.POINTER(i64),
+                                  C.POINTER(i64)]),
         "ks_density": (st, [vp, i32, vp, dbl, vp]),
         "ks_vxc": (st, [vp, vp, vp, vp]),
         "ks_hartree": (st, [vp, vp, dbl, i32, vp, i32, vp, C.POINTER(i32)]),
@@ -76,6 +89,7 @@ def load_library(path: str = LIB_PATH):
         "ks_step_submit": (st, [vp, i32, vp, dbl, vp, vp, dbl, i32, vp, vp]),
         "ks_step_wait": (st, [vp]),
         "ks_memory_bytes": (st, [vp, C.POINTER(C.c_size_t)]),
+        "ks_memory_usage": (st, [vp, i32, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
         "ks_launch_count": (st, [vp, C.POINTER(i64)]),
         "ks_sync": (st, [vp]),
         "ks_last_error": (C.c_char_p, [vp]),
@@ -122,23 +136,41 @@ def _check_host_tensor(t, dtype, shape, name):
 
 
 class Context:
-    """ks_create .. ks_destroy. Host mesh arrays are numpy; everything else lives in torch CUDA tensors."""
+    """ks_plan + ks_create .. ks_destroy. Host mesh arrays are numpy; everything else lives in torch CUDA tensors.
 
-    def __init__(self, xyz, tets, dirichlet, stream=None):
+    Every device byte the library uses is a torch uint8 tensor owned here (include/ks.h, "Memory"): the
+    persistent and workspace regions from ks_plan (the setup region is released after ks_create), the coarse
+    region from ks_coarse_plan, and the extension region (NEXT rows, host steps) from ks_ext_plan, attached on
+    the first call that needs it. `max_N` is the largest block of orbitals any call will use."""
+
+    def __init__(self, xyz, tets, dirichlet, stream=None, max_N: int = 64):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("libks needs a CUDA device (no CPU fallback)")
         L = load_library()
         self._L = L
+        self._h = None
         xyz = np.ascontiguousarray(xyz, dtype=np.float64)
         tets = np.ascontiguousarray(tets, dtype=np.int32)
         dirichlet = np.ascontiguousarray(dirichlet, dtype=np.uint8)
         self.n_nodes, self.n_tets = xyz.shape[0], tets.shape[0]
+        self.max_N = int(max_N)
         self.device = torch.device("cuda", torch.cuda.current_device())
         self.stream = stream if stream is not None else torch.cuda.current_stream()
+        sz = [C.c_size_t() for _ in range(3)]
+        s = L.ks_plan(self.n_nodes, xyz.ctypes.data, self.n_tets, tets.ctypes.data, dirichlet.ctypes.data,
+                      self.max_N, *[C.byref(x) for x in sz])
+        if s != KS_OK:
+            raise KSError(s, L.ks_last_error(None).decode())
+        self.plan = {"persistent": sz[0].value, "workspace": sz[1].value, "setup": sz[2].value}
+        self._mem = {"persistent": self._region(sz[0].value), "workspace": self._region(sz[1].value)}
+        setup = self._region(sz[2].value)
         h = C.c_void_p()
         s = L.ks_create(self.n_nodes, xyz.ctypes.data, self.n_tets, tets.ctypes.data, dirichlet.ctypes.data,
+                        self.max_N, self._mem["persistent"].data_ptr(), sz[0].value,
+                        self._mem["workspace"].data_ptr(), sz[1].value, setup.data_ptr(), sz[2].value,
                         C.c_void_p(self.stream.cuda_stream), C.byref(h))
+        del setup   # only used during ks_create (which synchronised the stream)
         if s != KS_OK:
             raise KSError(s, L.ks_last_error(None).decode())
         self._h = h
@@ -147,6 +179,35 @@ class Context:
         self.n_free, self.nnz = nf.value, nnz.value
         self.n_H = None
         self.mu = None
+        self._ext = (0, 0)   # (features, max_D) of the attached extension region
+
+    def _region(self, nbytes: int):
+        """A caller-owned device region for libks (torch's caching allocator; 512-byte aligned)."""
+        import torch
+        with torch.cuda.stream(self.stream):
+            return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=self.device)
+
+    def _need_ext(self, features: int, max_D: int = 0):
+        """Attach an extension region covering `features` and pencils up to max_D (re-planned when it grows)."""
+        have_f, have_D = self._ext
+        f = have_f | features
+        D = max(have_D, int(max_D))
+        if f == have_f and D == have_D:
+            return
+        n = C.c_size_t()
+        self._call(self._L.ks_ext_plan(self._h, f, D, C.byref(n)))
+        self._mem.pop("ext", None)
+        self._ext = (0, 0)
+        region = self._region(n.value)
+        self._call(self._L.ks_attach_ext(self._h, f, D, region.data_ptr(), n.value))
+        self._mem["ext"] = region
+        self._ext = (f, D)
+
+    def memory_usage(self, region: str):
+        """(capacity, used, peak) bytes of one region of the context (ks_memory_usage)."""
+        cap, used, peak = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        self._call(self._L.ks_memory_usage(self._h, REGIONS[region], C.byref(cap), C.byref(used), C.byref(peak)))
+        return cap.value, used.value, peak.value
 
     # -- plumbing --------------------------------------------------------------------------------
     def _call(self, status):
@@ -157,6 +218,7 @@ class Context:
         if getattr(self, "_h", None):
             self._L.ks_destroy(self._h)
             self._h = None
+        self._mem = {}
 
     def __del__(self):
         try:
@@ -264,7 +326,16 @@ class Context:
         _check_cuda_tensor(P_val, torch.float64, tuple(P_col.shape), "P_val")
         if P_col.dim() != 1:
             raise ValueError("P_col must be 1-D")
-        self._call(self._L.ks_set_coarse(self._h, int(n_H), _ptr(P_rowptr), _ptr(P_col), _ptr(P_val)))
+        n = C.c_size_t()
+        self._call(self._L.ks_coarse_plan(self._h, int(n_H), _ptr(P_rowptr), _ptr(P_col), _ptr(P_val), C.byref(n)))
+        self.n_H = None
+        self._mem.pop("coarse", None)
+        self._mem.pop("ext", None)   # ks_set_coarse detaches the extension region
+        self._ext = (0, 0)
+        region = self._region(n.value)
+        self._call(self._L.ks_set_coarse(self._h, int(n_H), _ptr(P_rowptr), _ptr(P_col), _ptr(P_val),
+                                         region.data_ptr(), n.value))
+        self._mem["coarse"] = region
         self.n_H = int(n_H)
 
     def project_augmented(self, Ut, FA=None, FB=None):
@@ -291,6 +362,7 @@ class Context:
         D = FA.shape[0]
         _check_cuda_tensor(FA, torch.float64, (D, D), "FA")
         _check_cuda_tensor(FB, torch.float64, (D, D), "FB")
+        self._need_ext(KS_EXT_EIG, D)
         ev = torch.empty(k, dtype=torch.float64, device=FA.device)
         Y = torch.empty((D, k), dtype=torch.float64, device=FA.device)
         self._call(self._L.ks_pencil_eig(self._h, D, int(k), _ptr(FA), _ptr(FB), _ptr(ev), _ptr(Y)))
@@ -317,6 +389,7 @@ class Context:
         N = _n_cols(U)
         _check_cuda_tensor(U, torch.float64, (self.n_free, N), "U")
         _check_cuda_tensor(lam, torch.float64, (N,), "lam")
+        self._need_ext(KS_EXT_EIG)
         hist = np.zeros((max_outer, N))
         outer = C.c_int32()
         self._call(self._L.ks_augmented_solve(self._h, N, _ptr(lam), _ptr(U), float(tol_eig), int(max_outer),
@@ -334,10 +407,15 @@ class Context:
         rp = torch.empty(self.n_free + 1, dtype=torch.int32, device=self.device)
         col = torch.empty(4 * self.n_free, dtype=torch.int32, device=self.device)
         val = torch.empty(4 * self.n_free, dtype=torch.float64, device=self.device)
+        wb = C.c_size_t()
+        self._call(self._L.ks_interpolation_plan(self._h, xyz_c.shape[0], xyz_c.ctypes.data, tets_c.shape[0],
+                                                 C.byref(wb)))
+        work = self._region(wb.value)   # call scratch (the call synchronises before returning)
         nH, pn = C.c_int64(), C.c_int64()
         self._call(self._L.ks_interpolation(self._h, xyz_c.shape[0], xyz_c.ctypes.data, tets_c.shape[0],
-                                            tets_c.ctypes.data, dir_c.ctypes.data, _ptr(rp), _ptr(col), _ptr(val),
-                                            C.byref(nH), C.byref(pn)))
+                                            tets_c.ctypes.data, dir_c.ctypes.data, work.data_ptr(), wb.value,
+                                            _ptr(rp), _ptr(col), _ptr(val), C.byref(nH), C.byref(pn)))
+        del work
         return rp, col[:pn.value], val[:pn.value], nH.value
 
     def density(self, U, f=2.0, rho=None):
@@ -372,6 +450,7 @@ class Context:
         if vh is None:
             vh = torch.zeros_like(rho)
         _check_cuda_tensor(vh, torch.float64, (self.n_nodes,), "vh")
+        self._need_ext(KS_EXT_SCF)
         mom = np.zeros(10)
         it = C.c_int32()
         self._call(self._L.ks_hartree(self._h, _ptr(rho), float(tol), int(max_iter), _ptr(vh), int(bool(warm)),
@@ -388,6 +467,7 @@ class Context:
         N = _n_cols(U)
         _check_cuda_tensor(U, torch.float64, (self.n_free, N), "U")
         _check_cuda_tensor(lam, torch.float64, (N,), "lam")
+        self._need_ext(KS_EXT_SCF)
         outer = C.c_int32()
         inner_steps = np.zeros(max_outer, np.int32)
         dres = np.zeros(max_outer)
@@ -410,6 +490,7 @@ class Context:
                                (U_host, (self.n_free, N), "U_host"), (FA_host, (D, D), "FA_host"),
                                (FB_host, (D, D), "FB_host")):
             _check_host_tensor(t, torch.float64, shape, name)
+        self._need_ext(KS_EXT_STEP)
         self._call(self._L.ks_step_submit(self._h, N, V_host.data_ptr(), float(mu), lam_host.data_ptr(),
                                           U_host.data_ptr(), float(tol), int(max_iter), FA_host.data_ptr(),
                                           FB_host.data_ptr()))

@@ -1,7 +1,8 @@
 /* A plain C99 consumer of libks (no Python, no torch): builds a small Kuhn mesh of the cube [-1, 1]^3 with
  * n^3 cells (6 tets per cell, Dirichlet boundary), uploads V = |x|^2 / 2 and N = 2 orbitals, and runs
- * ks_create -> ks_assemble_veff -> ks_block_solve -> ks_sync through the ABI of include/ks.h, with device
- * memory from the CUDA runtime's C API. Prints "ok <n_free> <iterations> <relres0> <relres1>" and returns 0,
+ * ks_plan -> ks_create -> ks_assemble_veff -> ks_block_solve -> ks_sync through the ABI of include/ks.h. All
+ * device memory is the consumer's own (CUDA runtime C API): the library's regions are allocated from the
+ * sizes ks_plan returns (include/ks.h, "Memory"); the setup region is freed right after ks_create. Prints "ok <n_free> <iterations> <relres0> <relres1>" and returns 0,
  * or prints the ks_last_error message and returns 1. Used by tests/test_abi.py (compile + link, CPU) and
  * tests/test_gpu_c_abi.py (run, GPU). */
 #include <math.h>
@@ -69,7 +70,15 @@ int main(void) {
           t++;
         }
   ks_ctx *ctx = NULL;
-  CHECK(ks_create(nn, xyz, nt, tets, dir, NULL, &ctx));
+  size_t b_persist = 0, b_work = 0, b_setup = 0;
+  CHECK(ks_plan(nn, xyz, nt, tets, dir, N, &b_persist, &b_work, &b_setup));
+  void *d_persist = NULL, *d_work = NULL, *d_setup = NULL;
+  if (cudaMalloc(&d_persist, b_persist) || cudaMalloc(&d_work, b_work) || cudaMalloc(&d_setup, b_setup)) {
+    printf("fail cudaMalloc (regions)\n");
+    return 1;
+  }
+  CHECK(ks_create(nn, xyz, nt, tets, dir, N, d_persist, b_persist, d_work, b_work, d_setup, b_setup, NULL, &ctx));
+  cudaFree(d_setup);   /* used only during ks_create */
   int64_t n_free = 0, nnz = 0;
   CHECK(ks_pattern(ctx, &n_free, &nnz, NULL, NULL, NULL, NULL, NULL, NULL));
   double *dV, *dlam, *dU, *dUt, *drel;
@@ -94,6 +103,8 @@ int main(void) {
   cudaMemcpy(rel, drel, sizeof(double) * N, cudaMemcpyDeviceToHost);
   printf("ok %lld %d %.3e %.3e\n", (long long)n_free, iters, rel[0], rel[1]);
   ks_destroy(ctx);
+  cudaFree(d_persist);
+  cudaFree(d_work);
   cudaFree(dV);
   cudaFree(dlam);
   cudaFree(dU);

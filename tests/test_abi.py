@@ -34,7 +34,7 @@ def test_library_exports_every_declared_symbol(lib):
     exported = set(re.findall(r" T (ks_\w+)", out))
     missing = [s for s in declared_symbols() if s not in exported]
     assert not missing, missing
-    assert lib.ks_abi_version() == 1
+    assert lib.ks_abi_version() == 2
     assert b"sm_100a" in lib.ks_build_info()
 
 
@@ -48,8 +48,10 @@ def test_library_is_sm100a_only():
 def test_null_context_arguments_rejected(lib):
     import ctypes as C
     h = C.c_void_p()
-    assert lib.ks_create(0, None, 0, None, None, None, C.byref(h)) == 1  # KS_E_ARG, no launch
+    assert lib.ks_create(0, None, 0, None, None, 1, None, 0, None, 0, None, 0, None, C.byref(h)) == 1  # KS_E_ARG
     assert b"KS_E_ARG" in lib.ks_last_error(None)
+    sz = [C.c_size_t() for _ in range(3)]
+    assert lib.ks_plan(0, None, 0, None, None, 1, *[C.byref(x) for x in sz]) == 1   # KS_E_ARG before any device call
     assert lib.ks_sync(None) == 1
 
 

@@ -26,7 +26,7 @@ def test_config5_sampled_parity():
     import paper_2404_19249_b200 as ks
     p = gen.make_problem(5)
     dev = torch.device("cuda", 0)
-    ctx = ks.Context(p.xyz, p.tets, p.dirichlet)
+    ctx = ks.Context(p.xyz, p.tets, p.dirichlet, max_N=p.N)
     ctx.assemble_veff(torch.from_numpy(p.V).to(dev), p.mu)
     ctx.set_coarse(p.n_H, torch.from_numpy(p.P_rowptr).to(dev), torch.from_numpy(p.P_col).to(dev),
                    torch.from_numpy(p.P_val).to(dev))
