@@ -260,6 +260,34 @@ ks_status ks_augmented_solve(ks_ctx *ctx, int32_t N, double *d_lambda, double *d
                              double *h_history);
 
 /*
+ * NEXT-4 / SURVEY.md §8(e): the row-slab partition of ONE block solve over several processes (one GPU each;
+ * the paper splits the BVPs over processes). The phases of the fused two-phase
+ * Jacobi-PCG of ks_block_solve run as separate launches over one rank's contiguous rows [row0, row1); the
+ * driver (paper_2404_19249_b200/slab.py) owns the partition (slab bounds balanced by nonzeros, halo ranges),
+ * exchanges the halo rows of z between neighbouring ranks before every ks_slab_spmm and all-gathers the
+ * per-column dots after every phase, summing them in rank order so all ranks derive the same alpha, beta.
+ *   NP: padded block width (power of two, 1..64); every block d_* is [n_free][NP] f64 in the global row
+ *   numbering (32-byte aligned for NP >= 4); a call reads the rows of d_U / d_Z referenced by its rows (own
+ *   rows + halo) and writes only its own rows. d_lambda [NP] (pad entries 0). h_* coefficient arrays [NP]
+ *   (host). d_dots: per-column sums over the rank's rows, [3][NP] (init: b.b, r.z, r.r), [NP] (spmm: p.q),
+ *   [2][NP] (update: r.z, r.r), deterministic.
+ *   ks_slab_init    b = (lambda+mu) M u, r = b - A u, z = r / d, p = z                (Aux_Linear_Problem)
+ *   ks_slab_spmm    w = A z; q = w + beta q, p = z + beta p, x = xin + alpha_x p (first != 0: q = A z only)
+ *   ks_slab_update  z -= alpha q / d
+ *   ks_slab_finish  x = xin + alpha_x p
+ * Asynchronous on the context's stream. Errors: KS_E_ARG (range, alignment), KS_E_STATE (not assembled).
+ */
+ks_status ks_slab_init(ks_ctx *ctx, int32_t NP, int64_t row0, int64_t row1, const double *d_lambda, const double *d_U,
+                       double *d_Z, double *d_P, double *d_dots);
+ks_status ks_slab_spmm(ks_ctx *ctx, int32_t NP, int64_t row0, int64_t row1, int32_t first, const double *h_alpha_x,
+                       const double *h_beta, const double *d_Z, double *d_Q, double *d_P, const double *d_Xin,
+                       double *d_X, double *d_dots);
+ks_status ks_slab_update(ks_ctx *ctx, int32_t NP, int64_t row0, int64_t row1, const double *h_alpha, double *d_Z,
+                         const double *d_Q, double *d_dots);
+ks_status ks_slab_finish(ks_ctx *ctx, int32_t NP, int64_t row0, int64_t row1, const double *h_alpha_x,
+                         const double *d_P, const double *d_Xin, double *d_X);
+
+/*
  * NEXT-3: the nonnested interpolation operator P = I_H^h of Algorithm 1
  * from an independent coarse tet mesh (nonnested, possibly unstructured, covering the
  * fine mesh's domain): row i holds the barycentric coordinates of fine free node i in the coarse tet that

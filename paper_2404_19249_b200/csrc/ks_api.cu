@@ -524,6 +524,58 @@ ks_status ks_project_augmented(ks_ctx *ctx, int32_t N, const double *d_Ut, doubl
   return ks_project_impl(ctx, N, d_Ut, d_FA, d_FB);
 }
 
+static ks_status check_slab(ks_ctx *ctx, int32_t NP, int64_t row0, int64_t row1, const void *const *ptrs, int np) {
+  if (!ctx) return KS_E_ARG;
+  if (NP < 1 || NP > KS_MAX_N || (NP & (NP - 1)))
+    return ks_fail(ctx, KS_E_ARG, "slab: NP = %d must be a power of two in [1, 64]", NP);
+  if (row0 < 0 || row1 <= row0 || row1 > ctx->n_free)
+    return ks_fail(ctx, KS_E_ARG, "slab: rows [%lld, %lld) outside [0, %lld)", (long long)row0, (long long)row1,
+                   (long long)ctx->n_free);
+  for (int i = 0; i < np; i++) {
+    if (!ptrs[i]) return ks_fail(ctx, KS_E_ARG, "slab: null pointer argument %d", i);
+    if (NP >= 4 && ((uintptr_t)ptrs[i] & 31)) return ks_fail(ctx, KS_E_ARG, "slab: blocks must be 32-byte aligned");
+  }
+  if (!ctx->assembled) return ks_fail(ctx, KS_E_STATE, "slab: call ks_assemble_veff first");
+  return KS_OK;
+}
+
+ks_status ks_slab_init(ks_ctx *ctx, int32_t NP, int64_t row0, int64_t row1, const double *d_lambda, const double *d_U,
+                       double *d_Z, double *d_P, double *d_dots) {
+  const void *p[] = {d_U, d_Z, d_P};
+  KS_TRY(check_slab(ctx, NP, row0, row1, p, 3));
+  if (!d_lambda || !d_dots) return ks_fail(ctx, KS_E_ARG, "ks_slab_init: null lambda / dots");
+  return ks_slab_phase_impl(ctx, 0, NP, row0, row1, 0, nullptr, nullptr, d_lambda, d_U, d_Z, nullptr, d_P, nullptr,
+                            nullptr, d_dots);
+}
+
+ks_status ks_slab_spmm(ks_ctx *ctx, int32_t NP, int64_t row0, int64_t row1, int32_t first, const double *h_alpha_x,
+                       const double *h_beta, const double *d_Z, double *d_Q, double *d_P, const double *d_Xin,
+                       double *d_X, double *d_dots) {
+  const void *p[] = {d_Z, d_Q, d_P, d_Xin, d_X};
+  KS_TRY(check_slab(ctx, NP, row0, row1, p, 5));
+  if (!h_alpha_x || !h_beta || !d_dots) return ks_fail(ctx, KS_E_ARG, "ks_slab_spmm: null coefficients / dots");
+  return ks_slab_phase_impl(ctx, 1, NP, row0, row1, first, h_alpha_x, h_beta, nullptr, nullptr,
+                            const_cast<double *>(d_Z), d_Q, d_P, d_Xin, d_X, d_dots);
+}
+
+ks_status ks_slab_update(ks_ctx *ctx, int32_t NP, int64_t row0, int64_t row1, const double *h_alpha, double *d_Z,
+                         const double *d_Q, double *d_dots) {
+  const void *p[] = {d_Z, d_Q};
+  KS_TRY(check_slab(ctx, NP, row0, row1, p, 2));
+  if (!h_alpha || !d_dots) return ks_fail(ctx, KS_E_ARG, "ks_slab_update: null coefficients / dots");
+  return ks_slab_phase_impl(ctx, 2, NP, row0, row1, 0, h_alpha, nullptr, nullptr, nullptr, d_Z,
+                            const_cast<double *>(d_Q), nullptr, nullptr, nullptr, d_dots);
+}
+
+ks_status ks_slab_finish(ks_ctx *ctx, int32_t NP, int64_t row0, int64_t row1, const double *h_alpha_x,
+                         const double *d_P, const double *d_Xin, double *d_X) {
+  const void *p[] = {d_P, d_Xin, d_X};
+  KS_TRY(check_slab(ctx, NP, row0, row1, p, 3));
+  if (!h_alpha_x) return ks_fail(ctx, KS_E_ARG, "ks_slab_finish: null coefficients");
+  return ks_slab_phase_impl(ctx, 3, NP, row0, row1, 0, h_alpha_x, nullptr, nullptr, nullptr, nullptr, nullptr,
+                            const_cast<double *>(d_P), d_Xin, d_X, nullptr);
+}
+
 ks_status ks_memory_bytes(const ks_ctx *ctx, size_t *bytes) {
   if (!ctx || !bytes) return KS_E_ARG;
   size_t b = 0;

@@ -86,6 +86,7 @@ struct ks_ctx {
   int *trace_count = nullptr;
 
   // solver workspace (KS_R_WORK, carved at ks_create for N <= max_N)
+  int tile_emax[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // largest sliced-ELL entries of a PCG tile, per log2(NP)
   double *r = nullptr, *p = nullptr, *q = nullptr, *xpad = nullptr, *upad = nullptr, *bpad = nullptr;
   double *partials = nullptr;       // [grid][4 * 64]
   unsigned *barrier = nullptr;      // grid barrier counter
@@ -270,6 +271,9 @@ ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, co
                              double *evecs, const double *Ywarm = nullptr, bool same_B = false);
 // Ywarm [D][k] (device, may alias evecs): start block of the filtered path (e.g. the previous inner step's
 // eigenvectors); same_B: F_B equals the previous call's (its Cholesky factor is reused)
+ks_status ks_slab_phase_impl(ks_ctx *ctx, int phase, int NP, int64_t row0, int64_t row1, int first,
+                             const double *h_alpha, const double *h_beta, const double *lambda, const double *U,
+                             double *Z, double *Q, double *P, const double *Xin, double *X, double *dots);
 ks_status ks_lift_impl(ks_ctx *ctx, int N, const double *Ut, int k, const double *Y, double *Unew);
 ks_status ks_augmented_solve_impl(ks_ctx *ctx, int N, double *lambda, double *U, double tol_eig, int max_outer,
                                   double tol_bvp, int32_t max_iter_bvp, int32_t *h_outer, double *h_history);

@@ -80,6 +80,9 @@ struct PcgArgs {
   int trace_cap;
   int64_t n;
   int N, ntiles, max_iter;
+  // staged S phase of the fused kernel: the largest sliced-ELL entry count of one tile and the stage size
+  int emax;
+  unsigned stage_bytes;
 };
 
 // out[j] = sum_{g < G} part[g*stride + j] for j < nv, fixed order, one warp per value.
@@ -355,6 +358,9 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
 #ifndef KS_PCG_PREFETCH
 #define KS_PCG_PREFETCH 1
 #endif
+#ifndef KS_PCG_PFDIST
+#define KS_PCG_PFDIST 1   // tiles ahead
+#endif
 __device__ __forceinline__ void l2_prefetch(const void *ptr, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
 }
@@ -373,6 +379,56 @@ __device__ __forceinline__ void prefetch_rows(const PcgArgs &a, int64_t row0, co
   }
 }
 
+// One row of w = A z with the row's sliced-ELL values and columns in shared memory (a staged tile, below):
+// the same slot groups and accumulation order as sell_row; the gathers of z stay global loads.
+template <int NP>
+__device__ __forceinline__ void sell_row_s(const double *vs, const int32_t *cs, int base, int groups,
+                                           const double *X, int sub, DV<SL<NP>::VEC> &ya) {
+  constexpr int VEC = SL<NP>::VEC;
+#pragma unroll
+  for (int v = 0; v < VEC; v++) ya.v[v] = 0.0;
+  const double *xs = X + sub * VEC;
+  int g = 0;
+  for (; g + 2 <= groups; g += 2) {
+    const int o = base + g * (4 * KS_SELL_C), o2 = o + 4 * KS_SELL_C;
+    const int4 c = *reinterpret_cast<const int4 *>(cs + o);
+    const int4 d = *reinterpret_cast<const int4 *>(cs + o2);
+    double av[8];
+    {
+      const double2 t0 = *reinterpret_cast<const double2 *>(vs + o), t1 = *reinterpret_cast<const double2 *>(vs + o + 2);
+      const double2 t2 = *reinterpret_cast<const double2 *>(vs + o2), t3 = *reinterpret_cast<const double2 *>(vs + o2 + 2);
+      av[0] = t0.x; av[1] = t0.y; av[2] = t1.x; av[3] = t1.y; av[4] = t2.x; av[5] = t2.y; av[6] = t3.x; av[7] = t3.y;
+    }
+    DV<VEC> x[8];
+    x[0] = DV<VEC>::ld(xs + (int64_t)c.x * NP);
+    x[1] = DV<VEC>::ld(xs + (int64_t)c.y * NP);
+    x[2] = DV<VEC>::ld(xs + (int64_t)c.z * NP);
+    x[3] = DV<VEC>::ld(xs + (int64_t)c.w * NP);
+    x[4] = DV<VEC>::ld(xs + (int64_t)d.x * NP);
+    x[5] = DV<VEC>::ld(xs + (int64_t)d.y * NP);
+    x[6] = DV<VEC>::ld(xs + (int64_t)d.z * NP);
+    x[7] = DV<VEC>::ld(xs + (int64_t)d.w * NP);
+#pragma unroll
+    for (int j = 0; j < 8; j++)
+#pragma unroll
+      for (int v = 0; v < VEC; v++) ya.v[v] = fma(av[j], x[j].v[v], ya.v[v]);
+  }
+  for (; g < groups; g++) {
+    const int o = base + g * (4 * KS_SELL_C);
+    const int4 c = *reinterpret_cast<const int4 *>(cs + o);
+    const double2 t0 = *reinterpret_cast<const double2 *>(vs + o), t1 = *reinterpret_cast<const double2 *>(vs + o + 2);
+    const DV<VEC> x0 = DV<VEC>::ld(xs + (int64_t)c.x * NP), x1 = DV<VEC>::ld(xs + (int64_t)c.y * NP);
+    const DV<VEC> x2 = DV<VEC>::ld(xs + (int64_t)c.z * NP), x3 = DV<VEC>::ld(xs + (int64_t)c.w * NP);
+#pragma unroll
+    for (int v = 0; v < VEC; v++) {
+      ya.v[v] = fma(t0.x, x0.v[v], ya.v[v]);
+      ya.v[v] = fma(t0.y, x1.v[v], ya.v[v]);
+      ya.v[v] = fma(t1.x, x2.v[v], ya.v[v]);
+      ya.v[v] = fma(t1.y, x3.v[v], ya.v[v]);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------------------------
 // Fused two-phase iteration (the default for the BVPs, KS_PCG_FUSED=0 selects the three-phase kernel above).
 // z = D^-1 r is stored instead of r, and q = A p is carried by the recurrence
@@ -384,11 +440,18 @@ __device__ __forceinline__ void prefetch_rows(const PcgArgs &a, int64_t row0, co
 // The same 10 vector touches per iteration as the three-phase form, one grid barrier fewer. The deferred
 // x_{k+1} = x_k + alpha_k p_k of the last iteration runs in a final streaming pass. Per-column freezing,
 // NOT_SPD / NONFINITE / NOT_CONVERGED semantics and the fixed reduction order are those of k_block_pcg.
-template <int NP>
+// STG: the S phases after the first stream each tile's sliced-ELL values and columns and its rows of q, p, x and
+// z into shared memory with bulk copies (cp.async.bulk, SASS UBLKCP), two stages, one producer thread: the
+// only global loads left on a row's dependency chain are the gathers of z.
+template <int NP, bool STG>
 __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(PcgArgs a) {
   constexpr int VEC = SL<NP, PCG_THREADS>::VEC, LPR = SL<NP, PCG_THREADS>::LPR, RPW = SL<NP, PCG_THREADS>::RPW,
                 TILE = SL<NP, PCG_THREADS>::TILE, CHUNK = SL<NP, PCG_THREADS>::CHUNK;
   constexpr int STRIDE = 4 * NP;
+  constexpr unsigned VB = TILE * NP * 8;   // bytes of one vector's tile rows
+  extern __shared__ __align__(128) unsigned char dyn[];
+  __shared__ __align__(8) uint64_t s_full[2];
+  unsigned pseq = 0;                        // stage uses so far (stage pseq & 1, parity (pseq >> 1) & 1)
 
   __shared__ double red[PCG_WARPS * 3 * NP];
   __shared__ double tot[3 * NP];
@@ -414,6 +477,14 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
     }
   };
   stamp();
+  if constexpr (STG) {
+    if (threadIdx.x == 0) {
+      mbar_init(&s_full[0], 1);
+      mbar_init(&s_full[1], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+  }
 
   // ---------------- init: b = (lambda+mu) M u, r = b - A u, z = r / d, p = z (x = u stays implicit) ------------
   {
@@ -495,11 +566,84 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
           acc[0][v] = 0.0;
         }
         const double *xin = xwritten ? a.X : a.U;
+        if (STG && !first) {
+          // ---- staged: tile k of this block in stage (pseq + k) & 1 ----
+          const int64_t my = a.ntiles > (int)blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / G + 1 : 0;
+          const unsigned EB = (unsigned)a.emax;
+          auto issue = [&](int64_t k) {   // one thread: the bulk copies of tile k
+            const int64_t r0 = ((int64_t)blockIdx.x + k * G) * TILE;
+            const int64_t rows = min((int64_t)TILE, n - r0);
+            const int32_t e0 = __ldg(a.sell_ptr + r0 / KS_SELL_C);
+            const int32_t e1 = __ldg(a.sell_ptr + (r0 + rows + KS_SELL_C - 1) / KS_SELL_C);
+            const unsigned q = pseq + (unsigned)k, eb = (unsigned)(e1 - e0), vb = (unsigned)(rows * NP * 8);
+            unsigned char *st = dyn + (size_t)(q & 1u) * a.stage_bytes;
+            uint64_t *bar = &s_full[q & 1u];
+            mbar_expect_tx(bar, eb * 12u + 4u * vb);
+            bulk_g2s(st, a.A + e0, eb * 8u, bar);
+            bulk_g2s(st + 8u * EB, a.sell_col + e0, eb * 4u, bar);
+            unsigned char *vbase = st + 12u * EB;
+            bulk_g2s(vbase, a.q + r0 * NP, vb, bar);
+            bulk_g2s(vbase + VB, a.p + r0 * NP, vb, bar);
+            bulk_g2s(vbase + 2 * VB, xin + r0 * NP, vb, bar);
+            bulk_g2s(vbase + 3 * VB, Z + r0 * NP, vb, bar);
+          };
+          if (threadIdx.x == 0) {
+            // q, p, x, z were written by the generic proxy before the grid barrier: order the bulk reads after
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            for (int64_t k = 0; k < 2 && k < my; k++) issue(k);
+          }
+          for (int64_t k = 0; k < my; k++) {
+            const unsigned q = pseq + (unsigned)k;
+            mbar_wait(&s_full[q & 1u], (q >> 1) & 1u);
+            const unsigned char *st = dyn + (size_t)(q & 1u) * a.stage_bytes;
+            const double *vs = reinterpret_cast<const double *>(st);
+            const int32_t *cs = reinterpret_cast<const int32_t *>(st + 8u * EB);
+            const double *qs = reinterpret_cast<const double *>(st + 12u * EB);
+            const int64_t t = (int64_t)blockIdx.x + k * G;
+            const int lr = warp * RPW + slot;
+            const int64_t row = t * TILE + lr;
+            if (row < n) {
+              const int32_t e0 = __ldg(a.sell_ptr + t * (TILE / KS_SELL_C));
+              const int32_t b = __ldg(a.sell_ptr + row / KS_SELL_C), e = __ldg(a.sell_ptr + row / KS_SELL_C + 1);
+              DV<VEC> w;
+              sell_row_s<NP>(vs, cs, (b - e0) + (int)(row % KS_SELL_C) * 4, (e - b) / (4 * KS_SELL_C), Z, sub, w);
+              const int so = lr * NP + sub * VEC;
+              double qv[VEC], pv[VEC], xv[VEC], zv[VEC];
+#pragma unroll
+              for (int v = 0; v < VEC; v += 2) {
+                const double2 q2 = *reinterpret_cast<const double2 *>(qs + so + v);
+                const double2 p2 = *reinterpret_cast<const double2 *>(qs + VB / 8 + so + v);
+                const double2 x2 = *reinterpret_cast<const double2 *>(qs + 2 * (VB / 8) + so + v);
+                const double2 z2 = *reinterpret_cast<const double2 *>(qs + 3 * (VB / 8) + so + v);
+                qv[v] = q2.x; qv[v + 1] = q2.y; pv[v] = p2.x; pv[v + 1] = p2.y;
+                xv[v] = x2.x; xv[v + 1] = x2.y; zv[v] = z2.x; zv[v + 1] = z2.y;
+              }
+              DV<VEC> qo, po, xo;
+#pragma unroll
+              for (int v = 0; v < VEC; v++) {
+                xo.v[v] = xv[v] + xa[v] * pv[v];
+                po.v[v] = zv[v] + be[v] * pv[v];
+                qo.v[v] = w.v[v] + be[v] * qv[v];
+                acc[0][v] += po.v[v] * qo.v[v];
+              }
+              const int64_t off = row * NP + sub * VEC;
+              qo.st(a.q + off);
+              po.st(a.p + off);
+              xo.st(a.X + off);
+            }
+            __syncthreads();   // every warp is done with this stage
+            if (threadIdx.x == 0 && k + 2 < my) issue(k + 2);
+          }
+          pseq += (unsigned)my;
+        } else {
         constexpr bool PF = KS_PCG_PREFETCH && NP >= 4;
-        if (PF && lane == 0) prefetch_rows<NP, RPW>(a, (int64_t)blockIdx.x * TILE + warp * RPW, xin, !first);
+        if (PF && lane == 0)
+          for (int d = 0; d < KS_PCG_PFDIST; d++)
+            prefetch_rows<NP, RPW>(a, (int64_t)(blockIdx.x + d * G) * TILE + warp * RPW, xin, !first);
         for (int tile = blockIdx.x; tile < a.ntiles; tile += G) {
           const int64_t row = (int64_t)tile * TILE + warp * RPW + slot;
-          if (PF && lane == 0) prefetch_rows<NP, RPW>(a, (int64_t)(tile + G) * TILE + warp * RPW, xin, !first);
+          if (PF && lane == 0)
+            prefetch_rows<NP, RPW>(a, (int64_t)(tile + KS_PCG_PFDIST * G) * TILE + warp * RPW, xin, !first);
           if (row < n) {
             DV<VEC> w, unused;
             sell_row<NP, 1>(a.sell_ptr, a.sell_col, a.A, nullptr, row, Z, sub, w, unused);
@@ -526,6 +670,7 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
             }
           }
         }
+        }   // unstaged
         if (!first) xwritten = true;
         block_cols<NP, 1>(acc, red, tot);
         for (int i = threadIdx.x; i < NP; i += blockDim.x) part_s[(int64_t)blockIdx.x * STRIDE + i] = tot[i];
@@ -682,11 +827,26 @@ __global__ void __launch_bounds__(256) k_spmm(const int32_t *__restrict__ row_pt
   y.store(Y + row * NP + sub * VEC);
 }
 
-template <int NP, bool FUSED>
-ks_status launch_pcg_t(ks_ctx *ctx, PcgArgs &a) {
-  auto kern = FUSED ? k_block_pcg_fused<NP> : k_block_pcg<NP>;
+// largest sliced-ELL entry count of a tile of `slices` consecutive slices
+__global__ void k_tile_emax(const int32_t *__restrict__ sell_ptr, int64_t n_slices, int slices, int *emax) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t s0 = t * slices;
+  if (s0 >= n_slices) return;
+  const int64_t s1 = s0 + slices < n_slices ? s0 + slices : n_slices;
+  atomicMax(emax, sell_ptr[s1] - sell_ptr[s0]);
+}
+
+#ifndef KS_PCG_STAGED
+#define KS_PCG_STAGED 1   // the staged S phase of the fused kernel when its two stages fit in shared memory
+#endif
+constexpr size_t PCG_STAGE_SMEM_MAX = 200 * 1024;
+
+template <int NP, bool FUSED, bool STG>
+ks_status launch_pcg_t(ks_ctx *ctx, PcgArgs &a, size_t dyn) {
+  auto kern = FUSED ? k_block_pcg_fused<NP, STG> : k_block_pcg<NP>;
+  if (dyn > 0) KS_CUDA(ctx, cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
   int per_sm = 0;
-  KS_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PCG_THREADS, 0));
+  KS_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PCG_THREADS, dyn));
   if (per_sm < 1) return ks_fail(ctx, KS_E_CUDA, "k_block_pcg<%d> cannot be resident", NP);
   if (per_sm > KS_PCG_GMAX_PER_SM) per_sm = KS_PCG_GMAX_PER_SM;   // the partials are planned for this many
   int G = per_sm * ctx->sm_count;
@@ -694,19 +854,46 @@ ks_status launch_pcg_t(ks_ctx *ctx, PcgArgs &a) {
   a.partials = ctx->partials;
   KS_CUDA(ctx, cudaMemsetAsync(ctx->barrier, 0, sizeof(unsigned), ctx->stream));
   void *args[] = {&a};
-  KS_CUDA(ctx, cudaLaunchCooperativeKernel((const void *)kern, dim3(G), dim3(PCG_THREADS), args, 0, ctx->stream));
+  KS_CUDA(ctx, cudaLaunchCooperativeKernel((const void *)kern, dim3(G), dim3(PCG_THREADS), args, dyn, ctx->stream));
   ctx->launches++;
   return KS_OK;
 }
 
 template <int NP>
 ks_status launch_pcg(ks_ctx *ctx, PcgArgs &a) {
-  a.ntiles = (int)((a.n + SL<NP, PCG_THREADS>::TILE - 1) / SL<NP, PCG_THREADS>::TILE);
+  constexpr int TILE = SL<NP, PCG_THREADS>::TILE;
+  a.ntiles = (int)((a.n + TILE - 1) / TILE);
+  a.emax = 0;
+  a.stage_bytes = 0;
   // the fused two-phase kernel serves the BVPs (right-hand side (lambda + mu) M u); the Poisson mode of the
   // Hartree solve (given B, up to ~10^3 iterations to 1e-12) keeps the three-phase recurrences
   const char *fz = getenv("KS_PCG_FUSED");
-  if (!a.B && !(fz && fz[0] == '0')) return launch_pcg_t<NP, true>(ctx, a);
-  return launch_pcg_t<NP, false>(ctx, a);
+  if (a.B || (fz && fz[0] == '0')) return launch_pcg_t<NP, false, false>(ctx, a, 0);
+  if constexpr (NP >= 4 && KS_PCG_STAGED) {
+    const char *sg = getenv("KS_PCG_STAGED");
+    if (!(sg && sg[0] == '0')) {
+      int &em = ctx->tile_emax[__builtin_ctz(NP)];
+      if (em == 0) {   // once per context and block width
+        KsScratch scratch(ctx, KS_R_WORK);
+        int *d = nullptr;
+        KS_TRY(ks_alloc_t(ctx, &d, 1, "tile emax"));
+        const int slices = TILE / KS_SELL_C;
+        const int64_t nt = (ctx->n_slices + slices - 1) / slices;
+        k_tile_emax<<<ks_blocks(nt, 256), 256, 0, ctx->stream>>>(ctx->sell_ptr, ctx->n_slices, slices, d);
+        KS_LAUNCHED(ctx);
+        KS_CUDA(ctx, cudaMemcpyAsync(&em, d, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        if (em <= 0) em = -1;
+      }
+      const size_t stage = (size_t)em * 12 + 4 * (size_t)TILE * NP * 8;
+      if (em > 0 && 2 * stage <= PCG_STAGE_SMEM_MAX) {
+        a.emax = em;
+        a.stage_bytes = (unsigned)stage;
+        return launch_pcg_t<NP, true, true>(ctx, a, 2 * stage);
+      }
+    }
+  }
+  return launch_pcg_t<NP, true, false>(ctx, a, 0);
 }
 
 template <int NP>

@@ -31,7 +31,8 @@ EXPORTS = ["ks_abi_version", "ks_build_info", "ks_plan", "ks_create", "ks_destro
            "ks_true_residual", "ks_coarse_plan", "ks_set_coarse", "ks_ext_plan", "ks_attach_ext",
            "ks_project_augmented", "ks_pencil_eig", "ks_lift", "ks_augmented_solve", "ks_interpolation_plan",
            "ks_interpolation", "ks_density", "ks_vxc", "ks_hartree", "ks_scf_solve", "ks_step_submit",
-           "ks_step_wait", "ks_memory_bytes", "ks_memory_usage", "ks_launch_count", "ks_sync", "ks_last_error"]
+           "ks_step_wait", "ks_memory_bytes", "ks_memory_usage", "ks_launch_count", "ks_sync", "ks_last_error",
+           "ks_slab_init", "ks_slab_spmm", "ks_slab_update", "ks_slab_finish"]
 
 
 class KSError(RuntimeError):
@@ -90,6 +91,10 @@ def load_library(path: str = LIB_PATH):
         "ks_step_wait": (st, [vp]),
         "ks_memory_bytes": (st, [vp, C.POINTER(C.c_size_t)]),
         "ks_memory_usage": (st, [vp, i32, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
+        "ks_slab_init": (st, [vp, i32, i64, i64, vp, vp, vp, vp, vp]),
+        "ks_slab_spmm": (st, [vp, i32, i64, i64, i32, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "ks_slab_update": (st, [vp, i32, i64, i64, vp, vp, vp, vp]),
+        "ks_slab_finish": (st, [vp, i32, i64, i64, vp, vp, vp, vp]),
         "ks_launch_count": (st, [vp, C.POINTER(i64)]),
         "ks_sync": (st, [vp]),
         "ks_last_error": (C.c_char_p, [vp]),

@@ -328,11 +328,11 @@ def test_config4_full_parity():
     assert np.all(np.abs(ev.cpu().numpy() - wo) <= 1e-9 * np.abs(wo).max())
 
 
-@pytest.mark.parametrize("c", [3])
-def test_block_solve_staged_s_phase(c, monkeypatch):
-    """The opt-in S phase with the orbital block staged in shared memory by bulk copies (KS_PCG_STAGE=1)
-    reaches the same solutions as the oracle."""
-    monkeypatch.setenv("KS_PCG_STAGE", "1")
+@pytest.mark.parametrize("c", [2, 3])
+def test_block_solve_three_phase_kernel(c, monkeypatch):
+    """The three-phase kernel (KS_PCG_FUSED=0: q = A p, then r, then x and p; the Poisson mode of the Hartree
+    solve always runs it) reaches the oracle's solutions like the default fused two-phase kernel."""
+    monkeypatch.setenv("KS_PCG_FUSED", "0")
     k = case(c)
     p = k.p
     ref, ut, it, rr, st = _solve_both(k, p.lam, p.U)
