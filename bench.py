@@ -40,6 +40,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c5", action="store_true",
+                    help="skip the C5 sub-record of the default C4 run (largest config, ~2 min of host setup)")
     ap.add_argument("--ref-budget-s", type=float, default=150.0,
                     help="reference arm: CPU seconds the K+W oracle steps may take in total")
     return ap.parse_args()
@@ -287,16 +289,36 @@ def load_peaks():
 # --------------------------------------------------------------------------------------------------
 # CPU oracle (reference arm / cpu_baseline)
 # --------------------------------------------------------------------------------------------------
-def oracle_step(om, p, ncols):
-    """assemble + block PCG on the first `ncols` orbitals + projection with them (plain oracle, 1 core)."""
+def oracle_step(om, p, ncols, phases=None):
+    """assemble + block PCG on the first `ncols` orbitals + projection with them (plain oracle, 1 core).
+    `phases` (dict, optional) receives the per-phase seconds and the oracle's iteration counts."""
     t0 = time.perf_counter()
     om.assemble_veff(p.V, p.mu)
+    t1 = time.perf_counter()
     U = np.ascontiguousarray(p.U[:, :ncols])
     r = om.block_pcg(p.lam[:ncols], U, tol=TOL, max_iter=MAX_ITER)
+    t2 = time.perf_counter()
     om.project(p.n_H, p.P_rowptr, p.P_col, p.P_val, r["Ut"])
-    dt = time.perf_counter() - t0
+    t3 = time.perf_counter()
     k = int(r["iters"].max())
-    return dt, k, ncols * p.n_free * k
+    if phases is not None:
+        phases.update(t_assemble_s=t1 - t0, t_solve_s=t2 - t1, t_project_s=t3 - t2,
+                      iters=[int(x) for x in r["iters"]])
+    return t3 - t0, k, ncols * p.n_free * k
+
+
+def host_info():
+    """The host the oracle runs on (PAPER.md:1058-1062 states its cores and CPU the same way)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
 
 
 def run_reference(args, p, rank, world):
@@ -324,7 +346,8 @@ def run_reference(args, p, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_config(p),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": dict({"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+                                 **host_info()),
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -332,11 +355,14 @@ def run_reference(args, p, rank, world):
 def cpu_baseline(p):
     import oracle
     om = oracle.Mesh.from_problem(p)
-    dt, k, units = oracle_step(om, p, p.N)
-    return {"value": units / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{p.cfg['name']} full step once: assemble_veff + block PCG on all {p.N} orbitals "
-                      f"({k} iterations to tol {TOL:g}) + projection, single-threaded C oracle, {dt:.1f} s",
-            "seconds": dt}
+    ph = {}
+    dt, k, units = oracle_step(om, p, p.N, ph)
+    return dict({"value": units / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+                 "sample": f"{p.cfg['name']} full step once: assemble_veff + block PCG on all {p.N} orbitals "
+                           f"({k} iterations to tol {TOL:g}) + projection, single-threaded C oracle, {dt:.1f} s",
+                 "seconds": dt, "phases_s": {"assemble_veff": ph["t_assemble_s"], "block_solve": ph["t_solve_s"],
+                                             "project_augmented": ph["t_project_s"]},
+                 "oracle_iters": ph["iters"]}, **host_info())
 
 
 def rank_seed(config, rank):
@@ -371,45 +397,41 @@ def workload_config(p):
 # --------------------------------------------------------------------------------------------------
 # GPU arm
 # --------------------------------------------------------------------------------------------------
-def run_ours(args, p, rank, world, local):
+def setup_ctx(p, dev, stream):
     import torch
-    import torch.distributed as dist
 
     import paper_2404_19249_b200 as ks
-
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    stream = torch.cuda.Stream(device=dev)
-    torch.cuda.set_stream(stream)
     ctx = ks.Context(p.xyz, p.tets, p.dirichlet, stream=stream, max_N=p.N)
-    V = torch.from_numpy(p.V).to(dev)
-    lam = torch.from_numpy(p.lam).to(dev)
-    U = torch.from_numpy(p.U).to(dev)
-    Ut = torch.empty_like(U)
+    bufs = dict(V=torch.from_numpy(p.V).to(dev), lam=torch.from_numpy(p.lam).to(dev), U=torch.from_numpy(p.U).to(dev))
+    bufs["Ut"] = torch.empty_like(bufs["U"])
     D = p.n_H + p.N
-    FA = torch.empty((D, D), dtype=torch.float64, device=dev)
-    FB = torch.empty_like(FA)
-    iters = torch.zeros(p.N, dtype=torch.int32, device=dev)
-    relres = torch.zeros(p.N, dtype=torch.float64, device=dev)
+    bufs["FA"] = torch.empty((D, D), dtype=torch.float64, device=dev)
+    bufs["FB"] = torch.empty_like(bufs["FA"])
+    bufs["iters"] = torch.zeros(p.N, dtype=torch.int32, device=dev)
+    bufs["relres"] = torch.zeros(p.N, dtype=torch.float64, device=dev)
     ctx.set_coarse(p.n_H, torch.from_numpy(p.P_rowptr).to(dev), torch.from_numpy(p.P_col).to(dev),
                    torch.from_numpy(p.P_val).to(dev))
     torch.cuda.synchronize()
+    return ctx, bufs
+
+
+def device_steps(ctx, b, p, steps, warmup, stream, world, local):
+    """W untimed steps, then K steps timed on the device (CUDA events on the context's stream, per step and
+    per call), clocks sampled during the timed region. Returns a dict of the timings."""
+    import torch
+    import torch.distributed as dist
 
     def step():
-        ctx.assemble_veff(V, p.mu)
-        ctx.block_solve(lam, U, Ut, tol=TOL, max_iter=MAX_ITER, iters=iters, relres=relres)
-        ctx.project_augmented(Ut, FA, FB)
+        ctx.assemble_veff(b["V"], p.mu)
+        ctx.block_solve(b["lam"], b["U"], b["Ut"], tol=TOL, max_iter=MAX_ITER, iters=b["iters"], relres=b["relres"])
+        ctx.project_augmented(b["Ut"], b["FA"], b["FB"])
 
-    for _ in range(max(3, args.warmup)):
+    for _ in range(max(3, warmup)):
         step()
     st = ctx.sync()
     if st != 0:
         raise RuntimeError(f"warm-up status {st}: {ctx.last_error()}")
-    k_iters = ctx.last_iterations()
-
-    # ---- device-timed region ----
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(steps)]
     clocks = Clocks(local)
     if world > 1:
         dist.barrier()
@@ -420,14 +442,14 @@ def run_ours(args, p, rank, world, local):
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
-    for s in range(args.steps):
+    for s in range(steps):
         e0, e1, e2, e3 = ev[s]
         e0.record(stream)
-        ctx.assemble_veff(V, p.mu)
+        ctx.assemble_veff(b["V"], p.mu)
         e1.record(stream)
-        ctx.block_solve(lam, U, Ut, tol=TOL, max_iter=MAX_ITER, iters=iters, relres=relres)
+        ctx.block_solve(b["lam"], b["U"], b["Ut"], tol=TOL, max_iter=MAX_ITER, iters=b["iters"], relres=b["relres"])
         e2.record(stream)
-        ctx.project_augmented(Ut, FA, FB)
+        ctx.project_augmented(b["Ut"], b["FA"], b["FB"])
         e3.record(stream)
     t_end.record(stream)
     torch.cuda.synchronize()
@@ -438,15 +460,83 @@ def run_ours(args, p, rank, world, local):
     st = ctx.sync()
     if st != 0:
         raise RuntimeError(f"timed-run status {st}: {ctx.last_error()}")
-    total_ms = t_start.elapsed_time(t_end)
-    t_asm = float(np.mean([a.elapsed_time(b) for a, b, _, _ in ev]))
-    t_solve = float(np.mean([b.elapsed_time(c) for _, b, c, _ in ev]))
-    t_proj = float(np.mean([c.elapsed_time(d) for _, _, c, d in ev]))
-    k_last = ctx.last_iterations()
-    units_rank = args.steps * p.N * p.n_free * k_last
+    step_ms = np.array([a.elapsed_time(d) for a, _, _, d in ev])
+    asm = np.array([a.elapsed_time(c) for a, c, _, _ in ev])
+    solve = np.array([c.elapsed_time(d) for _, c, d, _ in ev])
+    proj = np.array([c.elapsed_time(d) for _, _, c, d in ev])
+    return dict(total_ms=t_start.elapsed_time(t_end), step_ms=step_ms, asm=asm, solve=solve, proj=proj,
+                launches=launches, clocks=clk, k=ctx.last_iterations())
 
-    total_ms_max, units_all = combine_ranks(total_ms, units_rank, world, dev)
+
+def stats(x):
+    return {"mean": float(np.mean(x)), "median": float(np.median(x)), "min": float(np.min(x))}
+
+
+def roofline(p, nnz, k, t_solve_ms, peak, peak_kind):
+    """Dominant kernel: the block PCG, one launch per solve. Algorithmic bytes of SURVEY.md §8(d) (textbook
+    Jacobi-PCG, 11 vector touches per iteration) divided by the event-timed solve."""
+    n, N = p.n_free, p.N
+    alg = bytes_solve_init(n, nnz, N) + k * bytes_per_iteration(n, nnz, N)
+    achieved = alg / (t_solve_ms * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", f"traffic_C{p.cfg['name'][1:]}.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    return {"bound": "hbm", "kernel": "k_block_pcg_fused (persistent block Jacobi-PCG, one launch per solve)",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "peak_kind": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)", "alg_bytes_per_launch": int(alg),
+            "alg_bytes_def": "init (20 nnz + 12 n + 32 N n) + k x textbook B_it (12 nnz + 20 n + 88 N n)"}
+
+
+def c5_record(dev, stream, local, peak, peak_kind, steps=5, warmup=3):
+    """The largest config (C5: 7.0 M free nodes, 103.6 M nonzeros, N = 32) measured like the headline, as a
+    sub-record of the default run: value, per-call times, its own roofline and PCG phases."""
+    import torch
+    try:
+        p = gen.make_problem(5)
+        ctx, b = setup_ctx(p, dev, stream)
+        r = device_steps(ctx, b, p, steps, warmup, stream, 1, local)
+        t_solve = float(np.mean(r["solve"]))
+        out = {"config": dict(workload_config(p), nnz=int(ctx.nnz), block_iters=int(r["k"])),
+               "value": steps * p.N * p.n_free * r["k"] / (r["total_ms"] * 1e-3), "unit": UNIT,
+               "steps": steps, "warmup": warmup, "ms_per_step": r["total_ms"] / steps,
+               "step_ms": stats(r["step_ms"]),
+               "phases_ms": {"assemble_veff": stats(r["asm"]), "block_solve": stats(r["solve"]),
+                             "project_augmented": stats(r["proj"])},
+               "roofline": roofline(p, ctx.nnz, r["k"], t_solve, peak, peak_kind),
+               "pcg_phases": traced_phases(ctx, lambda: ctx.block_solve(b["lam"], b["U"], b["Ut"], tol=TOL,
+                                                                        max_iter=MAX_ITER), p.n_free, ctx.nnz,
+                                           p.N, peak),
+               "clocks": r["clocks"]}
+        ctx.close()
+        del b
+        torch.cuda.empty_cache()
+        return out
+    except Exception as ex:   # reported, never fatal for the headline line
+        return {"error": str(ex)[:300]}
+
+
+def run_ours(args, p, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2404_19249_b200 as ks
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    ctx, b = setup_ctx(p, dev, stream)
+    r = device_steps(ctx, b, p, args.steps, args.warmup, stream, world, local)
+    t_asm, t_solve, t_proj = float(np.mean(r["asm"])), float(np.mean(r["solve"])), float(np.mean(r["proj"]))
+    k_last = r["k"]
+    units_rank = args.steps * p.N * p.n_free * k_last
+    total_ms_max, units_all = combine_ranks(r["total_ms"], units_rank, world, dev)
     value = units_all / (total_ms_max * 1e-3)
+    D = p.n_H + p.N
 
     # ---- e2e through the public API with host (pinned) buffers: ks_step_submit / ks_step_wait ----
     # every step copies its inputs (V, lambda, U) from pinned host memory and its result (F_A, F_B) back;
@@ -478,35 +568,26 @@ def run_ours(args, p, rank, world, local):
         return
     peaks, peak_kind = load_peaks()
     n, nnz, N = p.n_free, ctx.nnz, p.N
-    alg = bytes_solve_init(n, nnz, N) + k_last * bytes_per_iteration(n, nnz, N)
-    achieved = alg / (t_solve * 1e-3) / 1e9
     peak = float(peaks["hbm_gbs"])
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", f"traffic_C{p.cfg['name'][1:]}.json")
-    if os.path.exists(tf):
-        try:
-            traffic = json.load(open(tf)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": dict(workload_config(p), nnz=int(nnz), block_iters=int(k_last),
                        parallelism=f"independent problem per GPU x{world}" if world > 1 else "1 GPU"),
-        "roofline": {"bound": "hbm", "kernel": "k_block_pcg (persistent block Jacobi-PCG, one launch per solve)",
-                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_kind": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
-                     "alg_bytes_per_launch": int(alg),
-                     "alg_bytes_def": "init (20 nnz + 12 n + 32 N n) + k x textbook B_it (12 nnz + 20 n + 88 N n)"},
+        "roofline": roofline(p, nnz, k_last, t_solve, peak, peak_kind),
         "phases_ms": {"assemble_veff": t_asm, "block_solve": t_solve, "project_augmented": t_proj},
+        "step_ms": stats(r["step_ms"]),
+        "phases_ms_stats": {"assemble_veff": stats(r["asm"]), "block_solve": stats(r["solve"]),
+                            "project_augmented": stats(r["proj"])},
         "solve_only_value": N * n * k_last / (t_solve * 1e-3),
-        "next1_ms": next1_times(ctx, Ut, FA, FB, N, stream, p.lam, U),
-        "next23": next_rows(ctx, p, U, stream, peak),
-        "pcg_phases": traced_phases(ctx, lambda: ctx.block_solve(lam, U, Ut, tol=TOL, max_iter=MAX_ITER, iters=iters,
-                                                                 relres=relres), n, nnz, N, peak),
-        "gpu_launches": int(launches),
-        "clocks": clk,
+        "next1_ms": next1_times(ctx, b["Ut"], b["FA"], b["FB"], N, stream, p.lam, b["U"]),
+        "next23": next_rows(ctx, p, b["U"], stream, peak),
+        "pcg_phases": traced_phases(ctx, lambda: ctx.block_solve(b["lam"], b["U"], b["Ut"], tol=TOL, max_iter=MAX_ITER,
+                                                                 iters=b["iters"], relres=b["relres"]), n, nnz, N,
+                                    peak),
+        "gpu_launches": int(r["launches"]),
+        "clocks": r["clocks"],
     }
     if e2e is not None:
         line["e2e"] = e2e
@@ -516,6 +597,11 @@ def run_ours(args, p, rank, world, local):
         except Exception as ex:  # keep the GPU line even if the oracle cannot run
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle",
                                     "sample": f"failed: {ex}"}
+    if world == 1 and args.config == 4 and not args.no_c5:
+        ctx.close()
+        del b
+        torch.cuda.empty_cache()
+        line["c5"] = c5_record(dev, stream, local, peak, peak_kind)
     print(json.dumps(line), flush=True)
 
 

@@ -29,7 +29,9 @@ Layout conventions (the interface both sides agree on; see include/ks.h):
 """
 from __future__ import annotations
 
+import json
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -68,27 +70,24 @@ def _uniform(seed, stream, index, lo, hi):
 # ---------------------------------------------------------------------------------------------
 # configs (BASELINE.json "configs")
 # ---------------------------------------------------------------------------------------------
-_CH4_H = 1.09 / math.sqrt(3.0)
+_CONFIG_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "configs")
 
-CONFIGS = {
-    1: dict(name="C1", L=8.0, n=16, grading=None, jitter=0.15,
-            nuclei=[((0.0, 0.0, 0.0), 1)], vnoise=0.05, N=1, orbitals="exp",
-            lam=("const", -0.5), nc=4),
-    2: dict(name="C2", L=10.0, n=32, grading=("power", 1.5), jitter=0.1,
-            nuclei=[((0.7, 0.0, 0.0), 1), ((-0.7, 0.0, 0.0), 1)], vnoise=0.05, N=4,
-            orbitals="gauss", lam=("uniform", -1.0, -0.2), nc=6),
-    3: dict(name="C3", L=12.0, n=64, grading=("equi", 1.5), jitter=0.0,
-            nuclei=[((0.0, 0.0, 0.0), 6),
-                    ((_CH4_H, _CH4_H, _CH4_H), 1), ((-_CH4_H, -_CH4_H, _CH4_H), 1),
-                    ((_CH4_H, -_CH4_H, -_CH4_H), 1), ((-_CH4_H, _CH4_H, -_CH4_H), 1)],
-            vnoise=0.0, N=8, orbitals="gauss", lam=("uniform", -12.0, -0.3), nc=8),
-    4: dict(name="C4", L=16.0, n=128, grading=("equi", 1.8), jitter=0.0,
-            nuclei=("ball", 12, 6.0), vnoise=0.0, N=16, orbitals="gauss",
-            lam=("uniform", -20.0, -0.1), nc=10),
-    5: dict(name="C5", L=20.0, n=192, grading=("equi", 1.8), jitter=0.0,
-            nuclei=("ball", 32, 10.0), vnoise=0.02, N=32, orbitals="gauss",
-            lam=("uniform", -20.0, -0.1), nc=12),
-}
+
+def _load_config(c: int) -> dict:
+    """configs/c<c>.json (the single source of the five workloads; JSON lists back to the tuples gen uses)."""
+    with open(os.path.join(_CONFIG_DIR, f"c{c}.json")) as f:
+        d = json.load(f)
+    for k in ("description", "readings", "seed"):
+        d.pop(k, None)
+    if d.get("grading") is not None:
+        d["grading"] = tuple(d["grading"])
+    d["lam"] = tuple(d["lam"])
+    nuc = d["nuclei"]
+    d["nuclei"] = tuple(nuc) if nuc and nuc[0] == "ball" else [(tuple(x), z) for x, z in nuc]
+    return d
+
+
+CONFIGS = {c: _load_config(c) for c in (1, 2, 3, 4, 5)}
 
 
 def make_config(c: int, **overrides) -> dict:

@@ -4,8 +4,18 @@
 
 #include <mutex>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "ks_internal.cuh"
 #include "ks_layout.cuh"
+
+// NVTX range per ABI call (SURVEY.md §5 tracing): nsys / ncu timelines show each call by name. NVTX3 is
+// header-only; without a tool attached a push/pop costs a few nanoseconds.
+struct KsNvtx {
+  explicit KsNvtx(const char *name) { nvtxRangePushA(name); }
+  ~KsNvtx() { nvtxRangePop(); }
+};
+#define KS_RANGE() KsNvtx ks_nvtx_range_(__func__)
 
 static std::mutex g_err_mu;
 static std::string g_create_err;
@@ -125,6 +135,7 @@ static int device_sm_count() {
 ks_status ks_plan(int64_t n_nodes, const double *h_xyz, int64_t n_tets, const int32_t *h_tets,
                   const uint8_t *h_dirichlet, int32_t max_N, size_t *persistent_bytes, size_t *workspace_bytes,
                   size_t *setup_bytes) {
+  KS_RANGE();
   KS_TRY(check_mesh_args(n_nodes, h_xyz, n_tets, h_tets, h_dirichlet, max_N));
   if (!persistent_bytes || !workspace_bytes || !setup_bytes) {
     set_create_err("KS_E_ARG: ks_plan needs non-null size outputs");
@@ -151,6 +162,7 @@ ks_status ks_create(int64_t n_nodes, const double *h_xyz, int64_t n_tets, const 
                     const uint8_t *h_dirichlet, int32_t max_N, void *d_persistent, size_t persistent_bytes,
                     void *d_workspace, size_t workspace_bytes, void *d_setup, size_t setup_bytes, void *stream,
                     ks_ctx **out) {
+  KS_RANGE();
   if (!out) return KS_E_ARG;
   *out = nullptr;
   KS_TRY(check_mesh_args(n_nodes, h_xyz, n_tets, h_tets, h_dirichlet, max_N));
@@ -198,6 +210,7 @@ ks_status ks_create(int64_t n_nodes, const double *h_xyz, int64_t n_tets, const 
 }
 
 void ks_destroy(ks_ctx *ctx) {
+  KS_RANGE();
   if (!ctx) return;
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   else cudaDeviceSynchronize();
@@ -206,6 +219,7 @@ void ks_destroy(ks_ctx *ctx) {
 }
 
 ks_status ks_set_stream(ks_ctx *ctx, void *stream) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   cudaStream_t ns = (cudaStream_t)stream;
   if (ns == ctx->stream) return KS_OK;
@@ -238,6 +252,7 @@ ks_status ks_pattern(const ks_ctx *ctx, int64_t *n_free, int64_t *nnz, const int
 
 ks_status ks_values(const ks_ctx *ctx, const double **d_K, const double **d_M, const double **d_MV,
                     const double **d_H, const double **d_A, const double **d_diag) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   if (d_K) *d_K = ctx->K;
   if (d_M) *d_M = ctx->M;
@@ -255,6 +270,7 @@ ks_status ks_values(const ks_ctx *ctx, const double **d_K, const double **d_M, c
 }
 
 ks_status ks_assemble_veff(ks_ctx *ctx, const double *d_veff, double mu) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   if (!d_veff) return ks_fail(ctx, KS_E_ARG, "ks_assemble_veff: d_veff is NULL");
   if (!(mu >= 0.0) || !isfinite(mu)) return ks_fail(ctx, KS_E_ARG, "ks_assemble_veff: mu = %g must be finite and >= 0", mu);
@@ -273,6 +289,7 @@ static const double *op_values(const ks_ctx *ctx, ks_op op) {
 }
 
 ks_status ks_spmm(ks_ctx *ctx, ks_op op, int32_t N, const double *d_X, double *d_Y) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   if (N < 1 || N > KS_MAX_N) return ks_fail(ctx, KS_E_ARG, "ks_spmm: N = %d outside [1, %d]", N, KS_MAX_N);
   if (!d_X || !d_Y || d_X == d_Y) return ks_fail(ctx, KS_E_ARG, "ks_spmm: X, Y must be distinct non-null");
@@ -287,6 +304,7 @@ ks_status ks_spmm(ks_ctx *ctx, ks_op op, int32_t N, const double *d_X, double *d
 
 ks_status ks_block_solve(ks_ctx *ctx, int32_t N, const double *d_lambda, const double *d_U, double *d_Ut,
                          double tol, int32_t max_iter, int32_t *d_iters, double *d_relres) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   if (N < 1 || N > KS_MAX_N) return ks_fail(ctx, KS_E_ARG, "ks_block_solve: N = %d outside [1, %d]", N, KS_MAX_N);
   if (!d_lambda || !d_U || !d_Ut) return ks_fail(ctx, KS_E_ARG, "ks_block_solve: null lambda/U/Ut");
@@ -299,6 +317,7 @@ ks_status ks_block_solve(ks_ctx *ctx, int32_t N, const double *d_lambda, const d
 }
 
 ks_status ks_last_iterations(ks_ctx *ctx, int32_t *h_block_iters) {
+  KS_RANGE();
   if (!ctx || !h_block_iters) return KS_E_ARG;
   KS_CUDA(ctx, cudaMemcpyAsync(h_block_iters, ctx->d_block_iters, 4, cudaMemcpyDeviceToHost, ctx->stream));
   KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -307,6 +326,7 @@ ks_status ks_last_iterations(ks_ctx *ctx, int32_t *h_block_iters) {
 
 ks_status ks_pencil_eig(ks_ctx *ctx, int64_t D, int32_t k, const double *d_FA, const double *d_FB, double *d_evals,
                         double *d_evecs) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   if (D < 1 || k < 1 || k > D || D > 65536) return ks_fail(ctx, KS_E_ARG, "ks_pencil_eig: need 1 <= k <= D <= 65536");
   if (!d_FA || !d_FB || !d_evals || !d_evecs) return ks_fail(ctx, KS_E_ARG, "ks_pencil_eig: null pointer");
@@ -314,6 +334,7 @@ ks_status ks_pencil_eig(ks_ctx *ctx, int64_t D, int32_t k, const double *d_FA, c
 }
 
 ks_status ks_lift(ks_ctx *ctx, int32_t N, const double *d_Ut, int32_t k, const double *d_Y, double *d_Unew) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   if (N < 1 || N > KS_MAX_N || k < 1 || !d_Ut || !d_Y || !d_Unew || d_Ut == d_Unew)
     return ks_fail(ctx, KS_E_ARG, "ks_lift: bad arguments");
@@ -323,6 +344,7 @@ ks_status ks_lift(ks_ctx *ctx, int32_t N, const double *d_Ut, int32_t k, const d
 
 ks_status ks_augmented_solve(ks_ctx *ctx, int32_t N, double *d_lambda, double *d_U, double tol_eig, int32_t max_outer,
                              double tol_bvp, int32_t max_iter_bvp, int32_t *h_outer, double *h_history) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   if (N < 1 || N > KS_MAX_N || !d_lambda || !d_U || !(tol_eig >= 0.0) || max_outer < 1 || !(tol_bvp > 0.0) ||
       max_iter_bvp < 1)
@@ -334,6 +356,7 @@ ks_status ks_augmented_solve(ks_ctx *ctx, int32_t N, double *d_lambda, double *d
 
 ks_status ks_interpolation_plan(ks_ctx *ctx, int64_t n_c, const double *h_xyz_c, int64_t m_c,
                                 size_t *work_bytes) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   if (n_c < 4 || m_c < 1 || n_c > 0x7fffffffLL || m_c > 0x7fffffffLL || !h_xyz_c || !work_bytes)
     return ks_fail(ctx, KS_E_ARG, "ks_interpolation_plan: bad arguments");
@@ -343,6 +366,7 @@ ks_status ks_interpolation_plan(ks_ctx *ctx, int64_t n_c, const double *h_xyz_c,
 ks_status ks_interpolation(ks_ctx *ctx, int64_t n_c, const double *h_xyz_c, int64_t m_c, const int32_t *h_tets_c,
                            const uint8_t *h_dirichlet_c, void *d_work, size_t work_bytes, int32_t *d_P_row_ptr,
                            int32_t *d_P_col, double *d_P_val, int64_t *h_n_H, int64_t *h_p_nnz) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   if (n_c < 4 || m_c < 1 || n_c > 0x7fffffffLL || m_c > 0x7fffffffLL || !h_xyz_c || !h_tets_c || !h_dirichlet_c ||
       !d_work || !d_P_row_ptr || !d_P_col || !d_P_val || !h_n_H || !h_p_nnz)
@@ -352,12 +376,14 @@ ks_status ks_interpolation(ks_ctx *ctx, int64_t n_c, const double *h_xyz_c, int6
 }
 
 ks_status ks_density(ks_ctx *ctx, int32_t N, const double *d_U, double f, double *d_rho) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   if (N < 1 || N > KS_MAX_N || !d_U || !d_rho || !(f >= 0.0)) return ks_fail(ctx, KS_E_ARG, "ks_density: bad arguments");
   return ks_density_impl(ctx, N, d_U, f, d_rho);
 }
 
 ks_status ks_vxc(ks_ctx *ctx, const double *d_rho, double *d_vxc, double *d_eps) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   if (!d_rho || !d_vxc) return ks_fail(ctx, KS_E_ARG, "ks_vxc: null pointer");
   return ks_vxc_impl(ctx, d_rho, d_vxc, d_eps);
@@ -365,6 +391,7 @@ ks_status ks_vxc(ks_ctx *ctx, const double *d_rho, double *d_vxc, double *d_eps)
 
 ks_status ks_hartree(ks_ctx *ctx, const double *d_rho, double tol, int32_t max_iter, double *d_vh, int32_t warm,
                      double *h_mom, int32_t *h_iters) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   if (!d_rho || !d_vh || !(tol > 0.0) || max_iter < 1) return ks_fail(ctx, KS_E_ARG, "ks_hartree: bad arguments");
   return ks_hartree_impl(ctx, d_rho, tol, max_iter, d_vh, warm, h_mom, h_iters);
@@ -374,6 +401,7 @@ ks_status ks_scf_solve(ks_ctx *ctx, int32_t N, const double *d_vext, double f, d
                        double *d_U, double tol, int32_t max_outer, int32_t inner, double inner_tol, double beta,
                        int32_t depth, double bvp_tol, double hartree_tol, int32_t *h_outer, int32_t *h_inner,
                        double *h_dres, double *h_lams) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   if (N < 1 || N > KS_MAX_N || !d_vext || !d_lambda || !d_U || !(f >= 0.0) || !(mu >= 0.0) || !(tol > 0.0) ||
       max_outer < 1 || inner < 1 || !(inner_tol > 0.0) || !(beta > 0.0 && beta <= 1.0) || depth < 1 || depth > 7 ||
@@ -386,6 +414,7 @@ ks_status ks_scf_solve(ks_ctx *ctx, int32_t N, const double *d_vext, double f, d
 
 ks_status ks_step_submit(ks_ctx *ctx, int32_t N, const double *h_V, double mu, const double *h_lambda,
                          const double *h_U, double tol, int32_t max_iter, double *h_FA, double *h_FB) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   if (N < 1 || N > KS_MAX_N || !h_V || !h_lambda || !h_U || !h_FA || !h_FB || !(tol > 0.0) || max_iter < 1 ||
       !(mu >= 0.0))
@@ -395,11 +424,13 @@ ks_status ks_step_submit(ks_ctx *ctx, int32_t N, const double *h_V, double mu, c
 }
 
 ks_status ks_step_wait(ks_ctx *ctx) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   return ks_step_wait_impl(ctx);
 }
 
 ks_status ks_solve_trace(ks_ctx *ctx, int32_t cap, uint64_t *h_ns, int32_t *h_count) {
+  KS_RANGE();
   if (!ctx || !h_count || (cap > 0 && !h_ns)) return KS_E_ARG;
   *h_count = 0;
   if (!ctx->trace) return KS_OK;
@@ -417,6 +448,7 @@ ks_status ks_solve_trace(ks_ctx *ctx, int32_t cap, uint64_t *h_ns, int32_t *h_co
 
 ks_status ks_true_residual(ks_ctx *ctx, int32_t N, const double *d_lambda, const double *d_U, const double *d_Ut,
                            double *d_relres) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   if (N < 1 || N > KS_MAX_N || !d_lambda || !d_U || !d_Ut || !d_relres)
     return ks_fail(ctx, KS_E_ARG, "ks_true_residual: bad arguments");
@@ -433,6 +465,7 @@ static ks_status check_coarse_args(ks_ctx *ctx, int64_t n_H, const int32_t *d_P_
 
 ks_status ks_coarse_plan(ks_ctx *ctx, int64_t n_H, const int32_t *d_P_row_ptr, const int32_t *d_P_col,
                          const double *d_P_val, size_t *coarse_bytes) {
+  KS_RANGE();
   if (!ctx || !coarse_bytes) return KS_E_ARG;
   KS_TRY(check_coarse_args(ctx, n_H, d_P_row_ptr, d_P_col, d_P_val));
   return ks_set_coarse_impl(ctx, n_H, d_P_row_ptr, d_P_col, d_P_val, true, coarse_bytes);
@@ -440,6 +473,7 @@ ks_status ks_coarse_plan(ks_ctx *ctx, int64_t n_H, const int32_t *d_P_row_ptr, c
 
 ks_status ks_set_coarse(ks_ctx *ctx, int64_t n_H, const int32_t *d_P_row_ptr, const int32_t *d_P_col,
                         const double *d_P_val, void *d_coarse, size_t coarse_bytes) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   KS_TRY(check_coarse_args(ctx, n_H, d_P_row_ptr, d_P_col, d_P_val));
   if (!d_coarse) return ks_fail(ctx, KS_E_ARG, "ks_set_coarse: null coarse region (size from ks_coarse_plan)");
@@ -475,6 +509,7 @@ static ks_status ext_sizes(ks_ctx *ctx, uint32_t features, int64_t max_D, KsExtS
 }
 
 ks_status ks_ext_plan(ks_ctx *ctx, uint32_t features, int64_t max_D, size_t *ext_bytes) {
+  KS_RANGE();
   if (!ctx || !ext_bytes) return KS_E_ARG;
   if (features == 0 || (features & ~(uint32_t)(KS_EXT_EIG | KS_EXT_SCF | KS_EXT_STEP)))
     return ks_fail(ctx, KS_E_ARG, "ks_ext_plan: features must be a nonempty KS_EXT_* mask");
@@ -489,6 +524,7 @@ ks_status ks_ext_plan(ks_ctx *ctx, uint32_t features, int64_t max_D, size_t *ext
 }
 
 ks_status ks_attach_ext(ks_ctx *ctx, uint32_t features, int64_t max_D, void *d_ext, size_t ext_bytes) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   if (features == 0 || (features & ~(uint32_t)(KS_EXT_EIG | KS_EXT_SCF | KS_EXT_STEP)) || !d_ext || max_D < 0 ||
       max_D > 65536)
@@ -516,6 +552,7 @@ ks_status ks_attach_ext(ks_ctx *ctx, uint32_t features, int64_t max_D, void *d_e
 }
 
 ks_status ks_project_augmented(ks_ctx *ctx, int32_t N, const double *d_Ut, double *d_FA, double *d_FB) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   if (N < 1 || N > KS_MAX_N) return ks_fail(ctx, KS_E_ARG, "ks_project_augmented: N = %d outside [1, %d]", N, KS_MAX_N);
   if (!d_Ut || !d_FA || !d_FB || d_FA == d_FB) return ks_fail(ctx, KS_E_ARG, "ks_project_augmented: bad pointers");
@@ -541,6 +578,7 @@ static ks_status check_slab(ks_ctx *ctx, int32_t NP, int64_t row0, int64_t row1,
 
 ks_status ks_slab_init(ks_ctx *ctx, int32_t NP, int64_t row0, int64_t row1, const double *d_lambda, const double *d_U,
                        double *d_Z, double *d_P, double *d_dots) {
+  KS_RANGE();
   const void *p[] = {d_U, d_Z, d_P};
   KS_TRY(check_slab(ctx, NP, row0, row1, p, 3));
   if (!d_lambda || !d_dots) return ks_fail(ctx, KS_E_ARG, "ks_slab_init: null lambda / dots");
@@ -551,6 +589,7 @@ ks_status ks_slab_init(ks_ctx *ctx, int32_t NP, int64_t row0, int64_t row1, cons
 ks_status ks_slab_spmm(ks_ctx *ctx, int32_t NP, int64_t row0, int64_t row1, int32_t first, const double *h_alpha_x,
                        const double *h_beta, const double *d_Z, double *d_Q, double *d_P, const double *d_Xin,
                        double *d_X, double *d_dots) {
+  KS_RANGE();
   const void *p[] = {d_Z, d_Q, d_P, d_Xin, d_X};
   KS_TRY(check_slab(ctx, NP, row0, row1, p, 5));
   if (!h_alpha_x || !h_beta || !d_dots) return ks_fail(ctx, KS_E_ARG, "ks_slab_spmm: null coefficients / dots");
@@ -560,6 +599,7 @@ ks_status ks_slab_spmm(ks_ctx *ctx, int32_t NP, int64_t row0, int64_t row1, int3
 
 ks_status ks_slab_update(ks_ctx *ctx, int32_t NP, int64_t row0, int64_t row1, const double *h_alpha, double *d_Z,
                          const double *d_Q, double *d_dots) {
+  KS_RANGE();
   const void *p[] = {d_Z, d_Q};
   KS_TRY(check_slab(ctx, NP, row0, row1, p, 2));
   if (!h_alpha || !d_dots) return ks_fail(ctx, KS_E_ARG, "ks_slab_update: null coefficients / dots");
@@ -569,6 +609,7 @@ ks_status ks_slab_update(ks_ctx *ctx, int32_t NP, int64_t row0, int64_t row1, co
 
 ks_status ks_slab_finish(ks_ctx *ctx, int32_t NP, int64_t row0, int64_t row1, const double *h_alpha_x,
                          const double *d_P, const double *d_Xin, double *d_X) {
+  KS_RANGE();
   const void *p[] = {d_P, d_Xin, d_X};
   KS_TRY(check_slab(ctx, NP, row0, row1, p, 3));
   if (!h_alpha_x) return ks_fail(ctx, KS_E_ARG, "ks_slab_finish: null coefficients");
@@ -599,6 +640,7 @@ ks_status ks_launch_count(const ks_ctx *ctx, int64_t *count) {
 }
 
 ks_status ks_sync(ks_ctx *ctx) {
+  KS_RANGE();
   if (!ctx) return KS_E_ARG;
   cudaError_t e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) return ks_cuda_check(ctx, e, "cudaStreamSynchronize");

@@ -358,6 +358,9 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
 #ifndef KS_PCG_PREFETCH
 #define KS_PCG_PREFETCH 1
 #endif
+#ifndef KS_PCG_CONTIG
+#define KS_PCG_CONTIG 0   // fused kernel: contiguous tile chunks per block instead of interleaved tiles
+#endif
 #ifndef KS_PCG_PFDIST
 #define KS_PCG_PFDIST 1   // tiles ahead
 #endif
@@ -452,6 +455,15 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
   extern __shared__ __align__(128) unsigned char dyn[];
   __shared__ __align__(8) uint64_t s_full[2];
   unsigned pseq = 0;                        // stage uses so far (stage pseq & 1, parity (pseq >> 1) & 1)
+  // the k-th row tile (= U/P chunk) of this block: interleaved over the blocks (t = b + k G, one sweeping
+  // front of gathers, KS_PCG_CONTIG=0) or contiguous chunks (t = b per + k: consecutive tiles of a block are
+  // grid neighbours, their gathers reuse L1)
+  const int tper = (a.ntiles + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int64_t my_tiles = KS_PCG_CONTIG ? max(0, min(tper, a.ntiles - (int)blockIdx.x * tper))
+                                         : (a.ntiles > (int)blockIdx.x ? (a.ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0);
+  auto tile_k = [&](int64_t kk) -> int64_t {
+    return KS_PCG_CONTIG ? (int64_t)blockIdx.x * tper + kk : (int64_t)blockIdx.x + kk * gridDim.x;
+  };
 
   __shared__ double red[PCG_WARPS * 3 * NP];
   __shared__ double tot[3 * NP];
@@ -499,8 +511,8 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
       const int c = sub * VEC + v;
       sh[v] = (c < a.N ? __ldg(a.lambda + c) : 0.0) + a.mu;
     }
-    for (int tile = blockIdx.x; tile < a.ntiles; tile += G) {
-      const int64_t row = (int64_t)tile * TILE + warp * RPW + slot;
+    for (int64_t kk = 0; kk < my_tiles; kk++) {
+      const int64_t row = tile_k(kk) * TILE + warp * RPW + slot;
       if (row < n) {
         DV<VEC> au, mu_;
         sell_row<NP, 2>(a.sell_ptr, a.sell_col, a.A, a.M, row, a.U, sub, au, mu_);
@@ -568,10 +580,10 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
         const double *xin = xwritten ? a.X : a.U;
         if (STG && !first) {
           // ---- staged: tile k of this block in stage (pseq + k) & 1 ----
-          const int64_t my = a.ntiles > (int)blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / G + 1 : 0;
+          const int64_t my = my_tiles;
           const unsigned EB = (unsigned)a.emax;
           auto issue = [&](int64_t k) {   // one thread: the bulk copies of tile k
-            const int64_t r0 = ((int64_t)blockIdx.x + k * G) * TILE;
+            const int64_t r0 = tile_k(k) * TILE;
             const int64_t rows = min((int64_t)TILE, n - r0);
             const int32_t e0 = __ldg(a.sell_ptr + r0 / KS_SELL_C);
             const int32_t e1 = __ldg(a.sell_ptr + (r0 + rows + KS_SELL_C - 1) / KS_SELL_C);
@@ -599,7 +611,7 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
             const double *vs = reinterpret_cast<const double *>(st);
             const int32_t *cs = reinterpret_cast<const int32_t *>(st + 8u * EB);
             const double *qs = reinterpret_cast<const double *>(st + 12u * EB);
-            const int64_t t = (int64_t)blockIdx.x + k * G;
+            const int64_t t = tile_k(k);
             const int lr = warp * RPW + slot;
             const int64_t row = t * TILE + lr;
             if (row < n) {
@@ -639,11 +651,11 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
         constexpr bool PF = KS_PCG_PREFETCH && NP >= 4;
         if (PF && lane == 0)
           for (int d = 0; d < KS_PCG_PFDIST; d++)
-            prefetch_rows<NP, RPW>(a, (int64_t)(blockIdx.x + d * G) * TILE + warp * RPW, xin, !first);
-        for (int tile = blockIdx.x; tile < a.ntiles; tile += G) {
-          const int64_t row = (int64_t)tile * TILE + warp * RPW + slot;
-          if (PF && lane == 0)
-            prefetch_rows<NP, RPW>(a, (int64_t)(tile + KS_PCG_PFDIST * G) * TILE + warp * RPW, xin, !first);
+            if (d < my_tiles) prefetch_rows<NP, RPW>(a, tile_k(d) * TILE + warp * RPW, xin, !first);
+        for (int64_t kk = 0; kk < my_tiles; kk++) {
+          const int64_t row = tile_k(kk) * TILE + warp * RPW + slot;
+          if (PF && lane == 0 && kk + KS_PCG_PFDIST < my_tiles)
+            prefetch_rows<NP, RPW>(a, tile_k(kk + KS_PCG_PFDIST) * TILE + warp * RPW, xin, !first);
           if (row < n) {
             DV<VEC> w, unused;
             sell_row<NP, 1>(a.sell_ptr, a.sell_col, a.A, nullptr, row, Z, sub, w, unused);
@@ -703,7 +715,8 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
           al[v] = s_alpha[cb + v];
           acc[0][v] = acc[1][v] = 0.0;
         }
-        for (int ch = blockIdx.x; ch < nchunks; ch += G) {
+        for (int64_t kk = 0; kk < my_tiles; kk++) {
+          const int64_t ch = tile_k(kk);
           const int64_t e = (int64_t)ch * CHUNK + VEC * threadIdx.x;
           if (e < nel) {
             DV<VEC> z = DV<VEC>::ld(Z + e);
@@ -770,7 +783,8 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
 #pragma unroll
     for (int v = 0; v < VEC; v++) xa[v] = s_xalpha[cb + v];
     const double *xin = xwritten ? a.X : a.U;
-    for (int ch = blockIdx.x; ch < nchunks; ch += G) {
+    for (int64_t kk = 0; kk < my_tiles; kk++) {
+          const int64_t ch = tile_k(kk);
       const int64_t e = (int64_t)ch * CHUNK + VEC * threadIdx.x;
       if (e < nel) {
         DV<VEC> x = DV<VEC>::ld(xin + e);
@@ -869,7 +883,7 @@ ks_status launch_pcg(ks_ctx *ctx, PcgArgs &a) {
   // Hartree solve (given B, up to ~10^3 iterations to 1e-12) keeps the three-phase recurrences
   const char *fz = getenv("KS_PCG_FUSED");
   if (a.B || (fz && fz[0] == '0')) return launch_pcg_t<NP, false, false>(ctx, a, 0);
-  if constexpr (NP >= 4 && KS_PCG_STAGED) {
+  if constexpr (NP >= 4 && NP <= 16 && KS_PCG_STAGED) {   // measured slower at NP = 32 (C5, r02g)
     const char *sg = getenv("KS_PCG_STAGED");
     if (!(sg && sg[0] == '0')) {
       int &em = ctx->tile_emax[__builtin_ctz(NP)];
