@@ -534,6 +534,9 @@ ks_status ks_attach_ext(ks_ctx *ctx, uint32_t features, int64_t max_D, void *d_e
   KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   ctx->ext_features = 0;
   ctx->har2l_state = 0;
+  ctx->ef_LH_state = 0;
+  ctx->ef_L_D = 0;
+  ctx->ef_LH = ctx->ef_LHinv = ctx->ef_Linv = ctx->ef_TD = ctx->ef_aux = nullptr;
   KS_TRY(bind_region(ctx, KS_R_EXT, d_ext, ext_bytes, "d_ext"));
   {
     KsRegion rg(ctx, KS_R_EXT);

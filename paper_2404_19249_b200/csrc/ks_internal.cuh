@@ -146,6 +146,11 @@ struct ks_ctx {
   double *ef_buf = nullptr;         // [4][D][m] work blocks of the filtered eigensolver
   double *ef_small = nullptr;       // [m][m] device staging of the small Rayleigh-Ritz / SVQB matrices
   int64_t ef_L_D = 0;                // D of the Cholesky factor held in eig_B (0: none)
+  // cached Cholesky factor of the coarse block B_H (ks_outer.cu coarse_chol_reduction), per coarse space
+  int ef_LH_state = 0;              // 0: not built, 1: built, -1: unusable
+  double *ef_LH = nullptr, *ef_LHinv = nullptr;   // [n_H][n_H]
+  double *ef_Linv = nullptr, *ef_TD = nullptr;    // [D][D] L^-1, GEMM temporary
+  double *ef_aux = nullptr;                       // Kt, S, L_S^-1, T and a counter
   double *eig_A = nullptr, *eig_B = nullptr, *eig_w = nullptr, *eig_work = nullptr;
   int *eig_info = nullptr;
   double *outer_Ut = nullptr, *outer_FA = nullptr, *outer_FB = nullptr, *outer_Y = nullptr, *outer_lam = nullptr;

@@ -222,6 +222,13 @@ void ks_layout_ext(A &a, ks_ctx *c, const KsExtSizes &e) {
     a.add(&c->ef_buf, 4 * D * m, "filtered eig blocks");
     a.add(&c->ef_small, 2 * m * m + m + 1, "filtered eig small");
     a.add(&c->blas_ws, (int64_t)KS_EXT_BLAS_WS, "cuBLAS workspace");
+    if (e.nH > 0) {   // cached coarse factor and the explicit L^-1 of the fast reduction
+      a.add(&c->ef_LH, e.nH * e.nH, "L_H");
+      a.add(&c->ef_LHinv, e.nH * e.nH, "L_H^-1");
+      a.add(&c->ef_Linv, D * D, "L^-1");
+      a.add(&c->ef_TD, D * D, "reduction temporary");
+      a.add(&c->ef_aux, 2 * e.nH * N + 2 * N * N + 8, "Schur pieces");
+    }
     a.add(&c->outer_Ut, e.nf * N, "outer U~");
     a.add(&c->outer_FA, D * D, "outer F_A");
     a.add(&c->outer_FB, D * D, "outer F_B");

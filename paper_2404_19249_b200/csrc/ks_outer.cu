@@ -296,6 +296,51 @@ __global__ void k_cheb(const double *__restrict__ CY, const double *__restrict__
   Yn[x] = alpha * (CY[x] - c * Y[x]) + (Xp ? beta * Xp[x] : 0.0);
 }
 
+// number of entries of the leading n x n block of F (column-major, ld D) that differ from B (n x n)
+__global__ void k_block_mismatch(const double *__restrict__ F, int64_t D, const double *__restrict__ B, int64_t n,
+                                 int *__restrict__ count) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  bool bad = false;
+  if (x < n * n) bad = F[(x / n) * D + x % n] != B[x];
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicAdd(count, 1);
+}
+
+// explicit L = [[L_H, 0], [K, L_S]] and L^-1 = [[L_H^-1, 0], [BL, L_S^-1]] (D x D, column-major, upper zero)
+// from the cached coarse factor and the Schur-complement pieces (K = Kt^T, Kt [nH][Nc] column-major)
+__global__ void k_build_L(const double *__restrict__ LH, const double *__restrict__ LHinv, const double *__restrict__ Kt,
+                          const double *__restrict__ LS, const double *__restrict__ LSinv, int64_t nH, int64_t Nc,
+                          double *__restrict__ L, double *__restrict__ Linv) {
+  const int64_t D = nH + Nc;
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= D * D) return;
+  const int64_t i = x % D, j = x / D;   // row, column
+  double l = 0.0, li = 0.0;
+  if (i >= j) {
+    if (j < nH && i < nH) {
+      l = LH[j * nH + i];
+      li = LHinv[j * nH + i];
+    } else if (j < nH) {         // bottom-left: K (L^-1's block is written by a GEMM afterwards)
+      l = Kt[(i - nH) * nH + j];
+    } else {
+      l = LS[(j - nH) * Nc + (i - nH)];
+      li = LSinv[(j - nH) * Nc + (i - nH)];
+    }
+  }
+  L[x] = l;
+  Linv[x] = li;
+}
+
+__global__ void k_lower_only(double *__restrict__ A, int64_t n) {   // zero the strict upper triangle
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= n * n) return;
+  if (x % n < x / n) A[x] = 0.0;
+}
+
+__global__ void k_identity(double *__restrict__ A, int64_t n) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x < n * n) A[x] = (x % n == x / n) ? 1.0 : 0.0;
+}
+
 // T[j * D + i] = Y[i * k + j] for the first k columns of a column-major D x m block (Y row-major D x k)
 __global__ void k_put_cols(const double *__restrict__ Y, int64_t D, int k, double *__restrict__ T) {
   const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -341,7 +386,7 @@ static ks_status ensure_blas(ks_ctx *ctx) {
 // the filtered path on ctx->eig_A (A, overwritten by C) and ctx->eig_B (B, overwritten by L), after potrf.
 // *done = false: not converged (the caller runs the dense path on fresh copies)
 static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *evals, double *evecs, bool *done,
-                                     const double *Ywarm) {
+                                     const double *Ywarm, const double *Linv) {
   *done = false;
   KS_TRY(ensure_blas(ctx));
   cublasHandle_t hb = (cublasHandle_t)ctx->cublas;
@@ -349,11 +394,19 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
   const int m = k + EF_GUARD;
   const double one = 1.0, zero = 0.0;
   double *A = ctx->eig_A, *L = ctx->eig_B;
-  // C = L^-1 A L^-T (in A)
-  KS_BLAS(ctx, cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)D,
-                           (int)D, &one, L, (int)D, A, (int)D));
-  KS_BLAS(ctx, cublasDtrsm(hb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)D,
-                           (int)D, &one, L, (int)D, A, (int)D));
+  // C = L^-1 A L^-T (in A): two GEMMs with the explicit inverse when it is given (the coarse block's factor is
+  // cached, ks_pencil_eig_impl), else two triangular solves
+  if (Linv) {
+    KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, (int)D, (int)D, &one, Linv, (int)D, A, (int)D, &zero,
+                             ctx->ef_TD, (int)D));
+    KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, (int)D, (int)D, (int)D, &one, ctx->ef_TD, (int)D, Linv,
+                             (int)D, &zero, A, (int)D));
+  } else {
+    KS_BLAS(ctx, cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)D,
+                             (int)D, &one, L, (int)D, A, (int)D));
+    KS_BLAS(ctx, cublasDtrsm(hb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)D,
+                             (int)D, &one, L, (int)D, A, (int)D));
+  }
   // ef_buf [4][D][m], ef_small [2 m m + m + 1] (two m x m Grams, then V and lambda): the extension workspace
   // holds them for m <= max_N + EF_GUARD and D <= ext_D (ks_pencil_eig_impl routes larger k to the dense path)
   double *X = ctx->ef_buf, *CX = X + D * m, *T1 = CX + D * m, *T2 = T1 + D * m, *sm = ctx->ef_small;
@@ -484,8 +537,14 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
       KS_CUDA(ctx, cudaMemcpyAsync(sm, Tm.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice, st));
       KS_CUDA(ctx, cudaMemcpyAsync(sm + (int64_t)m * m, lam.data(), sizeof(double) * m, cudaMemcpyHostToDevice, st));
       KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, m, &one, X, (int)D, sm, m, &zero, T1, (int)D));
-      KS_BLAS(ctx, cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)D, k,
-                               &one, L, (int)D, T1, (int)D));
+      if (Linv) {   // y = L^-T x
+        KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, (int)D, k, (int)D, &one, Linv, (int)D, T1, (int)D, &zero,
+                                 T2, (int)D));
+        std::swap(T1, T2);
+      } else {
+        KS_BLAS(ctx, cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)D,
+                                 k, &one, L, (int)D, T1, (int)D));
+      }
       KS_CUDA(ctx, cudaMemcpyAsync(evals, sm + (int64_t)m * m, sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
       k_take_evecs<<<ks_blocks(D * k, 256), 256, 0, st>>>(T1, D, k, evecs);
       KS_LAUNCHED(ctx);
@@ -518,6 +577,87 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
   return KS_OK;
 }
 
+// The pencil of ks_project_augmented has F_B = [[B_H, c], [c^T, gamma]] with B_H = P^T M P fixed per coarse space.
+// Its Cholesky factor is L = [[L_H, 0], [K, L_S]] with L_H = chol(B_H) (cached once per coarse space, with
+// L_H^-1), K = c^T L_H^-T and L_S = chol(gamma - K K^T) (N x N), so L and L^-1 are formed in O(n_H^2 N) and
+// the reduction C = L^-1 F_A L^-T takes two GEMMs instead of a D x D factorisation and two triangular solves
+// (DESIGN.md §8.2). Returns false (caller: the general path) when the leading block of F_B is not bitwise the
+// cached B_H, N > max_N, or a factor is not positive definite. eig_B <- L, ctx->ef_Linv <- L^-1.
+static ks_status coarse_chol_reduction(ks_ctx *ctx, int64_t D, const double *FB, bool *ok) {
+  *ok = false;
+  const int64_t nH = ctx->n_H, Nc = D - nH;
+  if (nH < 1 || Nc < 1 || Nc > ctx->max_N || !ctx->ef_LH || !ctx->B_H) return KS_OK;
+  KS_TRY(ensure_blas(ctx));
+  cublasHandle_t hb = (cublasHandle_t)ctx->cublas;
+  cusolverDnHandle_t h = (cusolverDnHandle_t)ctx->cusolver;
+  cudaStream_t st = ctx->stream;
+  const double one = 1.0, mone = -1.0, zero = 0.0;
+  int lw = 0;
+  if (ctx->ef_LH_state == 0) {   // once per coarse space: L_H = chol(B_H), L_H^-1
+    ctx->ef_LH_state = -1;
+    KS_CUDA(ctx, cudaMemcpyAsync(ctx->ef_LH, ctx->B_H, sizeof(double) * nH * nH, cudaMemcpyDeviceToDevice, st));
+    if (cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, (int)nH, ctx->ef_LH, (int)nH, &lw) !=
+            CUSOLVER_STATUS_SUCCESS || lw > ctx->ext_lwork)
+      return KS_OK;
+    if (cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, (int)nH, ctx->ef_LH, (int)nH, ctx->eig_work, lw, ctx->eig_info) !=
+        CUSOLVER_STATUS_SUCCESS)
+      return KS_OK;
+    ctx->launches++;
+    int info = 0;
+    KS_CUDA(ctx, cudaMemcpyAsync(&info, ctx->eig_info, sizeof(int), cudaMemcpyDeviceToHost, st));
+    KS_CUDA(ctx, cudaStreamSynchronize(st));
+    if (info != 0) return KS_OK;
+    k_lower_only<<<ks_blocks(nH * nH, 256), 256, 0, st>>>(ctx->ef_LH, nH);
+    KS_LAUNCHED(ctx);
+    k_identity<<<ks_blocks(nH * nH, 256), 256, 0, st>>>(ctx->ef_LHinv, nH);
+    KS_LAUNCHED(ctx);
+    KS_BLAS(ctx, cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)nH,
+                             (int)nH, &one, ctx->ef_LH, (int)nH, ctx->ef_LHinv, (int)nH));
+    ctx->ef_LH_state = 1;
+  }
+  if (ctx->ef_LH_state != 1) return KS_OK;
+  double *Kt = ctx->ef_aux, *S = Kt + nH * Nc, *LSinv = S + Nc * Nc, *T = LSinv + Nc * Nc;   // T [Nc][nH]
+  int *mism = reinterpret_cast<int *>(T + Nc * nH);
+  KS_CUDA(ctx, cudaMemsetAsync(mism, 0, sizeof(int), st));
+  k_block_mismatch<<<ks_blocks(nH * nH, 256), 256, 0, st>>>(FB, D, ctx->B_H, nH, mism);
+  KS_LAUNCHED(ctx);
+  // Kt = L_H^-1 c (nH x Nc), S = gamma - Kt^T Kt
+  KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)nH, (int)Nc, (int)nH, &one, ctx->ef_LHinv, (int)nH,
+                           FB + nH * D, (int)D, &zero, Kt, (int)nH));
+  KS_CUDA(ctx, cudaMemcpy2DAsync(S, sizeof(double) * Nc, FB + nH * D + nH, sizeof(double) * D, sizeof(double) * Nc, Nc,
+                                 cudaMemcpyDeviceToDevice, st));
+  KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, (int)Nc, (int)Nc, (int)nH, &mone, Kt, (int)nH, Kt, (int)nH,
+                           &one, S, (int)Nc));
+  if (cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, (int)Nc, S, (int)Nc, &lw) != CUSOLVER_STATUS_SUCCESS ||
+      lw > ctx->ext_lwork)
+    return KS_OK;
+  if (cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, (int)Nc, S, (int)Nc, ctx->eig_work, lw, ctx->eig_info) !=
+      CUSOLVER_STATUS_SUCCESS)
+    return KS_OK;
+  ctx->launches++;
+  int hv[2] = {0, 0};
+  KS_CUDA(ctx, cudaMemcpyAsync(&hv[0], mism, sizeof(int), cudaMemcpyDeviceToHost, st));
+  KS_CUDA(ctx, cudaMemcpyAsync(&hv[1], ctx->eig_info, sizeof(int), cudaMemcpyDeviceToHost, st));
+  KS_CUDA(ctx, cudaStreamSynchronize(st));
+  if (hv[0] != 0 || hv[1] != 0) return KS_OK;   // not the cached coarse block, or the Schur complement not SPD
+  k_lower_only<<<ks_blocks(Nc * Nc, 256), 256, 0, st>>>(S, Nc);
+  KS_LAUNCHED(ctx);
+  k_identity<<<ks_blocks(Nc * Nc, 256), 256, 0, st>>>(LSinv, Nc);
+  KS_LAUNCHED(ctx);
+  KS_BLAS(ctx, cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)Nc,
+                           (int)Nc, &one, S, (int)Nc, LSinv, (int)Nc));
+  k_build_L<<<ks_blocks(D * D, 256), 256, 0, st>>>(ctx->ef_LH, ctx->ef_LHinv, Kt, S, LSinv, nH, Nc, ctx->eig_B,
+                                                     ctx->ef_Linv);
+  KS_LAUNCHED(ctx);
+  // bottom-left block of L^-1: -L_S^-1 K L_H^-1 = -L_S^-1 (Kt^T L_H^-1)
+  KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, (int)Nc, (int)nH, (int)nH, &one, Kt, (int)nH, ctx->ef_LHinv,
+                           (int)nH, &zero, T, (int)Nc));
+  KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)Nc, (int)nH, (int)Nc, &mone, LSinv, (int)Nc, T, (int)Nc,
+                           &zero, ctx->ef_Linv + nH, (int)D));
+  *ok = true;
+  return KS_OK;
+}
+
 ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, const double *FB, double *evals,
                              double *evecs, const double *Ywarm, bool same_B) {
   KS_TRY(ensure_solver_handle(ctx));
@@ -537,8 +677,10 @@ ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, co
   ctx->ef_L_D = 0;   // eig_B holds F_B (or L below)
   // the filtered subspace iteration for the lowest k when the block is small against D (KS_PENCIL_DENSE=1:
   // always the dense cuSOLVER path below; it is also the fallback)
+  bool fast = false;
+  if (filtered && !have_L) KS_TRY(coarse_chol_reduction(ctx, D, FB, &fast));
   if (filtered) {
-    if (!have_L) {
+    if (!have_L && !fast) {
     int lw = 0;
     if (cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, (int)D, ctx->eig_B, (int)D, &lw) !=
         CUSOLVER_STATUS_SUCCESS)
@@ -557,7 +699,7 @@ ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, co
     }
     ctx->ef_L_D = D;   // eig_B = L
     bool done = false;
-    KS_TRY(pencil_eig_filtered(ctx, D, k, evals, evecs, &done, Ywarm));
+    KS_TRY(pencil_eig_filtered(ctx, D, k, evals, evecs, &done, Ywarm, fast ? ctx->ef_Linv : nullptr));
     if (done) return KS_OK;
     ctx->ef_L_D = 0;
     // not converged: the dense path on fresh copies
