@@ -40,6 +40,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-small", action="store_true",
+                    help="skip the C1-C3 and small-mu sub-records of the default run")
     ap.add_argument("--no-c5", action="store_true",
                     help="skip the C5 sub-record of the default C4 run (largest config, ~2 min of host setup)")
     ap.add_argument("--ref-budget-s", type=float, default=150.0,
@@ -519,6 +521,41 @@ def c5_record(dev, stream, local, peak, peak_kind, steps=5, warmup=3):
         return {"error": str(ex)[:300]}
 
 
+SMALL_MU = {1: 1.0, 2: 1.0, 3: 32.0}   # the small-mu variants (more iterations, same bytes each)
+
+
+def small_records(dev, stream, local, steps=10, warmup=3):
+    """C1-C3 (correctness-sized; C1, C2 fit in L2) at the paper's mu and at a small mu: value, step time and block
+    iterations, device-timed like the headline."""
+    import torch
+    out = {}
+    try:
+        for c in (1, 2, 3):
+            p = gen.make_problem(c)
+            ctx, b = setup_ctx(p, dev, stream)
+            rec = {}
+            for tag, mu in (("paper_mu", p.mu), ("small_mu", SMALL_MU[c])):
+                q = p if mu == p.mu else _with_mu(p, mu)
+                r = device_steps(ctx, b, q, steps, warmup, stream, 1, local)
+                rec[tag] = {"mu": float(mu), "block_iters": int(r["k"]), "ms_per_step": r["total_ms"] / steps,
+                            "step_ms": stats(r["step_ms"]),
+                            "value": steps * p.N * p.n_free * r["k"] / (r["total_ms"] * 1e-3)}
+            out[p.cfg["name"]] = dict(rec, n_free=int(p.n_free), N=int(p.N), nnz=int(ctx.nnz))
+            ctx.close()
+            del b
+            torch.cuda.empty_cache()
+    except Exception as ex:   # reported, never fatal for the headline line
+        out["error"] = str(ex)[:300]
+    return out
+
+
+def _with_mu(p, mu):
+    import copy
+    q = copy.copy(p)
+    q.mu = float(mu)
+    return q
+
+
 def run_ours(args, p, rank, world, local):
     import torch
     import torch.distributed as dist
@@ -597,11 +634,14 @@ def run_ours(args, p, rank, world, local):
         except Exception as ex:  # keep the GPU line even if the oracle cannot run
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle",
                                     "sample": f"failed: {ex}"}
-    if world == 1 and args.config == 4 and not args.no_c5:
+    if world == 1 and args.config == 4 and not (args.no_c5 and args.no_small):
         ctx.close()
         del b
         torch.cuda.empty_cache()
-        line["c5"] = c5_record(dev, stream, local, peak, peak_kind)
+        if not args.no_small:
+            line["small_configs"] = small_records(dev, stream, local)
+        if not args.no_c5:
+            line["c5"] = c5_record(dev, stream, local, peak, peak_kind)
     print(json.dumps(line), flush=True)
 
 

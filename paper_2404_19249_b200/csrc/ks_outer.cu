@@ -1,10 +1,11 @@
 // ks_outer.cu -- NEXT-1: close the linear Algorithm-3 loop.
 //   ks_pencil_eig       lowest k eigenpairs of F_A y = lambda F_B y, the "small-scale algebraic eigenvalue
-//                       problem" on W (Nonlinear_Eig_Hh); dense, D = n_H + N
-//                       <= ~1400, by the cuSOLVER generalized symmetric eigensolver (a plain library call,
-//                       like cuBLAS for a plain GEMM): Cholesky of F_B, tridiagonal reduction, and only the
-//                       lowest k eigenpairs (index range, dsygvdx).
-//   ks_lift             U_new = P y_H + U~ y_t (the new orbitals in S_H + span{psi~}), own kernel.
+//                       problem" on W (Nonlinear_Eig_Hh), D = n_H + N <= ~1400.
+//                       Default: reduction to standard form (with the coarse block's Cholesky factor cached per
+//                       coarse space, coarse_chol_reduction) and a Chebyshev-filtered subspace iteration on
+//                       k + 8 vectors (pencil_eig_filtered). Fallback, and KS_PENCIL_DENSE=1: the dense cuSOLVER
+//                       generalized symmetric eigensolver (lowest k by index range, dsygvdx).
+//   ks_lift             U_new = P y_H + U~ y_t (the new orbitals in S_H + span{psi~}), own kernel (FP64 MMA).
 //   ks_augmented_solve  outer iterations with a fixed potential: block solve -> projection -> pencil
 //                       eig -> lift, until max |lambda_new - lambda| <= tol_eig * max |lambda|.
 #include <cusolverDn.h>

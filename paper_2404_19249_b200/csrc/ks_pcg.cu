@@ -358,6 +358,9 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg(PcgArgs 
 #ifndef KS_PCG_PREFETCH
 #define KS_PCG_PREFETCH 1
 #endif
+#ifndef KS_PCG_STG_MBAR
+#define KS_PCG_STG_MBAR 1   // staged S phase: per-stage empty mbarriers instead of a block barrier per tile
+#endif
 #ifndef KS_PCG_CONTIG
 #define KS_PCG_CONTIG 0   // fused kernel: contiguous tile chunks per block instead of interleaved tiles
 #endif
@@ -453,7 +456,7 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
   constexpr int STRIDE = 4 * NP;
   constexpr unsigned VB = TILE * NP * 8;   // bytes of one vector's tile rows
   extern __shared__ __align__(128) unsigned char dyn[];
-  __shared__ __align__(8) uint64_t s_full[2];
+  __shared__ __align__(8) uint64_t s_full[2], s_empty[2];
   unsigned pseq = 0;                        // stage uses so far (stage pseq & 1, parity (pseq >> 1) & 1)
   // the k-th row tile (= U/P chunk) of this block: interleaved over the blocks (t = b + k G, one sweeping
   // front of gathers, KS_PCG_CONTIG=0) or contiguous chunks (t = b per + k: consecutive tiles of a block are
@@ -493,6 +496,8 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
     if (threadIdx.x == 0) {
       mbar_init(&s_full[0], 1);
       mbar_init(&s_full[1], 1);
+      mbar_init(&s_empty[0], PCG_WARPS);   // one arrival per warp when it is done with a stage
+      mbar_init(&s_empty[1], PCG_WARPS);
       mbar_fence_init();
     }
     __syncthreads();
@@ -643,8 +648,18 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
               po.st(a.p + off);
               xo.st(a.X + off);
             }
+#if KS_PCG_STG_MBAR
+            // this warp is done with the stage; the producer refills it once all warps are (no block barrier)
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[q & 1u]);
+            if (threadIdx.x == 0 && k + 2 < my) {
+              mbar_wait(&s_empty[q & 1u], (q >> 1) & 1u);
+              issue(k + 2);
+            }
+#else
             __syncthreads();   // every warp is done with this stage
             if (threadIdx.x == 0 && k + 2 < my) issue(k + 2);
+#endif
           }
           pseq += (unsigned)my;
         } else {
@@ -853,6 +868,9 @@ __global__ void k_tile_emax(const int32_t *__restrict__ sell_ptr, int64_t n_slic
 #ifndef KS_PCG_STAGED
 #define KS_PCG_STAGED 1   // the staged S phase of the fused kernel when its two stages fit in shared memory
 #endif
+#ifndef KS_PCG_STAGED_MAXNP
+#define KS_PCG_STAGED_MAXNP 16   // up to which block width
+#endif
 constexpr size_t PCG_STAGE_SMEM_MAX = 200 * 1024;
 
 template <int NP, bool FUSED, bool STG>
@@ -883,7 +901,7 @@ ks_status launch_pcg(ks_ctx *ctx, PcgArgs &a) {
   // Hartree solve (given B, up to ~10^3 iterations to 1e-12) keeps the three-phase recurrences
   const char *fz = getenv("KS_PCG_FUSED");
   if (a.B || (fz && fz[0] == '0')) return launch_pcg_t<NP, false, false>(ctx, a, 0);
-  if constexpr (NP >= 4 && NP <= 16 && KS_PCG_STAGED) {   // measured slower at NP = 32 (C5, r02g)
+  if constexpr (NP >= 4 && NP <= KS_PCG_STAGED_MAXNP && KS_PCG_STAGED) {   // NP = 32 measured slower (C5, r02g)
     const char *sg = getenv("KS_PCG_STAGED");
     if (!(sg && sg[0] == '0')) {
       int &em = ctx->tile_emax[__builtin_ctz(NP)];

@@ -116,3 +116,64 @@ def test_two_contexts_on_two_streams_are_independent():
     for key, r in (("a", ref[0]), ("b", ref[1])):
         for x, y in zip(outs[key], r):
             assert torch.equal(x.cpu(), y)
+
+
+def test_regions_smaller_than_their_plan_are_refused():
+    """include/ks.h "Memory": a region smaller than its plan returns KS_E_WORKSPACE before any kernel writes past
+    it; a block wider than max_N returns KS_E_ARG; the setup region may be the workspace; the plan is exact
+    (the carved persistent layout uses every planned byte)."""
+    import ctypes as C
+
+    import paper_2404_19249_b200 as ks
+    L = ks.load_library()
+    p = gen.make_problem(1)
+    xyz = np.ascontiguousarray(p.xyz)
+    tets = np.ascontiguousarray(p.tets, dtype=np.int32)
+    dirn = np.ascontiguousarray(p.dirichlet, dtype=np.uint8)
+    sz = [C.c_size_t() for _ in range(3)]
+    assert L.ks_plan(p.n_nodes, xyz.ctypes.data, p.n_tets, tets.ctypes.data, dirn.ctypes.data, 2,
+                     *[C.byref(x) for x in sz]) == 0
+    persist, work, setup = (x.value for x in sz)
+    assert persist > 0 and work > 0 and setup > 0
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def create(pb, wb, sb, shared_setup=False):
+        P = torch.empty(max(pb, 1), dtype=torch.uint8, device=DEV)
+        W = torch.empty(max(wb, 1), dtype=torch.uint8, device=DEV)
+        S = torch.empty(max(sb, 1), dtype=torch.uint8, device=DEV)
+        h = C.c_void_p()
+        st = L.ks_create(p.n_nodes, xyz.ctypes.data, p.n_tets, tets.ctypes.data, dirn.ctypes.data, 2, P.data_ptr(),
+                         pb, W.data_ptr(), wb, None if shared_setup else S.data_ptr(), sb, C.c_void_p(stream),
+                         C.byref(h))
+        return st, h, (P, W, S)
+
+    for pb, wb, sb in ((persist - 256, work, setup), (persist, work - 256, setup), (persist, work, setup - 256)):
+        st, h, _ = create(pb, wb, sb)
+        assert st == ks.KS_E_WORKSPACE and not h.value, (pb, wb, sb, st)
+        assert b"KS_E_WORKSPACE" in L.ks_last_error(None)
+    # the workspace doubles as the setup region when it is large enough
+    st, h, keep = create(persist, max(work, setup), 0, shared_setup=True)
+    assert st == 0
+    cap, used, peak = C.c_size_t(), C.c_size_t(), C.c_size_t()
+    assert L.ks_memory_usage(h, 0, C.byref(cap), C.byref(used), C.byref(peak)) == 0
+    assert cap.value == used.value == persist
+    # N above the planned max_N
+    U = torch.zeros((p.n_free, 3), dtype=torch.float64, device=DEV)
+    Ut = torch.empty_like(U)
+    lam = torch.zeros(3, dtype=torch.float64, device=DEV)
+    V = torch.from_numpy(p.V).to(DEV)
+    assert L.ks_assemble_veff(h, V.data_ptr(), C.c_double(p.mu)) == 0
+    assert L.ks_block_solve(h, 3, lam.data_ptr(), U.data_ptr(), Ut.data_ptr(), C.c_double(1e-10), 100, None,
+                            None) == ks.KS_E_ARG
+    assert L.ks_sync(h) == 0
+    L.ks_destroy(h)
+    # a coarse region smaller than its plan
+    ctx = ks.Context(p.xyz, p.tets, p.dirichlet, max_N=2)
+    n = C.c_size_t()
+    Pr, Pc, Pv = dt(p.P_rowptr), dt(p.P_col), dt(p.P_val)
+    assert L.ks_coarse_plan(ctx._h, p.n_H, Pr.data_ptr(), Pc.data_ptr(), Pv.data_ptr(), C.byref(n)) == 0
+    small = torch.empty(n.value - 256, dtype=torch.uint8, device=DEV)
+    assert L.ks_set_coarse(ctx._h, p.n_H, Pr.data_ptr(), Pc.data_ptr(), Pv.data_ptr(), small.data_ptr(),
+                           n.value - 256) == ks.KS_E_WORKSPACE
+    ctx.set_coarse(p.n_H, Pr, Pc, Pv)   # the binding's planned region works
+    assert ctx.memory_usage("coarse")[0] == ctx.memory_usage("coarse")[1]
