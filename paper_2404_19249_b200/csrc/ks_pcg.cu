@@ -869,7 +869,7 @@ __global__ void k_tile_emax(const int32_t *__restrict__ sell_ptr, int64_t n_slic
 #define KS_PCG_STAGED 1   // the staged S phase of the fused kernel when its two stages fit in shared memory
 #endif
 #ifndef KS_PCG_STAGED_MAXNP
-#define KS_PCG_STAGED_MAXNP 16   // up to which block width
+#define KS_PCG_STAGED_MAXNP 32   // up to which block width (NP = 64: two stages do not fit)
 #endif
 constexpr size_t PCG_STAGE_SMEM_MAX = 200 * 1024;
 
@@ -901,7 +901,7 @@ ks_status launch_pcg(ks_ctx *ctx, PcgArgs &a) {
   // Hartree solve (given B, up to ~10^3 iterations to 1e-12) keeps the three-phase recurrences
   const char *fz = getenv("KS_PCG_FUSED");
   if (a.B || (fz && fz[0] == '0')) return launch_pcg_t<NP, false, false>(ctx, a, 0);
-  if constexpr (NP >= 4 && NP <= KS_PCG_STAGED_MAXNP && KS_PCG_STAGED) {   // NP = 32 measured slower (C5, r02g)
+  if constexpr (NP >= 4 && NP <= KS_PCG_STAGED_MAXNP && KS_PCG_STAGED) {
     const char *sg = getenv("KS_PCG_STAGED");
     if (!(sg && sg[0] == '0')) {
       int &em = ctx->tile_emax[__builtin_ctz(NP)];
