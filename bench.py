@@ -347,7 +347,10 @@ def run_reference(args, p, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": workload_config(p),
+            "data": "synthetic",
+            # the same workload keys as our arm's line (nnz of the free pattern, block iterations of the step)
+            "config": dict(workload_config(p), nnz=int(om.nnz), block_iters=int(ks[0]),
+                           parallelism=parallelism(world)),
             "cpu_baseline": dict({"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
                                  **host_info()),
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -385,6 +388,10 @@ def combine_ranks(ms, units, world, dev):
     u = torch.tensor([float(units)], dtype=torch.float64, device=dev)
     dist.all_reduce(u, op=dist.ReduceOp.SUM)
     return float(t.item()), float(u.item())
+
+
+def parallelism(world):
+    return f"independent problem per rank x{world}" if world > 1 else "single process"
 
 
 def workload_config(p):
@@ -617,7 +624,7 @@ def run_ours(args, p, rank, world, local):
         "warmup": max(3, args.warmup), "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": dict(workload_config(p), nnz=int(nnz), block_iters=int(k_last),
-                       parallelism=f"independent problem per GPU x{world}" if world > 1 else "1 GPU"),
+                       parallelism=parallelism(world)),
         "roofline": roofline(p, nnz, k_last, t_solve, peak, peak_kind),
         "phases_ms": {"assemble_veff": t_asm, "block_solve": t_solve, "project_augmented": t_proj},
         "step_ms": stats(r["step_ms"]),

@@ -435,6 +435,17 @@ __device__ __forceinline__ void sell_row_s(const double *vs, const int32_t *cs, 
   }
 }
 
+// the init phase's operators (A and M values, columns) of a warp's rows, one tile ahead
+template <int RPW>
+__device__ __forceinline__ void prefetch_init(const PcgArgs &a, int64_t row0) {
+  if (row0 >= a.n) return;
+  const int64_t rows = min((int64_t)RPW, a.n - row0);
+  const int32_t e0 = __ldg(a.sell_ptr + row0 / KS_SELL_C), e1 = __ldg(a.sell_ptr + (row0 + rows - 1) / KS_SELL_C + 1);
+  l2_prefetch(a.A + e0, (unsigned)(e1 - e0) * 8u);
+  l2_prefetch(a.M + e0, (unsigned)(e1 - e0) * 8u);
+  l2_prefetch(a.sell_col + e0, (unsigned)(e1 - e0) * 4u);
+}
+
 // ---------------------------------------------------------------------------------------------
 // Fused two-phase iteration (the default for the BVPs, KS_PCG_FUSED=0 selects the three-phase kernel above).
 // z = D^-1 r is stored instead of r, and q = A p is carried by the recurrence
@@ -516,8 +527,11 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
       const int c = sub * VEC + v;
       sh[v] = (c < a.N ? __ldg(a.lambda + c) : 0.0) + a.mu;
     }
+    constexpr bool PFI = KS_PCG_PREFETCH && NP >= 4;
+    if (PFI && lane == 0 && my_tiles > 0) prefetch_init<RPW>(a, tile_k(0) * TILE + warp * RPW);
     for (int64_t kk = 0; kk < my_tiles; kk++) {
       const int64_t row = tile_k(kk) * TILE + warp * RPW + slot;
+      if (PFI && lane == 0 && kk + 1 < my_tiles) prefetch_init<RPW>(a, tile_k(kk + 1) * TILE + warp * RPW);
       if (row < n) {
         DV<VEC> au, mu_;
         sell_row<NP, 2>(a.sell_ptr, a.sell_col, a.A, a.M, row, a.U, sub, au, mu_);
@@ -583,8 +597,8 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
           acc[0][v] = 0.0;
         }
         const double *xin = xwritten ? a.X : a.U;
-        if (STG && !first) {
-          // ---- staged: tile k of this block in stage (pseq + k) & 1 ----
+        if (STG) {
+          // ---- staged: tile k of this block in stage (pseq + k) & 1 (first S phase: the operator slices only) ----
           const int64_t my = my_tiles;
           const unsigned EB = (unsigned)a.emax;
           auto issue = [&](int64_t k) {   // one thread: the bulk copies of tile k
@@ -595,14 +609,16 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
             const unsigned q = pseq + (unsigned)k, eb = (unsigned)(e1 - e0), vb = (unsigned)(rows * NP * 8);
             unsigned char *st = dyn + (size_t)(q & 1u) * a.stage_bytes;
             uint64_t *bar = &s_full[q & 1u];
-            mbar_expect_tx(bar, eb * 12u + 4u * vb);
+            mbar_expect_tx(bar, eb * 12u + (first ? 0u : 4u * vb));
             bulk_g2s(st, a.A + e0, eb * 8u, bar);
             bulk_g2s(st + 8u * EB, a.sell_col + e0, eb * 4u, bar);
-            unsigned char *vbase = st + 12u * EB;
-            bulk_g2s(vbase, a.q + r0 * NP, vb, bar);
-            bulk_g2s(vbase + VB, a.p + r0 * NP, vb, bar);
-            bulk_g2s(vbase + 2 * VB, xin + r0 * NP, vb, bar);
-            bulk_g2s(vbase + 3 * VB, Z + r0 * NP, vb, bar);
+            if (!first) {
+              unsigned char *vbase = st + 12u * EB;
+              bulk_g2s(vbase, a.q + r0 * NP, vb, bar);
+              bulk_g2s(vbase + VB, a.p + r0 * NP, vb, bar);
+              bulk_g2s(vbase + 2 * VB, xin + r0 * NP, vb, bar);
+              bulk_g2s(vbase + 3 * VB, Z + r0 * NP, vb, bar);
+            }
           };
           if (threadIdx.x == 0) {
             // q, p, x, z were written by the generic proxy before the grid barrier: order the bulk reads after
@@ -624,6 +640,13 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
               const int32_t b = __ldg(a.sell_ptr + row / KS_SELL_C), e = __ldg(a.sell_ptr + row / KS_SELL_C + 1);
               DV<VEC> w;
               sell_row_s<NP>(vs, cs, (b - e0) + (int)(row % KS_SELL_C) * 4, (e - b) / (4 * KS_SELL_C), Z, sub, w);
+              const int64_t off0 = row * NP + sub * VEC;
+              if (first) {   // p = z (init), q = A p
+                const DV<VEC> pv0 = DV<VEC>::ld(a.p + off0);
+#pragma unroll
+                for (int v = 0; v < VEC; v++) acc[0][v] += pv0.v[v] * w.v[v];
+                w.st(a.q + off0);
+              } else {
               const int so = lr * NP + sub * VEC;
               double qv[VEC], pv[VEC], xv[VEC], zv[VEC];
 #pragma unroll
@@ -647,6 +670,7 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
               qo.st(a.q + off);
               po.st(a.p + off);
               xo.st(a.X + off);
+              }
             }
 #if KS_PCG_STG_MBAR
             // this warp is done with the stage; the producer refills it once all warps are (no block barrier)

@@ -69,8 +69,8 @@ def test_every_device_byte_is_caller_owned():
     assert ctx.memory_bytes() == regions
     assert torch.cuda.memory_allocated() >= regions
     # what is not torch's: the lazily loaded module image, library handles, copy streams (a few hundred MB at
-    # most), never the regions (C3: ~1.5 GB)
-    assert grown < 0.25 * regions + (512 << 20), (grown, regions)
+    # most), never the regions (C4: ~12 GB)
+    assert grown < (1 << 30), (grown, regions)
     for r in ("persistent", "coarse", "ext"):
         cap, used, peak = ctx.memory_usage(r)
         assert used == cap and peak == cap, (r, cap, used, peak)   # the plan is exact for the fixed layouts
