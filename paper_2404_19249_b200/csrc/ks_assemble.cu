@@ -91,6 +91,63 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
   }
 }
 
+// Hot-path assembly in sliced-ELL order: one warp per 8-row slice, one slot group (8 rows x 4
+// slots = 32 entries) per step, lane = (row % 8) * 4 + slot % 4. The entry's K and M come from their sliced-ELL
+// copies and the SELL values of A and H are written in place: every read of the fixed data and every write is
+// one coalesced 256-byte segment per warp. Each lane walks its entry's slice of the inverse map (through the
+// entry's CSR index) in ascending element order, as k_assemble_rows does: the same arithmetic and order per
+// entry. The ~24-long diagonal lists of a slice fall in one slot group, so per slice the walk costs about one
+// long group plus the short ones (the half-warp per row kernel waits for its diagonal lane on every row).
+template <int UNR>
+__global__ void __launch_bounds__(256) k_assemble_sell(const int32_t *__restrict__ sell_ptr,
+                                                       const int32_t *__restrict__ sell_col,
+                                                       const int32_t *__restrict__ sell_csr,
+                                                       const double *__restrict__ sK, const double *__restrict__ sM,
+                                                       const int32_t *__restrict__ inv_ptr,
+                                                       const int32_t *__restrict__ inv_idx, const double *__restrict__ w,
+                                                       const double *__restrict__ v_free, double mu, int64_t n_free,
+                                                       int64_t n_slices, double *__restrict__ sell_A,
+                                                       double *__restrict__ sell_H, double *__restrict__ diag,
+                                                       double *__restrict__ dinv) {
+  const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= n_slices) return;
+  const int32_t b = __ldg(sell_ptr + s), ng = (__ldg(sell_ptr + s + 1) - b) / (4 * KS_SELL_C);
+  const int64_t row = s * KS_SELL_C + (lane >> 2);
+  const double vi = row < n_free ? __ldg(v_free + row) : 0.0;
+  for (int g = 0; g < ng; g++) {
+    const int64_t sp = b + (int64_t)g * (4 * KS_SELL_C) + lane;
+    const int32_t e = __ldg(sell_csr + sp);
+    if (e < 0) continue;   // padding slot (stays 0)
+    const int32_t c = __ldg(sell_col + sp);
+    const double m = __ldg(sM + sp), kk = __ldg(sK + sp), vc = __ldg(v_free + c);
+    const int32_t q0 = __ldg(inv_ptr + e), q1 = __ldg(inv_ptr + e + 1);
+    double sum = 0.0;
+    for (int32_t qb = q0; qb < q1; qb += UNR) {
+      int32_t t[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; u++) t[u] = qb + u < q1 ? (__ldg(inv_idx + qb + u) >> 4) : -1;
+      double wt[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; u++) wt[u] = t[u] >= 0 ? __ldg(w + t[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < UNR; u++)
+        if (t[u] >= 0) sum += wt[u];
+    }
+    double mv;
+    if (c == row) mv = vi * m / 3.0 + sum / 60.0;
+    else mv = (vi + vc) * m / 6.0 + sum / 120.0;
+    const double h = 0.5 * kk + mv;
+    const double a = h + mu * m;
+    sell_A[sp] = a;
+    sell_H[sp] = h;
+    if (c == row) {
+      diag[row] = a;
+      dinv[row] = 1.0 / a;
+    }
+  }
+}
+
 }  // namespace
 
 ks_status ks_assemble_impl(ks_ctx *ctx, const double *d_veff, double mu) {
@@ -99,9 +156,18 @@ ks_status ks_assemble_impl(ks_ctx *ctx, const double *d_veff, double mu) {
   k_tet_weights<<<ks_blocks(n, 256), 256, 0, s>>>(ctx->tets, ctx->vol, d_veff, ctx->n_tets, ctx->node_of_free,
                                                   ctx->n_free, ctx->w_tet, ctx->v_free, ctx->d_flags);
   KS_LAUNCHED(ctx);
-  k_assemble_rows<false><<<ks_blocks(16 * ctx->n_free, 256), 256, 0, s>>>(
-      ctx->row_ptr, ctx->col, ctx->inv_ptr, ctx->inv_idx, ctx->w_tet, ctx->v_free, ctx->K, ctx->M, mu,
-      ctx->n_free, nullptr, nullptr, nullptr, ctx->diag, ctx->dinv, ctx->sell_ptr, ctx->sell_A, ctx->sell_H);
+#ifndef KS_ASM_SELL
+#define KS_ASM_SELL 1
+#endif
+  if (KS_ASM_SELL) {
+    k_assemble_sell<ASM_UNR><<<ks_blocks(32 * ctx->n_slices, 256), 256, 0, s>>>(
+        ctx->sell_ptr, ctx->sell_col, ctx->sell_csr, ctx->sell_K, ctx->sell_M, ctx->inv_ptr, ctx->inv_idx, ctx->w_tet,
+        ctx->v_free, mu, ctx->n_free, ctx->n_slices, ctx->sell_A, ctx->sell_H, ctx->diag, ctx->dinv);
+  } else {
+    k_assemble_rows<false><<<ks_blocks(16 * ctx->n_free, 256), 256, 0, s>>>(
+        ctx->row_ptr, ctx->col, ctx->inv_ptr, ctx->inv_idx, ctx->w_tet, ctx->v_free, ctx->K, ctx->M, mu,
+        ctx->n_free, nullptr, nullptr, nullptr, ctx->diag, ctx->dinv, ctx->sell_ptr, ctx->sell_A, ctx->sell_H);
+  }
   KS_LAUNCHED(ctx);
   ctx->views_fresh = false;
   ctx->mu = mu;

@@ -73,6 +73,7 @@ struct ks_ctx {
   int32_t *sell_col = nullptr;      // [sell_total]
   double *sell_A = nullptr, *sell_M = nullptr, *sell_H = nullptr;  // [sell_total]
   double *sell_K = nullptr;         // [sell_total] stiffness (Poisson operator of the Hartree solve)
+  int32_t *sell_csr = nullptr;      // [sell_total] CSR index of each slot (-1: padding), for the assembly
   double *dinvK = nullptr;          // [n_free + 2] 1 / diag(K)
   double *v_free = nullptr;         // [n_free] V at free nodes (assembly scratch)
   double mu = 0.0;

@@ -50,6 +50,17 @@ __global__ void k_sell_fill_val(const int32_t *__restrict__ row_ptr, const doubl
   for (int k = 0; k < K; k++) sval[base + (k >> 2) * (4 * KS_SELL_C) + (k & 3)] = k < len ? val[k0 + k] : 0.0;
 }
 
+__global__ void k_sell_fill_csr(const int32_t *__restrict__ row_ptr, int64_t n, const int32_t *__restrict__ sell_ptr,
+                                int32_t *__restrict__ scsr) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t s = i / KS_SELL_C;
+  const int32_t b = sell_ptr[s], K = (sell_ptr[s + 1] - b) / KS_SELL_C;
+  const int32_t k0 = row_ptr[i], len = row_ptr[i + 1] - k0;
+  const int64_t base = b + (i % KS_SELL_C) * 4;
+  for (int k = 0; k < K; k++) scsr[base + (k >> 2) * (4 * KS_SELL_C) + (k & 3)] = k < len ? k0 + k : -1;
+}
+
 __global__ void k_inv_diag(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                            const double *__restrict__ val, int64_t n, double *__restrict__ dinv) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -85,6 +96,8 @@ ks_status ks_sell_build(ks_ctx *ctx, int32_t *cnt, void *cub, size_t cub_bytes, 
   k_sell_fill_val<<<ks_blocks(n, 256), 256, 0, s>>>(ctx->row_ptr, ctx->K, n, ctx->sell_ptr, ctx->sell_K);
   KS_LAUNCHED(ctx);
   k_inv_diag<<<ks_blocks(n, 256), 256, 0, s>>>(ctx->row_ptr, ctx->col, ctx->K, n, ctx->dinvK);
+  KS_LAUNCHED(ctx);
+  k_sell_fill_csr<<<ks_blocks(n, 256), 256, 0, s>>>(ctx->row_ptr, n, ctx->sell_ptr, ctx->sell_csr);
   KS_LAUNCHED(ctx);
   return KS_OK;
 }

@@ -133,11 +133,11 @@ def test_scf_solve_matches_the_oracle_loop():
 
 @pytest.mark.slow
 def test_scf_solve_four_orbitals_matches_the_oracle_loop():
-    """Algorithm 3 with N = 4 doubly occupied orbitals (four Z = 2 centres, no symmetry) on a graded 24^3 fine
+    """Algorithm 3 with N = 4 doubly occupied orbitals (four Z = 3 centres, no symmetry) on a graded 24^3 fine
     mesh with an independent graded 6^3 coarse mesh: GPU (ks_scf_solve, P from ks_interpolation) against
     oracle.scf_solve, every outer iteration's Ritz values within 1e-9 relative. (The coarse mesh is small so the
     oracle's Jacobi eigensolves of every inner step stay cheap: D = 125 + 4.)"""
-    nuc = [((1.1, 0.3, -0.2), 2), ((-1.2, 0.2, 0.4), 2), ((0.2, 1.3, 0.1), 2), ((0.1, -1.0, -0.9), 2)]
+    nuc = [((1.1, 0.3, -0.2), 3), ((-1.2, 0.2, 0.4), 3), ((0.2, 1.3, 0.1), 3), ((0.1, -1.0, -0.9), 3)]
     mk = lambda n: gen.make_problem(dict(L=9.0, n=n, grading=("power", 1.5), jitter=0.0, nuclei=nuc, vnoise=0.0,
                                          N=4, orbitals="gauss", lam=("uniform", -2.0, -0.5), nc=2, seed=9))
     p, c = mk(24), mk(6)
@@ -146,12 +146,12 @@ def test_scf_solve_four_orbitals_matches_the_oracle_loop():
     rp, col, val, nH = ctx.interpolation(c.xyz, c.tets, c.dirichlet)
     ctx.set_coarse(nH, rp, col, val)
     lam, U = dt(p.lam), dt(p.U)
-    out = ctx.scf_solve(dt(p.V), lam, U, mu=4.0, tol=1e-10, max_outer=120, inner=30)
+    out = ctx.scf_solve(dt(p.V), lam, U, mu=6.0, tol=1e-10, max_outer=120, inner=30)
     assert ctx.sync() == 0
     om = oracle.Mesh.from_problem(p)
     orp, ocol, oval, onH = oracle.interpolation(p.xyz, p.free_nodes, c.xyz, c.tets, c.dirichlet)
     assert onH == nH
-    ref = oracle.scf_solve(om, onH, orp, ocol, oval, p.V, p.lam.copy(), p.U.copy(), mu=4.0, tol=1e-10,
+    ref = oracle.scf_solve(om, onH, orp, ocol, oval, p.V, p.lam.copy(), p.U.copy(), mu=6.0, tol=1e-10,
                            max_outer=120, inner=30)
     assert abs(out["outer"] - ref["outer"]) <= 1
     # outer iteration by outer iteration while both took the same inner steps (the same path up to rounding)
