@@ -10,6 +10,9 @@
 // since |T| (V_a + V_b)/120 = (V_a + V_b) M_T(a,b)/6 and 2|T| 2V_a/120 = V_a M_T(a,a)/3.
 // Kernel 1 computes w_T per tet and V at free nodes; kernel 2 gathers w_T through the inverse scatter map
 // (the element-to-nnz map grouped by target entry, ascending element) -- a fixed summation order.
+#include <cstdlib>
+#include <cstring>
+
 #include "ks_internal.cuh"
 
 namespace {
@@ -148,7 +151,133 @@ __global__ void __launch_bounds__(256) k_assemble_sell(const int32_t *__restrict
   }
 }
 
+// Star-mask variant (default when every free node's star has <= STAR_MAX tets). Every tet contributing to an
+// entry of row i contains node i, so it lies in the row's star: the tets containing node i, which is exactly the
+// inverse-map slice of the row's diagonal entry (ascending tet). A setup-time bit mask per sliced-ELL slot marks
+// which star tets contribute to the slot's entry (bit k = the k-th tet of the star; 0 = padding slot). A warp
+// first gathers the w_T of its slice's 8 stars (~24 tets each) into shared memory, 4 lanes per row; each lane
+// then sums the set bits of its slot's mask in ascending order. That is the entry's inverse-map slice in its
+// order, so the values are bitwise those of k_assemble_sell, without the per-entry inverse-map walk (no
+// sell_csr, inv_ptr or inv_idx reads per entry: one coalesced 8-byte mask per slot instead).
+// Stars of <= 32 tets (every Kuhn mesh: 24) use 32-bit masks, halving the mask stream.
+constexpr int STAR_MAX = 64, ASM_WARPS = 8;
+template <class MT>
+__global__ void __launch_bounds__(ASM_WARPS * 32) k_assemble_mask(
+    const int32_t *__restrict__ sell_ptr, const int32_t *__restrict__ sell_col, const MT *__restrict__ slot_mask,
+    const double *__restrict__ sK, const double *__restrict__ sM, const int2 *__restrict__ star,
+    const int32_t *__restrict__ inv_idx, const double *__restrict__ w, const double *__restrict__ v_free, double mu,
+    int64_t n_free, int64_t n_slices, double *__restrict__ sell_A, double *__restrict__ sell_H,
+    double *__restrict__ diag, double *__restrict__ dinv) {
+  __shared__ double ws[ASM_WARPS][KS_SELL_C][STAR_MAX + 1];   // +1: the 8 rows on different banks
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t s = (int64_t)blockIdx.x * ASM_WARPS + warp;
+  if (s >= n_slices) return;   // whole warps
+  double (*st)[STAR_MAX + 1] = ws[warp];
+  const int rl = lane >> 2;
+  const int64_t row = s * KS_SELL_C + rl;
+  if (row < n_free) {   // 4 lanes per row stage its star
+    const int2 sd = __ldg(star + row);
+#pragma unroll 4
+    for (int k = lane & 3; k < sd.y; k += 4) st[rl][k] = __ldg(w + (__ldg(inv_idx + sd.x + k) >> 4));
+  }
+  __syncwarp();
+  const int32_t b = __ldg(sell_ptr + s), ng = (__ldg(sell_ptr + s + 1) - b) / (4 * KS_SELL_C);
+  const double vi = row < n_free ? __ldg(v_free + row) : 0.0;
+  for (int g = 0; g < ng; g++) {
+    const int64_t sp = b + (int64_t)g * (4 * KS_SELL_C) + lane;
+    MT mk = __ldg(slot_mask + sp);
+    if (!mk) continue;   // padding slot (stays 0)
+    const int32_t c = __ldg(sell_col + sp);
+    const double m = __ldg(sM + sp), kk = __ldg(sK + sp), vc = __ldg(v_free + c);
+    double sum = 0.0;
+    do {
+      sum += st[rl][sizeof(MT) == 8 ? __ffsll((long long)mk) - 1 : __ffs((int)mk) - 1];
+      mk &= mk - 1;
+    } while (mk);
+    double mv;
+    if (c == row) mv = vi * m / 3.0 + sum / 60.0;
+    else mv = (vi + vc) * m / 6.0 + sum / 120.0;
+    const double h = 0.5 * kk + mv;
+    const double a = h + mu * m;
+    sell_A[sp] = a;
+    sell_H[sp] = h;
+    if (c == row) {
+      diag[row] = a;
+      dinv[row] = 1.0 / a;
+    }
+  }
+}
+
+// setup, thread per free row: star[i] = (first, length) of the row's diagonal inverse-map slice; *max_star =
+// the largest star
+__global__ void k_star(const int32_t *__restrict__ diag_pos, const int32_t *__restrict__ inv_ptr, int64_t n_free,
+                       int2 *__restrict__ star, int *__restrict__ max_star) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_free) return;
+  const int32_t ed = diag_pos[i];
+  const int32_t d0 = inv_ptr[ed], nd = inv_ptr[ed + 1] - d0;
+  star[i] = make_int2(d0, nd);
+  atomicMax(max_star, nd);
+}
+
+// setup, thread per free row (stars <= STAR_MAX): the bit mask of every sliced-ELL slot of the row (slot layout
+// of k_sell_fill_csr); bit k set = the k-th tet of the row's star contributes to the slot's entry
+template <class MT>
+__global__ void k_slot_masks(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ sell_ptr,
+                             const int2 *__restrict__ star, const int32_t *__restrict__ inv_ptr,
+                             const int32_t *__restrict__ inv_idx, int64_t n_free, MT *__restrict__ slot_mask) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_free) return;
+  const int64_t sl = i / KS_SELL_C;
+  const int32_t b = sell_ptr[sl], K = (sell_ptr[sl + 1] - b) / KS_SELL_C;
+  const int64_t base = b + (i % KS_SELL_C) * 4;
+  const int32_t k0 = row_ptr[i], len = row_ptr[i + 1] - k0;
+  const int2 sd = star[i];
+  for (int k = 0; k < K; k++) {
+    MT mk = 0;
+    if (k < len)
+      for (int32_t q = inv_ptr[k0 + k]; q < inv_ptr[k0 + k + 1]; q++) {
+        const int32_t t = inv_idx[q] >> 4;
+        int lo = 0, hi = sd.y;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if ((inv_idx[sd.x + mid] >> 4) < t) lo = mid + 1; else hi = mid;
+        }
+        mk |= (MT)1 << lo;
+      }
+    slot_mask[base + (k >> 2) * (4 * KS_SELL_C) + (k & 3)] = mk;
+  }
+}
+
 }  // namespace
+
+ks_status ks_star_setup(ks_ctx *ctx, int *d) {
+  KS_CUDA(ctx, cudaMemsetAsync(d, 0, sizeof(int), ctx->stream));
+  k_star<<<ks_blocks(ctx->n_free, 256), 256, 0, ctx->stream>>>(ctx->diag_pos, ctx->inv_ptr, ctx->n_free, ctx->star, d);
+  KS_LAUNCHED(ctx);
+  int h = 0;
+  KS_CUDA(ctx, cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  KS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->max_star = h;
+  // KS_ASM_MASK (read here, at ks_create; A/B and tests): "0" = no masks (the k_assemble_sell walk), "64" =
+  // 64-bit masks even for stars <= 32; unset: the narrowest mask the mesh allows
+  const char *e = getenv("KS_ASM_MASK");
+  ctx->mask_bits = h <= 32 ? 32 : h <= STAR_MAX ? 64 : 0;
+  if (e && !strcmp(e, "0")) ctx->mask_bits = 0;
+  if (e && !strcmp(e, "64") && ctx->mask_bits) ctx->mask_bits = 64;
+  if (ctx->mask_bits == 32) {
+    k_slot_masks<<<ks_blocks(ctx->n_free, 256), 256, 0, ctx->stream>>>(
+        ctx->row_ptr, ctx->sell_ptr, ctx->star, ctx->inv_ptr, ctx->inv_idx, ctx->n_free,
+        reinterpret_cast<uint32_t *>(ctx->slot_mask));
+    KS_LAUNCHED(ctx);
+  } else if (ctx->mask_bits == 64) {
+    k_slot_masks<<<ks_blocks(ctx->n_free, 256), 256, 0, ctx->stream>>>(ctx->row_ptr, ctx->sell_ptr, ctx->star,
+                                                                       ctx->inv_ptr, ctx->inv_idx, ctx->n_free,
+                                                                       ctx->slot_mask);
+    KS_LAUNCHED(ctx);
+  }
+  return KS_OK;
+}
 
 ks_status ks_assemble_impl(ks_ctx *ctx, const double *d_veff, double mu) {
   cudaStream_t s = ctx->stream;
@@ -159,7 +288,20 @@ ks_status ks_assemble_impl(ks_ctx *ctx, const double *d_veff, double mu) {
 #ifndef KS_ASM_SELL
 #define KS_ASM_SELL 1
 #endif
-  if (KS_ASM_SELL) {
+#ifndef KS_ASM_STAR
+#define KS_ASM_STAR 1
+#endif
+  const unsigned mask_blocks = (unsigned)((ctx->n_slices + ASM_WARPS - 1) / ASM_WARPS);
+  if (KS_ASM_STAR && ctx->mask_bits == 32) {
+    k_assemble_mask<<<mask_blocks, ASM_WARPS * 32, 0, s>>>(
+        ctx->sell_ptr, ctx->sell_col, reinterpret_cast<const uint32_t *>(ctx->slot_mask), ctx->sell_K, ctx->sell_M,
+        ctx->star, ctx->inv_idx, ctx->w_tet, ctx->v_free, mu, ctx->n_free, ctx->n_slices, ctx->sell_A, ctx->sell_H,
+        ctx->diag, ctx->dinv);
+  } else if (KS_ASM_STAR && ctx->mask_bits == 64) {
+    k_assemble_mask<<<mask_blocks, ASM_WARPS * 32, 0, s>>>(
+        ctx->sell_ptr, ctx->sell_col, ctx->slot_mask, ctx->sell_K, ctx->sell_M, ctx->star, ctx->inv_idx, ctx->w_tet,
+        ctx->v_free, mu, ctx->n_free, ctx->n_slices, ctx->sell_A, ctx->sell_H, ctx->diag, ctx->dinv);
+  } else if (KS_ASM_SELL) {
     k_assemble_sell<ASM_UNR><<<ks_blocks(32 * ctx->n_slices, 256), 256, 0, s>>>(
         ctx->sell_ptr, ctx->sell_col, ctx->sell_csr, ctx->sell_K, ctx->sell_M, ctx->inv_ptr, ctx->inv_idx, ctx->w_tet,
         ctx->v_free, mu, ctx->n_free, ctx->n_slices, ctx->sell_A, ctx->sell_H, ctx->diag, ctx->dinv);

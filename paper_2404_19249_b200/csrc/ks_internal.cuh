@@ -74,6 +74,10 @@ struct ks_ctx {
   double *sell_A = nullptr, *sell_M = nullptr, *sell_H = nullptr;  // [sell_total]
   double *sell_K = nullptr;         // [sell_total] stiffness (Poisson operator of the Hartree solve)
   int32_t *sell_csr = nullptr;      // [sell_total] CSR index of each slot (-1: padding), for the assembly
+  uint64_t *slot_mask = nullptr;    // [sell_total] star tets contributing to each slot's entry (ks_assemble.cu)
+  int2 *star = nullptr;             // [n_free] (first, length) of each row's star in inv_idx
+  int max_star = 1 << 30;           // largest star (tets containing a free node); set at ks_create
+  int mask_bits = 0;                // width of slot_mask's entries (32 / 64), 0 = masks not built
   double *dinvK = nullptr;          // [n_free + 2] 1 / diag(K)
   double *v_free = nullptr;         // [n_free] V at free nodes (assembly scratch)
   double mu = 0.0;
@@ -244,6 +248,7 @@ ks_status ks_pcg2l_run(ks_ctx *ctx, const double *b, const double *x0, double *x
 void ks_free_pcg2l(ks_ctx *ctx);
 ks_status ks_assemble_impl(ks_ctx *ctx, const double *d_veff, double mu);
 ks_status ks_materialize_views(ks_ctx *ctx);
+ks_status ks_star_setup(ks_ctx *ctx, int *d_tmp);  // d_tmp: one int of setup scratch
 ks_status ks_spmm_impl(ks_ctx *ctx, ks_op op, const double *val, int N, const double *X, double *Y);
 ks_status ks_solve_impl(ks_ctx *ctx, int N, const double *lambda, const double *U, double *Ut, double tol,
                         int max_iter, int32_t *iters, double *relres);

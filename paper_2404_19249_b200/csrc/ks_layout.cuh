@@ -63,6 +63,8 @@ void ks_layout_persist(A &a, ks_ctx *c, const KsMeshSizes &z) {
   a.add(&c->sell_H, z.sell_total, "sell H");
   a.add(&c->sell_K, z.sell_total, "sell K");
   a.add(&c->sell_csr, z.sell_total, "sell -> CSR entry");
+  a.add(&c->slot_mask, z.sell_total, "sell star masks");
+  a.add(&c->star, z.nf, "row stars");
   a.add(&c->dinvK, z.nf + 2, "1/diag K");
 }
 

@@ -304,6 +304,7 @@ ks_status ks_setup_mesh(ks_ctx *ctx, const double *h_xyz, const int32_t *h_tets,
   k_stiffness_mass<<<ks_blocks(nnz, T), T, 0, s>>>(ctx->inv_ptr, ctx->inv_idx, ctx->vol, grad, nnz, ctx->K, ctx->M);
   KS_LAUNCHED(ctx);
   KS_TRY(ks_sell_build(ctx, tp.sell_cnt, cub_tmp, cub_cap, z.sell_total));
+  KS_TRY(ks_star_setup(ctx, tp.n_sel));
   KS_CUDA(ctx, cudaStreamSynchronize(s));  // the setup temporaries are not referenced after this point
   return KS_OK;
 }

@@ -364,3 +364,29 @@ def test_pipelined_host_steps_equal_the_device_path():
     assert k.ctx.sync() == 0
     for (FA, FB), (FAr, FBr) in zip(outs, ref):
         assert np.array_equal(FA.numpy(), FAr) and np.array_equal(FB.numpy(), FBr)
+
+
+@pytest.mark.parametrize("c", [2, 3])
+def test_assembly_variants_are_bitwise_equal(c, monkeypatch):
+    """The star-mask assembly (32-bit masks: every star here has 24 tets; KS_ASM_MASK=64: 64-bit masks) and the
+    per-entry inverse-map walk (KS_ASM_MASK=0, the kernel for stars > 64 tets) sum every entry's element
+    contributions in the same ascending order: the sliced-ELL A, H, diag(A) they write, seen through a whole
+    solve + projection, are bitwise equal."""
+    p = case(c).p
+    outs = []
+    for mode in (None, "64", "0"):
+        if mode is None:
+            monkeypatch.delenv("KS_ASM_MASK", raising=False)
+        else:
+            monkeypatch.setenv("KS_ASM_MASK", mode)
+        ctx = _ks().Context(p.xyz, p.tets, p.dirichlet)   # the mode is fixed at ks_create
+        ctx.set_coarse(p.n_H, dt(p.P_rowptr), dt(p.P_col), dt(p.P_val))
+        ctx.assemble_veff(dt(p.V), p.mu)
+        Ut, it, rr = ctx.block_solve(dt(p.lam), dt(p.U))
+        FA, FB = ctx.project_augmented(Ut)
+        assert ctx.sync() == 0
+        outs.append([x.cpu().numpy() for x in (Ut, it, rr, FA, FB)])
+        del ctx
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert np.array_equal(a, b)
