@@ -37,6 +37,32 @@ __global__ void k_tet_weights(const int32_t *__restrict__ tets, const double *__
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, KSF_NONFINITE);
 }
 
+// Sum of w_T over an entry's slice [q0, q1) of the inverse map, ascending element. Off-diagonal entries
+// (4-6 tets) sum in that order; the diagonal (the row's whole star, ~24 tets) in four interleaved partial sums
+// p_r over the positions k = q - q0 with k % 4 = r, combined as (p0 + p1) + (p2 + p3): the order the star-mask
+// kernel's four lanes per row produce, so every assembly kernel writes bitwise the same values.
+template <int UNR>
+__device__ __forceinline__ double walk_sum(const int32_t *__restrict__ inv_idx, const double *__restrict__ w,
+                                           int32_t q0, int32_t q1, bool diag) {
+  static_assert(UNR % 4 == 0, "batches must keep k % 4 static");
+  double ps[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int32_t qb = q0; qb < q1; qb += UNR) {
+    int32_t t[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; u++) t[u] = qb + u < q1 ? (__ldg(inv_idx + qb + u) >> 4) : -1;
+    double wt[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; u++) wt[u] = t[u] >= 0 ? __ldg(w + t[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < UNR; u++)
+      if (t[u] >= 0) {
+        if (diag) ps[u & 3] += wt[u];
+        else ps[0] += wt[u];
+      }
+  }
+  return diag ? (ps[0] + ps[1]) + (ps[2] + ps[3]) : ps[0];
+}
+
 // Half-warp per row: lane j of the half handles entries row_ptr[i] + j, + 16, ... The contributions of an
 // entry (its slice of the inverse map, ascending element) are loaded ASM_UNR at a time before their w_T
 // gathers, and summed in that order. VIEWS = false (the hot path) writes the operators the solver and the
@@ -60,18 +86,7 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
     const int32_t c = __ldg(col + e);
     const double m = __ldg(M + e), kk = __ldg(K + e), vc = __ldg(v_free + c);
     const int32_t q0 = __ldg(inv_ptr + e), q1 = __ldg(inv_ptr + e + 1);
-    double s = 0.0;
-    for (int32_t qb = q0; qb < q1; qb += ASM_UNR) {
-      int32_t t[ASM_UNR];
-#pragma unroll
-      for (int u = 0; u < ASM_UNR; u++) t[u] = qb + u < q1 ? (__ldg(inv_idx + qb + u) >> 4) : -1;
-      double wt[ASM_UNR];
-#pragma unroll
-      for (int u = 0; u < ASM_UNR; u++) wt[u] = t[u] >= 0 ? __ldg(w + t[u]) : 0.0;
-#pragma unroll
-      for (int u = 0; u < ASM_UNR; u++)
-        if (t[u] >= 0) s += wt[u];
-    }
+    const double s = walk_sum<ASM_UNR>(inv_idx, w, q0, q1, c == row);
     double mv;
     if (c == row) mv = vi * m / 3.0 + s / 60.0;
     else mv = (vi + vc) * m / 6.0 + s / 120.0;
@@ -125,18 +140,7 @@ __global__ void __launch_bounds__(256) k_assemble_sell(const int32_t *__restrict
     const int32_t c = __ldg(sell_col + sp);
     const double m = __ldg(sM + sp), kk = __ldg(sK + sp), vc = __ldg(v_free + c);
     const int32_t q0 = __ldg(inv_ptr + e), q1 = __ldg(inv_ptr + e + 1);
-    double sum = 0.0;
-    for (int32_t qb = q0; qb < q1; qb += UNR) {
-      int32_t t[UNR];
-#pragma unroll
-      for (int u = 0; u < UNR; u++) t[u] = qb + u < q1 ? (__ldg(inv_idx + qb + u) >> 4) : -1;
-      double wt[UNR];
-#pragma unroll
-      for (int u = 0; u < UNR; u++) wt[u] = t[u] >= 0 ? __ldg(w + t[u]) : 0.0;
-#pragma unroll
-      for (int u = 0; u < UNR; u++)
-        if (t[u] >= 0) sum += wt[u];
-    }
+    const double sum = walk_sum<UNR>(inv_idx, w, q0, q1, c == row);
     double mv;
     if (c == row) mv = vi * m / 3.0 + sum / 60.0;
     else mv = (vi + vc) * m / 6.0 + sum / 120.0;
@@ -156,13 +160,19 @@ __global__ void __launch_bounds__(256) k_assemble_sell(const int32_t *__restrict
 // inverse-map slice of the row's diagonal entry (ascending tet). A setup-time bit mask per sliced-ELL slot marks
 // which star tets contribute to the slot's entry (bit k = the k-th tet of the star; 0 = padding slot). A warp
 // first gathers the w_T of its slice's 8 stars (~24 tets each) into shared memory, 4 lanes per row; each lane
-// then sums the set bits of its slot's mask in ascending order. That is the entry's inverse-map slice in its
-// order, so the values are bitwise those of k_assemble_sell, without the per-entry inverse-map walk (no
+// then sums the set bits of its slot's mask in ascending order (the diagonal: the whole star, summed while it is
+// staged, in walk_sum's order). That is the entry's inverse-map slice in walk_sum's order, so the values are
+// bitwise those of k_assemble_sell, without the per-entry inverse-map walk (no
 // sell_csr, inv_ptr or inv_idx reads per entry: one coalesced 8-byte mask per slot instead).
 // Stars of <= 32 tets (every Kuhn mesh: 24) use 32-bit masks, halving the mask stream.
 constexpr int STAR_MAX = 64, ASM_WARPS = 8;
+#ifdef KS_ASM_MINB
+#define KS_ASM_BOUNDS __launch_bounds__(ASM_WARPS * 32, KS_ASM_MINB)
+#else
+#define KS_ASM_BOUNDS __launch_bounds__(ASM_WARPS * 32)
+#endif
 template <class MT>
-__global__ void __launch_bounds__(ASM_WARPS * 32) k_assemble_mask(
+__global__ void KS_ASM_BOUNDS k_assemble_mask(
     const int32_t *__restrict__ sell_ptr, const int32_t *__restrict__ sell_col, const MT *__restrict__ slot_mask,
     const double *__restrict__ sK, const double *__restrict__ sM, const int2 *__restrict__ star,
     const int32_t *__restrict__ inv_idx, const double *__restrict__ w, const double *__restrict__ v_free, double mu,
@@ -175,11 +185,18 @@ __global__ void __launch_bounds__(ASM_WARPS * 32) k_assemble_mask(
   double (*st)[STAR_MAX + 1] = ws[warp];
   const int rl = lane >> 2;
   const int64_t row = s * KS_SELL_C + rl;
+  double dsum = 0.0;   // the diagonal's sum: the whole star, in walk_sum's four-partial order
   if (row < n_free) {   // 4 lanes per row stage its star
     const int2 sd = __ldg(star + row);
 #pragma unroll 4
-    for (int k = lane & 3; k < sd.y; k += 4) st[rl][k] = __ldg(w + (__ldg(inv_idx + sd.x + k) >> 4));
+    for (int k = lane & 3; k < sd.y; k += 4) {
+      const double x = __ldg(w + (__ldg(inv_idx + sd.x + k) >> 4));
+      st[rl][k] = x;
+      dsum += x;
+    }
   }
+  dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);   // p0 + p1 (= p1 + p0), p2 + p3
+  dsum += __shfl_xor_sync(0xffffffffu, dsum, 2);   // (p0 + p1) + (p2 + p3) on all four lanes
   __syncwarp();
   const int32_t b = __ldg(sell_ptr + s), ng = (__ldg(sell_ptr + s + 1) - b) / (4 * KS_SELL_C);
   const double vi = row < n_free ? __ldg(v_free + row) : 0.0;
@@ -189,11 +206,14 @@ __global__ void __launch_bounds__(ASM_WARPS * 32) k_assemble_mask(
     if (!mk) continue;   // padding slot (stays 0)
     const int32_t c = __ldg(sell_col + sp);
     const double m = __ldg(sM + sp), kk = __ldg(sK + sp), vc = __ldg(v_free + c);
-    double sum = 0.0;
-    do {
-      sum += st[rl][sizeof(MT) == 8 ? __ffsll((long long)mk) - 1 : __ffs((int)mk) - 1];
-      mk &= mk - 1;
-    } while (mk);
+    double sum = dsum;
+    if (c != row) {
+      sum = 0.0;
+      do {
+        sum += st[rl][sizeof(MT) == 8 ? __ffsll((long long)mk) - 1 : __ffs((int)mk) - 1];
+        mk &= mk - 1;
+      } while (mk);
+    }
     double mv;
     if (c == row) mv = vi * m / 3.0 + sum / 60.0;
     else mv = (vi + vc) * m / 6.0 + sum / 120.0;
