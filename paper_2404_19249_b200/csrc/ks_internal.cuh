@@ -120,6 +120,16 @@ struct ks_ctx {
   double *proj_up = nullptr;     // [n_free][NP] U~ in item order
   double *gram_part = nullptr;   // [blocks][2 N N]
   int64_t gram_cap = 0;
+  // item-ordered sliced-ELL copy of the pattern for the A_H pass (ks_project.cu k_proj_ai): every item starts on
+  // an 8-row slice; row position r of item it is slice islice0[it] + r / 8, lane row r % 8
+  int64_t n_islices = 0, isell_total = 0;
+  int32_t *islice0 = nullptr;    // [n_items+1] first item slice of each item
+  int32_t *isell_ptr = nullptr;  // [n_islices+1] first slot of each item slice
+  int2 *inat = nullptr;          // [n_free] per item position: (natural sliced-ELL slot of the row's slot 0, its
+                                 // slot groups); H is read in the natural layout the assembly writes
+  int32_t *isell_col = nullptr;  // [isell_total] natural column (padding: own row, pad rows: 0)
+  uint32_t *islot = nullptr;     // [isell_total] word (row, group g, parent t): bytes u = window slot of parent t
+                                 // of the column of slot 4g+u (255: absent)
 
   // NEXT-2 Hartree workspace (ks_scf.cu)
   double *har_w = nullptr, *har_c = nullptr, *har_b = nullptr, *har_x0 = nullptr, *har_x = nullptr;
@@ -248,6 +258,7 @@ ks_status ks_pcg2l_run(ks_ctx *ctx, const double *b, const double *x0, double *x
 void ks_free_pcg2l(ks_ctx *ctx);
 ks_status ks_assemble_impl(ks_ctx *ctx, const double *d_veff, double mu);
 ks_status ks_materialize_views(ks_ctx *ctx);
+
 ks_status ks_star_setup(ks_ctx *ctx, int *d_tmp);  // d_tmp: one int of setup scratch
 ks_status ks_spmm_impl(ks_ctx *ctx, ks_op op, const double *val, int N, const double *X, double *Y);
 ks_status ks_solve_impl(ks_ctx *ctx, int N, const double *lambda, const double *U, double *Ut, double tol,

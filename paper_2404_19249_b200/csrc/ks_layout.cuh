@@ -111,6 +111,7 @@ void ks_layout_work(A &a, ks_ctx *c, int64_t nf, int max_N, int sm_count) {
 // ---- KS_R_COARSE (ks_set_coarse): sizes known after the item grouping ----
 struct KsCoarseSizes {
   int64_t nf = 0, nnz = 0, pn = 0, ni = 0, dtot = 0, nH = 0, gram = 0;
+  int64_t nis = 0, istot = 0;   // item slices, item-layout slots
   int np = 2;   // projection block width (>= 2)
 };
 template <class A>
@@ -138,6 +139,11 @@ void ks_layout_coarse(A &a, ks_ctx *c, const KsCoarseSizes &s) {
   a.add(&c->bH_part, 4 * s.ni * s.np, "bH_part");
   a.add(&c->cH_part, 4 * s.ni * s.np, "cH_part");
   a.add(&c->gram_part, s.gram, "gram partials");
+  a.add(&c->islice0, s.ni + 1, "item first slice");
+  a.add(&c->isell_ptr, s.nis + 1, "item sell ptr");
+  a.add(&c->inat, s.nf, "item rows: natural sell base");
+  a.add(&c->isell_col, s.istot, "item sell col");
+  a.add(&c->islot, s.istot, "item sell window slots");
 }
 
 // temporaries of ks_set_coarse (call scratch in KS_R_WORK); the grouping arrays first live here too
@@ -149,6 +155,7 @@ struct KsCoarseTemps {
   uint64_t *key = nullptr, *key_sorted = nullptr;
   int32_t *rows = nullptr, *flag = nullptr, *gincl = nullptr, *gfirst = nullptr, *iflag = nullptr, *iincl = nullptr;
   int32_t *item_of_pos = nullptr, *ct_key = nullptr, *ct_key_sorted = nullptr, *ct_val = nullptr, *dcnt = nullptr;
+  int32_t *islice0 = nullptr, *isw = nullptr, *isell_ptr = nullptr;   // item slices (first, widths, slot offsets)
   int *dmax = nullptr;
   uint8_t *cub = nullptr;
   size_t cub_bytes = 0;
@@ -179,7 +186,7 @@ void ks_layout_coarse_temps_rows(A &a, KsCoarseTemps &t, int64_t nf, int64_t pn,
 }
 // the part sized by the item count
 template <class A>
-void ks_layout_coarse_temps_items(A &a, KsCoarseTemps &t, int64_t ni) {
+void ks_layout_coarse_temps_items(A &a, KsCoarseTemps &t, int64_t ni, int64_t nf) {
   a.add(&t.item_ptr, ni + 1, "c.item_ptr");
   a.add(&t.item_S, 4 * ni, "c.item_S");
   a.add(&t.item_D_ptr, ni + 1, "c.item_D_ptr");
@@ -187,6 +194,10 @@ void ks_layout_coarse_temps_items(A &a, KsCoarseTemps &t, int64_t ni) {
   a.add(&t.ct_key_sorted, 4 * ni, "c.ct_key_sorted");
   a.add(&t.ct_val, 4 * ni, "c.ct_val");
   a.add(&t.dcnt, ni + 1, "c.dcnt");
+  const int64_t nis = ni + (nf + 7) / 8;   // sum of ceil(rows / 8) over items
+  a.add(&t.islice0, ni + 1, "c.islice0");
+  a.add(&t.isw, nis + 1, "c.isw");
+  a.add(&t.isell_ptr, nis + 1, "c.isell_ptr");
 }
 
 // call scratch of KS_R_WORK: ks_set_coarse's temporaries (items <= rows, p_nnz <= 4 rows) and the
@@ -195,7 +206,7 @@ inline size_t ks_scratch_bound(const KsMeshSizes &z, int max_N, int sm_count, si
   KsSizer s;
   KsCoarseTemps t;
   ks_layout_coarse_temps_rows(s, t, z.nf, 4 * z.nf, coarse_cub);
-  ks_layout_coarse_temps_items(s, t, z.nf);
+  ks_layout_coarse_temps_items(s, t, z.nf, z.nf);
   KsSizer r;
   double *part = nullptr;
   r.add(&part, (int64_t)2 * max_N * 4 * sm_count, "true residual partials");

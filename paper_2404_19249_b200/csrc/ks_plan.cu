@@ -140,6 +140,9 @@ ks_status ks_coarse_cub_bytes(int64_t nf, size_t *bytes) {
   m = std::max(m, b);
   if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(nullptr, b, i32, i32, (int)(nf + 1));
   m = std::max(m, b);
+  // item slices of the item-ordered sliced-ELL copy: at most n_items + n_free / 8 <= 9 n_free / 8 (+ 1)
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(nullptr, b, i32, i32, (int)(nf + (nf + 7) / 8 + 1));
+  m = std::max(m, b);
   if (e == cudaSuccess) e = cub::DeviceReduce::Max(nullptr, b, i32, ip, (int)nf);
   m = std::max(m, b);
   if (e == cudaSuccess) e = cub::DeviceRadixSort::SortPairs(nullptr, b, i32, i32, i32, i32, (int)(4 * nf), 0, 32);

@@ -213,6 +213,59 @@ __global__ void k_lower_bound_ptr(const int32_t *__restrict__ keys, int64_t nk, 
   ptr[r] = (int32_t)lo;
 }
 
+// ---- item-ordered sliced-ELL copy of the pattern (k_proj_ai): items padded to whole 8-row slices ----
+__global__ void k_item_nslices(const int32_t *__restrict__ item_ptr, int64_t ni, int32_t *__restrict__ cnt) {
+  const int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (it < ni) cnt[it] = (item_ptr[it + 1] - item_ptr[it] + KS_SELL_C - 1) / KS_SELL_C;
+}
+// slots of every item slice: 8 rows x its longest row rounded up to a 4-slot group
+__global__ void k_islice_width(const int32_t *__restrict__ item_ptr, const int32_t *__restrict__ islice0,
+                               const int32_t *__restrict__ perm, const int32_t *__restrict__ row_ptr, int64_t ni,
+                               int32_t *__restrict__ isw) {
+  const int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (it >= ni) return;
+  const int32_t p0 = item_ptr[it], nr = item_ptr[it + 1] - p0;
+  for (int32_t r0 = 0; r0 < nr; r0 += KS_SELL_C) {
+    int32_t w = 0;
+    for (int32_t r = r0; r < nr && r < r0 + KS_SELL_C; r++) {
+      const int32_t i = perm[p0 + r];
+      w = max(w, row_ptr[i + 1] - row_ptr[i]);
+    }
+    isw[islice0[it] + r0 / KS_SELL_C] = (w + 3) / 4 * 4 * KS_SELL_C;
+  }
+}
+// thread per item position: the row's item-layout columns (padding: own row) and window-slot words
+// (word (g, t): byte u = slot of parent t of column 4g+u, 255 absent or padding), and its natural sliced-ELL base
+// and slot groups (H is read there)
+__global__ void k_isell_fill(const int32_t *__restrict__ perm, const int32_t *__restrict__ item_of_pos,
+                             const int32_t *__restrict__ item_ptr, const int32_t *__restrict__ islice0,
+                             const int32_t *__restrict__ isell_ptr, const int32_t *__restrict__ row_ptr,
+                             const int32_t *__restrict__ col, const int32_t *__restrict__ sell_ptr,
+                             const uint8_t *__restrict__ slotmap, int64_t n_free, int2 *__restrict__ inat,
+                             int32_t *__restrict__ icol, uint32_t *__restrict__ islot) {
+  const int64_t pos = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (pos >= n_free) return;
+  const int32_t i = perm[pos], it = item_of_pos[pos];
+  const int64_t ip = (int64_t)KS_SELL_C * islice0[it] + (pos - item_ptr[it]);
+  const int32_t sb = isell_ptr[ip / KS_SELL_C], groups = (isell_ptr[ip / KS_SELL_C + 1] - sb) / (4 * KS_SELL_C);
+  const int32_t base = sb + (int32_t)(ip % KS_SELL_C) * 4;
+  const int32_t k0 = row_ptr[i], len = row_ptr[i + 1] - k0;
+  const int32_t nb = sell_ptr[i / KS_SELL_C] + (i % KS_SELL_C) * 4;
+  inat[pos] = make_int2(nb, (len + 3) / 4);
+  for (int g = 0; g < groups; g++)
+    for (int q = 0; q < 4; q++) {
+      const int k = 4 * g + q;
+      const int64_t o = base + (int64_t)g * (4 * KS_SELL_C) + q;
+      icol[o] = k < len ? col[k0 + k] : i;
+      uint32_t w = 0;
+      for (int u = 3; u >= 0; u--) {
+        const int ku = 4 * g + u;
+        w = (w << 8) | (ku < len ? (uint32_t)slotmap[4 * (int64_t)(k0 + ku) + q] : 255u);
+      }
+      islot[o] = w;
+    }
+}
+
 // ---------------------------------------------------------------------------------------------
 // projection kernels (v2)
 // ---------------------------------------------------------------------------------------------
@@ -328,6 +381,102 @@ __global__ void __launch_bounds__(ITEM_ROWS, KS_PA_MINB) k_proj_a(const int32_t 
     // G = P_item^T W on the FP64 tensor cores: warp w takes the 8-column tiles w, w + 4, ... of the window;
     // k-steps of 4 rows; A[m = c][k = r] = P_rc (rows 4..7 zero), B[k = r][n = d] = W[r][d]. Rows past nr
     // and columns past dn are zeroed by select (stale shared memory).
+    const int lane = tid & 31, warp = tid >> 5, grp = lane >> 2, tig = lane & 3;
+    double *out = AH_part + 4 * (int64_t)d0;
+    for (int t = warp; 8 * t < dn; t += ITEM_ROWS / 32) {
+      const int d = 8 * t + grp;
+      double c0 = 0.0, c1 = 0.0;
+      for (int r0 = 0; r0 < nr; r0 += 4) {
+        const int r = r0 + tig;
+        const double av = (grp < 4 && r < nr) ? Ps[r * 4 + grp] : 0.0;
+        const double bv = (r < nr && d < dn) ? W[r * ws + d] : 0.0;
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(c0), "+d"(c1) : "d"(av), "d"(bv));
+      }
+      if (grp < 4) {
+        const int dd = 8 * t + 2 * tig;
+        if (dd < dn) out[grp * dn + dd] = c0;
+        if (dd + 1 < dn) out[grp * dn + dd + 1] = c1;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// k_proj_a on the item-ordered sliced-ELL copy (KS_PROJ_FUSED=3): thread = row of the item as in k_proj_a, but each
+// 4-slot group of the row is one coalesced 16-byte column load, one 16-byte window-slot load (the 4 parents' words)
+// and one 32-byte H sector (natural layout), instead of per-entry loads scattered over the rows of the item. Same
+// entries in the same order into the same window rows and the same k-step chain: bitwise k_proj_a's partials.
+#ifndef KS_PAI_G
+#define KS_PAI_G 4
+#endif
+#ifndef KS_PAI_MINB
+#define KS_PAI_MINB 1
+#endif
+constexpr int PAI_G = KS_PAI_G;   // slot groups (16 entries) in flight per thread
+__global__ void __launch_bounds__(ITEM_ROWS, KS_PAI_MINB) k_proj_ai(
+    const int32_t *__restrict__ item_ptr, const int32_t *__restrict__ islice0, const int32_t *__restrict__ isell_ptr,
+    const int32_t *__restrict__ isell_col, const int2 *__restrict__ inat, const double *__restrict__ sval,
+    const uint32_t *__restrict__ islot, const double *__restrict__ Pv4, const double *__restrict__ Pv4p,
+    const int32_t *__restrict__ D_ptr, int64_t n_items, int wcap, double *__restrict__ AH_part) {
+  extern __shared__ double smem[];
+  const int ws = wcap + 1;
+  double *W = smem;                              // [ITEM_ROWS][ws]
+  double *Ps = smem + ITEM_ROWS * ws;            // [ITEM_ROWS][4]
+  const int tid = threadIdx.x;
+  for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const int32_t p0 = __ldg(item_ptr + it), nr = __ldg(item_ptr + it + 1) - p0, s0 = __ldg(islice0 + it);
+    const int32_t d0 = __ldg(D_ptr + it), dn = __ldg(D_ptr + it + 1) - d0;
+    double *Wl = W + tid * ws;
+    for (int d = 0; d < dn; d++) Wl[d] = 0.0;
+    if (tid < nr) {
+      double pi0, pi1, pi2, pi3;
+      ldnc_v4(Pv4p + 4 * (int64_t)(p0 + tid), pi0, pi1, pi2, pi3);
+      Ps[tid * 4 + 0] = pi0; Ps[tid * 4 + 1] = pi1; Ps[tid * 4 + 2] = pi2; Ps[tid * 4 + 3] = pi3;
+      const int2 nat = __ldg(inat + p0 + tid);
+      const int64_t ib = __ldg(isell_ptr + s0 + tid / KS_SELL_C) + (tid % KS_SELL_C) * 4;
+      for (int g0 = 0; g0 < nat.y; g0 += PAI_G) {
+        int4 c[PAI_G];
+        uint4 sw[PAI_G];
+        double h[PAI_G][4];
+#pragma unroll
+        for (int q = 0; q < PAI_G; q++) {
+          const int g = g0 + q < nat.y ? g0 + q : g0;   // past the row: a repeat, masked below
+          const int64_t o = ib + (int64_t)g * (4 * KS_SELL_C);
+          c[q] = __ldg(reinterpret_cast<const int4 *>(isell_col + o));
+          sw[q] = __ldg(reinterpret_cast<const uint4 *>(islot + o));
+          ldnc_v4(sval + nat.x + (int64_t)g * (4 * KS_SELL_C), h[q][0], h[q][1], h[q][2], h[q][3]);
+        }
+        double pv[PAI_G][4][4];
+#pragma unroll
+        for (int q = 0; q < PAI_G; q++) {
+          ldnc_v4(Pv4 + 4 * (int64_t)c[q].x, pv[q][0][0], pv[q][0][1], pv[q][0][2], pv[q][0][3]);
+          ldnc_v4(Pv4 + 4 * (int64_t)c[q].y, pv[q][1][0], pv[q][1][1], pv[q][1][2], pv[q][1][3]);
+          ldnc_v4(Pv4 + 4 * (int64_t)c[q].z, pv[q][2][0], pv[q][2][1], pv[q][2][2], pv[q][2][3]);
+          ldnc_v4(Pv4 + 4 * (int64_t)c[q].w, pv[q][3][0], pv[q][3][1], pv[q][3][2], pv[q][3][3]);
+        }
+#pragma unroll
+        for (int q = 0; q < PAI_G; q++) {
+          if (g0 + q >= nat.y) break;
+          const uint32_t w4[4] = {sw[q].x, sw[q].y, sw[q].z, sw[q].w};
+#pragma unroll
+          for (int u = 0; u < 4; u++) {   // entry 4g+u; parent t's slot is byte u of word t
+            int sl[4];
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+              const int v = (int)((w4[t] >> (8 * u)) & 255u);
+              sl[t] = v == 255 ? wcap : v;
+            }
+            const double w0 = Wl[sl[0]], w1 = Wl[sl[1]], w2 = Wl[sl[2]], w3 = Wl[sl[3]];
+            Wl[sl[0]] = fma(h[q][u], pv[q][u][0], w0);
+            Wl[sl[1]] = fma(h[q][u], pv[q][u][1], w1);
+            Wl[sl[2]] = fma(h[q][u], pv[q][u][2], w2);
+            Wl[sl[3]] = fma(h[q][u], pv[q][u][3], w3);
+          }
+        }
+      }
+    }
+    __syncthreads();
     const int lane = tid & 31, warp = tid >> 5, grp = lane >> 2, tig = lane & 3;
     double *out = AH_part + 4 * (int64_t)d0;
     for (int t = warp; 8 * t < dn; t += ITEM_ROWS / 32) {
@@ -907,6 +1056,22 @@ __global__ void k_item_order(const int32_t *__restrict__ perm, const double *__r
   for (int t = 0; t < 4; t++) Pv4p[4 * pos + t] = Pv4[4 * (int64_t)i + t];
 }
 
+ks_status launch_proj_ai(ks_ctx *ctx, const double *op_sell_vals) {   // Op in the natural sliced-ELL layout
+  const int wcap = ctx->d_max;
+  const size_t sm = sizeof(double) * (size_t)ITEM_ROWS * (wcap + 1 + 4);
+  if (sm > 200 * 1024) return ks_fail(ctx, KS_E_ARG, "coarse window %d too large", ctx->d_max);
+  KS_CUDA(ctx, cudaFuncSetAttribute(k_proj_ai, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  int per_sm = 0;
+  KS_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_proj_ai, ITEM_ROWS, sm));
+  int64_t grid = (int64_t)(per_sm > 0 ? per_sm : 1) * ctx->sm_count * 4;
+  if (grid > ctx->n_items) grid = ctx->n_items;
+  k_proj_ai<<<(unsigned)(grid > 0 ? grid : 1), ITEM_ROWS, sm, ctx->stream>>>(
+      ctx->item_ptr, ctx->islice0, ctx->isell_ptr, ctx->isell_col, ctx->inat, op_sell_vals, ctx->islot, ctx->Pv4,
+      ctx->Pv4p, ctx->item_D_ptr, ctx->n_items, wcap, ctx->AH_part);
+  KS_LAUNCHED(ctx);
+  return KS_OK;
+}
+
 ks_status launch_proj_a(ks_ctx *ctx, const double *op_sell_vals) {   // Op in the sliced-ELL layout
   const int wcap = ctx->d_max;
   const size_t sm = sizeof(double) * (size_t)ITEM_ROWS * (wcap + 1 + 4);
@@ -921,6 +1086,13 @@ ks_status launch_proj_a(ks_ctx *ctx, const double *op_sell_vals) {   // Op in th
       ctx->item_D_ptr, ctx->n_items, wcap, ctx->AH_part);
   KS_LAUNCHED(ctx);
   return KS_OK;
+}
+
+// KS_PROJ_AI=0 selects k_proj_a (per-row entry loads) for the A_H pass (A/B knob; read per call, so
+// tests can compare both in one process); default: k_proj_ai on the item-ordered copy
+bool proj_ai_enabled() {
+  const char *e = getenv("KS_PROJ_AI");
+  return !(e && e[0] == '0');
 }
 
 // KS_PROJ_MMA=0 selects the FFMA item pass (A/B knob); default: tensor cores
@@ -1060,6 +1232,10 @@ void ks_free_coarse(ks_ctx *ctx) {
   ctx->Y_H = ctx->Y_M = ctx->proj_u = ctx->proj_up = ctx->bH_part = ctx->cH_part = ctx->gram_part = nullptr;
   ctx->gram_cap = 0;
   ctx->n_H = 0;
+  ctx->islice0 = ctx->isell_ptr = ctx->isell_col = nullptr;
+  ctx->inat = nullptr;
+  ctx->islot = nullptr;
+  ctx->n_islices = ctx->isell_total = 0;
 }
 
 static int proj_np(int max_N) {
@@ -1132,7 +1308,7 @@ ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, cons
   KS_CUDA(ctx, cudaMemcpyAsync(&h_items, t.iincl + nf - 1, 4, cudaMemcpyDeviceToHost, s));
   KS_CUDA(ctx, cudaStreamSynchronize(s));
   const int64_t ni = h_items;
-  ks_layout_coarse_temps_items(cv, t, ni);
+  ks_layout_coarse_temps_items(cv, t, ni, nf);
   KS_TRY(cv.st);
   int32_t h_nf = (int32_t)nf;
   KS_CUDA(ctx, cudaMemcpyAsync(t.item_ptr + ni, &h_nf, 4, cudaMemcpyHostToDevice, s));
@@ -1162,7 +1338,30 @@ ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, cons
   if (h_dmax > DMAX - 1)
     return ks_fail(ctx, KS_E_ARG, "an item touches %d coarse nodes (> %d): coarse mesh too fine for the fine mesh",
                    h_dmax, DMAX - 1);
+  // ---- item slices of the item-ordered sliced-ELL copy (k_proj_ai): counts, widths, slot offsets ----
+  KS_CUDA(ctx, cudaMemsetAsync(t.isw + ni, 0, 4, s));
+  k_item_nslices<<<ks_blocks(ni, 256), 256, 0, s>>>(t.item_ptr, ni, t.isw);
+  KS_LAUNCHED(ctx);
+  tb = cub_cap;
+  KS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(cub_tmp, tb, t.isw, t.islice0, (int)(ni + 1), s));
+  ctx->launches++;
+  int32_t h_nis = 0;
+  KS_CUDA(ctx, cudaMemcpyAsync(&h_nis, t.islice0 + ni, 4, cudaMemcpyDeviceToHost, s));
+  KS_CUDA(ctx, cudaStreamSynchronize(s));
+  k_islice_width<<<ks_blocks(ni, 128), 128, 0, s>>>(t.item_ptr, t.islice0, t.perm, ctx->row_ptr, ni, t.isw);
+  KS_LAUNCHED(ctx);
+  KS_CUDA(ctx, cudaMemsetAsync(t.isw + h_nis, 0, 4, s));
+  tb = cub_cap;
+  KS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(cub_tmp, tb, t.isw, t.isell_ptr, (int)(h_nis + 1), s));
+  ctx->launches++;
+  int32_t h_istot = 0;
+  KS_CUDA(ctx, cudaMemcpyAsync(&h_istot, t.isell_ptr + h_nis, 4, cudaMemcpyDeviceToHost, s));
+  KS_CUDA(ctx, cudaStreamSynchronize(s));
+  if (h_istot < 0) return ks_fail(ctx, KS_E_ARG, "item-ordered sliced-ELL copy exceeds 2^31 slots");
+
   KsCoarseSizes cs;
+  cs.nis = h_nis;
+  cs.istot = h_istot;
   cs.nf = nf;
   cs.nnz = ctx->nnz;
   cs.pn = pn;
@@ -1209,6 +1408,18 @@ ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, cons
                                                ctx->col, ctx->P_ptr, ctx->P_col, nf, ctx->slotmap);
   KS_LAUNCHED(ctx);
 
+  // ---- the item-ordered sliced-ELL copy of the pattern (columns, window slots) for k_proj_ai ----
+  ctx->n_islices = h_nis;
+  ctx->isell_total = h_istot;
+  KS_CUDA(ctx, cudaMemcpyAsync(ctx->islice0, t.islice0, 4 * (ni + 1), cudaMemcpyDeviceToDevice, s));
+  KS_CUDA(ctx, cudaMemcpyAsync(ctx->isell_ptr, t.isell_ptr, 4 * ((int64_t)h_nis + 1), cudaMemcpyDeviceToDevice, s));
+  KS_CUDA(ctx, cudaMemsetAsync(ctx->isell_col, 0, 4 * (size_t)h_istot, s));   // pad rows gather row 0
+  KS_CUDA(ctx, cudaMemsetAsync(ctx->islot, 0xff, 4 * (size_t)h_istot, s));
+  k_isell_fill<<<ks_blocks(nf, 128), 128, 0, s>>>(ctx->perm, t.item_of_pos, ctx->item_ptr, ctx->islice0,
+                                                  ctx->isell_ptr, ctx->row_ptr, ctx->col, ctx->sell_ptr, ctx->slotmap, nf, ctx->inat, ctx->isell_col,
+                                                  ctx->islot);
+  KS_LAUNCHED(ctx);
+
   // ---- coarse node -> items list (stable sort on the coarse id; pads sort last) ----
   int ct_bits = 1;
   while ((1ll << ct_bits) <= n_H) ct_bits++;
@@ -1250,7 +1461,8 @@ ks_status ks_project_impl(ks_ctx *ctx, int N, const double *Ut, double *FA, doub
     default: return ks_fail(ctx, KS_E_ARG, "N = %d unsupported", N);
   }
   // K8b: A_H item partials (unshifted H, reading Q1)
-  KS_TRY(launch_proj_a(ctx, ctx->sell_H));
+  if (proj_ai_enabled() && ctx->isell_col) KS_TRY(launch_proj_ai(ctx, ctx->sell_H));
+  else KS_TRY(launch_proj_a(ctx, ctx->sell_H));
   // K9: A_H, b_H, c_H
   KS_TRY(launch_final<true>(ctx, N, np, FA, FB, D, D));
   k_copy_block<<<ks_blocks(nH * nH, 256), 256, 0, s>>>(ctx->B_H, nH, FB, D);
