@@ -160,6 +160,8 @@ struct ks_ctx {
   void *cublas = nullptr;           // cuBLAS handle of the filtered pencil eigensolver (ks_outer.cu)
   double *ef_buf = nullptr;         // [4][D][m] work blocks of the filtered eigensolver
   double *ef_small = nullptr;       // [m][m] device staging of the small Rayleigh-Ritz / SVQB matrices
+  double *ef_dev = nullptr;         // scratch of the device-resident filtered iteration (ks_efdev.cu)
+  int ef_rounds = 0;                // Rayleigh-Ritz rounds of the last filtered solve
   int64_t ef_L_D = 0;                // D of the Cholesky factor held in eig_B (0: none)
   // cached Cholesky factor of the coarse block B_H (ks_outer.cu coarse_chol_reduction), per coarse space
   int ef_LH_state = 0;              // 0: not built, 1: built, -1: unusable
@@ -258,6 +260,10 @@ ks_status ks_pcg2l_run(ks_ctx *ctx, const double *b, const double *x0, double *x
 void ks_free_pcg2l(ks_ctx *ctx);
 ks_status ks_assemble_impl(ks_ctx *ctx, const double *d_veff, double mu);
 ks_status ks_materialize_views(ks_ctx *ctx);
+int64_t ks_ef_device_scratch(int sm_count, int m, int64_t D);
+ks_status ks_ef_device(ks_ctx *ctx, int64_t D, int k, int m, const double *C, const double *x0, double *x_out,
+                       const double *bound_dev, double *scratch, int maxit, int deg, double tol, int *status,
+                       int *rounds, bool *ran, double **lam_dev);
 
 ks_status ks_star_setup(ks_ctx *ctx, int *d_tmp);  // d_tmp: one int of setup scratch
 ks_status ks_spmm_impl(ks_ctx *ctx, ks_op op, const double *val, int N, const double *X, double *Y);

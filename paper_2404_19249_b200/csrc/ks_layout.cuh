@@ -235,6 +235,7 @@ void ks_layout_ext(A &a, ks_ctx *c, const KsExtSizes &e) {
     a.add(&c->eig_work, e.lwork, "cuSOLVER workspace");
     a.add(&c->ef_buf, 4 * D * m, "filtered eig blocks");
     a.add(&c->ef_small, 2 * m * m + m + 1, "filtered eig small");
+    a.add(&c->ef_dev, ks_ef_device_scratch(e.sm_count, (int)m, D), "filtered eig device scratch");
     a.add(&c->blas_ws, (int64_t)KS_EXT_BLAS_WS, "cuBLAS workspace");
     if (e.nH > 0) {   // cached coarse factor and the explicit L^-1 of the fast reduction
       a.add(&c->ef_LH, e.nH * e.nH, "L_H");

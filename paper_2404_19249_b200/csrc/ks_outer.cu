@@ -438,12 +438,38 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
   KS_CUDA(ctx, cudaMemsetAsync(sm, 0, sizeof(double), st));
   k_row_abs_max<<<ks_blocks(32 * D, 256), 256, 0, st>>>(A, D, reinterpret_cast<unsigned long long *>(sm));
   KS_LAUNCHED(ctx);
-  KS_CUDA(ctx, cudaMemcpyAsync(&bound, sm, sizeof(double), cudaMemcpyDeviceToHost, st));
-  KS_CUDA(ctx, cudaStreamSynchronize(st));
   const double tol = 1e-12;
-  std::vector<double> G((size_t)m * m), w, V, Tm, lam(m), res(k);
   int maxit = EF_MAXIT;   // KS_PENCIL_EF_MAXIT: test hook to exercise the dense fallback
   if (const char *e = getenv("KS_PENCIL_EF_MAXIT")) maxit = atoi(e);
+  // KS_PENCIL_DEVICE=1: the whole iteration as one cooperative kernel (ks_efdev.cu, measured slower)
+  const char *devrr = getenv("KS_PENCIL_DEVICE");
+  if (devrr && devrr[0] == '1' && ctx->ef_dev) {
+    int stv = 0, rounds = 0;
+    bool ran = false;
+    double *lam_dev = nullptr;
+    KS_TRY(ks_ef_device(ctx, D, k, m, A, X, CX, sm, ctx->ef_dev, maxit, EF_DEG, tol, &stv, &rounds, &ran, &lam_dev));
+    if (ran) {
+      ctx->ef_rounds = rounds;
+      if (stv != 1) return KS_OK;   // not converged or a collapsed block: the dense path
+      // the orthonormal block is in CX: y = L^-T x, eigenvalues, eigenvectors [D][k] row-major
+      if (Linv) {
+        KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, (int)D, k, (int)D, &one, Linv, (int)D, CX, (int)D, &zero,
+                                 T2, (int)D));
+      } else {
+        KS_CUDA(ctx, cudaMemcpyAsync(T2, CX, sizeof(double) * D * k, cudaMemcpyDeviceToDevice, st));
+        KS_BLAS(ctx, cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)D,
+                                 k, &one, L, (int)D, T2, (int)D));
+      }
+      KS_CUDA(ctx, cudaMemcpyAsync(evals, lam_dev, sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
+      k_take_evecs<<<ks_blocks(D * k, 256), 256, 0, st>>>(T2, D, k, evecs);
+      KS_LAUNCHED(ctx);
+      *done = true;
+      return KS_OK;
+    }
+  }
+  KS_CUDA(ctx, cudaMemcpyAsync(&bound, sm, sizeof(double), cudaMemcpyDeviceToHost, st));
+  KS_CUDA(ctx, cudaStreamSynchronize(st));
+  std::vector<double> G((size_t)m * m), w, V, Tm, lam(m), res(k);
   // host: Cholesky of the column-scaled Gram G = D R^T R D (upper R, column-major); false on a collapsed pivot
   auto host_chol = [&](const std::vector<double> &Gm, std::vector<double> &dsc, std::vector<double> &Rinv) -> bool {
     dsc.resize(m);
@@ -474,6 +500,7 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
   };
   std::vector<double> G2((size_t)m * m), dsc, Rinv, Hs((size_t)m * m);
   for (int it = 0; it < maxit; it++) {
+    ctx->ef_rounds = it + 1;
     // Rayleigh-Ritz on span(X) with the orthonormalisation folded in: T2 = C X, G = X^T X and H = X^T C X in
     // one round trip; on the host the small pencil (H, G) is reduced by the Cholesky factor of the scaled G
     // and diagonalised by Jacobi: V = D^-1 R^-1 W, X <- X V (orthonormal), CX <- (C X) V
@@ -485,7 +512,10 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
     KS_CUDA(ctx, cudaMemcpyAsync(G.data(), sm, sizeof(double) * m * m, cudaMemcpyDeviceToHost, st));
     KS_CUDA(ctx, cudaMemcpyAsync(G2.data(), sm + (int64_t)m * m, sizeof(double) * m * m, cudaMemcpyDeviceToHost, st));
     KS_CUDA(ctx, cudaStreamSynchronize(st));
-    if (!host_chol(G, dsc, Rinv)) return KS_OK;   // the block lost rank: dense path
+    if (!host_chol(G, dsc, Rinv)) {   // the block lost rank: dense path
+      if (getenv("KS_EF_VERBOSE")) fprintf(stderr, "ks_pencil_eig: round %d: Gram pivot collapsed\n", it + 1);
+      return KS_OK;
+    }
     // Hs = R^-T (D^-1 H D^-1) R^-1
     for (int j = 0; j < m; j++)
       for (int i = 0; i < m; i++) G2[(size_t)j * m + i] /= dsc[i] * dsc[j];
@@ -526,6 +556,7 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
     KS_CUDA(ctx, cudaStreamSynchronize(st));
     double rmax = 0.0;
     for (int j = 0; j < k; j++) rmax = std::fmax(rmax, std::sqrt(res[j]));
+    if (getenv("KS_EF_VERBOSE")) fprintf(stderr, "ks_pencil_eig: round %d rmax %.3e (tol %.3e)\n", it + 1, rmax, tol * bound);
     if (!std::isfinite(rmax)) return KS_OK;
     if (rmax <= tol * bound) {
       // one more Cholesky-QR pass (X V is orthonormal only up to cond(X)^2 eps), then y = L^-T x, evals
@@ -552,7 +583,7 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
       *done = true;
       return KS_OK;
     }
-    // Chebyshev filter of degree EF_DEG damping [lam_m, bound]; X_prev = X, Y = sigma/e (C X - c X)
+    // Chebyshev filter damping [lam_m, bound]
     const double a = lam[m - 1], b = bound, e = 0.5 * (b - a), c = 0.5 * (b + a);
     if (!(e > 0.0)) return KS_OK;
     double sigma = e / (lam[0] - c);

@@ -11,6 +11,7 @@ import gen  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--env", default="", help="NAME=VALUE set before the timed calls (A/B knob)")
 a = ap.parse_args()
 
 import torch  # noqa: E402
@@ -27,6 +28,11 @@ Ut, _, _ = ctx.block_solve(t(p.lam), t(p.U))
 FA, FB = ctx.project_augmented(Ut)
 ev, Y = ctx.pencil_eig(FA, FB, p.N)
 torch.cuda.synchronize()
+if a.env:
+    k_, v_ = a.env.split("=", 1)
+    os.environ[k_] = v_
+    ev, Y = ctx.pencil_eig(FA, FB, p.N)
+    torch.cuda.synchronize()
 s = torch.cuda.current_stream()
 for r in range(a.reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -37,3 +43,14 @@ for r in range(a.reps):
     torch.cuda.synchronize()
     print(f"pencil_eig D={FA.shape[0]} k={p.N}: events {e0.elapsed_time(e1):.3f} ms, wall {1e3*(time.perf_counter()-w0):.3f} ms")
 assert ctx.sync() == 0
+if os.environ.get("KS_EF_TRACE") == "1":   # phase times of the device-resident loop (ks_efdev.cu stamps, CTA 0)
+    import numpy as np
+    t = ctx.solve_trace().astype(np.int64).reshape(-1, 2)
+    names = {1: "gemm", 2: "gram", 3: "chol", 4: "reduce", 5: "jacobi", 6: "update", 7: "resid", 8: "filter"}
+    tot = {}
+    for (tag0, t0), (tag1, t1) in zip(t[:-1], t[1:]):
+        if tag1 in names:
+            tot[names[tag1]] = tot.get(names[tag1], 0.0) + (t1 - t0) / 1e3
+    rounds = int((t[:, 0] == 0).sum())
+    print("device loop rounds", rounds, "phase totals us:", {k: round(v, 1) for k, v in tot.items()},
+          "total", round(float((t[-1, 1] - t[0, 1]) / 1e3), 1))
