@@ -171,6 +171,9 @@ constexpr int STAR_MAX = 64, ASM_WARPS = 8;
 #else
 #define KS_ASM_BOUNDS __launch_bounds__(ASM_WARPS * 32)
 #endif
+#ifndef KS_ASM_NGC
+#define KS_ASM_NGC 2   // slot groups whose loads are issued together (before the star staging for the first chunk)
+#endif
 template <class MT>
 __global__ void KS_ASM_BOUNDS k_assemble_mask(
     const int32_t *__restrict__ sell_ptr, const int32_t *__restrict__ sell_col, const MT *__restrict__ slot_mask,
@@ -178,6 +181,8 @@ __global__ void KS_ASM_BOUNDS k_assemble_mask(
     const int32_t *__restrict__ inv_idx, const double *__restrict__ w, const double *__restrict__ v_free, double mu,
     int64_t n_free, int64_t n_slices, double *__restrict__ sell_A, double *__restrict__ sell_H,
     double *__restrict__ diag, double *__restrict__ dinv) {
+  constexpr int NGC = KS_ASM_NGC;
+  constexpr int KPL = (sizeof(MT) == 8 ? STAR_MAX : 32) / 4;   // star entries per lane (4 lanes per row)
   __shared__ double ws[ASM_WARPS][KS_SELL_C][STAR_MAX + 1];   // +1: the 8 rows on different banks
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t s = (int64_t)blockIdx.x * ASM_WARPS + warp;
@@ -185,45 +190,82 @@ __global__ void KS_ASM_BOUNDS k_assemble_mask(
   double (*st)[STAR_MAX + 1] = ws[warp];
   const int rl = lane >> 2;
   const int64_t row = s * KS_SELL_C + rl;
+  const int32_t b = __ldg(sell_ptr + s), ng = (__ldg(sell_ptr + s + 1) - b) / (4 * KS_SELL_C);
+  // the entry loads of the first NGC slot groups go out first: they do not depend on the star
+  MT mk[NGC];
+  int32_t cg[NGC];
+  double mg[NGC], kg[NGC];
+  auto load_groups = [&](int g0) {
+#pragma unroll
+    for (int q = 0; q < NGC; q++) {
+      mk[q] = 0;
+      if (g0 + q < ng) {
+        const int64_t sp = b + (int64_t)(g0 + q) * (4 * KS_SELL_C) + lane;
+        mk[q] = __ldg(slot_mask + sp);
+        cg[q] = __ldg(sell_col + sp);
+        mg[q] = __ldg(sM + sp);
+        kg[q] = __ldg(sK + sp);
+      }
+    }
+  };
+  load_groups(0);
+  // 4 lanes per row stage its star: every inverse-map index first, then every w_T gather
   double dsum = 0.0;   // the diagonal's sum: the whole star, in walk_sum's four-partial order
-  if (row < n_free) {   // 4 lanes per row stage its star
+  if (row < n_free) {
     const int2 sd = __ldg(star + row);
-#pragma unroll 4
-    for (int k = lane & 3; k < sd.y; k += 4) {
-      const double x = __ldg(w + (__ldg(inv_idx + sd.x + k) >> 4));
-      st[rl][k] = x;
-      dsum += x;
+    int32_t ix[KPL];
+#pragma unroll
+    for (int j = 0; j < KPL; j++) {
+      const int k = (lane & 3) + 4 * j;
+      ix[j] = k < sd.y ? __ldg(inv_idx + sd.x + k) : -1;
+    }
+    double x[KPL];
+#pragma unroll
+    for (int j = 0; j < KPL; j++) x[j] = ix[j] >= 0 ? __ldg(w + (ix[j] >> 4)) : 0.0;
+#pragma unroll
+    for (int j = 0; j < KPL; j++) {
+      const int k = (lane & 3) + 4 * j;
+      if (k < sd.y) {
+        st[rl][k] = x[j];
+        dsum += x[j];
+      }
     }
   }
   dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);   // p0 + p1 (= p1 + p0), p2 + p3
   dsum += __shfl_xor_sync(0xffffffffu, dsum, 2);   // (p0 + p1) + (p2 + p3) on all four lanes
   __syncwarp();
-  const int32_t b = __ldg(sell_ptr + s), ng = (__ldg(sell_ptr + s + 1) - b) / (4 * KS_SELL_C);
   const double vi = row < n_free ? __ldg(v_free + row) : 0.0;
-  for (int g = 0; g < ng; g++) {
-    const int64_t sp = b + (int64_t)g * (4 * KS_SELL_C) + lane;
-    MT mk = __ldg(slot_mask + sp);
-    if (!mk) continue;   // padding slot (stays 0)
-    const int32_t c = __ldg(sell_col + sp);
-    const double m = __ldg(sM + sp), kk = __ldg(sK + sp), vc = __ldg(v_free + c);
-    double sum = dsum;
-    if (c != row) {
-      sum = 0.0;
-      do {
-        sum += st[rl][sizeof(MT) == 8 ? __ffsll((long long)mk) - 1 : __ffs((int)mk) - 1];
-        mk &= mk - 1;
-      } while (mk);
-    }
-    double mv;
-    if (c == row) mv = vi * m / 3.0 + sum / 60.0;
-    else mv = (vi + vc) * m / 6.0 + sum / 120.0;
-    const double h = 0.5 * kk + mv;
-    const double a = h + mu * m;
-    sell_A[sp] = a;
-    sell_H[sp] = h;
-    if (c == row) {
-      diag[row] = a;
-      dinv[row] = 1.0 / a;
+  for (int g0 = 0; g0 < ng; g0 += NGC) {
+    if (g0 > 0) load_groups(g0);
+    double vc[NGC];
+#pragma unroll
+    for (int q = 0; q < NGC; q++) vc[q] = mk[q] ? __ldg(v_free + cg[q]) : 0.0;
+#pragma unroll
+    for (int q = 0; q < NGC; q++) {
+      MT m_ = mk[q];
+      if (!m_) continue;   // padding slot (stays 0) or past the slice
+      const int64_t sp = b + (int64_t)(g0 + q) * (4 * KS_SELL_C) + lane;
+      const int32_t c = cg[q];
+      const double m = mg[q], kk = kg[q];
+      double sum = dsum;
+      if (c != row) {
+        sum = 0.0;
+        do {
+          sum += st[rl][sizeof(MT) == 8 ? __ffsll((long long)m_) - 1 : __ffs((int)m_) - 1];
+          m_ &= m_ - 1;
+        } while (m_);
+      }
+      double mv;
+      if (c == row) mv = vi * m / 3.0 + sum / 60.0;
+      else mv = (vi + vc[q]) * m / 6.0 + sum / 120.0;
+      const double h = 0.5 * kk + mv;
+      const double a = h + mu * m;
+      sell_A[sp] = a;
+      sell_H[sp] = h;
+      if (c == row) {
+        diag[row] = a;
+        dinv[row] = 1.0 / a;
+      }
     }
   }
 }
