@@ -83,6 +83,7 @@ struct PcgArgs {
   // staged S phase of the fused kernel: the largest sliced-ELL entry count of one tile and the stage size
   int emax;
   unsigned stage_bytes;
+  int stage_init;   // the init phase's A, M values and columns fit a stage (20 bytes per slot): staged too
 };
 
 // out[j] = sum_{g < G} part[g*stride + j] for j < nv, fixed order, one warp per value.
@@ -386,11 +387,16 @@ __device__ __forceinline__ void prefetch_rows(const PcgArgs &a, int64_t row0, co
 }
 
 // One row of w = A z with the row's sliced-ELL values and columns in shared memory (a staged tile, below):
-// the same slot groups and accumulation order as sell_row; the gathers of z stay global loads.
-template <int NP>
+// the same slot groups and accumulation order as sell_row; the gathers of z stay global loads. OWN: also return
+// the row's own gathered vector (its diagonal slot; padding slots gather the own row as well).
+template <int NP, bool OWN = false>
 __device__ __forceinline__ void sell_row_s(const double *vs, const int32_t *cs, int base, int groups,
-                                           const double *X, int sub, DV<SL<NP>::VEC> &ya) {
+                                           const double *X, int sub, DV<SL<NP>::VEC> &ya,
+                                           int64_t row = 0, DV<SL<NP>::VEC> *own = nullptr) {
   constexpr int VEC = SL<NP>::VEC;
+  auto take = [&](int32_t col, const DV<VEC> &x) {
+    if (OWN && col == row) *own = x;
+  };
 #pragma unroll
   for (int v = 0; v < VEC; v++) ya.v[v] = 0.0;
   const double *xs = X + sub * VEC;
@@ -418,11 +424,75 @@ __device__ __forceinline__ void sell_row_s(const double *vs, const int32_t *cs, 
     for (int j = 0; j < 8; j++)
 #pragma unroll
       for (int v = 0; v < VEC; v++) ya.v[v] = fma(av[j], x[j].v[v], ya.v[v]);
+    if (OWN) {
+      take(c.x, x[0]); take(c.y, x[1]); take(c.z, x[2]); take(c.w, x[3]);
+      take(d.x, x[4]); take(d.y, x[5]); take(d.z, x[6]); take(d.w, x[7]);
+    }
   }
   for (; g < groups; g++) {
     const int o = base + g * (4 * KS_SELL_C);
     const int4 c = *reinterpret_cast<const int4 *>(cs + o);
     const double2 t0 = *reinterpret_cast<const double2 *>(vs + o), t1 = *reinterpret_cast<const double2 *>(vs + o + 2);
+    const DV<VEC> x0 = DV<VEC>::ld(xs + (int64_t)c.x * NP), x1 = DV<VEC>::ld(xs + (int64_t)c.y * NP);
+    const DV<VEC> x2 = DV<VEC>::ld(xs + (int64_t)c.z * NP), x3 = DV<VEC>::ld(xs + (int64_t)c.w * NP);
+    if (OWN) {
+      take(c.x, x0); take(c.y, x1); take(c.z, x2); take(c.w, x3);
+    }
+#pragma unroll
+    for (int v = 0; v < VEC; v++) {
+      ya.v[v] = fma(t0.x, x0.v[v], ya.v[v]);
+      ya.v[v] = fma(t0.y, x1.v[v], ya.v[v]);
+      ya.v[v] = fma(t1.x, x2.v[v], ya.v[v]);
+      ya.v[v] = fma(t1.y, x3.v[v], ya.v[v]);
+    }
+  }
+}
+
+// One row of ya = A x, yb = M x from a staged tile (A values, M values and columns in shared memory): the slot
+// groups and the accumulation order of sell_row<NP, 2>; the gathers of x stay global loads.
+template <int NP>
+__device__ __forceinline__ void sell_row_s2(const double *vs, const double *ms, const int32_t *cs, int base, int groups,
+                                            const double *X, int sub, DV<SL<NP>::VEC> &ya, DV<SL<NP>::VEC> &yb) {
+  constexpr int VEC = SL<NP>::VEC;
+#pragma unroll
+  for (int v = 0; v < VEC; v++) ya.v[v] = yb.v[v] = 0.0;
+  const double *xs = X + sub * VEC;
+  int g = 0;
+  for (; g + 2 <= groups; g += 2) {
+    const int o = base + g * (4 * KS_SELL_C), o2 = o + 4 * KS_SELL_C;
+    const int4 c = *reinterpret_cast<const int4 *>(cs + o);
+    const int4 d = *reinterpret_cast<const int4 *>(cs + o2);
+    double av[8], bv[8];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int oo = h ? o2 : o;
+      const double2 t0 = *reinterpret_cast<const double2 *>(vs + oo), t1 = *reinterpret_cast<const double2 *>(vs + oo + 2);
+      const double2 u0 = *reinterpret_cast<const double2 *>(ms + oo), u1 = *reinterpret_cast<const double2 *>(ms + oo + 2);
+      av[4 * h] = t0.x; av[4 * h + 1] = t0.y; av[4 * h + 2] = t1.x; av[4 * h + 3] = t1.y;
+      bv[4 * h] = u0.x; bv[4 * h + 1] = u0.y; bv[4 * h + 2] = u1.x; bv[4 * h + 3] = u1.y;
+    }
+    DV<VEC> x[8];
+    x[0] = DV<VEC>::ld(xs + (int64_t)c.x * NP);
+    x[1] = DV<VEC>::ld(xs + (int64_t)c.y * NP);
+    x[2] = DV<VEC>::ld(xs + (int64_t)c.z * NP);
+    x[3] = DV<VEC>::ld(xs + (int64_t)c.w * NP);
+    x[4] = DV<VEC>::ld(xs + (int64_t)d.x * NP);
+    x[5] = DV<VEC>::ld(xs + (int64_t)d.y * NP);
+    x[6] = DV<VEC>::ld(xs + (int64_t)d.z * NP);
+    x[7] = DV<VEC>::ld(xs + (int64_t)d.w * NP);
+#pragma unroll
+    for (int j = 0; j < 8; j++)
+#pragma unroll
+      for (int v = 0; v < VEC; v++) {
+        ya.v[v] = fma(av[j], x[j].v[v], ya.v[v]);
+        yb.v[v] = fma(bv[j], x[j].v[v], yb.v[v]);
+      }
+  }
+  for (; g < groups; g++) {
+    const int o = base + g * (4 * KS_SELL_C);
+    const int4 c = *reinterpret_cast<const int4 *>(cs + o);
+    const double2 t0 = *reinterpret_cast<const double2 *>(vs + o), t1 = *reinterpret_cast<const double2 *>(vs + o + 2);
+    const double2 u0 = *reinterpret_cast<const double2 *>(ms + o), u1 = *reinterpret_cast<const double2 *>(ms + o + 2);
     const DV<VEC> x0 = DV<VEC>::ld(xs + (int64_t)c.x * NP), x1 = DV<VEC>::ld(xs + (int64_t)c.y * NP);
     const DV<VEC> x2 = DV<VEC>::ld(xs + (int64_t)c.z * NP), x3 = DV<VEC>::ld(xs + (int64_t)c.w * NP);
 #pragma unroll
@@ -431,6 +501,10 @@ __device__ __forceinline__ void sell_row_s(const double *vs, const int32_t *cs, 
       ya.v[v] = fma(t0.y, x1.v[v], ya.v[v]);
       ya.v[v] = fma(t1.x, x2.v[v], ya.v[v]);
       ya.v[v] = fma(t1.y, x3.v[v], ya.v[v]);
+      yb.v[v] = fma(u0.x, x0.v[v], yb.v[v]);
+      yb.v[v] = fma(u0.y, x1.v[v], yb.v[v]);
+      yb.v[v] = fma(u1.x, x2.v[v], yb.v[v]);
+      yb.v[v] = fma(u1.y, x3.v[v], yb.v[v]);
     }
   }
 }
@@ -528,13 +602,42 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
       sh[v] = (c < a.N ? __ldg(a.lambda + c) : 0.0) + a.mu;
     }
     constexpr bool PFI = KS_PCG_PREFETCH && NP >= 4;
-    if (PFI && lane == 0 && my_tiles > 0) prefetch_init<RPW>(a, tile_k(0) * TILE + warp * RPW);
+    const bool sti = STG && a.stage_init;   // staged init: each tile's A, M values and columns by bulk copies
+    const unsigned EB = (unsigned)a.emax;
+    auto issue_init = [&](int64_t k) {   // one thread: the bulk copies of tile k into stage (pseq + k) & 1
+      const int64_t r0 = tile_k(k) * TILE;
+      const int64_t rows = min((int64_t)TILE, n - r0);
+      const int32_t e0 = __ldg(a.sell_ptr + r0 / KS_SELL_C);
+      const int32_t e1 = __ldg(a.sell_ptr + (r0 + rows + KS_SELL_C - 1) / KS_SELL_C);
+      const unsigned q = pseq + (unsigned)k, eb = (unsigned)(e1 - e0);
+      unsigned char *st = dyn + (size_t)(q & 1u) * a.stage_bytes;
+      uint64_t *bar = &s_full[q & 1u];
+      mbar_expect_tx(bar, eb * 20u);
+      bulk_g2s(st, a.A + e0, eb * 8u, bar);
+      bulk_g2s(st + 8u * EB, a.sell_col + e0, eb * 4u, bar);
+      bulk_g2s(st + 12u * EB, a.M + e0, eb * 8u, bar);
+    };
+    if (sti && threadIdx.x == 0)
+      for (int64_t k = 0; k < 2 && k < my_tiles; k++) issue_init(k);
+    if (!sti && PFI && lane == 0 && my_tiles > 0) prefetch_init<RPW>(a, tile_k(0) * TILE + warp * RPW);
     for (int64_t kk = 0; kk < my_tiles; kk++) {
       const int64_t row = tile_k(kk) * TILE + warp * RPW + slot;
-      if (PFI && lane == 0 && kk + 1 < my_tiles) prefetch_init<RPW>(a, tile_k(kk + 1) * TILE + warp * RPW);
+      if (!sti && PFI && lane == 0 && kk + 1 < my_tiles) prefetch_init<RPW>(a, tile_k(kk + 1) * TILE + warp * RPW);
+      const unsigned q = pseq + (unsigned)kk;
+      if (sti) mbar_wait(&s_full[q & 1u], (q >> 1) & 1u);
       if (row < n) {
         DV<VEC> au, mu_;
-        sell_row<NP, 2>(a.sell_ptr, a.sell_col, a.A, a.M, row, a.U, sub, au, mu_);
+        if (sti) {
+          const unsigned char *st = dyn + (size_t)(q & 1u) * a.stage_bytes;
+          const int64_t t = tile_k(kk);
+          const int32_t e0 = __ldg(a.sell_ptr + t * (TILE / KS_SELL_C));
+          const int32_t b = __ldg(a.sell_ptr + row / KS_SELL_C), e = __ldg(a.sell_ptr + row / KS_SELL_C + 1);
+          sell_row_s2<NP>(reinterpret_cast<const double *>(st), reinterpret_cast<const double *>(st + 12u * EB),
+                          reinterpret_cast<const int32_t *>(st + 8u * EB), (b - e0) + (int)(row % KS_SELL_C) * 4,
+                          (e - b) / (4 * KS_SELL_C), a.U, sub, au, mu_);
+        } else {
+          sell_row<NP, 2>(a.sell_ptr, a.sell_col, a.A, a.M, row, a.U, sub, au, mu_);
+        }
         const int64_t off = row * NP + sub * VEC;
         const double dinv = __ldg(a.dinv + row);
         DV<VEC> z;
@@ -550,7 +653,16 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
         z.st(Z + off);
         z.st(a.p + off);
       }
+      if (sti) {   // this warp is done with the stage; the producer refills it once all warps are
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[q & 1u]);
+        if (threadIdx.x == 0 && kk + 2 < my_tiles) {
+          mbar_wait(&s_empty[q & 1u], (q >> 1) & 1u);
+          issue_init(kk + 2);
+        }
+      }
     }
+    if (sti) pseq += (unsigned)my_tiles;
     block_cols<NP, 3>(acc, red, tot);
     for (int i = threadIdx.x; i < 3 * NP; i += blockDim.x) part_a[(int64_t)blockIdx.x * STRIDE + i] = tot[i];
     grid_barrier(a.bar, target);
@@ -639,14 +751,16 @@ __global__ void __launch_bounds__(PCG_THREADS, KS_PCG_MINB) k_block_pcg_fused(Pc
               const int32_t e0 = __ldg(a.sell_ptr + t * (TILE / KS_SELL_C));
               const int32_t b = __ldg(a.sell_ptr + row / KS_SELL_C), e = __ldg(a.sell_ptr + row / KS_SELL_C + 1);
               DV<VEC> w;
-              sell_row_s<NP>(vs, cs, (b - e0) + (int)(row % KS_SELL_C) * 4, (e - b) / (4 * KS_SELL_C), Z, sub, w);
               const int64_t off0 = row * NP + sub * VEC;
-              if (first) {   // p = z (init), q = A p
-                const DV<VEC> pv0 = DV<VEC>::ld(a.p + off0);
+              if (first) {   // p = z (init: bitwise), q = A p; p's row is the own gathered row of z
+                DV<VEC> pv0;
+                sell_row_s<NP, true>(vs, cs, (b - e0) + (int)(row % KS_SELL_C) * 4, (e - b) / (4 * KS_SELL_C), Z, sub,
+                                     w, row, &pv0);
 #pragma unroll
                 for (int v = 0; v < VEC; v++) acc[0][v] += pv0.v[v] * w.v[v];
                 w.st(a.q + off0);
               } else {
+              sell_row_s<NP>(vs, cs, (b - e0) + (int)(row % KS_SELL_C) * 4, (e - b) / (4 * KS_SELL_C), Z, sub, w);
               const int so = lr * NP + sub * VEC;
               double qv[VEC], pv[VEC], xv[VEC], zv[VEC];
 #pragma unroll
@@ -921,6 +1035,7 @@ ks_status launch_pcg(ks_ctx *ctx, PcgArgs &a) {
   a.ntiles = (int)((a.n + TILE - 1) / TILE);
   a.emax = 0;
   a.stage_bytes = 0;
+  a.stage_init = 0;
   // the fused two-phase kernel serves the BVPs (right-hand side (lambda + mu) M u); the Poisson mode of the
   // Hartree solve (given B, up to ~10^3 iterations to 1e-12) keeps the three-phase recurrences
   const char *fz = getenv("KS_PCG_FUSED");
@@ -945,6 +1060,8 @@ ks_status launch_pcg(ks_ctx *ctx, PcgArgs &a) {
       if (em > 0 && 2 * stage <= PCG_STAGE_SMEM_MAX) {
         a.emax = em;
         a.stage_bytes = (unsigned)stage;
+        const char *si = getenv("KS_PCG_STAGE_INIT");   // A/B: 0 = the init phase unstaged
+        a.stage_init = (size_t)em * 20 <= stage && !(si && si[0] == '0');
         return launch_pcg_t<NP, true, true>(ctx, a, 2 * stage);
       }
     }
