@@ -196,7 +196,8 @@ ks_status ks_true_residual(ks_ctx *ctx, int32_t N, const double *d_lambda, const
  *   n_H coarse free nodes; d_P_row_ptr [n_free+1] i32, d_P_col [p_nnz] i32 (< n_H), d_P_val [p_nnz] f64.
  * ks_coarse_plan groups the fine rows by parent set (in the workspace's call scratch) and returns the size of
  * the coarse region; ks_set_coarse builds, in the caller's d_coarse region: the copy of P, the item tables,
- * the pattern of H P, cached B_H = P^T M P and the projection workspace for N <= max_N. Both synchronise the
+ * the pattern of H P (window slots, also as an item-ordered sliced-ELL copy for the A_H pass), cached
+ * B_H = P^T M P and the projection workspace for N <= max_N. Both synchronise the
  * stream. Requires n_H >= 1, at most 4 entries per row. A new coarse space detaches the extension workspace.
  */
 ks_status ks_coarse_plan(ks_ctx *ctx, int64_t n_H, const int32_t *d_P_row_ptr, const int32_t *d_P_col,
@@ -227,7 +228,8 @@ ks_status ks_project_augmented(ks_ctx *ctx, int32_t N, const double *d_Ut, doubl
  * ks_pencil_eig: lowest k eigenpairs of F_A y = lambda F_B y (Nonlinear_Eig_Hh on W; "a
  * small-scale algebraic eigenvalue problem solved in serial"), on the context's stream.
  * It reduces to standard form by Cholesky, then runs a Chebyshev-filtered subspace iteration on k + 8 vectors
- * when k + 8 <= D / 2. The fallback is the dense cuSOLVER generalized symmetric
+ * when k + 8 <= D / 2 (KS_PENCIL_DEVICE=1 runs that iteration as one cooperative kernel with
+ * the Rayleigh-Ritz steps on the device). The fallback is the dense cuSOLVER generalized symmetric
  * eigensolver, which is always used when the environment variable KS_PENCIL_DENSE=1 is set.
  *   D = n_H + N >= 1, 1 <= k <= D; d_FA, d_FB [D][D] f64 symmetric (e.g. from ks_project_augmented), not
  *   modified; d_evals [k] f64 ascending; d_evecs [D][k] f64 row-major, column j = eigenvector j, normalised
