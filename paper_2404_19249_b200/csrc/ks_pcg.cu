@@ -1060,8 +1060,7 @@ ks_status launch_pcg(ks_ctx *ctx, PcgArgs &a) {
       if (em > 0 && 2 * stage <= PCG_STAGE_SMEM_MAX) {
         a.emax = em;
         a.stage_bytes = (unsigned)stage;
-        const char *si = getenv("KS_PCG_STAGE_INIT");   // A/B: 0 = the init phase unstaged
-        a.stage_init = (size_t)em * 20 <= stage && !(si && si[0] == '0');
+        a.stage_init = (size_t)em * 20 <= stage;   // the init phase's A, M values and columns fit a stage
         return launch_pcg_t<NP, true, true>(ctx, a, 2 * stage);
       }
     }
