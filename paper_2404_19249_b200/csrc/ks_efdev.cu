@@ -233,7 +233,7 @@ __device__ bool efd_chol(int m, int ld, const double *G, double *B1, double *B2,
 // a_pq^2 <= 1e-36 |a_pp a_qq|, the host routine's rule). Disjoint rotations commute, so every 2 x 2 block of A is
 // updated as J_a^T B J_b in one pass (columns first, as the host routine) and V <- V J. Sweeps until one without a
 // rotation (at most 60).
-__device__ void efd_jacobi(int m, int ld, double *A, double *V, double *rc, const unsigned char *pr, int *cnt) {
+__device__ int efd_jacobi(int m, int ld, double *A, double *V, double *rc, const unsigned char *pr, int *cnt) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = m + (m & 1), half = n / 2;
   for (int j = warp; j < m; j += EFD_NW)
@@ -290,8 +290,9 @@ __device__ void efd_jacobi(int m, int ld, double *A, double *V, double *rc, cons
     }
     const int rotated = *cnt;
     __syncthreads();
-    if (rotated == 0) break;
+    if (rotated == 0) return sweep + 1;
   }
+  return 60;
 }
 
 __global__ void __launch_bounds__(EFD_THREADS, 1) k_ef_iterate(EfdArgs a) {
@@ -406,8 +407,8 @@ __global__ void __launch_bounds__(EFD_THREADS, 1) k_ef_iterate(EfdArgs a) {
       for (int i = lane; i < m; i += 32) B1[j * ld + i] = i == j ? B4[j * ld + i] : 0.5 * (B4[j * ld + i] + B4[i * ld + j]);
     __syncthreads();
     stamp(4);
-    efd_jacobi(m, ld, B1, B3, rc, pr, flag + 1);   // eigenvalues on diag(B1), vectors in B3
-    stamp(5);
+    const int sweeps = efd_jacobi(m, ld, B1, B3, rc, pr, flag + 1);   // eigenvalues on diag(B1), vectors in B3
+    stamp(5 + 100 * sweeps);   // (the trace records the sweep count with the Jacobi stamp)
     // ascending order (ties by index)
     for (int j = tid; j < m; j += EFD_THREADS) {
       const double dj = B1[j * ld + j];

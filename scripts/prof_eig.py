@@ -48,9 +48,14 @@ if os.environ.get("KS_EF_TRACE") == "1":   # phase times of the device-resident 
     t = ctx.solve_trace().astype(np.int64).reshape(-1, 2)
     names = {1: "gemm", 2: "gram", 3: "chol", 4: "reduce", 5: "jacobi", 6: "update", 7: "resid", 8: "filter"}
     tot = {}
+    sweeps = []
     for (tag0, t0), (tag1, t1) in zip(t[:-1], t[1:]):
+        if tag1 % 100 == 5 and tag1 >= 100:
+            sweeps.append(int(tag1 // 100))
+            tag1 = 5
         if tag1 in names:
             tot[names[tag1]] = tot.get(names[tag1], 0.0) + (t1 - t0) / 1e3
+    print("jacobi sweeps per Rayleigh-Ritz step:", sweeps)
     rounds = int((t[:, 0] == 0).sum())
     print("device loop rounds", rounds, "phase totals us:", {k: round(v, 1) for k, v in tot.items()},
           "total", round(float((t[-1, 1] - t[0, 1]) / 1e3), 1))
