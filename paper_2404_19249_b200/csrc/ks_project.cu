@@ -7,8 +7,9 @@
 // coarse nodes with P_ic != 0) and cut into "items" of <= ITEM_ROWS rows. Every contribution of a row
 // lands in coarse rows c in S, so one warp can accumulate an item privately:
 //   K8a k_proj_y      Y_H = H U~ and Y_M = M U~ on the sliced-ELL copies (one pass, shared col stream)
-//   K8b k_proj_a      item partials sum_i P_ic (Op P)_{i,d}, d in the item's coarse window D (slot map
-//                     and a 4-wide table of P rows precomputed in ks_set_coarse), Op = H (A_H) or M (B_H)
+//   K8b k_proj_ai     item partials sum_i P_ic (H P)_{i,d}, d in the item's coarse window D, on an item-ordered
+//                     sliced-ELL copy of the pattern (columns, window slots) built by ks_set_coarse; k_proj_a (the
+//                     same sums with per-entry loads) serves Op = M (cached B_H) and Op = K (Hartree coarse operator)
 //   K8c k_proj_bg     item partials sum_i P_ic Y_H[i] / Y_M[i] (b_H, c_H) and, per warp, the Gram
 //                     partials beta, gamma = U~^T Y (symmetric: upper 4x4 tiles), rows in item order
 //   K9  k_proj_final  one block per coarse node c: fixed-order sums over the items containing c;
@@ -403,7 +404,7 @@ __global__ void __launch_bounds__(ITEM_ROWS, KS_PA_MINB) k_proj_a(const int32_t 
   }
 }
 
-// k_proj_a on the item-ordered sliced-ELL copy (KS_PROJ_FUSED=3): thread = row of the item as in k_proj_a, but each
+// k_proj_a on the item-ordered sliced-ELL copy (default; KS_PROJ_AI=0: k_proj_a): thread = row of the item as in k_proj_a, but each
 // 4-slot group of the row is one coalesced 16-byte column load, one 16-byte window-slot load (the 4 parents' words)
 // and one 32-byte H sector (natural layout), instead of per-entry loads scattered over the rows of the item. Same
 // entries in the same order into the same window rows and the same k-step chain: bitwise k_proj_a's partials.
