@@ -376,6 +376,7 @@ ks_status ks_assemble_impl(ks_ctx *ctx, const double *d_veff, double mu) {
   ctx->views_fresh = false;
   ctx->mu = mu;
   ctx->assembled = true;
+  ctx->ah_fresh = 0;   // H changed: the projection's A_H partials are stale
   return KS_OK;
 }
 

@@ -115,6 +115,8 @@ struct ks_ctx {
   int32_t *CT_val = nullptr;     // [4 n_items] entries 4 item + q
   double *B_H = nullptr;         // [n_H n_H] cached P^T M P
   double *AH_part = nullptr;     // [4 d_total] per-item partials of P^T Op P
+  int ah_fresh = 0;              // AH_part holds the A_H partials of the current H (1: k_proj_ai, 2: k_proj_a); reset by
+                                 // an assembly, a coarse space and every other use of AH_part
   double *bH_part = nullptr, *cH_part = nullptr;  // [4 n_items NP]
   double *Y_H = nullptr, *Y_M = nullptr, *proj_u = nullptr;  // [n_free][NP] (Y_H, Y_M in item order)
   double *proj_up = nullptr;     // [n_free][NP] U~ in item order

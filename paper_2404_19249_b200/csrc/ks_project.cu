@@ -1218,6 +1218,7 @@ int64_t proj_gram_cap(int sm_count, int np_max) {
 // dense P^T Op P [n_H][n_H] for an operator in the sliced-ELL layout (the A-part of the item pass)
 ks_status ks_coarse_galerkin(ks_ctx *ctx, const double *op_sell_vals, double *out) {
   if (ctx->n_H <= 0) return ks_fail(ctx, KS_E_STATE, "no coarse space");
+  ctx->ah_fresh = 0;   // AH_part is reused for this operator
   KS_TRY(launch_proj_a(ctx, op_sell_vals));
   return launch_final<false>(ctx, 0, 16, out, nullptr, ctx->n_H, 0);
 }
@@ -1237,6 +1238,7 @@ void ks_free_coarse(ks_ctx *ctx) {
   ctx->inat = nullptr;
   ctx->islot = nullptr;
   ctx->n_islices = ctx->isell_total = 0;
+  ctx->ah_fresh = 0;
 }
 
 static int proj_np(int max_N) {
@@ -1433,6 +1435,7 @@ ks_status ks_set_coarse_impl(ks_ctx *ctx, int64_t n_H, const int32_t *Pptr, cons
 
   // ---- cached B_H = P^T M P (A-part of the item pass with M) ----
   ctx->n_H = n_H;
+  ctx->ah_fresh = 0;
   KS_TRY(launch_proj_a(ctx, ctx->sell_M));
   KS_TRY(launch_final<false>(ctx, 0, 16, ctx->B_H, nullptr, n_H, 0));
   KS_CUDA(ctx, cudaStreamSynchronize(s));   // the call scratch is released at return
@@ -1462,8 +1465,14 @@ ks_status ks_project_impl(ks_ctx *ctx, int N, const double *Ut, double *FA, doub
     default: return ks_fail(ctx, KS_E_ARG, "N = %d unsupported", N);
   }
   // K8b: A_H item partials (unshifted H, reading Q1)
-  if (proj_ai_enabled() && ctx->isell_col) KS_TRY(launch_proj_ai(ctx, ctx->sell_H));
-  else KS_TRY(launch_proj_a(ctx, ctx->sell_H));
+  // (A_H depends on H only: repeated projections of one assembly, e.g. the outer iterations of
+  // ks_augmented_solve at a fixed potential, reuse the item partials)
+  const int ah_mode = proj_ai_enabled() && ctx->isell_col ? 1 : 2;
+  if (ctx->ah_fresh != ah_mode) {
+    if (ah_mode == 1) KS_TRY(launch_proj_ai(ctx, ctx->sell_H));
+    else KS_TRY(launch_proj_a(ctx, ctx->sell_H));
+    ctx->ah_fresh = ah_mode;
+  }
   // K9: A_H, b_H, c_H
   KS_TRY(launch_final<true>(ctx, N, np, FA, FB, D, D));
   k_copy_block<<<ks_blocks(nH * nH, 256), 256, 0, s>>>(ctx->B_H, nH, FB, D);

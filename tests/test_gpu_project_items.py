@@ -82,3 +82,31 @@ def test_coarse_space_changes(monkeypatch):
     om.assemble_veff(V2, 2.0 * p2.mu)
     ctx.assemble_veff(dt(V2), 2.0 * p2.mu)
     check_against_oracle(ctx, om, p2, Ut, what="after a new assembly")
+
+
+def test_repeated_projections_reuse_A_H_until_H_or_its_storage_changes(monkeypatch):
+    """A_H = P^T H P depends on H only: projections of one assembly reuse its item partials (the outer iterations of
+    ks_augmented_solve), bitwise equal to a fresh computation; a two-level Hartree solve (which builds P^T K P in
+    the same partial storage) and a new assembly invalidate them."""
+    monkeypatch.delenv("KS_PROJ_AI", raising=False)
+    p = small(N=8, nc=3)
+    om = oracle.Mesh.from_problem(p)
+    om.assemble_veff(p.V, p.mu)
+    ctx = _ks().Context(p.xyz, p.tets, p.dirichlet)
+    ctx.set_coarse(p.n_H, dt(p.P_rowptr), dt(p.P_col), dt(p.P_val))
+    ctx.assemble_veff(dt(p.V), p.mu)
+    rng = np.random.default_rng(11)
+    U1 = p.U + 0.1 * rng.standard_normal(p.U.shape)
+    U2 = p.U + 0.1 * rng.standard_normal(p.U.shape)
+    F1 = check_against_oracle(ctx, om, p, U1, what="first")
+    F2 = check_against_oracle(ctx, om, p, U2, what="second, reused A_H")
+    nH = p.n_H
+    assert np.array_equal(F1[0][:nH, :nH], F2[0][:nH, :nH])
+    rho = ctx.density(dt(p.U), 2.0)
+    ctx.hartree(rho, tol=1e-8)   # P^T K P through the same item partials
+    F3 = check_against_oracle(ctx, om, p, U1, what="after a two-level Hartree solve")
+    assert np.array_equal(F3[0], F1[0]) and np.array_equal(F3[1], F1[1])
+    V2 = p.V + 0.2 * np.cos(np.arange(p.V.size))
+    om.assemble_veff(V2, p.mu)
+    ctx.assemble_veff(dt(V2), p.mu)
+    check_against_oracle(ctx, om, p, U1, what="after a new assembly")
