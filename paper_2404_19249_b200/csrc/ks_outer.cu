@@ -297,6 +297,20 @@ __global__ void k_cheb(const double *__restrict__ CY, const double *__restrict__
   Yn[x] = alpha * (CY[x] - c * Y[x]) + (Xp ? beta * Xp[x] : 0.0);
 }
 
+// A <- A - c I with the diagonal saved (save[i] = A_ii), and its exact restoration: the Chebyshev steps take
+// alpha (A - c I) Y + beta Y_prev as one GEMM (beta accumulates into Y_prev's buffer)
+__global__ void k_shift_diag(double *__restrict__ A, int64_t D, double c, double *__restrict__ save) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= D) return;
+  const double a = A[i * D + i];
+  save[i] = a;
+  A[i * D + i] = a - c;
+}
+__global__ void k_restore_diag(double *__restrict__ A, int64_t D, const double *__restrict__ save) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < D) A[i * D + i] = save[i];
+}
+
 // number of entries of the leading n x n block of F (column-major, ld D) that differ from B (n x n)
 __global__ void k_block_mismatch(const double *__restrict__ F, int64_t D, const double *__restrict__ B, int64_t n,
                                  int *__restrict__ count) {
@@ -443,6 +457,9 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
   if (const char *e = getenv("KS_PENCIL_EF_MAXIT")) maxit = atoi(e);
   // KS_PENCIL_DEVICE=1: the whole iteration as one cooperative kernel (ks_efdev.cu, measured slower)
   const char *devrr = getenv("KS_PENCIL_DEVICE");
+  // KS_EF_FUSED=0: the Chebyshev step as a GEMM plus an element-wise kernel (the round-1 form; A/B only)
+  const char *fe = getenv("KS_EF_FUSED");
+  const bool fused_cheb = !(fe && fe[0] == '0');
   if (devrr && devrr[0] == '1' && ctx->ef_dev) {
     int stv = 0, rounds = 0;
     bool ran = false;
@@ -592,17 +609,33 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
     double *Xp = X, *Y = T1, *Yn = T2;
     k_cheb<<<ks_blocks(len, 256), 256, 0, st>>>(CX, X, nullptr, len, sigma / e, c, 0.0, Y);
     KS_LAUNCHED(ctx);
-    for (int d = 2; d <= EF_DEG; d++) {
-      const double s2 = 1.0 / (s1 - sigma);
-      KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, (int)D, &one, A, (int)D, Y, (int)D, &zero, CX,
-                               (int)D));
-      k_cheb<<<ks_blocks(len, 256), 256, 0, st>>>(CX, Y, Xp, len, 2.0 * s2 / e, c, -sigma * s2, Yn);
+    if (fused_cheb) {
+      // Y_{d} = (2 s2 / e) (C - c I) Y_{d-1} - sigma s2 Y_{d-2}: one GEMM per degree, accumulated into Y_{d-2}'s
+      // buffer; C's diagonal is shifted for the filter and restored bitwise after it (T2 holds the saved diagonal)
+      k_shift_diag<<<ks_blocks(D, 256), 256, 0, st>>>(A, D, c, T2);
       KS_LAUNCHED(ctx);
-      double *t = Xp;
-      Xp = Y;
-      Y = Yn;
-      Yn = t;
-      sigma = s2;
+      for (int d = 2; d <= EF_DEG; d++) {
+        const double s2 = 1.0 / (s1 - sigma), al = 2.0 * s2 / e, be = -sigma * s2;
+        KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, (int)D, &al, A, (int)D, Y, (int)D, &be, Xp,
+                                 (int)D));
+        std::swap(Xp, Y);
+        sigma = s2;
+      }
+      k_restore_diag<<<ks_blocks(D, 256), 256, 0, st>>>(A, D, T2);
+      KS_LAUNCHED(ctx);
+    } else {
+      for (int d = 2; d <= EF_DEG; d++) {
+        const double s2 = 1.0 / (s1 - sigma);
+        KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, (int)D, &one, A, (int)D, Y, (int)D, &zero, CX,
+                                 (int)D));
+        k_cheb<<<ks_blocks(len, 256), 256, 0, st>>>(CX, Y, Xp, len, 2.0 * s2 / e, c, -sigma * s2, Yn);
+        KS_LAUNCHED(ctx);
+        double *t = Xp;
+        Xp = Y;
+        Y = Yn;
+        Yn = t;
+        sigma = s2;
+      }
     }
     if (Y != X) KS_CUDA(ctx, cudaMemcpyAsync(X, Y, sizeof(double) * len, cudaMemcpyDeviceToDevice, st));
   }
