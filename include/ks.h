@@ -239,6 +239,15 @@ ks_status ks_project_augmented(ks_ctx *ctx, int32_t N, const double *d_Ut, doubl
 ks_status ks_pencil_eig(ks_ctx *ctx, int64_t D, int32_t k, const double *d_FA, const double *d_FB,
                         double *d_evals, double *d_evecs);
 
+/* The host routine behind the Rayleigh-Ritz steps of ks_pencil_eig's filtered iteration: all
+ * eigenpairs of a small dense symmetric matrix. Host only: no context, no device work, callable without a GPU.
+ *   n >= 1; h_A [n][n] f64 symmetric (host, not modified); h_w [n] f64 (host, output) ascending eigenvalues;
+ *   h_V [n][n] f64 (host, output): h_V[j*n + i] = component i of eigenvector j, orthonormal.
+ *   method 0: Householder tridiagonalisation + implicit QL (the default of the filtered iteration);
+ *   method 1: cyclic Jacobi (its fallback, KS_EF_HOSTEIG=jacobi).
+ *   Errors: KS_E_ARG (null pointer, n < 1, unknown method), KS_E_NOT_CONVERGED (QL iteration count ran out). */
+ks_status ks_host_sym_eig(int32_t n, const double *h_A, double *h_w, double *h_V, int32_t method);
+
 /*
  * ks_lift: the new orbitals in W (Algorithm 3: psi in S_H + span{psi~}):
  *   U_new[i][j] = sum_c P_ic Y[c][j] + sum_m U~[i][m] Y[n_H + m][j]

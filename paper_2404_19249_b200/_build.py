@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "nvcc")
 CUDA_LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.realpath(
     __import__("shutil").which(NVCC) or "/usr/local/cuda/bin/nvcc"))), "lib64")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v",
          "-I" + os.path.join(ROOT, "include")]
 
 

@@ -217,7 +217,7 @@ inline size_t ks_scratch_bound(const KsMeshSizes &z, int max_N, int sm_count, si
 #define KS_EXT_NSLOT2L 8     // block partial slots of the two-level Hartree kernel (ks_pcg2l.cu NSLOT)
 #define KS_EXT_AMAX 8        // Anderson history bound (ks_scf.cu AMAX)
 #define KS_EXT_DEPTH_MAX 7   // largest Anderson depth ks_scf_solve accepts
-#define KS_EXT_EF_GUARD 8    // guard vectors of the filtered pencil eigensolver (ks_outer.cu EF_GUARD)
+#define KS_EXT_EF_GUARD 24   // most guard vectors of the filtered pencil eigensolver (ks_outer.cu EF_GUARD_MAX)
 #define KS_EXT_BLAS_WS (32u << 20)   // cuBLAS workspace handed over with cublasSetWorkspace
 struct KsExtSizes {
   unsigned features = 0;

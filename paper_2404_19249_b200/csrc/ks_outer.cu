@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
 #include <vector>
 
 #include "ks_internal.cuh"
@@ -225,11 +226,12 @@ ks_status ks_cusolver_lwork(ks_ctx *ctx, int64_t D, int64_t nH, int64_t *lwork) 
 //           residual ||C x_j - lambda_j x_j|| <= tol * (Gershgorin bound of C); otherwise a degree-DEG
 //           Chebyshev filter damping [lambda_m, bound] (3-term recurrence, one GEMM per degree).
 //   end     y_j = L^-T x_j, F_B-orthonormal by construction.
-// The small dense problems (m <= k + 8 <= 72) are solved on the host by cyclic Jacobi. It falls back to the
-// dense cuSOLVER path if it does not converge.
+// The small dense problems (m <= k + 8 <= 72) are solved on the host: Householder tridiagonalisation + implicit
+// QL (cyclic Jacobi as its fallback and A/B, KS_EF_HOSTEIG=jacobi). It falls back to the dense cuSOLVER path if
+// it does not converge.
 namespace {
 
-constexpr int EF_GUARD = 8, EF_DEG = 20, EF_MAXIT = 40;
+constexpr int EF_GUARD = 8, EF_GUARD_MAX = KS_EXT_EF_GUARD, EF_DEG = 20, EF_DEG_GROW = 0, EF_DEG_MAX = 20, EF_MAXIT = 40;
 
 // cyclic Jacobi for a symmetric n x n (column-major, overwritten): ascending eigenvalues w, eigenvectors V
 void host_jacobi_eig(std::vector<double> &A, int n, std::vector<double> &w, std::vector<double> &V) {
@@ -275,6 +277,118 @@ void host_jacobi_eig(std::vector<double> &A, int n, std::vector<double> &w, std:
     for (int r = 0; r < n; r++) V2[(size_t)j * n + r] = V[(size_t)idx[j] * n + r];
   }
   V.swap(V2);
+}
+
+// symmetric n x n (column-major, overwritten): ascending eigenvalues w, eigenvectors V (column j = V[j*n..]).
+// Householder reduction to tridiagonal form, then the implicit QL iteration with Wilkinson shifts on (d, e),
+// the rotations accumulated into the Householder basis. false if a QL sweep count runs out.
+bool host_tridiag_ql_eig(std::vector<double> &A, int n, std::vector<double> &w, std::vector<double> &V) {
+  std::vector<double> d(n), e(n, 0.0), v(n), p(n), beta(n, 0.0);
+  // A <- H_k ... A ... H_k, the Householder vectors kept below the subdiagonal (v_0 implicit in beta/first entry)
+  std::vector<double> Hv((size_t)n * n, 0.0);
+  for (int k = 0; k + 2 < n; k++) {
+    double *col = &A[(size_t)k * n];
+    double nrm2 = 0.0;
+    for (int i = k + 1; i < n; i++) nrm2 += col[i] * col[i];
+    const double nrm = std::sqrt(nrm2);
+    d[k] = col[k];
+    if (nrm == 0.0) { e[k] = 0.0; continue; }
+    const double alpha = col[k + 1] > 0.0 ? -nrm : nrm;
+    for (int i = k + 1; i < n; i++) v[i] = col[i];
+    v[k + 1] -= alpha;
+    double vv = 0.0;
+    for (int i = k + 1; i < n; i++) vv += v[i] * v[i];
+    const double b = 2.0 / vv;
+    // p = b A22 v, w = p - (b/2)(v.p) v, A22 -= v w^T + w v^T
+    for (int i = k + 1; i < n; i++) p[i] = 0.0;
+    for (int j = k + 1; j < n; j++) {
+      const double *aj = &A[(size_t)j * n];
+      const double vj = v[j];
+      for (int i = k + 1; i < n; i++) p[i] += aj[i] * vj;
+    }
+    double vp = 0.0;
+    for (int i = k + 1; i < n; i++) { p[i] *= b; vp += v[i] * p[i]; }
+    const double K = 0.5 * b * vp;
+    for (int i = k + 1; i < n; i++) p[i] -= K * v[i];
+    for (int j = k + 1; j < n; j++) {
+      double *aj = &A[(size_t)j * n];
+      const double vj = v[j], pj = p[j];
+      for (int i = k + 1; i < n; i++) aj[i] -= v[i] * pj + p[i] * vj;
+    }
+    e[k] = alpha;
+    beta[k] = b;
+    for (int i = k + 1; i < n; i++) Hv[(size_t)k * n + i] = v[i];
+  }
+  if (n >= 2) {
+    d[n - 2] = A[(size_t)(n - 2) * n + (n - 2)];
+    e[n - 2] = A[(size_t)(n - 2) * n + (n - 1)];
+  }
+  d[n - 1] = A[(size_t)(n - 1) * n + (n - 1)];
+  // Z = H_0 H_1 ... H_{n-3}, stored by rows of Z^T: Zt[j*n + r] = Z[r][j] (column j contiguous)
+  std::vector<double> Z((size_t)n * n, 0.0);
+  for (int i = 0; i < n; i++) Z[(size_t)i * n + i] = 1.0;
+  for (int k = n - 3; k >= 0; k--) {
+    if (beta[k] == 0.0) continue;
+    const double *hv = &Hv[(size_t)k * n];
+    for (int j = k + 1; j < n; j++) {   // column j of Z: z -= beta v (v.z)
+      double *zj = &Z[(size_t)j * n];
+      double s = 0.0;
+      for (int i = k + 1; i < n; i++) s += hv[i] * zj[i];
+      s *= beta[k];
+      for (int i = k + 1; i < n; i++) zj[i] -= s * hv[i];
+    }
+  }
+  // implicit QL on (d, e): e[i] couples i and i+1
+  for (int l = 0; l < n; l++) {
+    for (int iter = 0;; iter++) {
+      int m = l;
+      for (; m + 1 < n; m++) {
+        const double dd = std::fabs(d[m]) + std::fabs(d[m + 1]);
+        if (std::fabs(e[m]) <= 2.3e-16 * dd) break;
+      }
+      if (m == l) break;
+      if (iter == 80) return false;
+      double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+      double r = std::sqrt(g * g + 1.0);
+      g = d[m] - d[l] + e[l] / (g + (g >= 0.0 ? r : -r));
+      double s = 1.0, c = 1.0, pp = 0.0;
+      int i = m - 1;
+      for (; i >= l; i--) {
+        double f = s * e[i];
+        const double bb = c * e[i];
+        r = std::sqrt(f * f + g * g);
+        e[i + 1] = r;
+        if (r == 0.0) { d[i + 1] -= pp; e[m] = 0.0; break; }
+        s = f / r;
+        c = g / r;
+        g = d[i + 1] - pp;
+        r = (d[i] - g) * s + 2.0 * c * bb;
+        pp = s * r;
+        d[i + 1] = g + pp;
+        g = c * r - bb;
+        double *zi = &Z[(size_t)i * n], *zi1 = &Z[(size_t)(i + 1) * n];
+        for (int k = 0; k < n; k++) {
+          f = zi1[k];
+          zi1[k] = s * zi[k] + c * f;
+          zi[k] = c * zi[k] - s * f;
+        }
+      }
+      if (r == 0.0 && i >= l) continue;
+      d[l] -= pp;
+      e[l] = g;
+      e[m] = 0.0;
+    }
+  }
+  std::vector<int> idx(n);
+  for (int i = 0; i < n; i++) idx[i] = i;
+  std::sort(idx.begin(), idx.end(), [&](int a, int b) { return d[a] < d[b]; });
+  w.resize(n);
+  V.resize((size_t)n * n);
+  for (int j = 0; j < n; j++) {
+    w[j] = d[idx[j]];
+    for (int r2 = 0; r2 < n; r2++) V[(size_t)j * n + r2] = Z[(size_t)idx[j] * n + r2];
+  }
+  return true;
 }
 
 // Gershgorin bound max_j sum_i |C_ij| (symmetric, column-major): one warp per column, the maximum through
@@ -377,7 +491,27 @@ __global__ void k_resid(const double *__restrict__ CX, const double *__restrict_
   if (threadIdx.x == 0) out[j] = s;
 }
 
+// guard vectors of the filtered iteration: EF_GUARD, or KS_EF_GUARD (A/B) up to the extension region's capacity
+int ef_guard() {
+  int g = EF_GUARD;
+  if (const char *e = getenv("KS_EF_GUARD")) g = std::min(EF_GUARD_MAX, std::max(1, atoi(e)));
+  return g;
+}
+
 }  // namespace
+
+extern "C" ks_status ks_host_sym_eig(int32_t n, const double *h_A, double *h_w, double *h_V, int32_t method) {
+  if (n < 1 || !h_A || !h_w || !h_V || method < 0 || method > 1) return KS_E_ARG;
+  std::vector<double> A(h_A, h_A + (size_t)n * n), w, V;
+  if (method == 0) {
+    if (!host_tridiag_ql_eig(A, n, w, V)) return KS_E_NOT_CONVERGED;
+  } else {
+    host_jacobi_eig(A, n, w, V);
+  }
+  std::copy(w.begin(), w.end(), h_w);
+  std::copy(V.begin(), V.end(), h_V);
+  return KS_OK;
+}
 
 static ks_status ensure_blas(ks_ctx *ctx) {
   if (!ctx->cublas) {
@@ -406,7 +540,7 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
   KS_TRY(ensure_blas(ctx));
   cublasHandle_t hb = (cublasHandle_t)ctx->cublas;
   cudaStream_t st = ctx->stream;
-  const int m = k + EF_GUARD;
+  const int m = k + ef_guard();
   const double one = 1.0, zero = 0.0;
   double *A = ctx->eig_A, *L = ctx->eig_B;
   // C = L^-1 A L^-T (in A): two GEMMs with the explicit inverse when it is given (the coarse block's factor is
@@ -515,7 +649,15 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
     }
     return true;
   };
-  std::vector<double> G2((size_t)m * m), dsc, Rinv, Hs((size_t)m * m);
+  std::vector<double> G2((size_t)m * m), dsc, Rinv, Hs((size_t)m * m), Hq;
+  double host_us = 0.0;   // host share of the Rayleigh-Ritz steps (KS_EF_VERBOSE)
+  const char *he = getenv("KS_EF_HOSTEIG");
+  const bool jacobi_rr = he && he[0] == 'j';
+  // filter degree of round it: min(deg_max, deg0 + grow * it) (KS_EF_DEG / KS_EF_DEG_GROW / KS_EF_DEG_MAX; A/B)
+  int deg0 = EF_DEG, deg_grow = EF_DEG_GROW, deg_max = EF_DEG_MAX;
+  if (const char *e = getenv("KS_EF_DEG")) deg0 = std::max(2, atoi(e));
+  if (const char *e = getenv("KS_EF_DEG_GROW")) deg_grow = std::max(0, atoi(e));
+  if (const char *e = getenv("KS_EF_DEG_MAX")) deg_max = std::max(2, atoi(e));
   for (int it = 0; it < maxit; it++) {
     ctx->ef_rounds = it + 1;
     // Rayleigh-Ritz on span(X) with the orthonormalisation folded in: T2 = C X, G = X^T X and H = X^T C X in
@@ -529,6 +671,7 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
     KS_CUDA(ctx, cudaMemcpyAsync(G.data(), sm, sizeof(double) * m * m, cudaMemcpyDeviceToHost, st));
     KS_CUDA(ctx, cudaMemcpyAsync(G2.data(), sm + (int64_t)m * m, sizeof(double) * m * m, cudaMemcpyDeviceToHost, st));
     KS_CUDA(ctx, cudaStreamSynchronize(st));
+    const auto h0 = std::chrono::steady_clock::now();
     if (!host_chol(G, dsc, Rinv)) {   // the block lost rank: dense path
       if (getenv("KS_EF_VERBOSE")) fprintf(stderr, "ks_pencil_eig: round %d: Gram pivot collapsed\n", it + 1);
       return KS_OK;
@@ -552,7 +695,14 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
       for (int j = 0; j < m; j++)
         for (int i = 0; i < j; i++) Hs[(size_t)j * m + i] = Hs[(size_t)i * m + j] = 0.5 * (Hs[(size_t)j * m + i] + Hs[(size_t)i * m + j]);
     }
-    host_jacobi_eig(Hs, m, w, V);
+    // the small symmetric eigenproblem: Householder + implicit QL (KS_EF_HOSTEIG=jacobi: cyclic Jacobi, which is
+    // also the fallback should a QL iteration count run out)
+    if (jacobi_rr) {
+      host_jacobi_eig(Hs, m, w, V);
+    } else {
+      Hq = Hs;
+      if (!host_tridiag_ql_eig(Hq, m, w, V)) host_jacobi_eig(Hs, m, w, V);
+    }
     lam = w;
     Tm.assign((size_t)m * m, 0.0);   // D^-1 R^-1 W
     for (int j = 0; j < m; j++)
@@ -561,6 +711,7 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
         for (int l = i; l < m; l++) v += Rinv[(size_t)l * m + i] * V[(size_t)j * m + l];
         Tm[(size_t)j * m + i] = v / dsc[i];
       }
+    host_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
     KS_CUDA(ctx, cudaMemcpyAsync(sm, Tm.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice, st));
     KS_CUDA(ctx, cudaMemcpyAsync(sm + (int64_t)m * m, lam.data(), sizeof(double) * m, cudaMemcpyHostToDevice, st));
     KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, m, &one, X, (int)D, sm, m, &zero, T1, (int)D));
@@ -573,7 +724,9 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
     KS_CUDA(ctx, cudaStreamSynchronize(st));
     double rmax = 0.0;
     for (int j = 0; j < k; j++) rmax = std::fmax(rmax, std::sqrt(res[j]));
-    if (getenv("KS_EF_VERBOSE")) fprintf(stderr, "ks_pencil_eig: round %d rmax %.3e (tol %.3e)\n", it + 1, rmax, tol * bound);
+    if (getenv("KS_EF_VERBOSE"))
+      fprintf(stderr, "ks_pencil_eig: round %d rmax %.3e (tol %.3e), host Rayleigh-Ritz so far %.0f us\n", it + 1, rmax,
+              tol * bound, host_us);
     if (!std::isfinite(rmax)) return KS_OK;
     if (rmax <= tol * bound) {
       // one more Cholesky-QR pass (X V is orthonormal only up to cond(X)^2 eps), then y = L^-T x, evals
@@ -606,6 +759,7 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
     double sigma = e / (lam[0] - c);
     const double s1 = 2.0 / sigma;
     const int64_t len = D * m;
+    const int deg = std::max(2, std::min(std::max(deg_max, deg0), deg0 + deg_grow * it));
     double *Xp = X, *Y = T1, *Yn = T2;
     k_cheb<<<ks_blocks(len, 256), 256, 0, st>>>(CX, X, nullptr, len, sigma / e, c, 0.0, Y);
     KS_LAUNCHED(ctx);
@@ -614,7 +768,7 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
       // buffer; C's diagonal is shifted for the filter and restored bitwise after it (T2 holds the saved diagonal)
       k_shift_diag<<<ks_blocks(D, 256), 256, 0, st>>>(A, D, c, T2);
       KS_LAUNCHED(ctx);
-      for (int d = 2; d <= EF_DEG; d++) {
+      for (int d = 2; d <= deg; d++) {
         const double s2 = 1.0 / (s1 - sigma), al = 2.0 * s2 / e, be = -sigma * s2;
         KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, (int)D, &al, A, (int)D, Y, (int)D, &be, Xp,
                                  (int)D));
@@ -624,7 +778,7 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
       k_restore_diag<<<ks_blocks(D, 256), 256, 0, st>>>(A, D, T2);
       KS_LAUNCHED(ctx);
     } else {
-      for (int d = 2; d <= EF_DEG; d++) {
+      for (int d = 2; d <= deg; d++) {
         const double s2 = 1.0 / (s1 - sigma);
         KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, (int)D, &one, A, (int)D, Y, (int)D, &zero, CX,
                                  (int)D));
@@ -734,7 +888,7 @@ ks_status ks_pencil_eig_impl(ks_ctx *ctx, int64_t D, int k, const double *FA, co
                    (long long)ctx->ext_D);
   // symmetric matrices: row-major == column-major
   const char *dense = getenv("KS_PENCIL_DENSE");
-  const bool filtered = !(dense && dense[0] == '1') && k <= ctx->max_N && k + EF_GUARD <= D / 2;
+  const bool filtered = !(dense && dense[0] == '1') && k <= ctx->max_N && k + ef_guard() <= D / 2;
   const bool have_L = filtered && same_B && ctx->ef_L_D == D;
   KS_CUDA(ctx, cudaMemcpyAsync(ctx->eig_A, FA, sizeof(double) * D * D, cudaMemcpyDeviceToDevice, ctx->stream));
   if (!have_L)

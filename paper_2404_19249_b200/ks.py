@@ -29,7 +29,7 @@ OPS = {"K": 0, "M": 1, "MV": 2, "H": 3, "A": 4}
 EXPORTS = ["ks_abi_version", "ks_build_info", "ks_plan", "ks_create", "ks_destroy", "ks_set_stream", "ks_pattern",
            "ks_values", "ks_assemble_veff", "ks_spmm", "ks_block_solve", "ks_last_iterations", "ks_solve_trace",
            "ks_true_residual", "ks_coarse_plan", "ks_set_coarse", "ks_ext_plan", "ks_attach_ext",
-           "ks_project_augmented", "ks_pencil_eig", "ks_lift", "ks_augmented_solve", "ks_interpolation_plan",
+           "ks_project_augmented", "ks_pencil_eig", "ks_host_sym_eig", "ks_lift", "ks_augmented_solve", "ks_interpolation_plan",
            "ks_interpolation", "ks_density", "ks_vxc", "ks_hartree", "ks_scf_solve", "ks_step_submit",
            "ks_step_wait", "ks_memory_bytes", "ks_memory_usage", "ks_launch_count", "ks_sync", "ks_last_error",
            "ks_slab_init", "ks_slab_spmm", "ks_slab_update", "ks_slab_finish"]
@@ -77,6 +77,7 @@ def load_library(path: str = LIB_PATH):
         "ks_attach_ext": (st, [vp, C.c_uint32, i64, vp, C.c_size_t]),
         "ks_project_augmented": (st, [vp, i32, vp, vp, vp]),
         "ks_pencil_eig": (st, [vp, i64, i32, vp, vp, vp, vp]),
+        "ks_host_sym_eig": (st, [i32, vp, vp, vp, i32]),
         "ks_lift": (st, [vp, i32, vp, i32, vp, vp]),
         "ks_augmented_solve": (st, [vp, i32, vp, vp, dbl, i32, dbl, i32, C.POINTER(i32), vp]),
         "ks_interpolation_plan": (st, [vp, i64, vp, i64, C.POINTER(C.c_size_t)]),
@@ -533,6 +534,22 @@ def _raw_tensor(dptr: int, count: int, dtype, device):
     obj.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (dptr, False), "version": 3,
                                    "strides": None}
     return torch.as_tensor(obj, device=device)
+
+
+def host_sym_eig(A, method: int = 0):
+    """ks_host_sym_eig: all eigenpairs of a small symmetric matrix with the host routine behind ks_pencil_eig's
+    Rayleigh-Ritz steps (method 0: Householder + implicit QL, 1: cyclic Jacobi). A: numpy float64 [n][n].
+    Returns (w [n] ascending, V [n][n] with V[:, j] the eigenvector j). Runs without a GPU."""
+    import numpy as np
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    if A.ndim != 2 or A.shape[0] != A.shape[1] or A.shape[0] < 1:
+        raise KSError(KS_E_ARG, "host_sym_eig: A must be a square matrix")
+    n = A.shape[0]
+    w, Vt = np.empty(n), np.empty((n, n))
+    st = load_library().ks_host_sym_eig(n, A.ctypes.data, w.ctypes.data, Vt.ctypes.data, int(method))
+    if st != KS_OK:
+        raise KSError(st, "ks_host_sym_eig failed")
+    return w, Vt.T.copy()
 
 
 def solve_step_host(ctx: Context, V_host, mu, lam_host, U_host, out=None, tol=1e-10, max_iter=2000, wait=True):

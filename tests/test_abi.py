@@ -89,3 +89,47 @@ def c_consumer_build(out):
 def test_c_consumer_compiles_and_links(lib, tmp_path):
     r = c_consumer_build(str(tmp_path / "c_consumer"))
     assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.parametrize("method", [0, 1])
+def test_host_sym_eig_matches_lapack(method):
+    """ks_host_sym_eig (the host routine of the filtered pencil eigensolver's Rayleigh-Ritz steps; host only, so it
+    runs without a GPU): eigenvalues against numpy's LAPACK eigh, residual and orthonormality, for random,
+    nearly diagonal (a converged Rayleigh-Ritz step), exactly diagonal, repeated-eigenvalue, decoupled and
+    tiny matrices, by Householder + QL (0) and by cyclic Jacobi (1)."""
+    import numpy as np
+    import paper_2404_19249_b200 as ks
+    rng = np.random.default_rng(7)
+    cases = []
+    for n in (1, 2, 3, 5, 24, 40, 72):
+        R = rng.standard_normal((n, n))
+        cases.append(0.5 * (R + R.T) + np.diag(np.arange(n, dtype=float)))
+        cases.append(np.diag(np.linspace(-18.0, 30.0, n)) + 1e-7 * 0.5 * (R + R.T))
+        cases.append(np.diag(np.linspace(-3.0, 4.0, n)[::-1]))
+        Q, _ = np.linalg.qr(R)
+        cases.append(Q @ np.diag(np.repeat(np.arange((n + 2) // 3, dtype=float), 3)[:n]) @ Q.T)
+        B = np.zeros((n, n))                      # two decoupled blocks: a zero sub-diagonal entry mid-matrix
+        h = n // 2
+        B[:h, :h] = cases[-4][:h, :h]
+        B[h:, h:] = cases[-4][h:, h:]
+        cases.append(B)
+    cases.append(np.zeros((6, 6)))
+    for A in cases:
+        A = 0.5 * (A + A.T)
+        n = A.shape[0]
+        w, V = ks.host_sym_eig(A, method)
+        ref = np.linalg.eigvalsh(A)
+        scale = max(np.abs(ref).max(), 1e-300)
+        assert np.all(np.diff(w) >= 0)
+        assert np.abs(w - ref).max() <= 1e-13 * n * scale
+        assert np.abs(A @ V - V * w).max() <= 1e-13 * n * scale
+        assert np.abs(V.T @ V - np.eye(n)).max() <= 1e-13 * n
+
+
+def test_host_sym_eig_rejects_bad_arguments():
+    import numpy as np
+    import paper_2404_19249_b200 as ks
+    with pytest.raises(ks.KSError):
+        ks.host_sym_eig(np.zeros((2, 3)))
+    with pytest.raises(ks.KSError):
+        ks.host_sym_eig(np.eye(3), method=2)
