@@ -425,6 +425,80 @@ __global__ void k_restore_diag(double *__restrict__ A, int64_t D, const double *
   if (i < D) A[i * D + i] = save[i];
 }
 
+// Out = alpha (A - c I) Y + beta Out for a symmetric A [D][D] and column-major D x m blocks (ld D), m small: the
+// product of the filtered iteration (one launch per Chebyshev step instead of a cuBLAS GEMM and its split-K
+// reduction). One CTA per RT rows of the output. A work item is (4 columns, one of KS slices of
+// the k range); a warp takes items w, w + 12, ... with its lanes on consecutive k, so the row of A (= its column,
+// A is symmetric) and the columns of Y are read coalesced, holds the RT x 4 partial products in registers, and
+// leaves their butterfly sums in shared memory. The k slices are then added in ascending order: deterministic.
+constexpr int SG_WARPS = 12, SG_CT = 4, SG_RT = 8;
+template <int RT>
+__global__ void __launch_bounds__(SG_WARPS * 32, 1) k_sym_gemm(const double *__restrict__ A, const double *__restrict__ Y,
+                                                                 double *__restrict__ Out, int D, int m, int KS, int chunk,
+                                                                 double alpha, double c, double beta) {
+  extern __shared__ double sg_red[];   // [items][RT][SG_CT]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i0 = blockIdx.x * RT;
+  const int ncg = (m + SG_CT - 1) / SG_CT, items = ncg * KS;
+  for (int item = warp; item < items; item += SG_WARPS) {
+    const int cg = item / KS, ks = item - cg * KS;
+    const int kb = ks * chunk, ke = min(D, kb + chunk);
+    const double *ap[RT], *yp[SG_CT];
+#pragma unroll
+    for (int r = 0; r < RT; r++) ap[r] = A + (int64_t)min(i0 + r, D - 1) * D;
+#pragma unroll
+    for (int q = 0; q < SG_CT; q++) yp[q] = Y + (int64_t)min(cg * SG_CT + q, m - 1) * D;
+    double acc[RT][SG_CT];
+#pragma unroll
+    for (int r = 0; r < RT; r++)
+#pragma unroll
+      for (int q = 0; q < SG_CT; q++) acc[r][q] = 0.0;
+    int k0 = kb + lane;
+    for (; k0 + 32 < ke; k0 += 64) {   // two k per lane in flight
+      const int k1 = k0 + 32;
+      double a0[RT], a1[RT], y0[SG_CT], y1[SG_CT];
+#pragma unroll
+      for (int r = 0; r < RT; r++) { a0[r] = ap[r][k0]; a1[r] = ap[r][k1]; }
+#pragma unroll
+      for (int q = 0; q < SG_CT; q++) { y0[q] = yp[q][k0]; y1[q] = yp[q][k1]; }
+#pragma unroll
+      for (int r = 0; r < RT; r++)
+#pragma unroll
+        for (int q = 0; q < SG_CT; q++) acc[r][q] = fma(a1[r], y1[q], fma(a0[r], y0[q], acc[r][q]));
+    }
+    for (; k0 < ke; k0 += 32) {
+      double a0[RT], y0[SG_CT];
+#pragma unroll
+      for (int r = 0; r < RT; r++) a0[r] = ap[r][k0];
+#pragma unroll
+      for (int q = 0; q < SG_CT; q++) y0[q] = yp[q][k0];
+#pragma unroll
+      for (int r = 0; r < RT; r++)
+#pragma unroll
+        for (int q = 0; q < SG_CT; q++) acc[r][q] = fma(a0[r], y0[q], acc[r][q]);
+    }
+#pragma unroll
+    for (int r = 0; r < RT; r++)
+#pragma unroll
+      for (int q = 0; q < SG_CT; q++) {
+        const double v = warp_sum(acc[r][q]);
+        if (lane == 0) sg_red[(item * RT + r) * SG_CT + q] = v;
+      }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < RT * m; t += blockDim.x) {
+    const int j = t / RT, r = t - j * RT, i = i0 + r;   // consecutive threads on consecutive rows of a column
+    if (i >= D) continue;
+    const int cg = j / SG_CT, q = j - cg * SG_CT;
+    double sacc = 0.0;
+    for (int ks = 0; ks < KS; ks++) sacc += sg_red[((cg * KS + ks) * RT + r) * SG_CT + q];
+    const int64_t o = (int64_t)j * D + i;
+    double v = alpha * (sacc - c * Y[o]);
+    if (beta != 0.0) v = fma(beta, Out[o], v);
+    Out[o] = v;
+  }
+}
+
 // number of entries of the leading n x n block of F (column-major, ld D) that differ from B (n x n)
 __global__ void k_block_mismatch(const double *__restrict__ F, int64_t D, const double *__restrict__ B, int64_t n,
                                  int *__restrict__ count) {
@@ -527,6 +601,31 @@ static ks_status ensure_blas(ks_ctx *ctx) {
   return KS_OK;
 }
 
+// launches k_sym_gemm when the sizes fit it (one wave of 8-row CTAs, i.e. D <= 8 SMs: C4's D = 745; measured slower
+// than cuBLAS with 12-row CTAs at C5's D = 1363); false: use cuBLAS
+static bool sym_gemm_fits(const ks_ctx *ctx, int64_t D, int m) {
+  const int ncg = (m + SG_CT - 1) / SG_CT;
+  return ncg <= 24 && (D + SG_RT - 1) / SG_RT <= ctx->sm_count && D >= 64;
+}
+static bool sym_gemm(ks_ctx *ctx, const double *A, const double *Y, double *Out, int64_t D, int m, double alpha,
+                     double c, double beta) {
+  const int ncg = (m + SG_CT - 1) / SG_CT;
+  constexpr int RT = SG_RT;
+  if (!sym_gemm_fits(ctx, D, m)) return false;
+  // k slices: the KS in 1..12 with the fewest serial lane steps per warp (items per warp x steps per item)
+  int KS = 1, chunk = (int)D, best = 1 << 30;
+  for (int t = 1; t <= 12; t++) {
+    const int ch = (((int)D + t - 1) / t + 31) / 32 * 32, it = ncg * t;
+    const int cost = ((it + SG_WARPS - 1) / SG_WARPS) * (ch / 32 + 2);
+    if ((int64_t)ch * (t - 1) < D && cost < best) { best = cost; KS = t; chunk = ch; }
+  }
+  const size_t smem = sizeof(double) * ncg * KS * RT * SG_CT;
+  if (smem > 48 * 1024) return false;
+  const int grid = (int)((D + RT - 1) / RT);
+  k_sym_gemm<RT><<<grid, SG_WARPS * 32, smem, ctx->stream>>>(A, Y, Out, (int)D, m, KS, chunk, alpha, c, beta);
+  return true;
+}
+
 #define KS_BLAS(ctx, call)                                                                         \
   do {                                                                                             \
     if ((call) != CUBLAS_STATUS_SUCCESS) return ks_fail(ctx, KS_E_CUDA, "cuBLAS call failed: " #call); \
@@ -594,6 +693,9 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
   // KS_EF_FUSED=0: the Chebyshev step as a GEMM plus an element-wise kernel (the round-1 form; A/B only)
   const char *fe = getenv("KS_EF_FUSED");
   const bool fused_cheb = !(fe && fe[0] == '0');
+  // KS_EF_GEMM=cublas: the D x D by D x m products through cuBLAS instead of k_sym_gemm (A/B)
+  const char *ge = getenv("KS_EF_GEMM");
+  const bool own_gemm = !(ge && ge[0] == 'c') && sym_gemm_fits(ctx, D, m);
   if (devrr && devrr[0] == '1' && ctx->ef_dev) {
     int stv = 0, rounds = 0;
     bool ran = false;
@@ -663,8 +765,13 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
     // Rayleigh-Ritz on span(X) with the orthonormalisation folded in: T2 = C X, G = X^T X and H = X^T C X in
     // one round trip; on the host the small pencil (H, G) is reduced by the Cholesky factor of the scaled G
     // and diagonalised by Jacobi: V = D^-1 R^-1 W, X <- X V (orthonormal), CX <- (C X) V
-    KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, (int)D, &one, A, (int)D, X, (int)D, &zero, T2,
-                             (int)D));
+    if (own_gemm) {
+      sym_gemm(ctx, A, X, T2, D, m, 1.0, 0.0, 0.0);
+      KS_LAUNCHED(ctx);
+    } else {
+      KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, (int)D, &one, A, (int)D, X, (int)D, &zero, T2,
+                               (int)D));
+    }
     KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, (int)D, &one, X, (int)D, X, (int)D, &zero, sm, m));
     KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, (int)D, &one, X, (int)D, T2, (int)D, &zero,
                              sm + (int64_t)m * m, m));
@@ -763,9 +870,19 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
     double *Xp = X, *Y = T1, *Yn = T2;
     k_cheb<<<ks_blocks(len, 256), 256, 0, st>>>(CX, X, nullptr, len, sigma / e, c, 0.0, Y);
     KS_LAUNCHED(ctx);
-    if (fused_cheb) {
-      // Y_{d} = (2 s2 / e) (C - c I) Y_{d-1} - sigma s2 Y_{d-2}: one GEMM per degree, accumulated into Y_{d-2}'s
-      // buffer; C's diagonal is shifted for the filter and restored bitwise after it (T2 holds the saved diagonal)
+    if (fused_cheb && own_gemm) {
+      // Y_{d} = (2 s2 / e) (C - c I) Y_{d-1} - sigma s2 Y_{d-2}: one k_sym_gemm launch per degree, accumulated into
+      // Y_{d-2}'s buffer
+      for (int d = 2; d <= deg; d++) {
+        const double s2 = 1.0 / (s1 - sigma), al = 2.0 * s2 / e, be = -sigma * s2;
+        if (!sym_gemm(ctx, A, Y, Xp, D, m, al, c, be)) return ks_fail(ctx, KS_E_STATE, "ks_pencil_eig: k_sym_gemm sizes");
+        KS_LAUNCHED(ctx);
+        std::swap(Xp, Y);
+        sigma = s2;
+      }
+    } else if (fused_cheb) {
+      // the same with one cuBLAS GEMM per degree; C's diagonal is shifted for the filter and restored bitwise after
+      // it (T2 holds the saved diagonal)
       k_shift_diag<<<ks_blocks(D, 256), 256, 0, st>>>(A, D, c, T2);
       KS_LAUNCHED(ctx);
       for (int d = 2; d <= deg; d++) {
