@@ -228,9 +228,10 @@ ks_status ks_project_augmented(ks_ctx *ctx, int32_t N, const double *d_Ut, doubl
  * ks_pencil_eig: lowest k eigenpairs of F_A y = lambda F_B y (Nonlinear_Eig_Hh on W; "a
  * small-scale algebraic eigenvalue problem solved in serial"), on the context's stream.
  * It reduces to standard form by Cholesky, then runs a Chebyshev-filtered subspace iteration on k + 8 vectors
- * when k + 8 <= D / 2 (KS_PENCIL_DEVICE=1 runs that iteration as one cooperative kernel with
- * the Rayleigh-Ritz steps on the device). The fallback is the dense cuSOLVER generalized symmetric
- * eigensolver, which is always used when the environment variable KS_PENCIL_DENSE=1 is set.
+ * when k + 8 <= D / 2 (its D x D by D x m products, Gram matrices and rotations are the library's
+ * own kernels, the m x m eigenproblems run on the host, see ks_host_sym_eig; KS_PENCIL_DEVICE=1 runs the iteration
+ * as one cooperative kernel with the Rayleigh-Ritz steps on the device). The fallback is the dense cuSOLVER
+ * generalized symmetric eigensolver, which is always used when the environment variable KS_PENCIL_DENSE=1 is set.
  *   D = n_H + N >= 1, 1 <= k <= D; d_FA, d_FB [D][D] f64 symmetric (e.g. from ks_project_augmented), not
  *   modified; d_evals [k] f64 ascending; d_evecs [D][k] f64 row-major, column j = eigenvector j, normalised
  *   y^T F_B y = 1 (sign arbitrary). Synchronises the stream (reads the solver status).

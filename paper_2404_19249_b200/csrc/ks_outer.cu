@@ -3,7 +3,8 @@
 //                       problem" on W (Nonlinear_Eig_Hh), D = n_H + N <= ~1400.
 //                       Default: reduction to standard form (with the coarse block's Cholesky factor cached per
 //                       coarse space, coarse_chol_reduction) and a Chebyshev-filtered subspace iteration on
-//                       k + 8 vectors (pencil_eig_filtered). Fallback, and KS_PENCIL_DENSE=1: the dense cuSOLVER
+//                       k + 8 vectors (pencil_eig_filtered: k_sym_gemm, k_gram_pair, k_rotate_resid, the m x m
+//                       eigenproblems on the host). Fallback, and KS_PENCIL_DENSE=1: the dense cuSOLVER
 //                       generalized symmetric eigensolver (lowest k by index range, dsygvdx).
 //   ks_lift             U_new = P y_H + U~ y_t (the new orbitals in S_H + span{psi~}), own kernel (FP64 MMA).
 //   ks_augmented_solve  outer iterations with a fixed potential: block solve -> projection -> pencil
@@ -426,76 +427,177 @@ __global__ void k_restore_diag(double *__restrict__ A, int64_t D, const double *
 }
 
 // Out = alpha (A - c I) Y + beta Out for a symmetric A [D][D] and column-major D x m blocks (ld D), m small: the
-// product of the filtered iteration (one launch per Chebyshev step instead of a cuBLAS GEMM and its split-K
-// reduction). One CTA per RT rows of the output. A work item is (4 columns, one of KS slices of
-// the k range); a warp takes items w, w + 12, ... with its lanes on consecutive k, so the row of A (= its column,
-// A is symmetric) and the columns of Y are read coalesced, holds the RT x 4 partial products in registers, and
-// leaves their butterfly sums in shared memory. The k slices are then added in ascending order: deterministic.
-constexpr int SG_WARPS = 12, SG_CT = 4, SG_RT = 8;
+// product of the filtered iteration in one launch (instead of a cuBLAS GEMM and its split-K reduction, DESIGN.md
+// §8.2), on the FP64 tensor cores with the operands staged through shared memory. One CTA per RT output rows and all
+// m columns. Chunks of SG2_KC values of k of the CTA's RT rows of A (= its columns: A is symmetric) and
+// of all m columns of Y are copied by cp.async (8 bytes each, no alignment needed: D may be odd) into a ring of
+// SG2_STAGES stages with a row pitch = 4 (mod 16) doubles (conflict-free fragment loads), so the bytes in flight do
+// not occupy registers. A unit is an 8 x 8 output tile; KSPLIT warps share a unit, each taking a contiguous part of
+// every chunk in k-steps of 4 (mma.m8n8k4.f64: A[m = lane/4][k = lane%4], B[k = lane%4][n = lane/4],
+// C[m = lane/4][n = 2 (lane%4) + v]) with four accumulator pairs in rotation; the KSPLIT partial tiles are added in
+// ascending order: deterministic.
+constexpr int SG_WARPS = 12;
+constexpr int SG2_KC = 128, SG2_STAGES = 3, SG2_PITCH = SG2_KC + 4;
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void sg_mma884(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
 template <int RT>
 __global__ void __launch_bounds__(SG_WARPS * 32, 1) k_sym_gemm(const double *__restrict__ A, const double *__restrict__ Y,
-                                                                 double *__restrict__ Out, int D, int m, int KS, int chunk,
-                                                                 double alpha, double c, double beta) {
-  extern __shared__ double sg_red[];   // [items][RT][SG_CT]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+                                                                  double *__restrict__ Out, int D, int m, int KSPLIT,
+                                                                  double alpha, double c, double beta) {
+  extern __shared__ __align__(16) double sg2[];   // [STAGES][RT + m][PITCH], then red [SG_WARPS][8][8]
+  const int rows = RT + m;
+  double *red = sg2 + (size_t)SG2_STAGES * rows * SG2_PITCH;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, grp = lane >> 2, tig = lane & 3;
   const int i0 = blockIdx.x * RT;
-  const int ncg = (m + SG_CT - 1) / SG_CT, items = ncg * KS;
-  for (int item = warp; item < items; item += SG_WARPS) {
-    const int cg = item / KS, ks = item - cg * KS;
-    const int kb = ks * chunk, ke = min(D, kb + chunk);
-    const double *ap[RT], *yp[SG_CT];
+  const int nct = (m + 7) / 8;
+  const int nchunks = (D + SG2_KC - 1) / SG2_KC;
+  auto fill = [&](int chunk) {
+    double *st = sg2 + (size_t)(chunk % SG2_STAGES) * rows * SG2_PITCH;
+    const int kbase = chunk * SG2_KC;
+    for (int row = warp; row < rows; row += SG_WARPS) {   // a warp per staged row, lanes on consecutive k
+      const double *src = (row < RT ? A + (int64_t)min(i0 + row, D - 1) * D : Y + (int64_t)(row - RT) * D) + kbase;
+      double *dst = st + row * SG2_PITCH;
 #pragma unroll
-    for (int r = 0; r < RT; r++) ap[r] = A + (int64_t)min(i0 + r, D - 1) * D;
-#pragma unroll
-    for (int q = 0; q < SG_CT; q++) yp[q] = Y + (int64_t)min(cg * SG_CT + q, m - 1) * D;
-    double acc[RT][SG_CT];
-#pragma unroll
-    for (int r = 0; r < RT; r++)
-#pragma unroll
-      for (int q = 0; q < SG_CT; q++) acc[r][q] = 0.0;
-    int k0 = kb + lane;
-    for (; k0 + 32 < ke; k0 += 64) {   // two k per lane in flight
-      const int k1 = k0 + 32;
-      double a0[RT], a1[RT], y0[SG_CT], y1[SG_CT];
-#pragma unroll
-      for (int r = 0; r < RT; r++) { a0[r] = ap[r][k0]; a1[r] = ap[r][k1]; }
-#pragma unroll
-      for (int q = 0; q < SG_CT; q++) { y0[q] = yp[q][k0]; y1[q] = yp[q][k1]; }
-#pragma unroll
-      for (int r = 0; r < RT; r++)
-#pragma unroll
-        for (int q = 0; q < SG_CT; q++) acc[r][q] = fma(a1[r], y1[q], fma(a0[r], y0[q], acc[r][q]));
-    }
-    for (; k0 < ke; k0 += 32) {
-      double a0[RT], y0[SG_CT];
-#pragma unroll
-      for (int r = 0; r < RT; r++) a0[r] = ap[r][k0];
-#pragma unroll
-      for (int q = 0; q < SG_CT; q++) y0[q] = yp[q][k0];
-#pragma unroll
-      for (int r = 0; r < RT; r++)
-#pragma unroll
-        for (int q = 0; q < SG_CT; q++) acc[r][q] = fma(a0[r], y0[q], acc[r][q]);
-    }
-#pragma unroll
-    for (int r = 0; r < RT; r++)
-#pragma unroll
-      for (int q = 0; q < SG_CT; q++) {
-        const double v = warp_sum(acc[r][q]);
-        if (lane == 0) sg_red[(item * RT + r) * SG_CT + q] = v;
+      for (int u = 0; u < SG2_KC / 32; u++) {
+        const int kk = u * 32 + lane;
+        if (kbase + kk < D) cp_async8(dst + kk, src + kk);
+        else dst[kk] = 0.0;
       }
+    }
+  };
+  for (int sgi = 0; sgi < SG2_STAGES - 1; sgi++) {
+    if (sgi < nchunks) fill(sgi);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  const int unit = warp / KSPLIT, kq = warp - unit * KSPLIT;
+  const int rt = unit / nct, ct = unit - rt * nct;
+  const bool active = unit < (RT / 8) * nct;
+  const int arow = rt * 8 + grp, brow = RT + min(ct * 8 + grp, m - 1);
+  const int klen = SG2_KC / KSPLIT, k0 = kq * klen;
+  double c0[4] = {0.0, 0.0, 0.0, 0.0}, c1[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int ch = 0; ch < nchunks; ch++) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(SG2_STAGES - 2) : "memory");
+    __syncthreads();   // chunk ch has landed for every thread; every warp is done with chunk ch - 1
+    if (ch + SG2_STAGES - 1 < nchunks) fill(ch + SG2_STAGES - 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if (active) {
+      const double *st = sg2 + (size_t)(ch % SG2_STAGES) * rows * SG2_PITCH;
+      const double *pa = st + arow * SG2_PITCH + k0 + tig, *pb = st + brow * SG2_PITCH + k0 + tig;
+      for (int kk = 0; kk < klen; kk += 16) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) { av[u] = pa[kk + 4 * u]; bv[u] = pb[kk + 4 * u]; }
+#pragma unroll
+        for (int u = 0; u < 4; u++) sg_mma884(c0[u], c1[u], av[u], bv[u]);
+      }
+    }
+  }
+  if (active) {
+    red[(warp * 8 + grp) * 8 + 2 * tig] = (c0[0] + c0[1]) + (c0[2] + c0[3]);
+    red[(warp * 8 + grp) * 8 + 2 * tig + 1] = (c1[0] + c1[1]) + (c1[2] + c1[3]);
   }
   __syncthreads();
   for (int t = threadIdx.x; t < RT * m; t += blockDim.x) {
-    const int j = t / RT, r = t - j * RT, i = i0 + r;   // consecutive threads on consecutive rows of a column
+    const int j = t / RT, r = t - j * RT, i = i0 + r;
     if (i >= D) continue;
-    const int cg = j / SG_CT, q = j - cg * SG_CT;
+    const int u = (r >> 3) * nct + (j >> 3);
     double sacc = 0.0;
-    for (int ks = 0; ks < KS; ks++) sacc += sg_red[((cg * KS + ks) * RT + r) * SG_CT + q];
+    for (int q = 0; q < KSPLIT; q++) sacc += red[((u * KSPLIT + q) * 8 + (r & 7)) * 8 + (j & 7)];
     const int64_t o = (int64_t)j * D + i;
     double v = alpha * (sacc - c * Y[o]);
     if (beta != 0.0) v = fma(beta, Out[o], v);
     Out[o] = v;
+  }
+}
+
+// The two Gram matrices of the Rayleigh-Ritz step in one launch: G = X^T X and H = X^T (C X), m x m column-major,
+// for column-major D x m blocks. One warp per pair a <= b (lanes on consecutive k, four k per lane in flight),
+// butterfly sums, the entry mirrored (H is symmetric up to rounding; the host symmetrises the reduced matrix).
+__global__ void __launch_bounds__(SG_WARPS * 32) k_gram_pair(const double *__restrict__ X, const double *__restrict__ CXb,
+                                                             int D, int m, double *__restrict__ G, double *__restrict__ H) {
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * SG_WARPS + (threadIdx.x >> 5);
+  if (gw >= m * m) return;
+  const int a = gw % m, b = gw / m;
+  if (a > b) return;
+  const double *xa = X + (int64_t)a * D, *xb = X + (int64_t)b * D, *cb = CXb + (int64_t)b * D;
+  double g = 0.0, h = 0.0;
+  int k = lane;
+  for (; k + 96 < D; k += 128) {
+    double va[4], vb[4], vc[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) { va[u] = xa[k + 32 * u]; vb[u] = xb[k + 32 * u]; vc[u] = cb[k + 32 * u]; }
+#pragma unroll
+    for (int u = 0; u < 4; u++) { g = fma(va[u], vb[u], g); h = fma(va[u], vc[u], h); }
+  }
+  for (; k < D; k += 32) { const double va = xa[k]; g = fma(va, xb[k], g); h = fma(va, cb[k], h); }
+  g = warp_sum(g);
+  h = warp_sum(h);
+  if (lane == 0) {
+    G[b * m + a] = g; G[a * m + b] = g;
+    H[b * m + a] = h; H[a * m + b] = h;
+  }
+}
+
+// The Rayleigh-Ritz rotation and the residuals in one launch: Xn = X T, CXn = (C X) T for the m x m matrix T
+// (column-major), and per block of RR_ROWS rows the partial sums of (CXn_ij - lam_j Xn_ij)^2 for the k wanted
+// columns (part [row blocks][k], summed on the host in ascending block order). A CTA takes RR_ROWS rows and 8
+// output columns: its rows of X and C X staged in shared memory (a thread per row), T's 8 columns l-major.
+constexpr int RR_ROWS = 128, RR_JB = 8;
+__global__ void __launch_bounds__(RR_ROWS) k_rotate_resid(const double *__restrict__ X, const double *__restrict__ CXb,
+                                                          const double *__restrict__ T, const double *__restrict__ lam,
+                                                          int D, int m, int k, double *__restrict__ Xn,
+                                                          double *__restrict__ CXn, double *__restrict__ part) {
+  extern __shared__ __align__(16) double rr_s[];   // xs [m][RR_ROWS], cs [m][RR_ROWS], ts [m][RR_JB], wsum [4][RR_JB]
+  double *xs = rr_s, *cs = xs + (size_t)m * RR_ROWS, *ts = cs + (size_t)m * RR_ROWS, *wsum = ts + (size_t)m * RR_JB;
+  const int tid = threadIdx.x, i = blockIdx.x * RR_ROWS + tid, jb = blockIdx.y * RR_JB;
+  const bool row_ok = i < D;
+  for (int l = 0; l < m; l++) {
+    xs[l * RR_ROWS + tid] = row_ok ? X[(int64_t)l * D + i] : 0.0;
+    cs[l * RR_ROWS + tid] = row_ok ? CXb[(int64_t)l * D + i] : 0.0;
+  }
+  for (int x = tid; x < m * RR_JB; x += RR_ROWS) {
+    const int l = x / RR_JB, q = x - l * RR_JB;
+    ts[x] = jb + q < m ? T[(int64_t)(jb + q) * m + l] : 0.0;
+  }
+  __syncthreads();
+  double ax[RR_JB], ac[RR_JB];
+#pragma unroll
+  for (int q = 0; q < RR_JB; q++) ax[q] = ac[q] = 0.0;
+  for (int l = 0; l < m; l++) {
+    const double xv = xs[l * RR_ROWS + tid], cv = cs[l * RR_ROWS + tid];
+#pragma unroll
+    for (int q = 0; q < RR_JB; q++) {
+      const double w = ts[l * RR_JB + q];
+      ax[q] = fma(xv, w, ax[q]);
+      ac[q] = fma(cv, w, ac[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < RR_JB; q++) {
+    const int j = jb + q;
+    if (j < m && row_ok) {
+      Xn[(int64_t)j * D + i] = ax[q];
+      CXn[(int64_t)j * D + i] = ac[q];
+    }
+    double r = 0.0;
+    if (j < k && row_ok) {
+      r = ac[q] - lam[j] * ax[q];
+      r *= r;
+    }
+    r = warp_sum(r);
+    if ((tid & 31) == 0) wsum[(tid >> 5) * RR_JB + q] = r;
+  }
+  __syncthreads();
+  if (tid < RR_JB && jb + tid < k) {
+    double sacc = 0.0;
+    for (int w = 0; w < RR_ROWS / 32; w++) sacc += wsum[w * RR_JB + tid];
+    part[(int64_t)blockIdx.x * k + jb + tid] = sacc;
   }
 }
 
@@ -601,28 +703,40 @@ static ks_status ensure_blas(ks_ctx *ctx) {
   return KS_OK;
 }
 
-// launches k_sym_gemm when the sizes fit it (one wave of 8-row CTAs, i.e. D <= 8 SMs: C4's D = 745; measured slower
-// than cuBLAS with 12-row CTAs at C5's D = 1363); false: use cuBLAS
+// plan of k_sym_gemm: warps per 8 x 8 output tile and dynamic shared memory; false when the sizes do not fit, i.e.
+// more than one wave of 8-row CTAs (D > 8 SMs: with 16-row CTAs every CTA still stages all of Y, and at C5's
+// D = 1363 that was slower than cuBLAS) or more column tiles than warps: cuBLAS serves those
+struct SymGemmPlan {
+  int KSPLIT = 1;
+  size_t smem = 0;
+};
+constexpr int SG_RT = 8;
+static bool sym_gemm_plan(const ks_ctx *ctx, int64_t D, int m, SymGemmPlan *pl) {
+  const int nct = (m + 7) / 8;
+  if (D < 64 || m < 1 || (D + SG_RT - 1) / SG_RT > ctx->sm_count || nct > SG_WARPS) return false;
+  int KSPLIT = 1;
+  while (KSPLIT < 4 && nct * KSPLIT * 2 <= SG_WARPS) KSPLIT *= 2;
+  const size_t smem = sizeof(double) * ((size_t)SG2_STAGES * (SG_RT + m) * SG2_PITCH + (size_t)SG_WARPS * 64);
+  if (smem > 220 * 1024) return false;
+  pl->KSPLIT = KSPLIT;
+  pl->smem = smem;
+  return true;
+}
 static bool sym_gemm_fits(const ks_ctx *ctx, int64_t D, int m) {
-  const int ncg = (m + SG_CT - 1) / SG_CT;
-  return ncg <= 24 && (D + SG_RT - 1) / SG_RT <= ctx->sm_count && D >= 64;
+  SymGemmPlan pl;
+  return sym_gemm_plan(ctx, D, m, &pl);
 }
 static bool sym_gemm(ks_ctx *ctx, const double *A, const double *Y, double *Out, int64_t D, int m, double alpha,
                      double c, double beta) {
-  const int ncg = (m + SG_CT - 1) / SG_CT;
-  constexpr int RT = SG_RT;
-  if (!sym_gemm_fits(ctx, D, m)) return false;
-  // k slices: the KS in 1..12 with the fewest serial lane steps per warp (items per warp x steps per item)
-  int KS = 1, chunk = (int)D, best = 1 << 30;
-  for (int t = 1; t <= 12; t++) {
-    const int ch = (((int)D + t - 1) / t + 31) / 32 * 32, it = ncg * t;
-    const int cost = ((it + SG_WARPS - 1) / SG_WARPS) * (ch / 32 + 2);
-    if ((int64_t)ch * (t - 1) < D && cost < best) { best = cost; KS = t; chunk = ch; }
+  SymGemmPlan pl;
+  if (!sym_gemm_plan(ctx, D, m, &pl)) return false;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute((const void *)k_sym_gemm<SG_RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    attr = true;
   }
-  const size_t smem = sizeof(double) * ncg * KS * RT * SG_CT;
-  if (smem > 48 * 1024) return false;
-  const int grid = (int)((D + RT - 1) / RT);
-  k_sym_gemm<RT><<<grid, SG_WARPS * 32, smem, ctx->stream>>>(A, Y, Out, (int)D, m, KS, chunk, alpha, c, beta);
+  const int grid = (int)((D + SG_RT - 1) / SG_RT);
+  k_sym_gemm<SG_RT><<<grid, SG_WARPS * 32, pl.smem, ctx->stream>>>(A, Y, Out, (int)D, m, pl.KSPLIT, alpha, c, beta);
   return true;
 }
 
@@ -696,6 +810,16 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
   // KS_EF_GEMM=cublas: the D x D by D x m products through cuBLAS instead of k_sym_gemm (A/B)
   const char *ge = getenv("KS_EF_GEMM");
   const bool own_gemm = !(ge && ge[0] == 'c') && sym_gemm_fits(ctx, D, m);
+  // KS_EF_RR=cublas: the Gram matrices, the rotation and the residuals of the Rayleigh-Ritz step by cuBLAS GEMMs and
+  // k_resid (5 launches) instead of k_gram_pair and k_rotate_resid (A/B)
+  const char *re = getenv("KS_EF_RR");
+  const int64_t rr_blocks = (D + RR_ROWS - 1) / RR_ROWS;
+  const size_t rr_smem = sizeof(double) * ((size_t)2 * m * RR_ROWS + (size_t)m * RR_JB + (RR_ROWS / 32) * RR_JB);
+  const bool own_rr = !(re && re[0] == 'c') && rr_blocks * k <= (int64_t)m * m && rr_smem <= 200 * 1024;
+  if (own_rr && rr_smem > 48 * 1024)
+    KS_CUDA(ctx, cudaFuncSetAttribute((const void *)k_rotate_resid, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)rr_smem));
+  std::vector<double> rpart;
   if (devrr && devrr[0] == '1' && ctx->ef_dev) {
     int stv = 0, rounds = 0;
     bool ran = false;
@@ -772,9 +896,14 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
       KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, (int)D, &one, A, (int)D, X, (int)D, &zero, T2,
                                (int)D));
     }
-    KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, (int)D, &one, X, (int)D, X, (int)D, &zero, sm, m));
-    KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, (int)D, &one, X, (int)D, T2, (int)D, &zero,
-                             sm + (int64_t)m * m, m));
+    if (own_rr) {
+      k_gram_pair<<<(m * m + SG_WARPS - 1) / SG_WARPS, SG_WARPS * 32, 0, st>>>(X, T2, (int)D, m, sm, sm + (int64_t)m * m);
+      KS_LAUNCHED(ctx);
+    } else {
+      KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, (int)D, &one, X, (int)D, X, (int)D, &zero, sm, m));
+      KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, (int)D, &one, X, (int)D, T2, (int)D, &zero,
+                               sm + (int64_t)m * m, m));
+    }
     KS_CUDA(ctx, cudaMemcpyAsync(G.data(), sm, sizeof(double) * m * m, cudaMemcpyDeviceToHost, st));
     KS_CUDA(ctx, cudaMemcpyAsync(G2.data(), sm + (int64_t)m * m, sizeof(double) * m * m, cudaMemcpyDeviceToHost, st));
     KS_CUDA(ctx, cudaStreamSynchronize(st));
@@ -821,16 +950,32 @@ static ks_status pencil_eig_filtered(ks_ctx *ctx, int64_t D, int k, double *eval
     host_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
     KS_CUDA(ctx, cudaMemcpyAsync(sm, Tm.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice, st));
     KS_CUDA(ctx, cudaMemcpyAsync(sm + (int64_t)m * m, lam.data(), sizeof(double) * m, cudaMemcpyHostToDevice, st));
-    KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, m, &one, X, (int)D, sm, m, &zero, T1, (int)D));
-    KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, m, &one, T2, (int)D, sm, m, &zero, CX, (int)D));
-    std::swap(X, T1);
-    // wanted residuals
-    k_resid<<<k, 32, 0, st>>>(CX, X, sm + (int64_t)m * m, D, k, T2);
-    KS_LAUNCHED(ctx);
-    KS_CUDA(ctx, cudaMemcpyAsync(res.data(), T2, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
-    KS_CUDA(ctx, cudaStreamSynchronize(st));
     double rmax = 0.0;
-    for (int j = 0; j < k; j++) rmax = std::fmax(rmax, std::sqrt(res[j]));
+    if (own_rr) {   // rotation and wanted residuals in one launch; the row-block partials summed here in order
+      double *part = sm + (int64_t)m * m + m;
+      k_rotate_resid<<<dim3((unsigned)rr_blocks, (unsigned)((m + RR_JB - 1) / RR_JB)), RR_ROWS, rr_smem, st>>>(
+          X, T2, sm, sm + (int64_t)m * m, (int)D, m, k, T1, CX, part);
+      KS_LAUNCHED(ctx);
+      std::swap(X, T1);
+      rpart.resize((size_t)rr_blocks * k);
+      KS_CUDA(ctx, cudaMemcpyAsync(rpart.data(), part, sizeof(double) * rr_blocks * k, cudaMemcpyDeviceToHost, st));
+      KS_CUDA(ctx, cudaStreamSynchronize(st));
+      for (int j = 0; j < k; j++) {
+        double sacc = 0.0;
+        for (int64_t rb = 0; rb < rr_blocks; rb++) sacc += rpart[(size_t)rb * k + j];
+        rmax = std::fmax(rmax, std::sqrt(sacc));
+      }
+    } else {
+      KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, m, &one, X, (int)D, sm, m, &zero, T1, (int)D));
+      KS_BLAS(ctx, cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)D, m, m, &one, T2, (int)D, sm, m, &zero, CX, (int)D));
+      std::swap(X, T1);
+      // wanted residuals
+      k_resid<<<k, 32, 0, st>>>(CX, X, sm + (int64_t)m * m, D, k, T2);
+      KS_LAUNCHED(ctx);
+      KS_CUDA(ctx, cudaMemcpyAsync(res.data(), T2, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+      KS_CUDA(ctx, cudaStreamSynchronize(st));
+      for (int j = 0; j < k; j++) rmax = std::fmax(rmax, std::sqrt(res[j]));
+    }
     if (getenv("KS_EF_VERBOSE"))
       fprintf(stderr, "ks_pencil_eig: round %d rmax %.3e (tol %.3e), host Rayleigh-Ritz so far %.0f us\n", it + 1, rmax,
               tol * bound, host_us);

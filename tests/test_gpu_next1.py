@@ -165,14 +165,15 @@ def test_pencil_eig_falls_back_to_the_dense_path(monkeypatch):
 
 
 @pytest.mark.parametrize("c", [2, 3, 4])
-@pytest.mark.parametrize("variant", ["KS_PENCIL_DEVICE=1", "KS_EF_HOSTEIG=jacobi", "KS_EF_GEMM=cublas"])
+@pytest.mark.parametrize("variant", ["KS_PENCIL_DEVICE=1", "KS_EF_HOSTEIG=jacobi", "KS_EF_GEMM=cublas", "KS_EF_RR=cublas"])
 def test_filtered_loop_variants_agree(c, variant, monkeypatch):
     """The filtered iteration's variants give the same eigenvalues (1e-10 relative) and F_B-orthonormal eigenvectors
     that agree up to sign: the default (host Rayleigh-Ritz, cuBLAS filter) and the whole loop as one cooperative
     kernel (KS_PENCIL_DEVICE=1, ks_efdev.cu: Rayleigh-Ritz, convergence test and filter on the device), and the
     default loop with the host's small eigenproblems by cyclic Jacobi instead of Householder + QL
-    (KS_EF_HOSTEIG=jacobi) or its D x D by D x m products by cuBLAS instead of k_sym_gemm (KS_EF_GEMM=cublas). Each
-    is bitwise reproducible."""
+    (KS_EF_HOSTEIG=jacobi) or its D x D by D x m products by cuBLAS instead of k_sym_gemm (KS_EF_GEMM=cublas), or its
+    Gram matrices, rotation and residuals by cuBLAS and k_resid instead of k_gram_pair and k_rotate_resid
+    (KS_EF_RR=cublas). Each is bitwise reproducible."""
     p = gen.make_problem(c)
     ctx = _ctx(p, p.mu)
     Ut, _, _ = ctx.block_solve(dt(p.lam), dt(p.U))
