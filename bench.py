@@ -188,7 +188,7 @@ def traced_phases(ctx, solve, n, nnz, N, peak):
 def next1_times(ctx, Ut, FA, FB, N, stream, p_lam=None, U0=None):
     """NEXT-1 (not part of the timed step): the pencil eigensolve of the step's F_A, F_B (D = n_H + N; the
     Chebyshev-filtered subspace iteration, dense cuSOLVER with KS_PENCIL_DENSE=1) and the lift
-    U_new = P y_H + U~ y_t, each timed with CUDA events after one warm-up call; and one whole outer iteration
+    U_new = P y_H + U~ y_t, each timed with CUDA events after one warm-up call (median and minimum of 5); and one whole outer iteration
     of the linear Algorithm 3 (ks_augmented_solve) from the step's inputs."""
     import torch
     try:
@@ -196,12 +196,16 @@ def next1_times(ctx, Ut, FA, FB, N, stream, p_lam=None, U0=None):
         ev, Y = ctx.pencil_eig(FA, FB, N)
         Un = ctx.lift(Ut, Y)
         for name, fn in (("pencil_eig", lambda: ctx.pencil_eig(FA, FB, N)), ("lift", lambda: ctx.lift(Ut, Y, Un))):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            fn()
-            b.record(stream)
-            torch.cuda.synchronize()
-            out[name] = a.elapsed_time(b)
+            ts = []
+            for rep in range(5):   # median of 5 (a single call varies by ~10 % with the host's Rayleigh-Ritz steps)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                fn()
+                b.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            out[name] = float(np.median(ts))
+            out[name + "_min"] = float(min(ts))
         out["D"] = int(FA.shape[0])
         # one outer iteration of the linear Algorithm 3 (block solve -> projection -> pencil eigensolve ->
         # lift, ks_augmented_solve with tol_eig = inf: it stops after the first iteration), on copies
